@@ -1,0 +1,202 @@
+"""ctypes loader for liboracle.so (TEST INFRASTRUCTURE; see oracle/__init__.py).
+
+Argument marshalling only: every step of the method runs in hodlr_oracle.c.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "hodlr_oracle.c")
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+SE, MATERN32, MATERN52 = 0, 1, 2
+KERNELS = {"se": SE, "matern32": MATERN32, "matern52": MATERN52}
+STATUS = {0: "OK", 1: "EINVAL", 2: "ENOTPD", 3: "ERANKCAP", 4: "ESTATE", 5: "ENOMEM"}
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"oracle {STATUS.get(code, code)}: {msg}")
+        self.code = code
+        self.status = STATUS.get(code, str(code))
+
+
+def build_oracle(force: bool = False) -> str:
+    """Compile hodlr_oracle.c with gcc -O2 -ffp-contract=off (no BLAS/OpenMP)."""
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC) \
+            or os.path.getmtime(_LIB_PATH) < os.path.getmtime(os.path.join(_HERE, "hodlr_oracle.h")):
+        tmp = _LIB_PATH + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-Wall",
+                               "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB_PATH)
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        lib = C.CDLL(build_oracle())
+        P, I64, I32, D = C.c_void_p, C.c_int64, C.c_int, C.c_double
+        lib.oracle_kernel.argtypes = [I32, P, D]; lib.oracle_kernel.restype = D
+        lib.oracle_aca_dense.argtypes = [P, I64, I64, I64, D, I32, P, P, P]; lib.oracle_aca_dense.restype = I32
+        lib.oracle_build.argtypes = [P, I64, I32, P, D, I32, D, I32, P]; lib.oracle_build.restype = I32
+        for f in ("oracle_factor",):
+            getattr(lib, f).argtypes = [P]; getattr(lib, f).restype = I32
+        lib.oracle_logdet.argtypes = [P, P]; lib.oracle_logdet.restype = I32
+        lib.oracle_solve.argtypes = [P, P, P, I64, I64]; lib.oracle_solve.restype = I32
+        lib.oracle_gp_loglik.argtypes = [P, P, P]; lib.oracle_gp_loglik.restype = I32
+        lib.oracle_apply.argtypes = [P, P, P]; lib.oracle_apply.restype = I32
+        lib.oracle_kappa.argtypes = [P]; lib.oracle_kappa.restype = I32
+        lib.oracle_num_nodes.argtypes = [P]; lib.oracle_num_nodes.restype = I64
+        for f in ("oracle_get_perm", "oracle_get_sorted", "oracle_get_ranks"):
+            getattr(lib, f).argtypes = [P, P]; getattr(lib, f).restype = I32
+        lib.oracle_get_tree.argtypes = [P, P, P]; lib.oracle_get_tree.restype = I32
+        lib.oracle_get_factors.argtypes = [P, I64, P, P]; lib.oracle_get_factors.restype = I32
+        lib.oracle_get_logdet_parts.argtypes = [P, P, P]; lib.oracle_get_logdet_parts.restype = I32
+        lib.oracle_free.argtypes = [P]; lib.oracle_free.restype = None
+        lib.oracle_last_error.argtypes = []; lib.oracle_last_error.restype = C.c_char_p
+        lib.oracle_dense.argtypes = [P, I64, I32, P, D, P, P, P]; lib.oracle_dense.restype = I32
+        _lib = lib
+        return lib
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _check(lib, code):
+    if code != 0:
+        raise OracleError(code, lib.oracle_last_error().decode())
+
+
+def kernel_value(kernel: int, theta, d: float) -> float:
+    lib = _load()
+    th = np.ascontiguousarray(theta, dtype=np.float64)
+    return lib.oracle_kernel(int(kernel), _ptr(th), float(d))
+
+
+def aca_dense(A: np.ndarray, eps: float, cap: int | None = None):
+    """O4 on an explicit dense block; returns (U, V, rank)."""
+    lib = _load()
+    A = np.asfortranarray(A, dtype=np.float64)
+    m1, m2 = A.shape
+    cap = min(m1, m2) if cap is None else cap
+    U = np.zeros((cap, m1)); V = np.zeros((cap, m2)); r = C.c_int(0)
+    _check(lib, lib.oracle_aca_dense(_ptr(A), m1, m2, m1, float(eps), int(cap), _ptr(U), _ptr(V), C.byref(r)))
+    k = r.value
+    return U[:k].T.copy(), V[:k].T.copy(), k
+
+
+def dense_check(x, kernel: int, theta, sigma2: float, y=None):
+    """O11: dense Cholesky log det (+ solve).  Returns (logdet, x or None)."""
+    lib = _load()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    th = np.ascontiguousarray(theta, dtype=np.float64)
+    ld = C.c_double(0.0)
+    out = None
+    if y is not None:
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        out = np.zeros_like(y)
+    _check(lib, lib.oracle_dense(_ptr(x), x.size, int(kernel), _ptr(th), float(sigma2),
+                                 _ptr(y) if y is not None else None, C.byref(ld),
+                                 _ptr(out) if out is not None else None))
+    return ld.value, out
+
+
+class OracleHODLR:
+    """build -> factor -> {logdet, solve, gp_loglik}*, host memory, original point order."""
+
+    def __init__(self, x, kernel: int, theta, sigma2: float, leaf: int, eps: float, rank_cap: int = 0):
+        self._lib = _load()
+        self.x = np.ascontiguousarray(x, dtype=np.float64)
+        self.n = self.x.size
+        th = np.ascontiguousarray(theta, dtype=np.float64)
+        h = C.c_void_p(0)
+        _check(self._lib, self._lib.oracle_build(_ptr(self.x), self.n, int(kernel), _ptr(th), float(sigma2),
+                                                 int(leaf), float(eps), int(rank_cap), C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.oracle_free(h)
+            self._h = None
+
+    def factor(self):
+        _check(self._lib, self._lib.oracle_factor(self._h))
+        return self
+
+    def logdet(self) -> float:
+        v = C.c_double(0.0)
+        _check(self._lib, self._lib.oracle_logdet(self._h, C.byref(v)))
+        return v.value
+
+    def solve(self, y):
+        y = np.asarray(y, dtype=np.float64)
+        one = y.ndim == 1
+        Y = np.asfortranarray(y.reshape(self.n, -1))
+        X = np.zeros_like(Y, order="F")
+        _check(self._lib, self._lib.oracle_solve(self._h, _ptr(Y), _ptr(X), Y.shape[1], self.n))
+        return X[:, 0].copy() if one else X
+
+    def gp_loglik(self, y) -> float:
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        v = C.c_double(0.0)
+        _check(self._lib, self._lib.oracle_gp_loglik(self._h, _ptr(y), C.byref(v)))
+        return v.value
+
+    def apply(self, v):
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        out = np.zeros_like(v)
+        _check(self._lib, self._lib.oracle_apply(self._h, _ptr(v), _ptr(out)))
+        return out
+
+    @property
+    def kappa(self) -> int:
+        return self._lib.oracle_kappa(self._h)
+
+    def perm(self):
+        p = np.zeros(self.n, dtype=np.int64)
+        self._lib.oracle_get_perm(self._h, _ptr(p))
+        return p
+
+    def sorted_x(self):
+        p = np.zeros(self.n)
+        self._lib.oracle_get_sorted(self._h, _ptr(p))
+        return p
+
+    def tree(self):
+        nn = self._lib.oracle_num_nodes(self._h)
+        lo = np.zeros(nn, dtype=np.int64); hi = np.zeros(nn, dtype=np.int64)
+        self._lib.oracle_get_tree(self._h, _ptr(lo), _ptr(hi))
+        return lo, hi
+
+    def ranks(self):
+        ni = (1 << self.kappa) - 1
+        r = np.zeros(max(ni, 1), dtype=np.int32)
+        self._lib.oracle_get_ranks(self._h, _ptr(r))
+        return r[:ni]
+
+    def factors(self, node: int):
+        lo, hi = self.tree()
+        m1 = hi[2 * node + 1] - lo[2 * node + 1]; m2 = hi[2 * node + 2] - lo[2 * node + 2]
+        r = int(self.ranks()[node])
+        U = np.zeros((max(r, 1), m1)); V = np.zeros((max(r, 1), m2))
+        _check(self._lib, self._lib.oracle_get_factors(self._h, node, _ptr(U), _ptr(V)))
+        return U[:r].T.copy(), V[:r].T.copy()
+
+    def logdet_parts(self):
+        nl = 1 << self.kappa; ni = nl - 1
+        a = np.zeros(nl); b = np.zeros(max(ni, 1))
+        _check(self._lib, self._lib.oracle_get_logdet_parts(self._h, _ptr(a), _ptr(b)))
+        return a, b[:ni]
