@@ -1,0 +1,134 @@
+/*
+ * hodlr.h -- C-ABI of the B200-native HODLR library (libhodlr_b200.so).
+ *
+ * Hot path of Ambikasaran et al., "Fast Direct Methods for Gaussian Processes"
+ * (arXiv:1403.6015): factor the GP covariance C = sigma2 I + K(x; theta) of
+ * 1-D points x into the HODLR product K_kappa K_{kappa-1} ... K_0
+ * (equation_HODLR_factorization), then log det C
+ * (equation_determinant_completely_multiplicative),
+ * the solve C^{-1} y (eq-fac) and the GP
+ * log-likelihood (eq. 1), all in FP64 on one B200 (sm_100a).
+ *
+ * Every step runs in hand-written CUDA kernels; there is no CPU fallback.
+ * The signatures carry plain pointers and sizes only (no torch types).
+ *
+ * Pointers: x, y and the solution are DEVICE pointers (contiguous FP64,
+ * the caller's original point order), caller-owned, read or written only
+ * during the call.  Scalars returned "_host" are host pointers.
+ * Ownership: hodlr_build copies x (sorted copy + permutation) into the handle;
+ * the handle owns all factors and device memory until hodlr_free.
+ * Ordering: all device work is enqueued on `cuda_stream` (NULL = legacy
+ * default stream); every call synchronises that stream before it returns its
+ * status, so statuses are final.
+ * State machine: build -> factor -> {logdet, solve, gp_loglik}*.  Any other
+ * order returns HODLR_ESTATE.  After factor the handle is read-only; one
+ * handle must not be used from two threads at once.
+ * Errors: every call returns a hodlr_status; hodlr_last_error() gives a
+ * thread-local message for the last failing call.
+ */
+#ifndef HODLR_B200_H
+#define HODLR_B200_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hodlr_s *hodlr_t;   /* opaque handle; owns all device memory */
+
+typedef enum {
+  HODLR_OK = 0,
+  HODLR_EINVAL = 1,    /* bad argument: n < 1, leaf < 1, eps not in (0,1), sigma2 < 0, ell <= 0, a < 0,
+                          unknown kernel, NaN/Inf in x or y, nrhs < 1, ld < n */
+  HODLR_ENOTPD = 2,    /* non-positive leaf Cholesky pivot, zero LU pivot or det <= 0 in a coupling
+                          system S_c; logdet/loglik return -INFINITY */
+  HODLR_ERANKCAP = 3,  /* an ACA block reached the rank cap without meeting eps (R12) */
+  HODLR_ESTATE = 4,    /* call out of order */
+  HODLR_ENOMEM = 5,    /* device allocation failed */
+  HODLR_ECUDA = 6,     /* CUDA runtime error (message has the CUDA error string) */
+  HODLR_ENCCL = 7      /* NCCL error (multi-GPU) */
+} hodlr_status;
+
+/* Covariance functions (Table I), theta = {a, ell}:
+ *   SE:        a^2 exp(-d^2 / (2 ell^2))
+ *   MATERN32:  a^2 (1 + s) exp(-s),          s = sqrt(3) |d| / ell
+ *   MATERN52:  a^2 (1 + s + s^2/3) exp(-s),  s = sqrt(5) |d| / ell
+ * C_ij = k(x_i - x_j) + sigma2 [i == j]. */
+typedef enum { HODLR_SE = 0, HODLR_MATERN32 = 1, HODLR_MATERN52 = 2 } hodlr_kernel;
+
+/* Multi-GPU descriptor (subtree sharding).  NULL => one GPU. */
+typedef struct {
+  int32_t rank, nranks;
+  const void *nccl_unique_id;   /* 128-byte ncclUniqueId from rank 0, broadcast by the caller */
+} hodlr_dist;
+
+/* Optional build options.  NULL => defaults. */
+typedef struct {
+  int32_t rank_cap;             /* max ACA rank per block; 0 => 64 (always clamped to min(m1, m2)) */
+  int32_t reserved[7];
+} hodlr_opts;
+
+typedef struct {
+  int32_t kappa;                /* tree depth, floor(log2(n / leaf)) (Fig. 6 line 1) */
+  int32_t leaf_min, leaf_max;   /* leaf block sizes, in [leaf, 2 leaf) */
+  int32_t K;                    /* ancestor columns per leaf = sum of per-depth max ranks */
+  int32_t max_rank_by_depth[64];   /* depth e = 1..kappa: max rank of the depth-(e-1) blocks */
+  double  mean_rank_by_depth[64];
+  int64_t factor_bytes;         /* device bytes held by the handle after factor */
+  double  t_build, t_factor, t_logdet, t_solve;   /* seconds (CUDA events), last call of each */
+  int64_t rank_cap_hits;        /* blocks that hit the rank cap */
+  int32_t aca_steps;            /* ACA pivot steps executed (max rank + 1) */
+  int32_t gpu_launches_last;    /* kernels launched by the last API call */
+} hodlr_info_t;
+
+/* "Assembly": stable sort of x (O(n), K1), balanced count-median
+ * tree with kappa = floor(log2(n/leaf)) levels, and ACA compression of every
+ * off-diagonal block K[c1,c2] ~ U V^T to relative eps (sec. 3.1).
+ * x: device, n doubles.  theta: HOST pointer to {a, ell}.  *out receives the handle. */
+hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const double *theta,
+                         double sigma2, int32_t leaf, double eps, const hodlr_dist *dist,
+                         const hodlr_opts *opts, void *cuda_stream, hodlr_t *out);
+
+/* "Factor" (Fig. 6): leaf Cholesky of K_kappa, bottom-up SMW coupling systems
+ * S_c = [[I, V^T K_c2^{-1} V], [U^T K_c1^{-1} U, I]] (equation_Low_Rank_Update)
+ * and their LU factors; accumulates log det C. */
+hodlr_status hodlr_factor(hodlr_t h);
+
+/* "Det." (sec. 4): log det C = sum_leaves 2 sum log L_ii + sum_c log det S_c.
+ * logdet_host: host double.  -INFINITY with HODLR_ENOTPD if the factorization failed. */
+hodlr_status hodlr_logdet(hodlr_t h, double *logdet_host);
+
+/* Solve C X = Y (eq-fac).  y, x: device, column-major n x nrhs with leading
+ * dimension ld >= n, original point order.  x may not alias y. */
+hodlr_status hodlr_solve(hodlr_t h, const double *y, double *x, int64_t nrhs, int64_t ld);
+
+/* GP log-likelihood (eq. 1): -1/2 y^T C^{-1} y - 1/2 log det C - (n/2) log(2 pi).
+ * y: device, n doubles.  out_host: host double (-INFINITY with HODLR_ENOTPD on failure). */
+hodlr_status gp_loglik(hodlr_t h, const double *y, double *out_host);
+
+/* Sizes, ranks and phase times.  info: host struct. */
+hodlr_status hodlr_info(hodlr_t h, hodlr_info_t *info);
+
+/* Copy the sorted points (n doubles) and the permutation perm[i] = original index of sorted
+ * position i (n int64) to DEVICE buffers; either may be NULL.  For parity tests (bit-exact). */
+hodlr_status hodlr_get_order(hodlr_t h, double *xs_dev, int64_t *perm_dev);
+
+/* Copy the tree (node ranges [lo, hi) in heap order, 2^(kappa+1)-1 nodes) and the ACA ranks of the
+ * 2^kappa - 1 internal nodes to HOST buffers; either may be NULL. */
+hodlr_status hodlr_get_tree(hodlr_t h, int64_t *lo_host, int64_t *hi_host, int32_t *ranks_host);
+
+/* Per-leaf (2^kappa) and per-internal-node (heap order) log det partials, HOST buffers. */
+hodlr_status hodlr_get_logdet_parts(hodlr_t h, double *leaf_parts_host, double *node_parts_host);
+
+/* Release everything the handle owns (stream-ordered).  NULL is a no-op. */
+void hodlr_free(hodlr_t h);
+
+/* Thread-local message of the last failing call (never NULL). */
+const char *hodlr_last_error(void);
+
+/* Library self-description, e.g. "hodlr_b200 sm_100a". */
+const char *hodlr_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

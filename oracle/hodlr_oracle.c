@@ -62,7 +62,17 @@ static double dot(const double *a, const double *b, int64_t m) {
 }
 
 /* Returns ORACLE_OK or ORACLE_ERANKCAP/ENOMEM; B->r is the rank. */
-static int aca(entry_fn f, const void *ctx, int64_t m1, int64_t m2, double eps, int cap, lowrank *B) {
+/* rowkey (may be NULL): coordinates of the rows (sorted).  Rows with a key equal to a used pivot row
+ * have identical residual rows and are treated as used as well (R2). */
+static void mark_row_run(char *used_r, const double *rowkey, int64_t m1, int64_t ik) {
+  used_r[ik] = 1;
+  if (!rowkey) return;
+  for (int64_t i = ik - 1; i >= 0 && rowkey[i] == rowkey[ik]; i--) used_r[i] = 1;
+  for (int64_t i = ik + 1; i < m1 && rowkey[i] == rowkey[ik]; i++) used_r[i] = 1;
+}
+
+static int aca(entry_fn f, const void *ctx, int64_t m1, int64_t m2, double eps, int cap, lowrank *B,
+               const double *rowkey) {
   memset(B, 0, sizeof *B);
   B->m1 = m1; B->m2 = m2;
   int64_t mn = m1 < m2 ? m1 : m2;
@@ -80,7 +90,7 @@ static int aca(entry_fn f, const void *ctx, int64_t m1, int64_t m2, double eps, 
       for (int l = 0; l < k; l++) v -= B->U[l][ik] * B->V[l][j];
       vt[j] = v;
     }
-    used_r[ik] = 1;
+    mark_row_run(used_r, rowkey, m1, ik);
     /* step 2: jk = smallest unused column maximising |v~_j| */
     int64_t jk = -1; double best = -1.0;
     for (int64_t j = 0; j < m2; j++)
@@ -139,7 +149,7 @@ int oracle_aca_dense(const double *A, int64_t m1, int64_t m2, int64_t lda, doubl
     return fail(ORACLE_EINVAL, "aca_dense: bad arguments");
   dense_ctx ctx = { A, lda };
   lowrank B;
-  int st = aca(dense_entry, &ctx, m1, m2, eps, cap, &B);
+  int st = aca(dense_entry, &ctx, m1, m2, eps, cap, &B, NULL);
   *rank = B.r;
   for (int l = 0; l < B.r; l++) {
     memcpy(U + (int64_t)l * m1, B.U[l], sizeof(double) * (size_t)m1);
@@ -254,7 +264,8 @@ int oracle_build(const double *x, int64_t n, int kernel, const double *theta, do
   for (int64_t c = 0; c < h->ninternal; c++) {
     int64_t c1 = 2 * c + 1, c2 = 2 * c + 2;
     blk_ctx ctx = { h, h->lo[c1], h->lo[c2] };
-    int st = aca(kernel_entry, &ctx, h->hi[c1] - h->lo[c1], h->hi[c2] - h->lo[c2], eps, rank_cap, &h->blk[c]);
+    int st = aca(kernel_entry, &ctx, h->hi[c1] - h->lo[c1], h->hi[c2] - h->lo[c2], eps, rank_cap, &h->blk[c],
+                 h->xs + h->lo[c1]);
     if (st != ORACLE_OK) {
       int code = st;
       char msg[400]; snprintf(msg, sizeof msg, "%.360s", g_err);

@@ -1,0 +1,391 @@
+// aca.cu -- G3: batched adaptive cross approximation of every off-diagonal block, all levels
+// concurrently (sec. 3.1; concrete pivot/stop rules DESIGN.md R1-R4, R12, R16).
+//
+// For internal node b with children c1 (rows) and c2 (columns) the block A = K[c1, c2] is
+// approximated by sum_k U'[:,k] V'[:,k]^T.  One ACA step k is two grid-wide passes over ALL
+// active blocks of ALL depths (one CTA per <= 128-chunk of a block side):
+//   row pass : v~_j = k(x_ik - x_j) - sum_{l<k} U'[ik,l] V'[j,l]  for j in c2; V'[:,k] = v~;
+//              argmax |v~_j| over unused columns; dots V'_l . v~ ; ||v~||^2
+//   col pass : u_i = (k(x_i - x_jk) - sum_{l<k} V'[jk,l] U'[i,l]) / v~_jk for i in c1; U'[:,k] = u;
+//              argmax |u_i| over unused rows; dots U'_l . u ; ||u||^2
+// The last CTA of each block to finish a pass reduces the per-CTA records in a fixed order
+// (deterministic) and advances the block state (pivot, ||S||_F^2 update, stop test).
+// The previous factor columns of the CTA's chunk are staged in shared memory once per sub-tile
+// and reused for the residual and for the dot products.
+#include "hodlr_internal.cuh"
+#include <vector>
+#include <algorithm>
+
+namespace {
+
+// ---------------------------------------------------------------------------------------------
+// shared reduction of the per-thread candidates + per-warp dot accumulators into one record
+// ---------------------------------------------------------------------------------------------
+__device__ void block_record(double best_abs, long long best_idx, double best_val, double nrm2,
+                             const double *acc /*[8]*/, int k, double *rec) {
+  __shared__ double s_abs[ACA_SUB / 32], s_val[ACA_SUB / 32], s_n2[ACA_SUB / 32];
+  __shared__ long long s_idx[ACA_SUB / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double a2 = __shfl_down_sync(0xffffffffu, best_abs, o);
+    long long i2 = __shfl_down_sync(0xffffffffu, best_idx, o);
+    double v2 = __shfl_down_sync(0xffffffffu, best_val, o);
+    if (amax_better(best_abs, best_idx, a2, i2)) { best_abs = a2; best_idx = i2; best_val = v2; }
+    nrm2 += __shfl_down_sync(0xffffffffu, nrm2, o);
+  }
+  // per-warp dot partials: warp w owns l = w + 8 s
+  for (int s = 0; s < 8; s++) {
+    int l = warp + 8 * s;
+    double v = warp_sum(acc[s]);
+    if (lane == 0 && l < k) rec[4 + l] = v;
+  }
+  if (lane == 0) { s_abs[warp] = best_abs; s_idx[warp] = best_idx; s_val[warp] = best_val; s_n2[warp] = nrm2; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double ba = s_abs[0], bv = s_val[0], n2 = s_n2[0]; long long bi = s_idx[0];
+    for (int w = 1; w < ACA_SUB / 32; w++) {
+      if (amax_better(ba, bi, s_abs[w], s_idx[w])) { ba = s_abs[w]; bi = s_idx[w]; bv = s_val[w]; }
+      n2 += s_n2[w];
+    }
+    rec[0] = ba; rec[1] = (double)bi; rec[2] = bv; rec[3] = n2;
+  }
+}
+
+// Reduce the nq records of a block in fixed order.  Results in shared out[]: [0] abs [1] idx [2] val
+// [3] nrm2 [4+l] dots.  Called by all threads of the last CTA.
+__device__ void reduce_records(const double *rec0, int nq, int k, double *out) {
+  __shared__ double s_abs[ACA_SUB], s_val[ACA_SUB];
+  __shared__ long long s_idx[ACA_SUB];
+  const int t = threadIdx.x;
+  double ba = 0.0, bv = 0.0; long long bi = -1;
+  for (int q = t; q < nq; q += ACA_SUB) {
+    const double *r = rec0 + (long long)q * ACA_RECW;
+    double a = __ldcg(r + 0); long long i = (long long)__ldcg(r + 1);
+    if (amax_better(ba, bi, a, i)) { ba = a; bi = i; bv = __ldcg(r + 2); }
+  }
+  s_abs[t] = ba; s_idx[t] = bi; s_val[t] = bv;
+  // sums: thread j (j <= k) sums column (3 + j) over q in order; j = 0 -> nrm2, j >= 1 -> dot l = j - 1
+  if (t <= k) {
+    double s = 0.0;
+    for (int q = 0; q < nq; q++) s += __ldcg(rec0 + (long long)q * ACA_RECW + 3 + t);
+    out[3 + t] = s;
+  }
+  __syncthreads();
+  if (t == 0) {
+    for (int j = 1; j < ACA_SUB; j++)
+      if (amax_better(ba, bi, s_abs[j], s_idx[j])) { ba = s_abs[j]; bi = s_idx[j]; bv = s_val[j]; }
+    out[0] = ba; out[1] = (double)bi; out[2] = bv;
+  }
+  __syncthreads();
+}
+
+// Rows with the same coordinate as a used pivot row have identical residual rows: mark the whole
+// run of equal sorted coordinates inside c1 as used (R2).  Single thread.
+__device__ void mark_row_run(const AcaCtx &c, unsigned char *used, long long lo1, long long m1, long long ik) {
+  const double v = c.xs[lo1 + ik];
+  used[lo1 + ik] = 1;
+  for (long long i = ik - 1; i >= 0 && c.xs[lo1 + i] == v; i--) used[lo1 + i] = 1;
+  for (long long i = ik + 1; i < m1 && c.xs[lo1 + i] == v; i++) used[lo1 + i] = 1;
+}
+
+__global__ void k_aca_init(AcaCtx c, int nblocks, int cap) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nblocks) return;
+  long long c1 = 2LL * b + 1, c2 = 2LL * b + 2;
+  long long m1 = c.hi[c1] - c.lo[c1], m2 = c.hi[c2] - c.lo[c2];
+  long long mn = m1 < m2 ? m1 : m2;
+  AcaState *s = &c.st[b];
+  s->k = 0; s->done = 0; s->cnt_r = 0; s->cnt_c = 0;
+  s->cap = (int)(cap < mn ? cap : mn);
+  s->ipiv = m1 - 1;                      // DESIGN.md R2: last row of c1 (the point nearest c2)
+  s->jpiv = -1; s->pivval = 0.0; s->S2 = 0.0; s->nv2 = 0.0;
+  int e = c.bdepth[b] + 1;
+  mark_row_run(c, c.used + (long long)(e - 1) * c.n, c.lo[c1], m1, m1 - 1);
+  c.rank[b] = 0;
+}
+
+// Row pass: one CTA per (block, chunk of c2).
+__global__ void __launch_bounds__(ACA_SUB) k_aca_row(AcaCtx c) {
+  extern __shared__ double sm[];
+  const AcaItem it = c.items[blockIdx.x];
+  const int b = it.block;
+  AcaState *st = &c.st[b];
+  if (st->done) return;
+  const int k = st->k;
+  const long long n = c.n;
+  const long long c1 = 2LL * b + 1, c2 = 2LL * b + 2;
+  const long long lo1 = c.lo[c1], lo2 = c.lo[c2], m2 = c.hi[c2] - lo2;
+  const int e = c.bdepth[b] + 1;
+  double *slot = c.Xh + c.dt->colbase[e] * n;
+  const unsigned char *used = c.used + (long long)(e - 1) * n;
+  const long long ig = lo1 + st->ipiv;
+  const double xi = c.xs[ig];
+  __shared__ double Ui[ACA_MAXCAP];
+  double *Vs = sm;                       // [k][ACA_SUB]
+  double *vb = sm + (long long)k * ACA_SUB;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  for (int l = t; l < k; l += ACA_SUB) Ui[l] = slot[(long long)l * n + ig];
+  double acc[8];
+#pragma unroll
+  for (int s = 0; s < 8; s++) acc[s] = 0.0;
+  double best_abs = 0.0, best_val = 0.0, nrm2 = 0.0; long long best_idx = -1;
+  __syncthreads();
+  for (long long s0 = it.start; s0 < it.start + it.len; s0 += ACA_SUB) {
+    const long long j = s0 + t;
+    const bool valid = j < it.start + it.len && j < m2;
+    const long long gj = lo2 + j;
+    double v = 0.0;
+    if (valid) {
+      v = kval(c.kp, xi - c.xs[gj]);
+      for (int l = 0; l < k; l++) {
+        double vl = slot[(long long)l * n + gj];
+        Vs[l * ACA_SUB + t] = vl;
+        v -= Ui[l] * vl;
+      }
+      slot[(long long)k * n + gj] = v;                  // V'[:,k] = raw residual row
+      if (!used[gj] && amax_better(best_abs, best_idx, fabs(v), j)) { best_abs = fabs(v); best_idx = j; best_val = v; }
+      nrm2 += v * v;
+    } else {
+      for (int l = 0; l < k; l++) Vs[l * ACA_SUB + t] = 0.0;
+    }
+    vb[t] = v;
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < 8; s++) {
+      int l = warp + 8 * s;
+      if (l < k) {
+        double a = 0.0;
+        for (int q = lane; q < ACA_SUB; q += 32) a += Vs[l * ACA_SUB + q] * vb[q];
+        acc[s] += a;
+      }
+    }
+    __syncthreads();
+  }
+  const int nq = c.nq[b];
+  double *rec0 = c.rec + c.recbase[b] * ACA_RECW;
+  block_record(best_abs, best_idx, best_val, nrm2, acc, k, rec0 + (long long)it.q * ACA_RECW);
+  __shared__ int amLast;
+  __threadfence();
+  __syncthreads();
+  if (t == 0) amLast = (atomicAdd(&st->cnt_r, 1) == nq - 1);
+  __syncthreads();
+  if (!amLast) return;
+  __threadfence();
+  __shared__ double out[4 + ACA_MAXCAP];
+  reduce_records(rec0, nq, k, out);
+  if (t < k) st->dV[t] = out[4 + t];
+  if (t == 0) {
+    st->cnt_r = 0;
+    long long jk = (long long)out[1];
+    if (jk < 0 || out[0] == 0.0) {                      // exactly-zero residual row: rank k
+      st->done = 1; c.rank[b] = k; atomicSub(c.active, 1);
+    } else {
+      st->jpiv = jk; st->pivval = out[2]; st->nv2 = out[3];
+      c.used[(long long)(e - 1) * n + lo2 + jk] = 1;
+    }
+  }
+}
+
+// Column pass: one CTA per (block, chunk of c1).
+__global__ void __launch_bounds__(ACA_SUB) k_aca_col(AcaCtx c, int *flags) {
+  extern __shared__ double sm[];
+  const AcaItem it = c.items[blockIdx.x];
+  const int b = it.block;
+  AcaState *st = &c.st[b];
+  if (st->done) return;
+  const int k = st->k;
+  const long long n = c.n;
+  const long long c1 = 2LL * b + 1, c2 = 2LL * b + 2;
+  const long long lo1 = c.lo[c1], m1 = c.hi[c1] - lo1, lo2 = c.lo[c2], m2 = c.hi[c2] - lo2;
+  const int e = c.bdepth[b] + 1;
+  double *slot = c.Xh + c.dt->colbase[e] * n;
+  const unsigned char *used = c.used + (long long)(e - 1) * n;
+  const long long jg = lo2 + st->jpiv;
+  const double xj = c.xs[jg];
+  const double rp = 1.0 / st->pivval;
+  __shared__ double Vj[ACA_MAXCAP];
+  double *Us = sm;
+  double *ub = sm + (long long)k * ACA_SUB;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  for (int l = t; l < k; l += ACA_SUB) Vj[l] = slot[(long long)l * n + jg];
+  double acc[8];
+#pragma unroll
+  for (int s = 0; s < 8; s++) acc[s] = 0.0;
+  double best_abs = 0.0, best_val = 0.0, nrm2 = 0.0; long long best_idx = -1;
+  __syncthreads();
+  for (long long s0 = it.start; s0 < it.start + it.len; s0 += ACA_SUB) {
+    const long long i = s0 + t;
+    const bool valid = i < it.start + it.len && i < m1;
+    const long long gi = lo1 + i;
+    double u = 0.0;
+    if (valid) {
+      u = kval(c.kp, c.xs[gi] - xj);
+      for (int l = 0; l < k; l++) {
+        double ul = slot[(long long)l * n + gi];
+        Us[l * ACA_SUB + t] = ul;
+        u -= Vj[l] * ul;
+      }
+      u *= rp;
+      slot[(long long)k * n + gi] = u;                  // U'[:,k] = column residual / pivot
+      if (!used[gi] && amax_better(best_abs, best_idx, fabs(u), i)) { best_abs = fabs(u); best_idx = i; best_val = u; }
+      nrm2 += u * u;
+    } else {
+      for (int l = 0; l < k; l++) Us[l * ACA_SUB + t] = 0.0;
+    }
+    ub[t] = u;
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < 8; s++) {
+      int l = warp + 8 * s;
+      if (l < k) {
+        double a = 0.0;
+        for (int q = lane; q < ACA_SUB; q += 32) a += Us[l * ACA_SUB + q] * ub[q];
+        acc[s] += a;
+      }
+    }
+    __syncthreads();
+  }
+  const int nq = c.nq[b];
+  double *rec0 = c.rec + c.recbase[b] * ACA_RECW;
+  block_record(best_abs, best_idx, best_val, nrm2, acc, k, rec0 + (long long)it.q * ACA_RECW);
+  __shared__ int amLast;
+  __threadfence();
+  __syncthreads();
+  if (t == 0) amLast = (atomicAdd(&st->cnt_c, 1) == nq - 1);
+  __syncthreads();
+  if (!amLast) return;
+  __threadfence();
+  __shared__ double out[4 + ACA_MAXCAP];
+  reduce_records(rec0, nq, k, out);
+  if (t == 0) {
+    st->cnt_c = 0;
+    // ||S_{k+1}||^2 = ||S_k||^2 + 2 sum_{l<k} (U'_k.U'_l)(V'_l.V'_k) + ||U'_k||^2 ||V'_k||^2
+    double cross = 0.0;
+    for (int l = 0; l < k; l++) cross += out[4 + l] * st->dV[l];
+    const double nu2 = out[3], nv2 = st->nv2;
+    const double S2 = st->S2 + 2.0 * cross + nu2 * nv2;
+    st->S2 = S2;
+    const int k1 = k + 1;
+    st->k = k1;
+    const long long mn = m1 < m2 ? m1 : m2;
+    int done = 0;
+    if (sqrt(nu2) * sqrt(nv2) <= c.eps * sqrt(fabs(S2))) done = 1;     // stop term is kept
+    else if (k1 == mn) done = 1;
+    else if (k1 == st->cap) { done = 2; atomicAdd(&flags[5], 1); }
+    else {
+      long long ik = (long long)out[1];
+      if (ik < 0 || out[0] == 0.0) done = 1;
+      else { st->ipiv = ik; mark_row_run(c, c.used + (long long)(e - 1) * n, lo1, m1, ik); }
+    }
+    if (done) { st->done = done; c.rank[b] = k1; atomicSub(c.active, 1); }
+  }
+}
+
+}  // namespace
+
+hodlr_status hodlr_aca(hodlr_s *h) {
+  const long long nb = h->ninternal;
+  if (nb == 0) return HODLR_OK;
+  const long long n = h->n;
+  // ---- host plan: chunking per block side, items sorted big blocks first ----
+  std::vector<AcaItem> items_r, items_c;
+  std::vector<int> nq_r(nb), nq_c(nb);
+  std::vector<long long> rb_r(nb), rb_c(nb);
+  std::vector<int> bdepth(nb);
+  long long nrec_r = 0, nrec_c = 0;
+  for (long long b = 0; b < nb; b++) {
+    bdepth[b] = hodlr_depth_of(b);
+    long long m1 = h->h_hi[2 * b + 1] - h->h_lo[2 * b + 1], m2 = h->h_hi[2 * b + 2] - h->h_lo[2 * b + 2];
+    for (int side = 0; side < 2; side++) {
+      long long m = side == 0 ? m2 : m1;
+      long long chunk = (m + 127) / 128;
+      chunk = ((chunk + ACA_SUB - 1) / ACA_SUB) * ACA_SUB;
+      if (chunk < ACA_SUB) chunk = ACA_SUB;
+      int q = 0;
+      for (long long s = 0; s < m; s += chunk, q++) {
+        AcaItem it; it.block = (int)b; it.q = q; it.start = s; it.len = (int)std::min(chunk, m - s); it.pad = 0;
+        (side == 0 ? items_r : items_c).push_back(it);
+      }
+      if (side == 0) { nq_r[b] = q; rb_r[b] = nrec_r; nrec_r += q; }
+      else { nq_c[b] = q; rb_c[b] = nrec_c; nrec_c += q; }
+    }
+  }
+  // ---- device buffers ----
+  AcaItem *d_items_r = (AcaItem *)hodlr_dalloc(h, sizeof(AcaItem) * items_r.size());
+  AcaItem *d_items_c = (AcaItem *)hodlr_dalloc(h, sizeof(AcaItem) * items_c.size());
+  int *d_nq = (int *)hodlr_dalloc(h, sizeof(int) * 2 * nb);
+  long long *d_rb = (long long *)hodlr_dalloc(h, sizeof(long long) * 2 * nb);
+  double *d_rec = (double *)hodlr_dalloc(h, sizeof(double) * ACA_RECW * (size_t)(nrec_r + nrec_c));
+  h->ast = (AcaState *)hodlr_dalloc(h, sizeof(AcaState) * nb);
+  h->rank = (int *)hodlr_dalloc(h, sizeof(int) * nb);
+  h->bdepth = (int *)hodlr_dalloc(h, sizeof(int) * nb);
+  h->used = (unsigned char *)hodlr_dalloc(h, (size_t)h->kappa * n);
+  if (!d_items_r || !d_items_c || !d_nq || !d_rb || !d_rec || !h->ast || !h->rank || !h->bdepth || !h->used)
+    return hodlr_set_error(HODLR_ENOMEM, "aca: device allocation failed");
+  std::vector<int> nq_all(nq_r); nq_all.insert(nq_all.end(), nq_c.begin(), nq_c.end());
+  std::vector<long long> rb_all(rb_r); rb_all.insert(rb_all.end(), rb_c.begin(), rb_c.end());
+  HCUDA(cudaMemcpyAsync(d_items_r, items_r.data(), sizeof(AcaItem) * items_r.size(), cudaMemcpyHostToDevice, h->st));
+  HCUDA(cudaMemcpyAsync(d_items_c, items_c.data(), sizeof(AcaItem) * items_c.size(), cudaMemcpyHostToDevice, h->st));
+  HCUDA(cudaMemcpyAsync(d_nq, nq_all.data(), sizeof(int) * 2 * nb, cudaMemcpyHostToDevice, h->st));
+  HCUDA(cudaMemcpyAsync(d_rb, rb_all.data(), sizeof(long long) * 2 * nb, cudaMemcpyHostToDevice, h->st));
+  HCUDA(cudaMemcpyAsync(h->bdepth, bdepth.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, h->st));
+  HCUDA(cudaMemsetAsync(h->used, 0, (size_t)h->kappa * n, h->st));
+  int nbi = (int)nb;
+  HCUDA(cudaMemcpyAsync(h->dflags + 4, &nbi, sizeof(int), cudaMemcpyHostToDevice, h->st));
+  // the pageable copies above are staged synchronously by the runtime, so the vectors may die
+
+  AcaCtx c;
+  c.kp = h->kp; c.n = n; c.eps = h->eps; c.xs = h->xs; c.lo = h->lo; c.hi = h->hi; c.Xh = h->Xh;
+  c.used = h->used; c.st = h->ast; c.active = h->dflags + 4; c.rank = h->rank; c.bdepth = h->bdepth;
+  c.dt = h->d_dt;
+  k_aca_init<<<(int)((nb + 255) / 256), 256, 0, h->st>>>(c, (int)nb, h->cap);
+  HLAUNCH(h, "k_aca_init");
+
+  AcaCtx cr = c, cc = c;
+  cr.items = d_items_r; cr.nq = d_nq; cr.recbase = d_rb; cr.rec = d_rec;
+  cc.items = d_items_c; cc.nq = d_nq + nb; cc.recbase = d_rb + nb; cc.rec = d_rec + ACA_RECW * nrec_r;
+  static bool attr_set = false;
+  if (!attr_set) {
+    size_t maxsm = (size_t)(ACA_MAXCAP + 1) * ACA_SUB * sizeof(double);
+    HCUDA(cudaFuncSetAttribute(k_aca_row, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
+    HCUDA(cudaFuncSetAttribute(k_aca_col, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
+    attr_set = true;
+  }
+  int *pinned = nullptr;
+  HCUDA(cudaMallocHost(&pinned, sizeof(int) * 8));
+  cudaEvent_t evs[8];
+  for (int i = 0; i < 8; i++) HCUDA(cudaEventCreateWithFlags(&evs[i], cudaEventDisableTiming));
+  int issued = 0, checked = 0, steps = 0;
+  hodlr_status status = HODLR_OK;
+  const int maxsteps = h->cap + 1;
+  for (int k = 0; k < maxsteps; k++) {
+    size_t smem = (size_t)(k + 1) * ACA_SUB * sizeof(double);
+    k_aca_row<<<(int)items_r.size(), ACA_SUB, smem, h->st>>>(cr);
+    HLAUNCH(h, "k_aca_row");
+    k_aca_col<<<(int)items_c.size(), ACA_SUB, smem, h->st>>>(cc, h->dflags);
+    HLAUNCH(h, "k_aca_col");
+    steps = k + 1;
+    // lagged poll of the active-block counter (no pipeline bubble)
+    int slot = issued % 8;
+    HCUDA(cudaMemcpyAsync(&pinned[slot], h->dflags + 4, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+    HCUDA(cudaEventRecord(evs[slot], h->st));
+    issued++;
+    bool stop = false;
+    while (checked < issued) {
+      int cs = checked % 8;
+      cudaError_t q = (issued - checked >= 3) ? cudaEventSynchronize(evs[cs]) : cudaEventQuery(evs[cs]);
+      if (q == cudaErrorNotReady) break;
+      if (q != cudaSuccess) { status = hodlr_cuda_check(q, "aca poll"); stop = true; break; }
+      if (pinned[cs] == 0) stop = true;
+      checked++;
+    }
+    if (stop) break;
+  }
+  HCUDA(cudaStreamSynchronize(h->st));
+  for (int i = 0; i < 8; i++) cudaEventDestroy(evs[i]);
+  cudaFreeHost(pinned);
+  if (status != HODLR_OK) return status;
+  h->aca_steps = steps;
+  return HODLR_OK;
+}

@@ -1,0 +1,311 @@
+// api.cu -- the C-ABI of include/hodlr.h: validation, host plan, memory, phase orchestration.
+#include "hodlr_internal.cuh"
+#include <stdio.h>
+#include <stdarg.h>
+#include <string.h>
+#include <limits.h>
+#include <new>
+#include <vector>
+
+static thread_local char g_err[1024] = "";
+
+hodlr_status hodlr_set_error(hodlr_status code, const char *fmt, ...) {
+  va_list ap; va_start(ap, fmt); vsnprintf(g_err, sizeof g_err, fmt, ap); va_end(ap);
+  return code;
+}
+
+hodlr_status hodlr_cuda_check(cudaError_t e, const char *what) {
+  if (e == cudaErrorMemoryAllocation) return hodlr_set_error(HODLR_ENOMEM, "%s: %s", what, cudaGetErrorString(e));
+  return hodlr_set_error(HODLR_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+void *hodlr_dalloc(hodlr_s *h, size_t bytes) {
+  void *p = nullptr;
+  if (bytes == 0) bytes = 8;
+  if (cudaMallocAsync(&p, bytes, h->st) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+  if (h->nallocs >= (int)(sizeof(h->allocs) / sizeof(h->allocs[0]))) { cudaFreeAsync(p, h->st); return nullptr; }
+  h->allocs[h->nallocs++] = p;
+  h->bytes += (long long)bytes;
+  return p;
+}
+
+static void setup_pool(int dev) {
+  static int done_dev = -1;
+  if (done_dev == dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    unsigned long long thr = ~0ULL;    // keep freed blocks in the pool: repeated builds reuse them
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done_dev = dev;
+}
+
+static hodlr_status finish(hodlr_s *h, hodlr_status st, double *tsec) {
+  cudaError_t e1 = cudaEventRecord(h->ev1, h->st);
+  cudaError_t e2 = cudaStreamSynchronize(h->st);
+  if (st != HODLR_OK) return st;
+  if (e1 != cudaSuccess) return hodlr_cuda_check(e1, "event record");
+  if (e2 != cudaSuccess) return hodlr_cuda_check(e2, "stream synchronize");
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, h->ev0, h->ev1) == cudaSuccess && tsec) *tsec = ms * 1e-3;
+  return HODLR_OK;
+}
+
+extern "C" {
+
+const char *hodlr_last_error(void) { return g_err; }
+const char *hodlr_version(void) { return "hodlr_b200 0.1 sm_100a fp64"; }
+
+void hodlr_free(hodlr_t h) {
+  if (!h) return;
+  for (int i = h->nallocs - 1; i >= 0; i--) cudaFreeAsync(h->allocs[i], h->st);
+  cudaStreamSynchronize(h->st);
+  if (h->ev0) cudaEventDestroy(h->ev0);
+  if (h->ev1) cudaEventDestroy(h->ev1);
+  delete[] h->h_lo; delete[] h->h_hi; delete[] h->h_rank;
+  delete h;
+}
+
+hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const double *theta, double sigma2,
+                         int32_t leaf, double eps, const hodlr_dist *dist, const hodlr_opts *opts, void *cuda_stream,
+                         hodlr_t *out) {
+  if (!out) return hodlr_set_error(HODLR_EINVAL, "build: out is NULL");
+  *out = nullptr;
+  if (!x || !theta) return hodlr_set_error(HODLR_EINVAL, "build: NULL x or theta");
+  if (n < 1) return hodlr_set_error(HODLR_EINVAL, "build: n = %lld < 1", (long long)n);
+  if (leaf < 1) return hodlr_set_error(HODLR_EINVAL, "build: leaf = %d < 1", leaf);
+  if (!(eps > 0.0 && eps < 1.0)) return hodlr_set_error(HODLR_EINVAL, "build: eps = %g not in (0, 1)", eps);
+  if (!(sigma2 >= 0.0) || !isfinite(sigma2)) return hodlr_set_error(HODLR_EINVAL, "build: sigma2 = %g", sigma2);
+  if (!(theta[1] > 0.0) || !isfinite(theta[1])) return hodlr_set_error(HODLR_EINVAL, "build: ell = %g <= 0", theta[1]);
+  if (!(theta[0] >= 0.0) || !isfinite(theta[0])) return hodlr_set_error(HODLR_EINVAL, "build: a = %g < 0", theta[0]);
+  if ((int)kernel < 0 || (int)kernel > 2) return hodlr_set_error(HODLR_EINVAL, "build: unknown kernel %d", (int)kernel);
+  if (dist && dist->nranks > 1) return hodlr_set_error(HODLR_EINVAL, "build: multi-GPU sharding not available in this build");
+  int cap = (opts && opts->rank_cap > 0) ? opts->rank_cap : 64;
+  if (cap > ACA_MAXCAP) return hodlr_set_error(HODLR_EINVAL, "build: rank_cap %d > %d", cap, ACA_MAXCAP);
+  hodlr_s *h = new (std::nothrow) hodlr_s();
+  if (!h) return hodlr_set_error(HODLR_ENOMEM, "build: host allocation failed");
+  memset((void *)h, 0, sizeof(*h));
+  h->st = (cudaStream_t)cuda_stream;
+  hodlr_status st = HODLR_OK;
+  cudaError_t ce = cudaGetDevice(&h->dev);
+  if (ce != cudaSuccess) { delete h; return hodlr_cuda_check(ce, "cudaGetDevice"); }
+  setup_pool(h->dev);
+  cudaEventCreate(&h->ev0); cudaEventCreate(&h->ev1);
+  cudaEventRecord(h->ev0, h->st);
+  h->n = n; h->leaf = leaf; h->eps = eps; h->cap = cap; h->theta[0] = theta[0]; h->theta[1] = theta[1];
+  h->kp.kern = (int)kernel; h->kp.a2 = theta[0] * theta[0]; h->kp.s2 = sigma2;
+  h->kp.c = kernel == HODLR_SE ? 1.0 / (2.0 * theta[1] * theta[1])
+                               : (kernel == HODLR_MATERN32 ? sqrt(3.0) : sqrt(5.0)) / theta[1];
+  // O2-equivalent tree: kappa = largest integer with leaf * 2^kappa <= n
+  int kappa = 0;
+  while (((long long)leaf << (kappa + 1)) <= n && kappa < HODLR_MAXDEPTH - 2) kappa++;
+  h->kappa = kappa;
+  h->nnodes = (1LL << (kappa + 1)) - 1; h->ninternal = (1LL << kappa) - 1; h->nleaves = 1LL << kappa;
+  h->h_lo = new long long[h->nnodes]; h->h_hi = new long long[h->nnodes];
+  h->h_rank = new int[h->ninternal > 0 ? h->ninternal : 1]();
+  h->h_lo[0] = 0; h->h_hi[0] = n;
+  for (long long c = 0; c < h->ninternal; c++) {          // count-median split, left = ceil(m/2)
+    long long m = h->h_hi[c] - h->h_lo[c], half = (m + 1) / 2;
+    h->h_lo[2 * c + 1] = h->h_lo[c]; h->h_hi[2 * c + 1] = h->h_lo[c] + half;
+    h->h_lo[2 * c + 2] = h->h_lo[c] + half; h->h_hi[2 * c + 2] = h->h_hi[c];
+  }
+  h->leaf_min = INT_MAX; h->leaf_max = 0;
+  for (long long l = 0; l < h->nleaves; l++) {
+    long long m = h->h_hi[h->ninternal + l] - h->h_lo[h->ninternal + l];
+    if (m < h->leaf_min) h->leaf_min = (int)m;
+    if (m > h->leaf_max) h->leaf_max = (int)m;
+  }
+  // panel slots: depth e holds min(cap, max node size at depth e) columns
+  long long cols = 0;
+  for (int e = 1; e <= kappa; e++) {
+    long long mmax = 0;
+    for (long long id = (1LL << e) - 1; id < (2LL << e) - 1; id++) mmax = std::max(mmax, h->h_hi[id] - h->h_lo[id]);
+    h->dt.capd[e] = (int)std::min<long long>(cap, mmax);
+    h->dt.colbase[e] = cols;
+    cols += h->dt.capd[e];
+  }
+  h->xh_cols = cols;
+  h->xs = (double *)hodlr_dalloc(h, sizeof(double) * n);
+  h->perm = (long long *)hodlr_dalloc(h, sizeof(long long) * n);
+  h->lo = (long long *)hodlr_dalloc(h, sizeof(long long) * h->nnodes);
+  h->hi = (long long *)hodlr_dalloc(h, sizeof(long long) * h->nnodes);
+  h->dflags = (int *)hodlr_dalloc(h, sizeof(int) * 16);
+  h->d_dt = (DepthTab *)hodlr_dalloc(h, sizeof(DepthTab));
+  h->Xh = (double *)hodlr_dalloc(h, sizeof(double) * (size_t)n * (size_t)(cols > 0 ? cols : 1));
+  if (!h->xs || !h->perm || !h->lo || !h->hi || !h->dflags || !h->d_dt || !h->Xh) {
+    hodlr_free(h);
+    return hodlr_set_error(HODLR_ENOMEM, "build: device allocation of %.2f GB failed",
+                           1e-9 * (double)(8.0 * n * (cols + 4)));
+  }
+  int fl[16] = {0}; fl[2] = INT_MAX;
+#define CK(call) do { cudaError_t _e = (call); if (_e != cudaSuccess) { st = hodlr_cuda_check(_e, #call); goto fail; } } while (0)
+  CK(cudaMemcpyAsync(h->dflags, fl, sizeof(fl), cudaMemcpyHostToDevice, h->st));
+  CK(cudaMemcpyAsync(h->lo, h->h_lo, sizeof(long long) * h->nnodes, cudaMemcpyHostToDevice, h->st));
+  CK(cudaMemcpyAsync(h->hi, h->h_hi, sizeof(long long) * h->nnodes, cudaMemcpyHostToDevice, h->st));
+  CK(cudaMemcpyAsync(h->d_dt, &h->dt, sizeof(DepthTab), cudaMemcpyHostToDevice, h->st));
+  st = hodlr_sort_and_tree(h, x);
+  if (st != HODLR_OK) goto fail;
+  {
+    int f0 = 0;
+    CK(cudaMemcpyAsync(&f0, h->dflags, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    if (f0) { st = hodlr_set_error(HODLR_EINVAL, "build: x contains NaN or Inf"); goto fail; }
+  }
+  st = hodlr_aca(h);
+  if (st != HODLR_OK) goto fail;
+  {
+    int f5 = 0;
+    CK(cudaMemcpyAsync(&f5, h->dflags + 5, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+    if (h->ninternal > 0)
+      CK(cudaMemcpyAsync(h->h_rank, h->rank, sizeof(int) * h->ninternal, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    h->rank_cap_hits = f5;
+    if (f5) { st = hodlr_set_error(HODLR_ERANKCAP, "build: %d block(s) reached the rank cap %d without meeting eps", f5, cap); goto fail; }
+  }
+  h->dt.Kdim[0] = 0;
+  for (int e = 1; e <= kappa; e++) {
+    int r = 0;
+    for (long long b = (1LL << (e - 1)) - 1; b < (1LL << e) - 1; b++) r = std::max(r, h->h_rank[b]);
+    h->dt.rdep[e] = r;
+    h->dt.Kdim[e] = h->dt.Kdim[e - 1] + r;
+  }
+  CK(cudaMemcpyAsync(h->d_dt, &h->dt, sizeof(DepthTab), cudaMemcpyHostToDevice, h->st));
+  st = finish(h, HODLR_OK, &h->t_build);
+  if (st != HODLR_OK) goto fail;
+  h->state = 1;
+  *out = h;
+  return HODLR_OK;
+fail:
+  cudaStreamSynchronize(h->st);
+  hodlr_free(h);
+  return st;
+#undef CK
+}
+
+hodlr_status hodlr_factor(hodlr_t h) {
+  if (!h) return hodlr_set_error(HODLR_EINVAL, "factor: NULL handle");
+  if (h->state != 1) return hodlr_set_error(HODLR_ESTATE, "factor: handle is not in the built state");
+  h->launches = 0;
+  cudaEventRecord(h->ev0, h->st);
+  hodlr_status st = hodlr_factor_impl(h);
+  st = finish(h, st, &h->t_factor);
+  if (st != HODLR_OK) { h->state = -1; h->logdet = -INFINITY; return st; }
+  int f[3];
+  cudaError_t e = cudaMemcpy(f, h->dflags, sizeof(f), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return hodlr_cuda_check(e, "factor flags");
+  if (f[1]) {
+    h->state = -1; h->logdet = -INFINITY;
+    return hodlr_set_error(HODLR_ENOTPD, "factor: node %d is not positive definite (%d failures)", f[2], f[1]);
+  }
+  e = cudaMemcpy(&h->logdet, h->d_logdet, sizeof(double), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return hodlr_cuda_check(e, "factor logdet");
+  h->state = 2;
+  return HODLR_OK;
+}
+
+hodlr_status hodlr_logdet(hodlr_t h, double *logdet_host) {
+  if (!h || !logdet_host) return hodlr_set_error(HODLR_EINVAL, "logdet: NULL argument");
+  if (h->state == -1) { *logdet_host = -INFINITY; return hodlr_set_error(HODLR_ENOTPD, "logdet: factorization failed"); }
+  if (h->state != 2) return hodlr_set_error(HODLR_ESTATE, "logdet: not factored");
+  *logdet_host = h->logdet;
+  h->t_logdet = 0.0;
+  return HODLR_OK;
+}
+
+static hodlr_status check_y_flag(hodlr_t h) {
+  int f3 = 0;
+  cudaError_t e = cudaMemcpy(&f3, h->dflags + 3, sizeof(int), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return hodlr_cuda_check(e, "solve flags");
+  if (f3) {
+    int z = 0;
+    cudaMemcpy(h->dflags + 3, &z, sizeof(int), cudaMemcpyHostToDevice);
+    return hodlr_set_error(HODLR_EINVAL, "y contains NaN or Inf");
+  }
+  return HODLR_OK;
+}
+
+hodlr_status hodlr_solve(hodlr_t h, const double *y, double *x, int64_t nrhs, int64_t ld) {
+  if (!h || !y || !x) return hodlr_set_error(HODLR_EINVAL, "solve: NULL argument");
+  if (h->state == -1) return hodlr_set_error(HODLR_ENOTPD, "solve: factorization failed");
+  if (h->state != 2) return hodlr_set_error(HODLR_ESTATE, "solve: not factored");
+  if (nrhs < 1 || ld < h->n) return hodlr_set_error(HODLR_EINVAL, "solve: nrhs = %lld, ld = %lld", (long long)nrhs, (long long)ld);
+  h->launches = 0;
+  cudaEventRecord(h->ev0, h->st);
+  hodlr_status st = HODLR_OK;
+  for (int64_t j = 0; j < nrhs && st == HODLR_OK; j++) st = hodlr_solve_impl(h, y + j * ld, x + j * ld, false);
+  st = finish(h, st, &h->t_solve);
+  if (st != HODLR_OK) return st;
+  return check_y_flag(h);
+}
+
+hodlr_status gp_loglik(hodlr_t h, const double *y, double *out_host) {
+  if (!h || !y || !out_host) return hodlr_set_error(HODLR_EINVAL, "gp_loglik: NULL argument");
+  if (h->state == -1) { *out_host = -INFINITY; return hodlr_set_error(HODLR_ENOTPD, "gp_loglik: factorization failed"); }
+  if (h->state != 2) return hodlr_set_error(HODLR_ESTATE, "gp_loglik: not factored");
+  h->launches = 0;
+  cudaEventRecord(h->ev0, h->st);
+  hodlr_status st = hodlr_solve_impl(h, y, nullptr, true);
+  double yCy = 0.0;
+  if (st == HODLR_OK) {   // h at the root = y^T C^{-1} y
+    double hh[2] = {0.0, 0.0};
+    cudaError_t e = cudaMemcpyAsync(hh, h->hvec, sizeof(hh), cudaMemcpyDeviceToHost, h->st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->st);
+    yCy = hh[0] + hh[1];
+    if (e != cudaSuccess) st = hodlr_cuda_check(e, "gp_loglik copy");
+  }
+  double tdummy = 0;
+  st = finish(h, st, &tdummy);
+  if (st != HODLR_OK) return st;
+  st = check_y_flag(h);
+  if (st != HODLR_OK) return st;
+  // -1/2 y^T C^{-1} y - 1/2 log det C - (n/2) log(2 pi)   (eq. 1)
+  *out_host = -0.5 * yCy - 0.5 * h->logdet - 0.5 * (double)h->n * log(2.0 * M_PI);
+  return HODLR_OK;
+}
+
+hodlr_status hodlr_info(hodlr_t h, hodlr_info_t *info) {
+  if (!h || !info) return hodlr_set_error(HODLR_EINVAL, "info: NULL argument");
+  memset(info, 0, sizeof(*info));
+  info->kappa = h->kappa; info->leaf_min = h->leaf_min; info->leaf_max = h->leaf_max;
+  info->K = h->dt.Kdim[h->kappa];
+  for (int e = 1; e <= h->kappa && e < 64; e++) {
+    info->max_rank_by_depth[e] = h->dt.rdep[e];
+    double s = 0; long long c = 0;
+    for (long long b = (1LL << (e - 1)) - 1; b < (1LL << e) - 1; b++) { s += h->h_rank[b]; c++; }
+    info->mean_rank_by_depth[e] = c ? s / c : 0.0;
+  }
+  info->factor_bytes = h->bytes;
+  info->t_build = h->t_build; info->t_factor = h->t_factor; info->t_logdet = h->t_logdet; info->t_solve = h->t_solve;
+  info->rank_cap_hits = h->rank_cap_hits;
+  info->aca_steps = h->aca_steps;
+  info->gpu_launches_last = h->launches;
+  return HODLR_OK;
+}
+
+hodlr_status hodlr_get_order(hodlr_t h, double *xs_dev, int64_t *perm_dev) {
+  if (!h) return hodlr_set_error(HODLR_EINVAL, "get_order: NULL handle");
+  if (xs_dev) { cudaError_t e = cudaMemcpyAsync(xs_dev, h->xs, sizeof(double) * h->n, cudaMemcpyDeviceToDevice, h->st); if (e) return hodlr_cuda_check(e, "get_order"); }
+  if (perm_dev) { cudaError_t e = cudaMemcpyAsync(perm_dev, h->perm, sizeof(long long) * h->n, cudaMemcpyDeviceToDevice, h->st); if (e) return hodlr_cuda_check(e, "get_order"); }
+  cudaError_t e = cudaStreamSynchronize(h->st);
+  return e == cudaSuccess ? HODLR_OK : hodlr_cuda_check(e, "get_order");
+}
+
+hodlr_status hodlr_get_tree(hodlr_t h, int64_t *lo_host, int64_t *hi_host, int32_t *ranks_host) {
+  if (!h) return hodlr_set_error(HODLR_EINVAL, "get_tree: NULL handle");
+  if (lo_host) memcpy(lo_host, h->h_lo, sizeof(long long) * h->nnodes);
+  if (hi_host) memcpy(hi_host, h->h_hi, sizeof(long long) * h->nnodes);
+  if (ranks_host && h->ninternal) memcpy(ranks_host, h->h_rank, sizeof(int) * h->ninternal);
+  return HODLR_OK;
+}
+
+hodlr_status hodlr_get_logdet_parts(hodlr_t h, double *leaf_parts_host, double *node_parts_host) {
+  if (!h) return hodlr_set_error(HODLR_EINVAL, "get_logdet_parts: NULL handle");
+  if (h->state != 2) return hodlr_set_error(HODLR_ESTATE, "get_logdet_parts: not factored");
+  cudaError_t e = cudaSuccess;
+  if (leaf_parts_host) e = cudaMemcpy(leaf_parts_host, h->leaf_ld, sizeof(double) * h->nleaves, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && node_parts_host && h->ninternal)
+    e = cudaMemcpy(node_parts_host, h->node_ld, sizeof(double) * h->ninternal, cudaMemcpyDeviceToHost);
+  return e == cudaSuccess ? HODLR_OK : hodlr_cuda_check(e, "get_logdet_parts");
+}
+
+}  // extern "C"

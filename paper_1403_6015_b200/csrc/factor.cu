@@ -1,0 +1,386 @@
+// factor.cu -- G4/G5/G7: the "Factor" phase (Fig. 6) in projected-Gram form.
+//
+// Paper: apply K_kappa^{-1} (leaf blocks) and then every finer level's block inverse to each
+// coarser left factor (Fig. 6 lines 8-12), forming S_c = [[I, V^T K_c2^{-1} V], [U^T K_c1^{-1} U, I]]
+// at each node (equation_Low_Rank_Update + SMW).
+//
+// B200 form (same factorization, never materialises the processed panel):
+// for every node a define Pi_a = E_a^T K_aa^{-1} E_a where E_a = the original ACA left factors of
+// all ancestors of a (and a itself) restricted to the rows of a.
+//   leaf:  Pi_l = Z^T Z,  Z = L^{-1} E_l,  A_l = L L^T              (k_leaf_factor)
+//   node c at depth d with children c1, c2, s = depth-(d+1) columns, a = columns of depths <= d:
+//     S_c = [[I, Pi_c2[s,s]], [Pi_c1[s,s], I]],  B_c = [Pi_c2[s,a]; Pi_c1[s,a]],  T_c = S_c^{-1} B_c
+//     Pi_c = Pi_c1[a,a] + Pi_c2[a,a] - B_c[r:]^T T_c[:r] - B_c[:r]^T T_c[r:]   (k_tree_factor)
+// because E^T K_cc^{-1} E = E^T D^{-1} E - E^T D^{-1} L S^{-1} R D^{-1} E with D = diag(K_c1, K_c2),
+// L = blockdiag(U, V), R = [[0, V^T], [U^T, 0]] (SMW).  log det C = sum_l 2 sum log L_ii +
+// sum_c log det S_c (Sylvester + multiplicativity).
+#include "hodlr_internal.cuh"
+#include <limits.h>
+
+namespace {
+
+constexpr int LT = 256;      // threads per leaf CTA
+constexpr int TT = 256;      // threads per tree CTA
+
+__device__ __forceinline__ long long P(long long i, long long j) { return i * (i + 1) / 2 + j; }
+
+struct LeafCtx {
+  KParams kp;
+  long long n, ninternal, nleaves;
+  int kappa, K, ldz;
+  const double *xs;
+  const long long *lo, *hi;
+  const double *Xh;
+  const int *rank;
+  const DepthTab *dt;
+  double *Lf; long long lstride;
+  double *Pi;               // leaf Pi storage, K x K per leaf
+  double *leaf_ld;
+  int *flags;
+  double *scratch;          // per-CTA fallback storage when shared memory is too small
+  long long scratch_per_cta;
+  int use_smem;
+  int mmax;                 // max leaf size
+  long long lsz;            // packed triangle capacity mmax(mmax+1)/2 + 1
+};
+
+__global__ void __launch_bounds__(LT) k_leaf_factor(LeafCtx c) {
+  extern __shared__ double sm[];
+  __shared__ long long colsrc[1024];
+  __shared__ int bad;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int K = c.K, ldz = c.ldz;
+  double *base = c.use_smem ? sm : c.scratch + (long long)blockIdx.x * c.scratch_per_cta;
+  for (long long leaf = blockIdx.x; leaf < c.nleaves; leaf += gridDim.x) {
+    const long long id = c.ninternal + leaf, lo = c.lo[id], m = c.hi[id] - lo;
+    double *xl = base;                       // m
+    double *L = base + c.mmax;               // packed lower m(m+1)/2
+    double *Z = L + c.lsz;                   // m x ldz
+    for (long long i = t; i < m; i += LT) xl[i] = c.xs[lo + i];
+    if (t == 0) bad = 0;
+    __syncthreads();
+    // assemble A_l = K[l,l] + s2 I (lower triangle)
+    const long long np = m * (m + 1) / 2;
+    for (long long p = t; p < np; p += LT) {
+      long long i = (long long)((sqrt(8.0 * (double)p + 1.0) - 1.0) * 0.5);
+      while (i * (i + 1) / 2 > p) i--;
+      while ((i + 1) * (i + 2) / 2 <= p) i++;
+      long long j = p - i * (i + 1) / 2;
+      double v = kval(c.kp, xl[i] - xl[j]);
+      if (i == j) v += c.kp.s2;
+      L[p] = v;
+    }
+    __syncthreads();
+    // right-looking Cholesky A = L L^T
+    for (long long j = 0; j < m; j++) {
+      if (t == 0) {
+        double d = L[P(j, j)];
+        if (!(d > 0.0)) { bad = 1; d = 1.0; }
+        L[P(j, j)] = sqrt(d);
+      }
+      __syncthreads();
+      const double ljj = L[P(j, j)];
+      for (long long i = j + 1 + t; i < m; i += LT) L[P(i, j)] /= ljj;
+      __syncthreads();
+      for (long long i = j + 1 + warp; i < m; i += LT / 32) {
+        const double lij = L[P(i, j)];
+        for (long long k = j + 1 + lane; k <= i; k += 32) L[P(i, k)] -= lij * L[P(k, j)];
+      }
+      __syncthreads();
+    }
+    if (t == 0) {
+      double s = 0.0;
+      for (long long j = 0; j < m; j++) s += log(L[P(j, j)]);
+      c.leaf_ld[leaf] = 2.0 * s;
+      if (bad) { atomicAdd(&c.flags[1], 1); atomicMin(&c.flags[2], (int)id); }
+    }
+    double *Lg = c.Lf + leaf * c.lstride;
+    for (long long p = t; p < np; p += LT) Lg[p] = L[p];
+    if (K > 0) {
+      // column map: leaf column order = depth 1 .. kappa; zero beyond each ancestor block's rank
+      if (t == 0) {
+        long long a = id;
+        for (int e = c.kappa; e >= 1; e--) {
+          long long b = (a - 1) / 2;
+          int rb = c.rank[b];
+          for (int q = 0; q < c.dt->rdep[e]; q++)
+            colsrc[c.dt->Kdim[e - 1] + q] = q < rb ? c.dt->colbase[e] + q : -1;
+          a = b;
+        }
+      }
+      __syncthreads();
+      for (long long p = t; p < (long long)K * m; p += LT) {
+        long long col = p / m, i = p - col * m;
+        long long src = colsrc[col];
+        Z[i * ldz + col] = src >= 0 ? c.Xh[src * c.n + lo + i] : 0.0;
+      }
+      __syncthreads();
+      // Z <- L^{-1} Z  (forward substitution, one column per thread)
+      for (int col = t; col < K; col += LT) {
+        for (long long i = 0; i < m; i++) {
+          double s = Z[i * ldz + col];
+          const double *Li = L + P(i, 0);
+          for (long long j = 0; j < i; j++) s -= Li[j] * Z[j * ldz + col];
+          Z[i * ldz + col] = s / Li[i];
+        }
+      }
+      __syncthreads();
+      // Pi_l = Z^T Z  (symmetric; both triangles written)
+      double *Pl = c.Pi + leaf * (long long)K * K;
+      const long long npk = (long long)K * (K + 1) / 2;
+      for (long long p = t; p < npk; p += LT) {
+        long long a = (long long)((sqrt(8.0 * (double)p + 1.0) - 1.0) * 0.5);
+        while (a * (a + 1) / 2 > p) a--;
+        while ((a + 1) * (a + 2) / 2 <= p) a++;
+        long long b = p - a * (a + 1) / 2;
+        double s = 0.0;
+        for (long long i = 0; i < m; i++) s += Z[i * ldz + a] * Z[i * ldz + b];
+        Pl[a * K + b] = s;
+        Pl[b * K + a] = s;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+struct TreeCtx {
+  int d;                    // depth of the nodes of this launch
+  int r, q, Kd, K1;
+  const double *Pi1;        // children Pi base (depth d+1)
+  double *Pic;              // this depth's Pi base
+  double *Sst;              // per node: S (q*q), LU(S) (q*q), pivots (q)
+  double *BT;               // per node: B, T_hi, T_lo (q*Kd each)
+  double *node_ld;
+  int *flags;
+};
+
+// x <- S^{-1} x for one column with stride ld, using the LU factors and pivots
+__device__ __forceinline__ void lu_solve_col(const double *S, const int *piv, int q, double *x, int ld) {
+  for (int k = 0; k < q; k++) { int p = piv[k]; if (p != k) { double t = x[k * ld]; x[k * ld] = x[p * ld]; x[p * ld] = t; } }
+  for (int a = 0; a < q; a++) { double s = x[a * ld]; for (int k = 0; k < a; k++) s -= S[a * q + k] * x[k * ld]; x[a * ld] = s; }
+  for (int a = q - 1; a >= 0; a--) { double s = x[a * ld]; for (int k = a + 1; k < q; k++) s -= S[a * q + k] * x[k * ld]; x[a * ld] = s / S[a * q + a]; }
+}
+
+// One CTA per depth-d node c: S_c, its LU and log det; T_c = S_c^{-1} B_c kept as a double-double
+// pair (double solve + two refinement steps with compensated residuals); Pi_c by a compensated
+// Schur update, rounded to double.
+__global__ void __launch_bounds__(TT) k_tree_factor(TreeCtx c) {
+  extern __shared__ double sm[];
+  __shared__ int pivs[2 * ACA_MAXCAP];
+  __shared__ int zero_piv;
+  const int t = threadIdx.x;
+  const long long i = blockIdx.x;
+  const long long node = (1LL << c.d) - 1 + i;
+  const int r = c.r, q = c.q, Kd = c.Kd, K1 = c.K1;
+  const double *P1 = c.Pi1 + (2 * i) * (long long)K1 * K1;
+  const double *P2 = c.Pi1 + (2 * i + 1) * (long long)K1 * K1;
+  const long long qK = (long long)q * Kd;
+  double *S0 = sm;                   // q x q original
+  double *S = S0 + q * q;            // q x q LU
+  double *B = S + q * q;             // q x Kd
+  double *Th = B + qK;               // q x Kd
+  double *Tl = Th + qK;              // q x Kd
+  double *R = Tl + qK;               // q x Kd residual scratch
+  for (int p = t; p < q * q; p += TT) {
+    int a = p / q, b = p - a * q;
+    double v = a == b ? 1.0 : 0.0;
+    if (a < r && b >= r) v = P2[(long long)(Kd + a) * K1 + Kd + (b - r)];
+    if (a >= r && b < r) v = P1[(long long)(Kd + a - r) * K1 + Kd + b];
+    S0[p] = v; S[p] = v;
+  }
+  for (long long p = t; p < qK; p += TT) {
+    long long a = p / Kd, b = p - a * Kd;
+    double v = a < r ? P2[(long long)(Kd + a) * K1 + b] : P1[(long long)(Kd + a - r) * K1 + b];
+    B[p] = v; Th[p] = v; Tl[p] = 0.0;
+  }
+  if (t == 0) zero_piv = 0;
+  __syncthreads();
+  // LU with partial pivoting (row of max |.|, first index on ties)
+  for (int k = 0; k < q; k++) {
+    if (t == 0) {
+      int p = k; double best = fabs(S[k * q + k]);
+      for (int a = k + 1; a < q; a++) if (fabs(S[a * q + k]) > best) { best = fabs(S[a * q + k]); p = a; }
+      pivs[k] = p;
+      if (best == 0.0) zero_piv = 1;
+    }
+    __syncthreads();
+    const int p = pivs[k];
+    if (p != k) for (int j = t; j < q; j += TT) { double x = S[k * q + j]; S[k * q + j] = S[p * q + j]; S[p * q + j] = x; }
+    __syncthreads();
+    const double ukk = S[k * q + k];
+    if (ukk != 0.0) {
+      for (int a = k + 1 + t; a < q; a += TT) {
+        double l = S[a * q + k] / ukk;
+        S[a * q + k] = l;
+        for (int j = k + 1; j < q; j++) S[a * q + j] -= l * S[k * q + j];
+      }
+    }
+    __syncthreads();
+  }
+  if (t == 0) {
+    int sg = 1; double la = 0.0;
+    for (int k = 0; k < q; k++) {
+      if (pivs[k] != k) sg = -sg;
+      double u = S[k * q + k];
+      if (u < 0.0) sg = -sg;
+      la += log(fabs(u));
+    }
+    c.node_ld[node] = la;
+    if (zero_piv || sg <= 0) { atomicAdd(&c.flags[1], 1); atomicMin(&c.flags[2], (int)node); }
+  }
+  if (!zero_piv) {
+    for (int col = t; col < Kd; col += TT) {
+      lu_solve_col(S, pivs, q, Th + col, Kd);
+      for (int it = 0; it < 2; it++) {        // iterative refinement, residual in double-double
+        for (int a = 0; a < q; a++) {
+          Acc2 A = acc2(B[a * Kd + col]);
+          for (int k = 0; k < q; k++) acc_fma_dd(A, -S0[a * q + k], Th[k * Kd + col], Tl[k * Kd + col]);
+          R[a * Kd + col] = acc_val(A);
+        }
+        lu_solve_col(S, pivs, q, R + col, Kd);
+        for (int a = 0; a < q; a++) Tl[a * Kd + col] += R[a * Kd + col];
+      }
+    }
+  }
+  __syncthreads();
+  // Pi_c = Pi_c1[a,a] + Pi_c2[a,a] - B[r:]^T T[:r] - B[:r]^T T[r:]  (lower triangle, mirrored)
+  double *Pc = c.Pic + i * (long long)Kd * Kd;
+  const long long npk = (long long)Kd * (Kd + 1) / 2;
+  for (long long p = t; p < npk; p += TT) {
+    long long a = (long long)((sqrt(8.0 * (double)p + 1.0) - 1.0) * 0.5);
+    while (a * (a + 1) / 2 > p) a--;
+    while ((a + 1) * (a + 2) / 2 <= p) a++;
+    long long b = p - a * (a + 1) / 2;
+    Acc2 A = acc2(P1[a * K1 + b]);
+    acc_add(A, P2[a * K1 + b]);
+    for (int u = 0; u < r; u++) acc_fma_dd(A, -B[(long long)(r + u) * Kd + a], Th[(long long)u * Kd + b], Tl[(long long)u * Kd + b]);
+    for (int u = 0; u < r; u++) acc_fma_dd(A, -B[(long long)u * Kd + a], Th[(long long)(r + u) * Kd + b], Tl[(long long)(r + u) * Kd + b]);
+    const double v = acc_val(A);
+    Pc[a * Kd + b] = v;
+    Pc[b * Kd + a] = v;
+  }
+  // persist S, LU(S) (+ pivots as doubles), B, T_hi, T_lo for the solve
+  double *Sg = c.Sst + i * (long long)(2 * q * q + q);
+  for (int p = t; p < 2 * q * q; p += TT) Sg[p] = S0[p];         // S0 and S are contiguous
+  for (int p = t; p < q; p += TT) Sg[2 * q * q + p] = (double)pivs[p];
+  double *BTg = c.BT + i * 3LL * qK;
+  for (long long p = t; p < 3LL * qK; p += TT) BTg[p] = B[p];    // B, Th, Tl are contiguous
+}
+
+// log det = leaves (left to right), then internal nodes by depth kappa-1..0, left to right;
+// per-thread Neumaier over a contiguous segment, combined in order by thread 0.
+__global__ void k_logdet_reduce(const double *leaf_ld, const double *node_ld, long long nleaves, int kappa,
+                                double *out) {
+  __shared__ double ss[256], cc[256];
+  const long long N = nleaves + nleaves - 1;
+  const int t = threadIdx.x;
+  long long per = (N + 255) / 256, v0 = t * per, v1 = v0 + per < N ? v0 + per : N;
+  double s = 0.0, comp = 0.0;
+  for (long long v = v0; v < v1; v++) {
+    double x;
+    if (v < nleaves) x = leaf_ld[v];
+    else {
+      long long u = v - nleaves;       // depth kappa-1 first
+      int d = kappa - 1;
+      while (u >= (1LL << d)) { u -= (1LL << d); d--; }
+      x = node_ld[(1LL << d) - 1 + u];
+    }
+    double tt = s + x;
+    if (fabs(s) >= fabs(x)) comp += (s - tt) + x; else comp += (x - tt) + s;
+    s = tt;
+  }
+  ss[t] = s; cc[t] = comp;
+  __syncthreads();
+  if (t == 0) {
+    double S = 0.0, Cc = 0.0;
+    for (int j = 0; j < 256; j++) {
+      double x = ss[j];
+      double tt = S + x;
+      if (fabs(S) >= fabs(x)) Cc += (S - tt) + x; else Cc += (x - tt) + S;
+      S = tt;
+      Cc += cc[j];
+    }
+    *out = S + Cc;
+  }
+}
+
+}  // namespace
+
+hodlr_status hodlr_factor_impl(hodlr_s *h) {
+  const int kappa = h->kappa;
+  DepthTab &dt = h->dt;
+  const int K = dt.Kdim[kappa];
+  const long long nl = h->nleaves;
+  // ---- storage ----
+  const int mmax = h->leaf_max;
+  h->lstride = (long long)mmax * (mmax + 1) / 2;
+  h->Lf = (double *)hodlr_dalloc(h, sizeof(double) * h->lstride * nl);
+  h->leaf_ld = (double *)hodlr_dalloc(h, sizeof(double) * nl);
+  h->node_ld = (double *)hodlr_dalloc(h, sizeof(double) * (h->ninternal > 0 ? h->ninternal : 1));
+  h->d_logdet = (double *)hodlr_dalloc(h, sizeof(double));
+  long long piTot = 0, sTot = 0, btTot = 0;
+  for (int e = kappa; e >= 0; e--) {
+    dt.piOff[e] = piTot;
+    piTot += (1LL << e) * (long long)dt.Kdim[e] * dt.Kdim[e];
+  }
+  for (int d = 0; d < kappa; d++) {
+    long long q = 2LL * dt.rdep[d + 1];
+    dt.nodeS[d] = sTot; sTot += (1LL << d) * (2 * q * q + q);
+    dt.nodeBT[d] = btTot; btTot += (1LL << d) * 3 * q * dt.Kdim[d];
+  }
+  h->Pipool = (double *)hodlr_dalloc(h, sizeof(double) * (piTot > 0 ? piTot : 1));
+  h->Spool = (double *)hodlr_dalloc(h, sizeof(double) * (sTot > 0 ? sTot : 1));
+  h->BTpool = (double *)hodlr_dalloc(h, sizeof(double) * (btTot > 0 ? btTot : 1));
+  if (!h->Lf || !h->leaf_ld || !h->node_ld || !h->d_logdet || !h->Pipool || !h->Spool || !h->BTpool)
+    return hodlr_set_error(HODLR_ENOMEM, "factor: device allocation failed");
+  HCUDA(cudaMemcpyAsync(h->d_dt, &dt, sizeof(DepthTab), cudaMemcpyHostToDevice, h->st));
+  // ---- leaves ----
+  LeafCtx lc;
+  lc.kp = h->kp; lc.n = h->n; lc.ninternal = h->ninternal; lc.nleaves = nl; lc.kappa = kappa; lc.K = K;
+  lc.ldz = K | 1; lc.xs = h->xs; lc.lo = h->lo; lc.hi = h->hi; lc.Xh = h->Xh; lc.rank = h->rank;
+  lc.dt = h->d_dt; lc.Lf = h->Lf; lc.lstride = h->lstride; lc.Pi = h->Pipool + dt.piOff[kappa];
+  lc.leaf_ld = h->leaf_ld; lc.flags = h->dflags;
+  if (K > 1024) return hodlr_set_error(HODLR_EINVAL, "factor: K = %d ancestor columns exceeds 1024", K);
+  lc.mmax = mmax;
+  lc.lsz = (long long)mmax * (mmax + 1) / 2 + 1;
+  size_t need = sizeof(double) * (mmax + lc.lsz + (size_t)mmax * lc.ldz);
+  int maxsm = 0;
+  HCUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
+  int grid = (int)nl;
+  lc.scratch = nullptr; lc.scratch_per_cta = 0;
+  if (need <= (size_t)maxsm - 12 * 1024) {
+    lc.use_smem = 1;
+    HCUDA(cudaFuncSetAttribute(k_leaf_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
+  } else {
+    lc.use_smem = 0; need = 0;
+    grid = (int)(nl < 148 * 4 ? nl : 148 * 4);
+    lc.scratch_per_cta = mmax + lc.lsz + (long long)mmax * lc.ldz;
+    lc.scratch = (double *)hodlr_dalloc(h, sizeof(double) * lc.scratch_per_cta * grid);
+    if (!lc.scratch) return hodlr_set_error(HODLR_ENOMEM, "factor: scratch allocation failed");
+  }
+  k_leaf_factor<<<grid, LT, need, h->st>>>(lc);
+  HLAUNCH(h, "k_leaf_factor");
+  // ---- tree, bottom-up ----
+  size_t tree_smem_max = 0;
+  for (int d = 0; d < kappa; d++) {
+    size_t q = 2 * (size_t)dt.rdep[d + 1];
+    tree_smem_max = std::max(tree_smem_max, sizeof(double) * (2 * q * q + 4 * q * dt.Kdim[d]));
+  }
+  if (tree_smem_max > (size_t)maxsm - 2048)
+    return hodlr_set_error(HODLR_EINVAL, "factor: coupling system too large for shared memory");
+  if (kappa > 0)
+    HCUDA(cudaFuncSetAttribute(k_tree_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tree_smem_max));
+  for (int d = kappa - 1; d >= 0; d--) {
+    TreeCtx tc;
+    tc.d = d; tc.r = dt.rdep[d + 1]; tc.q = 2 * tc.r; tc.Kd = dt.Kdim[d]; tc.K1 = dt.Kdim[d + 1];
+    tc.Pi1 = h->Pipool + dt.piOff[d + 1]; tc.Pic = h->Pipool + dt.piOff[d];
+    tc.Sst = h->Spool + dt.nodeS[d]; tc.BT = h->BTpool + dt.nodeBT[d];
+    tc.node_ld = h->node_ld; tc.flags = h->dflags;
+    size_t smem = sizeof(double) * (2ULL * tc.q * tc.q + 4ULL * tc.q * tc.Kd);
+    k_tree_factor<<<(int)(1LL << d), TT, smem, h->st>>>(tc);
+    HLAUNCH(h, "k_tree_factor");
+  }
+  k_logdet_reduce<<<1, 256, 0, h->st>>>(h->leaf_ld, h->node_ld, nl, kappa, h->d_logdet);
+  HLAUNCH(h, "k_logdet_reduce");
+  return HODLR_OK;
+}

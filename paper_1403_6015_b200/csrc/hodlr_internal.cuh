@@ -1,0 +1,194 @@
+// hodlr_internal.cuh -- shared internals of libhodlr_b200 (product path; no oracle code).
+//
+// Layout in HBM:
+//   xs[n], perm[n]            sorted points, permutation (sorted position -> original index)
+//   lo[], hi[]                node ranges, heap order: node (d, i) has id 2^d - 1 + i
+//   Xh                        ACA factors, column-major per depth "slot": depth e = 1..kappa owns
+//                             capd[e] columns of n doubles starting at column colbase[e]; column l
+//                             of slot e holds, on the rows of each depth-e node a, the l-th left
+//                             factor of a (U' of a left child, V' of a right child)
+//   Lf                        leaf Cholesky factors, packed lower row-major, lstride doubles/leaf
+//   per depth d:  S LU (q x q), piv, B (q x Kd), T (q x Kd), Pi (Kd x Kd) per node
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math.h>
+#include "../../include/hodlr.h"
+#include <algorithm>
+
+#define HODLR_MAXDEPTH 48
+#define ACA_MAXCAP 64      // hard ceiling on the ACA rank cap (records/state are sized by it)
+#define ACA_RECW (4 + ACA_MAXCAP)
+#define ACA_SUB 256        // threads per ACA CTA == sub-tile width
+
+// ----------------------------------------------------------------------------------------------
+// Covariance functions, Table I; C_ij = k(x_i - x_j) + s2 [i == j]
+// (PAPER.md:1251-1256).  kp = {a^2, c} with c = 1/(2 ell^2) for SE, sqrt(3)/ell or sqrt(5)/ell
+// for Matern-3/2 and -5/2.
+// ----------------------------------------------------------------------------------------------
+struct KParams { int kern; double a2; double c; double s2; };
+
+__device__ __forceinline__ double kval(const KParams &kp, double d) {
+  if (kp.kern == HODLR_SE) return kp.a2 * exp(-(d * d) * kp.c);
+  double s = fabs(d) * kp.c;
+  double e = exp(-s);
+  if (kp.kern == HODLR_MATERN32) return kp.a2 * (1.0 + s) * e;
+  return kp.a2 * (1.0 + s + s * s * (1.0 / 3.0)) * e;
+}
+
+// ----------------------------------------------------------------------------------------------
+// ACA per-block state (device).  Stored factors: V'[:,k] = raw residual row v~, U'[:,k] = u / v~_jk
+// (same product U V^T as the paper's normalisation; R16).
+// ----------------------------------------------------------------------------------------------
+struct AcaState {
+  int k;            // number of terms so far
+  int done;         // 0 active, 1 finished, 2 hit the rank cap without meeting eps
+  int cnt_r, cnt_c; // CTA arrival counters (last-CTA reduction)
+  int cap;          // min(rank_cap, m1, m2)
+  int pad;
+  long long ipiv;   // current row pivot (local in c1)
+  long long jpiv;   // current column pivot (local in c2)
+  double pivval;    // v~_jk
+  double S2;        // ||S_k||_F^2 estimate
+  double nv2;       // ||V'[:,k]||^2 of the current step
+  double dV[ACA_MAXCAP];   // V'_l . V'_k, l < k, of the current step
+};
+
+struct AcaItem { int block; int q; long long start; int len; int pad; };
+
+// Per-depth metadata passed by value.
+struct DepthTab {
+  long long colbase[HODLR_MAXDEPTH + 2];   // first column of slot e
+  int capd[HODLR_MAXDEPTH + 2];            // columns allocated in slot e
+  int rdep[HODLR_MAXDEPTH + 2];            // max rank of depth-(e-1) blocks (after build)
+  int Kdim[HODLR_MAXDEPTH + 2];            // Kdim[e] = sum_{e'=1..e} rdep[e']
+  long long nodeS[HODLR_MAXDEPTH + 2];     // per depth d: offset of S LU storage (doubles)
+  long long nodeBT[HODLR_MAXDEPTH + 2];    // per depth d: offset of B/T storage (doubles)
+  long long nodeV[HODLR_MAXDEPTH + 2];     // per depth d: offset of per-node vectors (g, w) (doubles)
+  long long nodeT[HODLR_MAXDEPTH + 2];     // per depth d: offset of per-node t (doubles)
+  long long piOff[HODLR_MAXDEPTH + 2];     // per depth e: offset of Pi storage (doubles)
+};
+
+struct AcaCtx {
+  KParams kp;
+  long long n;
+  double eps;
+  const double *xs;
+  const long long *lo, *hi;
+  double *Xh;
+  unsigned char *used;      // kappa x n flags: used[(e-1)*n + row]
+  AcaState *st;
+  const AcaItem *items;
+  const int *nq;            // chunks per block for this pass
+  const long long *recbase; // record base per block for this pass
+  double *rec;              // records
+  int *active;
+  int *rank;
+  const int *bdepth;        // depth of each internal block
+  DepthTab *dt;             // device copy
+};
+
+// ----------------------------------------------------------------------------------------------
+// Handle
+// ----------------------------------------------------------------------------------------------
+struct hodlr_s {
+  cudaStream_t st;
+  int dev;
+  long long n;
+  KParams kp;
+  double theta[2];
+  int leaf;
+  double eps;
+  int cap;
+  int kappa;
+  long long nnodes, ninternal, nleaves;
+  int leaf_min, leaf_max;
+  int state;                 // 1 built, 2 factored, -1 factor failed
+  int launches;              // kernels launched by the current call
+  int aca_steps;
+  long long rank_cap_hits;
+  // host copies
+  long long *h_lo, *h_hi;
+  int *h_rank;
+  DepthTab dt;
+  // device
+  double *xs;
+  long long *perm;
+  long long *lo, *hi;
+  double *Xh;
+  long long xh_cols;
+  unsigned char *used;
+  AcaState *ast;
+  int *rank;
+  int *bdepth;
+  int *dflags;               // [0] nonfinite x, [1] notpd, [2] notpd node+1 (min), [3] nonfinite y, [4] active
+  DepthTab *d_dt;
+  // factor storage
+  double *Lf; long long lstride;
+  double *Spool;  int *Piv;  double *BTpool; double *Pipool;
+  double *leaf_ld, *node_ld, *d_logdet;
+  double logdet;
+  // solve workspace
+  double *Vpool, *Tvec, *hvec;
+  // bookkeeping
+  long long bytes;
+  double t_build, t_factor, t_logdet, t_solve;
+  cudaEvent_t ev0, ev1;
+  void *allocs[64]; int nallocs;
+};
+
+// helpers implemented in api.cu
+hodlr_status hodlr_set_error(hodlr_status code, const char *fmt, ...);
+hodlr_status hodlr_cuda_check(cudaError_t e, const char *what);
+void *hodlr_dalloc(hodlr_s *h, size_t bytes);
+
+// phase entry points (one per .cu file)
+hodlr_status hodlr_sort_and_tree(hodlr_s *h, const double *x);
+hodlr_status hodlr_aca(hodlr_s *h);
+hodlr_status hodlr_factor_impl(hodlr_s *h);
+hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_only);
+
+static inline int hodlr_depth_of(long long id) { int d = 0; while (id >= ((2LL << d) - 1)) d++; return d; }
+
+#define HCUDA(call) do { cudaError_t _e = (call); if (_e != cudaSuccess) return hodlr_cuda_check(_e, #call); } while (0)
+#define HLAUNCH(h, name) do { (h)->launches++; cudaError_t _e = cudaGetLastError(); \
+    if (_e != cudaSuccess) return hodlr_cuda_check(_e, "launch " name); } while (0)
+
+// ----------------------------------------------------------------------------------------------
+// Block-level reduction helpers
+// ----------------------------------------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ----------------------------------------------------------------------------------------------
+// Compensated (double-double) arithmetic for the small coupling systems:
+// error-free transformations TwoSum / TwoProduct (FMA) and a Dot2-style accumulator.
+// ----------------------------------------------------------------------------------------------
+__device__ __forceinline__ void two_sum(double a, double b, double &s, double &e) {
+  s = a + b; double bb = s - a; e = (a - (s - bb)) + (b - bb);
+}
+__device__ __forceinline__ void two_prod(double a, double b, double &p, double &e) { p = a * b; e = fma(a, b, -p); }
+struct Acc2 { double s, c; };
+__device__ __forceinline__ Acc2 acc2(double x) { Acc2 A; A.s = x; A.c = 0.0; return A; }
+__device__ __forceinline__ void acc_add(Acc2 &A, double x) { double s, e; two_sum(A.s, x, s, e); A.s = s; A.c += e; }
+__device__ __forceinline__ void acc_add_dd(Acc2 &A, double xh, double xl) { acc_add(A, xh); A.c += xl; }
+__device__ __forceinline__ void acc_fma(Acc2 &A, double a, double b) {          // A += a * b
+  double p, e; two_prod(a, b, p, e); acc_add(A, p); A.c += e;
+}
+__device__ __forceinline__ void acc_fma_dd(Acc2 &A, double a, double bh, double bl) {   // A += a * (bh + bl)
+  acc_fma(A, a, bh); A.c = fma(a, bl, A.c);
+}
+__device__ __forceinline__ double acc_val(const Acc2 &A) { return A.s + A.c; }
+__device__ __forceinline__ void acc_dd(const Acc2 &A, double &hi, double &lo) { two_sum(A.s, A.c, hi, lo); }
+
+// argmax with ties -> smallest index; (abs, idx) with idx < 0 meaning "no candidate"
+__device__ __forceinline__ bool amax_better(double a1, long long i1, double a2, long long i2) {
+  if (i2 < 0) return false;
+  if (i1 < 0) return true;
+  if (a2 > a1) return true;
+  if (a2 == a1 && i2 < i1) return true;
+  return false;
+}

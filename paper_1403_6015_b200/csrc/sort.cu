@@ -1,0 +1,144 @@
+// sort.cu -- G1: stable ascending argsort of the FP64 points (the kd-tree
+// ordering reduces to a sort in 1-D; ties keep the lower original index).
+//
+// LSD radix sort on order-preserving 64-bit keys, 8 passes of 8-bit digits.  Each pass:
+//   hist    : per 4096-key tile digit counts             (HBM-bound, 8 B/key read)
+//   scan    : exclusive scan of the digit-major count table (one CTA)
+//   scatter : stable tile-local ranks via __match_any_sync + per-warp counters, then scatter
+//             (HBM-bound, 16 B/key read + 16 B/key write)
+// Stability: tiles are ranked in order, warps within a tile in order, keys within a warp in order.
+#include "hodlr_internal.cuh"
+
+namespace {
+
+constexpr int TILE = 4096;
+constexpr int STHREADS = 512;    // 16 warps x 256 keys
+
+__global__ void k_make_keys(const double *__restrict__ x, long long n, unsigned long long *__restrict__ key,
+                            long long *__restrict__ idx, int *__restrict__ flags) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double v = x[i];
+  if (!isfinite(v)) atomicOr(&flags[0], 1);
+  if (v == 0.0) v = 0.0;                        // -0.0 -> +0.0 before sorting
+  unsigned long long b = __double_as_longlong(v);
+  b ^= (b >> 63) ? 0xffffffffffffffffULL : 0x8000000000000000ULL;
+  key[i] = b;
+  idx[i] = i;
+}
+
+__global__ void __launch_bounds__(STHREADS) k_hist(const unsigned long long *__restrict__ key, long long n, int shift,
+                                                   int ntiles, unsigned int *__restrict__ cnt) {
+  __shared__ unsigned int c[256];
+  for (int t = threadIdx.x; t < 256; t += STHREADS) c[t] = 0;
+  __syncthreads();
+  long long base = (long long)blockIdx.x * TILE;
+  for (int t = threadIdx.x; t < TILE; t += STHREADS) {
+    long long p = base + t;
+    if (p < n) atomicAdd(&c[(key[p] >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < 256; t += STHREADS) cnt[(long long)t * ntiles + blockIdx.x] = c[t];
+}
+
+// exclusive scan of m entries in one CTA of 1024 threads
+__global__ void __launch_bounds__(1024) k_scan(unsigned int *__restrict__ a, long long m) {
+  __shared__ unsigned long long part[1024];
+  long long per = (m + 1023) / 1024;
+  long long b = threadIdx.x * per, e = b + per < m ? b + per : m;
+  unsigned long long s = 0;
+  for (long long i = b; i < e; i++) s += a[i];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {         // Hillis-Steele inclusive scan
+    unsigned long long v = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
+    __syncthreads();
+    part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  unsigned long long run = part[threadIdx.x] - s;
+  for (long long i = b; i < e; i++) { unsigned int t = a[i]; a[i] = (unsigned int)run; run += t; }
+}
+
+__global__ void __launch_bounds__(STHREADS) k_scatter(const unsigned long long *__restrict__ kin,
+                                                      const long long *__restrict__ iin, long long n, int shift,
+                                                      int ntiles, const unsigned int *__restrict__ gscan,
+                                                      unsigned long long *__restrict__ kout,
+                                                      long long *__restrict__ iout) {
+  __shared__ unsigned int wc[16][256];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int t = threadIdx.x; t < 16 * 256; t += STHREADS) (&wc[0][0])[t] = 0;
+  __syncthreads();
+  const long long base = (long long)blockIdx.x * TILE + warp * 256;
+  unsigned long long k[8]; long long id[8]; unsigned int loc[8]; int dig[8];
+  const unsigned int lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int r = 0; r < 8; r++) {
+    long long p = base + r * 32 + lane;
+    bool valid = p < n;
+    k[r] = valid ? kin[p] : 0ull;
+    id[r] = valid ? iin[p] : 0;
+    int d = valid ? (int)((k[r] >> shift) & 255u) : 256;
+    dig[r] = d;
+    unsigned int peers = __match_any_sync(0xffffffffu, d);
+    unsigned int before = 0;
+    if (valid) before = wc[warp][d];
+    __syncwarp();
+    if (valid && lane == __ffs(peers) - 1) wc[warp][d] = before + __popc(peers);
+    __syncwarp();
+    loc[r] = before + __popc(peers & lt);
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < 256; d += STHREADS) {
+    unsigned int run = 0;
+    for (int w = 0; w < 16; w++) { unsigned int t = wc[w][d]; wc[w][d] = run; run += t; }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 8; r++) {
+    if (dig[r] == 256) continue;
+    long long dst = (long long)gscan[(long long)dig[r] * ntiles + blockIdx.x] + wc[warp][dig[r]] + loc[r];
+    kout[dst] = k[r];
+    iout[dst] = id[r];
+  }
+}
+
+__global__ void k_finish(const unsigned long long *__restrict__ key, const long long *__restrict__ idx, long long n,
+                         double *__restrict__ xs, long long *__restrict__ perm) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  unsigned long long b = key[i];
+  b ^= (b >> 63) ? 0x8000000000000000ULL : 0xffffffffffffffffULL;
+  xs[i] = __longlong_as_double((long long)b);
+  perm[i] = idx[i];
+}
+
+}  // namespace
+
+hodlr_status hodlr_sort_and_tree(hodlr_s *h, const double *x) {
+  const long long n = h->n;
+  const int ntiles = (int)((n + TILE - 1) / TILE);
+  unsigned long long *k0 = (unsigned long long *)hodlr_dalloc(h, sizeof(unsigned long long) * n);
+  unsigned long long *k1 = (unsigned long long *)hodlr_dalloc(h, sizeof(unsigned long long) * n);
+  long long *i0 = (long long *)hodlr_dalloc(h, sizeof(long long) * n);
+  long long *i1 = (long long *)hodlr_dalloc(h, sizeof(long long) * n);
+  unsigned int *cnt = (unsigned int *)hodlr_dalloc(h, sizeof(unsigned int) * 256 * (size_t)ntiles);
+  if (!k0 || !k1 || !i0 || !i1 || !cnt) return hodlr_set_error(HODLR_ENOMEM, "sort: device allocation failed");
+  int nb = (int)((n + 255) / 256);
+  k_make_keys<<<nb, 256, 0, h->st>>>(x, n, k0, i0, h->dflags);
+  HLAUNCH(h, "k_make_keys");
+  for (int pass = 0; pass < 8; pass++) {
+    int shift = pass * 8;
+    k_hist<<<ntiles, STHREADS, 0, h->st>>>(k0, n, shift, ntiles, cnt);
+    HLAUNCH(h, "k_hist");
+    k_scan<<<1, 1024, 0, h->st>>>(cnt, 256LL * ntiles);
+    HLAUNCH(h, "k_scan");
+    k_scatter<<<ntiles, STHREADS, 0, h->st>>>(k0, i0, n, shift, ntiles, cnt, k1, i1);
+    HLAUNCH(h, "k_scatter");
+    unsigned long long *tk = k0; k0 = k1; k1 = tk;
+    long long *ti = i0; i0 = i1; i1 = ti;
+  }
+  k_finish<<<nb, 256, 0, h->st>>>(k0, i0, n, h->xs, h->perm);
+  HLAUNCH(h, "k_finish");
+  return HODLR_OK;
+}

@@ -1,0 +1,221 @@
+"""Thin ctypes binding of include/hodlr.h (argument marshalling only).
+
+Every step of the hot path runs in libhodlr_b200.so's CUDA kernels.  There is
+no CPU fallback: if the library or a CUDA device is missing, calls raise.
+PyTorch supplies device memory (tensors) and the stream.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import torch
+
+from . import build as _build
+
+HODLR_SE, HODLR_MATERN32, HODLR_MATERN52 = 0, 1, 2
+KERNELS = {"se": HODLR_SE, "matern32": HODLR_MATERN32, "matern52": HODLR_MATERN52}
+STATUS = {0: "OK", 1: "EINVAL", 2: "ENOTPD", 3: "ERANKCAP", 4: "ESTATE", 5: "ENOMEM", 6: "ECUDA", 7: "ENCCL"}
+
+EXPORTS = ("hodlr_build", "hodlr_factor", "hodlr_logdet", "hodlr_solve", "gp_loglik", "hodlr_info",
+           "hodlr_get_order", "hodlr_get_tree", "hodlr_get_logdet_parts", "hodlr_free", "hodlr_last_error",
+           "hodlr_version")
+
+
+class HodlrError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"hodlr {STATUS.get(code, code)}: {msg}")
+        self.code = code
+        self.status = STATUS.get(code, str(code))
+
+
+class hodlr_dist(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("nccl_unique_id", C.c_void_p)]
+
+
+class hodlr_opts(C.Structure):
+    _fields_ = [("rank_cap", C.c_int32), ("reserved", C.c_int32 * 7)]
+
+
+class hodlr_info_t(C.Structure):
+    _fields_ = [("kappa", C.c_int32), ("leaf_min", C.c_int32), ("leaf_max", C.c_int32), ("K", C.c_int32),
+                ("max_rank_by_depth", C.c_int32 * 64), ("mean_rank_by_depth", C.c_double * 64),
+                ("factor_bytes", C.c_int64), ("t_build", C.c_double), ("t_factor", C.c_double),
+                ("t_logdet", C.c_double), ("t_solve", C.c_double), ("rank_cap_hits", C.c_int64),
+                ("aca_steps", C.c_int32), ("gpu_launches_last", C.c_int32)]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def library_path() -> str:
+    return _build.LIB
+
+
+def load(build_if_missing: bool = True):
+    """Load libhodlr_b200.so (building it with nvcc if missing).  Raises if unavailable."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        path = _build.LIB
+        if not os.path.exists(path):
+            if not build_if_missing:
+                raise RuntimeError(f"{path} missing; run python -m paper_1403_6015_b200.build")
+            _build.build()
+        lib = C.CDLL(path)
+        P, I64, I32, D = C.c_void_p, C.c_int64, C.c_int32, C.c_double
+        lib.hodlr_build.argtypes = [P, I64, I32, P, D, I32, D, P, P, P, P]
+        lib.hodlr_factor.argtypes = [P]
+        lib.hodlr_logdet.argtypes = [P, P]
+        lib.hodlr_solve.argtypes = [P, P, P, I64, I64]
+        lib.gp_loglik.argtypes = [P, P, P]
+        lib.hodlr_info.argtypes = [P, P]
+        lib.hodlr_get_order.argtypes = [P, P, P]
+        lib.hodlr_get_tree.argtypes = [P, P, P, P]
+        lib.hodlr_get_logdet_parts.argtypes = [P, P, P]
+        for f in ("hodlr_build", "hodlr_factor", "hodlr_logdet", "hodlr_solve", "gp_loglik", "hodlr_info",
+                  "hodlr_get_order", "hodlr_get_tree", "hodlr_get_logdet_parts"):
+            getattr(lib, f).restype = I32
+        lib.hodlr_free.argtypes = [P]; lib.hodlr_free.restype = None
+        lib.hodlr_last_error.argtypes = []; lib.hodlr_last_error.restype = C.c_char_p
+        lib.hodlr_version.argtypes = []; lib.hodlr_version.restype = C.c_char_p
+        _lib = lib
+        return lib
+
+
+def _check(code: int):
+    if code != 0:
+        raise HodlrError(code, load().hodlr_last_error().decode())
+
+
+def _dev_f64(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or t.device.type != "cuda" or t.dtype != torch.float64:
+        raise TypeError(f"{name} must be a CUDA float64 tensor")
+    return t.contiguous()
+
+
+def _stream_ptr(stream) -> int:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return int(s.cuda_stream)
+
+
+# ------------------------------------------------------------------ C-ABI mirrors
+def hodlr_build(x: torch.Tensor, kernel: int, theta, sigma2: float, leaf: int, eps: float,
+                rank_cap: int = 0, stream=None) -> int:
+    lib = load()
+    x = _dev_f64(x, "x")
+    th = (C.c_double * 2)(float(theta[0]), float(theta[1]))
+    opts = hodlr_opts(int(rank_cap))
+    h = C.c_void_p(0)
+    _check(lib.hodlr_build(x.data_ptr(), x.numel(), int(kernel), th, float(sigma2), int(leaf), float(eps),
+                           None, C.byref(opts), _stream_ptr(stream), C.byref(h)))
+    return h.value
+
+
+def hodlr_factor(h: int):
+    _check(load().hodlr_factor(h))
+
+
+def hodlr_logdet(h: int) -> float:
+    v = C.c_double(0.0)
+    _check(load().hodlr_logdet(h, C.byref(v)))
+    return v.value
+
+
+def hodlr_solve(h: int, y: torch.Tensor, x: torch.Tensor | None = None) -> torch.Tensor:
+    """y: (n,) or (n, nrhs) CUDA float64 (column-major storage is made internally)."""
+    lib = load()
+    y = _dev_f64(y, "y")
+    one = y.dim() == 1
+    Y = y.reshape(y.shape[0], -1).t().contiguous()          # nrhs x n rows = column-major n x nrhs
+    X = torch.empty_like(Y)
+    _check(lib.hodlr_solve(h, Y.data_ptr(), X.data_ptr(), Y.shape[0], Y.shape[1]))
+    out = X[0] if one else X.t()
+    if x is not None:
+        x.copy_(out)
+        return x
+    return out
+
+
+def gp_loglik(h: int, y: torch.Tensor) -> float:
+    y = _dev_f64(y, "y")
+    v = C.c_double(0.0)
+    _check(load().gp_loglik(h, y.data_ptr(), C.byref(v)))
+    return v.value
+
+
+def hodlr_info(h: int) -> dict:
+    info = hodlr_info_t()
+    _check(load().hodlr_info(h, C.byref(info)))
+    k = info.kappa
+    return {"kappa": k, "leaf_min": info.leaf_min, "leaf_max": info.leaf_max, "K": info.K,
+            "max_rank_by_depth": list(info.max_rank_by_depth[1:k + 1]),
+            "mean_rank_by_depth": list(info.mean_rank_by_depth[1:k + 1]),
+            "factor_bytes": info.factor_bytes, "t_build": info.t_build, "t_factor": info.t_factor,
+            "t_logdet": info.t_logdet, "t_solve": info.t_solve, "rank_cap_hits": info.rank_cap_hits,
+            "aca_steps": info.aca_steps, "gpu_launches_last": info.gpu_launches_last}
+
+
+def hodlr_free(h: int):
+    if h:
+        load().hodlr_free(h)
+
+
+class HODLR:
+    """build -> factor -> {logdet, solve, gp_loglik}* on one GPU; inputs are CUDA float64 tensors."""
+
+    def __init__(self, x: torch.Tensor, kernel, theta, sigma2: float, leaf: int, eps: float,
+                 rank_cap: int = 0, stream=None):
+        if isinstance(kernel, str):
+            kernel = KERNELS[kernel]
+        self.n = x.numel()
+        self._h = hodlr_build(x, kernel, theta, sigma2, leaf, eps, rank_cap, stream)
+
+    def __del__(self):
+        h = getattr(self, "_h", 0)
+        if h:
+            hodlr_free(h)
+            self._h = 0
+
+    def close(self):
+        self.__del__()
+
+    def factor(self):
+        hodlr_factor(self._h)
+        return self
+
+    def logdet(self) -> float:
+        return hodlr_logdet(self._h)
+
+    def solve(self, y: torch.Tensor) -> torch.Tensor:
+        return hodlr_solve(self._h, y)
+
+    def gp_loglik(self, y: torch.Tensor) -> float:
+        return gp_loglik(self._h, y)
+
+    def info(self) -> dict:
+        return hodlr_info(self._h)
+
+    def order(self):
+        xs = torch.empty(self.n, dtype=torch.float64, device="cuda")
+        perm = torch.empty(self.n, dtype=torch.int64, device="cuda")
+        _check(load().hodlr_get_order(self._h, xs.data_ptr(), perm.data_ptr()))
+        return xs, perm
+
+    def tree(self):
+        import numpy as np
+        k = self.info()["kappa"]
+        nn = (1 << (k + 1)) - 1; ni = (1 << k) - 1
+        lo = np.zeros(nn, dtype=np.int64); hi = np.zeros(nn, dtype=np.int64); r = np.zeros(max(ni, 1), dtype=np.int32)
+        _check(load().hodlr_get_tree(self._h, lo.ctypes.data, hi.ctypes.data, r.ctypes.data))
+        return lo, hi, r[:ni]
+
+    def logdet_parts(self):
+        import numpy as np
+        k = self.info()["kappa"]
+        a = np.zeros(1 << k); b = np.zeros(max((1 << k) - 1, 1))
+        _check(load().hodlr_get_logdet_parts(self._h, a.ctypes.data, b.ctypes.data))
+        return a, b[:(1 << k) - 1]

@@ -1,0 +1,193 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the same seeded inputs.
+
+Tolerances (north_star): integer structures (perm, tree) bit-exact;
+|d logdet| / |logdet| <= 1e-9 and ||dx|| / ||x|| <= 1e-9 at eps = 1e-12.  ACA pivots/ranks are
+FP-derived (R11) and are reported, with a loose bound on the mismatch.
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import OracleHODLR, OracleError  # noqa: E402
+from paper_1403_6015_b200 import inputs  # noqa: E402
+
+LD_TOL = 1e-9
+X_TOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def hb():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1403_6015_b200.hodlr as hb
+    hb.load()
+    return hb
+
+
+def run_both(hb, x, y, kernel, theta, s2, leaf, eps, rank_cap=0):
+    o = OracleHODLR(x, kernel, theta, s2, leaf, eps, rank_cap).factor()
+    ld_o = o.logdet(); x_o = o.solve(y); ll_o = o.gp_loglik(y)
+    xd = torch.from_numpy(x).cuda(); yd = torch.from_numpy(y).cuda()
+    g = hb.HODLR(xd, kernel, theta, s2, leaf, eps, rank_cap).factor()
+    ld_g = g.logdet(); x_g = g.solve(yd).cpu().numpy(); ll_g = g.gp_loglik(yd)
+    return o, g, (ld_o, x_o, ll_o), (ld_g, x_g, ll_g)
+
+
+def check_parity(o, g, ro, rg, ld_tol=LD_TOL, x_tol=X_TOL, exact_structure=True):
+    ld_o, x_o, ll_o = ro
+    ld_g, x_g, ll_g = rg
+    print(f"[parity] n={x_o.size} logdet rel {abs(ld_g - ld_o) / abs(ld_o):.2e} "
+          f"solve rel {np.linalg.norm(x_g - x_o) / np.linalg.norm(x_o):.2e} loglik rel {abs(ll_g - ll_o) / abs(ll_o):.2e}")
+    assert abs(ld_g - ld_o) <= ld_tol * abs(ld_o) + 1e-12, (ld_g, ld_o)
+    assert np.linalg.norm(x_g - x_o) <= x_tol * np.linalg.norm(x_o), np.linalg.norm(x_g - x_o) / np.linalg.norm(x_o)
+    assert abs(ll_g - ll_o) <= ld_tol * (abs(ll_o) + abs(ld_o)), (ll_g, ll_o)
+    if exact_structure:
+        xs_g, perm_g = g.order()
+        np.testing.assert_array_equal(perm_g.cpu().numpy(), o.perm())
+        np.testing.assert_array_equal(xs_g.cpu().numpy(), o.sorted_x())
+        lo_g, hi_g, r_g = g.tree()
+        lo_o, hi_o = o.tree()
+        np.testing.assert_array_equal(lo_g, lo_o)
+        np.testing.assert_array_equal(hi_g, hi_o)
+        r_o = o.ranks()
+        if len(r_o):
+            mism = np.mean(r_g != r_o)
+            assert mism <= 0.25, f"rank mismatch fraction {mism}"
+            assert np.all(np.abs(r_g.astype(int) - r_o.astype(int)) <= 2)
+
+
+CFG_CASES = [
+    ("cfg1", 2048),
+    ("cfg2", 65536),
+    ("cfg3", 1 << 16),
+    ("cfg5", 1 << 15),
+]
+
+
+@pytest.mark.parametrize("name,n", CFG_CASES, ids=[f"{a}-{b}" for a, b in CFG_CASES])
+def test_config_parity(hb, name, n):
+    cfg = inputs.scaled(inputs.CONFIGS[name], n)
+    x = inputs.points(cfg); y = inputs.rhs(cfg)
+    o, g, ro, rg = run_both(hb, x, y, cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, 1e-12)
+    check_parity(o, g, ro, rg)
+
+
+@pytest.mark.parametrize("k", [0, 17, 63])
+def test_cfg4_sweep_parity(hb, k):
+    cfg = inputs.CONFIGS["cfg4"]
+    ell, s2 = inputs.sweep_settings(cfg)
+    c = inputs.scaled(cfg, 1 << 14)
+    x = inputs.points(c); y = inputs.rhs(c)
+    o, g, ro, rg = run_both(hb, x, y, cfg.kernel, (1.0, ell[k]), s2[k], cfg.leaf, 1e-12)
+    check_parity(o, g, ro, rg, x_tol=1e-8)   # conditioning floor at the sweep corners (R15)
+
+
+@pytest.mark.parametrize("n,leaf", [(1, 64), (17, 64), (64, 64), (127, 64), (128, 64), (1999, 50), (3001, 37),
+                                    (4097, 128)])
+def test_edge_sizes(hb, n, leaf):
+    rng = np.random.default_rng(n)
+    x = rng.uniform(-3, 3, n); y = rng.standard_normal(n)
+    o, g, ro, rg = run_both(hb, x, y, 0, (1.0, 1 / math.sqrt(2)), 1.0, leaf, 1e-12)
+    check_parity(o, g, ro, rg)
+
+
+@pytest.mark.parametrize("kernel", [0, 1, 2])
+def test_unsorted_with_ties(hb, kernel):
+    rng = np.random.default_rng(9)
+    n = 5000
+    x = np.round(rng.uniform(0, 20, n), 2)      # many exact ties
+    x[::101] = -0.0
+    y = rng.standard_normal(n)
+    o, g, ro, rg = run_both(hb, x, y, kernel, (1.3, 0.7), 1e-2, 64, 1e-12)
+    check_parity(o, g, ro, rg)
+
+
+def test_multi_rhs(hb):
+    rng = np.random.default_rng(3)
+    n = 3000
+    x = rng.uniform(0, 5, n); Y = rng.standard_normal((n, 3))
+    o = OracleHODLR(x, 1, (1.0, 0.5), 1e-3, 64, 1e-12).factor()
+    g = hb.HODLR(torch.from_numpy(x).cuda(), 1, (1.0, 0.5), 1e-3, 64, 1e-12).factor()
+    Xg = g.solve(torch.from_numpy(Y).cuda()).cpu().numpy()
+    Xo = o.solve(Y)
+    assert np.linalg.norm(Xg - Xo) <= X_TOL * np.linalg.norm(Xo)
+
+
+def test_logdet_parts_match(hb):
+    cfg = inputs.CONFIGS["cfg1"]
+    x = inputs.points(cfg)
+    o = OracleHODLR(x, cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, 1e-12).factor()
+    g = hb.HODLR(torch.from_numpy(x).cuda(), cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, 1e-12).factor()
+    la_o, nb_o = o.logdet_parts()
+    la_g, nb_g = g.logdet_parts()
+    np.testing.assert_allclose(la_g, la_o, rtol=1e-12)          # leaf Cholesky: same matrix, same algorithm
+    np.testing.assert_allclose(nb_g, nb_o, rtol=1e-6, atol=1e-9)  # coupling dets: eps-level differences
+
+
+def test_closed_forms_on_gpu(hb):
+    """Pins that hold independently of the oracle: K = 0 and the rank-1 Sylvester case."""
+    n, s2 = 2048, 1e-2
+    rng = np.random.default_rng(1)
+    x = rng.uniform(0, 1, n); y = rng.standard_normal(n)
+    g = hb.HODLR(torch.from_numpy(x).cuda(), 0, (0.0, 0.1), s2, 64, 1e-12).factor()
+    assert g.logdet() == pytest.approx(n * math.log(s2), rel=1e-14)
+    np.testing.assert_allclose(g.solve(torch.from_numpy(y).cuda()).cpu().numpy(), y / s2, rtol=1e-14)
+    g = hb.HODLR(torch.from_numpy(x[:1024]).cuda(), 0, (1.0, 1e20), s2, 64, 1e-12).factor()
+    assert g.logdet() == pytest.approx(1023 * math.log(s2) + math.log(s2 + 1024), rel=1e-12)
+
+
+def test_errors(hb):
+    xd = torch.linspace(0, 1, 100, dtype=torch.float64, device="cuda")
+    for kw in [dict(leaf=0), dict(eps=0.0), dict(s2=-1.0), dict(theta=(1.0, 0.0)), dict(kernel=5)]:
+        args = dict(kernel=0, theta=(1.0, 0.1), s2=1e-2, leaf=16, eps=1e-12)
+        args.update(kw)
+        with pytest.raises(hb.HodlrError) as e:
+            hb.HODLR(xd, args["kernel"], args["theta"], args["s2"], args["leaf"], args["eps"])
+        assert e.value.status == "EINVAL"
+    bad = xd.clone(); bad[7] = float("nan")
+    with pytest.raises(hb.HodlrError) as e:
+        hb.HODLR(bad, 0, (1.0, 0.1), 1e-2, 16, 1e-12)
+    assert e.value.status == "EINVAL"
+    g = hb.HODLR(xd, 0, (1.0, 0.1), 1e-2, 16, 1e-12)
+    with pytest.raises(hb.HodlrError) as e:
+        g.solve(torch.ones(100, dtype=torch.float64, device="cuda"))
+    assert e.value.status == "ESTATE"
+    g.factor()
+    yb = torch.ones(100, dtype=torch.float64, device="cuda"); yb[3] = float("inf")
+    with pytest.raises(hb.HodlrError) as e:
+        g.solve(yb)
+    assert e.value.status == "EINVAL"
+    dup = torch.from_numpy(np.repeat(np.linspace(0, 1, 50), 2)).cuda()
+    gd = hb.HODLR(dup, 0, (1.0, 0.1), 0.0, 16, 1e-12)
+    with pytest.raises(hb.HodlrError) as e:
+        gd.factor()
+    assert e.value.status == "ENOTPD"
+    with pytest.raises(hb.HodlrError):
+        gd.logdet()
+    rng = np.random.default_rng(0)
+    xr = torch.from_numpy(rng.uniform(0, 1, 512)).cuda()
+    with pytest.raises(hb.HodlrError) as e:
+        hb.HODLR(xr, 0, (1.0, 0.01), 1e-2, 16, 1e-12, rank_cap=2)
+    assert e.value.status == "ERANKCAP"
+
+
+def test_full_size_cfg3_bench_config(hb):
+    """BASELINE.json config 3 at full size in the bench's configuration (n = 2^20, eps = 1e-10):
+    sampled rows of the residual C x - y computed one by one on the CPU, and the oracle's log det."""
+    cfg = inputs.CONFIGS["cfg3"]
+    x = inputs.points(cfg); y = inputs.rhs(cfg)
+    g = hb.HODLR(torch.from_numpy(x).cuda(), cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, cfg.eps).factor()
+    ld_g = g.logdet()
+    xg = g.solve(torch.from_numpy(y).cuda()).cpu().numpy()
+    rng = np.random.default_rng(123)
+    rows = rng.choice(cfg.n, 64, replace=False)
+    for i in rows:
+        ci = np.exp(-(x[i] - x) ** 2 / (2 * cfg.ell ** 2)) * cfg.a ** 2
+        ci[i] += cfg.sigma2
+        assert abs(ci @ xg - y[i]) <= 1e-6 * np.abs(y).max()
+    o = OracleHODLR(x, cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, cfg.eps).factor()
+    assert abs(ld_g - o.logdet()) <= LD_TOL * abs(o.logdet())

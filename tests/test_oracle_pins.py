@@ -260,12 +260,17 @@ CASES = [
 ]
 
 
+CASES.append(("exact-duplicates", 3000, 0.0, 12.0, SE, (1.3, 0.7), 1e-2, 64))
+
+
 @pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
 def test_hodlr_vs_dense(case):
     """log det <= 1e-12 rel and solve <= 1e-9 rel against numpy dense (independent LAPACK path)."""
     _, n, lo, hi, k, th, s2, p = case
     rng = np.random.default_rng(11)
     x = rng.uniform(lo, hi, n); y = rng.standard_normal(n)
+    if case[0] == "exact-duplicates":     # ~2.5 points per distinct value, plus a block of zeros (DESIGN.md R2)
+        x = np.round(x, 2); x[::97] = 0.0
     h = OracleHODLR(x, k, th, s2, p, 1e-12).factor()
     C = dense_C(x, k, th, s2)
     sd, ld = np.linalg.slogdet(C)
