@@ -1,0 +1,338 @@
+#!/usr/bin/env python
+"""bench.py -- HODLR factor + logdet + solve throughput on B200 (BASELINE.json config 3).
+
+One "step" is one pass of the whole hot path over the config-3 workload with the inputs resident
+in HBM: hodlr_build (sort + tree + ACA, the paper's "Assembly"), hodlr_factor, hodlr_logdet and
+hodlr_solve of one right-hand side (PAPER.md:1270-1281 columns Assembly/Factor/Det./Solve).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0 (contract in the task statement).
+--impl reference times the CPU oracle (oracle/, plain single-threaded C) on a bounded sample of
+the same workload; it is the reference arm of this tier (there is no reference implementation).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1403_6015_b200 import inputs  # noqa: E402
+
+METRIC = "HODLR factor+logdet+solve seconds and points/s at n=2^20, 1/2/4/8 B200"
+UNIT = "points/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--config", default="cfg3")
+    p.add_argument("--cpu-sample", type=int, default=1 << 17, help="oracle sample size (points)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def workload_desc(cfg):
+    kname = {0: "squared-exponential", 1: "Matern-3/2", 2: "Matern-5/2"}[cfg.kernel]
+    return (f"{cfg.name}: n={cfg.n} 1-D x~U[{cfg.lo:g},{cfg.hi:g}] sorted (seed {cfg.seed}), {kname} a={cfg.a:g} "
+            f"ell={cfg.ell:g} sigma2={cfg.sigma2:g}, y~N(0,1), leaf {cfg.leaf}, eps={cfg.eps:g}, FP64")
+
+
+# ------------------------------------------------------------------ oracle (CPU) timing
+def oracle_sample(cfg, n_sample):
+    """Time the oracle as it stands (build + factor + logdet + solve) on the first n_sample points of the
+    same density (interval scaled), single-threaded.  Returns (seconds, n_sample)."""
+    from oracle import OracleHODLR
+    c = inputs.scaled(cfg, n_sample)
+    x = inputs.points(c); y = inputs.rhs(c)
+    t0 = time.perf_counter()
+    h = OracleHODLR(x, c.kernel, c.theta, c.sigma2, c.leaf, c.eps).factor()
+    h.logdet()
+    h.solve(y)
+    return time.perf_counter() - t0, n_sample
+
+
+def cpu_baseline_obj(cfg, n_sample):
+    t, ns = oracle_sample(cfg, n_sample)
+    return {"value": ns / t, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"oracle (oracle/hodlr_oracle.c, gcc -O2, 1 thread) build+factor+logdet+solve on n={ns} "
+                      f"points of the {cfg.name} workload (same density: interval scaled to "
+                      f"[{cfg.lo:g},{cfg.lo + (cfg.hi - cfg.lo) * ns / cfg.n:g}]), {t:.2f} s"}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    cfg = inputs.CONFIGS[args.config]
+    ns = args.cpu_sample
+    for _ in range(args.warmup):
+        oracle_sample(cfg, ns)
+    ts = [oracle_sample(cfg, ns)[0] for _ in range(args.steps)]
+    t = sum(ts) / len(ts)
+    value = ns / t
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_desc(cfg), "sample_points": ns, "parallelism": "1 CPU thread"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"n={ns} points of {cfg.name} (same density), per step"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    def __init__(self, dev):
+        self.dev = dev
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill(); out, _ = self.proc.communicate()
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                s = float(f[0]); m = float(f[1])
+            except ValueError:
+                continue
+            mx = max(mx, m)
+            if s > 0.5 * m:                      # under load
+                sm.append(s)
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(getattr(self, "lines", []))}
+
+
+# ------------------------------------------------------------------ algorithmic counts
+def algorithmic(info, n, leaf):
+    """Per-launch algorithmic FLOPs / bytes of each kernel family for the formulation implemented."""
+    K = info["K"]
+    r = info["max_rank_by_depth"]
+    p = leaf
+    nl = n // p
+    # leaf factor (one launch): assemble p^2/2 entries (~30 flop each), Cholesky p^3/3, Z = L^{-1}E (p^2 K),
+    # Pi = Z^T Z (p K^2, symmetric half); bytes: read E (8 n K), write L (4 n (p+1)) and Pi (8 K^2 per leaf)
+    leaf_flops = nl * (30 * p * p / 2 + p ** 3 / 3 + p * p * K + p * K * K)
+    leaf_bytes = 8 * n * K + 4 * n * (p + 1) + 8 * nl * K * K
+    # ACA: n * K entry evaluations (~30 flop) + 2 n sum r^2 arithmetic x2 (row and column residual + dots)
+    aca_flops = n * K * 30 + 4 * n * sum(x * x for x in r)
+    aca_bytes = 8 * n * K + 4 * n * sum(x * x for x in r)
+    return {"leaf_factor": (leaf_flops, leaf_bytes), "aca": (aca_flops, aca_bytes)}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+def fp64_peak_tflops(peaks, sm_mhz):
+    """FP64 peak: B200 issues 64 FP64 FMA/clk/SM (DFMA and DMMA alike): 148 * 64 * 2 * f.  Uses the
+    measured fp64 number in MEASURED_PEAKS.json if present, else this unit count at the clock seen."""
+    if "fp64_tflops" in peaks:
+        return peaks["fp64_tflops"], "measured (MEASURED_PEAKS.json fp64_tflops)"
+    f = (sm_mhz or peaks.get("clocks_under_load", {}).get("sm_mhz_median") or 1965.0) * 1e6
+    return 148 * 64 * 2 * f / 1e12, f"derived: 148 SMs x 64 FP64 FMA/clk x 2 x {f / 1e6:.0f} MHz (guide unit counts)"
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    ws, rank, local = dist_env()
+    if ws > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", init_method="env://")
+    dev = torch.cuda.current_device()
+    from paper_1403_6015_b200 import hodlr as hb
+    hb.load()
+    cfg = inputs.CONFIGS[args.config]
+    n = cfg.n
+    x = inputs.points(cfg); y = inputs.rhs(cfg)
+    xd = torch.from_numpy(x).to(dev); yd = torch.from_numpy(y).to(dev)
+    xh = torch.from_numpy(x).pin_memory(); yh = torch.from_numpy(y).pin_memory()
+    sol_h = torch.empty(n, dtype=torch.float64).pin_memory()
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)     # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def step(xin, yin):
+        h = hb.HODLR(xin, cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, cfg.eps)
+        h.factor()
+        ld = h.logdet()
+        sol = h.solve(yin)
+        info = h.info()
+        h.close()
+        return ld, sol, info
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step(xd, yd)
+    torch.cuda.synchronize()
+    # ---------------- device-resident timed region
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    fam_ms = {}
+    infos = []
+    barrier(); torch.cuda.synchronize()
+    l0 = hb.hodlr_launch_count()
+    with ClockSampler(dev) as clk:
+        for i in range(args.steps):
+            flush.zero_()                                    # L2 flush between timed steps (untimed)
+            evs[i][0].record(stream)
+            ld, sol, info = step(xd, yd)
+            evs[i][1].record(stream)
+            infos.append(info)
+        torch.cuda.synchronize()
+    barrier()
+    launches = hb.hodlr_launch_count() - l0
+    ms = [a.elapsed_time(b) for a, b in evs]
+    t_step = sum(ms) / len(ms) / 1e3
+    for inf in infos:
+        for k, v in inf["kernel_ms"].items():
+            fam_ms[k] = fam_ms.get(k, 0.0) + v
+    fam_ms = {k: v / len(infos) for k, v in fam_ms.items()}
+    t_max = t_step
+    if ws > 1:
+        tt = torch.tensor([t_step], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+    # ---------------- end-to-end through the C-ABI with host buffers
+    for _ in range(1):
+        xd.copy_(xh, non_blocking=True); yd.copy_(yh, non_blocking=True)
+        _, s, _ = step(xd, yd); sol_h.copy_(s, non_blocking=True); torch.cuda.synchronize()
+    e2e_ms = []
+    barrier(); torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        xd.copy_(xh, non_blocking=True); yd.copy_(yh, non_blocking=True)
+        ld_e, s, _ = step(xd, yd)
+        sol_h.copy_(s, non_blocking=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms.append(a.elapsed_time(b))
+    barrier()
+    t_e2e = sum(e2e_ms) / len(e2e_ms) / 1e3
+    if ws > 1:
+        tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = float(tt.item())
+    # sanity: solution is finite and the log det is the expected magnitude
+    assert math.isfinite(ld) and torch.isfinite(sol).all().item()
+    if rank != 0:
+        if ws > 1:
+            dist.destroy_process_group()
+        return 0
+    info = infos[-1]
+    clocks = clk.summary()
+    peaks = load_peaks()
+    # ---------------- roofline of the dominant kernel family
+    alg = algorithmic(info, n, cfg.leaf)
+    dom = max(fam_ms, key=lambda k: fam_ms[k])
+    calls = info["kernel_calls"][dom] or 1
+    t_launch = fam_ms[dom] / calls / 1e3
+    if dom in alg:
+        fl, by = alg[dom]
+        if dom == "leaf_factor":
+            peak, how = fp64_peak_tflops(peaks, clocks.get("sm_mhz"))
+            achieved = fl / t_launch / 1e12
+            roof = {"kernel": "k_leaf_factor", "bound": "alu", "achieved": achieved, "peak": peak,
+                    "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None, "peak_source": how,
+                    "algorithmic_flops_per_launch": fl, "launch_ms": 1e3 * t_launch}
+        else:
+            peak = peaks.get("hbm_gbs", 6650.0)
+            achieved = by / t_launch / 1e9
+            roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": None,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650",
+                    "algorithmic_bytes_per_launch": by, "launch_ms": 1e3 * t_launch}
+    else:
+        roof = {"kernel": dom, "bound": "alu", "achieved": None, "peak": None, "unit": None, "frac": None,
+                "traffic": None}
+    cpu = None
+    if not args.no_cpu_baseline and ws == 1:
+        cpu = cpu_baseline_obj(cfg, args.cpu_sample)
+    value = n * ws / t_max
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t_max, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_desc(cfg), "n": n,
+                       "parallelism": "replicas" if ws > 1 else "1 GPU",
+                       "l2": "flushed between timed steps (512 MB device write, untimed)",
+                       "kappa": info["kappa"], "K": info["K"], "ranks_by_depth": info["max_rank_by_depth"],
+                       "phase_ms": {"assembly(build)": 1e3 * info["t_build"], "factor": 1e3 * info["t_factor"],
+                                    "det": 1e3 * info["t_logdet"], "solve": 1e3 * info["t_solve"]},
+                       "kernel_family_ms": fam_ms, "seconds_per_step": t_max,
+                       "gpu_launches_per_step": launches / args.steps},
+            "roofline": roof, "cpu_baseline": cpu,
+            "e2e": {"value": n * ws / t_e2e, "unit": UNIT, "h2d_bytes_per_step": 16 * n,
+                    "d2h_bytes_per_step": 8 * n + 8, "ms_per_step": 1e3 * t_e2e},
+            "gpu_launches": launches, "clocks": clocks}
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -78,6 +78,11 @@ typedef struct {
   int64_t rank_cap_hits;        /* blocks that hit the rank cap */
   int32_t aca_steps;            /* ACA pivot steps executed (max rank + 1) */
   int32_t gpu_launches_last;    /* kernels launched by the last API call */
+  /* Device time (ms, CUDA events on the handle's stream) accumulated since build, and call counts, per
+   * kernel family: [0] sort, [1] ACA, [2] leaf factor, [3] coupling tree, [4] solve leaf up,
+   * [5] solve tree up/down, [6] solve leaf down. */
+  double  kernel_ms[16];
+  int64_t kernel_calls[16];
 } hodlr_info_t;
 
 /* "Assembly": stable sort of x (O(n), K1), balanced count-median
@@ -127,6 +132,9 @@ const char *hodlr_last_error(void);
 
 /* Library self-description, e.g. "hodlr_b200 sm_100a". */
 const char *hodlr_version(void);
+
+/* Number of CUDA kernels this library has launched in the process (all handles). */
+int64_t hodlr_launch_count(void);
 
 #ifdef __cplusplus
 }

@@ -339,6 +339,7 @@ hodlr_status hodlr_aca(hodlr_s *h) {
   c.kp = h->kp; c.n = n; c.eps = h->eps; c.xs = h->xs; c.lo = h->lo; c.hi = h->hi; c.Xh = h->Xh;
   c.used = h->used; c.st = h->ast; c.active = h->dflags + 4; c.rank = h->rank; c.bdepth = h->bdepth;
   c.dt = h->d_dt;
+  ph_begin(h, PH_ACA);
   k_aca_init<<<(int)((nb + 255) / 256), 256, 0, h->st>>>(c, (int)nb, h->cap);
   HLAUNCH(h, "k_aca_init");
 
@@ -382,6 +383,7 @@ hodlr_status hodlr_aca(hodlr_s *h) {
     }
     if (stop) break;
   }
+  ph_end(h, PH_ACA);
   HCUDA(cudaStreamSynchronize(h->st));
   for (int i = 0; i < 8; i++) cudaEventDestroy(evs[i]);
   cudaFreeHost(pinned);

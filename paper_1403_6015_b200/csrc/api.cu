@@ -8,6 +8,7 @@
 #include <vector>
 
 static thread_local char g_err[1024] = "";
+long long hodlr_global_launches = 0;
 
 hodlr_status hodlr_set_error(hodlr_status code, const char *fmt, ...) {
   va_list ap; va_start(ap, fmt); vsnprintf(g_err, sizeof g_err, fmt, ap); va_end(ap);
@@ -48,6 +49,12 @@ static hodlr_status finish(hodlr_s *h, hodlr_status st, double *tsec) {
   if (e2 != cudaSuccess) return hodlr_cuda_check(e2, "stream synchronize");
   float ms = 0.f;
   if (cudaEventElapsedTime(&ms, h->ev0, h->ev1) == cudaSuccess && tsec) *tsec = ms * 1e-3;
+  for (int p = 0; p < PH_N; p++) {
+    if (!h->ph_pending[p]) continue;
+    float pm = 0.f;
+    if (cudaEventElapsedTime(&pm, h->ph_ev[p][0], h->ph_ev[p][1]) == cudaSuccess) { h->ph_ms[p] += pm; h->ph_calls[p]++; }
+    h->ph_pending[p] = 0;
+  }
   return HODLR_OK;
 }
 
@@ -55,6 +62,7 @@ extern "C" {
 
 const char *hodlr_last_error(void) { return g_err; }
 const char *hodlr_version(void) { return "hodlr_b200 0.1 sm_100a fp64"; }
+int64_t hodlr_launch_count(void) { return hodlr_global_launches; }
 
 void hodlr_free(hodlr_t h) {
   if (!h) return;
@@ -62,6 +70,7 @@ void hodlr_free(hodlr_t h) {
   cudaStreamSynchronize(h->st);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
+  for (int p = 0; p < PH_N; p++) for (int j = 0; j < 2; j++) if (h->ph_ev[p][j]) cudaEventDestroy(h->ph_ev[p][j]);
   delete[] h->h_lo; delete[] h->h_hi; delete[] h->h_rank;
   delete h;
 }
@@ -91,7 +100,9 @@ hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const 
   if (ce != cudaSuccess) { delete h; return hodlr_cuda_check(ce, "cudaGetDevice"); }
   setup_pool(h->dev);
   cudaEventCreate(&h->ev0); cudaEventCreate(&h->ev1);
+  for (int p = 0; p < PH_N; p++) for (int j = 0; j < 2; j++) cudaEventCreate(&h->ph_ev[p][j]);
   cudaEventRecord(h->ev0, h->st);
+  h->launches = 0;
   h->n = n; h->leaf = leaf; h->eps = eps; h->cap = cap; h->theta[0] = theta[0]; h->theta[1] = theta[1];
   h->kp.kern = (int)kernel; h->kp.a2 = theta[0] * theta[0]; h->kp.s2 = sigma2;
   h->kp.c = kernel == HODLR_SE ? 1.0 / (2.0 * theta[1] * theta[1])
@@ -279,6 +290,7 @@ hodlr_status hodlr_info(hodlr_t h, hodlr_info_t *info) {
   info->rank_cap_hits = h->rank_cap_hits;
   info->aca_steps = h->aca_steps;
   info->gpu_launches_last = h->launches;
+  for (int p = 0; p < PH_N && p < 16; p++) { info->kernel_ms[p] = h->ph_ms[p]; info->kernel_calls[p] = h->ph_calls[p]; }
   return HODLR_OK;
 }
 

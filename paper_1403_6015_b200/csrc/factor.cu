@@ -358,8 +358,10 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
     lc.scratch = (double *)hodlr_dalloc(h, sizeof(double) * lc.scratch_per_cta * grid);
     if (!lc.scratch) return hodlr_set_error(HODLR_ENOMEM, "factor: scratch allocation failed");
   }
+  ph_begin(h, PH_LEAF);
   k_leaf_factor<<<grid, LT, need, h->st>>>(lc);
   HLAUNCH(h, "k_leaf_factor");
+  ph_end(h, PH_LEAF);
   // ---- tree, bottom-up ----
   size_t tree_smem_max = 0;
   for (int d = 0; d < kappa; d++) {
@@ -370,6 +372,7 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
     return hodlr_set_error(HODLR_EINVAL, "factor: coupling system too large for shared memory");
   if (kappa > 0)
     HCUDA(cudaFuncSetAttribute(k_tree_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tree_smem_max));
+  ph_begin(h, PH_TREE);
   for (int d = kappa - 1; d >= 0; d--) {
     TreeCtx tc;
     tc.d = d; tc.r = dt.rdep[d + 1]; tc.q = 2 * tc.r; tc.Kd = dt.Kdim[d]; tc.K1 = dt.Kdim[d + 1];
@@ -382,5 +385,6 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
   }
   k_logdet_reduce<<<1, 256, 0, h->st>>>(h->leaf_ld, h->node_ld, nl, kappa, h->d_logdet);
   HLAUNCH(h, "k_logdet_reduce");
+  ph_end(h, PH_TREE);
   return HODLR_OK;
 }

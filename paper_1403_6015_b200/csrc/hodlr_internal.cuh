@@ -89,6 +89,11 @@ struct AcaCtx {
 };
 
 // ----------------------------------------------------------------------------------------------
+// Per-kernel-family device timing (CUDA events on the handle's stream)
+// ----------------------------------------------------------------------------------------------
+enum { PH_SORT = 0, PH_ACA, PH_LEAF, PH_TREE, PH_SLEAF_UP, PH_STREE, PH_SLEAF_DOWN, PH_N };
+
+// ----------------------------------------------------------------------------------------------
 // Handle
 // ----------------------------------------------------------------------------------------------
 struct hodlr_s {
@@ -134,13 +139,21 @@ struct hodlr_s {
   long long bytes;
   double t_build, t_factor, t_logdet, t_solve;
   cudaEvent_t ev0, ev1;
+  cudaEvent_t ph_ev[PH_N][2];
+  int ph_pending[PH_N];
+  double ph_ms[PH_N];        // accumulated device ms per kernel family (since build)
+  long long ph_calls[PH_N];
   void *allocs[64]; int nallocs;
 };
+
+static inline void ph_begin(hodlr_s *h, int p) { cudaEventRecord(h->ph_ev[p][0], h->st); }
+static inline void ph_end(hodlr_s *h, int p) { cudaEventRecord(h->ph_ev[p][1], h->st); h->ph_pending[p] = 1; }
 
 // helpers implemented in api.cu
 hodlr_status hodlr_set_error(hodlr_status code, const char *fmt, ...);
 hodlr_status hodlr_cuda_check(cudaError_t e, const char *what);
 void *hodlr_dalloc(hodlr_s *h, size_t bytes);
+extern long long hodlr_global_launches;
 
 // phase entry points (one per .cu file)
 hodlr_status hodlr_sort_and_tree(hodlr_s *h, const double *x);
@@ -151,7 +164,7 @@ hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_on
 static inline int hodlr_depth_of(long long id) { int d = 0; while (id >= ((2LL << d) - 1)) d++; return d; }
 
 #define HCUDA(call) do { cudaError_t _e = (call); if (_e != cudaSuccess) return hodlr_cuda_check(_e, #call); } while (0)
-#define HLAUNCH(h, name) do { (h)->launches++; cudaError_t _e = cudaGetLastError(); \
+#define HLAUNCH(h, name) do { (h)->launches++; hodlr_global_launches++; cudaError_t _e = cudaGetLastError(); \
     if (_e != cudaSuccess) return hodlr_cuda_check(_e, "launch " name); } while (0)
 
 // ----------------------------------------------------------------------------------------------

@@ -229,18 +229,24 @@ hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_on
   size_t smem_dn = sizeof(double) * (h->lstride + h->leaf_max);
   HCUDA(cudaFuncSetAttribute(k_leaf_up, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_up));
   HCUDA(cudaFuncSetAttribute(k_leaf_down, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_dn));
+  ph_begin(h, PH_SLEAF_UP);
   k_leaf_up<<<(int)h->nleaves, ST, smem_up, h->st>>>(c);
   HLAUNCH(h, "k_leaf_up");
+  ph_end(h, PH_SLEAF_UP);
+  ph_begin(h, PH_STREE);
   for (int d = kappa - 1; d >= 0; d--) {
     k_tree_up<<<(int)(1LL << d), ST, 0, h->st>>>(c, d);
     HLAUNCH(h, "k_tree_up");
   }
-  if (up_only) return HODLR_OK;
+  if (up_only) { ph_end(h, PH_STREE); return HODLR_OK; }
   for (int d = 0; d < kappa; d++) {
     k_tree_down<<<(int)(1LL << d), ST, 0, h->st>>>(c, d);
     HLAUNCH(h, "k_tree_down");
   }
+  ph_end(h, PH_STREE);
+  ph_begin(h, PH_SLEAF_DOWN);
   k_leaf_down<<<(int)h->nleaves, ST, smem_dn, h->st>>>(c);
   HLAUNCH(h, "k_leaf_down");
+  ph_end(h, PH_SLEAF_DOWN);
   return HODLR_OK;
 }

@@ -125,6 +125,7 @@ hodlr_status hodlr_sort_and_tree(hodlr_s *h, const double *x) {
   unsigned int *cnt = (unsigned int *)hodlr_dalloc(h, sizeof(unsigned int) * 256 * (size_t)ntiles);
   if (!k0 || !k1 || !i0 || !i1 || !cnt) return hodlr_set_error(HODLR_ENOMEM, "sort: device allocation failed");
   int nb = (int)((n + 255) / 256);
+  ph_begin(h, PH_SORT);
   k_make_keys<<<nb, 256, 0, h->st>>>(x, n, k0, i0, h->dflags);
   HLAUNCH(h, "k_make_keys");
   for (int pass = 0; pass < 8; pass++) {
@@ -140,5 +141,6 @@ hodlr_status hodlr_sort_and_tree(hodlr_s *h, const double *x) {
   }
   k_finish<<<nb, 256, 0, h->st>>>(k0, i0, n, h->xs, h->perm);
   HLAUNCH(h, "k_finish");
+  ph_end(h, PH_SORT);
   return HODLR_OK;
 }

@@ -20,7 +20,7 @@ STATUS = {0: "OK", 1: "EINVAL", 2: "ENOTPD", 3: "ERANKCAP", 4: "ESTATE", 5: "ENO
 
 EXPORTS = ("hodlr_build", "hodlr_factor", "hodlr_logdet", "hodlr_solve", "gp_loglik", "hodlr_info",
            "hodlr_get_order", "hodlr_get_tree", "hodlr_get_logdet_parts", "hodlr_free", "hodlr_last_error",
-           "hodlr_version")
+           "hodlr_version", "hodlr_launch_count")
 
 
 class HodlrError(RuntimeError):
@@ -43,7 +43,10 @@ class hodlr_info_t(C.Structure):
                 ("max_rank_by_depth", C.c_int32 * 64), ("mean_rank_by_depth", C.c_double * 64),
                 ("factor_bytes", C.c_int64), ("t_build", C.c_double), ("t_factor", C.c_double),
                 ("t_logdet", C.c_double), ("t_solve", C.c_double), ("rank_cap_hits", C.c_int64),
-                ("aca_steps", C.c_int32), ("gpu_launches_last", C.c_int32)]
+                ("aca_steps", C.c_int32), ("gpu_launches_last", C.c_int32),
+                ("kernel_ms", C.c_double * 16), ("kernel_calls", C.c_int64 * 16)]
+
+KERNEL_FAMILIES = ("sort", "aca", "leaf_factor", "coupling_tree", "solve_leaf_up", "solve_tree", "solve_leaf_down")
 
 
 _lib = None
@@ -82,6 +85,7 @@ def load(build_if_missing: bool = True):
         lib.hodlr_free.argtypes = [P]; lib.hodlr_free.restype = None
         lib.hodlr_last_error.argtypes = []; lib.hodlr_last_error.restype = C.c_char_p
         lib.hodlr_version.argtypes = []; lib.hodlr_version.restype = C.c_char_p
+        lib.hodlr_launch_count.argtypes = []; lib.hodlr_launch_count.restype = C.c_int64
         _lib = lib
         return lib
 
@@ -156,7 +160,13 @@ def hodlr_info(h: int) -> dict:
             "mean_rank_by_depth": list(info.mean_rank_by_depth[1:k + 1]),
             "factor_bytes": info.factor_bytes, "t_build": info.t_build, "t_factor": info.t_factor,
             "t_logdet": info.t_logdet, "t_solve": info.t_solve, "rank_cap_hits": info.rank_cap_hits,
-            "aca_steps": info.aca_steps, "gpu_launches_last": info.gpu_launches_last}
+            "aca_steps": info.aca_steps, "gpu_launches_last": info.gpu_launches_last,
+            "kernel_ms": {f: info.kernel_ms[i] for i, f in enumerate(KERNEL_FAMILIES)},
+            "kernel_calls": {f: info.kernel_calls[i] for i, f in enumerate(KERNEL_FAMILIES)}}
+
+
+def hodlr_launch_count() -> int:
+    return int(load().hodlr_launch_count())
 
 
 def hodlr_free(h: int):

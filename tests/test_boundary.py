@@ -14,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def header_functions():
     src = open(os.path.join(ROOT, "include", "hodlr.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(?:hodlr_status|void|const char\s*\*)\s*(\w+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(?:hodlr_status|void|int64_t|const char\s*\*)\s*(\w+)\s*\(", src)))
 
 
 def test_header_declares_the_north_star_entry_points():
