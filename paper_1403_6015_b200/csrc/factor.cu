@@ -359,8 +359,15 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
     if (!lc.scratch) return hodlr_set_error(HODLR_ENOMEM, "factor: scratch allocation failed");
   }
   ph_begin(h, PH_LEAF);
-  k_leaf_factor<<<grid, LT, need, h->st>>>(lc);
-  HLAUNCH(h, "k_leaf_factor");
+  bool fast = false;
+  {
+    hodlr_status fs = hodlr_leaf_factor_mma(h, K, h->Pipool + dt.piOff[kappa], &fast);
+    if (fs != HODLR_OK) return fs;
+  }
+  if (!fast) {
+    k_leaf_factor<<<grid, LT, need, h->st>>>(lc);
+    HLAUNCH(h, "k_leaf_factor");
+  }
   ph_end(h, PH_LEAF);
   // ---- tree, bottom-up ----
   size_t tree_smem_max = 0;

@@ -159,6 +159,7 @@ extern long long hodlr_global_launches;
 hodlr_status hodlr_sort_and_tree(hodlr_s *h, const double *x);
 hodlr_status hodlr_aca(hodlr_s *h);
 hodlr_status hodlr_factor_impl(hodlr_s *h);
+hodlr_status hodlr_leaf_factor_mma(hodlr_s *h, int K, double *Pi_leaf, bool *used);
 hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_only);
 
 static inline int hodlr_depth_of(long long id) { int d = 0; while (id >= ((2LL << d) - 1)) d++; return d; }

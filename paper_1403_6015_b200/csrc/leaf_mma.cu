@@ -1,0 +1,331 @@
+// leaf_mma.cu -- G4/G5 fast path: per-leaf Cholesky, panel solve and projected Gram on the FP64
+// tensor pipe (mma.sync f64, "DMMA"), one CTA per leaf, everything resident on chip.
+//
+// For a leaf l with rows [lo, lo+m), m <= P (P = 64 or 128), and its ancestor-factor panel
+// E_l = Xh[l rows, K columns] (Fig. 6 lines 7-12):
+//   A_l = K[l,l] + s2 I = L L^T   left-looking over 8-column tiles: C(I,J) = A(I,J) - sum_k L(I,k) L(J,k)^T
+//                                  accumulated in registers (DMMA m8n8k4), 8x8 POTRF + triangular inverse
+//                                  of the diagonal tile by one warp, panel L(I,J) = C(I,J) Linv(J)^T
+//   Z   = L^{-1} E_l              each warp owns <= 2 8-column tiles of Z and sweeps them down the 16 row
+//                                  blocks entirely in registers (Z_b <- Linv(b) Z_b; Z_i -= L(i,b) Z_b),
+//                                  no block-level synchronisation
+//   Pi_l = Z^T Z                  SYRK with DMMA m16n8k8, 16x16 register blocks
+// Layout: L tiles in "fragment order" (element (r, c) of an 8x8 tile at (c>>2)*32 + r*4 + (c&3), so an
+// A/B fragment half is 32 contiguous doubles); Z column-major with leading dimension P + 4 (conflict-free
+// fragment loads).  Rows m..P-1 are padded with the identity (A) and zeros (E).
+#include "hodlr_internal.cuh"
+
+namespace {
+
+constexpr int NTH = 256;   // 8 warps
+constexpr int NW = NTH / 32;
+
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void dmma16(double *c, double a0, double a1, double a2, double a3, double b0, double b1) {
+  asm volatile("mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+               : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+               : "d"(a0), "d"(a1), "d"(a2), "d"(a3), "d"(b0), "d"(b1));
+}
+__device__ __forceinline__ int tix(int I, int J) { return I * (I + 1) / 2 + J; }
+__device__ __forceinline__ int fo(int r, int c) { return (c >> 2) * 32 + r * 4 + (c & 3); }
+// offset of this lane's C/D pair (row lane>>2, cols 2(lane&3), +1) inside a fragment-order tile
+__device__ __forceinline__ int cpos(int lane) { int q = lane & 3; return (q >> 1) * 32 + (lane >> 2) * 4 + 2 * (q & 1); }
+
+// From an 8x8 tile held in C layout (c0, c1 at row lane>>2, cols 2(lane&3)+{0,1}) produce the two B-operand
+// halves (row (lane&3) + 4h, col lane>>2).
+__device__ __forceinline__ void c_to_b(double c0, double c1, int lane, double &b0, double &b1) {
+  const int col = lane >> 2, sel = col & 1;
+  const int s0 = 4 * (lane & 3) + (col >> 1), s1 = s0 + 16;
+  const double x0 = __shfl_sync(0xffffffffu, c0, s0), x1 = __shfl_sync(0xffffffffu, c1, s0);
+  const double y0 = __shfl_sync(0xffffffffu, c0, s1), y1 = __shfl_sync(0xffffffffu, c1, s1);
+  b0 = sel ? x1 : x0;
+  b1 = sel ? y1 : y0;
+}
+
+struct LeafMmaCtx {
+  KParams kp;
+  long long n, ninternal;
+  int kappa, K, Kp, Kz;
+  const double *xs;
+  const long long *lo, *hi;
+  const double *Xh;
+  const int *rank;
+  const DepthTab *dt;
+  double *Lf; long long lstride;
+  double *Pi;
+  double *leaf_ld;
+  int *flags;
+};
+
+// One warp, every lane computes the same 8x8 POTRF redundantly (no shuffles on the critical path),
+// then writes its fragment positions of L and of L^{-1}.
+__device__ void potrf8(double *tile, double *linv, double *diag8, int *bad) {
+  const int lane = threadIdx.x & 31;
+  double a[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; i++)
+#pragma unroll
+    for (int j = 0; j <= i; j++) a[i][j] = tile[fo(i, j)];
+  double inv[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) {
+    double d = a[j][j];
+    if (!(d > 0.0)) { if (lane == 0) *bad = 1; d = 1.0; }
+    // 1/sqrt(d): hardware approximation (rsqrt.approx.f64) + 2 Newton steps (no slow-path call)
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    r = r * fma(-0.5 * d * r, r, 1.5);
+    r = r * fma(-0.5 * d * r, r, 1.5);
+    inv[j] = r;
+    a[j][j] = d * r;
+#pragma unroll
+    for (int i = j + 1; i < 8; i++) a[i][j] *= r;
+#pragma unroll
+    for (int k = j + 1; k < 8; k++)
+#pragma unroll
+      for (int i = k; i < 8; i++) a[i][k] -= a[i][j] * a[k][j];
+  }
+  // every lane holds the same factor: all lanes store every element (same address, same value)
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 8; i++)
+#pragma unroll
+    for (int j = 0; j < 8; j++) tile[fo(i, j)] = j <= i ? a[i][j] : 0.0;
+  if (lane < 8) diag8[lane] = tile[fo(lane, lane)];
+  // L^{-1} column by column (forward substitution)
+#pragma unroll
+  for (int cc = 0; cc < 8; cc++) {
+    double y[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+      if (i < cc) { y[i] = 0.0; continue; }
+      double s = (i == cc) ? 1.0 : 0.0;
+#pragma unroll
+      for (int k = cc; k < i; k++) s -= a[i][k] * y[k];
+      y[i] = s * inv[i];
+    }
+#pragma unroll
+    for (int i = 0; i < 8; i++) linv[fo(i, cc)] = y[i];
+  }
+  __syncwarp();
+}
+
+template <int P>
+__global__ void __launch_bounds__(NTH, 1) k_leaf_factor_mma(LeafMmaCtx c) {
+  constexpr int T = P / 8;
+  constexpr int NTILE = T * (T + 1) / 2;
+  constexpr int LDR = P + 4;
+  extern __shared__ double sm[];
+  __shared__ int bad;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int K = c.K, Kp = c.Kp, Kc = Kp / 8, Kz = c.Kz;   // Kz = columns allocated in sZ (multiple of 16)
+  double *sL = sm;                              // NTILE * 64
+  double *sLi = sL + NTILE * 64;                // T * 64
+  double *sZ = sLi + T * 64;                    // Kz * LDR (column-major)
+  double *sx = sZ + (long long)Kz * LDR;        // P
+  double *sdiag = sx + P;                       // P
+  long long *colsrc = (long long *)(sdiag + P); // Kz
+  const long long leaf = blockIdx.x;
+  const long long id = c.ninternal + leaf, lo = c.lo[id];
+  const int m = (int)(c.hi[id] - lo);
+  if (t == 0) bad = 0;
+  for (int i = t; i < P; i += NTH) sx[i] = i < m ? c.xs[lo + i] : 0.0;
+  if (t == 0) {   // ancestor column map: depth 1..kappa, zero beyond each ancestor block's rank
+    long long a = id;
+    for (int e = c.kappa; e >= 1; e--) {
+      long long b = (a - 1) / 2;
+      int rb = c.rank[b];
+      for (int q = 0; q < c.dt->rdep[e]; q++) colsrc[c.dt->Kdim[e - 1] + q] = q < rb ? c.dt->colbase[e] + q : -1;
+      a = b;
+    }
+    for (int q = K; q < Kz; q++) colsrc[q] = -1;
+  }
+  __syncthreads();
+  // E_l -> sZ (column-major), asynchronous copies overlapped with the assembly and the Cholesky
+  for (int p = t; p < Kz * P; p += NTH) {
+    const int col = p / P, row = p - col * P;
+    const long long src = colsrc[col];
+    double *dst = sZ + col * LDR + row;
+    if (src >= 0 && row < m) {
+      const double *g = c.Xh + src * c.n + lo + row;
+      unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" :: "r"(sa), "l"(g));
+    } else {
+      *dst = 0.0;
+    }
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
+  // assemble A_l = K[l,l] + s2 I into the lower tiles (fragment order), identity padding beyond m
+  for (int ti = warp; ti < NTILE; ti += NW) {
+    int I = 0;
+    while ((I + 1) * (I + 2) / 2 <= ti) I++;
+    const int J = ti - I * (I + 1) / 2;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int r = lane >> 2, cc = (lane & 3) + 4 * h;
+      const int i = 8 * I + r, j = 8 * J + cc;
+      double v;
+      if (i < m && j < m) { v = kval(c.kp, sx[i] - sx[j]); if (i == j) v += c.kp.s2; }
+      else v = (i == j) ? 1.0 : 0.0;
+      sL[ti * 64 + 32 * h + lane] = v;
+    }
+  }
+  __syncthreads();
+  // ---------------- Cholesky, left-looking over tile columns J ----------------
+  const int cp = cpos(lane);
+  for (int J = 0; J < T; J++) {
+    // C(I,J) = A(I,J) - sum_{k<J} L(I,k) L(J,k)^T for I >= J; warp w owns I = J + w, J + w + 8
+    for (int I = J + warp; I < T; I += NW) {
+      double *tc = sL + tix(I, J) * 64;
+      double d0 = tc[cp], d1 = tc[cp + 1], e0 = 0.0, e1 = 0.0;
+      const double *tI = sL + tix(I, 0) * 64, *tJ = sL + tix(J, 0) * 64;
+      int k = 0;
+      for (; k + 1 < J; k += 2) {
+        dmma(d0, d1, -tI[k * 64 + lane], tJ[k * 64 + lane]);
+        dmma(e0, e1, -tI[(k + 1) * 64 + lane], tJ[(k + 1) * 64 + lane]);
+        dmma(d0, d1, -tI[k * 64 + 32 + lane], tJ[k * 64 + 32 + lane]);
+        dmma(e0, e1, -tI[(k + 1) * 64 + 32 + lane], tJ[(k + 1) * 64 + 32 + lane]);
+      }
+      if (k < J) {
+        dmma(d0, d1, -tI[k * 64 + lane], tJ[k * 64 + lane]);
+        dmma(e0, e1, -tI[k * 64 + 32 + lane], tJ[k * 64 + 32 + lane]);
+      }
+      tc[cp] = d0 + e0; tc[cp + 1] = d1 + e1;
+    }
+    __syncthreads();
+    if (warp == 0) potrf8(sL + tix(J, J) * 64, sLi + J * 64, sdiag + 8 * J, &bad);
+    __syncthreads();
+    // panel: L(I,J) = C(I,J) Linv(J)^T for I > J
+    const double *Li = sLi + J * 64;
+    for (int I = J + 1 + warp; I < T; I += NW) {
+      double *tl = sL + tix(I, J) * 64;
+      const double a0 = tl[lane], a1 = tl[32 + lane];
+      double d0 = 0.0, d1 = 0.0;
+      dmma(d0, d1, a0, Li[lane]);
+      dmma(d0, d1, a1, Li[32 + lane]);
+      __syncwarp();
+      tl[cp] = d0; tl[cp + 1] = d1;
+    }
+    __syncthreads();
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  __syncthreads();
+  // ---------------- Z = L^{-1} E, register-resident per warp (tiles cc = warp, warp + 8) ----------------
+  {
+    const int g = lane >> 2, q2 = 2 * (lane & 3);
+    for (int cc = warp; cc < Kc; cc += NW) {
+      double z[T][2];
+#pragma unroll
+      for (int i = 0; i < T; i++) {
+        z[i][0] = sZ[(8 * cc + q2) * LDR + 8 * i + g];
+        z[i][1] = sZ[(8 * cc + q2 + 1) * LDR + 8 * i + g];
+      }
+#pragma unroll
+      for (int b = 0; b < T; b++) {
+        const double *Li = sLi + b * 64;
+        double b0, b1;
+        c_to_b(z[b][0], z[b][1], lane, b0, b1);
+        double d0 = 0.0, d1 = 0.0;
+        dmma(d0, d1, Li[lane], b0);
+        dmma(d0, d1, Li[32 + lane], b1);
+        z[b][0] = d0; z[b][1] = d1;
+        c_to_b(d0, d1, lane, b0, b1);
+#pragma unroll
+        for (int i = b + 1; i < T; i++) {
+          const double *tA = sL + tix(i, b) * 64;
+          dmma(z[i][0], z[i][1], -tA[lane], b0);
+          dmma(z[i][0], z[i][1], -tA[32 + lane], b1);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < T; i++) {
+        sZ[(8 * cc + q2) * LDR + 8 * i + g] = z[i][0];
+        sZ[(8 * cc + q2 + 1) * LDR + 8 * i + g] = z[i][1];
+      }
+    }
+  }
+  __syncthreads();
+  // ---------------- outputs: log det partial, packed L for the solve ----------------
+  if (warp == 0) {          // 2 sum log L_ii: per-lane partials, then a fixed-order warp reduction
+    double s = 0.0;
+    for (int i = lane; i < m; i += 32) s += log(sdiag[i]);
+    s = warp_sum(s);
+    if (lane == 0) {
+      c.leaf_ld[leaf] = 2.0 * s;
+      if (bad) { atomicAdd(&c.flags[1], 1); atomicMin(&c.flags[2], (int)id); }
+    }
+  }
+  double *Lg = c.Lf + leaf * c.lstride;
+  for (int i = warp; i < m; i += NW) {
+    const int base = i * (i + 1) / 2;
+    for (int j = lane; j <= i; j += 32) Lg[base + j] = sL[tix(i >> 3, j >> 3) * 64 + fo(i & 7, j & 7)];
+  }
+  if (K == 0) return;
+  // ---------------- Pi_l = Z^T Z: 16x16 output blocks, DMMA m16n8k8 ----------------
+  const int Kc16 = Kz / 16;
+  const int nblk = Kc16 * (Kc16 + 1) / 2;
+  double *Pl = c.Pi + leaf * (long long)K * K;
+  const int kend = (m + 7) & ~7;
+  const int g = lane >> 2, tq = lane & 3;
+  for (int blk = warp; blk < nblk; blk += NW) {
+    int BI = 0;
+    while ((BI + 1) * (BI + 2) / 2 <= blk) BI++;
+    const int BJ = blk - BI * (BI + 1) / 2;
+    double acc0[4] = {0, 0, 0, 0}, acc1[4] = {0, 0, 0, 0};
+    const double *pa0 = sZ + (16 * BI + g) * LDR + tq;
+    const double *pa1 = pa0 + 8 * LDR;
+    const double *pb0 = sZ + (16 * BJ + g) * LDR + tq;
+    const double *pb1 = pb0 + 8 * LDR;
+    for (int k0 = 0; k0 < kend; k0 += 8) {
+      const double a0 = pa0[k0], a1 = pa1[k0], a2 = pa0[k0 + 4], a3 = pa1[k0 + 4];
+      dmma16(acc0, a0, a1, a2, a3, pb0[k0], pb0[k0 + 4]);
+      dmma16(acc1, a0, a1, a2, a3, pb1[k0], pb1[k0 + 4]);
+    }
+    // acc0: rows 16BI + g (+8), cols 16BJ + 2tq (+1); acc1: same rows, cols + 8
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const double v = q < 4 ? acc0[q] : acc1[q - 4];
+      const int row = 16 * BI + g + ((q & 2) ? 8 : 0);
+      const int col = 16 * BJ + 2 * tq + (q & 1) + (q >= 4 ? 8 : 0);
+      if (row < K && col < K && row >= col) {
+        Pl[(long long)row * K + col] = v;
+        Pl[(long long)col * K + row] = v;
+      }
+    }
+  }
+}
+
+}  // namespace
+
+// Runs the fast path if it applies (leaf <= 128 and the panel fits in shared memory); *used reports it.
+hodlr_status hodlr_leaf_factor_mma(hodlr_s *h, int K, double *Pi_leaf, bool *used) {
+  *used = false;
+  const int mmax = h->leaf_max;
+  const int P = mmax <= 64 ? 64 : (mmax <= 128 ? 128 : 0);
+  if (P == 0) return HODLR_OK;
+  const int Kp = (K + 7) / 8 * 8;
+  if (Kp / 8 > 16) return HODLR_OK;                  // register sweep covers <= 2 tiles per warp
+  const int Kz = (K + 15) / 16 * 16;
+  const int T = P / 8, NTILE = T * (T + 1) / 2, LDR = P + 4;
+  const size_t smem = sizeof(double) * ((size_t)NTILE * 64 + T * 64 + (size_t)Kz * LDR + 2 * P + Kz);
+  int maxsm = 0;
+  HCUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
+  if (smem + 64 > (size_t)maxsm) return HODLR_OK;
+  LeafMmaCtx c;
+  c.kp = h->kp; c.n = h->n; c.ninternal = h->ninternal; c.kappa = h->kappa; c.K = K; c.Kp = Kp; c.Kz = Kz;
+  c.xs = h->xs; c.lo = h->lo; c.hi = h->hi; c.Xh = h->Xh; c.rank = h->rank; c.dt = h->d_dt;
+  c.Lf = h->Lf; c.lstride = h->lstride; c.Pi = Pi_leaf; c.leaf_ld = h->leaf_ld; c.flags = h->dflags;
+  if (P == 64) {
+    HCUDA(cudaFuncSetAttribute(k_leaf_factor_mma<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_leaf_factor_mma<64><<<(int)h->nleaves, NTH, smem, h->st>>>(c);
+  } else {
+    HCUDA(cudaFuncSetAttribute(k_leaf_factor_mma<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_leaf_factor_mma<128><<<(int)h->nleaves, NTH, smem, h->st>>>(c);
+  }
+  HLAUNCH(h, "k_leaf_factor_mma");
+  *used = true;
+  return HODLR_OK;
+}
