@@ -7,34 +7,40 @@
 // B200 form (same factorization, never materialises the processed panel):
 // for every node a define Pi_a = E_a^T K_aa^{-1} E_a where E_a = the original ACA left factors of
 // all ancestors of a (and a itself) restricted to the rows of a.
-//   leaf:  Pi_l = Z^T Z,  Z = L^{-1} E_l,  A_l = L L^T              (k_leaf_factor)
+//   leaf:  Pi_l = Z^T Z,  Z = L^{-1} E_l,  A_l = L L^T     (leaf_mma.cu fast path, k_leaf_factor fallback)
 //   node c at depth d with children c1, c2, s = depth-(d+1) columns, a = columns of depths <= d:
 //     S_c = [[I, Pi_c2[s,s]], [Pi_c1[s,s], I]],  B_c = [Pi_c2[s,a]; Pi_c1[s,a]],  T_c = S_c^{-1} B_c
 //     Pi_c = Pi_c1[a,a] + Pi_c2[a,a] - B_c[r:]^T T_c[:r] - B_c[:r]^T T_c[r:]   (k_tree_factor)
 // because E^T K_cc^{-1} E = E^T D^{-1} E - E^T D^{-1} L S^{-1} R D^{-1} E with D = diag(K_c1, K_c2),
 // L = blockdiag(U, V), R = [[0, V^T], [U^T, 0]] (SMW).  log det C = sum_l 2 sum log L_ii +
 // sum_c log det S_c (Sylvester + multiplicativity).
+// The Schur updates cancel heavily (the top-level S_c reach cond ~1e11), so T_c is kept as a
+// double-double pair and Pi_c is accumulated with compensated arithmetic.
 #include "hodlr_internal.cuh"
 #include <limits.h>
 
 namespace {
 
-constexpr int LT = 256;      // threads per leaf CTA
+constexpr int LT = 256;      // threads per leaf CTA (fallback kernel)
 constexpr int TT = 256;      // threads per tree CTA
 
 __device__ __forceinline__ long long P(long long i, long long j) { return i * (i + 1) / 2 + j; }
 
+// ---------------------------------------------------------------------------------------------
+// Fallback leaf kernel (any leaf size; scalar FP64): Cholesky, Z = L^{-1} E, Pi = Z^T Z.
+// Outputs in the shared storage formats (L tiles + Linv tiles, packed Pi).
+// ---------------------------------------------------------------------------------------------
 struct LeafCtx {
   KParams kp;
   long long n, ninternal, nleaves;
-  int kappa, K, ldz;
+  int kappa, K, ldz, T;
   const double *xs;
   const long long *lo, *hi;
   const double *Xh;
   const int *rank;
   const DepthTab *dt;
   double *Lf; long long lstride;
-  double *Pi;               // leaf Pi storage, K x K per leaf
+  double *Pi;               // leaf Pi storage, packed K(K+1)/2 per leaf
   double *leaf_ld;
   int *flags;
   double *scratch;          // per-CTA fallback storage when shared memory is too small
@@ -59,7 +65,6 @@ __global__ void __launch_bounds__(LT) k_leaf_factor(LeafCtx c) {
     for (long long i = t; i < m; i += LT) xl[i] = c.xs[lo + i];
     if (t == 0) bad = 0;
     __syncthreads();
-    // assemble A_l = K[l,l] + s2 I (lower triangle)
     const long long np = m * (m + 1) / 2;
     for (long long p = t; p < np; p += LT) {
       long long i = (long long)((sqrt(8.0 * (double)p + 1.0) - 1.0) * 0.5);
@@ -71,8 +76,7 @@ __global__ void __launch_bounds__(LT) k_leaf_factor(LeafCtx c) {
       L[p] = v;
     }
     __syncthreads();
-    // right-looking Cholesky A = L L^T
-    for (long long j = 0; j < m; j++) {
+    for (long long j = 0; j < m; j++) {        // right-looking Cholesky A = L L^T
       if (t == 0) {
         double d = L[P(j, j)];
         if (!(d > 0.0)) { bad = 1; d = 1.0; }
@@ -94,11 +98,39 @@ __global__ void __launch_bounds__(LT) k_leaf_factor(LeafCtx c) {
       c.leaf_ld[leaf] = 2.0 * s;
       if (bad) { atomicAdd(&c.flags[1], 1); atomicMin(&c.flags[2], (int)id); }
     }
+    // L as fragment-order tiles (identity padding) and the inverse diagonal tiles
+    const int T = c.T, NT = T * (T + 1) / 2;
     double *Lg = c.Lf + leaf * c.lstride;
-    for (long long p = t; p < np; p += LT) Lg[p] = L[p];
+    for (long long p = t; p < (long long)NT * 64; p += LT) {
+      const int ti = (int)(p >> 6), e = (int)(p & 63);
+      int I = 0;
+      while ((I + 1) * (I + 2) / 2 <= ti) I++;
+      const int J = ti - I * (I + 1) / 2;
+      const int cc = (e >> 5) * 4 + (e & 3), r = (e & 31) >> 2;
+      const long long i = 8 * I + r, j = 8 * J + cc;
+      Lg[p] = (i < m && j <= i) ? L[P(i, j)] : (i == j ? 1.0 : 0.0);
+    }
+    for (int b = t; b < T; b += LT) {          // Linv(b): forward substitution on the 8x8 diagonal tile
+      double l[8][8];
+      for (int i = 0; i < 8; i++)
+        for (int j = 0; j <= i; j++) {
+          const long long gi = 8 * b + i, gj = 8 * b + j;
+          l[i][j] = gi < m ? L[P(gi, gj)] : (i == j ? 1.0 : 0.0);
+        }
+      double *li = Lg + (long long)(NT + b) * 64;
+      for (int cc = 0; cc < 8; cc++) {
+        double y[8];
+        for (int i = 0; i < 8; i++) {
+          if (i < cc) { y[i] = 0.0; continue; }
+          double s = (i == cc) ? 1.0 : 0.0;
+          for (int k = cc; k < i; k++) s -= l[i][k] * y[k];
+          y[i] = s / l[i][i];
+        }
+        for (int i = 0; i < 8; i++) li[fo(i, cc)] = y[i];
+      }
+    }
     if (K > 0) {
-      // column map: leaf column order = depth 1 .. kappa; zero beyond each ancestor block's rank
-      if (t == 0) {
+      if (t == 0) {   // column map: leaf column order = depth 1 .. kappa; zero beyond each block's rank
         long long a = id;
         for (int e = c.kappa; e >= 1; e--) {
           long long b = (a - 1) / 2;
@@ -115,8 +147,7 @@ __global__ void __launch_bounds__(LT) k_leaf_factor(LeafCtx c) {
         Z[i * ldz + col] = src >= 0 ? c.Xh[src * c.n + lo + i] : 0.0;
       }
       __syncthreads();
-      // Z <- L^{-1} Z  (forward substitution, one column per thread)
-      for (int col = t; col < K; col += LT) {
+      for (int col = t; col < K; col += LT) {     // Z <- L^{-1} Z
         for (long long i = 0; i < m; i++) {
           double s = Z[i * ldz + col];
           const double *Li = L + P(i, 0);
@@ -125,8 +156,7 @@ __global__ void __launch_bounds__(LT) k_leaf_factor(LeafCtx c) {
         }
       }
       __syncthreads();
-      // Pi_l = Z^T Z  (symmetric; both triangles written)
-      double *Pl = c.Pi + leaf * (long long)K * K;
+      double *Pl = c.Pi + leaf * ((long long)K * (K + 1) / 2);   // Pi_l = Z^T Z, packed lower
       const long long npk = (long long)K * (K + 1) / 2;
       for (long long p = t; p < npk; p += LT) {
         long long a = (long long)((sqrt(8.0 * (double)p + 1.0) - 1.0) * 0.5);
@@ -135,8 +165,7 @@ __global__ void __launch_bounds__(LT) k_leaf_factor(LeafCtx c) {
         long long b = p - a * (a + 1) / 2;
         double s = 0.0;
         for (long long i = 0; i < m; i++) s += Z[i * ldz + a] * Z[i * ldz + b];
-        Pl[a * K + b] = s;
-        Pl[b * K + a] = s;
+        Pl[p] = s;
       }
     }
     __syncthreads();
@@ -146,8 +175,8 @@ __global__ void __launch_bounds__(LT) k_leaf_factor(LeafCtx c) {
 struct TreeCtx {
   int d;                    // depth of the nodes of this launch
   int r, q, Kd, K1;
-  const double *Pi1;        // children Pi base (depth d+1)
-  double *Pic;              // this depth's Pi base
+  const double *Pi1;        // children Pi base (depth d+1), packed K1(K1+1)/2 per node
+  double *Pic;              // this depth's Pi base, packed Kd(Kd+1)/2 per node
   double *Sst;              // per node: S (q*q), LU(S) (q*q), pivots (q)
   double *BT;               // per node: B, T_hi, T_lo (q*Kd each)
   double *node_ld;
@@ -171,9 +200,10 @@ __global__ void __launch_bounds__(TT) k_tree_factor(TreeCtx c) {
   const int t = threadIdx.x;
   const long long i = blockIdx.x;
   const long long node = (1LL << c.d) - 1 + i;
-  const int r = c.r, q = c.q, Kd = c.Kd, K1 = c.K1;
-  const double *P1 = c.Pi1 + (2 * i) * (long long)K1 * K1;
-  const double *P2 = c.Pi1 + (2 * i + 1) * (long long)K1 * K1;
+  const int r = c.r, q = c.q, Kd = c.Kd;
+  const long long K1 = c.K1;
+  const double *P1 = c.Pi1 + (2 * i) * (K1 * (K1 + 1) / 2);
+  const double *P2 = c.Pi1 + (2 * i + 1) * (K1 * (K1 + 1) / 2);
   const long long qK = (long long)q * Kd;
   double *S0 = sm;                   // q x q original
   double *S = S0 + q * q;            // q x q LU
@@ -184,24 +214,28 @@ __global__ void __launch_bounds__(TT) k_tree_factor(TreeCtx c) {
   for (int p = t; p < q * q; p += TT) {
     int a = p / q, b = p - a * q;
     double v = a == b ? 1.0 : 0.0;
-    if (a < r && b >= r) v = P2[(long long)(Kd + a) * K1 + Kd + (b - r)];
-    if (a >= r && b < r) v = P1[(long long)(Kd + a - r) * K1 + Kd + b];
+    if (a < r && b >= r) v = P2[pk(Kd + a, Kd + (b - r))];
+    if (a >= r && b < r) v = P1[pk(Kd + a - r, Kd + b)];
     S0[p] = v; S[p] = v;
   }
   for (long long p = t; p < qK; p += TT) {
     long long a = p / Kd, b = p - a * Kd;
-    double v = a < r ? P2[(long long)(Kd + a) * K1 + b] : P1[(long long)(Kd + a - r) * K1 + b];
+    double v = a < r ? P2[P(Kd + a, b)] : P1[P(Kd + a - r, b)];
     B[p] = v; Th[p] = v; Tl[p] = 0.0;
   }
   if (t == 0) zero_piv = 0;
   __syncthreads();
   // LU with partial pivoting (row of max |.|, first index on ties)
   for (int k = 0; k < q; k++) {
-    if (t == 0) {
-      int p = k; double best = fabs(S[k * q + k]);
-      for (int a = k + 1; a < q; a++) if (fabs(S[a * q + k]) > best) { best = fabs(S[a * q + k]); p = a; }
-      pivs[k] = p;
-      if (best == 0.0) zero_piv = 1;
+    if (t < 32) {
+      int p = k; double best = -1.0;
+      for (int a = k + t; a < q; a += 32) { double v = fabs(S[a * q + k]); if (v > best) { best = v; p = a; } }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        double b2 = __shfl_down_sync(0xffffffffu, best, o); int p2 = __shfl_down_sync(0xffffffffu, p, o);
+        if (b2 > best || (b2 == best && p2 < p)) { best = b2; p = p2; }
+      }
+      if (t == 0) { pivs[k] = p; if (!(best > 0.0)) zero_piv = 1; }
     }
     __syncthreads();
     const int p = pivs[k];
@@ -209,11 +243,13 @@ __global__ void __launch_bounds__(TT) k_tree_factor(TreeCtx c) {
     __syncthreads();
     const double ukk = S[k * q + k];
     if (ukk != 0.0) {
-      for (int a = k + 1 + t; a < q; a += TT) {
-        double l = S[a * q + k] / ukk;
-        S[a * q + k] = l;
-        for (int j = k + 1; j < q; j++) S[a * q + j] -= l * S[k * q + j];
+      const int rows = q - 1 - k, cols = q - 1 - k;   // trailing block a > k, j > k
+      for (int e = t; e < rows * cols; e += TT) {
+        const int a = k + 1 + e / cols, j = k + 1 + e % cols;
+        S[a * q + j] -= (S[a * q + k] / ukk) * S[k * q + j];
       }
+      __syncthreads();
+      for (int a = k + 1 + t; a < q; a += TT) S[a * q + k] /= ukk;
     }
     __syncthreads();
   }
@@ -228,36 +264,38 @@ __global__ void __launch_bounds__(TT) k_tree_factor(TreeCtx c) {
     c.node_ld[node] = la;
     if (zero_piv || sg <= 0) { atomicAdd(&c.flags[1], 1); atomicMin(&c.flags[2], (int)node); }
   }
-  if (!zero_piv) {
-    for (int col = t; col < Kd; col += TT) {
-      lu_solve_col(S, pivs, q, Th + col, Kd);
-      for (int it = 0; it < 2; it++) {        // iterative refinement, residual in double-double
-        for (int a = 0; a < q; a++) {
-          Acc2 A = acc2(B[a * Kd + col]);
-          for (int k = 0; k < q; k++) acc_fma_dd(A, -S0[a * q + k], Th[k * Kd + col], Tl[k * Kd + col]);
-          R[a * Kd + col] = acc_val(A);
-        }
+  if (!zero_piv && Kd > 0) {
+    for (int col = t; col < Kd; col += TT) lu_solve_col(S, pivs, q, Th + col, Kd);
+    __syncthreads();
+    for (int it = 0; it < 2; it++) {          // iterative refinement, residual in double-double
+      for (long long e = t; e < qK; e += TT) {
+        const int a = (int)(e / Kd), col = (int)(e - (long long)a * Kd);
+        Acc2 A = acc2(B[e]);
+        for (int k = 0; k < q; k++) acc_fma_dd(A, -S0[a * q + k], Th[k * Kd + col], Tl[k * Kd + col]);
+        R[e] = acc_val(A);
+      }
+      __syncthreads();
+      for (int col = t; col < Kd; col += TT) {
         lu_solve_col(S, pivs, q, R + col, Kd);
         for (int a = 0; a < q; a++) Tl[a * Kd + col] += R[a * Kd + col];
       }
+      __syncthreads();
     }
   }
   __syncthreads();
-  // Pi_c = Pi_c1[a,a] + Pi_c2[a,a] - B[r:]^T T[:r] - B[:r]^T T[r:]  (lower triangle, mirrored)
-  double *Pc = c.Pic + i * (long long)Kd * Kd;
+  // Pi_c = Pi_c1[a,a] + Pi_c2[a,a] - B[r:]^T T[:r] - B[:r]^T T[r:]  (packed lower triangle)
+  double *Pc = c.Pic + i * ((long long)Kd * (Kd + 1) / 2);
   const long long npk = (long long)Kd * (Kd + 1) / 2;
   for (long long p = t; p < npk; p += TT) {
     long long a = (long long)((sqrt(8.0 * (double)p + 1.0) - 1.0) * 0.5);
     while (a * (a + 1) / 2 > p) a--;
     while ((a + 1) * (a + 2) / 2 <= p) a++;
     long long b = p - a * (a + 1) / 2;
-    Acc2 A = acc2(P1[a * K1 + b]);
-    acc_add(A, P2[a * K1 + b]);
+    Acc2 A = acc2(P1[p]);                     // packed index of (a, b) is p in both children too
+    acc_add(A, P2[p]);
     for (int u = 0; u < r; u++) acc_fma_dd(A, -B[(long long)(r + u) * Kd + a], Th[(long long)u * Kd + b], Tl[(long long)u * Kd + b]);
     for (int u = 0; u < r; u++) acc_fma_dd(A, -B[(long long)u * Kd + a], Th[(long long)(r + u) * Kd + b], Tl[(long long)(r + u) * Kd + b]);
-    const double v = acc_val(A);
-    Pc[a * Kd + b] = v;
-    Pc[b * Kd + a] = v;
+    Pc[p] = acc_val(A);
   }
   // persist S, LU(S) (+ pivots as doubles), B, T_hi, T_lo for the solve
   double *Sg = c.Sst + i * (long long)(2 * q * q + q);
@@ -313,7 +351,9 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
   const long long nl = h->nleaves;
   // ---- storage ----
   const int mmax = h->leaf_max;
-  h->lstride = (long long)mmax * (mmax + 1) / 2;
+  const int Pfast = mmax <= 64 ? 64 : (mmax <= 128 ? 128 : 0);
+  h->ltiles = Pfast ? Pfast / 8 : (mmax + 7) / 8;
+  h->lstride = (long long)(h->ltiles * (h->ltiles + 1) / 2 + h->ltiles) * 64;
   h->Lf = (double *)hodlr_dalloc(h, sizeof(double) * h->lstride * nl);
   h->leaf_ld = (double *)hodlr_dalloc(h, sizeof(double) * nl);
   h->node_ld = (double *)hodlr_dalloc(h, sizeof(double) * (h->ninternal > 0 ? h->ninternal : 1));
@@ -321,7 +361,7 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
   long long piTot = 0, sTot = 0, btTot = 0;
   for (int e = kappa; e >= 0; e--) {
     dt.piOff[e] = piTot;
-    piTot += (1LL << e) * (long long)dt.Kdim[e] * dt.Kdim[e];
+    piTot += (1LL << e) * ((long long)dt.Kdim[e] * (dt.Kdim[e] + 1) / 2);
   }
   for (int d = 0; d < kappa; d++) {
     long long q = 2LL * dt.rdep[d + 1];
@@ -334,42 +374,43 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
   if (!h->Lf || !h->leaf_ld || !h->node_ld || !h->d_logdet || !h->Pipool || !h->Spool || !h->BTpool)
     return hodlr_set_error(HODLR_ENOMEM, "factor: device allocation failed");
   HCUDA(cudaMemcpyAsync(h->d_dt, &dt, sizeof(DepthTab), cudaMemcpyHostToDevice, h->st));
-  // ---- leaves ----
-  LeafCtx lc;
-  lc.kp = h->kp; lc.n = h->n; lc.ninternal = h->ninternal; lc.nleaves = nl; lc.kappa = kappa; lc.K = K;
-  lc.ldz = K | 1; lc.xs = h->xs; lc.lo = h->lo; lc.hi = h->hi; lc.Xh = h->Xh; lc.rank = h->rank;
-  lc.dt = h->d_dt; lc.Lf = h->Lf; lc.lstride = h->lstride; lc.Pi = h->Pipool + dt.piOff[kappa];
-  lc.leaf_ld = h->leaf_ld; lc.flags = h->dflags;
   if (K > 1024) return hodlr_set_error(HODLR_EINVAL, "factor: K = %d ancestor columns exceeds 1024", K);
-  lc.mmax = mmax;
-  lc.lsz = (long long)mmax * (mmax + 1) / 2 + 1;
-  size_t need = sizeof(double) * (mmax + lc.lsz + (size_t)mmax * lc.ldz);
   int maxsm = 0;
   HCUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
-  int grid = (int)nl;
-  lc.scratch = nullptr; lc.scratch_per_cta = 0;
-  if (need <= (size_t)maxsm - 12 * 1024) {
-    lc.use_smem = 1;
-    HCUDA(cudaFuncSetAttribute(k_leaf_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
-  } else {
-    lc.use_smem = 0; need = 0;
-    grid = (int)(nl < 148 * 4 ? nl : 148 * 4);
-    lc.scratch_per_cta = mmax + lc.lsz + (long long)mmax * lc.ldz;
-    lc.scratch = (double *)hodlr_dalloc(h, sizeof(double) * lc.scratch_per_cta * grid);
-    if (!lc.scratch) return hodlr_set_error(HODLR_ENOMEM, "factor: scratch allocation failed");
-  }
+  // ---- leaves ----
   ph_begin(h, PH_LEAF);
   bool fast = false;
-  {
+  if (Pfast) {
     hodlr_status fs = hodlr_leaf_factor_mma(h, K, h->Pipool + dt.piOff[kappa], &fast);
     if (fs != HODLR_OK) return fs;
   }
   if (!fast) {
+    LeafCtx lc;
+    lc.kp = h->kp; lc.n = h->n; lc.ninternal = h->ninternal; lc.nleaves = nl; lc.kappa = kappa; lc.K = K;
+    lc.ldz = K | 1; lc.T = h->ltiles; lc.xs = h->xs; lc.lo = h->lo; lc.hi = h->hi; lc.Xh = h->Xh; lc.rank = h->rank;
+    lc.dt = h->d_dt; lc.Lf = h->Lf; lc.lstride = h->lstride; lc.Pi = h->Pipool + dt.piOff[kappa];
+    lc.leaf_ld = h->leaf_ld; lc.flags = h->dflags;
+    lc.mmax = mmax;
+    lc.lsz = (long long)mmax * (mmax + 1) / 2 + 1;
+    size_t need = sizeof(double) * (mmax + lc.lsz + (size_t)mmax * lc.ldz);
+    int grid = (int)nl;
+    lc.scratch = nullptr; lc.scratch_per_cta = 0;
+    if (need <= (size_t)maxsm - 12 * 1024) {
+      lc.use_smem = 1;
+      HCUDA(cudaFuncSetAttribute(k_leaf_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
+    } else {
+      lc.use_smem = 0; need = 0;
+      grid = (int)(nl < 148 * 4 ? nl : 148 * 4);
+      lc.scratch_per_cta = mmax + lc.lsz + (long long)mmax * lc.ldz;
+      lc.scratch = (double *)hodlr_dalloc(h, sizeof(double) * lc.scratch_per_cta * grid);
+      if (!lc.scratch) return hodlr_set_error(HODLR_ENOMEM, "factor: scratch allocation failed");
+    }
     k_leaf_factor<<<grid, LT, need, h->st>>>(lc);
     HLAUNCH(h, "k_leaf_factor");
   }
   ph_end(h, PH_LEAF);
   // ---- tree, bottom-up ----
+  ph_begin(h, PH_TREE);
   size_t tree_smem_max = 0;
   for (int d = 0; d < kappa; d++) {
     size_t q = 2 * (size_t)dt.rdep[d + 1];
@@ -379,7 +420,6 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
     return hodlr_set_error(HODLR_EINVAL, "factor: coupling system too large for shared memory");
   if (kappa > 0)
     HCUDA(cudaFuncSetAttribute(k_tree_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tree_smem_max));
-  ph_begin(h, PH_TREE);
   for (int d = kappa - 1; d >= 0; d--) {
     TreeCtx tc;
     tc.d = d; tc.r = dt.rdep[d + 1]; tc.q = 2 * tc.r; tc.Kd = dt.Kdim[d]; tc.K1 = dt.Kdim[d + 1];

@@ -129,7 +129,7 @@ struct hodlr_s {
   int *dflags;               // [0] nonfinite x, [1] notpd, [2] notpd node+1 (min), [3] nonfinite y, [4] active
   DepthTab *d_dt;
   // factor storage
-  double *Lf; long long lstride;
+  double *Lf; long long lstride; int ltiles;   // leaf factor tiles (see storage helpers)
   double *Spool;  int *Piv;  double *BTpool; double *Pipool;
   double *leaf_ld, *node_ld, *d_logdet;
   double logdet;
@@ -197,6 +197,17 @@ __device__ __forceinline__ void acc_fma_dd(Acc2 &A, double a, double bh, double 
 }
 __device__ __forceinline__ double acc_val(const Acc2 &A) { return A.s + A.c; }
 __device__ __forceinline__ void acc_dd(const Acc2 &A, double &hi, double &lo) { two_sum(A.s, A.c, hi, lo); }
+
+// ----------------------------------------------------------------------------------------------
+// Storage helpers shared by the factor and solve kernels.
+//   Leaf factors: per leaf, T = ceil(leaf_max / 8) tile rows; lower 8x8 tiles of L in "fragment order"
+//   (tile (I,J), I >= J, at tix(I,J)*64; element (r,c) at fo(r,c)), followed by the T inverse diagonal
+//   tiles Linv(b) at (NTILE + b)*64.  Padding rows beyond the leaf size are identity.
+//   Pi: packed lower triangle, row-major: (a, b), a >= b, at a(a+1)/2 + b.
+// ----------------------------------------------------------------------------------------------
+__device__ __forceinline__ int tix(int I, int J) { return I * (I + 1) / 2 + J; }
+__device__ __forceinline__ int fo(int r, int c) { return (c >> 2) * 32 + r * 4 + (c & 3); }
+__device__ __forceinline__ long long pk(long long a, long long b) { return a >= b ? a * (a + 1) / 2 + b : b * (b + 1) / 2 + a; }
 
 // argmax with ties -> smallest index; (abs, idx) with idx < 0 meaning "no candidate"
 __device__ __forceinline__ bool amax_better(double a1, long long i1, double a2, long long i2) {

@@ -29,8 +29,6 @@ __device__ __forceinline__ void dmma16(double *c, double a0, double a1, double a
                : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
                : "d"(a0), "d"(a1), "d"(a2), "d"(a3), "d"(b0), "d"(b1));
 }
-__device__ __forceinline__ int tix(int I, int J) { return I * (I + 1) / 2 + J; }
-__device__ __forceinline__ int fo(int r, int c) { return (c >> 2) * 32 + r * 4 + (c & 3); }
 // offset of this lane's C/D pair (row lane>>2, cols 2(lane&3), +1) inside a fragment-order tile
 __device__ __forceinline__ int cpos(int lane) { int q = lane & 3; return (q >> 1) * 32 + (lane >> 2) * 4 + 2 * (q & 1); }
 
@@ -258,16 +256,13 @@ __global__ void __launch_bounds__(NTH, 1) k_leaf_factor_mma(LeafMmaCtx c) {
       if (bad) { atomicAdd(&c.flags[1], 1); atomicMin(&c.flags[2], (int)id); }
     }
   }
-  double *Lg = c.Lf + leaf * c.lstride;
-  for (int i = warp; i < m; i += NW) {
-    const int base = i * (i + 1) / 2;
-    for (int j = lane; j <= i; j += 32) Lg[base + j] = sL[tix(i >> 3, j >> 3) * 64 + fo(i & 7, j & 7)];
-  }
+  double *Lg = c.Lf + leaf * c.lstride;            // L tiles then Linv tiles (contiguous in shared memory)
+  for (int p = t; p < (NTILE + T) * 64; p += NTH) Lg[p] = sL[p];
   if (K == 0) return;
   // ---------------- Pi_l = Z^T Z: 16x16 output blocks, DMMA m16n8k8 ----------------
   const int Kc16 = Kz / 16;
   const int nblk = Kc16 * (Kc16 + 1) / 2;
-  double *Pl = c.Pi + leaf * (long long)K * K;
+  double *Pl = c.Pi + leaf * ((long long)K * (K + 1) / 2);
   const int kend = (m + 7) & ~7;
   const int g = lane >> 2, tq = lane & 3;
   for (int blk = warp; blk < nblk; blk += NW) {
@@ -290,10 +285,7 @@ __global__ void __launch_bounds__(NTH, 1) k_leaf_factor_mma(LeafMmaCtx c) {
       const double v = q < 4 ? acc0[q] : acc1[q - 4];
       const int row = 16 * BI + g + ((q & 2) ? 8 : 0);
       const int col = 16 * BJ + 2 * tq + (q & 1) + (q >= 4 ? 8 : 0);
-      if (row < K && col < K && row >= col) {
-        Pl[(long long)row * K + col] = v;
-        Pl[(long long)col * K + row] = v;
-      }
+      if (row < K && col < K && row >= col) Pl[(long long)row * (row + 1) / 2 + col] = v;
     }
   }
 }

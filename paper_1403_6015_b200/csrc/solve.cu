@@ -7,17 +7,19 @@
 //   down (node c)  f = t_c + T_c w_c;  w_c1 = [w_c, -f[:r]],  w_c2 = [w_c, -f[r:]]   (k_tree_down)
 //   down (leaves)  x_l = A_l^{-1} (b_l + E_l w_l)                                   (k_leaf_down)
 // h_root = y^T C^{-1} y gives the log-likelihood without the down pass (eq. 1).
+// Leaf triangular solves are blocked over 8-row tiles with the stored inverse diagonal tiles; one warp
+// per leaf, one warp per tree node (t_c by a double solve + 2 compensated refinement steps).
 #include "hodlr_internal.cuh"
 
 namespace {
 
-constexpr int ST = 256;
-
-__device__ __forceinline__ long long P(long long i, long long j) { return i * (i + 1) / 2 + j; }
+constexpr int ST = 256;          // threads per CTA (8 warps)
+constexpr int NWS = ST / 32;
+constexpr int RPL = 8;           // rows per lane: leaves up to 256 rows
 
 struct SolveCtx {
   long long n, ninternal, nleaves;
-  int kappa, K;
+  int kappa, K, T;
   const long long *lo, *hi, *perm;
   const double *Xh;
   const int *rank;
@@ -25,106 +27,236 @@ struct SolveCtx {
   const double *Lf; long long lstride;
   const double *Spool, *BTpool;
   double *V;        // per-level node vectors (g on the way up, w on the way down)
-  double *Tv;       // per-node t (q doubles, depth-d offset nodeT[d])
+  double *Tv;       // per-node t_c (q hi, q lo doubles; depth-d offset nodeT[d])
   double *hv;       // per-node h = y_c^T K_cc^{-1} y_c as a double-double pair (heap id)
   const double *y;
   double *x;
   int *flags;
-  int mmax;
 };
 
-// warp 0: solve L L^T w = b in place (packed lower row-major L in shared memory)
-__device__ void chol_solve_warp(const double *L, double *b, long long m) {
-  const int lane = threadIdx.x & 31;
-  for (long long i = 0; i < m; i++) {
-    double s = 0.0;
-    for (long long j = lane; j < i; j += 32) s += L[P(i, j)] * b[j];
-    s = warp_sum(s);
-    if (lane == 0) b[i] = (b[i] - s) / L[P(i, i)];
-    __syncwarp();
-  }
-  for (long long i = m - 1; i >= 0; i--) {
-    double s = 0.0;
-    for (long long k = i + 1 + lane; k < m; k += 32) s += L[P(k, i)] * b[k];
-    s = warp_sum(s);
-    if (lane == 0) b[i] = (b[i] - s) / L[P(i, i)];
-    __syncwarp();
+// Rows of the leaf owned by this lane: i = lane + 32 s.  v[s] holds the working vector.
+// Forward: v <- L^{-1} v with L in fragment-order tiles (Lg) and the inverse diagonal tiles (Li).
+__device__ __forceinline__ void tile_fwd(const double *Lg, const double *Li, int T, double v[RPL], int lane) {
+  for (int b = 0; b < T; b++) {
+    const int rb = 8 * b;
+    double vb[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const int row = rb + k, s = row >> 5;
+      double val = 0.0;
+#pragma unroll
+      for (int ss = 0; ss < RPL; ss++) if (ss == s) val = v[ss];
+      vb[k] = __shfl_sync(0xffffffffu, val, row & 31);
+    }
+    double z[8];                       // z_b = Linv(b) v_b
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k <= r; k++) acc += Li[b * 64 + fo(r, k)] * vb[k];
+      z[r] = acc;
+    }
+#pragma unroll
+    for (int s = 0; s < RPL; s++) {
+      const int i = lane + 32 * s;
+      if (i >= 8 * T) break;
+      if (i >= rb && i < rb + 8) {
+#pragma unroll
+        for (int r = 0; r < 8; r++) if (i == rb + r) v[s] = z[r];
+      } else if (i >= rb + 8) {        // v_i -= L(I, b) z
+        const double *t = Lg + tix(i >> 3, b) * 64;
+        const int r = i & 7;
+        double acc = v[s];
+#pragma unroll
+        for (int k = 0; k < 8; k++) acc -= t[fo(r, k)] * z[k];
+        v[s] = acc;
+      }
+    }
   }
 }
 
-__device__ void leaf_colmap(const SolveCtx &c, long long id, long long *colsrc) {
-  long long a = id;
-  for (int e = c.kappa; e >= 1; e--) {
-    long long b = (a - 1) / 2;
-    int rb = c.rank[b];
-    for (int q = 0; q < c.dt->rdep[e]; q++) colsrc[c.dt->Kdim[e - 1] + q] = q < rb ? c.dt->colbase[e] + q : -1;
-    a = b;
+// Backward: v <- L^{-T} v.
+__device__ __forceinline__ void tile_bwd(const double *Lg, const double *Li, int T, double v[RPL], int lane) {
+  for (int b = T - 1; b >= 0; b--) {
+    const int rb = 8 * b;
+    double vb[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const int row = rb + k, s = row >> 5;
+      double val = 0.0;
+#pragma unroll
+      for (int ss = 0; ss < RPL; ss++) if (ss == s) val = v[ss];
+      vb[k] = __shfl_sync(0xffffffffu, val, row & 31);
+    }
+    double z[8];                       // w_b = Linv(b)^T v_b
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = r; k < 8; k++) acc += Li[b * 64 + fo(k, r)] * vb[k];
+      z[r] = acc;
+    }
+#pragma unroll
+    for (int s = 0; s < RPL; s++) {
+      const int j = lane + 32 * s;
+      if (j >= 8 * T) break;
+      if (j >= rb && j < rb + 8) {
+#pragma unroll
+        for (int r = 0; r < 8; r++) if (j == rb + r) v[s] = z[r];
+      } else if (j < rb) {             // v_j -= sum_r L(b, J)[r][j%8] z_r
+        const double *t = Lg + tix(b, j >> 3) * 64;
+        const int cj = j & 7;
+        double acc = v[s];
+#pragma unroll
+        for (int r = 0; r < 8; r++) acc -= t[fo(r, cj)] * z[r];
+        v[s] = acc;
+      }
+    }
   }
 }
 
+__device__ void leaf_colmap(const SolveCtx &c, long long id, int *colsrc, int lane) {
+  if (lane == 0) {
+    long long a = id;
+    for (int e = c.kappa; e >= 1; e--) {
+      long long b = (a - 1) / 2;
+      int rb = c.rank[b];
+      for (int q = 0; q < c.dt->rdep[e]; q++) colsrc[c.dt->Kdim[e - 1] + q] = q < rb ? (int)(c.dt->colbase[e] + q) : -1;
+      a = b;
+    }
+  }
+  __syncwarp();
+}
+
+// one warp per leaf
 __global__ void __launch_bounds__(ST) k_leaf_up(SolveCtx c) {
-  extern __shared__ double sm[];
-  __shared__ long long colsrc[1024];
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const long long leaf = blockIdx.x, id = c.ninternal + leaf, lo = c.lo[id], m = c.hi[id] - lo;
-  double *L = sm;                        // packed
-  double *b = sm + c.lstride;            // m
-  double *w = b + c.mmax;                // m
+  __shared__ int colsrc_s[NWS][1024];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long leaf = (long long)blockIdx.x * NWS + wid;
+  if (leaf >= c.nleaves) return;
+  int *colsrc = colsrc_s[wid];
+  const long long id = c.ninternal + leaf, lo = c.lo[id];
+  const int m = (int)(c.hi[id] - lo);
   const double *Lg = c.Lf + leaf * c.lstride;
-  for (long long p = t; p < m * (m + 1) / 2; p += ST) L[p] = Lg[p];
-  for (long long i = t; i < m; i += ST) {
-    double v = c.y[c.perm[lo + i]];
-    if (!isfinite(v)) atomicOr(&c.flags[3], 1);
-    b[i] = v; w[i] = v;
+  const double *Li = Lg + (long long)(c.T * (c.T + 1) / 2) * 64;
+  double b[RPL], v[RPL];
+  bool bad = false;
+#pragma unroll
+  for (int s = 0; s < RPL; s++) {
+    const int i = lane + 32 * s;
+    b[s] = i < m ? c.y[c.perm[lo + i]] : 0.0;
+    if (!isfinite(b[s])) bad = true;
+    v[s] = b[s];
   }
-  if (t == 0) leaf_colmap(c, id, colsrc);
-  __syncthreads();
-  if (warp == 0) chol_solve_warp(L, w, m);
-  __syncthreads();
-  if (warp == 0) {
-    double s = 0.0;
-    for (long long i = lane; i < m; i += 32) s += b[i] * w[i];
-    s = warp_sum(s);
-    if (lane == 0) { c.hv[2 * id] = s; c.hv[2 * id + 1] = 0.0; }
-  }
+  if (bad) atomicOr(&c.flags[3], 1);
+  leaf_colmap(c, id, colsrc, lane);
+  tile_fwd(Lg, Li, c.T, v, lane);
+  tile_bwd(Lg, Li, c.T, v, lane);          // v = A^{-1} b
+  double hs = 0.0;
+#pragma unroll
+  for (int s = 0; s < RPL; s++) hs += b[s] * v[s];
+  hs = warp_sum(hs);
+  if (lane == 0) { c.hv[2 * id] = hs; c.hv[2 * id + 1] = 0.0; }
   double *g = c.V + c.dt->nodeV[c.kappa] + leaf * (long long)c.K;
-  for (int col = warp; col < c.K; col += ST / 32) {
-    long long src = colsrc[col];
+  for (int col = 0; col < c.K; col++) {    // g = E^T w
+    const long long src = colsrc[col];
     double s = 0.0;
-    if (src >= 0) for (long long i = lane; i < m; i += 32) s += c.Xh[src * c.n + lo + i] * w[i];
+    if (src >= 0) {
+      const double *e = c.Xh + src * c.n + lo;
+#pragma unroll
+      for (int ss = 0; ss < RPL; ss++) { const int i = lane + 32 * ss; if (i < m) s += e[i] * v[ss]; }
+    }
     s = warp_sum(s);
     if (lane == 0) g[col] = s;
   }
 }
 
-// t = S^{-1} rhs for one short vector: double solve + two refinement steps with a compensated
-// residual; result as a double-double pair (th, tl).  Single thread.
-__device__ void dd_small_solve(const double *S0, const double *LU, const double *pivd, int q,
-                               double *th, double *tl, double *tmp) {
-  const double *rhs = th;   // th holds the rhs on entry
-  for (int a = 0; a < q; a++) { tmp[a] = rhs[a]; tl[a] = 0.0; }
-  // tmp keeps the rhs; th <- LU^{-1} rhs
-  for (int k = 0; k < q; k++) { int p = (int)pivd[k]; if (p != k) { double x = th[k]; th[k] = th[p]; th[p] = x; } }
-  for (int a = 0; a < q; a++) { double s = th[a]; for (int k = 0; k < a; k++) s -= LU[a * q + k] * th[k]; th[a] = s; }
-  for (int a = q - 1; a >= 0; a--) { double s = th[a]; for (int k = a + 1; k < q; k++) s -= LU[a * q + k] * th[k]; th[a] = s / LU[a * q + a]; }
-  double res[2 * ACA_MAXCAP];
+__global__ void __launch_bounds__(ST) k_leaf_down(SolveCtx c) {
+  __shared__ int colsrc_s[NWS][1024];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long leaf = (long long)blockIdx.x * NWS + wid;
+  if (leaf >= c.nleaves) return;
+  int *colsrc = colsrc_s[wid];
+  const long long id = c.ninternal + leaf, lo = c.lo[id];
+  const int m = (int)(c.hi[id] - lo);
+  const double *Lg = c.Lf + leaf * c.lstride;
+  const double *Li = Lg + (long long)(c.T * (c.T + 1) / 2) * 64;
+  leaf_colmap(c, id, colsrc, lane);
+  const double *w = c.V + c.dt->nodeV[c.kappa] + leaf * (long long)c.K;
+  double v[RPL];
+#pragma unroll
+  for (int s = 0; s < RPL; s++) {
+    const int i = lane + 32 * s;
+    v[s] = i < m ? c.y[c.perm[lo + i]] : 0.0;
+  }
+  for (int col = 0; col < c.K; col++) {    // v = b + E w
+    const long long src = colsrc[col];
+    if (src < 0) continue;
+    const double wc = w[col];
+    const double *e = c.Xh + src * c.n + lo;
+#pragma unroll
+    for (int s = 0; s < RPL; s++) { const int i = lane + 32 * s; if (i < m) v[s] += e[i] * wc; }
+  }
+  tile_fwd(Lg, Li, c.T, v, lane);
+  tile_bwd(Lg, Li, c.T, v, lane);
+#pragma unroll
+  for (int s = 0; s < RPL; s++) {
+    const int i = lane + 32 * s;
+    if (i < m) c.x[c.perm[lo + i]] = v[s];
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Tree passes: one warp per node.  Per-warp shared scratch for the short vectors.
+// ---------------------------------------------------------------------------------------------
+constexpr int QMAX = 2 * ACA_MAXCAP;
+
+// x (length q, shared) <- LU^{-1} x ; one warp
+__device__ void lu_solve_warp(const double *LU, const double *pivd, int q, double *x, int lane) {
+  if (lane == 0)
+    for (int k = 0; k < q; k++) { int p = (int)pivd[k]; if (p != k) { double t = x[k]; x[k] = x[p]; x[p] = t; } }
+  __syncwarp();
+  for (int k = 0; k < q; k++) {                 // unit lower
+    const double xk = x[k];
+    __syncwarp();
+    for (int a = k + 1 + lane; a < q; a += 32) x[a] -= LU[a * q + k] * xk;
+    __syncwarp();
+  }
+  for (int k = q - 1; k >= 0; k--) {           // upper
+    if (lane == 0) x[k] /= LU[k * q + k];
+    __syncwarp();
+    const double xk = x[k];
+    __syncwarp();
+    for (int a = lane; a < k; a += 32) x[a] -= LU[a * q + k] * xk;
+    __syncwarp();
+  }
+}
+
+// t = S^{-1} rhs as (th, tl): double solve + 2 refinement steps with compensated residuals.
+__device__ void dd_solve_warp(const double *S0, const double *LU, const double *pivd, int q,
+                              const double *rhs, double *th, double *tl, double *tmp, int lane) {
+  for (int a = lane; a < q; a += 32) { th[a] = rhs[a]; tl[a] = 0.0; }
+  __syncwarp();
+  lu_solve_warp(LU, pivd, q, th, lane);
   for (int it = 0; it < 2; it++) {
-    for (int a = 0; a < q; a++) {
-      Acc2 A = acc2(tmp[a]);
+    for (int a = lane; a < q; a += 32) {
+      Acc2 A = acc2(rhs[a]);
       for (int k = 0; k < q; k++) acc_fma_dd(A, -S0[a * q + k], th[k], tl[k]);
-      res[a] = acc_val(A);
+      tmp[a] = acc_val(A);
     }
-    for (int k = 0; k < q; k++) { int p = (int)pivd[k]; if (p != k) { double x = res[k]; res[k] = res[p]; res[p] = x; } }
-    for (int a = 0; a < q; a++) { double s = res[a]; for (int k = 0; k < a; k++) s -= LU[a * q + k] * res[k]; res[a] = s; }
-    for (int a = q - 1; a >= 0; a--) { double s = res[a]; for (int k = a + 1; k < q; k++) s -= LU[a * q + k] * res[k]; res[a] = s / LU[a * q + a]; }
-    for (int a = 0; a < q; a++) tl[a] += res[a];
+    __syncwarp();
+    lu_solve_warp(LU, pivd, q, tmp, lane);
+    for (int a = lane; a < q; a += 32) tl[a] += tmp[a];
+    __syncwarp();
   }
 }
 
 __global__ void __launch_bounds__(ST) k_tree_up(SolveCtx c, int d) {
-  __shared__ double th[2 * ACA_MAXCAP], tl[2 * ACA_MAXCAP], tmp[2 * ACA_MAXCAP];
-  const int t = threadIdx.x;
-  const long long i = blockIdx.x, node = (1LL << d) - 1 + i;
+  __shared__ double sv[NWS][4][QMAX];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long i = (long long)blockIdx.x * NWS + wid;
+  if (i >= (1LL << d)) return;
+  const long long node = (1LL << d) - 1 + i;
   const int r = c.dt->rdep[d + 1], q = 2 * r, Kd = c.dt->Kdim[d], K1 = c.dt->Kdim[d + 1];
   const double *g1 = c.V + c.dt->nodeV[d + 1] + (2 * i) * (long long)K1;
   const double *g2 = g1 + K1;
@@ -132,9 +264,13 @@ __global__ void __launch_bounds__(ST) k_tree_up(SolveCtx c, int d) {
   const double *LU = S0 + q * q;
   const double *pivd = LU + q * q;
   const double *B = c.BTpool + c.dt->nodeBT[d] + i * 3LL * q * Kd;
-  if (t == 0) {
-    for (int u = 0; u < r; u++) { th[u] = g2[Kd + u]; th[r + u] = g1[Kd + u]; }
-    dd_small_solve(S0, LU, pivd, q, th, tl, tmp);
+  double *rhs = sv[wid][0], *th = sv[wid][1], *tl = sv[wid][2], *tmp = sv[wid][3];
+  for (int u = lane; u < r; u += 32) { rhs[u] = g2[Kd + u]; rhs[r + u] = g1[Kd + u]; }
+  __syncwarp();
+  dd_solve_warp(S0, LU, pivd, q, rhs, th, tl, tmp, lane);
+  double *tg = c.Tv + c.dt->nodeT[d] + i * 2LL * q;
+  for (int u = lane; u < q; u += 32) { tg[u] = th[u]; tg[q + u] = tl[u]; }
+  if (lane == 0) {
     Acc2 A = acc2(c.hv[2 * (2 * node + 1)]);
     acc_add_dd(A, c.hv[2 * (2 * node + 2)], c.hv[2 * (2 * node + 2) + 1]);
     A.c += c.hv[2 * (2 * node + 1) + 1];
@@ -142,11 +278,8 @@ __global__ void __launch_bounds__(ST) k_tree_up(SolveCtx c, int d) {
     for (int u = 0; u < r; u++) acc_fma_dd(A, -g2[Kd + u], th[r + u], tl[r + u]);
     acc_dd(A, c.hv[2 * node], c.hv[2 * node + 1]);
   }
-  __syncthreads();
-  double *tg = c.Tv + c.dt->nodeT[d] + i * 2LL * q;
-  for (int u = t; u < q; u += ST) { tg[u] = th[u]; tg[q + u] = tl[u]; }
   double *gc = c.V + c.dt->nodeV[d] + i * (long long)Kd;
-  for (int a = t; a < Kd; a += ST) {
+  for (int a = lane; a < Kd; a += 32) {
     Acc2 A = acc2(g1[a]);
     acc_add(A, g2[a]);
     for (int u = 0; u < r; u++) acc_fma_dd(A, -B[(long long)(r + u) * Kd + a], th[u], tl[u]);
@@ -156,52 +289,28 @@ __global__ void __launch_bounds__(ST) k_tree_up(SolveCtx c, int d) {
 }
 
 __global__ void __launch_bounds__(ST) k_tree_down(SolveCtx c, int d) {
-  __shared__ double f[2 * ACA_MAXCAP];
-  const int t = threadIdx.x;
-  const long long i = blockIdx.x;
+  __shared__ double sf[NWS][QMAX];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long i = (long long)blockIdx.x * NWS + wid;
+  if (i >= (1LL << d)) return;
   const int r = c.dt->rdep[d + 1], q = 2 * r, Kd = c.dt->Kdim[d], K1 = c.dt->Kdim[d + 1];
   const double *wc = c.V + c.dt->nodeV[d] + i * (long long)Kd;
   const long long qK = (long long)q * Kd;
   const double *Th = c.BTpool + c.dt->nodeBT[d] + i * 3LL * qK + qK;
   const double *Tl = Th + qK;
   const double *tg = c.Tv + c.dt->nodeT[d] + i * 2LL * q;
-  for (int u = t; u < q; u += ST) {
+  double *f = sf[wid];
+  for (int u = lane; u < q; u += 32) {
     Acc2 A = acc2(tg[u]);
     A.c += tg[q + u];
     for (int a = 0; a < Kd; a++) acc_fma_dd(A, wc[a], Th[(long long)u * Kd + a], Tl[(long long)u * Kd + a]);
     f[u] = acc_val(A);
   }
-  __syncthreads();
+  __syncwarp();
   double *w1 = c.V + c.dt->nodeV[d + 1] + (2 * i) * (long long)K1;
   double *w2 = w1 + K1;
-  for (int a = t; a < Kd; a += ST) { w1[a] = wc[a]; w2[a] = wc[a]; }
-  for (int u = t; u < r; u += ST) { w1[Kd + u] = -f[u]; w2[Kd + u] = -f[r + u]; }
-}
-
-__global__ void __launch_bounds__(ST) k_leaf_down(SolveCtx c) {
-  extern __shared__ double sm[];
-  __shared__ long long colsrc[1024];
-  const int t = threadIdx.x, warp = t >> 5;
-  const long long leaf = blockIdx.x, id = c.ninternal + leaf, lo = c.lo[id], m = c.hi[id] - lo;
-  double *L = sm;
-  double *v = sm + c.lstride;
-  const double *Lg = c.Lf + leaf * c.lstride;
-  for (long long p = t; p < m * (m + 1) / 2; p += ST) L[p] = Lg[p];
-  if (t == 0) leaf_colmap(c, id, colsrc);
-  __syncthreads();
-  const double *w = c.V + c.dt->nodeV[c.kappa] + leaf * (long long)c.K;
-  for (long long i = t; i < m; i += ST) {
-    double s = c.y[c.perm[lo + i]];
-    for (int col = 0; col < c.K; col++) {
-      long long src = colsrc[col];
-      if (src >= 0) s += c.Xh[src * c.n + lo + i] * w[col];
-    }
-    v[i] = s;
-  }
-  __syncthreads();
-  if (warp == 0) chol_solve_warp(L, v, m);
-  __syncthreads();
-  for (long long i = t; i < m; i += ST) c.x[c.perm[lo + i]] = v[i];
+  for (int a = lane; a < Kd; a += 32) { const double v = wc[a]; w1[a] = v; w2[a] = v; }
+  for (int u = lane; u < r; u += 32) { w1[Kd + u] = -f[u]; w2[Kd + u] = -f[r + u]; }
 }
 
 }  // namespace
@@ -210,6 +319,7 @@ __global__ void __launch_bounds__(ST) k_leaf_down(SolveCtx c) {
 hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_only) {
   const int kappa = h->kappa;
   DepthTab &dt = h->dt;
+  if (h->leaf_max > 32 * RPL) return hodlr_set_error(HODLR_EINVAL, "solve: leaf size %d > %d", h->leaf_max, 32 * RPL);
   if (!h->Vpool) {
     long long vTot = 0, tTot = 0;
     for (int e = 0; e <= kappa; e++) { dt.nodeV[e] = vTot; vTot += (1LL << e) * (long long)dt.Kdim[e]; }
@@ -222,30 +332,28 @@ hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_on
   }
   SolveCtx c;
   c.n = h->n; c.ninternal = h->ninternal; c.nleaves = h->nleaves; c.kappa = kappa; c.K = dt.Kdim[kappa];
+  c.T = h->ltiles;
   c.lo = h->lo; c.hi = h->hi; c.perm = h->perm; c.Xh = h->Xh; c.rank = h->rank; c.dt = h->d_dt;
   c.Lf = h->Lf; c.lstride = h->lstride; c.Spool = h->Spool; c.BTpool = h->BTpool;
-  c.V = h->Vpool; c.Tv = h->Tvec; c.hv = h->hvec; c.y = y; c.x = x; c.flags = h->dflags; c.mmax = h->leaf_max;
-  size_t smem_up = sizeof(double) * (h->lstride + 2LL * h->leaf_max);
-  size_t smem_dn = sizeof(double) * (h->lstride + h->leaf_max);
-  HCUDA(cudaFuncSetAttribute(k_leaf_up, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_up));
-  HCUDA(cudaFuncSetAttribute(k_leaf_down, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_dn));
+  c.V = h->Vpool; c.Tv = h->Tvec; c.hv = h->hvec; c.y = y; c.x = x; c.flags = h->dflags;
+  const int lgrid = (int)((h->nleaves + NWS - 1) / NWS);
   ph_begin(h, PH_SLEAF_UP);
-  k_leaf_up<<<(int)h->nleaves, ST, smem_up, h->st>>>(c);
+  k_leaf_up<<<lgrid, ST, 0, h->st>>>(c);
   HLAUNCH(h, "k_leaf_up");
   ph_end(h, PH_SLEAF_UP);
   ph_begin(h, PH_STREE);
   for (int d = kappa - 1; d >= 0; d--) {
-    k_tree_up<<<(int)(1LL << d), ST, 0, h->st>>>(c, d);
+    k_tree_up<<<(int)(((1LL << d) + NWS - 1) / NWS), ST, 0, h->st>>>(c, d);
     HLAUNCH(h, "k_tree_up");
   }
   if (up_only) { ph_end(h, PH_STREE); return HODLR_OK; }
   for (int d = 0; d < kappa; d++) {
-    k_tree_down<<<(int)(1LL << d), ST, 0, h->st>>>(c, d);
+    k_tree_down<<<(int)(((1LL << d) + NWS - 1) / NWS), ST, 0, h->st>>>(c, d);
     HLAUNCH(h, "k_tree_down");
   }
   ph_end(h, PH_STREE);
   ph_begin(h, PH_SLEAF_DOWN);
-  k_leaf_down<<<(int)h->nleaves, ST, smem_dn, h->st>>>(c);
+  k_leaf_down<<<lgrid, ST, 0, h->st>>>(c);
   HLAUNCH(h, "k_leaf_down");
   ph_end(h, PH_SLEAF_DOWN);
   return HODLR_OK;

@@ -3,7 +3,7 @@
 //
 // LSD radix sort on order-preserving 64-bit keys, 8 passes of 8-bit digits.  Each pass:
 //   hist    : per 4096-key tile digit counts             (HBM-bound, 8 B/key read)
-//   scan    : exclusive scan of the digit-major count table (one CTA)
+//   scan    : per-digit exclusive scan over tiles (256 CTAs) + digit totals
 //   scatter : stable tile-local ranks via __match_any_sync + per-warp counters, then scatter
 //             (HBM-bound, 16 B/key read + 16 B/key write)
 // Stability: tiles are ranked in order, warps within a tile in order, keys within a warp in order.
@@ -41,31 +41,37 @@ __global__ void __launch_bounds__(STHREADS) k_hist(const unsigned long long *__r
   for (int t = threadIdx.x; t < 256; t += STHREADS) cnt[(long long)t * ntiles + blockIdx.x] = c[t];
 }
 
-// exclusive scan of m entries in one CTA of 1024 threads
-__global__ void __launch_bounds__(1024) k_scan(unsigned int *__restrict__ a, long long m) {
-  __shared__ unsigned long long part[1024];
-  long long per = (m + 1023) / 1024;
-  long long b = threadIdx.x * per, e = b + per < m ? b + per : m;
-  unsigned long long s = 0;
-  for (long long i = b; i < e; i++) s += a[i];
+// per digit d (one CTA each): exclusive scan of cnt[d][0..ntiles) in place, digit total to tot[d]
+__global__ void __launch_bounds__(256) k_scan_digit(unsigned int *__restrict__ cnt, int ntiles,
+                                                    unsigned int *__restrict__ tot) {
+  __shared__ unsigned int part[256];
+  unsigned int *a = cnt + (long long)blockIdx.x * ntiles;
+  const int per = (ntiles + 255) / 256;
+  const int b = threadIdx.x * per, e = min(b + per, ntiles);
+  unsigned int v[16];
+  unsigned int s = 0;
+  for (int i = b, k = 0; i < e; i++, k++) { v[k] = a[i]; s += v[k]; }
   part[threadIdx.x] = s;
   __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {         // Hillis-Steele inclusive scan
-    unsigned long long v = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
+  for (int o = 1; o < 256; o <<= 1) {
+    unsigned int x = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
     __syncthreads();
-    part[threadIdx.x] += v;
+    part[threadIdx.x] += x;
     __syncthreads();
   }
-  unsigned long long run = part[threadIdx.x] - s;
-  for (long long i = b; i < e; i++) { unsigned int t = a[i]; a[i] = (unsigned int)run; run += t; }
+  unsigned int run = part[threadIdx.x] - s;
+  for (int i = b, k = 0; i < e; i++, k++) { a[i] = run; run += v[k]; }
+  if (threadIdx.x == 255) tot[blockIdx.x] = part[255];
 }
 
 __global__ void __launch_bounds__(STHREADS) k_scatter(const unsigned long long *__restrict__ kin,
                                                       const long long *__restrict__ iin, long long n, int shift,
                                                       int ntiles, const unsigned int *__restrict__ gscan,
+                                                      const unsigned int *__restrict__ tot,
                                                       unsigned long long *__restrict__ kout,
                                                       long long *__restrict__ iout) {
   __shared__ unsigned int wc[16][256];
+  __shared__ unsigned int dbase[256];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int t = threadIdx.x; t < 16 * 256; t += STHREADS) (&wc[0][0])[t] = 0;
   __syncthreads();
@@ -93,11 +99,20 @@ __global__ void __launch_bounds__(STHREADS) k_scatter(const unsigned long long *
     unsigned int run = 0;
     for (int w = 0; w < 16; w++) { unsigned int t = wc[w][d]; wc[w][d] = run; run += t; }
   }
+  if (threadIdx.x < 32) {          // exclusive scan of the 256 digit totals (8 per lane)
+    const int l = threadIdx.x;
+    unsigned int v[8], s = 0;
+    for (int k = 0; k < 8; k++) { v[k] = tot[8 * l + k]; s += v[k]; }
+    unsigned int inc = s;
+    for (int o = 1; o < 32; o <<= 1) { unsigned int x = __shfl_up_sync(0xffffffffu, inc, o); if (l >= o) inc += x; }
+    unsigned int run = inc - s;
+    for (int k = 0; k < 8; k++) { dbase[8 * l + k] = run; run += v[k]; }
+  }
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < 8; r++) {
     if (dig[r] == 256) continue;
-    long long dst = (long long)gscan[(long long)dig[r] * ntiles + blockIdx.x] + wc[warp][dig[r]] + loc[r];
+    long long dst = (long long)dbase[dig[r]] + gscan[(long long)dig[r] * ntiles + blockIdx.x] + wc[warp][dig[r]] + loc[r];
     kout[dst] = k[r];
     iout[dst] = id[r];
   }
@@ -122,7 +137,9 @@ hodlr_status hodlr_sort_and_tree(hodlr_s *h, const double *x) {
   unsigned long long *k1 = (unsigned long long *)hodlr_dalloc(h, sizeof(unsigned long long) * n);
   long long *i0 = (long long *)hodlr_dalloc(h, sizeof(long long) * n);
   long long *i1 = (long long *)hodlr_dalloc(h, sizeof(long long) * n);
-  unsigned int *cnt = (unsigned int *)hodlr_dalloc(h, sizeof(unsigned int) * 256 * (size_t)ntiles);
+  unsigned int *cnt = (unsigned int *)hodlr_dalloc(h, sizeof(unsigned int) * (256 * (size_t)ntiles + 256));
+  unsigned int *tot = cnt + 256 * (size_t)ntiles;
+  if (ntiles > 256 * 16) return hodlr_set_error(HODLR_EINVAL, "sort: n too large for the radix tile table");
   if (!k0 || !k1 || !i0 || !i1 || !cnt) return hodlr_set_error(HODLR_ENOMEM, "sort: device allocation failed");
   int nb = (int)((n + 255) / 256);
   ph_begin(h, PH_SORT);
@@ -132,9 +149,9 @@ hodlr_status hodlr_sort_and_tree(hodlr_s *h, const double *x) {
     int shift = pass * 8;
     k_hist<<<ntiles, STHREADS, 0, h->st>>>(k0, n, shift, ntiles, cnt);
     HLAUNCH(h, "k_hist");
-    k_scan<<<1, 1024, 0, h->st>>>(cnt, 256LL * ntiles);
-    HLAUNCH(h, "k_scan");
-    k_scatter<<<ntiles, STHREADS, 0, h->st>>>(k0, i0, n, shift, ntiles, cnt, k1, i1);
+    k_scan_digit<<<256, 256, 0, h->st>>>(cnt, ntiles, tot);
+    HLAUNCH(h, "k_scan_digit");
+    k_scatter<<<ntiles, STHREADS, 0, h->st>>>(k0, i0, n, shift, ntiles, cnt, tot, k1, i1);
     HLAUNCH(h, "k_scatter");
     unsigned long long *tk = k0; k0 = k1; k1 = tk;
     long long *ti = i0; i0 = i1; i1 = ti;
