@@ -18,6 +18,11 @@
 
 namespace {
 
+__device__ __forceinline__ void cp_async8(double *dst_smem, const double *src) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(dst_smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" :: "r"(sa), "l"(src));
+}
+
 // ---------------------------------------------------------------------------------------------
 // shared reduction of the per-thread candidates + per-warp dot accumulators into one record
 // ---------------------------------------------------------------------------------------------
@@ -137,12 +142,12 @@ __global__ void __launch_bounds__(ACA_SUB) k_aca_row(AcaCtx c) {
     const long long gj = lo2 + j;
     double v = 0.0;
     if (valid) {
+      const double *src = slot + gj;
+      for (int l = 0; l < k; l++) cp_async8(Vs + l * ACA_SUB + t, src + (long long)l * n);   // all k loads in flight
+      asm volatile("cp.async.commit_group;\n" ::);
       v = kval(c.kp, xi - c.xs[gj]);
-      for (int l = 0; l < k; l++) {
-        double vl = slot[(long long)l * n + gj];
-        Vs[l * ACA_SUB + t] = vl;
-        v -= Ui[l] * vl;
-      }
+      asm volatile("cp.async.wait_group 0;\n" ::);
+      for (int l = 0; l < k; l++) v -= Ui[l] * Vs[l * ACA_SUB + t];
       slot[(long long)k * n + gj] = v;                  // V'[:,k] = raw residual row
       if (!used[gj] && amax_better(best_abs, best_idx, fabs(v), j)) { best_abs = fabs(v); best_idx = j; best_val = v; }
       nrm2 += v * v;
@@ -220,12 +225,12 @@ __global__ void __launch_bounds__(ACA_SUB) k_aca_col(AcaCtx c, int *flags) {
     const long long gi = lo1 + i;
     double u = 0.0;
     if (valid) {
+      const double *src = slot + gi;
+      for (int l = 0; l < k; l++) cp_async8(Us + l * ACA_SUB + t, src + (long long)l * n);
+      asm volatile("cp.async.commit_group;\n" ::);
       u = kval(c.kp, c.xs[gi] - xj);
-      for (int l = 0; l < k; l++) {
-        double ul = slot[(long long)l * n + gi];
-        Us[l * ACA_SUB + t] = ul;
-        u -= Vj[l] * ul;
-      }
+      asm volatile("cp.async.wait_group 0;\n" ::);
+      for (int l = 0; l < k; l++) u -= Vj[l] * Us[l * ACA_SUB + t];
       u *= rp;
       slot[(long long)k * n + gi] = u;                  // U'[:,k] = column residual / pivot
       if (!used[gi] && amax_better(best_abs, best_idx, fabs(u), i)) { best_abs = fabs(u); best_idx = i; best_val = u; }
@@ -282,6 +287,148 @@ __global__ void __launch_bounds__(ACA_SUB) k_aca_col(AcaCtx c, int *flags) {
   }
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// Fused ACA for blocks with max(m1, m2) <= ACA_FUSED_MAX: one CTA runs every pivot step of one
+// block (same arithmetic and conventions as the row/column passes above, block-level reductions,
+// pivot bookkeeping in shared memory).  Runs concurrently with the step-synchronous big blocks.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ void block_argmax_n2(double &ba, long long &bi, double &bv, double &n2,
+                                                double *s_abs, long long *s_idx, double *s_val, double *s_n2) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double a2 = __shfl_down_sync(0xffffffffu, ba, o);
+    long long i2 = __shfl_down_sync(0xffffffffu, bi, o);
+    double v2 = __shfl_down_sync(0xffffffffu, bv, o);
+    if (amax_better(ba, bi, a2, i2)) { ba = a2; bi = i2; bv = v2; }
+    n2 += __shfl_down_sync(0xffffffffu, n2, o);
+  }
+  if (lane == 0) { s_abs[warp] = ba; s_idx[warp] = bi; s_val[warp] = bv; s_n2[warp] = n2; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < ACA_SUB / 32; w++) {
+      if (amax_better(s_abs[0], s_idx[0], s_abs[w], s_idx[w])) { s_abs[0] = s_abs[w]; s_idx[0] = s_idx[w]; s_val[0] = s_val[w]; }
+      s_n2[0] += s_n2[w];
+    }
+  }
+  __syncthreads();
+  ba = s_abs[0]; bi = s_idx[0]; bv = s_val[0]; n2 = s_n2[0];
+}
+
+__global__ void __launch_bounds__(ACA_SUB) k_aca_fused(AcaCtx c, const int *blocks, int *flags) {
+  __shared__ double vbuf[ACA_FUSED_MAX];
+  __shared__ unsigned char usedR[ACA_FUSED_MAX], usedC[ACA_FUSED_MAX];
+  __shared__ double Ui[ACA_MAXCAP], dV[ACA_MAXCAP], dots[ACA_MAXCAP];
+  __shared__ double s_abs[ACA_SUB / 32], s_val[ACA_SUB / 32], s_n2[ACA_SUB / 32];
+  __shared__ long long s_idx[ACA_SUB / 32];
+  __shared__ long long s_ipiv, s_jpiv;
+  __shared__ double s_pval, s_nv2, s_S2;
+  __shared__ int s_k, s_done;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int b = blocks[blockIdx.x];
+  const long long n = c.n;
+  const long long c1 = 2LL * b + 1, c2 = 2LL * b + 2;
+  const long long lo1 = c.lo[c1], m1 = c.hi[c1] - lo1, lo2 = c.lo[c2], m2 = c.hi[c2] - lo2;
+  const long long mn = m1 < m2 ? m1 : m2;
+  const int cap = c.st[b].cap;
+  const int e = c.bdepth[b] + 1;
+  double *slot = c.Xh + c.dt->colbase[e] * n;
+  for (int i = t; i < ACA_FUSED_MAX; i += ACA_SUB) { usedR[i] = 0; usedC[i] = 0; }
+  __syncthreads();
+  if (t == 0) {
+    s_k = 0; s_done = 0; s_S2 = 0.0; s_ipiv = m1 - 1;
+    const double v = c.xs[lo1 + m1 - 1];          // mark the run of the first pivot row (R2)
+    for (long long i = m1 - 1; i >= 0 && c.xs[lo1 + i] == v; i--) usedR[i] = 1;
+  }
+  __syncthreads();
+  for (;;) {
+    const int k = s_k;
+    // ---------------- row pass ----------------
+    const long long ig = lo1 + s_ipiv;
+    const double xi = c.xs[ig];
+    for (int l = t; l < k; l += ACA_SUB) Ui[l] = slot[(long long)l * n + ig];
+    __syncthreads();
+    double ba = 0.0, bv = 0.0, n2 = 0.0; long long bi = -1;
+    for (long long j = t; j < m2; j += ACA_SUB) {
+      const long long gj = lo2 + j;
+      double v = kval(c.kp, xi - c.xs[gj]);
+#pragma unroll 8
+      for (int l = 0; l < k; l++) v -= Ui[l] * __ldcg(slot + (long long)l * n + gj);
+      slot[(long long)k * n + gj] = v;
+      vbuf[j] = v;
+      if (!usedC[j] && amax_better(ba, bi, fabs(v), j)) { ba = fabs(v); bi = j; bv = v; }
+      n2 += v * v;
+    }
+    block_argmax_n2(ba, bi, bv, n2, s_abs, s_idx, s_val, s_n2);
+    for (int l = warp; l < k; l += ACA_SUB / 32) {
+      double s = 0.0;
+#pragma unroll 8
+      for (long long j = lane; j < m2; j += 32) s += __ldcg(slot + (long long)l * n + lo2 + j) * vbuf[j];
+      s = warp_sum(s);
+      if (lane == 0) dV[l] = s;
+    }
+    if (t == 0) {
+      if (bi < 0 || ba == 0.0) { s_done = 1; }            // exactly-zero residual row: rank k
+      else { s_jpiv = bi; s_pval = bv; s_nv2 = n2; usedC[bi] = 1; }
+    }
+    __syncthreads();
+    if (s_done) break;
+    // ---------------- column pass ----------------
+    const long long jg = lo2 + s_jpiv;
+    const double xj = c.xs[jg];
+    const double rp = 1.0 / s_pval;
+    for (int l = t; l < k; l += ACA_SUB) Ui[l] = slot[(long long)l * n + jg];
+    __syncthreads();
+    ba = 0.0; bv = 0.0; n2 = 0.0; bi = -1;
+    for (long long i = t; i < m1; i += ACA_SUB) {
+      const long long gi = lo1 + i;
+      double u = kval(c.kp, c.xs[gi] - xj);
+#pragma unroll 8
+      for (int l = 0; l < k; l++) u -= Ui[l] * __ldcg(slot + (long long)l * n + gi);
+      u *= rp;
+      slot[(long long)k * n + gi] = u;
+      vbuf[i] = u;
+      if (!usedR[i] && amax_better(ba, bi, fabs(u), i)) { ba = fabs(u); bi = i; bv = u; }
+      n2 += u * u;
+    }
+    block_argmax_n2(ba, bi, bv, n2, s_abs, s_idx, s_val, s_n2);
+    for (int l = warp; l < k; l += ACA_SUB / 32) {
+      double s = 0.0;
+#pragma unroll 8
+      for (long long i = lane; i < m1; i += 32) s += __ldcg(slot + (long long)l * n + lo1 + i) * vbuf[i];
+      s = warp_sum(s);
+      if (lane == 0) dots[l] = s;
+    }
+    __syncthreads();
+    if (t == 0) {
+      double cross = 0.0;
+      for (int l = 0; l < k; l++) cross += dots[l] * dV[l];
+      const double nu2 = n2, nv2 = s_nv2;
+      const double S2 = s_S2 + 2.0 * cross + nu2 * nv2;
+      s_S2 = S2;
+      const int k1 = k + 1;
+      s_k = k1;
+      int done = 0;
+      if (sqrt(nu2) * sqrt(nv2) <= c.eps * sqrt(fabs(S2))) done = 1;
+      else if (k1 == mn) done = 1;
+      else if (k1 == cap) { done = 2; atomicAdd(&flags[5], 1); }
+      else if (bi < 0 || ba == 0.0) done = 1;
+      else {
+        s_ipiv = bi;
+        const double v = c.xs[lo1 + bi];
+        usedR[bi] = 1;
+        for (long long i = bi - 1; i >= 0 && c.xs[lo1 + i] == v; i--) usedR[i] = 1;
+        for (long long i = bi + 1; i < m1 && c.xs[lo1 + i] == v; i++) usedR[i] = 1;
+      }
+      s_done = done;
+    }
+    __syncthreads();
+    if (s_done) break;
+  }
+  if (t == 0) c.rank[b] = s_k;
+}
+
 }  // namespace
 
 hodlr_status hodlr_aca(hodlr_s *h) {
@@ -294,14 +441,18 @@ hodlr_status hodlr_aca(hodlr_s *h) {
   std::vector<long long> rb_r(nb), rb_c(nb);
   std::vector<int> bdepth(nb);
   long long nrec_r = 0, nrec_c = 0;
+  std::vector<int> fused_blocks;
+  int nbig = 0;
   for (long long b = 0; b < nb; b++) {
     bdepth[b] = hodlr_depth_of(b);
     long long m1 = h->h_hi[2 * b + 1] - h->h_lo[2 * b + 1], m2 = h->h_hi[2 * b + 2] - h->h_lo[2 * b + 2];
+    if (std::max(m1, m2) <= ACA_FUSED_MAX) { fused_blocks.push_back((int)b); nq_r[b] = nq_c[b] = 0; rb_r[b] = rb_c[b] = 0; continue; }
+    nbig++;
     for (int side = 0; side < 2; side++) {
       long long m = side == 0 ? m2 : m1;
       long long chunk = (m + 127) / 128;
       chunk = ((chunk + ACA_SUB - 1) / ACA_SUB) * ACA_SUB;
-      if (chunk < ACA_SUB) chunk = ACA_SUB;
+      if (chunk < ACA_BIG_CHUNK) chunk = ACA_BIG_CHUNK;
       int q = 0;
       for (long long s = 0; s < m; s += chunk, q++) {
         AcaItem it; it.block = (int)b; it.q = q; it.start = s; it.len = (int)std::min(chunk, m - s); it.pad = 0;
@@ -312,8 +463,9 @@ hodlr_status hodlr_aca(hodlr_s *h) {
     }
   }
   // ---- device buffers ----
-  AcaItem *d_items_r = (AcaItem *)hodlr_dalloc(h, sizeof(AcaItem) * items_r.size());
-  AcaItem *d_items_c = (AcaItem *)hodlr_dalloc(h, sizeof(AcaItem) * items_c.size());
+  AcaItem *d_items_r = (AcaItem *)hodlr_dalloc(h, sizeof(AcaItem) * (items_r.size() + 1));
+  AcaItem *d_items_c = (AcaItem *)hodlr_dalloc(h, sizeof(AcaItem) * (items_c.size() + 1));
+  int *d_fused = (int *)hodlr_dalloc(h, sizeof(int) * (fused_blocks.size() + 1));
   int *d_nq = (int *)hodlr_dalloc(h, sizeof(int) * 2 * nb);
   long long *d_rb = (long long *)hodlr_dalloc(h, sizeof(long long) * 2 * nb);
   double *d_rec = (double *)hodlr_dalloc(h, sizeof(double) * ACA_RECW * (size_t)(nrec_r + nrec_c));
@@ -321,18 +473,18 @@ hodlr_status hodlr_aca(hodlr_s *h) {
   h->rank = (int *)hodlr_dalloc(h, sizeof(int) * nb);
   h->bdepth = (int *)hodlr_dalloc(h, sizeof(int) * nb);
   h->used = (unsigned char *)hodlr_dalloc(h, (size_t)h->kappa * n);
-  if (!d_items_r || !d_items_c || !d_nq || !d_rb || !d_rec || !h->ast || !h->rank || !h->bdepth || !h->used)
+  if (!d_items_r || !d_items_c || !d_fused || !d_nq || !d_rb || !d_rec || !h->ast || !h->rank || !h->bdepth || !h->used)
     return hodlr_set_error(HODLR_ENOMEM, "aca: device allocation failed");
   std::vector<int> nq_all(nq_r); nq_all.insert(nq_all.end(), nq_c.begin(), nq_c.end());
   std::vector<long long> rb_all(rb_r); rb_all.insert(rb_all.end(), rb_c.begin(), rb_c.end());
-  HCUDA(cudaMemcpyAsync(d_items_r, items_r.data(), sizeof(AcaItem) * items_r.size(), cudaMemcpyHostToDevice, h->st));
-  HCUDA(cudaMemcpyAsync(d_items_c, items_c.data(), sizeof(AcaItem) * items_c.size(), cudaMemcpyHostToDevice, h->st));
+  if (!items_r.empty()) HCUDA(cudaMemcpyAsync(d_items_r, items_r.data(), sizeof(AcaItem) * items_r.size(), cudaMemcpyHostToDevice, h->st));
+  if (!items_c.empty()) HCUDA(cudaMemcpyAsync(d_items_c, items_c.data(), sizeof(AcaItem) * items_c.size(), cudaMemcpyHostToDevice, h->st));
+  if (!fused_blocks.empty()) HCUDA(cudaMemcpyAsync(d_fused, fused_blocks.data(), sizeof(int) * fused_blocks.size(), cudaMemcpyHostToDevice, h->st));
   HCUDA(cudaMemcpyAsync(d_nq, nq_all.data(), sizeof(int) * 2 * nb, cudaMemcpyHostToDevice, h->st));
   HCUDA(cudaMemcpyAsync(d_rb, rb_all.data(), sizeof(long long) * 2 * nb, cudaMemcpyHostToDevice, h->st));
   HCUDA(cudaMemcpyAsync(h->bdepth, bdepth.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, h->st));
   HCUDA(cudaMemsetAsync(h->used, 0, (size_t)h->kappa * n, h->st));
-  int nbi = (int)nb;
-  HCUDA(cudaMemcpyAsync(h->dflags + 4, &nbi, sizeof(int), cudaMemcpyHostToDevice, h->st));
+  HCUDA(cudaMemcpyAsync(h->dflags + 4, &nbig, sizeof(int), cudaMemcpyHostToDevice, h->st));
   // the pageable copies above are staged synchronously by the runtime, so the vectors may die
 
   AcaCtx c;
@@ -342,6 +494,14 @@ hodlr_status hodlr_aca(hodlr_s *h) {
   ph_begin(h, PH_ACA);
   k_aca_init<<<(int)((nb + 255) / 256), 256, 0, h->st>>>(c, (int)nb, h->cap);
   HLAUNCH(h, "k_aca_init");
+  // small blocks: one fused CTA per block on the side stream, concurrent with the big-block steps
+  if (!fused_blocks.empty()) {
+    HCUDA(cudaEventRecord(h->ev_fork, h->st));
+    HCUDA(cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
+    k_aca_fused<<<(int)fused_blocks.size(), ACA_SUB, 0, h->st2>>>(c, d_fused, h->dflags);
+    HLAUNCH(h, "k_aca_fused");
+    HCUDA(cudaEventRecord(h->ev_join, h->st2));
+  }
 
   AcaCtx cr = c, cc = c;
   cr.items = d_items_r; cr.nq = d_nq; cr.recbase = d_rb; cr.rec = d_rec;
@@ -359,7 +519,7 @@ hodlr_status hodlr_aca(hodlr_s *h) {
   for (int i = 0; i < 8; i++) HCUDA(cudaEventCreateWithFlags(&evs[i], cudaEventDisableTiming));
   int issued = 0, checked = 0, steps = 0;
   hodlr_status status = HODLR_OK;
-  const int maxsteps = h->cap + 1;
+  const int maxsteps = nbig > 0 ? h->cap + 1 : 0;
   for (int k = 0; k < maxsteps; k++) {
     size_t smem = (size_t)(k + 1) * ACA_SUB * sizeof(double);
     k_aca_row<<<(int)items_r.size(), ACA_SUB, smem, h->st>>>(cr);
@@ -383,6 +543,7 @@ hodlr_status hodlr_aca(hodlr_s *h) {
     }
     if (stop) break;
   }
+  if (!fused_blocks.empty()) HCUDA(cudaStreamWaitEvent(h->st, h->ev_join, 0));
   ph_end(h, PH_ACA);
   HCUDA(cudaStreamSynchronize(h->st));
   for (int i = 0; i < 8; i++) cudaEventDestroy(evs[i]);

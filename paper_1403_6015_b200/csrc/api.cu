@@ -68,6 +68,9 @@ void hodlr_free(hodlr_t h) {
   if (!h) return;
   for (int i = h->nallocs - 1; i >= 0; i--) cudaFreeAsync(h->allocs[i], h->st);
   cudaStreamSynchronize(h->st);
+  if (h->st2) cudaStreamDestroy(h->st2);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
   for (int p = 0; p < PH_N; p++) for (int j = 0; j < 2; j++) if (h->ph_ev[p][j]) cudaEventDestroy(h->ph_ev[p][j]);
@@ -100,6 +103,8 @@ hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const 
   if (ce != cudaSuccess) { delete h; return hodlr_cuda_check(ce, "cudaGetDevice"); }
   setup_pool(h->dev);
   cudaEventCreate(&h->ev0); cudaEventCreate(&h->ev1);
+  cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming); cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming);
+  cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking);
   for (int p = 0; p < PH_N; p++) for (int j = 0; j < 2; j++) cudaEventCreate(&h->ph_ev[p][j]);
   cudaEventRecord(h->ev0, h->st);
   h->launches = 0;

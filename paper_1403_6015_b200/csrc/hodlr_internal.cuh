@@ -20,6 +20,8 @@
 #define ACA_MAXCAP 64      // hard ceiling on the ACA rank cap (records/state are sized by it)
 #define ACA_RECW (4 + ACA_MAXCAP)
 #define ACA_SUB 256        // threads per ACA CTA == sub-tile width
+#define ACA_FUSED_MAX 4096 // blocks with both sides <= this run the fused single-CTA ACA
+#define ACA_BIG_CHUNK 2048 // minimum chunk per CTA for the step-synchronous big blocks
 
 // ----------------------------------------------------------------------------------------------
 // Covariance functions, Table I; C_ij = k(x_i - x_j) + s2 [i == j]
@@ -98,6 +100,8 @@ enum { PH_SORT = 0, PH_ACA, PH_LEAF, PH_TREE, PH_SLEAF_UP, PH_STREE, PH_SLEAF_DO
 // ----------------------------------------------------------------------------------------------
 struct hodlr_s {
   cudaStream_t st;
+  cudaStream_t st2;           // side stream (fused small-block ACA)
+  cudaEvent_t ev_fork, ev_join;
   int dev;
   long long n;
   KParams kp;
