@@ -161,7 +161,7 @@ def algorithmic(info, n, leaf):
     # leaf factor (one launch): assemble p^2/2 entries (~30 flop each), Cholesky p^3/3, Z = L^{-1}E (p^2 K),
     # Pi = Z^T Z (p K^2, symmetric half); bytes: read E (8 n K), write L (4 n (p+1)) and Pi (8 K^2 per leaf)
     leaf_flops = nl * (30 * p * p / 2 + p ** 3 / 3 + p * p * K + p * K * K)
-    leaf_bytes = 8 * n * K + 4 * n * (p + 1) + 8 * nl * K * K
+    leaf_bytes = 8 * n * K + 4 * n * (p + 1) + 4 * nl * K * (K + 1)
     # ACA: n * K entry evaluations (~30 flop) + 2 n sum r^2 arithmetic x2 (row and column residual + dots)
     aca_flops = n * K * 30 + 4 * n * sum(x * x for x in r)
     aca_bytes = 8 * n * K + 4 * n * sum(x * x for x in r)
@@ -177,12 +177,17 @@ def load_peaks():
 
 
 def fp64_peak_tflops(peaks, sm_mhz):
-    """FP64 peak: B200 issues 64 FP64 FMA/clk/SM (DFMA and DMMA alike): 148 * 64 * 2 * f.  Uses the
-    measured fp64 number in MEASURED_PEAKS.json if present, else this unit count at the clock seen."""
+    """FP64 tensor (DMMA) peak.  MEASURED_PEAKS.json has no FP64 figure; use the DMMA microbenchmark
+    (tools/fp64_peak.cu, profiles/fp64_peak_r01.json: 37.13 TFLOP/s at 1965 MHz = 148 SM x 64 FMA/clk x 2)."""
     if "fp64_tflops" in peaks:
         return peaks["fp64_tflops"], "measured (MEASURED_PEAKS.json fp64_tflops)"
-    f = (sm_mhz or peaks.get("clocks_under_load", {}).get("sm_mhz_median") or 1965.0) * 1e6
-    return 148 * 64 * 2 * f / 1e12, f"derived: 148 SMs x 64 FP64 FMA/clk x 2 x {f / 1e6:.0f} MHz (guide unit counts)"
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak_r01.json")) as f:
+            v = json.load(f)["fp64_dmma_m8n8k4_tflops"]
+        return v, "measured DMMA peak, tools/fp64_peak.cu (profiles/fp64_peak_r01.json), 1965 MHz"
+    except (OSError, KeyError, ValueError):
+        f = (sm_mhz or 1965.0) * 1e6
+        return 148 * 64 * 2 * f / 1e12, f"derived: 148 SMs x 64 FP64 FMA/clk x 2 x {f / 1e6:.0f} MHz"
 
 
 # ------------------------------------------------------------------ our arm
@@ -289,7 +294,7 @@ def run_ours(args):
         if dom == "leaf_factor":
             peak, how = fp64_peak_tflops(peaks, clocks.get("sm_mhz"))
             achieved = fl / t_launch / 1e12
-            roof = {"kernel": "k_leaf_factor", "bound": "alu", "achieved": achieved, "peak": peak,
+            roof = {"kernel": "k_leaf_factor_mma", "bound": "tensor", "achieved": achieved, "peak": peak,
                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None, "peak_source": how,
                     "algorithmic_flops_per_launch": fl, "launch_ms": 1e3 * t_launch}
         else:
