@@ -63,7 +63,7 @@ typedef struct {
 
 /* Optional build options.  NULL => defaults. */
 typedef struct {
-  int32_t rank_cap;             /* max ACA rank per block; 0 => 64 (always clamped to min(m1, m2)) */
+  int32_t rank_cap;             /* max ACA rank per block, <= 64; 0 => 48 (always clamped to min(m1, m2)) */
   int32_t reserved[7];
 } hodlr_opts;
 

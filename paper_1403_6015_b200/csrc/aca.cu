@@ -429,6 +429,13 @@ __global__ void __launch_bounds__(ACA_SUB) k_aca_fused(AcaCtx c, const int *bloc
   if (t == 0) c.rank[b] = s_k;
 }
 
+// Device-side loop control for the conditional-while CUDA graph: keep iterating while big blocks are
+// active and the step count is below the cap.
+__global__ void k_aca_cond(cudaGraphConditionalHandle hdl, const int *active, int *step, int maxsteps) {
+  const int s = ++(*step);
+  cudaGraphSetConditional(hdl, (*active > 0 && s < maxsteps) ? 1u : 0u);
+}
+
 }  // namespace
 
 hodlr_status hodlr_aca(hodlr_s *h) {
@@ -506,49 +513,70 @@ hodlr_status hodlr_aca(hodlr_s *h) {
   AcaCtx cr = c, cc = c;
   cr.items = d_items_r; cr.nq = d_nq; cr.recbase = d_rb; cr.rec = d_rec;
   cc.items = d_items_c; cc.nq = d_nq + nb; cc.recbase = d_rb + nb; cc.rec = d_rec + ACA_RECW * nrec_r;
-  static bool attr_set = false;
-  if (!attr_set) {
-    size_t maxsm = (size_t)(ACA_MAXCAP + 1) * ACA_SUB * sizeof(double);
-    HCUDA(cudaFuncSetAttribute(k_aca_row, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
-    HCUDA(cudaFuncSetAttribute(k_aca_col, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
-    attr_set = true;
+  // big blocks: the pivot-step loop runs on the device as a conditional-while CUDA graph
+  // (row pass, column pass, loop test) -- no host polling between steps
+  const size_t smem = (size_t)(h->cap + 1) * ACA_SUB * sizeof(double);
+  static int attr_bytes = 0;
+  if ((int)smem > attr_bytes) {
+    HCUDA(cudaFuncSetAttribute(k_aca_row, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    HCUDA(cudaFuncSetAttribute(k_aca_col, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_bytes = (int)smem;
   }
-  int *pinned = nullptr;
-  HCUDA(cudaMallocHost(&pinned, sizeof(int) * 8));
-  cudaEvent_t evs[8];
-  for (int i = 0; i < 8; i++) HCUDA(cudaEventCreateWithFlags(&evs[i], cudaEventDisableTiming));
-  int issued = 0, checked = 0, steps = 0;
   hodlr_status status = HODLR_OK;
-  const int maxsteps = nbig > 0 ? h->cap + 1 : 0;
-  for (int k = 0; k < maxsteps; k++) {
-    size_t smem = (size_t)(k + 1) * ACA_SUB * sizeof(double);
-    k_aca_row<<<(int)items_r.size(), ACA_SUB, smem, h->st>>>(cr);
-    HLAUNCH(h, "k_aca_row");
-    k_aca_col<<<(int)items_c.size(), ACA_SUB, smem, h->st>>>(cc, h->dflags);
-    HLAUNCH(h, "k_aca_col");
-    steps = k + 1;
-    // lagged poll of the active-block counter (no pipeline bubble)
-    int slot = issued % 8;
-    HCUDA(cudaMemcpyAsync(&pinned[slot], h->dflags + 4, sizeof(int), cudaMemcpyDeviceToHost, h->st));
-    HCUDA(cudaEventRecord(evs[slot], h->st));
-    issued++;
-    bool stop = false;
-    while (checked < issued) {
-      int cs = checked % 8;
-      cudaError_t q = (issued - checked >= 3) ? cudaEventSynchronize(evs[cs]) : cudaEventQuery(evs[cs]);
-      if (q == cudaErrorNotReady) break;
-      if (q != cudaSuccess) { status = hodlr_cuda_check(q, "aca poll"); stop = true; break; }
-      if (pinned[cs] == 0) stop = true;
-      checked++;
+  int steps = 0;
+  if (nbig > 0) {
+    HCUDA(cudaMemsetAsync(h->dflags + 6, 0, sizeof(int), h->st));
+    cudaGraph_t g = nullptr, body = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    cudaGraphConditionalHandle hdl;
+    cudaError_t e = cudaGraphCreate(&g, 0);
+    if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&hdl, g, 1, cudaGraphCondAssignDefault);
+    cudaGraphNodeParams cpar = {};
+    cudaGraphNode_t cnode;
+    if (e == cudaSuccess) {
+      cpar.type = cudaGraphNodeTypeConditional;
+      cpar.conditional.handle = hdl; cpar.conditional.type = cudaGraphCondTypeWhile; cpar.conditional.size = 1;
+      e = cudaGraphAddNode(&cnode, g, nullptr, 0, &cpar);
     }
-    if (stop) break;
+    int *active = h->dflags + 4, *stepc = h->dflags + 6, *flags = h->dflags;
+    int maxsteps = h->cap + 1;
+    void *arow[] = {&cr};
+    void *acol[] = {&cc, &flags};
+    void *acond[] = {&hdl, &active, &stepc, &maxsteps};
+    cudaGraphNode_t n1, n2, n3;
+    if (e == cudaSuccess) {
+      body = cpar.conditional.phGraph_out[0];
+      cudaKernelNodeParams k1 = {};
+      k1.func = (void *)k_aca_row; k1.gridDim = dim3((unsigned)items_r.size()); k1.blockDim = dim3(ACA_SUB);
+      k1.sharedMemBytes = (unsigned)smem; k1.kernelParams = arow;
+      e = cudaGraphAddKernelNode(&n1, body, nullptr, 0, &k1);
+    }
+    if (e == cudaSuccess) {
+      cudaKernelNodeParams k2 = {};
+      k2.func = (void *)k_aca_col; k2.gridDim = dim3((unsigned)items_c.size()); k2.blockDim = dim3(ACA_SUB);
+      k2.sharedMemBytes = (unsigned)smem; k2.kernelParams = acol;
+      e = cudaGraphAddKernelNode(&n2, body, &n1, 1, &k2);
+    }
+    if (e == cudaSuccess) {
+      cudaKernelNodeParams k3 = {};
+      k3.func = (void *)k_aca_cond; k3.gridDim = dim3(1); k3.blockDim = dim3(1); k3.kernelParams = acond;
+      e = cudaGraphAddKernelNode(&n3, body, &n2, 1, &k3);
+    }
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&ge, g, 0);
+    if (e == cudaSuccess) e = cudaGraphLaunch(ge, h->st);
+    if (e != cudaSuccess) status = hodlr_cuda_check(e, "aca graph");
+    h->launches += 3; hodlr_global_launches += 3;     // per iteration; the step count is added below
+    if (ge) cudaGraphExecDestroy(ge);
+    if (g) cudaGraphDestroy(g);
   }
   if (!fused_blocks.empty()) HCUDA(cudaStreamWaitEvent(h->st, h->ev_join, 0));
   ph_end(h, PH_ACA);
   HCUDA(cudaStreamSynchronize(h->st));
-  for (int i = 0; i < 8; i++) cudaEventDestroy(evs[i]);
-  cudaFreeHost(pinned);
   if (status != HODLR_OK) return status;
+  if (nbig > 0) {
+    HCUDA(cudaMemcpy(&steps, h->dflags + 6, sizeof(int), cudaMemcpyDeviceToHost));
+    h->launches += 3 * (steps - 1); hodlr_global_launches += 3 * (steps - 1);
+  }
   h->aca_steps = steps;
   return HODLR_OK;
 }

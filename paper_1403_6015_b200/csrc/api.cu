@@ -92,7 +92,7 @@ hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const 
   if (!(theta[0] >= 0.0) || !isfinite(theta[0])) return hodlr_set_error(HODLR_EINVAL, "build: a = %g < 0", theta[0]);
   if ((int)kernel < 0 || (int)kernel > 2) return hodlr_set_error(HODLR_EINVAL, "build: unknown kernel %d", (int)kernel);
   if (dist && dist->nranks > 1) return hodlr_set_error(HODLR_EINVAL, "build: multi-GPU sharding not available in this build");
-  int cap = (opts && opts->rank_cap > 0) ? opts->rank_cap : 64;
+  int cap = (opts && opts->rank_cap > 0) ? opts->rank_cap : 48;
   if (cap > ACA_MAXCAP) return hodlr_set_error(HODLR_EINVAL, "build: rank_cap %d > %d", cap, ACA_MAXCAP);
   hodlr_s *h = new (std::nothrow) hodlr_s();
   if (!h) return hodlr_set_error(HODLR_ENOMEM, "build: host allocation failed");

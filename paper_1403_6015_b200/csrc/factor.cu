@@ -196,7 +196,7 @@ __device__ __forceinline__ void lu_solve_col(const double *S, const int *piv, in
 __global__ void __launch_bounds__(TT) k_tree_factor(TreeCtx c) {
   extern __shared__ double sm[];
   __shared__ int pivs[2 * ACA_MAXCAP];
-  __shared__ int zero_piv;
+  __shared__ int zero_piv, nref;
   const int t = threadIdx.x;
   const long long i = blockIdx.x;
   const long long node = (1LL << c.d) - 1 + i;
@@ -263,11 +263,16 @@ __global__ void __launch_bounds__(TT) k_tree_factor(TreeCtx c) {
     }
     c.node_ld[node] = la;
     if (zero_piv || sg <= 0) { atomicAdd(&c.flags[1], 1); atomicMin(&c.flags[2], (int)node); }
+    // refinement steps: one when the pivot growth ratio is mild, two otherwise (cond(S_c) up to ~1e12)
+    double umax = 0.0, umin = 1e300;
+    for (int k = 0; k < q; k++) { const double u = fabs(S[k * q + k]); umax = fmax(umax, u); umin = fmin(umin, u); }
+    nref = (umin > 0.0 && umax < 1e6 * umin) ? 1 : 2;
   }
+  __syncthreads();
   if (!zero_piv && Kd > 0) {
     for (int col = t; col < Kd; col += TT) lu_solve_col(S, pivs, q, Th + col, Kd);
     __syncthreads();
-    for (int it = 0; it < 2; it++) {          // iterative refinement, residual in double-double
+    for (int it = 0; it < nref; it++) {       // iterative refinement, residual in double-double
       for (long long e = t; e < qK; e += TT) {
         const int a = (int)(e / Kd), col = (int)(e - (long long)a * Kd);
         Acc2 A = acc2(B[e]);

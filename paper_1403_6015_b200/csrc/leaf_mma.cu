@@ -43,6 +43,9 @@ __device__ __forceinline__ void c_to_b(double c0, double c1, int lane, double &b
   b1 = sel ? y1 : y0;
 }
 
+// (I, J) of packed lower tile index ti, for T <= 16 (136 tiles)
+__constant__ unsigned char c_tileI[136], c_tileJ[136];
+
 struct LeafMmaCtx {
   KParams kp;
   long long n, ninternal;
@@ -143,24 +146,37 @@ __global__ void __launch_bounds__(NTH, 1) k_leaf_factor_mma(LeafMmaCtx c) {
   }
   __syncthreads();
   // E_l -> sZ (column-major), asynchronous copies overlapped with the assembly and the Cholesky
-  for (int p = t; p < Kz * P; p += NTH) {
-    const int col = p / P, row = p - col * P;
-    const long long src = colsrc[col];
-    double *dst = sZ + col * LDR + row;
-    if (src >= 0 && row < m) {
-      const double *g = c.Xh + src * c.n + lo + row;
-      unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" :: "r"(sa), "l"(g));
-    } else {
-      *dst = 0.0;
+  const bool al16 = ((c.n | lo) & 1) == 0;      // 16-byte aligned column segments (row pairs)
+  if (al16) {
+    for (int p = t; p < Kz * (P / 2); p += NTH) {
+      const int col = p / (P / 2), row = 2 * (p - col * (P / 2));
+      const long long src = colsrc[col];
+      double *dst = sZ + col * LDR + row;
+      if (src >= 0 && row + 1 < m) {
+        unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(sa), "l"(c.Xh + src * c.n + lo + row));
+      } else {
+        dst[0] = (src >= 0 && row < m) ? c.Xh[src * c.n + lo + row] : 0.0;
+        dst[1] = 0.0;
+      }
+    }
+  } else {
+    for (int p = t; p < Kz * P; p += NTH) {
+      const int col = p / P, row = p - col * P;
+      const long long src = colsrc[col];
+      double *dst = sZ + col * LDR + row;
+      if (src >= 0 && row < m) {
+        unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" :: "r"(sa), "l"(c.Xh + src * c.n + lo + row));
+      } else {
+        *dst = 0.0;
+      }
     }
   }
   asm volatile("cp.async.commit_group;\n" ::);
   // assemble A_l = K[l,l] + s2 I into the lower tiles (fragment order), identity padding beyond m
   for (int ti = warp; ti < NTILE; ti += NW) {
-    int I = 0;
-    while ((I + 1) * (I + 2) / 2 <= ti) I++;
-    const int J = ti - I * (I + 1) / 2;
+    const int I = c_tileI[ti], J = c_tileJ[ti];
 #pragma unroll
     for (int h = 0; h < 2; h++) {
       const int r = lane >> 2, cc = (lane & 3) + 4 * h;
@@ -173,28 +189,49 @@ __global__ void __launch_bounds__(NTH, 1) k_leaf_factor_mma(LeafMmaCtx c) {
   }
   __syncthreads();
   // ---------------- Cholesky, left-looking over tile columns J ----------------
+  // Per column: warp 0 forms the diagonal tile C(J,J) and factors it (POTRF + inverse) while warps 1-7
+  // form the sub-diagonal tiles C(I,J) = A(I,J) - sum_{k<J} L(I,k) L(J,k)^T; then all warps apply
+  // Linv(J)^T to the panel.
   const int cp = cpos(lane);
   for (int J = 0; J < T; J++) {
-    // C(I,J) = A(I,J) - sum_{k<J} L(I,k) L(J,k)^T for I >= J; warp w owns I = J + w, J + w + 8
-    for (int I = J + warp; I < T; I += NW) {
-      double *tc = sL + tix(I, J) * 64;
+    const double *tJ = sL + tix(J, 0) * 64;
+    if (warp == 0) {
+      double *tc = sL + tix(J, J) * 64;
       double d0 = tc[cp], d1 = tc[cp + 1], e0 = 0.0, e1 = 0.0;
-      const double *tI = sL + tix(I, 0) * 64, *tJ = sL + tix(J, 0) * 64;
       int k = 0;
       for (; k + 1 < J; k += 2) {
-        dmma(d0, d1, -tI[k * 64 + lane], tJ[k * 64 + lane]);
-        dmma(e0, e1, -tI[(k + 1) * 64 + lane], tJ[(k + 1) * 64 + lane]);
-        dmma(d0, d1, -tI[k * 64 + 32 + lane], tJ[k * 64 + 32 + lane]);
-        dmma(e0, e1, -tI[(k + 1) * 64 + 32 + lane], tJ[(k + 1) * 64 + 32 + lane]);
+        dmma(d0, d1, -tJ[k * 64 + lane], tJ[k * 64 + lane]);
+        dmma(e0, e1, -tJ[(k + 1) * 64 + lane], tJ[(k + 1) * 64 + lane]);
+        dmma(d0, d1, -tJ[k * 64 + 32 + lane], tJ[k * 64 + 32 + lane]);
+        dmma(e0, e1, -tJ[(k + 1) * 64 + 32 + lane], tJ[(k + 1) * 64 + 32 + lane]);
       }
       if (k < J) {
-        dmma(d0, d1, -tI[k * 64 + lane], tJ[k * 64 + lane]);
-        dmma(e0, e1, -tI[k * 64 + 32 + lane], tJ[k * 64 + 32 + lane]);
+        dmma(d0, d1, -tJ[k * 64 + lane], tJ[k * 64 + lane]);
+        dmma(e0, e1, -tJ[k * 64 + 32 + lane], tJ[k * 64 + 32 + lane]);
       }
+      __syncwarp();
       tc[cp] = d0 + e0; tc[cp + 1] = d1 + e1;
+      __syncwarp();
+      potrf8(tc, sLi + J * 64, sdiag + 8 * J, &bad);
+    } else {
+      for (int I = J + warp; I < T; I += NW - 1) {
+        double *tc = sL + tix(I, J) * 64;
+        double d0 = tc[cp], d1 = tc[cp + 1], e0 = 0.0, e1 = 0.0;
+        const double *tI = sL + tix(I, 0) * 64;
+        int k = 0;
+        for (; k + 1 < J; k += 2) {
+          dmma(d0, d1, -tI[k * 64 + lane], tJ[k * 64 + lane]);
+          dmma(e0, e1, -tI[(k + 1) * 64 + lane], tJ[(k + 1) * 64 + lane]);
+          dmma(d0, d1, -tI[k * 64 + 32 + lane], tJ[k * 64 + 32 + lane]);
+          dmma(e0, e1, -tI[(k + 1) * 64 + 32 + lane], tJ[(k + 1) * 64 + 32 + lane]);
+        }
+        if (k < J) {
+          dmma(d0, d1, -tI[k * 64 + lane], tJ[k * 64 + lane]);
+          dmma(e0, e1, -tI[k * 64 + 32 + lane], tJ[k * 64 + 32 + lane]);
+        }
+        tc[cp] = d0 + e0; tc[cp + 1] = d1 + e1;
+      }
     }
-    __syncthreads();
-    if (warp == 0) potrf8(sL + tix(J, J) * 64, sLi + J * 64, sdiag + 8 * J, &bad);
     __syncthreads();
     // panel: L(I,J) = C(I,J) Linv(J)^T for I > J
     const double *Li = sLi + J * 64;
@@ -266,9 +303,7 @@ __global__ void __launch_bounds__(NTH, 1) k_leaf_factor_mma(LeafMmaCtx c) {
   const int kend = (m + 7) & ~7;
   const int g = lane >> 2, tq = lane & 3;
   for (int blk = warp; blk < nblk; blk += NW) {
-    int BI = 0;
-    while ((BI + 1) * (BI + 2) / 2 <= blk) BI++;
-    const int BJ = blk - BI * (BI + 1) / 2;
+    const int BI = c_tileI[blk], BJ = c_tileJ[blk];
     double acc0[4] = {0, 0, 0, 0}, acc1[4] = {0, 0, 0, 0};
     const double *pa0 = sZ + (16 * BI + g) * LDR + tq;
     const double *pa1 = pa0 + 8 * LDR;
@@ -306,6 +341,15 @@ hodlr_status hodlr_leaf_factor_mma(hodlr_s *h, int K, double *Pi_leaf, bool *use
   int maxsm = 0;
   HCUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
   if (smem + 64 > (size_t)maxsm) return HODLR_OK;
+  static bool tables = false;
+  if (!tables) {
+    unsigned char ti[136], tj[136];
+    int q = 0;
+    for (int I = 0; I < 16; I++) for (int J = 0; J <= I; J++) { ti[q] = (unsigned char)I; tj[q] = (unsigned char)J; q++; }
+    HCUDA(cudaMemcpyToSymbol(c_tileI, ti, sizeof(ti)));
+    HCUDA(cudaMemcpyToSymbol(c_tileJ, tj, sizeof(tj)));
+    tables = true;
+  }
   LeafMmaCtx c;
   c.kp = h->kp; c.n = h->n; c.ninternal = h->ninternal; c.kappa = h->kappa; c.K = K; c.Kp = Kp; c.Kz = Kz;
   c.xs = h->xs; c.lo = h->lo; c.hi = h->hi; c.Xh = h->Xh; c.rank = h->rank; c.dt = h->d_dt;

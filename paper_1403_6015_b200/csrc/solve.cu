@@ -252,7 +252,7 @@ __device__ void dd_solve_warp(const double *S0, const double *LU, const double *
 }
 
 __global__ void __launch_bounds__(ST) k_tree_up(SolveCtx c, int d) {
-  __shared__ double sv[NWS][4][QMAX];
+  extern __shared__ double dsm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const long long i = (long long)blockIdx.x * NWS + wid;
   if (i >= (1LL << d)) return;
@@ -260,11 +260,12 @@ __global__ void __launch_bounds__(ST) k_tree_up(SolveCtx c, int d) {
   const int r = c.dt->rdep[d + 1], q = 2 * r, Kd = c.dt->Kdim[d], K1 = c.dt->Kdim[d + 1];
   const double *g1 = c.V + c.dt->nodeV[d + 1] + (2 * i) * (long long)K1;
   const double *g2 = g1 + K1;
-  const double *S0 = c.Spool + c.dt->nodeS[d] + i * (long long)(2 * q * q + q);
-  const double *LU = S0 + q * q;
-  const double *pivd = LU + q * q;
+  const double *Sg = c.Spool + c.dt->nodeS[d] + i * (long long)(2 * q * q + q);
   const double *B = c.BTpool + c.dt->nodeBT[d] + i * 3LL * q * Kd;
-  double *rhs = sv[wid][0], *th = sv[wid][1], *tl = sv[wid][2], *tmp = sv[wid][3];
+  // per-warp staging: S0, LU, pivots, rhs, th, tl, tmp (global latency stays out of the sequential solves)
+  double *S0 = dsm + (long long)wid * (2 * q * q + 5 * q);
+  double *LU = S0 + q * q, *pivd = LU + q * q, *rhs = pivd + q, *th = rhs + q, *tl = th + q, *tmp = tl + q;
+  for (int p = lane; p < 2 * q * q + q; p += 32) S0[p] = Sg[p];
   for (int u = lane; u < r; u += 32) { rhs[u] = g2[Kd + u]; rhs[r + u] = g1[Kd + u]; }
   __syncwarp();
   dd_solve_warp(S0, LU, pivd, q, rhs, th, tl, tmp, lane);
@@ -282,7 +283,9 @@ __global__ void __launch_bounds__(ST) k_tree_up(SolveCtx c, int d) {
   for (int a = lane; a < Kd; a += 32) {
     Acc2 A = acc2(g1[a]);
     acc_add(A, g2[a]);
+#pragma unroll 4
     for (int u = 0; u < r; u++) acc_fma_dd(A, -B[(long long)(r + u) * Kd + a], th[u], tl[u]);
+#pragma unroll 4
     for (int u = 0; u < r; u++) acc_fma_dd(A, -B[(long long)u * Kd + a], th[r + u], tl[r + u]);
     gc[a] = acc_val(A);
   }
@@ -303,6 +306,7 @@ __global__ void __launch_bounds__(ST) k_tree_down(SolveCtx c, int d) {
   for (int u = lane; u < q; u += 32) {
     Acc2 A = acc2(tg[u]);
     A.c += tg[q + u];
+#pragma unroll 8
     for (int a = 0; a < Kd; a++) acc_fma_dd(A, wc[a], Th[(long long)u * Kd + a], Tl[(long long)u * Kd + a]);
     f[u] = acc_val(A);
   }
@@ -342,8 +346,15 @@ hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_on
   HLAUNCH(h, "k_leaf_up");
   ph_end(h, PH_SLEAF_UP);
   ph_begin(h, PH_STREE);
+  size_t up_smem_max = 0;
+  for (int d = 0; d < kappa; d++) {
+    const size_t q = 2 * (size_t)dt.rdep[d + 1];
+    up_smem_max = std::max(up_smem_max, sizeof(double) * NWS * (2 * q * q + 5 * q));
+  }
+  if (kappa > 0) HCUDA(cudaFuncSetAttribute(k_tree_up, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)up_smem_max));
   for (int d = kappa - 1; d >= 0; d--) {
-    k_tree_up<<<(int)(((1LL << d) + NWS - 1) / NWS), ST, 0, h->st>>>(c, d);
+    const size_t q = 2 * (size_t)dt.rdep[d + 1];
+    k_tree_up<<<(int)(((1LL << d) + NWS - 1) / NWS), ST, sizeof(double) * NWS * (2 * q * q + 5 * q), h->st>>>(c, d);
     HLAUNCH(h, "k_tree_up");
   }
   if (up_only) { ph_end(h, PH_STREE); return HODLR_OK; }
