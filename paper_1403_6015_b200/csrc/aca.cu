@@ -2,88 +2,24 @@
 // concurrently (sec. 3.1; concrete pivot/stop rules DESIGN.md R1-R4, R12, R16).
 //
 // For internal node b with children c1 (rows) and c2 (columns) the block A = K[c1, c2] is
-// approximated by sum_k U'[:,k] V'[:,k]^T.  One ACA step k is two grid-wide passes over ALL
-// active blocks of ALL depths (one CTA per <= 128-chunk of a block side):
+// approximated by sum_k U'[:,k] V'[:,k]^T.  Blocks with both sides <= ACA_FUSED_MAX run every step
+// in one CTA (k_aca_fused).  For the bigger blocks one ACA step k is two grid-wide passes over ALL
+// active big blocks of ALL depths (k_aca_pass<row>, k_aca_pass<col>; one CTA per chunk of a side):
 //   row pass : v~_j = k(x_ik - x_j) - sum_{l<k} U'[ik,l] V'[j,l]  for j in c2; V'[:,k] = v~;
 //              argmax |v~_j| over unused columns; dots V'_l . v~ ; ||v~||^2
 //   col pass : u_i = (k(x_i - x_jk) - sum_{l<k} V'[jk,l] U'[i,l]) / v~_jk for i in c1; U'[:,k] = u;
 //              argmax |u_i| over unused rows; dots U'_l . u ; ||u||^2
 // The last CTA of each block to finish a pass reduces the per-CTA records in a fixed order
 // (deterministic) and advances the block state (pivot, ||S||_F^2 update, stop test).
-// The previous factor columns of the CTA's chunk are staged in shared memory once per sub-tile
-// and reused for the residual and for the dot products.
+// The previous factor columns are streamed once; the dot products come from F_l . a and the
+// running Gram matrix of the factor columns (see k_aca_pass).
 #include "hodlr_internal.cuh"
 #include <vector>
 #include <algorithm>
+#include <stdlib.h>
 
 namespace {
 
-__device__ __forceinline__ void cp_async8(double *dst_smem, const double *src) {
-  unsigned sa = (unsigned)__cvta_generic_to_shared(dst_smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" :: "r"(sa), "l"(src));
-}
-
-// ---------------------------------------------------------------------------------------------
-// shared reduction of the per-thread candidates + per-warp dot accumulators into one record
-// ---------------------------------------------------------------------------------------------
-__device__ void block_record(double best_abs, long long best_idx, double best_val, double nrm2,
-                             const double *acc /*[8]*/, int k, double *rec) {
-  __shared__ double s_abs[ACA_SUB / 32], s_val[ACA_SUB / 32], s_n2[ACA_SUB / 32];
-  __shared__ long long s_idx[ACA_SUB / 32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    double a2 = __shfl_down_sync(0xffffffffu, best_abs, o);
-    long long i2 = __shfl_down_sync(0xffffffffu, best_idx, o);
-    double v2 = __shfl_down_sync(0xffffffffu, best_val, o);
-    if (amax_better(best_abs, best_idx, a2, i2)) { best_abs = a2; best_idx = i2; best_val = v2; }
-    nrm2 += __shfl_down_sync(0xffffffffu, nrm2, o);
-  }
-  // per-warp dot partials: warp w owns l = w + 8 s
-  for (int s = 0; s < 8; s++) {
-    int l = warp + 8 * s;
-    double v = warp_sum(acc[s]);
-    if (lane == 0 && l < k) rec[4 + l] = v;
-  }
-  if (lane == 0) { s_abs[warp] = best_abs; s_idx[warp] = best_idx; s_val[warp] = best_val; s_n2[warp] = nrm2; }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double ba = s_abs[0], bv = s_val[0], n2 = s_n2[0]; long long bi = s_idx[0];
-    for (int w = 1; w < ACA_SUB / 32; w++) {
-      if (amax_better(ba, bi, s_abs[w], s_idx[w])) { ba = s_abs[w]; bi = s_idx[w]; bv = s_val[w]; }
-      n2 += s_n2[w];
-    }
-    rec[0] = ba; rec[1] = (double)bi; rec[2] = bv; rec[3] = n2;
-  }
-}
-
-// Reduce the nq records of a block in fixed order.  Results in shared out[]: [0] abs [1] idx [2] val
-// [3] nrm2 [4+l] dots.  Called by all threads of the last CTA.
-__device__ void reduce_records(const double *rec0, int nq, int k, double *out) {
-  __shared__ double s_abs[ACA_SUB], s_val[ACA_SUB];
-  __shared__ long long s_idx[ACA_SUB];
-  const int t = threadIdx.x;
-  double ba = 0.0, bv = 0.0; long long bi = -1;
-  for (int q = t; q < nq; q += ACA_SUB) {
-    const double *r = rec0 + (long long)q * ACA_RECW;
-    double a = __ldcg(r + 0); long long i = (long long)__ldcg(r + 1);
-    if (amax_better(ba, bi, a, i)) { ba = a; bi = i; bv = __ldcg(r + 2); }
-  }
-  s_abs[t] = ba; s_idx[t] = bi; s_val[t] = bv;
-  // sums: thread j (j <= k) sums column (3 + j) over q in order; j = 0 -> nrm2, j >= 1 -> dot l = j - 1
-  if (t <= k) {
-    double s = 0.0;
-    for (int q = 0; q < nq; q++) s += __ldcg(rec0 + (long long)q * ACA_RECW + 3 + t);
-    out[3 + t] = s;
-  }
-  __syncthreads();
-  if (t == 0) {
-    for (int j = 1; j < ACA_SUB; j++)
-      if (amax_better(ba, bi, s_abs[j], s_idx[j])) { ba = s_abs[j]; bi = s_idx[j]; bv = s_val[j]; }
-    out[0] = ba; out[1] = (double)bi; out[2] = bv;
-  }
-  __syncthreads();
-}
 
 // Rows with the same coordinate as a used pivot row have identical residual rows: mark the whole
 // run of equal sorted coordinates inside c1 as used (R2).  Single thread.
@@ -110,189 +46,13 @@ __global__ void k_aca_init(AcaCtx c, int nblocks, int cap) {
   c.rank[b] = 0;
 }
 
-// Row pass: one CTA per (block, chunk of c2).
-__global__ void __launch_bounds__(ACA_SUB) k_aca_row(AcaCtx c) {
-  extern __shared__ double sm[];
-  const AcaItem it = c.items[blockIdx.x];
-  const int b = it.block;
-  AcaState *st = &c.st[b];
-  if (st->done) return;
-  const int k = st->k;
-  const long long n = c.n;
-  const long long c1 = 2LL * b + 1, c2 = 2LL * b + 2;
-  const long long lo1 = c.lo[c1], lo2 = c.lo[c2], m2 = c.hi[c2] - lo2;
-  const int e = c.bdepth[b] + 1;
-  double *slot = c.Xh + c.dt->colbase[e] * n;
-  const unsigned char *used = c.used + (long long)(e - 1) * n;
-  const long long ig = lo1 + st->ipiv;
-  const double xi = c.xs[ig];
-  __shared__ double Ui[ACA_MAXCAP];
-  double *Vs = sm;                       // [k][ACA_SUB]
-  double *vb = sm + (long long)k * ACA_SUB;
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  for (int l = t; l < k; l += ACA_SUB) Ui[l] = slot[(long long)l * n + ig];
-  double acc[8];
+__device__ __forceinline__ double warp_allsum(double v) {   // xor butterfly: every lane gets the same bits
 #pragma unroll
-  for (int s = 0; s < 8; s++) acc[s] = 0.0;
-  double best_abs = 0.0, best_val = 0.0, nrm2 = 0.0; long long best_idx = -1;
-  __syncthreads();
-  for (long long s0 = it.start; s0 < it.start + it.len; s0 += ACA_SUB) {
-    const long long j = s0 + t;
-    const bool valid = j < it.start + it.len && j < m2;
-    const long long gj = lo2 + j;
-    double v = 0.0;
-    if (valid) {
-      const double *src = slot + gj;
-      for (int l = 0; l < k; l++) cp_async8(Vs + l * ACA_SUB + t, src + (long long)l * n);   // all k loads in flight
-      asm volatile("cp.async.commit_group;\n" ::);
-      v = kval(c.kp, xi - c.xs[gj]);
-      asm volatile("cp.async.wait_group 0;\n" ::);
-      for (int l = 0; l < k; l++) v -= Ui[l] * Vs[l * ACA_SUB + t];
-      slot[(long long)k * n + gj] = v;                  // V'[:,k] = raw residual row
-      if (!used[gj] && amax_better(best_abs, best_idx, fabs(v), j)) { best_abs = fabs(v); best_idx = j; best_val = v; }
-      nrm2 += v * v;
-    } else {
-      for (int l = 0; l < k; l++) Vs[l * ACA_SUB + t] = 0.0;
-    }
-    vb[t] = v;
-    __syncthreads();
-#pragma unroll
-    for (int s = 0; s < 8; s++) {
-      int l = warp + 8 * s;
-      if (l < k) {
-        double a = 0.0;
-        for (int q = lane; q < ACA_SUB; q += 32) a += Vs[l * ACA_SUB + q] * vb[q];
-        acc[s] += a;
-      }
-    }
-    __syncthreads();
-  }
-  const int nq = c.nq[b];
-  double *rec0 = c.rec + c.recbase[b] * ACA_RECW;
-  block_record(best_abs, best_idx, best_val, nrm2, acc, k, rec0 + (long long)it.q * ACA_RECW);
-  __shared__ int amLast;
-  __threadfence();
-  __syncthreads();
-  if (t == 0) amLast = (atomicAdd(&st->cnt_r, 1) == nq - 1);
-  __syncthreads();
-  if (!amLast) return;
-  __threadfence();
-  __shared__ double out[4 + ACA_MAXCAP];
-  reduce_records(rec0, nq, k, out);
-  if (t < k) st->dV[t] = out[4 + t];
-  if (t == 0) {
-    st->cnt_r = 0;
-    long long jk = (long long)out[1];
-    if (jk < 0 || out[0] == 0.0) {                      // exactly-zero residual row: rank k
-      st->done = 1; c.rank[b] = k; atomicSub(c.active, 1);
-    } else {
-      st->jpiv = jk; st->pivval = out[2]; st->nv2 = out[3];
-      c.used[(long long)(e - 1) * n + lo2 + jk] = 1;
-    }
-  }
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
 }
 
-// Column pass: one CTA per (block, chunk of c1).
-__global__ void __launch_bounds__(ACA_SUB) k_aca_col(AcaCtx c, int *flags) {
-  extern __shared__ double sm[];
-  const AcaItem it = c.items[blockIdx.x];
-  const int b = it.block;
-  AcaState *st = &c.st[b];
-  if (st->done) return;
-  const int k = st->k;
-  const long long n = c.n;
-  const long long c1 = 2LL * b + 1, c2 = 2LL * b + 2;
-  const long long lo1 = c.lo[c1], m1 = c.hi[c1] - lo1, lo2 = c.lo[c2], m2 = c.hi[c2] - lo2;
-  const int e = c.bdepth[b] + 1;
-  double *slot = c.Xh + c.dt->colbase[e] * n;
-  const unsigned char *used = c.used + (long long)(e - 1) * n;
-  const long long jg = lo2 + st->jpiv;
-  const double xj = c.xs[jg];
-  const double rp = 1.0 / st->pivval;
-  __shared__ double Vj[ACA_MAXCAP];
-  double *Us = sm;
-  double *ub = sm + (long long)k * ACA_SUB;
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  for (int l = t; l < k; l += ACA_SUB) Vj[l] = slot[(long long)l * n + jg];
-  double acc[8];
-#pragma unroll
-  for (int s = 0; s < 8; s++) acc[s] = 0.0;
-  double best_abs = 0.0, best_val = 0.0, nrm2 = 0.0; long long best_idx = -1;
-  __syncthreads();
-  for (long long s0 = it.start; s0 < it.start + it.len; s0 += ACA_SUB) {
-    const long long i = s0 + t;
-    const bool valid = i < it.start + it.len && i < m1;
-    const long long gi = lo1 + i;
-    double u = 0.0;
-    if (valid) {
-      const double *src = slot + gi;
-      for (int l = 0; l < k; l++) cp_async8(Us + l * ACA_SUB + t, src + (long long)l * n);
-      asm volatile("cp.async.commit_group;\n" ::);
-      u = kval(c.kp, c.xs[gi] - xj);
-      asm volatile("cp.async.wait_group 0;\n" ::);
-      for (int l = 0; l < k; l++) u -= Vj[l] * Us[l * ACA_SUB + t];
-      u *= rp;
-      slot[(long long)k * n + gi] = u;                  // U'[:,k] = column residual / pivot
-      if (!used[gi] && amax_better(best_abs, best_idx, fabs(u), i)) { best_abs = fabs(u); best_idx = i; best_val = u; }
-      nrm2 += u * u;
-    } else {
-      for (int l = 0; l < k; l++) Us[l * ACA_SUB + t] = 0.0;
-    }
-    ub[t] = u;
-    __syncthreads();
-#pragma unroll
-    for (int s = 0; s < 8; s++) {
-      int l = warp + 8 * s;
-      if (l < k) {
-        double a = 0.0;
-        for (int q = lane; q < ACA_SUB; q += 32) a += Us[l * ACA_SUB + q] * ub[q];
-        acc[s] += a;
-      }
-    }
-    __syncthreads();
-  }
-  const int nq = c.nq[b];
-  double *rec0 = c.rec + c.recbase[b] * ACA_RECW;
-  block_record(best_abs, best_idx, best_val, nrm2, acc, k, rec0 + (long long)it.q * ACA_RECW);
-  __shared__ int amLast;
-  __threadfence();
-  __syncthreads();
-  if (t == 0) amLast = (atomicAdd(&st->cnt_c, 1) == nq - 1);
-  __syncthreads();
-  if (!amLast) return;
-  __threadfence();
-  __shared__ double out[4 + ACA_MAXCAP];
-  reduce_records(rec0, nq, k, out);
-  if (t == 0) {
-    st->cnt_c = 0;
-    // ||S_{k+1}||^2 = ||S_k||^2 + 2 sum_{l<k} (U'_k.U'_l)(V'_l.V'_k) + ||U'_k||^2 ||V'_k||^2
-    double cross = 0.0;
-    for (int l = 0; l < k; l++) cross += out[4 + l] * st->dV[l];
-    const double nu2 = out[3], nv2 = st->nv2;
-    const double S2 = st->S2 + 2.0 * cross + nu2 * nv2;
-    st->S2 = S2;
-    const int k1 = k + 1;
-    st->k = k1;
-    const long long mn = m1 < m2 ? m1 : m2;
-    int done = 0;
-    if (sqrt(nu2) * sqrt(nv2) <= c.eps * sqrt(fabs(S2))) done = 1;     // stop term is kept
-    else if (k1 == mn) done = 1;
-    else if (k1 == st->cap) { done = 2; atomicAdd(&flags[5], 1); }
-    else {
-      long long ik = (long long)out[1];
-      if (ik < 0 || out[0] == 0.0) done = 1;
-      else { st->ipiv = ik; mark_row_run(c, c.used + (long long)(e - 1) * n, lo1, m1, ik); }
-    }
-    if (done) { st->done = done; c.rank[b] = k1; atomicSub(c.active, 1); }
-  }
-}
-
-
-// ---------------------------------------------------------------------------------------------
-// Fused ACA for blocks with max(m1, m2) <= ACA_FUSED_MAX: one CTA runs every pivot step of one
-// block (same arithmetic and conventions as the row/column passes above, block-level reductions,
-// pivot bookkeeping in shared memory).  Runs concurrently with the step-synchronous big blocks.
-// ---------------------------------------------------------------------------------------------
+// Block-wide argmax (ties -> smallest index) + sum of nrm2; result broadcast to every thread.
 __device__ __forceinline__ void block_argmax_n2(double &ba, long long &bi, double &bv, double &n2,
                                                 double *s_abs, long long *s_idx, double *s_val, double *s_n2) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -314,8 +74,189 @@ __device__ __forceinline__ void block_argmax_n2(double &ba, long long &bi, doubl
   }
   __syncthreads();
   ba = s_abs[0]; bi = s_idx[0]; bv = s_val[0]; n2 = s_n2[0];
+  __syncthreads();
 }
 
+// ---------------------------------------------------------------------------------------------
+// Step-synchronous pass over the big blocks.  ROW: elements j of c2 for the pivot row i_k,
+//   a_j = k(x_ik - x_j),  v~_j = a_j - sum_l U'[ik,l] V'[j,l]  -> V'[:,k]
+// COL: elements i of c1 for the pivot column j_k,
+//   a_i = k(x_i - x_jk), u_i = (a_i - sum_l V'[jk,l] U'[i,l]) / v~_jk  -> U'[:,k]
+// Each factor value is streamed once: the dot products F_l . r needed by the ||S_k||_F update are
+// formed as F_l . a - sum_m coef_m G[l,m] with the running Gram matrix G = F^T F of the previous
+// columns (kept per block), so no column has to be staged or re-read.  Per CTA: argmax over unused
+// indices, ||r||^2 and F_l . a for its chunk -> one record; the last CTA of a block reduces the
+// records in a fixed order (deterministic) and advances the block state.
+// ---------------------------------------------------------------------------------------------
+constexpr int ACA_E = 4;                       // elements per thread per sub-tile
+constexpr int ACA_TILE = ACA_SUB * ACA_E;
+
+template <bool ROW>
+__global__ void __launch_bounds__(ACA_SUB, 4) k_aca_pass(AcaCtx c, int *flags) {
+  const AcaItem it = c.items[blockIdx.x];
+  const int b = it.block;
+  AcaState *st = &c.st[b];
+  if (st->done) return;
+  const int k = st->k;
+  const long long n = c.n;
+  const long long c1 = 2LL * b + 1, c2 = 2LL * b + 2;
+  const long long lo1 = c.lo[c1], m1 = c.hi[c1] - lo1, lo2 = c.lo[c2], m2 = c.hi[c2] - lo2;
+  const int e = c.bdepth[b] + 1;
+  double *slot = c.Xh + c.dt->colbase[e] * n;
+  const unsigned char *used = c.used + (long long)(e - 1) * n;
+  const long long pg = ROW ? lo1 + st->ipiv : lo2 + st->jpiv;     // fixed row (ROW) / column (COL)
+  const double xp = c.xs[pg];
+  const long long lo = ROW ? lo2 : lo1;
+  const double scale = ROW ? 1.0 : 1.0 / st->pivval;
+  __shared__ double coef[ACA_MAXCAP];
+  __shared__ double sdot[ACA_SUB / 32][ACA_MAXCAP];
+  __shared__ double s_abs[ACA_SUB / 32], s_val[ACA_SUB / 32], s_n2[ACA_SUB / 32];
+  __shared__ long long s_idx[ACA_SUB / 32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  for (int l = t; l < k; l += ACA_SUB) coef[l] = slot[(long long)l * n + pg];
+  __syncthreads();
+  double w0 = 0.0, w1 = 0.0;                  // lane (l & 31) owns dot l: l < 32 in w0, l >= 32 in w1
+  double ba = 0.0, bv = 0.0, n2 = 0.0; long long bi = -1;
+  const long long end = it.start + it.len;
+  for (long long s0 = it.start; s0 < end; s0 += ACA_TILE) {
+    const long long g0 = lo + s0 + t;          // element q at g0 + q * ACA_SUB
+    const int nval = (int)min((long long)ACA_E, (end - s0 - t + ACA_SUB - 1) / ACA_SUB);   // valid elements
+    double a[ACA_E], r[ACA_E];
+#pragma unroll
+    for (int q = 0; q < ACA_E; q++) {
+      const double d = q < nval ? (ROW ? xp - c.xs[g0 + q * ACA_SUB] : c.xs[g0 + q * ACA_SUB] - xp) : 0.0;
+      a[q] = q < nval ? kval(c.kp, d) : 0.0;
+      r[q] = a[q];
+    }
+    constexpr int LS = 2;                      // factor columns per batch of loads
+    for (int l0 = 0; l0 < k; l0 += LS) {
+      double F[LS][ACA_E];
+#pragma unroll
+      for (int dl = 0; dl < LS; dl++) {
+        const double *col = slot + (long long)(l0 + dl) * n + g0;
+#pragma unroll
+        for (int q = 0; q < ACA_E; q++) F[dl][q] = (l0 + dl < k && q < nval) ? col[q * ACA_SUB] : 0.0;
+      }
+#pragma unroll
+      for (int dl = 0; dl < LS; dl++) {
+        const int l = l0 + dl;
+        if (l < k) {
+          const double cf = coef[l];
+          double p = 0.0;
+#pragma unroll
+          for (int q = 0; q < ACA_E; q++) { r[q] = fma(-cf, F[dl][q], r[q]); p = fma(F[dl][q], a[q], p); }
+          p = warp_allsum(p);
+          if (lane == (l & 31)) { if (l < 32) w0 += p; else w1 += p; }
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < ACA_E; q++) {
+      if (q >= nval) break;
+      const long long g = g0 + q * ACA_SUB;
+      const double v = r[q] * scale;
+      slot[(long long)k * n + g] = v;
+      if (!used[g] && amax_better(ba, bi, fabs(v), g - lo)) { ba = fabs(v); bi = g - lo; bv = v; }
+      n2 += v * v;
+    }
+  }
+  if (lane < k) sdot[warp][lane] = w0;
+  if (lane + 32 < k) sdot[warp][lane + 32] = w1;
+  block_argmax_n2(ba, bi, bv, n2, s_abs, s_idx, s_val, s_n2);
+  const int nq = c.nq[b];
+  double *rec0 = c.rec + c.recbase[b] * ACA_RECW;
+  double *rec = rec0 + (long long)it.q * ACA_RECW;
+  for (int l = t; l < k; l += ACA_SUB) {
+    double s = 0.0;
+    for (int w = 0; w < ACA_SUB / 32; w++) s += sdot[w][l];
+    rec[4 + l] = s;
+  }
+  if (t == 0) { rec[0] = ba; rec[1] = (double)bi; rec[2] = bv; rec[3] = n2; }
+  __shared__ int amLast;
+  __threadfence();
+  __syncthreads();
+  if (t == 0) amLast = (atomicAdd(ROW ? &st->cnt_r : &st->cnt_c, 1) == nq - 1);
+  __syncthreads();
+  if (!amLast) return;
+  __threadfence();
+  // ---- last CTA: reduce the nq records in a fixed order ----
+  ba = 0.0; bv = 0.0; bi = -1; n2 = 0.0;
+  for (int q = t; q < nq; q += ACA_SUB) {
+    const double *rq = rec0 + (long long)q * ACA_RECW;
+    const double aq = __ldcg(rq + 0); const long long iq = (long long)__ldcg(rq + 1);
+    if (amax_better(ba, bi, aq, iq)) { ba = aq; bi = iq; bv = __ldcg(rq + 2); }
+  }
+  __shared__ double part[ACA_SUB / 32][4 + ACA_MAXCAP];
+  {   // columns 3 (nrm2) .. 3 + k (dots): warp w sums records w, w + 8, ...; lane owns columns lane + 32 s
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int q = warp; q < nq; q += ACA_SUB / 32) {
+      const double *rq = rec0 + (long long)q * ACA_RECW + 3;
+#pragma unroll
+      for (int s = 0; s < 3; s++) if (lane + 32 * s <= k) acc[s] += __ldcg(rq + lane + 32 * s);
+    }
+#pragma unroll
+    for (int s = 0; s < 3; s++) if (lane + 32 * s <= k) part[warp][lane + 32 * s] = acc[s];
+  }
+  double dummy = 0.0;
+  block_argmax_n2(ba, bi, bv, dummy, s_abs, s_idx, s_val, s_n2);   // (syncs: part[] complete afterwards)
+  __shared__ double tot[1 + ACA_MAXCAP];
+  for (int cidx = t; cidx <= k; cidx += ACA_SUB) {
+    double s = 0.0;
+    for (int w = 0; w < ACA_SUB / 32; w++) s += part[w][cidx];
+    tot[cidx] = s;
+  }
+  __syncthreads();
+  const long long bidx = c.bigidx[b];
+  double *G = c.gram + bidx * (2LL * ACA_GSZ) + (ROW ? ACA_GSZ : 0);   // G_U then G_V
+  // dots with the new column: F_l . r = (F_l . a - sum_m coef_m G[l,m]) * scale
+  __shared__ double dnew[ACA_MAXCAP];
+  for (int l = t; l < k; l += ACA_SUB) {
+    double s = tot[1 + l];
+    for (int m = 0; m < k; m++) s = fma(-coef[m], __ldcg(G + pk(l, m)), s);
+    s *= scale;
+    dnew[l] = s;
+    G[pk(k, l)] = s;
+  }
+  __syncthreads();
+  if (t == 0) {
+    const double nr2 = tot[0];
+    G[pk(k, k)] = nr2;
+    if (ROW) {
+      for (int l = 0; l < k; l++) st->dV[l] = dnew[l];
+      st->cnt_r = 0;
+      if (bi < 0 || ba == 0.0) {                          // exactly-zero residual row: rank k
+        st->done = 1; c.rank[b] = k; atomicSub(c.active, 1);
+      } else {
+        st->jpiv = bi; st->pivval = bv; st->nv2 = nr2;
+        c.used[(long long)(e - 1) * n + lo2 + bi] = 1;
+      }
+    } else {
+      st->cnt_c = 0;
+      // ||S_{k+1}||^2 = ||S_k||^2 + 2 sum_{l<k} (U'_k.U'_l)(V'_l.V'_k) + ||U'_k||^2 ||V'_k||^2
+      double cross = 0.0;
+      for (int l = 0; l < k; l++) cross += dnew[l] * st->dV[l];
+      const double nu2 = nr2, nv2 = st->nv2;
+      const double S2 = st->S2 + 2.0 * cross + nu2 * nv2;
+      st->S2 = S2;
+      const int k1 = k + 1;
+      st->k = k1;
+      const long long mn = m1 < m2 ? m1 : m2;
+      int done = 0;
+      if (sqrt(nu2) * sqrt(nv2) <= c.eps * sqrt(fabs(S2))) done = 1;     // stop term is kept
+      else if (k1 == mn) done = 1;
+      else if (k1 == st->cap) { done = 2; atomicAdd(&flags[5], 1); }
+      else if (bi < 0 || ba == 0.0) done = 1;
+      else { st->ipiv = bi; mark_row_run(c, c.used + (long long)(e - 1) * n, lo1, m1, bi); }
+      if (done) { st->done = done; c.rank[b] = k1; atomicSub(c.active, 1); }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Fused ACA for blocks with max(m1, m2) <= ACA_FUSED_MAX: one CTA runs every pivot step of one
+// block (same arithmetic and conventions as the row/column passes above, block-level reductions,
+// pivot bookkeeping in shared memory).  Runs concurrently with the step-synchronous big blocks.
+// ---------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(ACA_SUB) k_aca_fused(AcaCtx c, const int *blocks, int *flags) {
   __shared__ double vbuf[ACA_FUSED_MAX];
   __shared__ unsigned char usedR[ACA_FUSED_MAX], usedC[ACA_FUSED_MAX];
@@ -449,16 +390,18 @@ hodlr_status hodlr_aca(hodlr_s *h) {
   std::vector<int> bdepth(nb);
   long long nrec_r = 0, nrec_c = 0;
   std::vector<int> fused_blocks;
+  std::vector<int> bigidx(nb, -1);
   int nbig = 0;
   for (long long b = 0; b < nb; b++) {
     bdepth[b] = hodlr_depth_of(b);
     long long m1 = h->h_hi[2 * b + 1] - h->h_lo[2 * b + 1], m2 = h->h_hi[2 * b + 2] - h->h_lo[2 * b + 2];
     if (std::max(m1, m2) <= ACA_FUSED_MAX) { fused_blocks.push_back((int)b); nq_r[b] = nq_c[b] = 0; rb_r[b] = rb_c[b] = 0; continue; }
+    bigidx[b] = nbig;
     nbig++;
     for (int side = 0; side < 2; side++) {
       long long m = side == 0 ? m2 : m1;
       long long chunk = (m + 127) / 128;
-      chunk = ((chunk + ACA_SUB - 1) / ACA_SUB) * ACA_SUB;
+      chunk = ((chunk + ACA_TILE - 1) / ACA_TILE) * ACA_TILE;
       if (chunk < ACA_BIG_CHUNK) chunk = ACA_BIG_CHUNK;
       int q = 0;
       for (long long s = 0; s < m; s += chunk, q++) {
@@ -480,6 +423,9 @@ hodlr_status hodlr_aca(hodlr_s *h) {
   h->rank = (int *)hodlr_dalloc(h, sizeof(int) * nb);
   h->bdepth = (int *)hodlr_dalloc(h, sizeof(int) * nb);
   h->used = (unsigned char *)hodlr_dalloc(h, (size_t)h->kappa * n);
+  int *d_bigidx = (int *)hodlr_dalloc(h, sizeof(int) * nb);
+  double *d_gram = (double *)hodlr_dalloc(h, sizeof(double) * 2 * ACA_GSZ * (size_t)(nbig > 0 ? nbig : 1));
+  if (!d_bigidx || !d_gram) return hodlr_set_error(HODLR_ENOMEM, "aca: device allocation failed");
   if (!d_items_r || !d_items_c || !d_fused || !d_nq || !d_rb || !d_rec || !h->ast || !h->rank || !h->bdepth || !h->used)
     return hodlr_set_error(HODLR_ENOMEM, "aca: device allocation failed");
   std::vector<int> nq_all(nq_r); nq_all.insert(nq_all.end(), nq_c.begin(), nq_c.end());
@@ -490,6 +436,7 @@ hodlr_status hodlr_aca(hodlr_s *h) {
   HCUDA(cudaMemcpyAsync(d_nq, nq_all.data(), sizeof(int) * 2 * nb, cudaMemcpyHostToDevice, h->st));
   HCUDA(cudaMemcpyAsync(d_rb, rb_all.data(), sizeof(long long) * 2 * nb, cudaMemcpyHostToDevice, h->st));
   HCUDA(cudaMemcpyAsync(h->bdepth, bdepth.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, h->st));
+  HCUDA(cudaMemcpyAsync(d_bigidx, bigidx.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, h->st));
   HCUDA(cudaMemsetAsync(h->used, 0, (size_t)h->kappa * n, h->st));
   HCUDA(cudaMemcpyAsync(h->dflags + 4, &nbig, sizeof(int), cudaMemcpyHostToDevice, h->st));
   // the pageable copies above are staged synchronously by the runtime, so the vectors may die
@@ -497,7 +444,7 @@ hodlr_status hodlr_aca(hodlr_s *h) {
   AcaCtx c;
   c.kp = h->kp; c.n = n; c.eps = h->eps; c.xs = h->xs; c.lo = h->lo; c.hi = h->hi; c.Xh = h->Xh;
   c.used = h->used; c.st = h->ast; c.active = h->dflags + 4; c.rank = h->rank; c.bdepth = h->bdepth;
-  c.dt = h->d_dt;
+  c.dt = h->d_dt; c.bigidx = d_bigidx; c.gram = d_gram;
   ph_begin(h, PH_ACA);
   k_aca_init<<<(int)((nb + 255) / 256), 256, 0, h->st>>>(c, (int)nb, h->cap);
   HLAUNCH(h, "k_aca_init");
@@ -515,15 +462,24 @@ hodlr_status hodlr_aca(hodlr_s *h) {
   cc.items = d_items_c; cc.nq = d_nq + nb; cc.recbase = d_rb + nb; cc.rec = d_rec + ACA_RECW * nrec_r;
   // big blocks: the pivot-step loop runs on the device as a conditional-while CUDA graph
   // (row pass, column pass, loop test) -- no host polling between steps
-  const size_t smem = (size_t)(h->cap + 1) * ACA_SUB * sizeof(double);
-  static int attr_bytes = 0;
-  if ((int)smem > attr_bytes) {
-    HCUDA(cudaFuncSetAttribute(k_aca_row, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    HCUDA(cudaFuncSetAttribute(k_aca_col, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_bytes = (int)smem;
-  }
   hodlr_status status = HODLR_OK;
   int steps = 0;
+  static int nograph = -1;     // HODLR_ACA_NOGRAPH=1: host-driven step loop (profilers see every launch)
+  if (nograph < 0) { const char *ev = getenv("HODLR_ACA_NOGRAPH"); nograph = ev && atoi(ev) ? 1 : 0; }
+  if (nbig > 0 && nograph) {
+    int *flags = h->dflags;
+    for (steps = 1; steps <= h->cap + 1; steps++) {
+      k_aca_pass<true><<<(unsigned)items_r.size(), ACA_SUB, 0, h->st>>>(cr, flags);
+      HLAUNCH(h, "k_aca_pass<row>");
+      k_aca_pass<false><<<(unsigned)items_c.size(), ACA_SUB, 0, h->st>>>(cc, flags);
+      HLAUNCH(h, "k_aca_pass<col>");
+      int act = 0;
+      HCUDA(cudaMemcpyAsync(&act, h->dflags + 4, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+      HCUDA(cudaStreamSynchronize(h->st));
+      if (act <= 0) break;
+    }
+    nbig = 0;
+  }
   if (nbig > 0) {
     HCUDA(cudaMemsetAsync(h->dflags + 6, 0, sizeof(int), h->st));
     cudaGraph_t g = nullptr, body = nullptr;
@@ -540,21 +496,21 @@ hodlr_status hodlr_aca(hodlr_s *h) {
     }
     int *active = h->dflags + 4, *stepc = h->dflags + 6, *flags = h->dflags;
     int maxsteps = h->cap + 1;
-    void *arow[] = {&cr};
+    void *arow[] = {&cr, &flags};
     void *acol[] = {&cc, &flags};
     void *acond[] = {&hdl, &active, &stepc, &maxsteps};
     cudaGraphNode_t n1, n2, n3;
     if (e == cudaSuccess) {
       body = cpar.conditional.phGraph_out[0];
       cudaKernelNodeParams k1 = {};
-      k1.func = (void *)k_aca_row; k1.gridDim = dim3((unsigned)items_r.size()); k1.blockDim = dim3(ACA_SUB);
-      k1.sharedMemBytes = (unsigned)smem; k1.kernelParams = arow;
+      k1.func = (void *)k_aca_pass<true>; k1.gridDim = dim3((unsigned)items_r.size()); k1.blockDim = dim3(ACA_SUB);
+      k1.sharedMemBytes = 0; k1.kernelParams = arow;
       e = cudaGraphAddKernelNode(&n1, body, nullptr, 0, &k1);
     }
     if (e == cudaSuccess) {
       cudaKernelNodeParams k2 = {};
-      k2.func = (void *)k_aca_col; k2.gridDim = dim3((unsigned)items_c.size()); k2.blockDim = dim3(ACA_SUB);
-      k2.sharedMemBytes = (unsigned)smem; k2.kernelParams = acol;
+      k2.func = (void *)k_aca_pass<false>; k2.gridDim = dim3((unsigned)items_c.size()); k2.blockDim = dim3(ACA_SUB);
+      k2.sharedMemBytes = 0; k2.kernelParams = acol;
       e = cudaGraphAddKernelNode(&n2, body, &n1, 1, &k2);
     }
     if (e == cudaSuccess) {

@@ -161,12 +161,7 @@ hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const 
   CK(cudaMemcpyAsync(h->d_dt, &h->dt, sizeof(DepthTab), cudaMemcpyHostToDevice, h->st));
   st = hodlr_sort_and_tree(h, x);
   if (st != HODLR_OK) goto fail;
-  {
-    int f0 = 0;
-    CK(cudaMemcpyAsync(&f0, h->dflags, sizeof(int), cudaMemcpyDeviceToHost, h->st));
-    CK(cudaStreamSynchronize(h->st));
-    if (f0) { st = hodlr_set_error(HODLR_EINVAL, "build: x contains NaN or Inf"); goto fail; }
-  }
+  if (h->x_nonfinite) { st = hodlr_set_error(HODLR_EINVAL, "build: x contains NaN or Inf"); goto fail; }
   st = hodlr_aca(h);
   if (st != HODLR_OK) goto fail;
   {

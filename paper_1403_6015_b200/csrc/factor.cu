@@ -18,6 +18,7 @@
 // double-double pair and Pi_c is accumulated with compensated arithmetic.
 #include "hodlr_internal.cuh"
 #include <limits.h>
+#include <stdlib.h>
 
 namespace {
 
@@ -174,140 +175,224 @@ __global__ void __launch_bounds__(LT) k_leaf_factor(LeafCtx c) {
 
 struct TreeCtx {
   int d;                    // depth of the nodes of this launch
-  int r, q, Kd, K1;
+  int r, q, Kd, K1, ldk;    // ldk: row stride of B / T in shared memory (Kd rounded up to 4)
+  int dd;                   // compensated (double-double) T and Pi
   const double *Pi1;        // children Pi base (depth d+1), packed K1(K1+1)/2 per node
   double *Pic;              // this depth's Pi base, packed Kd(Kd+1)/2 per node
-  double *Sst;              // per node: S (q*q), LU(S) (q*q), pivots (q)
+  double *Sst;              // per node: S (q*q), S^{-1} (q*q), spare (q)
   double *BT;               // per node: B, T_hi, T_lo (q*Kd each)
   double *node_ld;
   int *flags;
 };
 
-// x <- S^{-1} x for one column with stride ld, using the LU factors and pivots
-__device__ __forceinline__ void lu_solve_col(const double *S, const int *piv, int q, double *x, int ld) {
-  for (int k = 0; k < q; k++) { int p = piv[k]; if (p != k) { double t = x[k * ld]; x[k * ld] = x[p * ld]; x[p * ld] = t; } }
-  for (int a = 0; a < q; a++) { double s = x[a * ld]; for (int k = 0; k < a; k++) s -= S[a * q + k] * x[k * ld]; x[a * ld] = s; }
-  for (int a = q - 1; a >= 0; a--) { double s = x[a * ld]; for (int k = a + 1; k < q; k++) s -= S[a * q + k] * x[k * ld]; x[a * ld] = s / S[a * q + a]; }
+// Shared-memory footprint of one node (doubles), see tree_node().
+__host__ __device__ __forceinline__ long long tree_smem_doubles(int q, int ldk) {
+  return 3LL * q * q + 5LL * q + 4LL * q * ldk;
 }
 
-// One CTA per depth-d node c: S_c, its LU and log det; T_c = S_c^{-1} B_c kept as a double-double
-// pair (double solve + two refinement steps with compensated residuals); Pi_c by a compensated
-// Schur update, rounded to double.
-__global__ void __launch_bounds__(TT) k_tree_factor(TreeCtx c) {
-  extern __shared__ double sm[];
-  __shared__ int pivs[2 * ACA_MAXCAP];
-  __shared__ int zero_piv, nref;
-  const int t = threadIdx.x;
-  const long long i = blockIdx.x;
+// One CTA per depth-d node c (heap index (2^d - 1) + i):
+//   S_c = [[I, Pi_c2[s,s]], [Pi_c1[s,s], I]]; Gauss-Jordan with partial pivoting (row of max |.|, first
+//   index on ties -- the same pivots and U_kk as the LU of the paper's coupling system) gives log|det S_c|,
+//   its sign and S_c^{-1};
+//   T_c = S_c^{-1} B_c, refined in compensated arithmetic (T = T_hi + T_lo);
+//   Pi_c = Pi_c1[a,a] + Pi_c2[a,a] - sum_u B_c[(u+r) mod q, a] T_c[u, b], 2x4 register tiles per thread.
+template <bool DD>
+__device__ void tree_node(const TreeCtx &c, long long i, double *sm) {
+  const int t = threadIdx.x, NT = blockDim.x;
   const long long node = (1LL << c.d) - 1 + i;
-  const int r = c.r, q = c.q, Kd = c.Kd;
+  const int r = c.r, q = c.q, Kd = c.Kd, ldk = c.ldk, q2 = 2 * q;
   const long long K1 = c.K1;
   const double *P1 = c.Pi1 + (2 * i) * (K1 * (K1 + 1) / 2);
   const double *P2 = c.Pi1 + (2 * i + 1) * (K1 * (K1 + 1) / 2);
-  const long long qK = (long long)q * Kd;
-  double *S0 = sm;                   // q x q original
-  double *S = S0 + q * q;            // q x q LU
-  double *B = S + q * q;             // q x Kd
-  double *Th = B + qK;               // q x Kd
-  double *Tl = Th + qK;              // q x Kd
-  double *R = Tl + qK;               // q x Kd residual scratch
-  for (int p = t; p < q * q; p += TT) {
-    int a = p / q, b = p - a * q;
-    double v = a == b ? 1.0 : 0.0;
-    if (a < r && b >= r) v = P2[pk(Kd + a, Kd + (b - r))];
-    if (a >= r && b < r) v = P1[pk(Kd + a - r, Kd + b)];
-    S0[p] = v; S[p] = v;
+  double *W = sm;                    // q x 2q  [S | I] -> [I | S^{-1}]
+  double *S0 = W + q * q2;           // q x q
+  double *rowk = S0 + q * q;         // 2q
+  double *rowold = rowk + q2;        // 2q
+  double *colk = rowold + q2;        // q
+  double *B = colk + q;              // q x ldk
+  double *Th = B + (long long)q * ldk;
+  double *Tl = Th + (long long)q * ldk;
+  double *R = Tl + (long long)q * ldk;
+  __shared__ int s_p, s_zero, s_sign, s_nref;
+  __shared__ double s_la, s_umax, s_umin;
+  for (int p = t; p < q * q2; p += NT) {
+    const int a = p / q2, b = p - a * q2;
+    double v;
+    if (b >= q) v = (b - q == a) ? 1.0 : 0.0;
+    else {
+      v = a == b ? 1.0 : 0.0;
+      if (a < r && b >= r) v = P2[pk(Kd + a, Kd + (b - r))];
+      if (a >= r && b < r) v = P1[pk(Kd + a - r, Kd + b)];
+      S0[a * q + b] = v;
+    }
+    W[p] = v;
   }
-  for (long long p = t; p < qK; p += TT) {
-    long long a = p / Kd, b = p - a * Kd;
-    double v = a < r ? P2[P(Kd + a, b)] : P1[P(Kd + a - r, b)];
-    B[p] = v; Th[p] = v; Tl[p] = 0.0;
+  for (long long p = t; p < (long long)q * ldk; p += NT) {
+    const int a = (int)(p / ldk), b = (int)(p - (long long)a * ldk);
+    double v = 0.0;
+    if (b < Kd) v = a < r ? P2[pk(Kd + a, b)] : P1[pk(Kd + a - r, b)];
+    B[p] = v; Tl[p] = 0.0;
   }
-  if (t == 0) zero_piv = 0;
+  if (t == 0) { s_zero = 0; s_sign = 1; s_la = 0.0; s_umax = 0.0; s_umin = 1e300; }
   __syncthreads();
-  // LU with partial pivoting (row of max |.|, first index on ties)
+  // ---------------- Gauss-Jordan with partial pivoting ----------------
   for (int k = 0; k < q; k++) {
     if (t < 32) {
       int p = k; double best = -1.0;
-      for (int a = k + t; a < q; a += 32) { double v = fabs(S[a * q + k]); if (v > best) { best = v; p = a; } }
+      for (int a = k + t; a < q; a += 32) { const double v = fabs(W[a * q2 + k]); if (v > best) { best = v; p = a; } }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
-        double b2 = __shfl_down_sync(0xffffffffu, best, o); int p2 = __shfl_down_sync(0xffffffffu, p, o);
+        const double b2 = __shfl_down_sync(0xffffffffu, best, o); const int p2 = __shfl_down_sync(0xffffffffu, p, o);
         if (b2 > best || (b2 == best && p2 < p)) { best = b2; p = p2; }
       }
-      if (t == 0) { pivs[k] = p; if (!(best > 0.0)) zero_piv = 1; }
+      if (t == 0) {
+        s_p = p;
+        const double u = W[p * q2 + k];
+        if (p != k) s_sign = -s_sign;
+        if (u < 0.0) s_sign = -s_sign;
+        if (!(best > 0.0)) s_zero = 1;
+        else { s_la += log(best); s_umax = fmax(s_umax, best); s_umin = fmin(s_umin, best); }
+      }
     }
     __syncthreads();
-    const int p = pivs[k];
-    if (p != k) for (int j = t; j < q; j += TT) { double x = S[k * q + j]; S[k * q + j] = S[p * q + j]; S[p * q + j] = x; }
+    const int p = s_p;
+    for (int j = t; j < q2; j += NT) { rowk[j] = W[p * q2 + j]; rowold[j] = W[k * q2 + j]; }
+    for (int a = t; a < q; a += NT) colk[a] = W[(a == k ? p : (a == p ? k : a)) * q2 + k];
     __syncthreads();
-    const double ukk = S[k * q + k];
-    if (ukk != 0.0) {
-      const int rows = q - 1 - k, cols = q - 1 - k;   // trailing block a > k, j > k
-      for (int e = t; e < rows * cols; e += TT) {
-        const int a = k + 1 + e / cols, j = k + 1 + e % cols;
-        S[a * q + j] -= (S[a * q + k] / ukk) * S[k * q + j];
+    const double piv = rowk[k];
+    const double ip = piv != 0.0 ? 1.0 / piv : 0.0;
+    for (int e = t; e < q * q2; e += NT) {
+      const int a = e / q2, j = e - a * q2;
+      if (a == k) W[e] = rowk[j] * ip;
+      else {
+        const double src = a == p ? rowold[j] : W[e];
+        W[e] = fma(-colk[a] * ip, rowk[j], src);
       }
-      __syncthreads();
-      for (int a = k + 1 + t; a < q; a += TT) S[a * q + k] /= ukk;
     }
     __syncthreads();
   }
+  const bool zero = s_zero != 0;
   if (t == 0) {
-    int sg = 1; double la = 0.0;
-    for (int k = 0; k < q; k++) {
-      if (pivs[k] != k) sg = -sg;
-      double u = S[k * q + k];
-      if (u < 0.0) sg = -sg;
-      la += log(fabs(u));
-    }
-    c.node_ld[node] = la;
-    if (zero_piv || sg <= 0) { atomicAdd(&c.flags[1], 1); atomicMin(&c.flags[2], (int)node); }
+    c.node_ld[node] = s_la;
+    if (zero || s_sign <= 0) { atomicAdd(&c.flags[1], 1); atomicMin(&c.flags[2], (int)node); }
     // refinement steps: one when the pivot growth ratio is mild, two otherwise (cond(S_c) up to ~1e12)
-    double umax = 0.0, umin = 1e300;
-    for (int k = 0; k < q; k++) { const double u = fabs(S[k * q + k]); umax = fmax(umax, u); umin = fmin(umin, u); }
-    nref = (umin > 0.0 && umax < 1e6 * umin) ? 1 : 2;
+    s_nref = (!zero && s_umax < 1e6 * s_umin) ? 1 : 2;
   }
   __syncthreads();
-  if (!zero_piv && Kd > 0) {
-    for (int col = t; col < Kd; col += TT) lu_solve_col(S, pivs, q, Th + col, Kd);
+  const double *Si = W + q;           // S^{-1}, row stride 2q
+  if (!zero && Kd > 0) {
+    const long long qK = (long long)q * ldk;
+    for (long long e = t; e < qK; e += NT) {          // T_hi = S^{-1} B
+      const int a = (int)(e / ldk), col = (int)(e - (long long)a * ldk);
+      double s = 0.0;
+      for (int j = 0; j < q; j++) s = fma(Si[a * q2 + j], B[j * ldk + col], s);
+      Th[e] = s;
+    }
     __syncthreads();
-    for (int it = 0; it < nref; it++) {       // iterative refinement, residual in double-double
-      for (long long e = t; e < qK; e += TT) {
-        const int a = (int)(e / Kd), col = (int)(e - (long long)a * Kd);
-        Acc2 A = acc2(B[e]);
-        for (int k = 0; k < q; k++) acc_fma_dd(A, -S0[a * q + k], Th[k * Kd + col], Tl[k * Kd + col]);
-        R[e] = acc_val(A);
+    const int nref = s_nref;
+    for (int it = 0; it < nref; it++) {               // iterative refinement, residual compensated
+      for (long long e = t; e < qK; e += NT) {
+        const int a = (int)(e / ldk), col = (int)(e - (long long)a * ldk);
+        if (DD) {
+          Acc2 A = acc2(B[e]);
+          for (int k = 0; k < q; k++) acc_fma_dd(A, -S0[a * q + k], Th[k * ldk + col], Tl[k * ldk + col]);
+          R[e] = acc_val(A);
+        } else {
+          double s = B[e];
+          for (int k = 0; k < q; k++) s = fma(-S0[a * q + k], Th[k * ldk + col] + Tl[k * ldk + col], s);
+          R[e] = s;
+        }
       }
       __syncthreads();
-      for (int col = t; col < Kd; col += TT) {
-        lu_solve_col(S, pivs, q, R + col, Kd);
-        for (int a = 0; a < q; a++) Tl[a * Kd + col] += R[a * Kd + col];
+      for (long long e = t; e < qK; e += NT) {
+        const int a = (int)(e / ldk), col = (int)(e - (long long)a * ldk);
+        double s = 0.0;
+        for (int j = 0; j < q; j++) s = fma(Si[a * q2 + j], R[j * ldk + col], s);
+        Tl[e] += s;
       }
       __syncthreads();
     }
+    // ---------------- Pi_c, 2x4 register tiles over the packed lower triangle ----------------
+    // Bands of 4 rows; band P holds row tiles I = 2P, 2P+1 with column tiles J = 0..P (tile (I, J) =
+    // rows 2I, 2I+1, columns 4J..4J+3); tiles up to band P: (P+1)(P+2).
+    double *Pc = c.Pic + i * ((long long)Kd * (Kd + 1) / 2);
+    const int NB = (Kd + 3) >> 2;
+    const int ntile = NB * (NB + 1);
+    for (int tile = t; tile < ntile; tile += NT) {
+      int P = (int)((sqrt(4.0 * (double)tile + 1.0) - 1.0) * 0.5);
+      while (P * (P + 1) > tile) P--;
+      while ((P + 1) * (P + 2) <= tile) P++;
+      const int rem = tile - P * (P + 1);
+      const int I = 2 * P + rem / (P + 1), J = rem % (P + 1);
+      const int a0 = 2 * I, b0 = 4 * J;
+      double hs[2][4], ls[2][4];
+#pragma unroll
+      for (int ii = 0; ii < 2; ii++)
+#pragma unroll
+        for (int jj = 0; jj < 4; jj++) {
+          const int a = a0 + ii, b = b0 + jj;
+          double s = 0.0, e = 0.0;
+          if (a < Kd && b <= a) {
+            const long long pp = (long long)a * (a + 1) / 2 + b;   // packed (a, b): same index in both children
+            if (DD) two_sum(__ldg(P1 + pp), __ldg(P2 + pp), s, e); else s = __ldg(P1 + pp) + __ldg(P2 + pp);
+          }
+          hs[ii][jj] = s; ls[ii][jj] = e;
+        }
+      for (int u = 0; u < q; u++) {
+        const int ub = u < q - r ? u + r : u + r - q;
+        const double *bu = B + (long long)ub * ldk + a0;
+        const double *thu = Th + (long long)u * ldk + b0, *tlu = Tl + (long long)u * ldk + b0;
+        double bv[2], th[4], tl[4];
+#pragma unroll
+        for (int x = 0; x < 2; x++) bv[x] = -bu[x];
+#pragma unroll
+        for (int x = 0; x < 4; x++) { th[x] = thu[x]; tl[x] = tlu[x]; }
+#pragma unroll
+        for (int ii = 0; ii < 2; ii++)
+#pragma unroll
+          for (int jj = 0; jj < 4; jj++) {
+            if (DD) {
+              double pr, pe, s2, e2;
+              two_prod(bv[ii], th[jj], pr, pe);
+              two_sum(hs[ii][jj], pr, s2, e2);
+              hs[ii][jj] = s2;
+              ls[ii][jj] += e2 + fma(bv[ii], tl[jj], pe);
+            } else {
+              hs[ii][jj] = fma(bv[ii], th[jj] + tl[jj], hs[ii][jj]);
+            }
+          }
+      }
+#pragma unroll
+      for (int ii = 0; ii < 2; ii++)
+#pragma unroll
+        for (int jj = 0; jj < 4; jj++) {
+          const int a = a0 + ii, b = b0 + jj;
+          if (a < Kd && b <= a) Pc[(long long)a * (a + 1) / 2 + b] = hs[ii][jj] + ls[ii][jj];
+        }
+    }
+  }
+  // persist S, S^{-1}, B, T_hi, T_lo for the solve
+  double *Sg = c.Sst + i * (long long)(2 * q * q + q);
+  for (int p = t; p < q * q; p += NT) {
+    const int a = p / q, b = p - a * q;
+    Sg[p] = S0[p];
+    Sg[q * q + p] = Si[a * q2 + b];
+  }
+  const long long qKd = (long long)q * Kd;
+  double *BTg = c.BT + i * 3LL * qKd;
+  for (long long p = t; p < qKd; p += NT) {
+    const int a = (int)(p / Kd), b = (int)(p - (long long)a * Kd);
+    BTg[p] = B[a * ldk + b];
+    BTg[qKd + p] = Th[a * ldk + b];
+    BTg[2 * qKd + p] = Tl[a * ldk + b];
   }
   __syncthreads();
-  // Pi_c = Pi_c1[a,a] + Pi_c2[a,a] - B[r:]^T T[:r] - B[:r]^T T[r:]  (packed lower triangle)
-  double *Pc = c.Pic + i * ((long long)Kd * (Kd + 1) / 2);
-  const long long npk = (long long)Kd * (Kd + 1) / 2;
-  for (long long p = t; p < npk; p += TT) {
-    long long a = (long long)((sqrt(8.0 * (double)p + 1.0) - 1.0) * 0.5);
-    while (a * (a + 1) / 2 > p) a--;
-    while ((a + 1) * (a + 2) / 2 <= p) a++;
-    long long b = p - a * (a + 1) / 2;
-    Acc2 A = acc2(P1[p]);                     // packed index of (a, b) is p in both children too
-    acc_add(A, P2[p]);
-    for (int u = 0; u < r; u++) acc_fma_dd(A, -B[(long long)(r + u) * Kd + a], Th[(long long)u * Kd + b], Tl[(long long)u * Kd + b]);
-    for (int u = 0; u < r; u++) acc_fma_dd(A, -B[(long long)u * Kd + a], Th[(long long)(r + u) * Kd + b], Tl[(long long)(r + u) * Kd + b]);
-    Pc[p] = acc_val(A);
-  }
-  // persist S, LU(S) (+ pivots as doubles), B, T_hi, T_lo for the solve
-  double *Sg = c.Sst + i * (long long)(2 * q * q + q);
-  for (int p = t; p < 2 * q * q; p += TT) Sg[p] = S0[p];         // S0 and S are contiguous
-  for (int p = t; p < q; p += TT) Sg[2 * q * q + p] = (double)pivs[p];
-  double *BTg = c.BT + i * 3LL * qK;
-  for (long long p = t; p < 3LL * qK; p += TT) BTg[p] = B[p];    // B, Th, Tl are contiguous
+}
+
+template <bool DD>
+__global__ void __launch_bounds__(TT, 3) k_tree_factor(TreeCtx c) {
+  extern __shared__ double sm[];
+  tree_node<DD>(c, blockIdx.x, sm);
 }
 
 // log det = leaves (left to right), then internal nodes by depth kappa-1..0, left to right;
@@ -418,21 +503,30 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
   ph_begin(h, PH_TREE);
   size_t tree_smem_max = 0;
   for (int d = 0; d < kappa; d++) {
-    size_t q = 2 * (size_t)dt.rdep[d + 1];
-    tree_smem_max = std::max(tree_smem_max, sizeof(double) * (2 * q * q + 4 * q * dt.Kdim[d]));
+    const int q = 2 * dt.rdep[d + 1], ldk = (dt.Kdim[d] + 3) & ~3;
+    tree_smem_max = std::max(tree_smem_max, sizeof(double) * (size_t)tree_smem_doubles(q, ldk));
   }
   if (tree_smem_max > (size_t)maxsm - 2048)
     return hodlr_set_error(HODLR_EINVAL, "factor: coupling system too large for shared memory");
-  if (kappa > 0)
-    HCUDA(cudaFuncSetAttribute(k_tree_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tree_smem_max));
+  static size_t tree_attr = 0;
+  if (kappa > 0 && tree_smem_max > tree_attr) {
+    HCUDA(cudaFuncSetAttribute(k_tree_factor<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tree_smem_max));
+    HCUDA(cudaFuncSetAttribute(k_tree_factor<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tree_smem_max));
+    tree_attr = tree_smem_max;
+  }
+  // debug/experiment switch: depths >= HODLR_TREE_PLAIN_FROM use plain double (default: none)
+  static int plain_from = -1;
+  if (plain_from < 0) { const char *ev = getenv("HODLR_TREE_PLAIN_FROM"); plain_from = ev ? atoi(ev) : 1 << 20; }
   for (int d = kappa - 1; d >= 0; d--) {
     TreeCtx tc;
     tc.d = d; tc.r = dt.rdep[d + 1]; tc.q = 2 * tc.r; tc.Kd = dt.Kdim[d]; tc.K1 = dt.Kdim[d + 1];
+    tc.ldk = (tc.Kd + 3) & ~3; tc.dd = d < plain_from;
     tc.Pi1 = h->Pipool + dt.piOff[d + 1]; tc.Pic = h->Pipool + dt.piOff[d];
     tc.Sst = h->Spool + dt.nodeS[d]; tc.BT = h->BTpool + dt.nodeBT[d];
     tc.node_ld = h->node_ld; tc.flags = h->dflags;
-    size_t smem = sizeof(double) * (2ULL * tc.q * tc.q + 4ULL * tc.q * tc.Kd);
-    k_tree_factor<<<(int)(1LL << d), TT, smem, h->st>>>(tc);
+    const size_t smem = sizeof(double) * (size_t)tree_smem_doubles(tc.q, tc.ldk);
+    if (tc.dd) k_tree_factor<true><<<(int)(1LL << d), TT, smem, h->st>>>(tc);
+    else k_tree_factor<false><<<(int)(1LL << d), TT, smem, h->st>>>(tc);
     HLAUNCH(h, "k_tree_factor");
   }
   k_logdet_reduce<<<1, 256, 0, h->st>>>(h->leaf_ld, h->node_ld, nl, kappa, h->d_logdet);

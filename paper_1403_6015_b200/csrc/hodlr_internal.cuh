@@ -19,6 +19,7 @@
 #define HODLR_MAXDEPTH 48
 #define ACA_MAXCAP 64      // hard ceiling on the ACA rank cap (records/state are sized by it)
 #define ACA_RECW (4 + ACA_MAXCAP)
+#define ACA_GSZ (ACA_MAXCAP * (ACA_MAXCAP + 1) / 2)   // packed Gram matrix of one factor side
 #define ACA_SUB 256        // threads per ACA CTA == sub-tile width
 #define ACA_FUSED_MAX 4096 // blocks with both sides <= this run the fused single-CTA ACA
 #define ACA_BIG_CHUNK 2048 // minimum chunk per CTA for the step-synchronous big blocks
@@ -88,6 +89,8 @@ struct AcaCtx {
   int *rank;
   const int *bdepth;        // depth of each internal block
   DepthTab *dt;             // device copy
+  const int *bigidx;        // block -> ordinal among the step-synchronous (big) blocks, -1 otherwise
+  double *gram;             // per big block: packed G_U = U'^T U', then G_V = V'^T V' 
 };
 
 // ----------------------------------------------------------------------------------------------
@@ -115,6 +118,7 @@ struct hodlr_s {
   int state;                 // 1 built, 2 factored, -1 factor failed
   int launches;              // kernels launched by the current call
   int aca_steps;
+  int x_nonfinite;           // set by the sort: x contains NaN/Inf
   long long rank_cap_hits;
   // host copies
   long long *h_lo, *h_hi;
@@ -130,7 +134,8 @@ struct hodlr_s {
   AcaState *ast;
   int *rank;
   int *bdepth;
-  int *dflags;               // [0] nonfinite x, [1] notpd, [2] notpd node+1 (min), [3] nonfinite y, [4] active
+  int *dflags;               // [0] nonfinite x, [1] notpd, [2] notpd node (min), [3] nonfinite y, [4] active big
+                             // ACA blocks, [5] rank-cap hits, [6] ACA steps, [7] x not ascending
   DepthTab *d_dt;
   // factor storage
   double *Lf; long long lstride; int ltiles;   // leaf factor tiles (see storage helpers)

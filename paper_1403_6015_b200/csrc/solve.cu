@@ -211,33 +211,16 @@ __global__ void __launch_bounds__(ST) k_leaf_down(SolveCtx c) {
 // ---------------------------------------------------------------------------------------------
 constexpr int QMAX = 2 * ACA_MAXCAP;
 
-// x (length q, shared) <- LU^{-1} x ; one warp
-__device__ void lu_solve_warp(const double *LU, const double *pivd, int q, double *x, int lane) {
-  if (lane == 0)
-    for (int k = 0; k < q; k++) { int p = (int)pivd[k]; if (p != k) { double t = x[k]; x[k] = x[p]; x[p] = t; } }
-  __syncwarp();
-  for (int k = 0; k < q; k++) {                 // unit lower
-    const double xk = x[k];
-    __syncwarp();
-    for (int a = k + 1 + lane; a < q; a += 32) x[a] -= LU[a * q + k] * xk;
-    __syncwarp();
+// t = S^{-1} rhs as (th, tl): explicit inverse S^{-1} (from the factor phase) + 2 refinement steps with
+// compensated residuals.  One warp; all vectors in shared memory.
+__device__ void dd_solve_warp(const double *S0, const double *Si, int q, const double *rhs, double *th, double *tl,
+                              double *tmp, int lane) {
+  for (int a = lane; a < q; a += 32) {
+    double s = 0.0;
+    for (int j = 0; j < q; j++) s = fma(Si[a * q + j], rhs[j], s);
+    th[a] = s; tl[a] = 0.0;
   }
-  for (int k = q - 1; k >= 0; k--) {           // upper
-    if (lane == 0) x[k] /= LU[k * q + k];
-    __syncwarp();
-    const double xk = x[k];
-    __syncwarp();
-    for (int a = lane; a < k; a += 32) x[a] -= LU[a * q + k] * xk;
-    __syncwarp();
-  }
-}
-
-// t = S^{-1} rhs as (th, tl): double solve + 2 refinement steps with compensated residuals.
-__device__ void dd_solve_warp(const double *S0, const double *LU, const double *pivd, int q,
-                              const double *rhs, double *th, double *tl, double *tmp, int lane) {
-  for (int a = lane; a < q; a += 32) { th[a] = rhs[a]; tl[a] = 0.0; }
   __syncwarp();
-  lu_solve_warp(LU, pivd, q, th, lane);
   for (int it = 0; it < 2; it++) {
     for (int a = lane; a < q; a += 32) {
       Acc2 A = acc2(rhs[a]);
@@ -245,8 +228,11 @@ __device__ void dd_solve_warp(const double *S0, const double *LU, const double *
       tmp[a] = acc_val(A);
     }
     __syncwarp();
-    lu_solve_warp(LU, pivd, q, tmp, lane);
-    for (int a = lane; a < q; a += 32) tl[a] += tmp[a];
+    for (int a = lane; a < q; a += 32) {
+      double s = 0.0;
+      for (int j = 0; j < q; j++) s = fma(Si[a * q + j], tmp[j], s);
+      tl[a] += s;
+    }
     __syncwarp();
   }
 }
@@ -264,11 +250,11 @@ __global__ void __launch_bounds__(ST) k_tree_up(SolveCtx c, int d) {
   const double *B = c.BTpool + c.dt->nodeBT[d] + i * 3LL * q * Kd;
   // per-warp staging: S0, LU, pivots, rhs, th, tl, tmp (global latency stays out of the sequential solves)
   double *S0 = dsm + (long long)wid * (2 * q * q + 5 * q);
-  double *LU = S0 + q * q, *pivd = LU + q * q, *rhs = pivd + q, *th = rhs + q, *tl = th + q, *tmp = tl + q;
+  double *Si = S0 + q * q, *rhs = Si + q * q + q, *th = rhs + q, *tl = th + q, *tmp = tl + q;
   for (int p = lane; p < 2 * q * q + q; p += 32) S0[p] = Sg[p];
   for (int u = lane; u < r; u += 32) { rhs[u] = g2[Kd + u]; rhs[r + u] = g1[Kd + u]; }
   __syncwarp();
-  dd_solve_warp(S0, LU, pivd, q, rhs, th, tl, tmp, lane);
+  dd_solve_warp(S0, Si, q, rhs, th, tl, tmp, lane);
   double *tg = c.Tv + c.dt->nodeT[d] + i * 2LL * q;
   for (int u = lane; u < q; u += 32) { tg[u] = th[u]; tg[q + u] = tl[u]; }
   if (lane == 0) {

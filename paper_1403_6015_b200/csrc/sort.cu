@@ -14,13 +14,19 @@ namespace {
 constexpr int TILE = 4096;
 constexpr int STHREADS = 512;    // 16 warps x 256 keys
 
+// Keys + the identity result (xs = x, perm = iota) + a sortedness flag: an already ascending x
+// (ties included) has the identity as its stable argsort, and the radix passes are skipped.
 __global__ void k_make_keys(const double *__restrict__ x, long long n, unsigned long long *__restrict__ key,
-                            long long *__restrict__ idx, int *__restrict__ flags) {
+                            long long *__restrict__ idx, double *__restrict__ xs, long long *__restrict__ perm,
+                            int *__restrict__ flags) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
   double v = x[i];
   if (!isfinite(v)) atomicOr(&flags[0], 1);
   if (v == 0.0) v = 0.0;                        // -0.0 -> +0.0 before sorting
+  if (i + 1 < n && !(v <= x[i + 1])) atomicOr(&flags[7], 1);   // -0.0 <= +0.0 holds, so ties stay ties
+  xs[i] = v;
+  perm[i] = i;
   unsigned long long b = __double_as_longlong(v);
   b ^= (b >> 63) ? 0xffffffffffffffffULL : 0x8000000000000000ULL;
   key[i] = b;
@@ -143,8 +149,14 @@ hodlr_status hodlr_sort_and_tree(hodlr_s *h, const double *x) {
   if (!k0 || !k1 || !i0 || !i1 || !cnt) return hodlr_set_error(HODLR_ENOMEM, "sort: device allocation failed");
   int nb = (int)((n + 255) / 256);
   ph_begin(h, PH_SORT);
-  k_make_keys<<<nb, 256, 0, h->st>>>(x, n, k0, i0, h->dflags);
+  HCUDA(cudaMemsetAsync(h->dflags + 7, 0, sizeof(int), h->st));
+  k_make_keys<<<nb, 256, 0, h->st>>>(x, n, k0, i0, h->xs, h->perm, h->dflags);
   HLAUNCH(h, "k_make_keys");
+  int f[8];
+  HCUDA(cudaMemcpyAsync(f, h->dflags, sizeof(f), cudaMemcpyDeviceToHost, h->st));
+  HCUDA(cudaStreamSynchronize(h->st));
+  h->x_nonfinite = f[0];
+  if (f[0] || !f[7]) { ph_end(h, PH_SORT); return HODLR_OK; }   // NaN/Inf (EINVAL) or already sorted
   for (int pass = 0; pass < 8; pass++) {
     int shift = pass * 8;
     k_hist<<<ntiles, STHREADS, 0, h->st>>>(k0, n, shift, ntiles, cnt);
