@@ -17,6 +17,8 @@
 #include <vector>
 #include <algorithm>
 #include <stdlib.h>
+#include <string.h>
+#include <mutex>
 
 namespace {
 
@@ -92,7 +94,11 @@ constexpr int ACA_E = 4;                       // elements per thread per sub-ti
 constexpr int ACA_TILE = ACA_SUB * ACA_E;
 
 template <bool ROW>
-__global__ void __launch_bounds__(ACA_SUB, 4) k_aca_pass(AcaCtx c, int *flags) {
+__global__ void __launch_bounds__(ACA_SUB, 3) k_aca_pass(const AcaCtx *__restrict__ pc) {
+  __shared__ AcaCtx c;                         // context in shared memory: global stores cannot alias it
+  for (int i = threadIdx.x; i < (int)(sizeof(AcaCtx) / 8); i += ACA_SUB) ((long long *)&c)[i] = ((const long long *)pc)[i];
+  __syncthreads();
+  int *flags = c.flags;
   const AcaItem it = c.items[blockIdx.x];
   const int b = it.block;
   AcaState *st = &c.st[b];
@@ -122,13 +128,15 @@ __global__ void __launch_bounds__(ACA_SUB, 4) k_aca_pass(AcaCtx c, int *flags) {
     const long long g0 = lo + s0 + t;          // element q at g0 + q * ACA_SUB
     const int nval = (int)min((long long)ACA_E, (end - s0 - t + ACA_SUB - 1) / ACA_SUB);   // valid elements
     double a[ACA_E], r[ACA_E];
+    unsigned usedm = 0;                        // used flags, loaded up front (char loads cannot pass the stores)
 #pragma unroll
     for (int q = 0; q < ACA_E; q++) {
-      const double d = q < nval ? (ROW ? xp - c.xs[g0 + q * ACA_SUB] : c.xs[g0 + q * ACA_SUB] - xp) : 0.0;
-      a[q] = q < nval ? kval(c.kp, d) : 0.0;
+      const double xq = q < nval ? c.xs[g0 + q * ACA_SUB] : xp;
+      if (q < nval && used[g0 + q * ACA_SUB]) usedm |= 1u << q;
+      a[q] = q < nval ? kval(c.kp, ROW ? xp - xq : xq - xp) : 0.0;
       r[q] = a[q];
     }
-    constexpr int LS = 2;                      // factor columns per batch of loads
+    constexpr int LS = 4;                      // factor columns per batch of loads
     for (int l0 = 0; l0 < k; l0 += LS) {
       double F[LS][ACA_E];
 #pragma unroll
@@ -156,7 +164,7 @@ __global__ void __launch_bounds__(ACA_SUB, 4) k_aca_pass(AcaCtx c, int *flags) {
       const long long g = g0 + q * ACA_SUB;
       const double v = r[q] * scale;
       slot[(long long)k * n + g] = v;
-      if (!used[g] && amax_better(ba, bi, fabs(v), g - lo)) { ba = fabs(v); bi = g - lo; bv = v; }
+      if (!((usedm >> q) & 1u) && amax_better(ba, bi, fabs(v), g - lo)) { ba = fabs(v); bi = g - lo; bv = v; }
       n2 += v * v;
     }
   }
@@ -372,32 +380,46 @@ __global__ void __launch_bounds__(ACA_SUB) k_aca_fused(AcaCtx c, const int *bloc
 
 // Device-side loop control for the conditional-while CUDA graph: keep iterating while big blocks are
 // active and the step count is below the cap.
-__global__ void k_aca_cond(cudaGraphConditionalHandle hdl, const int *active, int *step, int maxsteps) {
-  const int s = ++(*step);
-  cudaGraphSetConditional(hdl, (*active > 0 && s < maxsteps) ? 1u : 0u);
+__global__ void k_aca_cond(cudaGraphConditionalHandle hdl, const AcaCtx *__restrict__ pc) {
+  const int s = ++(*pc->step);
+  cudaGraphSetConditional(hdl, (*pc->active > 0 && s < pc->maxsteps) ? 1u : 0u);
 }
 
 }  // namespace
 
-hodlr_status hodlr_aca(hodlr_s *h) {
-  const long long nb = h->ninternal;
-  if (nb == 0) return HODLR_OK;
-  const long long n = h->n;
-  // ---- host plan: chunking per block side, items sorted big blocks first ----
-  std::vector<AcaItem> items_r, items_c;
-  std::vector<int> nq_r(nb), nq_c(nb);
-  std::vector<long long> rb_r(nb), rb_c(nb);
-  std::vector<int> bdepth(nb);
-  long long nrec_r = 0, nrec_c = 0;
+// ---------------------------------------------------------------------------------------------
+// Host plan, cached per tree shape (n, leaf): chunk items of the big blocks, the fused small blocks, record
+// offsets, depths, and the instantiated conditional-while graph of the big-block step loop.  The graph's
+// kernels read their context from plan-owned device memory (rewritten per build), so repeated builds of the
+// same shape skip the planning and the graph instantiation.  A plan in use by another build is not shared.
+// ---------------------------------------------------------------------------------------------
+struct AcaPlan {
+  long long n; int leaf;
+  long long nb; int nbig;
   std::vector<int> fused_blocks;
-  std::vector<int> bigidx(nb, -1);
-  int nbig = 0;
+  size_t nitems_r = 0, nitems_c = 0;
+  long long nrec_r = 0, nrec_c = 0;
+  AcaItem *d_items_r = nullptr, *d_items_c = nullptr;
+  int *d_fused = nullptr, *d_nq = nullptr, *d_bigidx = nullptr, *d_bdepth = nullptr;
+  long long *d_rb = nullptr;
+  AcaCtx *d_ctx = nullptr;                 // [0] row pass, [1] column pass
+  cudaGraphExec_t ge = nullptr;
+  bool busy = false;
+};
+static std::mutex g_plan_mu;
+static std::vector<AcaPlan *> g_plans;
+
+static cudaError_t plan_create(AcaPlan *P, const hodlr_s *h) {
+  const long long nb = h->ninternal;
+  std::vector<AcaItem> items_r, items_c;
+  std::vector<int> nq_r(nb), nq_c(nb), bdepth(nb), bigidx(nb, -1);
+  std::vector<long long> rb_r(nb), rb_c(nb);
+  P->nbig = 0;
   for (long long b = 0; b < nb; b++) {
     bdepth[b] = hodlr_depth_of(b);
     long long m1 = h->h_hi[2 * b + 1] - h->h_lo[2 * b + 1], m2 = h->h_hi[2 * b + 2] - h->h_lo[2 * b + 2];
-    if (std::max(m1, m2) <= ACA_FUSED_MAX) { fused_blocks.push_back((int)b); nq_r[b] = nq_c[b] = 0; rb_r[b] = rb_c[b] = 0; continue; }
-    bigidx[b] = nbig;
-    nbig++;
+    if (std::max(m1, m2) <= ACA_FUSED_MAX) { P->fused_blocks.push_back((int)b); nq_r[b] = nq_c[b] = 0; rb_r[b] = rb_c[b] = 0; continue; }
+    bigidx[b] = P->nbig++;
     for (int side = 0; side < 2; side++) {
       long long m = side == 0 ? m2 : m1;
       long long chunk = (m + 127) / 128;
@@ -408,109 +430,60 @@ hodlr_status hodlr_aca(hodlr_s *h) {
         AcaItem it; it.block = (int)b; it.q = q; it.start = s; it.len = (int)std::min(chunk, m - s); it.pad = 0;
         (side == 0 ? items_r : items_c).push_back(it);
       }
-      if (side == 0) { nq_r[b] = q; rb_r[b] = nrec_r; nrec_r += q; }
-      else { nq_c[b] = q; rb_c[b] = nrec_c; nrec_c += q; }
+      if (side == 0) { nq_r[b] = q; rb_r[b] = P->nrec_r; P->nrec_r += q; }
+      else { nq_c[b] = q; rb_c[b] = P->nrec_c; P->nrec_c += q; }
     }
   }
-  // ---- device buffers ----
-  AcaItem *d_items_r = (AcaItem *)hodlr_dalloc(h, sizeof(AcaItem) * (items_r.size() + 1));
-  AcaItem *d_items_c = (AcaItem *)hodlr_dalloc(h, sizeof(AcaItem) * (items_c.size() + 1));
-  int *d_fused = (int *)hodlr_dalloc(h, sizeof(int) * (fused_blocks.size() + 1));
-  int *d_nq = (int *)hodlr_dalloc(h, sizeof(int) * 2 * nb);
-  long long *d_rb = (long long *)hodlr_dalloc(h, sizeof(long long) * 2 * nb);
-  double *d_rec = (double *)hodlr_dalloc(h, sizeof(double) * ACA_RECW * (size_t)(nrec_r + nrec_c));
-  h->ast = (AcaState *)hodlr_dalloc(h, sizeof(AcaState) * nb);
-  h->rank = (int *)hodlr_dalloc(h, sizeof(int) * nb);
-  h->bdepth = (int *)hodlr_dalloc(h, sizeof(int) * nb);
-  h->used = (unsigned char *)hodlr_dalloc(h, (size_t)h->kappa * n);
-  int *d_bigidx = (int *)hodlr_dalloc(h, sizeof(int) * nb);
-  double *d_gram = (double *)hodlr_dalloc(h, sizeof(double) * 2 * ACA_GSZ * (size_t)(nbig > 0 ? nbig : 1));
-  if (!d_bigidx || !d_gram) return hodlr_set_error(HODLR_ENOMEM, "aca: device allocation failed");
-  if (!d_items_r || !d_items_c || !d_fused || !d_nq || !d_rb || !d_rec || !h->ast || !h->rank || !h->bdepth || !h->used)
-    return hodlr_set_error(HODLR_ENOMEM, "aca: device allocation failed");
+  P->nitems_r = items_r.size(); P->nitems_c = items_c.size();
   std::vector<int> nq_all(nq_r); nq_all.insert(nq_all.end(), nq_c.begin(), nq_c.end());
   std::vector<long long> rb_all(rb_r); rb_all.insert(rb_all.end(), rb_c.begin(), rb_c.end());
-  if (!items_r.empty()) HCUDA(cudaMemcpyAsync(d_items_r, items_r.data(), sizeof(AcaItem) * items_r.size(), cudaMemcpyHostToDevice, h->st));
-  if (!items_c.empty()) HCUDA(cudaMemcpyAsync(d_items_c, items_c.data(), sizeof(AcaItem) * items_c.size(), cudaMemcpyHostToDevice, h->st));
-  if (!fused_blocks.empty()) HCUDA(cudaMemcpyAsync(d_fused, fused_blocks.data(), sizeof(int) * fused_blocks.size(), cudaMemcpyHostToDevice, h->st));
-  HCUDA(cudaMemcpyAsync(d_nq, nq_all.data(), sizeof(int) * 2 * nb, cudaMemcpyHostToDevice, h->st));
-  HCUDA(cudaMemcpyAsync(d_rb, rb_all.data(), sizeof(long long) * 2 * nb, cudaMemcpyHostToDevice, h->st));
-  HCUDA(cudaMemcpyAsync(h->bdepth, bdepth.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, h->st));
-  HCUDA(cudaMemcpyAsync(d_bigidx, bigidx.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, h->st));
-  HCUDA(cudaMemsetAsync(h->used, 0, (size_t)h->kappa * n, h->st));
-  HCUDA(cudaMemcpyAsync(h->dflags + 4, &nbig, sizeof(int), cudaMemcpyHostToDevice, h->st));
-  // the pageable copies above are staged synchronously by the runtime, so the vectors may die
-
-  AcaCtx c;
-  c.kp = h->kp; c.n = n; c.eps = h->eps; c.xs = h->xs; c.lo = h->lo; c.hi = h->hi; c.Xh = h->Xh;
-  c.used = h->used; c.st = h->ast; c.active = h->dflags + 4; c.rank = h->rank; c.bdepth = h->bdepth;
-  c.dt = h->d_dt; c.bigidx = d_bigidx; c.gram = d_gram;
-  ph_begin(h, PH_ACA);
-  k_aca_init<<<(int)((nb + 255) / 256), 256, 0, h->st>>>(c, (int)nb, h->cap);
-  HLAUNCH(h, "k_aca_init");
-  // small blocks: one fused CTA per block on the side stream, concurrent with the big-block steps
-  if (!fused_blocks.empty()) {
-    HCUDA(cudaEventRecord(h->ev_fork, h->st));
-    HCUDA(cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
-    k_aca_fused<<<(int)fused_blocks.size(), ACA_SUB, 0, h->st2>>>(c, d_fused, h->dflags);
-    HLAUNCH(h, "k_aca_fused");
-    HCUDA(cudaEventRecord(h->ev_join, h->st2));
+  cudaError_t e = cudaSuccess;
+#define PM(ptr, bytes) if (e == cudaSuccess) e = cudaMalloc((void **)&(ptr), (bytes) > 0 ? (bytes) : 8)
+  PM(P->d_items_r, sizeof(AcaItem) * items_r.size());
+  PM(P->d_items_c, sizeof(AcaItem) * items_c.size());
+  PM(P->d_fused, sizeof(int) * P->fused_blocks.size());
+  PM(P->d_nq, sizeof(int) * 2 * nb);
+  PM(P->d_rb, sizeof(long long) * 2 * nb);
+  PM(P->d_bigidx, sizeof(int) * nb);
+  PM(P->d_bdepth, sizeof(int) * nb);
+  PM(P->d_ctx, sizeof(AcaCtx) * 2);
+#undef PM
+#define PC(dst, src, bytes) if (e == cudaSuccess && (bytes) > 0) e = cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice)
+  PC(P->d_items_r, items_r.data(), sizeof(AcaItem) * items_r.size());
+  PC(P->d_items_c, items_c.data(), sizeof(AcaItem) * items_c.size());
+  PC(P->d_fused, P->fused_blocks.data(), sizeof(int) * P->fused_blocks.size());
+  PC(P->d_nq, nq_all.data(), sizeof(int) * 2 * nb);
+  PC(P->d_rb, rb_all.data(), sizeof(long long) * 2 * nb);
+  PC(P->d_bigidx, bigidx.data(), sizeof(int) * nb);
+  PC(P->d_bdepth, bdepth.data(), sizeof(int) * nb);
+#undef PC
+  if (e != cudaSuccess || P->nbig == 0) return e;
+  // conditional-while graph: row pass, column pass, loop test (no host polling between steps)
+  cudaGraph_t g = nullptr;
+  cudaGraphConditionalHandle hdl;
+  e = cudaGraphCreate(&g, 0);
+  if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&hdl, g, 1, cudaGraphCondAssignDefault);
+  cudaGraphNodeParams cpar = {};
+  cudaGraphNode_t cnode, n1, n2, n3;
+  if (e == cudaSuccess) {
+    cpar.type = cudaGraphNodeTypeConditional;
+    cpar.conditional.handle = hdl; cpar.conditional.type = cudaGraphCondTypeWhile; cpar.conditional.size = 1;
+    e = cudaGraphAddNode(&cnode, g, nullptr, 0, &cpar);
   }
-
-  AcaCtx cr = c, cc = c;
-  cr.items = d_items_r; cr.nq = d_nq; cr.recbase = d_rb; cr.rec = d_rec;
-  cc.items = d_items_c; cc.nq = d_nq + nb; cc.recbase = d_rb + nb; cc.rec = d_rec + ACA_RECW * nrec_r;
-  // big blocks: the pivot-step loop runs on the device as a conditional-while CUDA graph
-  // (row pass, column pass, loop test) -- no host polling between steps
-  hodlr_status status = HODLR_OK;
-  int steps = 0;
-  static int nograph = -1;     // HODLR_ACA_NOGRAPH=1: host-driven step loop (profilers see every launch)
-  if (nograph < 0) { const char *ev = getenv("HODLR_ACA_NOGRAPH"); nograph = ev && atoi(ev) ? 1 : 0; }
-  if (nbig > 0 && nograph) {
-    int *flags = h->dflags;
-    for (steps = 1; steps <= h->cap + 1; steps++) {
-      k_aca_pass<true><<<(unsigned)items_r.size(), ACA_SUB, 0, h->st>>>(cr, flags);
-      HLAUNCH(h, "k_aca_pass<row>");
-      k_aca_pass<false><<<(unsigned)items_c.size(), ACA_SUB, 0, h->st>>>(cc, flags);
-      HLAUNCH(h, "k_aca_pass<col>");
-      int act = 0;
-      HCUDA(cudaMemcpyAsync(&act, h->dflags + 4, sizeof(int), cudaMemcpyDeviceToHost, h->st));
-      HCUDA(cudaStreamSynchronize(h->st));
-      if (act <= 0) break;
-    }
-    nbig = 0;
-  }
-  if (nbig > 0) {
-    HCUDA(cudaMemsetAsync(h->dflags + 6, 0, sizeof(int), h->st));
-    cudaGraph_t g = nullptr, body = nullptr;
-    cudaGraphExec_t ge = nullptr;
-    cudaGraphConditionalHandle hdl;
-    cudaError_t e = cudaGraphCreate(&g, 0);
-    if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&hdl, g, 1, cudaGraphCondAssignDefault);
-    cudaGraphNodeParams cpar = {};
-    cudaGraphNode_t cnode;
-    if (e == cudaSuccess) {
-      cpar.type = cudaGraphNodeTypeConditional;
-      cpar.conditional.handle = hdl; cpar.conditional.type = cudaGraphCondTypeWhile; cpar.conditional.size = 1;
-      e = cudaGraphAddNode(&cnode, g, nullptr, 0, &cpar);
-    }
-    int *active = h->dflags + 4, *stepc = h->dflags + 6, *flags = h->dflags;
-    int maxsteps = h->cap + 1;
-    void *arow[] = {&cr, &flags};
-    void *acol[] = {&cc, &flags};
-    void *acond[] = {&hdl, &active, &stepc, &maxsteps};
-    cudaGraphNode_t n1, n2, n3;
-    if (e == cudaSuccess) {
-      body = cpar.conditional.phGraph_out[0];
-      cudaKernelNodeParams k1 = {};
-      k1.func = (void *)k_aca_pass<true>; k1.gridDim = dim3((unsigned)items_r.size()); k1.blockDim = dim3(ACA_SUB);
-      k1.sharedMemBytes = 0; k1.kernelParams = arow;
-      e = cudaGraphAddKernelNode(&n1, body, nullptr, 0, &k1);
-    }
+  const AcaCtx *pr = P->d_ctx, *pcc = P->d_ctx + 1;
+  void *arow[] = {(void *)&pr};
+  void *acol[] = {(void *)&pcc};
+  void *acond[] = {(void *)&hdl, (void *)&pr};
+  if (e == cudaSuccess) {
+    cudaGraph_t body = cpar.conditional.phGraph_out[0];
+    cudaKernelNodeParams k1 = {};
+    k1.func = (void *)k_aca_pass<true>; k1.gridDim = dim3((unsigned)P->nitems_r); k1.blockDim = dim3(ACA_SUB);
+    k1.kernelParams = arow;
+    e = cudaGraphAddKernelNode(&n1, body, nullptr, 0, &k1);
     if (e == cudaSuccess) {
       cudaKernelNodeParams k2 = {};
-      k2.func = (void *)k_aca_pass<false>; k2.gridDim = dim3((unsigned)items_c.size()); k2.blockDim = dim3(ACA_SUB);
-      k2.sharedMemBytes = 0; k2.kernelParams = acol;
+      k2.func = (void *)k_aca_pass<false>; k2.gridDim = dim3((unsigned)P->nitems_c); k2.blockDim = dim3(ACA_SUB);
+      k2.kernelParams = acol;
       e = cudaGraphAddKernelNode(&n2, body, &n1, 1, &k2);
     }
     if (e == cudaSuccess) {
@@ -518,20 +491,108 @@ hodlr_status hodlr_aca(hodlr_s *h) {
       k3.func = (void *)k_aca_cond; k3.gridDim = dim3(1); k3.blockDim = dim3(1); k3.kernelParams = acond;
       e = cudaGraphAddKernelNode(&n3, body, &n2, 1, &k3);
     }
-    if (e == cudaSuccess) e = cudaGraphInstantiate(&ge, g, 0);
-    if (e == cudaSuccess) e = cudaGraphLaunch(ge, h->st);
-    if (e != cudaSuccess) status = hodlr_cuda_check(e, "aca graph");
-    h->launches += 3; hodlr_global_launches += 3;     // per iteration; the step count is added below
-    if (ge) cudaGraphExecDestroy(ge);
-    if (g) cudaGraphDestroy(g);
   }
-  if (!fused_blocks.empty()) HCUDA(cudaStreamWaitEvent(h->st, h->ev_join, 0));
+  if (e == cudaSuccess) e = cudaGraphInstantiate(&P->ge, g, 0);
+  if (g) cudaGraphDestroy(g);
+  return e;
+}
+
+static AcaPlan *plan_acquire(const hodlr_s *h, hodlr_status *st) {
+  {
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    for (AcaPlan *P : g_plans)
+      if (!P->busy && P->n == h->n && P->leaf == h->leaf) { P->busy = true; return P; }
+  }
+  AcaPlan *P = new AcaPlan();
+  P->n = h->n; P->leaf = h->leaf; P->nb = h->ninternal; P->busy = true;
+  cudaError_t e = plan_create(P, h);
+  if (e != cudaSuccess) { *st = hodlr_cuda_check(e, "aca plan"); return nullptr; }   // (leaked on error)
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  g_plans.push_back(P);
+  return P;
+}
+
+static void plan_release(AcaPlan *P) { std::lock_guard<std::mutex> lk(g_plan_mu); P->busy = false; }
+
+hodlr_status hodlr_aca(hodlr_s *h) {
+  const long long nb = h->ninternal;
+  if (nb == 0) return HODLR_OK;
+  const long long n = h->n;
+  hodlr_status pst = HODLR_OK;
+  AcaPlan *P = plan_acquire(h, &pst);
+  if (!P) return pst;
+  struct Rel { AcaPlan *p; ~Rel() { plan_release(p); } } rel{P};
+  const int nbig = P->nbig;
+  // ---- per-handle state ----
+  double *d_rec = (double *)hodlr_dalloc(h, sizeof(double) * ACA_RECW * (size_t)(P->nrec_r + P->nrec_c + 1));
+  h->ast = (AcaState *)hodlr_dalloc(h, sizeof(AcaState) * nb);
+  h->rank = (int *)hodlr_dalloc(h, sizeof(int) * nb);
+  h->used = (unsigned char *)hodlr_dalloc(h, (size_t)h->kappa * n);
+  double *d_gram = (double *)hodlr_dalloc(h, sizeof(double) * 2 * ACA_GSZ * (size_t)(nbig > 0 ? nbig : 1));
+  if (!d_rec || !h->ast || !h->rank || !h->used || !d_gram) return hodlr_set_error(HODLR_ENOMEM, "aca: device allocation failed");
+  h->bdepth = P->d_bdepth;
+  // The step loop is latency-bound: everything of the ACA phase runs on a high-priority stream so that the
+  // leaf Cholesky (side stream, issued earlier) only fills the SM slots it leaves free.
+  cudaStream_t sm_main = h->st;
+  HCUDA(cudaEventRecord(h->ev_fork, sm_main));
+  HCUDA(cudaStreamWaitEvent(h->sthi, h->ev_fork, 0));
+  struct Restore { hodlr_s *h; cudaStream_t s; ~Restore() { h->st = s; } } restore{h, sm_main};   // every return path
+  h->st = h->sthi;
+  ph_begin(h, PH_ACA);
+  HCUDA(cudaMemsetAsync(h->used, 0, (size_t)h->kappa * n, h->st));
+  {
+    int init[3] = {nbig, 0, 0};   // dflags[4] active big blocks, [5] rank-cap hits, [6] step counter
+    HCUDA(cudaMemcpyAsync(h->dflags + 4, init, sizeof(init), cudaMemcpyHostToDevice, h->st));
+  }
+  AcaCtx c;
+  memset(&c, 0, sizeof(c));
+  c.kp = h->kp; c.n = n; c.eps = h->eps; c.xs = h->xs; c.lo = h->lo; c.hi = h->hi; c.Xh = h->Xh;
+  c.used = h->used; c.st = h->ast; c.active = h->dflags + 4; c.rank = h->rank; c.bdepth = P->d_bdepth;
+  c.dt = h->d_dt; c.bigidx = P->d_bigidx; c.gram = d_gram; c.flags = h->dflags; c.step = h->dflags + 6;
+  c.maxsteps = h->cap + 1;
+  AcaCtx cx[2] = {c, c};
+  cx[0].items = P->d_items_r; cx[0].nq = P->d_nq; cx[0].recbase = P->d_rb; cx[0].rec = d_rec;
+  cx[1].items = P->d_items_c; cx[1].nq = P->d_nq + nb; cx[1].recbase = P->d_rb + nb; cx[1].rec = d_rec + ACA_RECW * P->nrec_r;
+  HCUDA(cudaMemcpyAsync(P->d_ctx, cx, sizeof(cx), cudaMemcpyHostToDevice, h->st));
+  hodlr_trace("aca: planned + copies issued");
+  k_aca_init<<<(int)((nb + 255) / 256), 256, 0, h->st>>>(c, (int)nb, h->cap);
+  HLAUNCH(h, "k_aca_init");
+  // small blocks: one fused CTA per block on the side stream, concurrent with the big-block steps
+  if (!P->fused_blocks.empty()) {
+    HCUDA(cudaEventRecord(h->ev_fork, h->st));
+    HCUDA(cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
+    k_aca_fused<<<(int)P->fused_blocks.size(), ACA_SUB, 0, h->st2>>>(c, P->d_fused, h->dflags);
+    HLAUNCH(h, "k_aca_fused");
+    HCUDA(cudaEventRecord(h->ev_join, h->st2));
+  }
+  int steps = 0;
+  static int nograph = -1;     // HODLR_ACA_NOGRAPH=1: host-driven step loop (profilers see every launch)
+  if (nograph < 0) { const char *ev = getenv("HODLR_ACA_NOGRAPH"); nograph = ev && atoi(ev) ? 1 : 0; }
+  if (nbig > 0 && nograph) {
+    for (steps = 1; steps <= h->cap + 1; steps++) {
+      k_aca_pass<true><<<(unsigned)P->nitems_r, ACA_SUB, 0, h->st>>>(P->d_ctx);
+      HLAUNCH(h, "k_aca_pass<row>");
+      k_aca_pass<false><<<(unsigned)P->nitems_c, ACA_SUB, 0, h->st>>>(P->d_ctx + 1);
+      HLAUNCH(h, "k_aca_pass<col>");
+      int act = 0;
+      HCUDA(cudaMemcpyAsync(&act, h->dflags + 4, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+      HCUDA(cudaStreamSynchronize(h->st));
+      if (act <= 0) break;
+    }
+  } else if (nbig > 0) {
+    HCUDA(cudaGraphLaunch(P->ge, h->st));
+    hodlr_trace("aca: graph launched");
+  }
+  if (!P->fused_blocks.empty()) HCUDA(cudaStreamWaitEvent(h->st, h->ev_join, 0));
+  HCUDA(cudaEventRecord(h->ev_hi, h->sthi));
+  h->st = sm_main;
+  HCUDA(cudaStreamWaitEvent(h->st, h->ev_hi, 0));
   ph_end(h, PH_ACA);
   HCUDA(cudaStreamSynchronize(h->st));
-  if (status != HODLR_OK) return status;
-  if (nbig > 0) {
+  hodlr_trace("aca: synced");
+  if (nbig > 0 && !nograph) {
     HCUDA(cudaMemcpy(&steps, h->dflags + 6, sizeof(int), cudaMemcpyDeviceToHost));
-    h->launches += 3 * (steps - 1); hodlr_global_launches += 3 * (steps - 1);
+    h->launches += 3 * steps; hodlr_global_launches += 3 * steps;
   }
   h->aca_steps = steps;
   return HODLR_OK;

@@ -1,13 +1,28 @@
 // api.cu -- the C-ABI of include/hodlr.h: validation, host plan, memory, phase orchestration.
 #include "hodlr_internal.cuh"
 #include <stdio.h>
+#include <stdlib.h>
 #include <stdarg.h>
 #include <string.h>
 #include <limits.h>
 #include <new>
+#include <mutex>
 #include <vector>
 
+#include <chrono>
 static thread_local char g_err[1024] = "";
+
+void hodlr_trace(const char *what) {
+  static int on = -1;
+  if (on < 0) { const char *ev = getenv("HODLR_TRACE"); on = ev && atoi(ev) ? 1 : 0; }
+  if (!on) return;
+  static auto t0 = std::chrono::steady_clock::now();
+  static auto tl = t0;
+  auto now = std::chrono::steady_clock::now();
+  fprintf(stderr, "[hodlr %9.3f ms +%7.3f] %s\n", std::chrono::duration<double, std::milli>(now - t0).count(),
+          std::chrono::duration<double, std::milli>(now - tl).count(), what);
+  tl = now;
+}
 long long hodlr_global_launches = 0;
 
 hodlr_status hodlr_set_error(hodlr_status code, const char *fmt, ...) {
@@ -51,9 +66,12 @@ static hodlr_status finish(hodlr_s *h, hodlr_status st, double *tsec) {
   if (cudaEventElapsedTime(&ms, h->ev0, h->ev1) == cudaSuccess && tsec) *tsec = ms * 1e-3;
   for (int p = 0; p < PH_N; p++) {
     if (!h->ph_pending[p]) continue;
-    float pm = 0.f;
-    if (cudaEventElapsedTime(&pm, h->ph_ev[p][0], h->ph_ev[p][1]) == cudaSuccess) { h->ph_ms[p] += pm; h->ph_calls[p]++; }
-    h->ph_pending[p] = 0;
+    float pm = 0.f;   // side-stream phases may still be running: keep them pending until they complete
+    if (cudaEventElapsedTime(&pm, h->ph_ev[p][0], h->ph_ev[p][1]) == cudaSuccess) {
+      h->ph_ms[p] += pm; h->ph_calls[p]++; h->ph_pending[p] = 0;
+    } else {
+      cudaGetLastError();
+    }
   }
   return HODLR_OK;
 }
@@ -64,16 +82,61 @@ const char *hodlr_last_error(void) { return g_err; }
 const char *hodlr_version(void) { return "hodlr_b200 0.1 sm_100a fp64"; }
 int64_t hodlr_launch_count(void) { return hodlr_global_launches; }
 
+// Streams and events are pooled per device across handles (creating and destroying them per handle costs
+// more host time than a small factorization).
+struct HRes {
+  int dev;
+  cudaStream_t st2, st3, sthi;
+  cudaEvent_t ev0, ev1, ev_fork, ev_join, ev_chol, ev_hi;
+  cudaEvent_t ph_ev[PH_N][2];
+};
+static std::mutex g_res_mu;
+static std::vector<HRes> g_res_pool;
+
+static void res_acquire(hodlr_s *h) {
+  HRes r;
+  bool got = false;
+  {
+    std::lock_guard<std::mutex> lk(g_res_mu);
+    for (size_t i = 0; i < g_res_pool.size(); i++)
+      if (g_res_pool[i].dev == h->dev) { r = g_res_pool[i]; g_res_pool.erase(g_res_pool.begin() + i); got = true; break; }
+  }
+  if (!got) {
+    r.dev = h->dev;
+    cudaEventCreate(&r.ev0); cudaEventCreate(&r.ev1);
+    cudaEventCreateWithFlags(&r.ev_fork, cudaEventDisableTiming); cudaEventCreateWithFlags(&r.ev_join, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&r.ev_chol, cudaEventDisableTiming);
+    cudaStreamCreateWithFlags(&r.st2, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&r.st3, cudaStreamNonBlocking);
+    int lo_pri = 0, hi_pri = 0;
+    cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri);
+    cudaStreamCreateWithPriority(&r.sthi, cudaStreamNonBlocking, hi_pri);
+    cudaEventCreateWithFlags(&r.ev_hi, cudaEventDisableTiming);
+    for (int p = 0; p < PH_N; p++) for (int j = 0; j < 2; j++) cudaEventCreate(&r.ph_ev[p][j]);
+  }
+  h->st2 = r.st2; h->st3 = r.st3; h->ev0 = r.ev0; h->ev1 = r.ev1; h->ev_fork = r.ev_fork; h->ev_join = r.ev_join;
+  h->ev_chol = r.ev_chol; h->sthi = r.sthi; h->ev_hi = r.ev_hi;
+  for (int p = 0; p < PH_N; p++) for (int j = 0; j < 2; j++) h->ph_ev[p][j] = r.ph_ev[p][j];
+}
+
+static void res_release(hodlr_s *h) {
+  if (!h->st2) return;
+  HRes r;
+  r.dev = h->dev; r.st2 = h->st2; r.st3 = h->st3; r.ev0 = h->ev0; r.ev1 = h->ev1; r.ev_fork = h->ev_fork;
+  r.ev_join = h->ev_join; r.ev_chol = h->ev_chol; r.sthi = h->sthi; r.ev_hi = h->ev_hi;
+  for (int p = 0; p < PH_N; p++) for (int j = 0; j < 2; j++) r.ph_ev[p][j] = h->ph_ev[p][j];
+  std::lock_guard<std::mutex> lk(g_res_mu);
+  g_res_pool.push_back(r);
+}
+
 void hodlr_free(hodlr_t h) {
   if (!h) return;
+  if (h->st3 && h->ev_chol) { cudaEventRecord(h->ev_chol, h->st3); cudaStreamWaitEvent(h->st, h->ev_chol, 0); }
   for (int i = h->nallocs - 1; i >= 0; i--) cudaFreeAsync(h->allocs[i], h->st);
+  if (h->st3) cudaStreamSynchronize(h->st3);
+  if (h->st2) cudaStreamSynchronize(h->st2);
   cudaStreamSynchronize(h->st);
-  if (h->st2) cudaStreamDestroy(h->st2);
-  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
-  if (h->ev_join) cudaEventDestroy(h->ev_join);
-  if (h->ev0) cudaEventDestroy(h->ev0);
-  if (h->ev1) cudaEventDestroy(h->ev1);
-  for (int p = 0; p < PH_N; p++) for (int j = 0; j < 2; j++) if (h->ph_ev[p][j]) cudaEventDestroy(h->ph_ev[p][j]);
+  res_release(h);
   delete[] h->h_lo; delete[] h->h_hi; delete[] h->h_rank;
   delete h;
 }
@@ -102,10 +165,7 @@ hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const 
   cudaError_t ce = cudaGetDevice(&h->dev);
   if (ce != cudaSuccess) { delete h; return hodlr_cuda_check(ce, "cudaGetDevice"); }
   setup_pool(h->dev);
-  cudaEventCreate(&h->ev0); cudaEventCreate(&h->ev1);
-  cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming); cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming);
-  cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking);
-  for (int p = 0; p < PH_N; p++) for (int j = 0; j < 2; j++) cudaEventCreate(&h->ph_ev[p][j]);
+  res_acquire(h);
   cudaEventRecord(h->ev0, h->st);
   h->launches = 0;
   h->n = n; h->leaf = leaf; h->eps = eps; h->cap = cap; h->theta[0] = theta[0]; h->theta[1] = theta[1];
@@ -159,10 +219,29 @@ hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const 
   CK(cudaMemcpyAsync(h->lo, h->h_lo, sizeof(long long) * h->nnodes, cudaMemcpyHostToDevice, h->st));
   CK(cudaMemcpyAsync(h->hi, h->h_hi, sizeof(long long) * h->nnodes, cudaMemcpyHostToDevice, h->st));
   CK(cudaMemcpyAsync(h->d_dt, &h->dt, sizeof(DepthTab), cudaMemcpyHostToDevice, h->st));
+  hodlr_trace("build: enter");
   st = hodlr_sort_and_tree(h, x);
+  hodlr_trace("build: sort done (synced)");
   if (st != HODLR_OK) goto fail;
   if (h->x_nonfinite) { st = hodlr_set_error(HODLR_EINVAL, "build: x contains NaN or Inf"); goto fail; }
+  // The leaf Cholesky factors (part of "Factor", Fig. 6 line 7) do not depend on the compression: they are
+  // issued now on a side stream and overlap the ACA; hodlr_factor waits for them.
+  st = hodlr_leaf_alloc(h);
+  if (st != HODLR_OK) goto fail;
+  {
+    bool launched = false;
+    CK(cudaEventRecord(h->ev_fork, h->st));
+    CK(cudaStreamWaitEvent(h->st3, h->ev_fork, 0));
+    ph_begin(h, PH_CHOL, h->st3);
+    st = hodlr_leaf_chol_mma(h, h->st3, &launched);
+    if (st != HODLR_OK) goto fail;
+    ph_end(h, PH_CHOL, h->st3);
+    CK(cudaEventRecord(h->ev_chol, h->st3));
+    h->chol_done = launched ? 1 : 0;
+  }
+  hodlr_trace("build: chol launched");
   st = hodlr_aca(h);
+  hodlr_trace("build: aca returned");
   if (st != HODLR_OK) goto fail;
   {
     int f5 = 0;
@@ -182,6 +261,7 @@ hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const 
   }
   CK(cudaMemcpyAsync(h->d_dt, &h->dt, sizeof(DepthTab), cudaMemcpyHostToDevice, h->st));
   st = finish(h, HODLR_OK, &h->t_build);
+  hodlr_trace("build: finished");
   if (st != HODLR_OK) goto fail;
   h->state = 1;
   *out = h;
@@ -198,8 +278,11 @@ hodlr_status hodlr_factor(hodlr_t h) {
   if (h->state != 1) return hodlr_set_error(HODLR_ESTATE, "factor: handle is not in the built state");
   h->launches = 0;
   cudaEventRecord(h->ev0, h->st);
+  hodlr_trace("factor: enter");
   hodlr_status st = hodlr_factor_impl(h);
+  hodlr_trace("factor: launched");
   st = finish(h, st, &h->t_factor);
+  hodlr_trace("factor: finished");
   if (st != HODLR_OK) { h->state = -1; h->logdet = -INFINITY; return st; }
   int f[3];
   cudaError_t e = cudaMemcpy(f, h->dflags, sizeof(f), cudaMemcpyDeviceToHost);

@@ -99,35 +99,18 @@ __global__ void __launch_bounds__(LT) k_leaf_factor(LeafCtx c) {
       c.leaf_ld[leaf] = 2.0 * s;
       if (bad) { atomicAdd(&c.flags[1], 1); atomicMin(&c.flags[2], (int)id); }
     }
-    // L as fragment-order tiles (identity padding) and the inverse diagonal tiles
+    // X = L^{-1} as fragment-order tiles (identity padding beyond m): forward substitution L x = e_j,
+    // one thread per column (fallback path; the fast path forms X on the tensor pipe)
     const int T = c.T, NT = T * (T + 1) / 2;
     double *Lg = c.Lf + leaf * c.lstride;
-    for (long long p = t; p < (long long)NT * 64; p += LT) {
-      const int ti = (int)(p >> 6), e = (int)(p & 63);
-      int I = 0;
-      while ((I + 1) * (I + 2) / 2 <= ti) I++;
-      const int J = ti - I * (I + 1) / 2;
-      const int cc = (e >> 5) * 4 + (e & 3), r = (e & 31) >> 2;
-      const long long i = 8 * I + r, j = 8 * J + cc;
-      Lg[p] = (i < m && j <= i) ? L[P(i, j)] : (i == j ? 1.0 : 0.0);
-    }
-    for (int b = t; b < T; b += LT) {          // Linv(b): forward substitution on the 8x8 diagonal tile
-      double l[8][8];
-      for (int i = 0; i < 8; i++)
-        for (int j = 0; j <= i; j++) {
-          const long long gi = 8 * b + i, gj = 8 * b + j;
-          l[i][j] = gi < m ? L[P(gi, gj)] : (i == j ? 1.0 : 0.0);
-        }
-      double *li = Lg + (long long)(NT + b) * 64;
-      for (int cc = 0; cc < 8; cc++) {
-        double y[8];
-        for (int i = 0; i < 8; i++) {
-          if (i < cc) { y[i] = 0.0; continue; }
-          double s = (i == cc) ? 1.0 : 0.0;
-          for (int k = cc; k < i; k++) s -= l[i][k] * y[k];
-          y[i] = s / l[i][i];
-        }
-        for (int i = 0; i < 8; i++) li[fo(i, cc)] = y[i];
+    for (long long p = t; p < (long long)NT * 64; p += LT) Lg[p] = 0.0;
+    __syncthreads();
+    for (int j = t; j < 8 * T; j += LT) {
+      if (j >= m) { Lg[tix(j >> 3, j >> 3) * 64 + fo(j & 7, j & 7)] = 1.0; continue; }
+      for (int i = j; i < m; i++) {
+        double s = i == j ? 1.0 : 0.0;
+        for (int k = j; k < i; k++) s -= L[P(i, k)] * Lg[tix(k >> 3, j >> 3) * 64 + fo(k & 7, j & 7)];
+        Lg[tix(i >> 3, j >> 3) * 64 + fo(i & 7, j & 7)] = s / L[P(i, i)];
       }
     }
     if (K > 0) {
@@ -187,7 +170,7 @@ struct TreeCtx {
 
 // Shared-memory footprint of one node (doubles), see tree_node().
 __host__ __device__ __forceinline__ long long tree_smem_doubles(int q, int ldk) {
-  return 3LL * q * q + 5LL * q + 4LL * q * ldk;
+  return 3LL * q * q + 6LL * q + 4LL * q * ldk;
 }
 
 // One CTA per depth-d node c (heap index (2^d - 1) + i):
@@ -208,13 +191,13 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm) {
   double *S0 = W + q * q2;           // q x q
   double *rowk = S0 + q * q;         // 2q
   double *rowold = rowk + q2;        // 2q
-  double *colk = rowold + q2;        // q
-  double *B = colk + q;              // q x ldk
+  double *colk = rowold + q2;        // q: |U_kk|
+  double *mult = colk + q;           // q: elimination multipliers of the current step
+  double *B = mult + q;              // q x ldk
   double *Th = B + (long long)q * ldk;
   double *Tl = Th + (long long)q * ldk;
   double *R = Tl + (long long)q * ldk;
-  __shared__ int s_p, s_zero, s_sign, s_nref;
-  __shared__ double s_la, s_umax, s_umin;
+  __shared__ int s_zero, s_sign, s_nref, s_p;
   for (int p = t; p < q * q2; p += NT) {
     const int a = p / q2, b = p - a * q2;
     double v;
@@ -227,63 +210,78 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm) {
     }
     W[p] = v;
   }
-  for (long long p = t; p < (long long)q * ldk; p += NT) {
-    const int a = (int)(p / ldk), b = (int)(p - (long long)a * ldk);
+  for (int p = t; p < q * ldk; p += NT) {
+    const int a = p / ldk, b = p - a * ldk;
     double v = 0.0;
     if (b < Kd) v = a < r ? P2[pk(Kd + a, b)] : P1[pk(Kd + a - r, b)];
     B[p] = v; Tl[p] = 0.0;
   }
-  if (t == 0) { s_zero = 0; s_sign = 1; s_la = 0.0; s_umax = 0.0; s_umin = 1e300; }
   __syncthreads();
   // ---------------- Gauss-Jordan with partial pivoting ----------------
-  for (int k = 0; k < q; k++) {
-    if (t < 32) {
+  // q <= 16: warp 0 alone (no CTA barriers); larger systems: the whole CTA, 3 barriers per step.
+  const bool warp_gj = q <= 16;
+  if (!warp_gj || t < 32) {
+    const int lane = t & 31;
+    const int nthr = warp_gj ? 32 : NT;
+    int sign = 1, zero = 0;
+    for (int k = 0; k < q; k++) {
       int p = k; double best = -1.0;
-      for (int a = k + t; a < q; a += 32) { const double v = fabs(W[a * q2 + k]); if (v > best) { best = v; p = a; } }
+      if (t < 32) {
+        for (int a = k + lane; a < q; a += 32) { const double v = fabs(W[a * q2 + k]); if (v > best) { best = v; p = a; } }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double b2 = __shfl_down_sync(0xffffffffu, best, o); const int p2 = __shfl_down_sync(0xffffffffu, p, o);
-        if (b2 > best || (b2 == best && p2 < p)) { best = b2; p = p2; }
+        for (int o = 16; o > 0; o >>= 1) {   // xor butterfly: every lane ends with the same (best, p)
+          const double b2 = __shfl_xor_sync(0xffffffffu, best, o); const int p2 = __shfl_xor_sync(0xffffffffu, p, o);
+          if (b2 > best || (b2 == best && p2 < p)) { best = b2; p = p2; }
+        }
+        if (lane == 0) { colk[k] = best; s_p = p; }           // |U_kk| (log det below)
       }
-      if (t == 0) {
-        s_p = p;
-        const double u = W[p * q2 + k];
-        if (p != k) s_sign = -s_sign;
-        if (u < 0.0) s_sign = -s_sign;
-        if (!(best > 0.0)) s_zero = 1;
-        else { s_la += log(best); s_umax = fmax(s_umax, best); s_umin = fmin(s_umin, best); }
+      if (warp_gj) __syncwarp(); else __syncthreads();
+      p = s_p;
+      const double piv = W[p * q2 + k];
+      if (p != k) sign = -sign;
+      if (piv < 0.0) sign = -sign;
+      if (!(piv != 0.0)) zero = 1;
+      for (int j = t; j < q2; j += nthr) { rowk[j] = W[p * q2 + j]; rowold[j] = W[k * q2 + j]; }
+      for (int a = t; a < q; a += nthr) mult[a] = a == k ? 0.0 : (a == p ? W[k * q2 + k] : W[a * q2 + k]);
+      if (warp_gj) __syncwarp(); else __syncthreads();
+      const double ip = piv != 0.0 ? 1.0 / piv : 0.0;
+      for (int e = t; e < q * q2; e += nthr) {
+        const int a = e / q2, j = e - a * q2;
+        if (a == k) W[e] = rowk[j] * ip;
+        else {
+          const double src = a == p ? rowold[j] : W[e];
+          W[e] = fma(-mult[a] * ip, rowk[j], src);
+        }
       }
+      if (warp_gj) __syncwarp(); else __syncthreads();
     }
-    __syncthreads();
-    const int p = s_p;
-    for (int j = t; j < q2; j += NT) { rowk[j] = W[p * q2 + j]; rowold[j] = W[k * q2 + j]; }
-    for (int a = t; a < q; a += NT) colk[a] = W[(a == k ? p : (a == p ? k : a)) * q2 + k];
-    __syncthreads();
-    const double piv = rowk[k];
-    const double ip = piv != 0.0 ? 1.0 / piv : 0.0;
-    for (int e = t; e < q * q2; e += NT) {
-      const int a = e / q2, j = e - a * q2;
-      if (a == k) W[e] = rowk[j] * ip;
-      else {
-        const double src = a == p ? rowold[j] : W[e];
-        W[e] = fma(-colk[a] * ip, rowk[j], src);
-      }
-    }
-    __syncthreads();
-  }
-  const bool zero = s_zero != 0;
-  if (t == 0) {
-    c.node_ld[node] = s_la;
-    if (zero || s_sign <= 0) { atomicAdd(&c.flags[1], 1); atomicMin(&c.flags[2], (int)node); }
-    // refinement steps: one when the pivot growth ratio is mild, two otherwise (cond(S_c) up to ~1e12)
-    s_nref = (!zero && s_umax < 1e6 * s_umin) ? 1 : 2;
+    if (t == 0) { s_sign = sign; s_zero = zero; }
   }
   __syncthreads();
+  if (t < 32) {                                 // log|det S_c| = sum_k log|U_kk|, fixed-order warp reduction
+    double la = 0.0, umax = 0.0, umin = 1e300;
+    for (int k = t; k < q; k += 32) { const double u = colk[k]; la += log(u); umax = fmax(umax, u); umin = fmin(umin, u); }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      la += __shfl_xor_sync(0xffffffffu, la, o);
+      umax = fmax(umax, __shfl_xor_sync(0xffffffffu, umax, o));
+      umin = fmin(umin, __shfl_xor_sync(0xffffffffu, umin, o));
+    }
+    if (t == 0) {
+      const bool zero = s_zero != 0;
+      c.node_ld[node] = la;
+      if (zero || s_sign <= 0) { atomicAdd(&c.flags[1], 1); atomicMin(&c.flags[2], (int)node); }
+      // refinement steps: one when the pivot growth ratio is mild, two otherwise (cond(S_c) up to ~1e12)
+      s_nref = (!zero && umax < 1e6 * umin) ? 1 : 2;
+    }
+  }
+  __syncthreads();
+  const bool zero = s_zero != 0;
   const double *Si = W + q;           // S^{-1}, row stride 2q
   if (!zero && Kd > 0) {
-    const long long qK = (long long)q * ldk;
-    for (long long e = t; e < qK; e += NT) {          // T_hi = S^{-1} B
-      const int a = (int)(e / ldk), col = (int)(e - (long long)a * ldk);
+    const int qK = q * ldk;
+    for (int e = t; e < qK; e += NT) {                // T_hi = S^{-1} B
+      const int a = e / ldk, col = e - a * ldk;
       double s = 0.0;
       for (int j = 0; j < q; j++) s = fma(Si[a * q2 + j], B[j * ldk + col], s);
       Th[e] = s;
@@ -291,8 +289,8 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm) {
     __syncthreads();
     const int nref = s_nref;
     for (int it = 0; it < nref; it++) {               // iterative refinement, residual compensated
-      for (long long e = t; e < qK; e += NT) {
-        const int a = (int)(e / ldk), col = (int)(e - (long long)a * ldk);
+      for (int e = t; e < qK; e += NT) {
+        const int a = e / ldk, col = e - a * ldk;
         if (DD) {
           Acc2 A = acc2(B[e]);
           for (int k = 0; k < q; k++) acc_fma_dd(A, -S0[a * q + k], Th[k * ldk + col], Tl[k * ldk + col]);
@@ -304,8 +302,8 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm) {
         }
       }
       __syncthreads();
-      for (long long e = t; e < qK; e += NT) {
-        const int a = (int)(e / ldk), col = (int)(e - (long long)a * ldk);
+      for (int e = t; e < qK; e += NT) {
+        const int a = e / ldk, col = e - a * ldk;
         double s = 0.0;
         for (int j = 0; j < q; j++) s = fma(Si[a * q2 + j], R[j * ldk + col], s);
         Tl[e] += s;
@@ -434,6 +432,20 @@ __global__ void k_logdet_reduce(const double *leaf_ld, const double *node_ld, lo
 
 }  // namespace
 
+// Leaf factor storage (T = ceil(leaf_max / 8) tile rows, or 8 / 16 on the fast path): allocated at build time
+// because the leaf Cholesky runs during the build.
+hodlr_status hodlr_leaf_alloc(hodlr_s *h) {
+  const int mmax = h->leaf_max;
+  const int Pfast = mmax <= 64 ? 64 : (mmax <= 128 ? 128 : 0);
+  const long long nl = h->nleaves;
+  h->ltiles = Pfast ? Pfast / 8 : (mmax + 7) / 8;
+  h->lstride = (long long)(h->ltiles * (h->ltiles + 1) / 2) * 64;      // tiles of X = L^{-1}
+  h->Lf = (double *)hodlr_dalloc(h, sizeof(double) * h->lstride * nl);
+  h->leaf_ld = (double *)hodlr_dalloc(h, sizeof(double) * nl);
+  if (!h->Lf || !h->leaf_ld) return hodlr_set_error(HODLR_ENOMEM, "leaf factor allocation failed");
+  return HODLR_OK;
+}
+
 hodlr_status hodlr_factor_impl(hodlr_s *h) {
   const int kappa = h->kappa;
   DepthTab &dt = h->dt;
@@ -441,11 +453,6 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
   const long long nl = h->nleaves;
   // ---- storage ----
   const int mmax = h->leaf_max;
-  const int Pfast = mmax <= 64 ? 64 : (mmax <= 128 ? 128 : 0);
-  h->ltiles = Pfast ? Pfast / 8 : (mmax + 7) / 8;
-  h->lstride = (long long)(h->ltiles * (h->ltiles + 1) / 2 + h->ltiles) * 64;
-  h->Lf = (double *)hodlr_dalloc(h, sizeof(double) * h->lstride * nl);
-  h->leaf_ld = (double *)hodlr_dalloc(h, sizeof(double) * nl);
   h->node_ld = (double *)hodlr_dalloc(h, sizeof(double) * (h->ninternal > 0 ? h->ninternal : 1));
   h->d_logdet = (double *)hodlr_dalloc(h, sizeof(double));
   long long piTot = 0, sTot = 0, btTot = 0;
@@ -461,17 +468,18 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
   h->Pipool = (double *)hodlr_dalloc(h, sizeof(double) * (piTot > 0 ? piTot : 1));
   h->Spool = (double *)hodlr_dalloc(h, sizeof(double) * (sTot > 0 ? sTot : 1));
   h->BTpool = (double *)hodlr_dalloc(h, sizeof(double) * (btTot > 0 ? btTot : 1));
-  if (!h->Lf || !h->leaf_ld || !h->node_ld || !h->d_logdet || !h->Pipool || !h->Spool || !h->BTpool)
+  if (!h->node_ld || !h->d_logdet || !h->Pipool || !h->Spool || !h->BTpool)
     return hodlr_set_error(HODLR_ENOMEM, "factor: device allocation failed");
   HCUDA(cudaMemcpyAsync(h->d_dt, &dt, sizeof(DepthTab), cudaMemcpyHostToDevice, h->st));
   if (K > 1024) return hodlr_set_error(HODLR_EINVAL, "factor: K = %d ancestor columns exceeds 1024", K);
   int maxsm = 0;
   HCUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
   // ---- leaves ----
+  HCUDA(cudaStreamWaitEvent(h->st, h->ev_chol, 0));     // leaf Cholesky issued during the build
   ph_begin(h, PH_LEAF);
   bool fast = false;
-  if (Pfast) {
-    hodlr_status fs = hodlr_leaf_factor_mma(h, K, h->Pipool + dt.piOff[kappa], &fast);
+  {
+    hodlr_status fs = hodlr_leaf_factor_mma(h, K, h->Pipool + dt.piOff[kappa], &fast);   // needs the Cholesky kernel
     if (fs != HODLR_OK) return fs;
   }
   if (!fast) {

@@ -90,13 +90,16 @@ struct AcaCtx {
   const int *bdepth;        // depth of each internal block
   DepthTab *dt;             // device copy
   const int *bigidx;        // block -> ordinal among the step-synchronous (big) blocks, -1 otherwise
+  int *flags;               // handle flags (rank-cap hits in [5])
+  int *step;                // step counter of the device loop
+  int maxsteps;
   double *gram;             // per big block: packed G_U = U'^T U', then G_V = V'^T V' 
 };
 
 // ----------------------------------------------------------------------------------------------
 // Per-kernel-family device timing (CUDA events on the handle's stream)
 // ----------------------------------------------------------------------------------------------
-enum { PH_SORT = 0, PH_ACA, PH_LEAF, PH_TREE, PH_SLEAF_UP, PH_STREE, PH_SLEAF_DOWN, PH_N };
+enum { PH_SORT = 0, PH_ACA, PH_LEAF, PH_TREE, PH_SLEAF_UP, PH_STREE, PH_SLEAF_DOWN, PH_CHOL, PH_N };
 
 // ----------------------------------------------------------------------------------------------
 // Handle
@@ -104,7 +107,11 @@ enum { PH_SORT = 0, PH_ACA, PH_LEAF, PH_TREE, PH_SLEAF_UP, PH_STREE, PH_SLEAF_DO
 struct hodlr_s {
   cudaStream_t st;
   cudaStream_t st2;           // side stream (fused small-block ACA)
-  cudaEvent_t ev_fork, ev_join;
+  cudaStream_t st3;           // side stream (leaf Cholesky, overlapping the ACA)
+  cudaStream_t sthi;          // high-priority stream (ACA step loop)
+  cudaEvent_t ev_hi;
+  cudaEvent_t ev_fork, ev_join, ev_chol;
+  int chol_done;              // the leaf Cholesky kernel was issued on st3 (fast path)
   int dev;
   long long n;
   KParams kp;
@@ -155,8 +162,11 @@ struct hodlr_s {
   void *allocs[64]; int nallocs;
 };
 
-static inline void ph_begin(hodlr_s *h, int p) { cudaEventRecord(h->ph_ev[p][0], h->st); }
-static inline void ph_end(hodlr_s *h, int p) { cudaEventRecord(h->ph_ev[p][1], h->st); h->ph_pending[p] = 1; }
+static inline void ph_begin(hodlr_s *h, int p, cudaStream_t s = nullptr) { cudaEventRecord(h->ph_ev[p][0], s ? s : h->st); }
+static inline void ph_end(hodlr_s *h, int p, cudaStream_t s = nullptr) { cudaEventRecord(h->ph_ev[p][1], s ? s : h->st); h->ph_pending[p] = 1; }
+
+// HODLR_TRACE=1: host timestamps of the orchestration steps on stderr (development aid)
+void hodlr_trace(const char *what);
 
 // helpers implemented in api.cu
 hodlr_status hodlr_set_error(hodlr_status code, const char *fmt, ...);
@@ -169,6 +179,8 @@ hodlr_status hodlr_sort_and_tree(hodlr_s *h, const double *x);
 hodlr_status hodlr_aca(hodlr_s *h);
 hodlr_status hodlr_factor_impl(hodlr_s *h);
 hodlr_status hodlr_leaf_factor_mma(hodlr_s *h, int K, double *Pi_leaf, bool *used);
+hodlr_status hodlr_leaf_chol_mma(hodlr_s *h, cudaStream_t stream, bool *launched);
+hodlr_status hodlr_leaf_alloc(hodlr_s *h);
 hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_only);
 
 static inline int hodlr_depth_of(long long id) { int d = 0; while (id >= ((2LL << d) - 1)) d++; return d; }

@@ -1,5 +1,7 @@
 // leaf_mma.cu -- G4/G5 fast path: per-leaf Cholesky, panel solve and projected Gram on the FP64
-// tensor pipe (mma.sync f64, "DMMA"), one CTA per leaf, everything resident on chip.
+// tensor pipe (mma.sync f64, "DMMA"), one CTA per leaf, everything resident on chip.  Two kernels:
+// k_leaf_chol (no dependence on the ACA: runs on a side stream during the build) and k_leaf_zsyrk
+// (Z and Pi after the ACA).
 //
 // For a leaf l with rows [lo, lo+m), m <= P (P = 64 or 128), and its ancestor-factor panel
 // E_l = Xh[l rows, K columns] (Fig. 6 lines 7-12):
@@ -114,66 +116,41 @@ __device__ void potrf8(double *tile, double *linv, double *diag8, int *bad) {
   __syncwarp();
 }
 
+// Column map of leaf `id`: local column q (depth e block, Kdim[e-1] <= q < Kdim[e]) -> global Xh column, or -1
+// beyond the rank of that ancestor's block.  One thread per column (no serial walk).
+__device__ __forceinline__ long long leaf_colsrc(const LeafMmaCtx &c, long long id, int q) {
+  if (q >= c.K) return -1;
+  int e = 1;
+  while (c.dt->Kdim[e] <= q) e++;
+  const int qq = q - c.dt->Kdim[e - 1];
+  const long long b = ((id + 1) >> (c.kappa - e + 1)) - 1;     // ancestor at depth e - 1 (heap order)
+  return qq < c.rank[b] ? c.dt->colbase[e] + qq : -1;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Kernel 1 (does not depend on the ACA; launched on a side stream during the build):
+//   A_l = K[l,l] + s2 I = L L^T, left-looking over 8-column tiles, 2 CTAs per SM; then X = L^{-1}
+//   (column sweeps on the FP64 tensor pipe); writes the tiles of X and the log det partial 2 sum log L_ii.
+//   Only X is kept: Z = X E is a GEMM and the solve's triangular solves become matrix-vector products
+//   (explicit triangular inverse: DESIGN.md R6).
+// ---------------------------------------------------------------------------------------------
 template <int P>
-__global__ void __launch_bounds__(NTH, 1) k_leaf_factor_mma(LeafMmaCtx c) {
+__global__ void __launch_bounds__(NTH, 2) k_leaf_chol(LeafMmaCtx c) {
   constexpr int T = P / 8;
   constexpr int NTILE = T * (T + 1) / 2;
-  constexpr int LDR = P + 4;
   extern __shared__ double sm[];
   __shared__ int bad;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int K = c.K, Kp = c.Kp, Kc = Kp / 8, Kz = c.Kz;   // Kz = columns allocated in sZ (multiple of 16)
   double *sL = sm;                              // NTILE * 64
   double *sLi = sL + NTILE * 64;                // T * 64
-  double *sZ = sLi + T * 64;                    // Kz * LDR (column-major)
-  double *sx = sZ + (long long)Kz * LDR;        // P
+  double *sx = sLi + T * 64;                    // P
   double *sdiag = sx + P;                       // P
-  long long *colsrc = (long long *)(sdiag + P); // Kz
   const long long leaf = blockIdx.x;
   const long long id = c.ninternal + leaf, lo = c.lo[id];
   const int m = (int)(c.hi[id] - lo);
   if (t == 0) bad = 0;
   for (int i = t; i < P; i += NTH) sx[i] = i < m ? c.xs[lo + i] : 0.0;
-  if (t == 0) {   // ancestor column map: depth 1..kappa, zero beyond each ancestor block's rank
-    long long a = id;
-    for (int e = c.kappa; e >= 1; e--) {
-      long long b = (a - 1) / 2;
-      int rb = c.rank[b];
-      for (int q = 0; q < c.dt->rdep[e]; q++) colsrc[c.dt->Kdim[e - 1] + q] = q < rb ? c.dt->colbase[e] + q : -1;
-      a = b;
-    }
-    for (int q = K; q < Kz; q++) colsrc[q] = -1;
-  }
   __syncthreads();
-  // E_l -> sZ (column-major), asynchronous copies overlapped with the assembly and the Cholesky
-  const bool al16 = ((c.n | lo) & 1) == 0;      // 16-byte aligned column segments (row pairs)
-  if (al16) {
-    for (int p = t; p < Kz * (P / 2); p += NTH) {
-      const int col = p / (P / 2), row = 2 * (p - col * (P / 2));
-      const long long src = colsrc[col];
-      double *dst = sZ + col * LDR + row;
-      if (src >= 0 && row + 1 < m) {
-        unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(sa), "l"(c.Xh + src * c.n + lo + row));
-      } else {
-        dst[0] = (src >= 0 && row < m) ? c.Xh[src * c.n + lo + row] : 0.0;
-        dst[1] = 0.0;
-      }
-    }
-  } else {
-    for (int p = t; p < Kz * P; p += NTH) {
-      const int col = p / P, row = p - col * P;
-      const long long src = colsrc[col];
-      double *dst = sZ + col * LDR + row;
-      if (src >= 0 && row < m) {
-        unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" :: "r"(sa), "l"(c.Xh + src * c.n + lo + row));
-      } else {
-        *dst = 0.0;
-      }
-    }
-  }
-  asm volatile("cp.async.commit_group;\n" ::);
   // assemble A_l = K[l,l] + s2 I into the lower tiles (fragment order), identity padding beyond m
   for (int ti = warp; ti < NTILE; ti += NW) {
     const int I = c_tileI[ti], J = c_tileJ[ti];
@@ -246,20 +223,33 @@ __global__ void __launch_bounds__(NTH, 1) k_leaf_factor_mma(LeafMmaCtx c) {
     }
     __syncthreads();
   }
-  asm volatile("cp.async.wait_group 0;\n" ::);
-  __syncthreads();
-  // ---------------- Z = L^{-1} E, register-resident per warp (tiles cc = warp, warp + 8) ----------------
+  if (warp == 0) {          // 2 sum log L_ii: per-lane partials, then a fixed-order warp reduction
+    double s2 = 0.0;
+    for (int i = lane; i < m; i += 32) s2 += log(sdiag[i]);
+    s2 = warp_sum(s2);
+    if (lane == 0) {
+      c.leaf_ld[leaf] = 2.0 * s2;
+      if (bad) { atomicAdd(&c.flags[1], 1); atomicMin(&c.flags[2], (int)id); }
+    }
+  }
+  // ---- X = L^{-1} (lower, fragment-order tiles) written straight to global: column sweep with E = I,
+  // tile column J by one warp (pairs J = warp, T-1-warp balance the work), L read from shared memory ----
+  double *Xg = c.Lf + leaf * c.lstride;
   {
     const int g = lane >> 2, q2 = 2 * (lane & 3);
-    for (int cc = warp; cc < Kc; cc += NW) {
+    const int cp = cpos(lane);
+    for (int pass = 0; pass < 2; pass++) {
+      const int J = pass ? T - 1 - warp : warp;
+      if (J >= T || (pass && J < NW)) break;
       double z[T][2];
 #pragma unroll
       for (int i = 0; i < T; i++) {
-        z[i][0] = sZ[(8 * cc + q2) * LDR + 8 * i + g];
-        z[i][1] = sZ[(8 * cc + q2 + 1) * LDR + 8 * i + g];
+        z[i][0] = (i == J && g == q2) ? 1.0 : 0.0;
+        z[i][1] = (i == J && g == q2 + 1) ? 1.0 : 0.0;
       }
 #pragma unroll
       for (int b = 0; b < T; b++) {
+        if (b < J) continue;
         const double *Li = sLi + b * 64;
         double b0, b1;
         c_to_b(z[b][0], z[b][1], lane, b0, b1);
@@ -277,24 +267,97 @@ __global__ void __launch_bounds__(NTH, 1) k_leaf_factor_mma(LeafMmaCtx c) {
       }
 #pragma unroll
       for (int i = 0; i < T; i++) {
-        sZ[(8 * cc + q2) * LDR + 8 * i + g] = z[i][0];
-        sZ[(8 * cc + q2 + 1) * LDR + 8 * i + g] = z[i][1];
+        if (i < J) continue;
+        double2 v; v.x = z[i][0]; v.y = z[i][1];
+        *(double2 *)(Xg + tix(i, J) * 64 + cp) = v;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Kernel 2 (after the ACA): Z = X E_l (X = L^{-1}) and Pi_l = Z^T Z.  16 warps; X tiles and E staged with
+// 16-byte cp.async; every warp computes 8-column tiles of Z as a GEMM on the FP64 tensor pipe.
+// ---------------------------------------------------------------------------------------------
+constexpr int ZTH = 512;
+constexpr int ZW = ZTH / 32;
+
+template <int P>
+__global__ void __launch_bounds__(ZTH, 1) k_leaf_zsyrk(LeafMmaCtx c) {
+  constexpr int T = P / 8;
+  constexpr int NTILE = T * (T + 1) / 2;
+  constexpr int LDR = P + 4;
+  extern __shared__ double sm[];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int K = c.K, Kp = c.Kp, Kc = Kp / 8, Kz = c.Kz;
+  double *sX = sm;                              // NTILE * 64: tiles of X = L^{-1}
+  double *sZ = sX + NTILE * 64;                 // Kz * LDR (column-major)
+  long long *colsrc = (long long *)(sZ + (long long)Kz * LDR);   // Kz
+  const long long leaf = blockIdx.x;
+  const long long id = c.ninternal + leaf, lo = c.lo[id];
+  const int m = (int)(c.hi[id] - lo);
+  {
+    const double *Lg = c.Lf + leaf * c.lstride;
+    for (int p = t; p < NTILE * 32; p += ZTH) {
+      unsigned sa = (unsigned)__cvta_generic_to_shared(sX + 2 * p);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(sa), "l"(Lg + 2 * p));
+    }
+  }
+  for (int q = t; q < Kz; q += ZTH) colsrc[q] = leaf_colsrc(c, id, q);
+  __syncthreads();
+  const bool al16 = ((c.n | lo) & 1) == 0;      // 16-byte aligned column segments (row pairs)
+  if (al16) {
+    for (int p = t; p < Kz * (P / 2); p += ZTH) {
+      const int col = p / (P / 2), row = 2 * (p - col * (P / 2));
+      const long long src = colsrc[col];
+      double *dst = sZ + col * LDR + row;
+      if (src >= 0 && row + 1 < m) {
+        unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(sa), "l"(c.Xh + src * c.n + lo + row));
+      } else {
+        dst[0] = (src >= 0 && row < m) ? c.Xh[src * c.n + lo + row] : 0.0;
+        dst[1] = 0.0;
+      }
+    }
+  } else {
+    for (int p = t; p < Kz * P; p += ZTH) {
+      const int col = p / P, row = p - col * P;
+      const long long src = colsrc[col];
+      double *dst = sZ + col * LDR + row;
+      *dst = (src >= 0 && row < m) ? c.Xh[src * c.n + lo + row] : 0.0;
+    }
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  __syncthreads();
+  // ---------------- Z = X E (X = L^{-1}): GEMM, one 8-column tile of Z per warp, all row blocks as
+  // independent register accumulators (no sequential dependence) ----------------
+  {
+    const int g = lane >> 2, q2 = 2 * (lane & 3), kq = lane & 3;
+    for (int cc = warp; cc < Kc; cc += ZW) {
+      double acc[T][2];
+#pragma unroll
+      for (int i = 0; i < T; i++) { acc[i][0] = 0.0; acc[i][1] = 0.0; }
+      const double *zc = sZ + (8 * cc + g) * LDR;        // B operand: E(8 kb + kq (+4), 8 cc + g)
+#pragma unroll
+      for (int kb = 0; kb < T; kb++) {
+        const double b0 = zc[8 * kb + kq], b1 = zc[8 * kb + 4 + kq];
+#pragma unroll
+        for (int i = kb; i < T; i++) {
+          const double *tA = sX + tix(i, kb) * 64;
+          dmma(acc[i][0], acc[i][1], tA[lane], b0);
+          dmma(acc[i][0], acc[i][1], tA[32 + lane], b1);
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < T; i++) {
+        sZ[(8 * cc + q2) * LDR + 8 * i + g] = acc[i][0];
+        sZ[(8 * cc + q2 + 1) * LDR + 8 * i + g] = acc[i][1];
       }
     }
   }
   __syncthreads();
-  // ---------------- outputs: log det partial, packed L for the solve ----------------
-  if (warp == 0) {          // 2 sum log L_ii: per-lane partials, then a fixed-order warp reduction
-    double s = 0.0;
-    for (int i = lane; i < m; i += 32) s += log(sdiag[i]);
-    s = warp_sum(s);
-    if (lane == 0) {
-      c.leaf_ld[leaf] = 2.0 * s;
-      if (bad) { atomicAdd(&c.flags[1], 1); atomicMin(&c.flags[2], (int)id); }
-    }
-  }
-  double *Lg = c.Lf + leaf * c.lstride;            // L tiles then Linv tiles (contiguous in shared memory)
-  for (int p = t; p < (NTILE + T) * 64; p += NTH) Lg[p] = sL[p];
   if (K == 0) return;
   // ---------------- Pi_l = Z^T Z: 16x16 output blocks, DMMA m16n8k8 ----------------
   const int Kc16 = Kz / 16;
@@ -302,7 +365,7 @@ __global__ void __launch_bounds__(NTH, 1) k_leaf_factor_mma(LeafMmaCtx c) {
   double *Pl = c.Pi + leaf * ((long long)K * (K + 1) / 2);
   const int kend = (m + 7) & ~7;
   const int g = lane >> 2, tq = lane & 3;
-  for (int blk = warp; blk < nblk; blk += NW) {
+  for (int blk = warp; blk < nblk; blk += ZW) {
     const int BI = c_tileI[blk], BJ = c_tileJ[blk];
     double acc0[4] = {0, 0, 0, 0}, acc1[4] = {0, 0, 0, 0};
     const double *pa0 = sZ + (16 * BI + g) * LDR + tq;
@@ -327,41 +390,76 @@ __global__ void __launch_bounds__(NTH, 1) k_leaf_factor_mma(LeafMmaCtx c) {
 
 }  // namespace
 
-// Runs the fast path if it applies (leaf <= 128 and the panel fits in shared memory); *used reports it.
+// Leaf fast path applies for leaf <= 128 (P = 64 or 128).
+static int leaf_P(const hodlr_s *h) { return h->leaf_max <= 64 ? 64 : (h->leaf_max <= 128 ? 128 : 0); }
+
+static bool leaf_tables_ready = false;
+static hodlr_status leaf_tables() {
+  if (leaf_tables_ready) return HODLR_OK;
+  unsigned char ti[136], tj[136];
+  int q = 0;
+  for (int I = 0; I < 16; I++) for (int J = 0; J <= I; J++) { ti[q] = (unsigned char)I; tj[q] = (unsigned char)J; q++; }
+  HCUDA(cudaMemcpyToSymbol(c_tileI, ti, sizeof(ti)));
+  HCUDA(cudaMemcpyToSymbol(c_tileJ, tj, sizeof(tj)));
+  leaf_tables_ready = true;
+  return HODLR_OK;
+}
+
+static LeafMmaCtx leaf_ctx(hodlr_s *h, int K, double *Pi_leaf) {
+  LeafMmaCtx c;
+  c.kp = h->kp; c.n = h->n; c.ninternal = h->ninternal; c.kappa = h->kappa; c.K = K; c.Kp = (K + 7) / 8 * 8;
+  c.Kz = (K + 15) / 16 * 16;
+  c.xs = h->xs; c.lo = h->lo; c.hi = h->hi; c.Xh = h->Xh; c.rank = h->rank; c.dt = h->d_dt;
+  c.Lf = h->Lf; c.lstride = h->lstride; c.Pi = Pi_leaf; c.leaf_ld = h->leaf_ld; c.flags = h->dflags;
+  return c;
+}
+
+// Leaf Cholesky (kernel 1) on `stream`; *launched reports whether the fast path applies.
+hodlr_status hodlr_leaf_chol_mma(hodlr_s *h, cudaStream_t stream, bool *launched) {
+  *launched = false;
+  const int P = leaf_P(h);
+  if (P == 0 || h->nleaves == 0) return HODLR_OK;
+  hodlr_status ts = leaf_tables();
+  if (ts != HODLR_OK) return ts;
+  const int T = P / 8, NTILE = T * (T + 1) / 2;
+  const size_t smem = sizeof(double) * ((size_t)NTILE * 64 + T * 64 + 2 * P);
+  LeafMmaCtx c = leaf_ctx(h, 0, nullptr);
+  if (P == 64) {
+    HCUDA(cudaFuncSetAttribute(k_leaf_chol<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_leaf_chol<64><<<(int)h->nleaves, NTH, smem, stream>>>(c);
+  } else {
+    HCUDA(cudaFuncSetAttribute(k_leaf_chol<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_leaf_chol<128><<<(int)h->nleaves, NTH, smem, stream>>>(c);
+  }
+  HLAUNCH(h, "k_leaf_chol");
+  *launched = true;
+  return HODLR_OK;
+}
+
+// Z = L^{-1} E and Pi_l = Z^T Z (kernel 2) if the fast path applies (the Cholesky ran); *used reports it.
 hodlr_status hodlr_leaf_factor_mma(hodlr_s *h, int K, double *Pi_leaf, bool *used) {
   *used = false;
-  const int mmax = h->leaf_max;
-  const int P = mmax <= 64 ? 64 : (mmax <= 128 ? 128 : 0);
-  if (P == 0) return HODLR_OK;
+  const int P = leaf_P(h);
+  if (P == 0 || !h->chol_done) return HODLR_OK;
   const int Kp = (K + 7) / 8 * 8;
-  if (Kp / 8 > 16) return HODLR_OK;                  // register sweep covers <= 2 tiles per warp
+  if (Kp / 8 > ZW) return HODLR_OK;                  // one 8-column tile of Z per warp
   const int Kz = (K + 15) / 16 * 16;
   const int T = P / 8, NTILE = T * (T + 1) / 2, LDR = P + 4;
-  const size_t smem = sizeof(double) * ((size_t)NTILE * 64 + T * 64 + (size_t)Kz * LDR + 2 * P + Kz);
+  const size_t smem = sizeof(double) * ((size_t)NTILE * 64 + (size_t)Kz * LDR + Kz);
   int maxsm = 0;
   HCUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
   if (smem + 64 > (size_t)maxsm) return HODLR_OK;
-  static bool tables = false;
-  if (!tables) {
-    unsigned char ti[136], tj[136];
-    int q = 0;
-    for (int I = 0; I < 16; I++) for (int J = 0; J <= I; J++) { ti[q] = (unsigned char)I; tj[q] = (unsigned char)J; q++; }
-    HCUDA(cudaMemcpyToSymbol(c_tileI, ti, sizeof(ti)));
-    HCUDA(cudaMemcpyToSymbol(c_tileJ, tj, sizeof(tj)));
-    tables = true;
-  }
-  LeafMmaCtx c;
-  c.kp = h->kp; c.n = h->n; c.ninternal = h->ninternal; c.kappa = h->kappa; c.K = K; c.Kp = Kp; c.Kz = Kz;
-  c.xs = h->xs; c.lo = h->lo; c.hi = h->hi; c.Xh = h->Xh; c.rank = h->rank; c.dt = h->d_dt;
-  c.Lf = h->Lf; c.lstride = h->lstride; c.Pi = Pi_leaf; c.leaf_ld = h->leaf_ld; c.flags = h->dflags;
+  hodlr_status ts = leaf_tables();
+  if (ts != HODLR_OK) return ts;
+  LeafMmaCtx c = leaf_ctx(h, K, Pi_leaf);
   if (P == 64) {
-    HCUDA(cudaFuncSetAttribute(k_leaf_factor_mma<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_leaf_factor_mma<64><<<(int)h->nleaves, NTH, smem, h->st>>>(c);
+    HCUDA(cudaFuncSetAttribute(k_leaf_zsyrk<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_leaf_zsyrk<64><<<(int)h->nleaves, ZTH, smem, h->st>>>(c);
   } else {
-    HCUDA(cudaFuncSetAttribute(k_leaf_factor_mma<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_leaf_factor_mma<128><<<(int)h->nleaves, NTH, smem, h->st>>>(c);
+    HCUDA(cudaFuncSetAttribute(k_leaf_zsyrk<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_leaf_zsyrk<128><<<(int)h->nleaves, ZTH, smem, h->st>>>(c);
   }
-  HLAUNCH(h, "k_leaf_factor_mma");
+  HLAUNCH(h, "k_leaf_zsyrk");
   *used = true;
   return HODLR_OK;
 }

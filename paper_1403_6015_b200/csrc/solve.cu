@@ -7,15 +7,15 @@
 //   down (node c)  f = t_c + T_c w_c;  w_c1 = [w_c, -f[:r]],  w_c2 = [w_c, -f[r:]]   (k_tree_down)
 //   down (leaves)  x_l = A_l^{-1} (b_l + E_l w_l)                                   (k_leaf_down)
 // h_root = y^T C^{-1} y gives the log-likelihood without the down pass (eq. 1).
-// Leaf triangular solves are blocked over 8-row tiles with the stored inverse diagonal tiles; one warp
-// per leaf, one warp per tree node (t_c by a double solve + 2 compensated refinement steps).
+// Leaf passes use the stored X = L^{-1} (one CTA per leaf, two triangular matrix-vector products);
+// tree passes one warp per node (t_c by S_c^{-1} + 2 compensated refinement steps).
 #include "hodlr_internal.cuh"
 
 namespace {
 
 constexpr int ST = 256;          // threads per CTA (8 warps)
 constexpr int NWS = ST / 32;
-constexpr int RPL = 8;           // rows per lane: leaves up to 256 rows
+
 
 struct SolveCtx {
   long long n, ninternal, nleaves;
@@ -34,176 +34,176 @@ struct SolveCtx {
   int *flags;
 };
 
-// Rows of the leaf owned by this lane: i = lane + 32 s.  v[s] holds the working vector.
-// Forward: v <- L^{-1} v with L in fragment-order tiles (Lg) and the inverse diagonal tiles (Li).
-__device__ __forceinline__ void tile_fwd(const double *Lg, const double *Li, int T, double v[RPL], int lane) {
-  for (int b = 0; b < T; b++) {
-    const int rb = 8 * b;
-    double vb[8];
+// ---------------------------------------------------------------------------------------------
+// Leaf passes: one CTA (256 threads) per leaf; X = L^{-1} (fragment-order lower tiles) staged in shared
+// memory with 16-byte cp.async when it fits (T <= 16), read from global otherwise.
+//   u = X b   (row i: sum_{j <= i} X_ij b_j)        v = X^T u   (column j: sum_{i >= j} X_ij u_i)
+// so v = A_l^{-1} b with two parallel triangular matrix-vector products.
+// ---------------------------------------------------------------------------------------------
+
+// out = X in (lower) for rows < R = 8T; 2 threads per row (interleaved tile columns), partials in red[].
+__device__ void tri_mv(const double *X, int T, const double *in, double *out, double *red) {
+  const int t = threadIdx.x, R = 8 * T, NT = blockDim.x;
+  for (int w = t; w < 2 * R; w += NT) {
+    const int i = w % R, h = w / R, I = i >> 3, r = i & 7;
+    double s = 0.0;
+    for (int k = h; k <= I; k += 2) {
+      const double *tl = X + tix(I, k) * 64;
 #pragma unroll
-    for (int k = 0; k < 8; k++) {
-      const int row = rb + k, s = row >> 5;
-      double val = 0.0;
-#pragma unroll
-      for (int ss = 0; ss < RPL; ss++) if (ss == s) val = v[ss];
-      vb[k] = __shfl_sync(0xffffffffu, val, row & 31);
+      for (int cc = 0; cc < 8; cc++) s = fma(tl[fo(r, cc)], in[8 * k + cc], s);
     }
-    double z[8];                       // z_b = Linv(b) v_b
-#pragma unroll
-    for (int r = 0; r < 8; r++) {
-      double acc = 0.0;
-#pragma unroll
-      for (int k = 0; k <= r; k++) acc += Li[b * 64 + fo(r, k)] * vb[k];
-      z[r] = acc;
-    }
-#pragma unroll
-    for (int s = 0; s < RPL; s++) {
-      const int i = lane + 32 * s;
-      if (i >= 8 * T) break;
-      if (i >= rb && i < rb + 8) {
-#pragma unroll
-        for (int r = 0; r < 8; r++) if (i == rb + r) v[s] = z[r];
-      } else if (i >= rb + 8) {        // v_i -= L(I, b) z
-        const double *t = Lg + tix(i >> 3, b) * 64;
-        const int r = i & 7;
-        double acc = v[s];
-#pragma unroll
-        for (int k = 0; k < 8; k++) acc -= t[fo(r, k)] * z[k];
-        v[s] = acc;
-      }
-    }
+    red[w] = s;
   }
+  __syncthreads();
+  for (int i = t; i < R; i += NT) out[i] = red[i] + red[R + i];
+  __syncthreads();
 }
 
-// Backward: v <- L^{-T} v.
-__device__ __forceinline__ void tile_bwd(const double *Lg, const double *Li, int T, double v[RPL], int lane) {
-  for (int b = T - 1; b >= 0; b--) {
-    const int rb = 8 * b;
-    double vb[8];
+// out = X^T in for columns < R.
+__device__ void tri_mvt(const double *X, int T, const double *in, double *out, double *red) {
+  const int t = threadIdx.x, R = 8 * T, NT = blockDim.x;
+  for (int w = t; w < 2 * R; w += NT) {
+    const int j = w % R, h = w / R, J = j >> 3, cc = j & 7;
+    double s = 0.0;
+    for (int I = J + h; I < T; I += 2) {
+      const double *tl = X + tix(I, J) * 64;
 #pragma unroll
-    for (int k = 0; k < 8; k++) {
-      const int row = rb + k, s = row >> 5;
-      double val = 0.0;
-#pragma unroll
-      for (int ss = 0; ss < RPL; ss++) if (ss == s) val = v[ss];
-      vb[k] = __shfl_sync(0xffffffffu, val, row & 31);
+      for (int r = 0; r < 8; r++) s = fma(tl[fo(r, cc)], in[8 * I + r], s);
     }
-    double z[8];                       // w_b = Linv(b)^T v_b
-#pragma unroll
-    for (int r = 0; r < 8; r++) {
-      double acc = 0.0;
-#pragma unroll
-      for (int k = r; k < 8; k++) acc += Li[b * 64 + fo(k, r)] * vb[k];
-      z[r] = acc;
-    }
-#pragma unroll
-    for (int s = 0; s < RPL; s++) {
-      const int j = lane + 32 * s;
-      if (j >= 8 * T) break;
-      if (j >= rb && j < rb + 8) {
-#pragma unroll
-        for (int r = 0; r < 8; r++) if (j == rb + r) v[s] = z[r];
-      } else if (j < rb) {             // v_j -= sum_r L(b, J)[r][j%8] z_r
-        const double *t = Lg + tix(b, j >> 3) * 64;
-        const int cj = j & 7;
-        double acc = v[s];
-#pragma unroll
-        for (int r = 0; r < 8; r++) acc -= t[fo(r, cj)] * z[r];
-        v[s] = acc;
-      }
-    }
+    red[w] = s;
   }
+  __syncthreads();
+  for (int j = t; j < R; j += NT) out[j] = red[j] + red[R + j];
+  __syncthreads();
 }
 
-__device__ void leaf_colmap(const SolveCtx &c, long long id, int *colsrc, int lane) {
-  if (lane == 0) {
-    long long a = id;
-    for (int e = c.kappa; e >= 1; e--) {
-      long long b = (a - 1) / 2;
-      int rb = c.rank[b];
-      for (int q = 0; q < c.dt->rdep[e]; q++) colsrc[c.dt->Kdim[e - 1] + q] = q < rb ? (int)(c.dt->colbase[e] + q) : -1;
-      a = b;
-    }
-  }
-  __syncwarp();
+__device__ __forceinline__ int leaf_colsrc(const SolveCtx &c, long long id, int q) {
+  if (q >= c.K) return -1;
+  int e = 1;
+  while (c.dt->Kdim[e] <= q) e++;
+  const int qq = q - c.dt->Kdim[e - 1];
+  const long long b = ((id + 1) >> (c.kappa - e + 1)) - 1;     // ancestor at depth e - 1 (heap order)
+  return qq < c.rank[b] ? (int)(c.dt->colbase[e] + qq) : -1;
 }
 
-// one warp per leaf
-__global__ void __launch_bounds__(ST) k_leaf_up(SolveCtx c) {
-  __shared__ int colsrc_s[NWS][1024];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const long long leaf = (long long)blockIdx.x * NWS + wid;
-  if (leaf >= c.nleaves) return;
-  int *colsrc = colsrc_s[wid];
+constexpr int VMAX = 8 * 32;      // leaf rows handled (leaf_max < 2 leaf <= 256)
+constexpr int LT = 512;           // threads per leaf CTA
+
+__device__ __forceinline__ void cp16(double *dst, const double *src) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(sa), "l"(src));
+}
+__device__ __forceinline__ void cp8(double *dst, const double *src) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" :: "r"(sa), "l"(src));
+}
+
+// Stage X = L^{-1} (tiles) and the ancestor panel E_l (K columns x R rows, column-major, zero beyond each
+// block's rank) of one leaf into shared memory with cp.async; all bytes of the leaf in flight at once.
+__device__ void stage_leaf(const SolveCtx &c, long long leaf, long long id, long long lo, int m, int R,
+                           const int *colsrc, double *sX, double *sE) {
+  const int t = threadIdx.x, NT = blockDim.x;
+  const double *Xg = c.Lf + leaf * c.lstride;
+  const int nx2 = (c.T * (c.T + 1) / 2) * 32;
+  for (int p = t; p < nx2; p += NT) cp16(sX + 2 * p, Xg + 2 * p);
+  const bool al16 = ((c.n | lo) & 1) == 0;
+  if (al16) {
+    const int R2 = R / 2;
+    for (int p = t; p < c.K * R2; p += NT) {
+      const int q = p / R2, i = 2 * (p - q * R2);
+      const int src = colsrc[q];
+      double *dst = sE + q * R + i;
+      if (src >= 0 && i + 1 < m) cp16(dst, c.Xh + (long long)src * c.n + lo + i);
+      else { dst[0] = (src >= 0 && i < m) ? c.Xh[(long long)src * c.n + lo + i] : 0.0; dst[1] = 0.0; }
+    }
+  } else {
+    for (int p = t; p < c.K * R; p += NT) {
+      const int q = p / R, i = p - q * R;
+      const int src = colsrc[q];
+      double *dst = sE + q * R + i;
+      if (src >= 0 && i < m) cp8(dst, c.Xh + (long long)src * c.n + lo + i); else *dst = 0.0;
+    }
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
+}
+
+// up: v = A_l^{-1} b, g_l = E_l^T v, h_l = b . v
+__global__ void __launch_bounds__(LT, 1) k_leaf_up(SolveCtx c) {
+  extern __shared__ double sm[];
+  __shared__ double sb[VMAX], su[VMAX], red[2 * VMAX];
+  __shared__ int colsrc[1024];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, NW = LT / 32;
+  const long long leaf = blockIdx.x;
   const long long id = c.ninternal + leaf, lo = c.lo[id];
-  const int m = (int)(c.hi[id] - lo);
-  const double *Lg = c.Lf + leaf * c.lstride;
-  const double *Li = Lg + (long long)(c.T * (c.T + 1) / 2) * 64;
-  double b[RPL], v[RPL];
+  const int m = (int)(c.hi[id] - lo), R = 8 * c.T, K = c.K;
+  double *sX = sm, *sE = sm + 64 * (c.T * (c.T + 1) / 2);
+  for (int q = t; q < K; q += LT) colsrc[q] = leaf_colsrc(c, id, q);
   bool bad = false;
-#pragma unroll
-  for (int s = 0; s < RPL; s++) {
-    const int i = lane + 32 * s;
-    b[s] = i < m ? c.y[c.perm[lo + i]] : 0.0;
-    if (!isfinite(b[s])) bad = true;
-    v[s] = b[s];
+  for (int i = t; i < R; i += LT) {
+    const double v = i < m ? c.y[c.perm[lo + i]] : 0.0;
+    if (!isfinite(v)) bad = true;
+    sb[i] = v;
   }
   if (bad) atomicOr(&c.flags[3], 1);
-  leaf_colmap(c, id, colsrc, lane);
-  tile_fwd(Lg, Li, c.T, v, lane);
-  tile_bwd(Lg, Li, c.T, v, lane);          // v = A^{-1} b
+  __syncthreads();
+  stage_leaf(c, leaf, id, lo, m, R, colsrc, sX, sE);
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  __syncthreads();
+  tri_mv(sX, c.T, sb, su, red);           // u = X b
+  tri_mvt(sX, c.T, su, su, red);          // v = X^T u  (in place: tri_mvt reads su fully before its barrier)
   double hs = 0.0;
-#pragma unroll
-  for (int s = 0; s < RPL; s++) hs += b[s] * v[s];
+  for (int i = t; i < m; i += LT) hs += sb[i] * su[i];
   hs = warp_sum(hs);
-  if (lane == 0) { c.hv[2 * id] = hs; c.hv[2 * id + 1] = 0.0; }
-  double *g = c.V + c.dt->nodeV[c.kappa] + leaf * (long long)c.K;
-  for (int col = 0; col < c.K; col++) {    // g = E^T w
-    const long long src = colsrc[col];
-    double s = 0.0;
-    if (src >= 0) {
-      const double *e = c.Xh + src * c.n + lo;
-#pragma unroll
-      for (int ss = 0; ss < RPL; ss++) { const int i = lane + 32 * ss; if (i < m) s += e[i] * v[ss]; }
-    }
-    s = warp_sum(s);
-    if (lane == 0) g[col] = s;
+  if (lane == 0) red[warp] = hs;
+  double *g = c.V + c.dt->nodeV[c.kappa] + leaf * (long long)K;
+  for (int q = warp; q < K; q += NW) {    // g = E^T v: warp per column, lanes over rows
+    const double *e = sE + q * R;
+    double s2 = 0.0;
+    for (int i = lane; i < R; i += 32) s2 = fma(e[i], su[i], s2);
+    s2 = warp_sum(s2);
+    if (lane == 0) g[q] = s2;
+  }
+  __syncthreads();
+  if (t == 0) {
+    double h = 0.0;
+    for (int w = 0; w < NW; w++) h += red[w];
+    c.hv[2 * id] = h; c.hv[2 * id + 1] = 0.0;
   }
 }
 
-__global__ void __launch_bounds__(ST) k_leaf_down(SolveCtx c) {
-  __shared__ int colsrc_s[NWS][1024];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const long long leaf = (long long)blockIdx.x * NWS + wid;
-  if (leaf >= c.nleaves) return;
-  int *colsrc = colsrc_s[wid];
+// down: x_l = A_l^{-1} (b_l + E_l w_l)
+__global__ void __launch_bounds__(LT, 1) k_leaf_down(SolveCtx c) {
+  extern __shared__ double sm[];
+  __shared__ double sb[VMAX], su[VMAX], red[2 * VMAX];
+  __shared__ int colsrc[1024];
+  __shared__ double sw[1024];
+  __shared__ double part4[4 * VMAX];
+  const int t = threadIdx.x;
+  const long long leaf = blockIdx.x;
   const long long id = c.ninternal + leaf, lo = c.lo[id];
-  const int m = (int)(c.hi[id] - lo);
-  const double *Lg = c.Lf + leaf * c.lstride;
-  const double *Li = Lg + (long long)(c.T * (c.T + 1) / 2) * 64;
-  leaf_colmap(c, id, colsrc, lane);
-  const double *w = c.V + c.dt->nodeV[c.kappa] + leaf * (long long)c.K;
-  double v[RPL];
-#pragma unroll
-  for (int s = 0; s < RPL; s++) {
-    const int i = lane + 32 * s;
-    v[s] = i < m ? c.y[c.perm[lo + i]] : 0.0;
+  const int m = (int)(c.hi[id] - lo), R = 8 * c.T, K = c.K;
+  double *sX = sm, *sE = sm + 64 * (c.T * (c.T + 1) / 2);
+  const double *w = c.V + c.dt->nodeV[c.kappa] + leaf * (long long)K;
+  for (int q = t; q < K; q += LT) { colsrc[q] = leaf_colsrc(c, id, q); sw[q] = w[q]; }
+  __syncthreads();
+  stage_leaf(c, leaf, id, lo, m, R, colsrc, sX, sE);
+  for (int i = t; i < R; i += LT) sb[i] = i < m ? c.y[c.perm[lo + i]] : 0.0;
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  __syncthreads();
+  // b + E w: 4 threads per row (quarters of the columns), partials combined in a fixed order
+  for (int w4 = t; w4 < 4 * R; w4 += LT) {
+    const int i = w4 % R, h = w4 / R;
+    const int q0 = (K * h) / 4, q1 = (K * (h + 1)) / 4;
+    double s2 = 0.0;
+    for (int q = q0; q < q1; q++) s2 = fma(sE[q * R + i], sw[q], s2);
+    part4[w4] = s2;
   }
-  for (int col = 0; col < c.K; col++) {    // v = b + E w
-    const long long src = colsrc[col];
-    if (src < 0) continue;
-    const double wc = w[col];
-    const double *e = c.Xh + src * c.n + lo;
-#pragma unroll
-    for (int s = 0; s < RPL; s++) { const int i = lane + 32 * s; if (i < m) v[s] += e[i] * wc; }
-  }
-  tile_fwd(Lg, Li, c.T, v, lane);
-  tile_bwd(Lg, Li, c.T, v, lane);
-#pragma unroll
-  for (int s = 0; s < RPL; s++) {
-    const int i = lane + 32 * s;
-    if (i < m) c.x[c.perm[lo + i]] = v[s];
-  }
+  __syncthreads();
+  for (int i = t; i < R; i += LT) sb[i] += (part4[i] + part4[R + i]) + (part4[2 * R + i] + part4[3 * R + i]);
+  __syncthreads();
+  tri_mv(sX, c.T, sb, su, red);
+  tri_mvt(sX, c.T, su, sb, red);
+  for (int i = t; i < m; i += LT) c.x[c.perm[lo + i]] = sb[i];
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -309,7 +309,8 @@ __global__ void __launch_bounds__(ST) k_tree_down(SolveCtx c, int d) {
 hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_only) {
   const int kappa = h->kappa;
   DepthTab &dt = h->dt;
-  if (h->leaf_max > 32 * RPL) return hodlr_set_error(HODLR_EINVAL, "solve: leaf size %d > %d", h->leaf_max, 32 * RPL);
+  if (h->leaf_max > VMAX || dt.Kdim[kappa] > 1024)
+    return hodlr_set_error(HODLR_EINVAL, "solve: leaf size %d > %d or K > 1024", h->leaf_max, VMAX);
   if (!h->Vpool) {
     long long vTot = 0, tTot = 0;
     for (int e = 0; e <= kappa; e++) { dt.nodeV[e] = vTot; vTot += (1LL << e) * (long long)dt.Kdim[e]; }
@@ -326,9 +327,22 @@ hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_on
   c.lo = h->lo; c.hi = h->hi; c.perm = h->perm; c.Xh = h->Xh; c.rank = h->rank; c.dt = h->d_dt;
   c.Lf = h->Lf; c.lstride = h->lstride; c.Spool = h->Spool; c.BTpool = h->BTpool;
   c.V = h->Vpool; c.Tv = h->Tvec; c.hv = h->hvec; c.y = y; c.x = x; c.flags = h->dflags;
-  const int lgrid = (int)((h->nleaves + NWS - 1) / NWS);
+  const int lgrid = (int)h->nleaves;
+  const int R = 8 * h->ltiles;
+  // X tiles + E panel in shared memory
+  const size_t lsm = sizeof(double) * (64 * (size_t)(h->ltiles * (h->ltiles + 1) / 2) + (size_t)c.K * R);
+  int maxsm = 0;
+  HCUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
+  if (lsm + 32 * 1024 > (size_t)maxsm)
+    return hodlr_set_error(HODLR_EINVAL, "solve: leaf panel (%d x %d) exceeds shared memory", R, c.K);
+  static size_t lattr = 0;
+  if (lsm > lattr) {
+    HCUDA(cudaFuncSetAttribute(k_leaf_up, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
+    HCUDA(cudaFuncSetAttribute(k_leaf_down, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
+    lattr = lsm;
+  }
   ph_begin(h, PH_SLEAF_UP);
-  k_leaf_up<<<lgrid, ST, 0, h->st>>>(c);
+  k_leaf_up<<<lgrid, LT, lsm, h->st>>>(c);
   HLAUNCH(h, "k_leaf_up");
   ph_end(h, PH_SLEAF_UP);
   ph_begin(h, PH_STREE);
@@ -350,7 +364,7 @@ hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_on
   }
   ph_end(h, PH_STREE);
   ph_begin(h, PH_SLEAF_DOWN);
-  k_leaf_down<<<lgrid, ST, 0, h->st>>>(c);
+  k_leaf_down<<<lgrid, LT, lsm, h->st>>>(c);
   HLAUNCH(h, "k_leaf_down");
   ph_end(h, PH_SLEAF_DOWN);
   return HODLR_OK;

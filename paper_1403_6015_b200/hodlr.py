@@ -46,7 +46,8 @@ class hodlr_info_t(C.Structure):
                 ("aca_steps", C.c_int32), ("gpu_launches_last", C.c_int32),
                 ("kernel_ms", C.c_double * 16), ("kernel_calls", C.c_int64 * 16)]
 
-KERNEL_FAMILIES = ("sort", "aca", "leaf_factor", "coupling_tree", "solve_leaf_up", "solve_tree", "solve_leaf_down")
+KERNEL_FAMILIES = ("sort", "aca", "leaf_factor", "coupling_tree", "solve_leaf_up", "solve_tree", "solve_leaf_down",
+                   "leaf_chol")
 
 
 _lib = None

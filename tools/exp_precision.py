@@ -1,6 +1,6 @@
 """Experiment: GPU-vs-oracle parity as a function of HODLR_TREE_PLAIN_FROM (depths >= that value run
 the coupling-tree Schur updates in plain double).  Test tooling: prints one line per case.
-python tools/exp_precision.py <plain_from>   (the env var is read once per process)"""
+HODLR_TREE_PLAIN_FROM=<d> python tools/exp_precision.py [full]   (the env var is read once per process)"""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -11,6 +11,8 @@ from oracle import OracleHODLR
 
 CASES = [("cfg3", 1 << 16, None), ("cfg1", 2048, None), ("cfg2", 65536, None), ("cfg4", 1 << 14, (2.0, 1e-4)),
          ("cfg4", 1 << 14, (0.05, 1e-4))]
+if len(sys.argv) > 1 and sys.argv[1] == "full":
+    CASES = [("cfg3", 1 << 20, None), ("cfg4", 1 << 17, (2.0, 1e-4))]
 cache = "/tmp/exp_oracle"
 os.makedirs(cache, exist_ok=True)
 for name, n, over in CASES:
