@@ -55,10 +55,20 @@ typedef enum {
  * C_ij = k(x_i - x_j) + sigma2 [i == j]. */
 typedef enum { HODLR_SE = 0, HODLR_MATERN32 = 1, HODLR_MATERN52 = 2 } hodlr_kernel;
 
-/* Multi-GPU descriptor (subtree sharding).  NULL => one GPU. */
+/* Multi-GPU descriptor (subtree sharding, north_star).  NULL or nranks == 1 => one GPU.
+ * nranks = P must be a power of two with P <= 2^kappa.  Rank g owns the depth-log2(P) node g (sorted rows
+ * [lo, hi) of that node) and its whole subtree; the points are replicated (every rank passes the same x, y,
+ * theta, sigma2, leaf, eps).  The top log2(P) levels (their ACA blocks and coupling systems) are computed
+ * redundantly by every rank; the ranks exchange, by allgather: the per-depth ACA ranks (build), the projected
+ * Gram matrices of the depth-log2(P) nodes and the log det partials (factor), the solve's projections at
+ * depth log2(P) and the sorted solution slices (solve).  Transport: NCCL (nccl_unique_id: the 128-byte
+ * ncclUniqueId from hodlr_nccl_unique_id() on rank 0, broadcast by the caller; one GPU per rank), or an
+ * in-process group of virtual ranks (group: from hodlr_group_create, one host thread per rank, all on the
+ * current device) -- the latter runs the sharded path on one GPU.  Exactly one of the two must be set. */
 typedef struct {
   int32_t rank, nranks;
-  const void *nccl_unique_id;   /* 128-byte ncclUniqueId from rank 0, broadcast by the caller */
+  const void *nccl_unique_id;   /* 128 bytes, or NULL */
+  void *group;                  /* hodlr_group_create() handle, or NULL */
 } hodlr_dist;
 
 /* Optional build options.  NULL => defaults. */
@@ -83,6 +93,9 @@ typedef struct {
    * [5] solve tree up/down, [6] solve leaf down, [7] leaf Cholesky (side stream, overlaps the ACA). */
   double  kernel_ms[16];
   int64_t kernel_calls[16];
+  int32_t rank, nranks, split_depth;   /* sharding (split_depth = log2(nranks)); ranks/means above cover the
+                                          blocks this rank computed (its subtree and the top levels) */
+  int32_t pad_;
 } hodlr_info_t;
 
 /* "Assembly": stable sort of x (O(n), K1), balanced count-median
@@ -110,6 +123,16 @@ hodlr_status hodlr_solve(hodlr_t h, const double *y, double *x, int64_t nrhs, in
  * y: device, n doubles.  out_host: host double (-INFINITY with HODLR_ENOTPD on failure). */
 hodlr_status gp_loglik(hodlr_t h, const double *y, double *out_host);
 
+/* Config 4 (BASELINE.json): log-likelihoods (eq. 1) of B independent hyper-parameter settings on the same
+ * x, y (device, n doubles).  thetas: HOST B x 2 {a, ell}; sigma2s: HOST B; out_host: HOST B doubles (-INFINITY
+ * for a setting that failed).  One GPU runs `workers` settings concurrently (host threads, one stream each;
+ * <= 0 => 4).  With dist (nranks > 1) rank g computes settings g, g + P, ... and the values are allgathered, so
+ * every rank returns all B (replicas; the settings share nothing).  Returns the first failing setting's status
+ * (message names it), HODLR_OK if all succeeded. */
+hodlr_status gp_loglik_sweep(const double *x, const double *y, int64_t n, hodlr_kernel kernel, const double *thetas,
+                             const double *sigma2s, int32_t B, int32_t leaf, double eps, const hodlr_dist *dist,
+                             void *cuda_stream, int32_t workers, double *out_host);
+
 /* Sizes, ranks and phase times.  info: host struct. */
 hodlr_status hodlr_info(hodlr_t h, hodlr_info_t *info);
 
@@ -123,6 +146,20 @@ hodlr_status hodlr_get_tree(hodlr_t h, int64_t *lo_host, int64_t *hi_host, int32
 
 /* Per-leaf (2^kappa) and per-internal-node (heap order) log det partials, HOST buffers. */
 hodlr_status hodlr_get_logdet_parts(hodlr_t h, double *leaf_parts_host, double *node_parts_host);
+
+/* Fill out128 with a fresh ncclUniqueId (NCCL is loaded at run time with dlopen("libnccl.so.2")).
+ * HODLR_ENCCL if NCCL is unavailable. */
+hodlr_status hodlr_nccl_unique_id(void *out128);
+
+/* In-process group of nranks virtual ranks (host threads sharing one process and device).  Destroy only
+ * after every handle that uses it has been freed. */
+hodlr_status hodlr_group_create(int32_t nranks, void **group);
+void         hodlr_group_destroy(void *group);
+
+/* Host-side shard plan (no device work): tree depth kappa, split depth t = log2(nranks), the sorted row range
+ * [row_lo, row_hi) and leaf range [leaf_lo, leaf_hi) owned by `rank`.  HODLR_EINVAL for an invalid split. */
+hodlr_status hodlr_dist_plan(int64_t n, int32_t leaf, int32_t rank, int32_t nranks, int32_t *kappa, int32_t *t,
+                             int64_t *row_lo, int64_t *row_hi, int64_t *leaf_lo, int64_t *leaf_hi);
 
 /* Release everything the handle owns (stream-ordered).  NULL is a no-op. */
 void hodlr_free(hodlr_t h);

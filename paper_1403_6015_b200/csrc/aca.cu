@@ -394,7 +394,7 @@ __global__ void k_aca_cond(cudaGraphConditionalHandle hdl, const AcaCtx *__restr
 // same shape skip the planning and the graph instantiation.  A plan in use by another build is not shared.
 // ---------------------------------------------------------------------------------------------
 struct AcaPlan {
-  long long n; int leaf;
+  long long n; int leaf; int rank, nranks;
   long long nb; int nbig;
   std::vector<int> fused_blocks;
   size_t nitems_r = 0, nitems_c = 0;
@@ -417,6 +417,7 @@ static cudaError_t plan_create(AcaPlan *P, const hodlr_s *h) {
   P->nbig = 0;
   for (long long b = 0; b < nb; b++) {
     bdepth[b] = hodlr_depth_of(b);
+    if (!hodlr_owns_block(h, b)) { nq_r[b] = nq_c[b] = 0; rb_r[b] = rb_c[b] = 0; continue; }   // another rank's subtree
     long long m1 = h->h_hi[2 * b + 1] - h->h_lo[2 * b + 1], m2 = h->h_hi[2 * b + 2] - h->h_lo[2 * b + 2];
     if (std::max(m1, m2) <= ACA_FUSED_MAX) { P->fused_blocks.push_back((int)b); nq_r[b] = nq_c[b] = 0; rb_r[b] = rb_c[b] = 0; continue; }
     bigidx[b] = P->nbig++;
@@ -501,10 +502,12 @@ static AcaPlan *plan_acquire(const hodlr_s *h, hodlr_status *st) {
   {
     std::lock_guard<std::mutex> lk(g_plan_mu);
     for (AcaPlan *P : g_plans)
-      if (!P->busy && P->n == h->n && P->leaf == h->leaf) { P->busy = true; return P; }
+      if (!P->busy && P->n == h->n && P->leaf == h->leaf && P->rank == h->grank && P->nranks == h->nranks) {
+        P->busy = true; return P;
+      }
   }
   AcaPlan *P = new AcaPlan();
-  P->n = h->n; P->leaf = h->leaf; P->nb = h->ninternal; P->busy = true;
+  P->n = h->n; P->leaf = h->leaf; P->rank = h->grank; P->nranks = h->nranks; P->nb = h->ninternal; P->busy = true;
   cudaError_t e = plan_create(P, h);
   if (e != cudaSuccess) { *st = hodlr_cuda_check(e, "aca plan"); return nullptr; }   // (leaked on error)
   std::lock_guard<std::mutex> lk(g_plan_mu);

@@ -8,6 +8,7 @@
 #include <new>
 #include <mutex>
 #include <vector>
+#include <algorithm>
 
 #include <chrono>
 static thread_local char g_err[1024] = "";
@@ -137,6 +138,7 @@ void hodlr_free(hodlr_t h) {
   if (h->st2) cudaStreamSynchronize(h->st2);
   cudaStreamSynchronize(h->st);
   res_release(h);
+  hodlr_dist_fini(h);
   delete[] h->h_lo; delete[] h->h_hi; delete[] h->h_rank;
   delete h;
 }
@@ -154,7 +156,6 @@ hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const 
   if (!(theta[1] > 0.0) || !isfinite(theta[1])) return hodlr_set_error(HODLR_EINVAL, "build: ell = %g <= 0", theta[1]);
   if (!(theta[0] >= 0.0) || !isfinite(theta[0])) return hodlr_set_error(HODLR_EINVAL, "build: a = %g < 0", theta[0]);
   if ((int)kernel < 0 || (int)kernel > 2) return hodlr_set_error(HODLR_EINVAL, "build: unknown kernel %d", (int)kernel);
-  if (dist && dist->nranks > 1) return hodlr_set_error(HODLR_EINVAL, "build: multi-GPU sharding not available in this build");
   int cap = (opts && opts->rank_cap > 0) ? opts->rank_cap : 48;
   if (cap > ACA_MAXCAP) return hodlr_set_error(HODLR_EINVAL, "build: rank_cap %d > %d", cap, ACA_MAXCAP);
   hodlr_s *h = new (std::nothrow) hodlr_s();
@@ -191,6 +192,8 @@ hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const 
     if (m < h->leaf_min) h->leaf_min = (int)m;
     if (m > h->leaf_max) h->leaf_max = (int)m;
   }
+  st = hodlr_dist_init(h, dist);                       // subtree sharding
+  if (st != HODLR_OK) { hodlr_free(h); return st; }
   // panel slots: depth e holds min(cap, max node size at depth e) columns
   long long cols = 0;
   for (int e = 1; e <= kappa; e++) {
@@ -212,6 +215,20 @@ hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const 
     hodlr_free(h);
     return hodlr_set_error(HODLR_ENOMEM, "build: device allocation of %.2f GB failed",
                            1e-9 * (double)(8.0 * n * (cols + 4)));
+  }
+  if (h->nranks > 1) {          // row ranges of every rank's subtree (the solution allgather slices)
+    h->d_rowlo = (long long *)hodlr_dalloc(h, sizeof(long long) * h->nranks);
+    if (!h->d_rowlo) { hodlr_free(h); return hodlr_set_error(HODLR_ENOMEM, "build: device allocation failed"); }
+    std::vector<long long> rl(h->nranks);
+    h->rows_max = 0;
+    for (int r = 0; r < h->nranks; r++) {
+      const long long id = (1LL << h->tsplit) - 1 + r;
+      rl[r] = h->h_lo[id];
+      h->rows_max = std::max(h->rows_max, h->h_hi[id] - h->h_lo[id]);
+    }
+    if (cudaMemcpy(h->d_rowlo, rl.data(), sizeof(long long) * h->nranks, cudaMemcpyHostToDevice) != cudaSuccess) {
+      hodlr_free(h); return hodlr_set_error(HODLR_ECUDA, "build: copy failed");
+    }
   }
   int fl[16] = {0}; fl[2] = INT_MAX;
 #define CK(call) do { cudaError_t _e = (call); if (_e != cudaSuccess) { st = hodlr_cuda_check(_e, #call); goto fail; } } while (0)
@@ -249,15 +266,38 @@ hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const 
     if (h->ninternal > 0)
       CK(cudaMemcpyAsync(h->h_rank, h->rank, sizeof(int) * h->ninternal, cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
+    // per-depth max ranks (the panel layout K_e must agree on every rank) and the rank-cap hits
+    std::vector<double> loc(kappa + 2, 0.0);
+    for (int e = 1; e <= kappa; e++) {
+      int r = 0;
+      for (long long b = (1LL << (e - 1)) - 1; b < (1LL << e) - 1; b++) r = std::max(r, h->h_rank[b]);
+      loc[e] = r;
+    }
+    loc[0] = f5;
+    if (h->nranks > 1) {
+      const size_t per = kappa + 2;
+      double *dbuf = (double *)hodlr_dalloc(h, sizeof(double) * per * (h->nranks + 1));
+      if (!dbuf) { st = hodlr_set_error(HODLR_ENOMEM, "build: device allocation failed"); goto fail; }
+      std::vector<double> all(per * h->nranks);
+      CK(cudaMemcpyAsync(dbuf, loc.data(), sizeof(double) * per, cudaMemcpyHostToDevice, h->st));
+      st = hodlr_allgather(h, dbuf, dbuf + per, sizeof(double) * per);
+      if (st != HODLR_OK) goto fail;
+      CK(cudaMemcpyAsync(all.data(), dbuf + per, sizeof(double) * per * h->nranks, cudaMemcpyDeviceToHost, h->st));
+      CK(cudaStreamSynchronize(h->st));
+      for (size_t j = 0; j < per; j++) {
+        double v = 0.0;
+        for (int r = 0; r < h->nranks; r++) v = j == 0 ? v + all[r * per] : std::max(v, all[r * per + j]);
+        loc[j] = v;
+      }
+    }
+    f5 = (int)loc[0];
     h->rank_cap_hits = f5;
     if (f5) { st = hodlr_set_error(HODLR_ERANKCAP, "build: %d block(s) reached the rank cap %d without meeting eps", f5, cap); goto fail; }
-  }
-  h->dt.Kdim[0] = 0;
-  for (int e = 1; e <= kappa; e++) {
-    int r = 0;
-    for (long long b = (1LL << (e - 1)) - 1; b < (1LL << e) - 1; b++) r = std::max(r, h->h_rank[b]);
-    h->dt.rdep[e] = r;
-    h->dt.Kdim[e] = h->dt.Kdim[e - 1] + r;
+    h->dt.Kdim[0] = 0;
+    for (int e = 1; e <= kappa; e++) {
+      h->dt.rdep[e] = (int)loc[e];
+      h->dt.Kdim[e] = h->dt.Kdim[e - 1] + h->dt.rdep[e];
+    }
   }
   CK(cudaMemcpyAsync(h->d_dt, &h->dt, sizeof(DepthTab), cudaMemcpyHostToDevice, h->st));
   st = finish(h, HODLR_OK, &h->t_build);
@@ -365,13 +405,15 @@ hodlr_status hodlr_info(hodlr_t h, hodlr_info_t *info) {
   for (int e = 1; e <= h->kappa && e < 64; e++) {
     info->max_rank_by_depth[e] = h->dt.rdep[e];
     double s = 0; long long c = 0;
-    for (long long b = (1LL << (e - 1)) - 1; b < (1LL << e) - 1; b++) { s += h->h_rank[b]; c++; }
+    for (long long b = (1LL << (e - 1)) - 1; b < (1LL << e) - 1; b++)
+      if (hodlr_owns_block(h, b)) { s += h->h_rank[b]; c++; }
     info->mean_rank_by_depth[e] = c ? s / c : 0.0;
   }
   info->factor_bytes = h->bytes;
   info->t_build = h->t_build; info->t_factor = h->t_factor; info->t_logdet = h->t_logdet; info->t_solve = h->t_solve;
   info->rank_cap_hits = h->rank_cap_hits;
   info->aca_steps = h->aca_steps;
+  info->rank = h->grank; info->nranks = h->nranks; info->split_depth = h->tsplit;
   info->gpu_launches_last = h->launches;
   for (int p = 0; p < PH_N && p < 16; p++) { info->kernel_ms[p] = h->ph_ms[p]; info->kernel_calls[p] = h->ph_calls[p]; }
   return HODLR_OK;

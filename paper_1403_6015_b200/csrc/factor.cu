@@ -48,6 +48,7 @@ struct LeafCtx {
   long long scratch_per_cta;
   int use_smem;
   int mmax;                 // max leaf size
+  long long leaf0, nown;    // this rank's leaves [leaf0, leaf0 + nown)
   long long lsz;            // packed triangle capacity mmax(mmax+1)/2 + 1
 };
 
@@ -58,7 +59,7 @@ __global__ void __launch_bounds__(LT) k_leaf_factor(LeafCtx c) {
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int K = c.K, ldz = c.ldz;
   double *base = c.use_smem ? sm : c.scratch + (long long)blockIdx.x * c.scratch_per_cta;
-  for (long long leaf = blockIdx.x; leaf < c.nleaves; leaf += gridDim.x) {
+  for (long long leaf = c.leaf0 + blockIdx.x; leaf < c.leaf0 + c.nown; leaf += gridDim.x) {
     const long long id = c.ninternal + leaf, lo = c.lo[id], m = c.hi[id] - lo;
     double *xl = base;                       // m
     double *L = base + c.mmax;               // packed lower m(m+1)/2
@@ -158,6 +159,7 @@ __global__ void __launch_bounds__(LT) k_leaf_factor(LeafCtx c) {
 
 struct TreeCtx {
   int d;                    // depth of the nodes of this launch
+  long long i0;             // first node (index within depth d) of this launch
   int r, q, Kd, K1, ldk;    // ldk: row stride of B / T in shared memory (Kd rounded up to 4)
   int dd;                   // compensated (double-double) T and Pi
   const double *Pi1;        // children Pi base (depth d+1), packed K1(K1+1)/2 per node
@@ -390,15 +392,17 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm) {
 template <bool DD>
 __global__ void __launch_bounds__(TT, 3) k_tree_factor(TreeCtx c) {
   extern __shared__ double sm[];
-  tree_node<DD>(c, blockIdx.x, sm);
+  tree_node<DD>(c, c.i0 + blockIdx.x, sm);
 }
 
-// log det = leaves (left to right), then internal nodes by depth kappa-1..0, left to right;
-// per-thread Neumaier over a contiguous segment, combined in order by thread 0.
-__global__ void k_logdet_reduce(const double *leaf_ld, const double *node_ld, long long nleaves, int kappa,
-                                double *out) {
+// log det partial = leaves (left to right), then internal nodes of depth >= tsplit by depth kappa-1..tsplit,
+// left to right; per-thread Neumaier over a contiguous segment, combined in order by thread 0.
+// out[0] = partial, out[1] = failures seen by this rank.
+__global__ void k_logdet_reduce(const double *leaf_ld, const double *node_ld, long long nleaves, int kappa, int tsplit,
+                                const int *flags, double *out) {
   __shared__ double ss[256], cc[256];
-  const long long N = nleaves + nleaves - 1;
+  const long long nnode = nleaves - (1LL << tsplit);     // internal nodes of depth >= tsplit
+  const long long N = nleaves + nnode;
   const int t = threadIdx.x;
   long long per = (N + 255) / 256, v0 = t * per, v1 = v0 + per < N ? v0 + per : N;
   double s = 0.0, comp = 0.0;
@@ -426,7 +430,29 @@ __global__ void k_logdet_reduce(const double *leaf_ld, const double *node_ld, lo
       S = tt;
       Cc += cc[j];
     }
-    *out = S + Cc;
+    out[0] = S + Cc;
+    out[1] = (double)flags[1];
+  }
+}
+
+// log det = sum of the ranks' partials (rank order) + the top-level nodes (depth tsplit-1..0, left to right);
+// failures of any rank make every rank report ENOTPD.
+__global__ void k_logdet_final(const double *gathered, int nranks, const double *node_ld, int tsplit, int *flags,
+                               double *out) {
+  if (threadIdx.x != 0) return;
+  double S = 0.0, Cc = 0.0, fails = 0.0;
+  auto add = [&](double x) {
+    double tt = S + x;
+    if (fabs(S) >= fabs(x)) Cc += (S - tt) + x; else Cc += (x - tt) + S;
+    S = tt;
+  };
+  for (int r = 0; r < nranks; r++) { add(gathered[2 * r]); fails += gathered[2 * r + 1]; }
+  for (int d = tsplit - 1; d >= 0; d--)
+    for (long long i = 0; i < (1LL << d); i++) add(node_ld[(1LL << d) - 1 + i]);
+  *out = S + Cc;
+  if (nranks > 1 && fails > flags[1]) {
+    if (flags[1] == 0) flags[2] = -1;       // failure on another rank
+    flags[1] = (int)fails;
   }
 }
 
@@ -443,6 +469,7 @@ hodlr_status hodlr_leaf_alloc(hodlr_s *h) {
   h->Lf = (double *)hodlr_dalloc(h, sizeof(double) * h->lstride * nl);
   h->leaf_ld = (double *)hodlr_dalloc(h, sizeof(double) * nl);
   if (!h->Lf || !h->leaf_ld) return hodlr_set_error(HODLR_ENOMEM, "leaf factor allocation failed");
+  HCUDA(cudaMemsetAsync(h->leaf_ld, 0, sizeof(double) * nl, h->st));      // other ranks' leaves count 0
   return HODLR_OK;
 }
 
@@ -468,8 +495,10 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
   h->Pipool = (double *)hodlr_dalloc(h, sizeof(double) * (piTot > 0 ? piTot : 1));
   h->Spool = (double *)hodlr_dalloc(h, sizeof(double) * (sTot > 0 ? sTot : 1));
   h->BTpool = (double *)hodlr_dalloc(h, sizeof(double) * (btTot > 0 ? btTot : 1));
-  if (!h->node_ld || !h->d_logdet || !h->Pipool || !h->Spool || !h->BTpool)
+  double *ldx = (double *)hodlr_dalloc(h, sizeof(double) * 2 * (h->nranks + 1));   // log det exchange
+  if (!h->node_ld || !h->d_logdet || !h->Pipool || !h->Spool || !h->BTpool || !ldx)
     return hodlr_set_error(HODLR_ENOMEM, "factor: device allocation failed");
+  HCUDA(cudaMemsetAsync(h->node_ld, 0, sizeof(double) * (h->ninternal > 0 ? h->ninternal : 1), h->st));
   HCUDA(cudaMemcpyAsync(h->d_dt, &dt, sizeof(DepthTab), cudaMemcpyHostToDevice, h->st));
   if (K > 1024) return hodlr_set_error(HODLR_EINVAL, "factor: K = %d ancestor columns exceeds 1024", K);
   int maxsm = 0;
@@ -489,16 +518,17 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
     lc.dt = h->d_dt; lc.Lf = h->Lf; lc.lstride = h->lstride; lc.Pi = h->Pipool + dt.piOff[kappa];
     lc.leaf_ld = h->leaf_ld; lc.flags = h->dflags;
     lc.mmax = mmax;
+    hodlr_own_nodes(h, kappa, &lc.leaf0, &lc.nown);
     lc.lsz = (long long)mmax * (mmax + 1) / 2 + 1;
     size_t need = sizeof(double) * (mmax + lc.lsz + (size_t)mmax * lc.ldz);
-    int grid = (int)nl;
+    int grid = (int)lc.nown;
     lc.scratch = nullptr; lc.scratch_per_cta = 0;
     if (need <= (size_t)maxsm - 12 * 1024) {
       lc.use_smem = 1;
       HCUDA(cudaFuncSetAttribute(k_leaf_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
     } else {
       lc.use_smem = 0; need = 0;
-      grid = (int)(nl < 148 * 4 ? nl : 148 * 4);
+      grid = (int)(lc.nown < 148 * 4 ? lc.nown : 148 * 4);
       lc.scratch_per_cta = mmax + lc.lsz + (long long)mmax * lc.ldz;
       lc.scratch = (double *)hodlr_dalloc(h, sizeof(double) * lc.scratch_per_cta * grid);
       if (!lc.scratch) return hodlr_set_error(HODLR_ENOMEM, "factor: scratch allocation failed");
@@ -526,19 +556,35 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
   static int plain_from = -1;
   if (plain_from < 0) { const char *ev = getenv("HODLR_TREE_PLAIN_FROM"); plain_from = ev ? atoi(ev) : 1 << 20; }
   for (int d = kappa - 1; d >= 0; d--) {
+    if (d + 1 == h->tsplit && h->nranks > 1) {     // every rank gets the Pi of all depth-t subtree roots
+      const long long Kt = dt.Kdim[d + 1], sz = Kt * (Kt + 1) / 2;
+      double *base = h->Pipool + dt.piOff[d + 1];
+      hodlr_status xs = hodlr_allgather(h, base + h->grank * sz, base, sizeof(double) * sz);
+      if (xs != HODLR_OK) return xs;
+    }
+    long long i0, cnt;
+    hodlr_own_nodes(h, d, &i0, &cnt);
     TreeCtx tc;
-    tc.d = d; tc.r = dt.rdep[d + 1]; tc.q = 2 * tc.r; tc.Kd = dt.Kdim[d]; tc.K1 = dt.Kdim[d + 1];
+    tc.d = d; tc.i0 = i0; tc.r = dt.rdep[d + 1]; tc.q = 2 * tc.r; tc.Kd = dt.Kdim[d]; tc.K1 = dt.Kdim[d + 1];
     tc.ldk = (tc.Kd + 3) & ~3; tc.dd = d < plain_from;
     tc.Pi1 = h->Pipool + dt.piOff[d + 1]; tc.Pic = h->Pipool + dt.piOff[d];
     tc.Sst = h->Spool + dt.nodeS[d]; tc.BT = h->BTpool + dt.nodeBT[d];
     tc.node_ld = h->node_ld; tc.flags = h->dflags;
     const size_t smem = sizeof(double) * (size_t)tree_smem_doubles(tc.q, tc.ldk);
-    if (tc.dd) k_tree_factor<true><<<(int)(1LL << d), TT, smem, h->st>>>(tc);
-    else k_tree_factor<false><<<(int)(1LL << d), TT, smem, h->st>>>(tc);
+    if (tc.dd) k_tree_factor<true><<<(int)cnt, TT, smem, h->st>>>(tc);
+    else k_tree_factor<false><<<(int)cnt, TT, smem, h->st>>>(tc);
     HLAUNCH(h, "k_tree_factor");
   }
-  k_logdet_reduce<<<1, 256, 0, h->st>>>(h->leaf_ld, h->node_ld, nl, kappa, h->d_logdet);
+  // log det: this rank's leaves and subtree nodes (others are 0), exchanged with the failure counts, then the
+  // top-level nodes (computed redundantly by every rank) once
+  k_logdet_reduce<<<1, 256, 0, h->st>>>(h->leaf_ld, h->node_ld, nl, kappa, h->tsplit, h->dflags, ldx + 2 * h->nranks);
   HLAUNCH(h, "k_logdet_reduce");
+  {
+    hodlr_status xs = hodlr_allgather(h, ldx + 2 * h->nranks, ldx, sizeof(double) * 2);
+    if (xs != HODLR_OK) return xs;
+  }
+  k_logdet_final<<<1, 32, 0, h->st>>>(ldx, h->nranks, h->node_ld, h->tsplit, h->dflags, h->d_logdet);
+  HLAUNCH(h, "k_logdet_final");
   ph_end(h, PH_TREE);
   return HODLR_OK;
 }

@@ -122,6 +122,12 @@ struct hodlr_s {
   int kappa;
   long long nnodes, ninternal, nleaves;
   int leaf_min, leaf_max;
+  // subtree sharding (dist.cu): rank g of nranks = 2^tsplit owns the depth-tsplit node g and its subtree
+  int grank, nranks, tsplit;
+  void *comm;                // ncclComm_t (NCCL transport) or NULL
+  void *group;               // HodlrGroup (in-process transport) or NULL
+  long long *d_rowlo;        // per rank: first sorted row of its subtree (device, nranks entries)
+  long long rows_max;        // max subtree rows over the ranks (allgather slice size of the solution)
   int state;                 // 1 built, 2 factored, -1 factor failed
   int launches;              // kernels launched by the current call
   int aca_steps;
@@ -151,6 +157,7 @@ struct hodlr_s {
   double logdet;
   // solve workspace
   double *Vpool, *Tvec, *hvec;
+  double *xshard;            // sharded solve: sorted solution rows + allgather send/recv slices
   // bookkeeping
   long long bytes;
   double t_build, t_factor, t_logdet, t_solve;
@@ -184,6 +191,23 @@ hodlr_status hodlr_leaf_alloc(hodlr_s *h);
 hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_only);
 
 static inline int hodlr_depth_of(long long id) { int d = 0; while (id >= ((2LL << d) - 1)) d++; return d; }
+
+// Nodes of depth d this rank computes: all 2^d above the split depth, its own 2^(d - t) below it.
+static inline void hodlr_own_nodes(const hodlr_s *h, int d, long long *i0, long long *cnt) {
+  if (d < h->tsplit) { *i0 = 0; *cnt = 1LL << d; }
+  else { *cnt = 1LL << (d - h->tsplit); *i0 = (long long)h->grank * *cnt; }
+}
+// Is internal block b (heap id, depth d) computed by this rank?
+static inline bool hodlr_owns_block(const hodlr_s *h, long long b) {
+  const int d = hodlr_depth_of(b);
+  if (d < h->tsplit) return true;
+  return (((b + 1) >> (d - h->tsplit)) - 1) == ((1LL << h->tsplit) - 1 + h->grank);
+}
+
+// dist.cu
+hodlr_status hodlr_dist_init(hodlr_s *h, const hodlr_dist *d);
+void hodlr_dist_fini(hodlr_s *h);
+hodlr_status hodlr_allgather(hodlr_s *h, const void *send, void *recv, size_t bytes);   // bytes per rank
 
 #define HCUDA(call) do { cudaError_t _e = (call); if (_e != cudaSuccess) return hodlr_cuda_check(_e, #call); } while (0)
 #define HLAUNCH(h, name) do { (h)->launches++; hodlr_global_launches++; cudaError_t _e = cudaGetLastError(); \

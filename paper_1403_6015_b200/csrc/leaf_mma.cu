@@ -61,6 +61,7 @@ struct LeafMmaCtx {
   double *Pi;
   double *leaf_ld;
   int *flags;
+  long long leaf0;          // first leaf of this launch (this rank's subtree)
 };
 
 // One warp, every lane computes the same 8x8 POTRF redundantly (no shuffles on the critical path),
@@ -145,7 +146,7 @@ __global__ void __launch_bounds__(NTH, 2) k_leaf_chol(LeafMmaCtx c) {
   double *sLi = sL + NTILE * 64;                // T * 64
   double *sx = sLi + T * 64;                    // P
   double *sdiag = sx + P;                       // P
-  const long long leaf = blockIdx.x;
+  const long long leaf = c.leaf0 + blockIdx.x;
   const long long id = c.ninternal + leaf, lo = c.lo[id];
   const int m = (int)(c.hi[id] - lo);
   if (t == 0) bad = 0;
@@ -293,7 +294,7 @@ __global__ void __launch_bounds__(ZTH, 1) k_leaf_zsyrk(LeafMmaCtx c) {
   double *sX = sm;                              // NTILE * 64: tiles of X = L^{-1}
   double *sZ = sX + NTILE * 64;                 // Kz * LDR (column-major)
   long long *colsrc = (long long *)(sZ + (long long)Kz * LDR);   // Kz
-  const long long leaf = blockIdx.x;
+  const long long leaf = c.leaf0 + blockIdx.x;
   const long long id = c.ninternal + leaf, lo = c.lo[id];
   const int m = (int)(c.hi[id] - lo);
   {
@@ -411,6 +412,8 @@ static LeafMmaCtx leaf_ctx(hodlr_s *h, int K, double *Pi_leaf) {
   c.Kz = (K + 15) / 16 * 16;
   c.xs = h->xs; c.lo = h->lo; c.hi = h->hi; c.Xh = h->Xh; c.rank = h->rank; c.dt = h->d_dt;
   c.Lf = h->Lf; c.lstride = h->lstride; c.Pi = Pi_leaf; c.leaf_ld = h->leaf_ld; c.flags = h->dflags;
+  long long cnt;
+  hodlr_own_nodes(h, h->kappa, &c.leaf0, &cnt);
   return c;
 }
 
@@ -426,10 +429,10 @@ hodlr_status hodlr_leaf_chol_mma(hodlr_s *h, cudaStream_t stream, bool *launched
   LeafMmaCtx c = leaf_ctx(h, 0, nullptr);
   if (P == 64) {
     HCUDA(cudaFuncSetAttribute(k_leaf_chol<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_leaf_chol<64><<<(int)h->nleaves, NTH, smem, stream>>>(c);
+    k_leaf_chol<64><<<(int)(h->nleaves >> h->tsplit), NTH, smem, stream>>>(c);
   } else {
     HCUDA(cudaFuncSetAttribute(k_leaf_chol<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_leaf_chol<128><<<(int)h->nleaves, NTH, smem, stream>>>(c);
+    k_leaf_chol<128><<<(int)(h->nleaves >> h->tsplit), NTH, smem, stream>>>(c);
   }
   HLAUNCH(h, "k_leaf_chol");
   *launched = true;
@@ -454,10 +457,10 @@ hodlr_status hodlr_leaf_factor_mma(hodlr_s *h, int K, double *Pi_leaf, bool *use
   LeafMmaCtx c = leaf_ctx(h, K, Pi_leaf);
   if (P == 64) {
     HCUDA(cudaFuncSetAttribute(k_leaf_zsyrk<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_leaf_zsyrk<64><<<(int)h->nleaves, ZTH, smem, h->st>>>(c);
+    k_leaf_zsyrk<64><<<(int)(h->nleaves >> h->tsplit), ZTH, smem, h->st>>>(c);
   } else {
     HCUDA(cudaFuncSetAttribute(k_leaf_zsyrk<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_leaf_zsyrk<128><<<(int)h->nleaves, ZTH, smem, h->st>>>(c);
+    k_leaf_zsyrk<128><<<(int)(h->nleaves >> h->tsplit), ZTH, smem, h->st>>>(c);
   }
   HLAUNCH(h, "k_leaf_zsyrk");
   *used = true;

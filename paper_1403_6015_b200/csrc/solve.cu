@@ -31,7 +31,9 @@ struct SolveCtx {
   double *hv;       // per-node h = y_c^T K_cc^{-1} y_c as a double-double pair (heap id)
   const double *y;
   double *x;
+  double *xsorted;  // sharded solve: this rank's solution rows in sorted order (NULL on one GPU)
   int *flags;
+  long long leaf0;  // first leaf of this rank
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -133,7 +135,7 @@ __global__ void __launch_bounds__(LT, 1) k_leaf_up(SolveCtx c) {
   __shared__ double sb[VMAX], su[VMAX], red[2 * VMAX];
   __shared__ int colsrc[1024];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5, NW = LT / 32;
-  const long long leaf = blockIdx.x;
+  const long long leaf = c.leaf0 + blockIdx.x;
   const long long id = c.ninternal + leaf, lo = c.lo[id];
   const int m = (int)(c.hi[id] - lo), R = 8 * c.T, K = c.K;
   double *sX = sm, *sE = sm + 64 * (c.T * (c.T + 1) / 2);
@@ -179,7 +181,7 @@ __global__ void __launch_bounds__(LT, 1) k_leaf_down(SolveCtx c) {
   __shared__ double sw[1024];
   __shared__ double part4[4 * VMAX];
   const int t = threadIdx.x;
-  const long long leaf = blockIdx.x;
+  const long long leaf = c.leaf0 + blockIdx.x;
   const long long id = c.ninternal + leaf, lo = c.lo[id];
   const int m = (int)(c.hi[id] - lo), R = 8 * c.T, K = c.K;
   double *sX = sm, *sE = sm + 64 * (c.T * (c.T + 1) / 2);
@@ -203,7 +205,24 @@ __global__ void __launch_bounds__(LT, 1) k_leaf_down(SolveCtx c) {
   __syncthreads();
   tri_mv(sX, c.T, sb, su, red);
   tri_mvt(sX, c.T, su, sb, red);
-  for (int i = t; i < m; i += LT) c.x[c.perm[lo + i]] = sb[i];
+  if (c.xsorted) for (int i = t; i < m; i += LT) c.xsorted[lo + i] = sb[i];
+  else for (int i = t; i < m; i += LT) c.x[c.perm[lo + i]] = sb[i];
+}
+
+// sharded solve: x[perm[row_lo_r + i]] = slice_r[i] for every rank's slice of the gathered solution
+__global__ void k_unshard(const double *gathered, const long long *rowlo, int nranks, long long rows_max, long long n,
+                          const long long *perm, double *x) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= (long long)nranks * rows_max) return;
+  const int r = (int)(e / rows_max);
+  const long long i = e - (long long)r * rows_max;
+  const long long lo = rowlo[r], hi = r + 1 < nranks ? rowlo[r + 1] : n;
+  if (lo + i < hi) x[perm[lo + i]] = gathered[e];
+}
+
+__global__ void k_pack_rows(const double *xsorted, long long lo, long long m, double *send) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < m) send[i] = xsorted[lo + i];
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -237,11 +256,11 @@ __device__ void dd_solve_warp(const double *S0, const double *Si, int q, const d
   }
 }
 
-__global__ void __launch_bounds__(ST) k_tree_up(SolveCtx c, int d) {
+__global__ void __launch_bounds__(ST) k_tree_up(SolveCtx c, int d, long long i0, long long cnt) {
   extern __shared__ double dsm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const long long i = (long long)blockIdx.x * NWS + wid;
-  if (i >= (1LL << d)) return;
+  if ((long long)blockIdx.x * NWS + wid >= cnt) return;
+  const long long i = i0 + (long long)blockIdx.x * NWS + wid;
   const long long node = (1LL << d) - 1 + i;
   const int r = c.dt->rdep[d + 1], q = 2 * r, Kd = c.dt->Kdim[d], K1 = c.dt->Kdim[d + 1];
   const double *g1 = c.V + c.dt->nodeV[d + 1] + (2 * i) * (long long)K1;
@@ -277,11 +296,11 @@ __global__ void __launch_bounds__(ST) k_tree_up(SolveCtx c, int d) {
   }
 }
 
-__global__ void __launch_bounds__(ST) k_tree_down(SolveCtx c, int d) {
+__global__ void __launch_bounds__(ST) k_tree_down(SolveCtx c, int d, long long i0, long long cnt) {
   __shared__ double sf[NWS][QMAX];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const long long i = (long long)blockIdx.x * NWS + wid;
-  if (i >= (1LL << d)) return;
+  if ((long long)blockIdx.x * NWS + wid >= cnt) return;
+  const long long i = i0 + (long long)blockIdx.x * NWS + wid;
   const int r = c.dt->rdep[d + 1], q = 2 * r, Kd = c.dt->Kdim[d], K1 = c.dt->Kdim[d + 1];
   const double *wc = c.V + c.dt->nodeV[d] + i * (long long)Kd;
   const long long qK = (long long)q * Kd;
@@ -327,7 +346,17 @@ hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_on
   c.lo = h->lo; c.hi = h->hi; c.perm = h->perm; c.Xh = h->Xh; c.rank = h->rank; c.dt = h->d_dt;
   c.Lf = h->Lf; c.lstride = h->lstride; c.Spool = h->Spool; c.BTpool = h->BTpool;
   c.V = h->Vpool; c.Tv = h->Tvec; c.hv = h->hvec; c.y = y; c.x = x; c.flags = h->dflags;
-  const int lgrid = (int)h->nleaves;
+  long long lcnt;
+  hodlr_own_nodes(h, kappa, &c.leaf0, &lcnt);
+  c.xsorted = nullptr;
+  if (h->nranks > 1 && !up_only) {
+    if (!h->xshard) {
+      h->xshard = (double *)hodlr_dalloc(h, sizeof(double) * ((size_t)h->n + (size_t)h->rows_max * (h->nranks + 1)));
+      if (!h->xshard) return hodlr_set_error(HODLR_ENOMEM, "solve: device allocation failed");
+    }
+    c.xsorted = h->xshard;
+  }
+  const int lgrid = (int)lcnt;
   const int R = 8 * h->ltiles;
   // X tiles + E panel in shared memory
   const size_t lsm = sizeof(double) * (64 * (size_t)(h->ltiles * (h->ltiles + 1) / 2) + (size_t)c.K * R);
@@ -353,19 +382,44 @@ hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_on
   }
   if (kappa > 0) HCUDA(cudaFuncSetAttribute(k_tree_up, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)up_smem_max));
   for (int d = kappa - 1; d >= 0; d--) {
+    if (d + 1 == h->tsplit && h->nranks > 1) {   // projections g and h of all depth-t subtree roots
+      const long long Kt = dt.Kdim[d + 1];
+      double *gb = h->Vpool + dt.nodeV[d + 1];
+      hodlr_status xs = hodlr_allgather(h, gb + h->grank * Kt, gb, sizeof(double) * (Kt > 0 ? Kt : 1));
+      if (xs != HODLR_OK) return xs;
+      double *hb = h->hvec + 2 * ((1LL << (d + 1)) - 1);
+      xs = hodlr_allgather(h, hb + 2 * h->grank, hb, sizeof(double) * 2);
+      if (xs != HODLR_OK) return xs;
+    }
+    long long i0, cnt;
+    hodlr_own_nodes(h, d, &i0, &cnt);
     const size_t q = 2 * (size_t)dt.rdep[d + 1];
-    k_tree_up<<<(int)(((1LL << d) + NWS - 1) / NWS), ST, sizeof(double) * NWS * (2 * q * q + 5 * q), h->st>>>(c, d);
+    k_tree_up<<<(int)((cnt + NWS - 1) / NWS), ST, sizeof(double) * NWS * (2 * q * q + 5 * q), h->st>>>(c, d, i0, cnt);
     HLAUNCH(h, "k_tree_up");
   }
   if (up_only) { ph_end(h, PH_STREE); return HODLR_OK; }
   for (int d = 0; d < kappa; d++) {
-    k_tree_down<<<(int)(((1LL << d) + NWS - 1) / NWS), ST, 0, h->st>>>(c, d);
+    long long i0, cnt;
+    hodlr_own_nodes(h, d, &i0, &cnt);
+    k_tree_down<<<(int)((cnt + NWS - 1) / NWS), ST, 0, h->st>>>(c, d, i0, cnt);
     HLAUNCH(h, "k_tree_down");
   }
   ph_end(h, PH_STREE);
   ph_begin(h, PH_SLEAF_DOWN);
   k_leaf_down<<<lgrid, LT, lsm, h->st>>>(c);
   HLAUNCH(h, "k_leaf_down");
+  if (h->nranks > 1) {            // every rank returns the full solution: allgather the sorted row slices
+    const long long id = (1LL << h->tsplit) - 1 + h->grank;
+    const long long rlo = h->h_lo[id], rm = h->h_hi[id] - rlo;
+    double *send = h->xshard + h->n, *recv = send + h->rows_max;
+    k_pack_rows<<<(int)((rm + 255) / 256), 256, 0, h->st>>>(h->xshard, rlo, rm, send);
+    HLAUNCH(h, "k_pack_rows");
+    hodlr_status xs = hodlr_allgather(h, send, recv, sizeof(double) * h->rows_max);
+    if (xs != HODLR_OK) return xs;
+    const long long tot = (long long)h->nranks * h->rows_max;
+    k_unshard<<<(int)((tot + 255) / 256), 256, 0, h->st>>>(recv, h->d_rowlo, h->nranks, h->rows_max, h->n, h->perm, x);
+    HLAUNCH(h, "k_unshard");
+  }
   ph_end(h, PH_SLEAF_DOWN);
   return HODLR_OK;
 }

@@ -1,0 +1,93 @@
+// sweep.cu -- config 4 (BASELINE.json): GP log-likelihood (eq. 1) of B hyper-parameter
+// settings (a, ell, sigma2) on the same points and observations.  The settings are independent problems:
+// on one GPU up to `workers` of them run concurrently (host threads, one stream each, so the small top-level
+// kernels of different settings overlap); with dist (nranks > 1) rank g takes settings g, g + P, ... and the
+// values are allgathered ("replicas only").
+#include "hodlr_internal.cuh"
+#include <thread>
+#include <vector>
+#include <atomic>
+#include <string.h>
+#include <string>
+
+extern "C" hodlr_status gp_loglik_sweep(const double *x, const double *y, int64_t n, hodlr_kernel kernel,
+                                        const double *thetas, const double *sigma2s, int32_t B, int32_t leaf,
+                                        double eps, const hodlr_dist *dist, void *cuda_stream, int32_t workers,
+                                        double *out_host) {
+  if (!x || !y || !thetas || !sigma2s || !out_host || B < 1 || n < 1)
+    return hodlr_set_error(HODLR_EINVAL, "gp_loglik_sweep: bad arguments");
+  int dev = 0;
+  cudaError_t ce = cudaGetDevice(&dev);
+  if (ce != cudaSuccess) return hodlr_cuda_check(ce, "cudaGetDevice");
+  const int P = (dist && dist->nranks > 1) ? dist->nranks : 1;
+  const int g = P > 1 ? dist->rank : 0;
+  std::vector<int> mine;
+  for (int b = g; b < B; b += P) mine.push_back(b);
+  std::vector<double> val(B, 0.0);
+  std::vector<hodlr_status> stat(B, HODLR_OK);
+  std::vector<std::string> msg(B);
+  std::atomic<int> next(0);
+  const int W = std::max(1, std::min<int>(workers > 0 ? workers : 4, (int)mine.size()));
+  auto work = [&]() {
+    cudaSetDevice(dev);
+    cudaStream_t s;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    for (;;) {
+      const int k = next.fetch_add(1);
+      if (k >= (int)mine.size()) break;
+      const int b = mine[k];
+      hodlr_t h = nullptr;
+      double ll = -INFINITY;
+      hodlr_status st = hodlr_build(x, n, kernel, thetas + 2 * b, sigma2s[b], leaf, eps, nullptr, nullptr, s, &h);
+      if (st == HODLR_OK) st = hodlr_factor(h);
+      if (st == HODLR_OK) st = gp_loglik(h, y, &ll);
+      if (st != HODLR_OK) msg[b] = hodlr_last_error();
+      hodlr_free(h);
+      val[b] = st == HODLR_OK ? ll : -INFINITY;
+      stat[b] = st;
+    }
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+  };
+  // the caller's stream orders our reads of x and y after its prior work
+  ce = cudaStreamSynchronize((cudaStream_t)cuda_stream);
+  if (ce != cudaSuccess) return hodlr_cuda_check(ce, "gp_loglik_sweep: stream");
+  std::vector<std::thread> th;
+  for (int w = 0; w < W; w++) th.emplace_back(work);
+  for (auto &t : th) t.join();
+  if (P > 1) {     // allgather (value, status) of every rank's settings (slot k of rank r = setting r + k P)
+    hodlr_s ex;
+    memset((void *)&ex, 0, sizeof(ex));
+    ex.kappa = 1 << 20; ex.dev = dev; ex.st = (cudaStream_t)cuda_stream;
+    hodlr_status st = hodlr_dist_init(&ex, dist);
+    if (st != HODLR_OK) return st;
+    const int per = (B + P - 1) / P;
+    std::vector<double> send(2 * per, 0.0), all(2 * (size_t)per * P, 0.0);
+    for (int k = 0; k < (int)mine.size(); k++) { send[2 * k] = val[mine[k]]; send[2 * k + 1] = (double)stat[mine[k]]; }
+    double *dbuf = nullptr;
+    if (cudaMalloc(&dbuf, sizeof(double) * 2 * per * (P + 1)) != cudaSuccess) return hodlr_set_error(HODLR_ENOMEM, "sweep");
+    cudaMemcpy(dbuf, send.data(), sizeof(double) * 2 * per, cudaMemcpyHostToDevice);
+    st = hodlr_allgather(&ex, dbuf, dbuf + 2 * per, sizeof(double) * 2 * per);
+    if (st == HODLR_OK) {
+      cudaStreamSynchronize(ex.st);
+      cudaMemcpy(all.data(), dbuf + 2 * per, sizeof(double) * 2 * per * P, cudaMemcpyDeviceToHost);
+    }
+    cudaFree(dbuf);
+    hodlr_dist_fini(&ex);
+    if (st != HODLR_OK) return st;
+    for (int r = 0; r < P; r++)
+      for (int k = 0; r + k * P < B; k++) {
+        val[r + k * P] = all[2 * ((size_t)r * per + k)];
+        stat[r + k * P] = (hodlr_status)(int)all[2 * ((size_t)r * per + k) + 1];
+      }
+  }
+  hodlr_status first = HODLR_OK;
+  for (int b = 0; b < B; b++) {
+    out_host[b] = val[b];
+    if (first == HODLR_OK && stat[b] != HODLR_OK) {
+      first = stat[b];
+      hodlr_set_error(first, "gp_loglik_sweep: setting %d: %s", b, msg[b].empty() ? "(on another rank)" : msg[b].c_str());
+    }
+  }
+  return first;
+}

@@ -20,7 +20,8 @@ STATUS = {0: "OK", 1: "EINVAL", 2: "ENOTPD", 3: "ERANKCAP", 4: "ESTATE", 5: "ENO
 
 EXPORTS = ("hodlr_build", "hodlr_factor", "hodlr_logdet", "hodlr_solve", "gp_loglik", "hodlr_info",
            "hodlr_get_order", "hodlr_get_tree", "hodlr_get_logdet_parts", "hodlr_free", "hodlr_last_error",
-           "hodlr_version", "hodlr_launch_count")
+           "hodlr_version", "hodlr_launch_count", "hodlr_nccl_unique_id", "hodlr_group_create",
+           "hodlr_group_destroy", "hodlr_dist_plan", "gp_loglik_sweep")
 
 
 class HodlrError(RuntimeError):
@@ -31,7 +32,7 @@ class HodlrError(RuntimeError):
 
 
 class hodlr_dist(C.Structure):
-    _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("nccl_unique_id", C.c_void_p)]
+    _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("nccl_unique_id", C.c_void_p), ("group", C.c_void_p)]
 
 
 class hodlr_opts(C.Structure):
@@ -44,7 +45,8 @@ class hodlr_info_t(C.Structure):
                 ("factor_bytes", C.c_int64), ("t_build", C.c_double), ("t_factor", C.c_double),
                 ("t_logdet", C.c_double), ("t_solve", C.c_double), ("rank_cap_hits", C.c_int64),
                 ("aca_steps", C.c_int32), ("gpu_launches_last", C.c_int32),
-                ("kernel_ms", C.c_double * 16), ("kernel_calls", C.c_int64 * 16)]
+                ("kernel_ms", C.c_double * 16), ("kernel_calls", C.c_int64 * 16),
+                ("rank", C.c_int32), ("nranks", C.c_int32), ("split_depth", C.c_int32), ("pad_", C.c_int32)]
 
 KERNEL_FAMILIES = ("sort", "aca", "leaf_factor", "coupling_tree", "solve_leaf_up", "solve_tree", "solve_leaf_down",
                    "leaf_chol")
@@ -87,6 +89,12 @@ def load(build_if_missing: bool = True):
         lib.hodlr_last_error.argtypes = []; lib.hodlr_last_error.restype = C.c_char_p
         lib.hodlr_version.argtypes = []; lib.hodlr_version.restype = C.c_char_p
         lib.hodlr_launch_count.argtypes = []; lib.hodlr_launch_count.restype = C.c_int64
+        lib.hodlr_nccl_unique_id.argtypes = [P]; lib.hodlr_nccl_unique_id.restype = I32
+        lib.hodlr_group_create.argtypes = [I32, P]; lib.hodlr_group_create.restype = I32
+        lib.hodlr_group_destroy.argtypes = [P]; lib.hodlr_group_destroy.restype = None
+        lib.hodlr_dist_plan.argtypes = [I64, I32, I32, I32, P, P, P, P, P, P]; lib.hodlr_dist_plan.restype = I32
+        lib.gp_loglik_sweep.argtypes = [P, P, I64, I32, P, P, I32, I32, D, P, P, I32, P]
+        lib.gp_loglik_sweep.restype = I32
         _lib = lib
         return lib
 
@@ -109,14 +117,15 @@ def _stream_ptr(stream) -> int:
 
 # ------------------------------------------------------------------ C-ABI mirrors
 def hodlr_build(x: torch.Tensor, kernel: int, theta, sigma2: float, leaf: int, eps: float,
-                rank_cap: int = 0, stream=None) -> int:
+                rank_cap: int = 0, stream=None, dist: "hodlr_dist | None" = None) -> int:
     lib = load()
     x = _dev_f64(x, "x")
     th = (C.c_double * 2)(float(theta[0]), float(theta[1]))
     opts = hodlr_opts(int(rank_cap))
     h = C.c_void_p(0)
     _check(lib.hodlr_build(x.data_ptr(), x.numel(), int(kernel), th, float(sigma2), int(leaf), float(eps),
-                           None, C.byref(opts), _stream_ptr(stream), C.byref(h)))
+                           C.byref(dist) if dist is not None else None, C.byref(opts), _stream_ptr(stream),
+                           C.byref(h)))
     return h.value
 
 
@@ -152,6 +161,28 @@ def gp_loglik(h: int, y: torch.Tensor) -> float:
     return v.value
 
 
+def gp_loglik_sweep(x: torch.Tensor, y: torch.Tensor, kernel: int, thetas, sigma2s, leaf: int, eps: float,
+                    dist=None, workers: int = 0, stream=None):
+    """Config 4: log-likelihoods of B settings; thetas (B, 2) {a, ell}, sigma2s (B,).  Returns a numpy array."""
+    import numpy as np
+    lib = load()
+    x = _dev_f64(x, "x"); y = _dev_f64(y, "y")
+    th = np.ascontiguousarray(np.asarray(thetas, dtype=np.float64).reshape(-1, 2))
+    s2 = np.ascontiguousarray(np.asarray(sigma2s, dtype=np.float64).reshape(-1))
+    out = np.zeros(s2.size)
+    ds = dist.struct() if dist is not None else None
+    code = lib.gp_loglik_sweep(x.data_ptr(), y.data_ptr(), x.numel(), int(kernel), th.ctypes.data, s2.ctypes.data,
+                               s2.size, int(leaf), float(eps), C.byref(ds) if ds is not None else None,
+                               _stream_ptr(stream), int(workers), out.ctypes.data)
+    if code != 0 and not np.all(np.isneginf(out) | np.isfinite(out)):
+        _check(code)
+    if code != 0:
+        err = HodlrError(code, load().hodlr_last_error().decode())
+        err.values = out
+        raise err
+    return out
+
+
 def hodlr_info(h: int) -> dict:
     info = hodlr_info_t()
     _check(load().hodlr_info(h, C.byref(info)))
@@ -163,7 +194,8 @@ def hodlr_info(h: int) -> dict:
             "t_logdet": info.t_logdet, "t_solve": info.t_solve, "rank_cap_hits": info.rank_cap_hits,
             "aca_steps": info.aca_steps, "gpu_launches_last": info.gpu_launches_last,
             "kernel_ms": {f: info.kernel_ms[i] for i, f in enumerate(KERNEL_FAMILIES)},
-            "kernel_calls": {f: info.kernel_calls[i] for i, f in enumerate(KERNEL_FAMILIES)}}
+            "kernel_calls": {f: info.kernel_calls[i] for i, f in enumerate(KERNEL_FAMILIES)},
+            "rank": info.rank, "nranks": info.nranks, "split_depth": info.split_depth}
 
 
 def hodlr_launch_count() -> int:
@@ -175,20 +207,37 @@ def hodlr_free(h: int):
         load().hodlr_free(h)
 
 
+def hodlr_dist_plan(n: int, leaf: int, rank: int, nranks: int) -> dict:
+    """Host-side shard plan (no device work): kappa, split depth t, owned sorted rows and leaves."""
+    lib = load()
+    k, t = C.c_int32(0), C.c_int32(0)
+    rl, rh, ll, lh = C.c_int64(0), C.c_int64(0), C.c_int64(0), C.c_int64(0)
+    _check(lib.hodlr_dist_plan(int(n), int(leaf), int(rank), int(nranks), C.byref(k), C.byref(t), C.byref(rl),
+                               C.byref(rh), C.byref(ll), C.byref(lh)))
+    return {"kappa": k.value, "t": t.value, "row_lo": rl.value, "row_hi": rh.value,
+            "leaf_lo": ll.value, "leaf_hi": lh.value}
+
+
 class HODLR:
     """build -> factor -> {logdet, solve, gp_loglik}* on one GPU; inputs are CUDA float64 tensors."""
 
     def __init__(self, x: torch.Tensor, kernel, theta, sigma2: float, leaf: int, eps: float,
-                 rank_cap: int = 0, stream=None):
+                 rank_cap: int = 0, stream=None, dist=None):
+        """dist: None (one GPU) or a paper_1403_6015_b200.dist.Dist (subtree sharding)."""
         if isinstance(kernel, str):
             kernel = KERNELS[kernel]
         self.n = x.numel()
-        self._h = hodlr_build(x, kernel, theta, sigma2, leaf, eps, rank_cap, stream)
+        self._dist = dist                       # keeps the NCCL id / group alive
+        self._h = hodlr_build(x, kernel, theta, sigma2, leaf, eps, rank_cap, stream,
+                              dist.struct() if dist is not None else None)
 
     def __del__(self):
         h = getattr(self, "_h", 0)
         if h:
-            hodlr_free(h)
+            try:
+                hodlr_free(h)
+            except TypeError:                   # interpreter shutdown: module globals already cleared
+                pass
             self._h = 0
 
     def close(self):

@@ -1,0 +1,102 @@
+"""Subtree sharding on one B200 (-m gpu): P virtual ranks (host threads, in-process transport) run the
+sharded path -- own subtree ACA/leaves/tree levels, redundant top levels, allgather of the depth-log2(P)
+projected Gram matrices, log det partials, solve projections and solution slices -- and must reproduce the
+one-GPU factorization (same kernels on the same blocks: only the log det summation order differs) and the
+oracle."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import OracleHODLR  # noqa: E402
+from paper_1403_6015_b200 import inputs  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def hb():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1403_6015_b200.hodlr as hb
+    hb.load()
+    return hb
+
+
+def sharded(hb, P, x, y, kernel, theta, s2, leaf, eps):
+    from paper_1403_6015_b200.dist import run_virtual_ranks
+    xd = torch.from_numpy(x).cuda(); yd = torch.from_numpy(y).cuda()
+    torch.cuda.synchronize()
+
+    def fn(r, d):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            g = hb.HODLR(xd, kernel, theta, s2, leaf, eps, dist=d).factor()
+            out = (g.logdet(), g.solve(yd).cpu().numpy(), g.gp_loglik(yd), g.info())
+            g.close()
+        return out
+    return run_virtual_ranks(P, fn)
+
+
+CASES = [("cfg1", 2048, 2), ("cfg1", 2048, 8), ("cfg3", 1 << 16, 2), ("cfg3", 1 << 16, 8), ("cfg2", 65536, 4),
+         ("cfg5", 1 << 15, 4)]
+
+
+@pytest.mark.parametrize("name,n,P", CASES, ids=[f"{a}-{b}-P{c}" for a, b, c in CASES])
+def test_virtual_ranks_match_one_gpu(hb, name, n, P):
+    cfg = inputs.scaled(inputs.CONFIGS[name], n)
+    x = inputs.points(cfg); y = inputs.rhs(cfg)
+    g = hb.HODLR(torch.from_numpy(x).cuda(), cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, 1e-12).factor()
+    ld1 = g.logdet(); x1 = g.solve(torch.from_numpy(y).cuda()).cpu().numpy(); ll1 = g.gp_loglik(torch.from_numpy(y).cuda())
+    res = sharded(hb, P, x, y, cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, 1e-12)
+    for r, (ld, xs, ll, info) in enumerate(res):
+        assert info["rank"] == r and info["nranks"] == P and info["split_depth"] == P.bit_length() - 1
+        assert abs(ld - ld1) <= 1e-13 * abs(ld1), (r, ld, ld1)
+        assert np.linalg.norm(xs - x1) <= 1e-13 * np.linalg.norm(x1), (r, np.linalg.norm(xs - x1) / np.linalg.norm(x1))
+        assert abs(ll - ll1) <= 1e-13 * (abs(ll1) + abs(ld1))
+    print(f"[sharded] {name} n={n} P={P}: logdet rel {abs(res[0][0] - ld1) / abs(ld1):.1e} "
+          f"solve rel {np.linalg.norm(res[0][1] - x1) / np.linalg.norm(x1):.1e}")
+
+
+def test_virtual_ranks_match_oracle(hb):
+    cfg = inputs.scaled(inputs.CONFIGS["cfg3"], 1 << 14)
+    x = inputs.points(cfg); y = inputs.rhs(cfg)
+    o = OracleHODLR(x, cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, 1e-12).factor()
+    ld_o = o.logdet(); x_o = o.solve(y)
+    for ld, xs, ll, _ in sharded(hb, 4, x, y, cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, 1e-12):
+        assert abs(ld - ld_o) <= 1e-9 * abs(ld_o)
+        assert np.linalg.norm(xs - x_o) <= 1e-9 * np.linalg.norm(x_o)
+
+
+def test_sharded_errors(hb):
+    from paper_1403_6015_b200.dist import run_virtual_ranks
+    xd = torch.linspace(0, 1, 256, dtype=torch.float64, device="cuda")
+
+    def fn(r, d):
+        try:
+            hb.HODLR(xd, 0, (1.0, 0.1), 1e-2, 64, 1e-12, dist=d)     # kappa = 2 < log2(8)
+        except hb.HodlrError as e:
+            return e.status
+        return "OK"
+    assert run_virtual_ranks(8, fn) == ["EINVAL"] * 8
+
+
+def test_loglik_sweep_matches_single_settings(hb):
+    """Config 4 shape: several (ell, sigma2) settings through gp_loglik_sweep (concurrent workers, and 4
+    virtual ranks splitting the settings) equal the one-setting path and the oracle."""
+    from paper_1403_6015_b200.dist import run_virtual_ranks
+    cfg = inputs.CONFIGS["cfg4"]
+    ell, s2 = inputs.sweep_settings(cfg)
+    c = inputs.scaled(cfg, 1 << 13)
+    x = inputs.points(c); y = inputs.rhs(c)
+    ks = [0, 5, 17, 40, 63]
+    th = np.array([[cfg.a, ell[k]] for k in ks]); sg = np.array([s2[k] for k in ks])
+    xd = torch.from_numpy(x).cuda(); yd = torch.from_numpy(y).cuda()
+    vals = hb.gp_loglik_sweep(xd, yd, cfg.kernel, th, sg, cfg.leaf, 1e-12, workers=3)
+    for j, k in enumerate(ks):
+        one = hb.HODLR(xd, cfg.kernel, (cfg.a, ell[k]), s2[k], cfg.leaf, 1e-12).factor().gp_loglik(yd)
+        assert vals[j] == one
+        o = OracleHODLR(x, cfg.kernel, (cfg.a, ell[k]), s2[k], cfg.leaf, 1e-12).factor()
+        assert abs(vals[j] - o.gp_loglik(y)) <= 1e-9 * abs(o.gp_loglik(y)) + 1e-9 * abs(o.logdet())
+    res = run_virtual_ranks(4, lambda r, d: hb.gp_loglik_sweep(xd, yd, cfg.kernel, th, sg, cfg.leaf, 1e-12, dist=d))
+    for v in res:
+        np.testing.assert_array_equal(v, vals)
