@@ -175,6 +175,55 @@ __host__ __device__ __forceinline__ long long tree_smem_doubles(int q, int ldk) 
   return 3LL * q * q + 6LL * q + 4LL * q * ldk;
 }
 
+// Gauss-Jordan with partial pivoting on [S | I] (q <= QB rows, one row per lane, in registers): row swaps and
+// the pivot-row broadcast by shuffles, no shared-memory traffic or barriers.  Same pivots (row of max |.|,
+// first index on ties, explicit swaps) and U_kk as the LU of the coupling system.  On exit lane a < q writes
+// row a of S^{-1} to W[a][q..2q), lane 0 writes |U_kk| to ukk[k]; returns sign and zero-pivot flag.
+template <int QB>
+__device__ void gj_regs(double *W, int q, double *ukk, int &sign, int &zero) {
+  const int lane = threadIdx.x & 31, q2 = 2 * q;
+  double w[2 * QB];
+#pragma unroll
+  for (int j = 0; j < QB; j++) {
+    w[j] = (lane < q && j < q) ? W[lane * q2 + j] : 0.0;
+    w[QB + j] = (lane < q && j < q) ? W[lane * q2 + q + j] : 0.0;
+  }
+  sign = 1; zero = 0;
+#pragma unroll
+  for (int k = 0; k < QB; k++) {
+    if (k < q) {                                   // (warp-uniform; keeps the loop fully unrolled)
+      double best = (lane >= k && lane < q) ? fabs(w[k]) : -1.0;
+      int p = lane;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double b2 = __shfl_xor_sync(0xffffffffu, best, o); const int p2 = __shfl_xor_sync(0xffffffffu, p, o);
+        if (b2 > best || (b2 == best && p2 < p)) { best = b2; p = p2; }
+      }
+      if (p != k) {                                // swap rows k and p
+        sign = -sign;
+        const int src = lane == k ? p : (lane == p ? k : lane);
+#pragma unroll
+        for (int j = 0; j < 2 * QB; j++) w[j] = __shfl_sync(0xffffffffu, w[j], src);
+      }
+      const double piv = __shfl_sync(0xffffffffu, w[k], k);
+      if (piv < 0.0) sign = -sign;
+      if (!(piv != 0.0)) zero = 1;
+      if (lane == 0) ukk[k] = fabs(piv);
+      const double ip = piv != 0.0 ? 1.0 / piv : 0.0;
+      const double mlt = lane == k ? 0.0 : w[k] * ip;
+#pragma unroll
+      for (int j = 0; j < 2 * QB; j++) {
+        const double prj = __shfl_sync(0xffffffffu, w[j], k);
+        w[j] = lane == k ? w[j] * ip : fma(-mlt, prj, w[j]);
+      }
+    }
+  }
+  if (lane < q) {
+#pragma unroll
+    for (int j = 0; j < QB; j++) if (j < q) W[lane * q2 + q + j] = w[QB + j];
+  }
+}
+
 // One CTA per depth-d node c (heap index (2^d - 1) + i):
 //   S_c = [[I, Pi_c2[s,s]], [Pi_c1[s,s], I]]; Gauss-Jordan with partial pivoting (row of max |.|, first
 //   index on ties -- the same pivots and U_kk as the LU of the paper's coupling system) gives log|det S_c|,
@@ -220,34 +269,37 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm) {
   }
   __syncthreads();
   // ---------------- Gauss-Jordan with partial pivoting ----------------
-  // q <= 16: warp 0 alone (no CTA barriers); larger systems: the whole CTA, 3 barriers per step.
-  const bool warp_gj = q <= 16;
-  if (!warp_gj || t < 32) {
-    const int lane = t & 31;
-    const int nthr = warp_gj ? 32 : NT;
+  // q <= 8: warp 0 in registers (gj_regs); larger systems: the whole CTA, 3 barriers per step.
+  if (q <= 8) {
+    if (t < 32) {
+      int sign, zero;
+      gj_regs<8>(W, q, colk, sign, zero);
+      if (t == 0) { s_sign = sign; s_zero = zero; }
+    }
+  } else {
     int sign = 1, zero = 0;
     for (int k = 0; k < q; k++) {
       int p = k; double best = -1.0;
       if (t < 32) {
-        for (int a = k + lane; a < q; a += 32) { const double v = fabs(W[a * q2 + k]); if (v > best) { best = v; p = a; } }
+        for (int a = k + t; a < q; a += 32) { const double v = fabs(W[a * q2 + k]); if (v > best) { best = v; p = a; } }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {   // xor butterfly: every lane ends with the same (best, p)
           const double b2 = __shfl_xor_sync(0xffffffffu, best, o); const int p2 = __shfl_xor_sync(0xffffffffu, p, o);
           if (b2 > best || (b2 == best && p2 < p)) { best = b2; p = p2; }
         }
-        if (lane == 0) { colk[k] = best; s_p = p; }           // |U_kk| (log det below)
+        if (t == 0) { colk[k] = best; s_p = p; }            // |U_kk| (log det below)
       }
-      if (warp_gj) __syncwarp(); else __syncthreads();
+      __syncthreads();
       p = s_p;
       const double piv = W[p * q2 + k];
       if (p != k) sign = -sign;
       if (piv < 0.0) sign = -sign;
       if (!(piv != 0.0)) zero = 1;
-      for (int j = t; j < q2; j += nthr) { rowk[j] = W[p * q2 + j]; rowold[j] = W[k * q2 + j]; }
-      for (int a = t; a < q; a += nthr) mult[a] = a == k ? 0.0 : (a == p ? W[k * q2 + k] : W[a * q2 + k]);
-      if (warp_gj) __syncwarp(); else __syncthreads();
+      for (int j = t; j < q2; j += NT) { rowk[j] = W[p * q2 + j]; rowold[j] = W[k * q2 + j]; }
+      for (int a = t; a < q; a += NT) mult[a] = a == k ? 0.0 : (a == p ? W[k * q2 + k] : W[a * q2 + k]);
+      __syncthreads();
       const double ip = piv != 0.0 ? 1.0 / piv : 0.0;
-      for (int e = t; e < q * q2; e += nthr) {
+      for (int e = t; e < q * q2; e += NT) {
         const int a = e / q2, j = e - a * q2;
         if (a == k) W[e] = rowk[j] * ip;
         else {
@@ -255,7 +307,7 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm) {
           W[e] = fma(-mult[a] * ip, rowk[j], src);
         }
       }
-      if (warp_gj) __syncwarp(); else __syncthreads();
+      __syncthreads();
     }
     if (t == 0) { s_sign = sign; s_zero = zero; }
   }

@@ -158,6 +158,8 @@ struct hodlr_s {
   // solve workspace
   double *Vpool, *Tvec, *hvec;
   double *xshard;            // sharded solve: sorted solution rows + allgather send/recv slices
+  unsigned long long *stamps;  // HODLR_TRACE phase timestamps
+  int bulk_ok, bulk_checked;   // solve leaf staging by bulk copies
   // bookkeeping
   long long bytes;
   double t_build, t_factor, t_logdet, t_solve;

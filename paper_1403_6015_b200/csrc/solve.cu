@@ -1,25 +1,36 @@
 // solve.cu -- G11/G12: x = C^{-1} y by applying the inverse factors (eq-fac)
 // in projected form:
-//   up   (leaves)  w_l = A_l^{-1} b_l,  g_l = E_l^T w_l,  h_l = b_l . w_l            (k_leaf_up)
+//   up   (leaves)  v_l = A_l^{-1} b_l,  g_l = E_l^T v_l,  h_l = b_l . v_l
 //   up   (node c)  t_c = S_c^{-1} [g_c2[s]; g_c1[s]]
 //                  g_c = g_c1[a] + g_c2[a] - B_c[r:]^T t_c[:r] - B_c[:r]^T t_c[r:]
-//                  h_c = h_c1 + h_c2 - g_c1[s] . t_c[:r] - g_c2[s] . t_c[r:]          (k_tree_up)
-//   down (node c)  f = t_c + T_c w_c;  w_c1 = [w_c, -f[:r]],  w_c2 = [w_c, -f[r:]]   (k_tree_down)
-//   down (leaves)  x_l = A_l^{-1} (b_l + E_l w_l)                                   (k_leaf_down)
+//                  h_c = h_c1 + h_c2 - g_c1[s] . t_c[:r] - g_c2[s] . t_c[r:]
+//   down (node c)  f = t_c + T_c w_c;  w_c1 = [w_c, -f[:r]],  w_c2 = [w_c, -f[r:]]
+//   down (leaves)  x_l = A_l^{-1} (b_l + E_l w_l)
 // h_root = y^T C^{-1} y gives the log-likelihood without the down pass (eq. 1).
-// Leaf passes use the stored X = L^{-1} (one CTA per leaf, two triangular matrix-vector products);
-// tree passes one warp per node (t_c by S_c^{-1} + 2 compensated refinement steps).
+//
+// One persistent cooperative kernel (one 512-thread CTA per SM) runs the phases separated by grid barriers:
+// leaf up -> tree up, level by level -> tree down, level by level -> leaf down.  Leaf phases use the stored
+// X = L^{-1} (two triangular matrix-vector products) and stage X and the ancestor panel E_l in shared memory
+// with cp.async, prefetching the next leaf's X while E is used and its E while X is used.  Tree nodes: one
+// warp each (t_c by S_c^{-1} + 2 compensated refinement steps; compensated accumulations).
+// Under subtree sharding the kernel is split at the exchange of the depth-t projections.
 #include "hodlr_internal.cuh"
+#include <cooperative_groups.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+namespace cg = cooperative_groups;
 
 namespace {
 
-constexpr int ST = 256;          // threads per CTA (8 warps)
-constexpr int NWS = ST / 32;
-
+constexpr int LT = 512;           // threads per CTA
+constexpr int NWL = LT / 32;      // warps per CTA
+constexpr int VMAX = 8 * 32;      // leaf rows handled (leaf_max < 2 leaf <= 256)
 
 struct SolveCtx {
   long long n, ninternal, nleaves;
   int kappa, K, T;
+  int grank, tsplit;
   const long long *lo, *hi, *perm;
   const double *Xh;
   const int *rank;
@@ -33,51 +44,57 @@ struct SolveCtx {
   double *x;
   double *xsorted;  // sharded solve: this rank's solution rows in sorted order (NULL on one GPU)
   int *flags;
-  long long leaf0;  // first leaf of this rank
+  long long leaf0, nown;    // this rank's leaves
+  long long tree_scratch;   // doubles of per-warp scratch for the tree-up nodes
+  int tree_warps;           // warps per CTA that take tree-up nodes (scratch must fit)
+  unsigned long long *stamps;   // HODLR_TRACE: %globaltimer after each phase (block 0), or NULL
+  int bulk;                 // leaf staging by bulk copies (all column segments 16-byte aligned)
 };
 
-// ---------------------------------------------------------------------------------------------
-// Leaf passes: one CTA (256 threads) per leaf; X = L^{-1} (fragment-order lower tiles) staged in shared
-// memory with 16-byte cp.async when it fits (T <= 16), read from global otherwise.
-//   u = X b   (row i: sum_{j <= i} X_ij b_j)        v = X^T u   (column j: sum_{i >= j} X_ij u_i)
-// so v = A_l^{-1} b with two parallel triangular matrix-vector products.
-// ---------------------------------------------------------------------------------------------
-
-// out = X in (lower) for rows < R = 8T; 2 threads per row (interleaved tile columns), partials in red[].
-__device__ void tri_mv(const double *X, int T, const double *in, double *out, double *red) {
-  const int t = threadIdx.x, R = 8 * T, NT = blockDim.x;
-  for (int w = t; w < 2 * R; w += NT) {
-    const int i = w % R, h = w / R, I = i >> 3, r = i & 7;
-    double s = 0.0;
-    for (int k = h; k <= I; k += 2) {
-      const double *tl = X + tix(I, k) * 64;
-#pragma unroll
-      for (int cc = 0; cc < 8; cc++) s = fma(tl[fo(r, cc)], in[8 * k + cc], s);
-    }
-    red[w] = s;
-  }
-  __syncthreads();
-  for (int i = t; i < R; i += NT) out[i] = red[i] + red[R + i];
-  __syncthreads();
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t;
 }
 
-// out = X^T in for columns < R.
-__device__ void tri_mvt(const double *X, int T, const double *in, double *out, double *red) {
-  const int t = threadIdx.x, R = 8 * T, NT = blockDim.x;
-  for (int w = t; w < 2 * R; w += NT) {
-    const int j = w % R, h = w / R, J = j >> 3, cc = j & 7;
-    double s = 0.0;
-    for (int I = J + h; I < T; I += 2) {
-      const double *tl = X + tix(I, J) * 64;
-#pragma unroll
-      for (int r = 0; r < 8; r++) s = fma(tl[fo(r, cc)], in[8 * I + r], s);
-    }
-    red[w] = s;
-  }
-  __syncthreads();
-  for (int j = t; j < R; j += NT) out[j] = red[j] + red[R + j];
-  __syncthreads();
+struct Phases {
+  int leaf_up;      // run the leaf up pass
+  int up_hi, up_lo; // tree up levels d = up_hi down to up_lo (none if up_hi < up_lo)
+  int down;         // run the tree down levels and the leaf down pass
+};
+
+__device__ __forceinline__ void own_range(const SolveCtx &c, int d, long long &i0, long long &cnt) {
+  if (d < c.tsplit) { i0 = 0; cnt = 1LL << d; }
+  else { cnt = 1LL << (d - c.tsplit); i0 = (long long)c.grank * cnt; }
 }
+
+__device__ __forceinline__ void cp16(double *dst, const double *src) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(sa), "l"(src));
+}
+__device__ __forceinline__ void cp8(double *dst, const double *src) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" :: "r"(sa), "l"(src));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N> __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" :: "n"(N)); }
+
+// Bulk asynchronous copies (TMA engine, no tensor map) completing on an mbarrier
+__device__ __forceinline__ unsigned sptr(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long *bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" :: "r"(sptr(bar)));
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect(unsigned long long *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" :: "r"(sptr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               :: "r"(sptr(dst)), "l"(src), "r"(bytes), "r"(sptr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned phase) {
+  asm volatile("{\n .reg .pred p;\n W%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W%=;\n}\n"
+               :: "r"(sptr(bar)), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void fence_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
 __device__ __forceinline__ int leaf_colsrc(const SolveCtx &c, long long id, int q) {
   if (q >= c.K) return -1;
@@ -88,150 +105,260 @@ __device__ __forceinline__ int leaf_colsrc(const SolveCtx &c, long long id, int 
   return qq < c.rank[b] ? (int)(c.dt->colbase[e] + qq) : -1;
 }
 
-constexpr int VMAX = 8 * 32;      // leaf rows handled (leaf_max < 2 leaf <= 256)
-constexpr int LT = 512;           // threads per leaf CTA
-
-__device__ __forceinline__ void cp16(double *dst, const double *src) {
-  unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(sa), "l"(src));
-}
-__device__ __forceinline__ void cp8(double *dst, const double *src) {
-  unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" :: "r"(sa), "l"(src));
-}
-
-// Stage X = L^{-1} (tiles) and the ancestor panel E_l (K columns x R rows, column-major, zero beyond each
-// block's rank) of one leaf into shared memory with cp.async; all bytes of the leaf in flight at once.
-__device__ void stage_leaf(const SolveCtx &c, long long leaf, long long id, long long lo, int m, int R,
-                           const int *colsrc, double *sX, double *sE) {
-  const int t = threadIdx.x, NT = blockDim.x;
+// ---------------------------------------------------------------------------------------------
+// leaf staging: X = L^{-1} tiles, and the panel E_l (K columns x R rows, column-major, zero beyond each
+// ancestor block's rank); one commit group each
+// ---------------------------------------------------------------------------------------------
+__device__ void issue_x(const SolveCtx &c, long long leaf, double *sX) {
   const double *Xg = c.Lf + leaf * c.lstride;
   const int nx2 = (c.T * (c.T + 1) / 2) * 32;
-  for (int p = t; p < nx2; p += NT) cp16(sX + 2 * p, Xg + 2 * p);
-  const bool al16 = ((c.n | lo) & 1) == 0;
-  if (al16) {
-    const int R2 = R / 2;
-    for (int p = t; p < c.K * R2; p += NT) {
-      const int q = p / R2, i = 2 * (p - q * R2);
+  for (int p = threadIdx.x; p < nx2; p += LT) cp16(sX + 2 * p, Xg + 2 * p);
+  cp_commit();
+}
+
+__device__ void issue_e(const SolveCtx &c, long long leaf, const int *colsrc, double *sE) {
+  const long long id = c.ninternal + leaf, lo = c.lo[id];
+  const int m = (int)(c.hi[id] - lo), R = 8 * c.T;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (((c.n | lo) & 1) == 0) {               // warp per column, lanes over 16-byte row pairs
+    for (int q = warp; q < c.K; q += NWL) {
       const int src = colsrc[q];
-      double *dst = sE + q * R + i;
-      if (src >= 0 && i + 1 < m) cp16(dst, c.Xh + (long long)src * c.n + lo + i);
-      else { dst[0] = (src >= 0 && i < m) ? c.Xh[(long long)src * c.n + lo + i] : 0.0; dst[1] = 0.0; }
+      const double *g = c.Xh + (long long)src * c.n + lo;
+      double *dst = sE + q * R;
+      for (int i = 2 * lane; i < R; i += 64) {
+        if (src >= 0 && i + 1 < m) cp16(dst + i, g + i);
+        else { dst[i] = (src >= 0 && i < m) ? g[i] : 0.0; dst[i + 1] = 0.0; }
+      }
     }
   } else {
-    for (int p = t; p < c.K * R; p += NT) {
-      const int q = p / R, i = p - q * R;
+    for (int q = warp; q < c.K; q += NWL) {
       const int src = colsrc[q];
-      double *dst = sE + q * R + i;
-      if (src >= 0 && i < m) cp8(dst, c.Xh + (long long)src * c.n + lo + i); else *dst = 0.0;
+      const double *g = c.Xh + (long long)src * c.n + lo;
+      double *dst = sE + q * R;
+      for (int i = lane; i < R; i += 32) { if (src >= 0 && i < m) cp8(dst + i, g + i); else dst[i] = 0.0; }
     }
   }
-  asm volatile("cp.async.commit_group;\n" ::);
+  cp_commit();
 }
 
-// up: v = A_l^{-1} b, g_l = E_l^T v, h_l = b . v
-__global__ void __launch_bounds__(LT, 1) k_leaf_up(SolveCtx c) {
-  extern __shared__ double sm[];
-  __shared__ double sb[VMAX], su[VMAX], red[2 * VMAX];
-  __shared__ int colsrc[1024];
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, NW = LT / 32;
-  const long long leaf = c.leaf0 + blockIdx.x;
+// Bulk variants (every leaf start, leaf size and n even: 16-byte aligned column segments).  Warp 0 issues;
+// the previous readers of the buffer must have passed a barrier.
+__device__ void bulk_x(const SolveCtx &c, long long leaf, double *sX, unsigned long long *bar) {
+  if (threadIdx.x == 0) {
+    const unsigned bytes = (unsigned)((c.T * (c.T + 1) / 2) * 64 * sizeof(double));
+    fence_async();
+    mbar_expect(bar, bytes);
+    bulk_g2s(sX, c.Lf + leaf * c.lstride, bytes, bar);
+  }
+}
+
+__device__ void bulk_e(const SolveCtx &c, long long leaf, const int *colsrc, double *sE, unsigned long long *bar) {
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
   const long long id = c.ninternal + leaf, lo = c.lo[id];
-  const int m = (int)(c.hi[id] - lo), R = 8 * c.T, K = c.K;
-  double *sX = sm, *sE = sm + 64 * (c.T * (c.T + 1) / 2);
-  for (int q = t; q < K; q += LT) colsrc[q] = leaf_colsrc(c, id, q);
-  bool bad = false;
-  for (int i = t; i < R; i += LT) {
-    const double v = i < m ? c.y[c.perm[lo + i]] : 0.0;
-    if (!isfinite(v)) bad = true;
-    sb[i] = v;
-  }
-  if (bad) atomicOr(&c.flags[3], 1);
-  __syncthreads();
-  stage_leaf(c, leaf, id, lo, m, R, colsrc, sX, sE);
-  asm volatile("cp.async.wait_group 0;\n" ::);
-  __syncthreads();
-  tri_mv(sX, c.T, sb, su, red);           // u = X b
-  tri_mvt(sX, c.T, su, su, red);          // v = X^T u  (in place: tri_mvt reads su fully before its barrier)
-  double hs = 0.0;
-  for (int i = t; i < m; i += LT) hs += sb[i] * su[i];
-  hs = warp_sum(hs);
-  if (lane == 0) red[warp] = hs;
-  double *g = c.V + c.dt->nodeV[c.kappa] + leaf * (long long)K;
-  for (int q = warp; q < K; q += NW) {    // g = E^T v: warp per column, lanes over rows
-    const double *e = sE + q * R;
-    double s2 = 0.0;
-    for (int i = lane; i < R; i += 32) s2 = fma(e[i], su[i], s2);
-    s2 = warp_sum(s2);
-    if (lane == 0) g[q] = s2;
-  }
-  __syncthreads();
-  if (t == 0) {
-    double h = 0.0;
-    for (int w = 0; w < NW; w++) h += red[w];
-    c.hv[2 * id] = h; c.hv[2 * id + 1] = 0.0;
+  const int m = (int)(c.hi[id] - lo), R = 8 * c.T;
+  int nvalid = 0;
+  for (int q0 = 0; q0 < c.K; q0 += 32) nvalid += __popc(__ballot_sync(0xffffffffu, q0 + lane < c.K && colsrc[q0 + lane] >= 0));
+  if (lane == 0) { fence_async(); mbar_expect(bar, (unsigned)(nvalid * m * sizeof(double))); }
+  __syncwarp();
+  for (int q = lane; q < c.K; q += 32) {
+    const int src = colsrc[q];
+    if (src >= 0) bulk_g2s(sE + q * R, c.Xh + (long long)src * c.n + lo, (unsigned)(m * sizeof(double)), bar);
   }
 }
 
-// down: x_l = A_l^{-1} (b_l + E_l w_l)
-__global__ void __launch_bounds__(LT, 1) k_leaf_down(SolveCtx c) {
-  extern __shared__ double sm[];
-  __shared__ double sb[VMAX], su[VMAX], red[2 * VMAX];
-  __shared__ int colsrc[1024];
-  __shared__ double sw[1024];
-  __shared__ double part4[4 * VMAX];
+// zero the padding of E (rows m..R of valid columns, whole columns beyond the ranks): generic stores
+__device__ void zero_e_pad(const SolveCtx &c, long long leaf, const int *colsrc, double *sE) {
+  const long long id = c.ninternal + leaf;
+  const int m = (int)(c.hi[id] - c.lo[id]), R = 8 * c.T;
+  for (int p = threadIdx.x; p < c.K * R; p += LT) {
+    const int q = p / R, i = p - q * R;
+    if (colsrc[q] < 0 || i >= m) sE[p] = 0.0;
+  }
+}
+
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+// out = X in (lower) on the FP64 tensor pipe: warp I owns tile row I, C(I) = sum_{k <= I} X(I,k) B_k with B_k the
+// 8-vector in_k replicated over the 8 columns (A fragments straight from the fragment-order tiles:
+// conflict-free).  Two accumulators alternate over k.
+__device__ void tri_mv(const double *X, int T, const double *in, double *out, double *) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, tq = lane & 3;
+  for (int I = warp; I < T; I += NWL) {
+    double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+    int k = 0;
+    for (; k + 1 <= I; k += 2) {
+      const double *t0 = X + tix(I, k) * 64, *t1 = X + tix(I, k + 1) * 64;
+      dmma(c0, c1, t0[lane], in[8 * k + tq]);
+      dmma(e0, e1, t1[lane], in[8 * k + 8 + tq]);
+      dmma(c0, c1, t0[32 + lane], in[8 * k + 4 + tq]);
+      dmma(e0, e1, t1[32 + lane], in[8 * k + 12 + tq]);
+    }
+    if (k <= I) {
+      const double *t0 = X + tix(I, k) * 64;
+      dmma(c0, c1, t0[lane], in[8 * k + tq]);
+      dmma(c0, c1, t0[32 + lane], in[8 * k + 4 + tq]);
+    }
+    if (tq == 0) out[8 * I + g] = c0 + e0;
+  }
+  __syncthreads();
+}
+
+// out = X^T in: warp J owns tile column J, C(J) = sum_{I >= J} X(I,J)^T B_I; the A fragment of X(I,J)^T
+// (row g, column tq) is tile element (tq, g) at fo(tq, g) (2 wavefronts per half, the minimum for 64-bit).
+__device__ void tri_mvt(const double *X, int T, const double *in, double *out, double *) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, tq = lane & 3;
+  const int a0 = fo(tq, g), a1 = fo(tq + 4, g);
+  for (int J = warp; J < T; J += NWL) {
+    double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+    int I = J;
+    for (; I + 1 < T; I += 2) {
+      const double *t0 = X + tix(I, J) * 64, *t1 = X + tix(I + 1, J) * 64;
+      dmma(c0, c1, t0[a0], in[8 * I + tq]);
+      dmma(e0, e1, t1[a0], in[8 * I + 8 + tq]);
+      dmma(c0, c1, t0[a1], in[8 * I + 4 + tq]);
+      dmma(e0, e1, t1[a1], in[8 * I + 12 + tq]);
+    }
+    if (I < T) {
+      const double *t0 = X + tix(I, J) * 64;
+      dmma(c0, c1, t0[a0], in[8 * I + tq]);
+      dmma(c0, c1, t0[a1], in[8 * I + 4 + tq]);
+    }
+    __syncwarp();
+    if (tq == 0) out[8 * J + g] = c0 + e0;
+  }
+  __syncthreads();
+}
+
+struct LeafSmem {
+  double sb[VMAX], su[VMAX], red[4 * VMAX], sw[1024];
+  int colsrc[2][1024];
+  unsigned long long barX, barE;
+};
+
+// ---------------------------------------------------------------------------------------------
+// leaf up over this CTA's leaves (leaf0 + blockIdx.x + k gridDim.x), X and E issued ahead:
+//   wait X_i -> u = X b, v = X^T u -> issue X_{i+1} -> wait E_i -> g = E^T v, h -> issue E_{i+1}
+// BULK: bulk copies (TMA engine) completing on mbarriers; otherwise per-thread cp.async groups.
+// ---------------------------------------------------------------------------------------------
+template <bool BULK>
+__device__ void leaf_up_phase(const SolveCtx &c, double *sX, double *sE, LeafSmem &S, unsigned &phX, unsigned &phE) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int R = 8 * c.T, K = c.K;
+  long long leaf = c.leaf0 + blockIdx.x;
+  const long long end = c.leaf0 + c.nown;
+  if (leaf >= end) return;
+  int cur = 0;
+  for (int q = t; q < K; q += LT) S.colsrc[0][q] = leaf_colsrc(c, c.ninternal + leaf, q);
+  __syncthreads();
+  if (BULK) { zero_e_pad(c, leaf, S.colsrc[0], sE); bulk_x(c, leaf, sX, &S.barX); bulk_e(c, leaf, S.colsrc[0], sE, &S.barE); }
+  else { issue_x(c, leaf, sX); issue_e(c, leaf, S.colsrc[0], sE); }
+  for (; leaf < end; leaf += gridDim.x) {
+    const long long nxt = leaf + gridDim.x;
+    const long long id = c.ninternal + leaf, lo = c.lo[id];
+    const int m = (int)(c.hi[id] - lo);
+    bool bad = false;
+    for (int i = t; i < R; i += LT) {
+      const double v = i < m ? c.y[c.perm[lo + i]] : 0.0;
+      if (!isfinite(v)) bad = true;
+      S.sb[i] = v;
+    }
+    if (bad) atomicOr(&c.flags[3], 1);
+    if (nxt < end) for (int q = t; q < K; q += LT) S.colsrc[cur ^ 1][q] = leaf_colsrc(c, c.ninternal + nxt, q);
+    if (BULK) { mbar_wait(&S.barX, phX); phX ^= 1; } else cp_wait<1>();     // X_i
+    __syncthreads();
+    tri_mv(sX, c.T, S.sb, S.su, S.red);        // u = X b
+    tri_mvt(sX, c.T, S.su, S.red, nullptr);    // v = X^T u  (into red[0..R))
+    if (nxt < end) { if (BULK) bulk_x(c, nxt, sX, &S.barX); else issue_x(c, nxt, sX); }   // X is free
+    else if (!BULK) cp_commit();               // keep the group count uniform
+    double hs = 0.0;
+    for (int i = t; i < m; i += LT) hs += S.sb[i] * S.red[i];
+    hs = warp_sum(hs);
+    if (BULK) { mbar_wait(&S.barE, phE); phE ^= 1; } else cp_wait<1>();     // E_i
+    __syncthreads();
+    if (lane == 0) S.red[2 * VMAX + warp] = hs;
+    double *g = c.V + c.dt->nodeV[c.kappa] + leaf * (long long)K;
+    for (int q = warp; q < K; q += NWL) {      // g = E^T v: warp per column, lanes over rows
+      const double *e = sE + q * R;
+      double s2 = 0.0;
+      for (int i = lane; i < R; i += 32) s2 = fma(e[i], S.red[i], s2);
+      s2 = warp_sum(s2);
+      if (lane == 0) g[q] = s2;
+    }
+    __syncthreads();
+    if (t == 0) {
+      double h = 0.0;
+      for (int w = 0; w < NWL; w++) h += S.red[2 * VMAX + w];
+      c.hv[2 * id] = h; c.hv[2 * id + 1] = 0.0;
+    }
+    if (nxt < end) {
+      if (BULK) { zero_e_pad(c, nxt, S.colsrc[cur ^ 1], sE); bulk_e(c, nxt, S.colsrc[cur ^ 1], sE, &S.barE); }
+      else issue_e(c, nxt, S.colsrc[cur ^ 1], sE);
+    } else if (!BULK) cp_commit();
+    cur ^= 1;
+  }
+  if (!BULK) cp_wait<0>();
+  __syncthreads();
+}
+
+// leaf down: x_l = A_l^{-1} (b_l + E_l w_l):  wait E_i -> b + E w -> issue E_{i+1} -> wait X_i -> u, x -> issue X_{i+1}
+template <bool BULK>
+__device__ void leaf_down_phase(const SolveCtx &c, double *sX, double *sE, LeafSmem &S, unsigned &phX, unsigned &phE) {
   const int t = threadIdx.x;
-  const long long leaf = c.leaf0 + blockIdx.x;
-  const long long id = c.ninternal + leaf, lo = c.lo[id];
-  const int m = (int)(c.hi[id] - lo), R = 8 * c.T, K = c.K;
-  double *sX = sm, *sE = sm + 64 * (c.T * (c.T + 1) / 2);
-  const double *w = c.V + c.dt->nodeV[c.kappa] + leaf * (long long)K;
-  for (int q = t; q < K; q += LT) { colsrc[q] = leaf_colsrc(c, id, q); sw[q] = w[q]; }
+  const int R = 8 * c.T, K = c.K;
+  long long leaf = c.leaf0 + blockIdx.x;
+  const long long end = c.leaf0 + c.nown;
+  if (leaf >= end) return;
+  int cur = 0;
+  for (int q = t; q < K; q += LT) S.colsrc[0][q] = leaf_colsrc(c, c.ninternal + leaf, q);
   __syncthreads();
-  stage_leaf(c, leaf, id, lo, m, R, colsrc, sX, sE);
-  for (int i = t; i < R; i += LT) sb[i] = i < m ? c.y[c.perm[lo + i]] : 0.0;
-  asm volatile("cp.async.wait_group 0;\n" ::);
-  __syncthreads();
-  // b + E w: 4 threads per row (quarters of the columns), partials combined in a fixed order
-  for (int w4 = t; w4 < 4 * R; w4 += LT) {
-    const int i = w4 % R, h = w4 / R;
-    const int q0 = (K * h) / 4, q1 = (K * (h + 1)) / 4;
-    double s2 = 0.0;
-    for (int q = q0; q < q1; q++) s2 = fma(sE[q * R + i], sw[q], s2);
-    part4[w4] = s2;
+  if (BULK) { zero_e_pad(c, leaf, S.colsrc[0], sE); bulk_e(c, leaf, S.colsrc[0], sE, &S.barE); bulk_x(c, leaf, sX, &S.barX); }
+  else { issue_e(c, leaf, S.colsrc[0], sE); issue_x(c, leaf, sX); }
+  for (; leaf < end; leaf += gridDim.x) {
+    const long long nxt = leaf + gridDim.x;
+    const long long id = c.ninternal + leaf, lo = c.lo[id];
+    const int m = (int)(c.hi[id] - lo);
+    const double *w = c.V + c.dt->nodeV[c.kappa] + leaf * (long long)K;
+    for (int q = t; q < K; q += LT) S.sw[q] = w[q];
+    for (int i = t; i < R; i += LT) S.sb[i] = i < m ? c.y[c.perm[lo + i]] : 0.0;
+    if (nxt < end) for (int q = t; q < K; q += LT) S.colsrc[cur ^ 1][q] = leaf_colsrc(c, c.ninternal + nxt, q);
+    if (BULK) { mbar_wait(&S.barE, phE); phE ^= 1; } else cp_wait<1>();     // E_i
+    __syncthreads();
+    for (int w4 = t; w4 < 4 * R; w4 += LT) {   // b + E w: 4 threads per row (quarters of the columns)
+      const int i = w4 % R, h = w4 / R;
+      const int q0 = (K * h) / 4, q1 = (K * (h + 1)) / 4;
+      double s2 = 0.0;
+      for (int q = q0; q < q1; q++) s2 = fma(sE[q * R + i], S.sw[q], s2);
+      S.red[w4] = s2;
+    }
+    __syncthreads();
+    for (int i = t; i < R; i += LT) S.sb[i] += (S.red[i] + S.red[R + i]) + (S.red[2 * R + i] + S.red[3 * R + i]);
+    if (nxt < end) {                           // E is free (barrier above)
+      if (BULK) { zero_e_pad(c, nxt, S.colsrc[cur ^ 1], sE); bulk_e(c, nxt, S.colsrc[cur ^ 1], sE, &S.barE); }
+      else issue_e(c, nxt, S.colsrc[cur ^ 1], sE);
+    } else if (!BULK) cp_commit();
+    if (BULK) { mbar_wait(&S.barX, phX); phX ^= 1; } else cp_wait<1>();     // X_i
+    __syncthreads();
+    tri_mv(sX, c.T, S.sb, S.su, S.red);
+    tri_mvt(sX, c.T, S.su, S.sb, S.red);
+    if (nxt < end) { if (BULK) bulk_x(c, nxt, sX, &S.barX); else issue_x(c, nxt, sX); }
+    else if (!BULK) cp_commit();
+    if (c.xsorted) for (int i = t; i < m; i += LT) c.xsorted[lo + i] = S.sb[i];
+    else for (int i = t; i < m; i += LT) c.x[c.perm[lo + i]] = S.sb[i];
+    cur ^= 1;
   }
+  if (!BULK) cp_wait<0>();
   __syncthreads();
-  for (int i = t; i < R; i += LT) sb[i] += (part4[i] + part4[R + i]) + (part4[2 * R + i] + part4[3 * R + i]);
-  __syncthreads();
-  tri_mv(sX, c.T, sb, su, red);
-  tri_mvt(sX, c.T, su, sb, red);
-  if (c.xsorted) for (int i = t; i < m; i += LT) c.xsorted[lo + i] = sb[i];
-  else for (int i = t; i < m; i += LT) c.x[c.perm[lo + i]] = sb[i];
-}
-
-// sharded solve: x[perm[row_lo_r + i]] = slice_r[i] for every rank's slice of the gathered solution
-__global__ void k_unshard(const double *gathered, const long long *rowlo, int nranks, long long rows_max, long long n,
-                          const long long *perm, double *x) {
-  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (e >= (long long)nranks * rows_max) return;
-  const int r = (int)(e / rows_max);
-  const long long i = e - (long long)r * rows_max;
-  const long long lo = rowlo[r], hi = r + 1 < nranks ? rowlo[r + 1] : n;
-  if (lo + i < hi) x[perm[lo + i]] = gathered[e];
-}
-
-__global__ void k_pack_rows(const double *xsorted, long long lo, long long m, double *send) {
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i < m) send[i] = xsorted[lo + i];
 }
 
 // ---------------------------------------------------------------------------------------------
-// Tree passes: one warp per node.  Per-warp shared scratch for the short vectors.
+// tree nodes (one warp each)
 // ---------------------------------------------------------------------------------------------
-constexpr int QMAX = 2 * ACA_MAXCAP;
-
 // t = S^{-1} rhs as (th, tl): explicit inverse S^{-1} (from the factor phase) + 2 refinement steps with
-// compensated residuals.  One warp; all vectors in shared memory.
+// compensated residuals.  All vectors in the warp's shared scratch.
 __device__ void dd_solve_warp(const double *S0, const double *Si, int q, const double *rhs, double *th, double *tl,
                               double *tmp, int lane) {
   for (int a = lane; a < q; a += 32) {
@@ -256,21 +383,24 @@ __device__ void dd_solve_warp(const double *S0, const double *Si, int q, const d
   }
 }
 
-__global__ void __launch_bounds__(ST) k_tree_up(SolveCtx c, int d, long long i0, long long cnt) {
-  extern __shared__ double dsm[];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if ((long long)blockIdx.x * NWS + wid >= cnt) return;
-  const long long i = i0 + (long long)blockIdx.x * NWS + wid;
+__device__ void tree_up_node(const SolveCtx &c, int d, long long i, double *scr, int lane) {
   const long long node = (1LL << d) - 1 + i;
   const int r = c.dt->rdep[d + 1], q = 2 * r, Kd = c.dt->Kdim[d], K1 = c.dt->Kdim[d + 1];
   const double *g1 = c.V + c.dt->nodeV[d + 1] + (2 * i) * (long long)K1;
   const double *g2 = g1 + K1;
   const double *Sg = c.Spool + c.dt->nodeS[d] + i * (long long)(2 * q * q + q);
   const double *B = c.BTpool + c.dt->nodeBT[d] + i * 3LL * q * Kd;
-  // per-warp staging: S0, LU, pivots, rhs, th, tl, tmp (global latency stays out of the sequential solves)
-  double *S0 = dsm + (long long)wid * (2 * q * q + 5 * q);
+  double *S0 = scr;
   double *Si = S0 + q * q, *rhs = Si + q * q + q, *th = rhs + q, *tl = th + q, *tmp = tl + q;
-  for (int p = lane; p < 2 * q * q + q; p += 32) S0[p] = Sg[p];
+  {
+    const int np = 2 * q * q + q;
+    int p = lane;
+    for (; p + 96 < np; p += 128) {            // 4 independent loads in flight per lane
+      const double a0 = Sg[p], a1 = Sg[p + 32], a2 = Sg[p + 64], a3 = Sg[p + 96];
+      S0[p] = a0; S0[p + 32] = a1; S0[p + 64] = a2; S0[p + 96] = a3;
+    }
+    for (; p < np; p += 32) S0[p] = Sg[p];
+  }
   for (int u = lane; u < r; u += 32) { rhs[u] = g2[Kd + u]; rhs[r + u] = g1[Kd + u]; }
   __syncwarp();
   dd_solve_warp(S0, Si, q, rhs, th, tl, tmp, lane);
@@ -294,32 +424,154 @@ __global__ void __launch_bounds__(ST) k_tree_up(SolveCtx c, int d, long long i0,
     for (int u = 0; u < r; u++) acc_fma_dd(A, -B[(long long)u * Kd + a], th[r + u], tl[r + u]);
     gc[a] = acc_val(A);
   }
+  __syncwarp();
 }
 
-__global__ void __launch_bounds__(ST) k_tree_down(SolveCtx c, int d, long long i0, long long cnt) {
-  __shared__ double sf[NWS][QMAX];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if ((long long)blockIdx.x * NWS + wid >= cnt) return;
-  const long long i = i0 + (long long)blockIdx.x * NWS + wid;
+// Same as tree_up_node with the whole CTA on one node (levels with few nodes): every thread stages, warp 0
+// solves, all threads form g_c; the arithmetic and its order per output are identical.
+__device__ void tree_up_node_cta(const SolveCtx &c, int d, long long i, double *scr) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const long long node = (1LL << d) - 1 + i;
+  const int r = c.dt->rdep[d + 1], q = 2 * r, Kd = c.dt->Kdim[d], K1 = c.dt->Kdim[d + 1];
+  const double *g1 = c.V + c.dt->nodeV[d + 1] + (2 * i) * (long long)K1;
+  const double *g2 = g1 + K1;
+  const double *Sg = c.Spool + c.dt->nodeS[d] + i * (long long)(2 * q * q + q);
+  const double *B = c.BTpool + c.dt->nodeBT[d] + i * 3LL * q * Kd;
+  double *S0 = scr;
+  double *Si = S0 + q * q, *rhs = Si + q * q + q, *th = rhs + q, *tl = th + q, *tmp = tl + q;
+  for (int p = t; p < 2 * q * q + q; p += LT) S0[p] = Sg[p];
+  for (int u = t; u < r; u += LT) { rhs[u] = g2[Kd + u]; rhs[r + u] = g1[Kd + u]; }
+  __syncthreads();
+  if (warp == 0) {
+    dd_solve_warp(S0, Si, q, rhs, th, tl, tmp, lane);
+    double *tg = c.Tv + c.dt->nodeT[d] + i * 2LL * q;
+    for (int u = lane; u < q; u += 32) { tg[u] = th[u]; tg[q + u] = tl[u]; }
+    if (lane == 0) {
+      Acc2 A = acc2(c.hv[2 * (2 * node + 1)]);
+      acc_add_dd(A, c.hv[2 * (2 * node + 2)], c.hv[2 * (2 * node + 2) + 1]);
+      A.c += c.hv[2 * (2 * node + 1) + 1];
+      for (int u = 0; u < r; u++) acc_fma_dd(A, -g1[Kd + u], th[u], tl[u]);
+      for (int u = 0; u < r; u++) acc_fma_dd(A, -g2[Kd + u], th[r + u], tl[r + u]);
+      acc_dd(A, c.hv[2 * node], c.hv[2 * node + 1]);
+    }
+  }
+  __syncthreads();
+  double *gc = c.V + c.dt->nodeV[d] + i * (long long)Kd;
+  for (int a = t; a < Kd; a += LT) {
+    Acc2 A = acc2(g1[a]);
+    acc_add(A, g2[a]);
+    for (int u = 0; u < r; u++) acc_fma_dd(A, -B[(long long)(r + u) * Kd + a], th[u], tl[u]);
+    for (int u = 0; u < r; u++) acc_fma_dd(A, -B[(long long)u * Kd + a], th[r + u], tl[r + u]);
+    gc[a] = acc_val(A);
+  }
+  __syncthreads();
+}
+
+// f = t_c + T_c w_c with `parts` lanes per row u (interleaved a), partials combined by xor shuffles.
+__device__ void tree_down_node(const SolveCtx &c, int d, long long i, int lane) {
   const int r = c.dt->rdep[d + 1], q = 2 * r, Kd = c.dt->Kdim[d], K1 = c.dt->Kdim[d + 1];
   const double *wc = c.V + c.dt->nodeV[d] + i * (long long)Kd;
   const long long qK = (long long)q * Kd;
   const double *Th = c.BTpool + c.dt->nodeBT[d] + i * 3LL * qK + qK;
   const double *Tl = Th + qK;
   const double *tg = c.Tv + c.dt->nodeT[d] + i * 2LL * q;
-  double *f = sf[wid];
-  for (int u = lane; u < q; u += 32) {
-    Acc2 A = acc2(tg[u]);
-    A.c += tg[q + u];
-#pragma unroll 8
-    for (int a = 0; a < Kd; a++) acc_fma_dd(A, wc[a], Th[(long long)u * Kd + a], Tl[(long long)u * Kd + a]);
-    f[u] = acc_val(A);
-  }
-  __syncwarp();
   double *w1 = c.V + c.dt->nodeV[d + 1] + (2 * i) * (long long)K1;
   double *w2 = w1 + K1;
+  int parts = 1;
+  while (parts * 2 * q <= 32 && parts < 16) parts *= 2;
+  const int part = lane % parts;
+  for (int u0 = 0; u0 < q; u0 += 32 / parts) {
+    const int u = u0 + lane / parts;
+    Acc2 A = acc2(0.0);
+    if (u < q) {
+      if (part == 0) { A = acc2(tg[u]); A.c += tg[q + u]; }
+      const double *thu = Th + (long long)u * Kd, *tlu = Tl + (long long)u * Kd;
+      int a = part;
+      for (; a + 3 * parts < Kd; a += 4 * parts) {      // 4 iterations of loads in flight
+        const double w0 = wc[a], w1v = wc[a + parts], w2v = wc[a + 2 * parts], w3 = wc[a + 3 * parts];
+        const double h0 = thu[a], h1 = thu[a + parts], h2 = thu[a + 2 * parts], h3 = thu[a + 3 * parts];
+        const double l0 = tlu[a], l1 = tlu[a + parts], l2 = tlu[a + 2 * parts], l3 = tlu[a + 3 * parts];
+        acc_fma_dd(A, w0, h0, l0); acc_fma_dd(A, w1v, h1, l1); acc_fma_dd(A, w2v, h2, l2); acc_fma_dd(A, w3, h3, l3);
+      }
+      for (; a < Kd; a += parts) acc_fma_dd(A, wc[a], thu[a], tlu[a]);
+    }
+    for (int o = 1; o < parts; o <<= 1) {
+      const double s2 = __shfl_xor_sync(0xffffffffu, A.s, o), c2 = __shfl_xor_sync(0xffffffffu, A.c, o);
+      acc_add(A, s2); A.c += c2;
+    }
+    if (u < q && part == 0) {
+      const double f = acc_val(A);
+      if (u < r) w1[Kd + u] = -f; else w2[Kd + u - r] = -f;
+    }
+  }
   for (int a = lane; a < Kd; a += 32) { const double v = wc[a]; w1[a] = v; w2[a] = v; }
-  for (int u = lane; u < r; u += 32) { w1[Kd + u] = -f[u]; w2[Kd + u] = -f[r + u]; }
+}
+
+// ---------------------------------------------------------------------------------------------
+// the persistent cooperative kernel
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(LT, 1) k_solve(SolveCtx c0, Phases ph) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double sm[];
+  __shared__ LeafSmem S;
+  __shared__ DepthTab sdt;                     // the per-depth tables, read by every tree node
+  for (int i = threadIdx.x; i < (int)(sizeof(DepthTab) / 8); i += LT) ((long long *)&sdt)[i] = ((const long long *)c0.dt)[i];
+  if (threadIdx.x == 0) { mbar_init(&S.barX); mbar_init(&S.barE); }
+  __syncthreads();
+  SolveCtx c = c0;
+  c.dt = &sdt;
+  unsigned phX = 0, phE = 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double *sX = sm, *sE = sm + 64 * (c.T * (c.T + 1) / 2);
+  const long long gw = (long long)blockIdx.x * NWL + warp, nw = (long long)gridDim.x * NWL;
+  const bool stamp = c.stamps && blockIdx.x == 0 && threadIdx.x == 0;
+  int ns = 0;
+  if (stamp) c.stamps[ns++] = gtimer();
+  if (ph.leaf_up) {
+    if (c.bulk) leaf_up_phase<true>(c, sX, sE, S, phX, phE); else leaf_up_phase<false>(c, sX, sE, S, phX, phE);
+    grid.sync();
+    if (stamp) c.stamps[ns++] = gtimer();
+  }
+  {
+    const long long gwt = (long long)blockIdx.x * c.tree_warps + warp, nwt = (long long)gridDim.x * c.tree_warps;
+    for (int d = ph.up_hi; d >= ph.up_lo; d--) {
+      long long i0, cnt;
+      own_range(c, d, i0, cnt);
+      if (cnt <= gridDim.x) {                  // few nodes: one CTA each
+        if (blockIdx.x < cnt) tree_up_node_cta(c, d, i0 + blockIdx.x, sm);
+      } else if (warp < c.tree_warps) {
+        for (long long j = gwt; j < cnt; j += nwt) tree_up_node(c, d, i0 + j, sm + (size_t)warp * c.tree_scratch, lane);
+      }
+      grid.sync();
+      if (stamp) c.stamps[ns++] = gtimer();
+    }
+  }
+  if (!ph.down) return;
+  for (int d = 0; d < c.kappa; d++) {
+    long long i0, cnt;
+    own_range(c, d, i0, cnt);
+    for (long long j = gw; j < cnt; j += nw) tree_down_node(c, d, i0 + j, lane);
+    grid.sync();
+    if (stamp) c.stamps[ns++] = gtimer();
+  }
+  if (c.bulk) leaf_down_phase<true>(c, sX, sE, S, phX, phE); else leaf_down_phase<false>(c, sX, sE, S, phX, phE);
+  if (stamp) c.stamps[ns++] = gtimer();
+}
+
+// sharded solve: x[perm[row_lo_r + i]] = slice_r[i] for every rank's slice of the gathered solution
+__global__ void k_unshard(const double *gathered, const long long *rowlo, int nranks, long long rows_max, long long n,
+                          const long long *perm, double *x) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= (long long)nranks * rows_max) return;
+  const int r = (int)(e / rows_max);
+  const long long i = e - (long long)r * rows_max;
+  const long long lo = rowlo[r], hi = r + 1 < nranks ? rowlo[r + 1] : n;
+  if (lo + i < hi) x[perm[lo + i]] = gathered[e];
+}
+
+__global__ void k_pack_rows(const double *xsorted, long long lo, long long m, double *send) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < m) send[i] = xsorted[lo + i];
 }
 
 }  // namespace
@@ -342,12 +594,11 @@ hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_on
   }
   SolveCtx c;
   c.n = h->n; c.ninternal = h->ninternal; c.nleaves = h->nleaves; c.kappa = kappa; c.K = dt.Kdim[kappa];
-  c.T = h->ltiles;
+  c.T = h->ltiles; c.grank = h->grank; c.tsplit = h->tsplit;
   c.lo = h->lo; c.hi = h->hi; c.perm = h->perm; c.Xh = h->Xh; c.rank = h->rank; c.dt = h->d_dt;
   c.Lf = h->Lf; c.lstride = h->lstride; c.Spool = h->Spool; c.BTpool = h->BTpool;
   c.V = h->Vpool; c.Tv = h->Tvec; c.hv = h->hvec; c.y = y; c.x = x; c.flags = h->dflags;
-  long long lcnt;
-  hodlr_own_nodes(h, kappa, &c.leaf0, &lcnt);
+  hodlr_own_nodes(h, kappa, &c.leaf0, &c.nown);
   c.xsorted = nullptr;
   if (h->nranks > 1 && !up_only) {
     if (!h->xshard) {
@@ -356,70 +607,98 @@ hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_on
     }
     c.xsorted = h->xshard;
   }
-  const int lgrid = (int)lcnt;
+  // dynamic shared memory: the leaf staging (X tiles + E panel) or the tree-up scratch of every warp
   const int R = 8 * h->ltiles;
-  // X tiles + E panel in shared memory
-  const size_t lsm = sizeof(double) * (64 * (size_t)(h->ltiles * (h->ltiles + 1) / 2) + (size_t)c.K * R);
-  int maxsm = 0;
+  const size_t leaf_db = 64 * (size_t)(h->ltiles * (h->ltiles + 1) / 2) + (size_t)c.K * R;
+  size_t qmax = 0;
+  for (int d = 0; d < kappa; d++) qmax = std::max(qmax, 2 * (size_t)dt.rdep[d + 1]);
+  c.tree_scratch = (long long)std::max<size_t>(1, 2 * qmax * qmax + 5 * qmax);   // kappa = 0: no tree
+  int maxsm = 0, nsm = 0;
   HCUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
-  if (lsm + 32 * 1024 > (size_t)maxsm)
-    return hodlr_set_error(HODLR_EINVAL, "solve: leaf panel (%d x %d) exceeds shared memory", R, c.K);
-  static size_t lattr = 0;
-  if (lsm > lattr) {
-    HCUDA(cudaFuncSetAttribute(k_leaf_up, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
-    HCUDA(cudaFuncSetAttribute(k_leaf_down, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
-    lattr = lsm;
+  HCUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->dev));
+  static int static_smem = -1;
+  if (static_smem < 0) {
+    cudaFuncAttributes fa;
+    HCUDA(cudaFuncGetAttributes(&fa, k_solve));
+    static_smem = (int)fa.sharedSizeBytes;
   }
-  ph_begin(h, PH_SLEAF_UP);
-  k_leaf_up<<<lgrid, LT, lsm, h->st>>>(c);
-  HLAUNCH(h, "k_leaf_up");
-  ph_end(h, PH_SLEAF_UP);
-  ph_begin(h, PH_STREE);
-  size_t up_smem_max = 0;
-  for (int d = 0; d < kappa; d++) {
-    const size_t q = 2 * (size_t)dt.rdep[d + 1];
-    up_smem_max = std::max(up_smem_max, sizeof(double) * NWS * (2 * q * q + 5 * q));
+  const size_t avail = ((size_t)maxsm - (size_t)static_smem - 256) / sizeof(double);
+  const size_t need = std::max(leaf_db, (size_t)c.tree_scratch);
+  if (need > avail)
+    return hodlr_set_error(HODLR_EINVAL, "solve: leaf panel (%d x %d) or coupling size %zu exceeds shared memory", R, c.K, qmax);
+  const size_t dsm_d = std::min(avail, std::max(leaf_db, (size_t)NWL * (size_t)c.tree_scratch));
+  c.tree_warps = (int)std::min<size_t>(NWL, dsm_d / (size_t)c.tree_scratch);
+  const size_t dsm = sizeof(double) * dsm_d;
+  static int trace = -1;
+  if (trace < 0) { const char *ev = getenv("HODLR_TRACE"); trace = ev && atoi(ev) ? 1 : 0; }
+  c.stamps = nullptr;
+  if (trace) {
+    if (!h->stamps) h->stamps = (unsigned long long *)hodlr_dalloc(h, sizeof(unsigned long long) * 128);
+    c.stamps = h->stamps;
   }
-  if (kappa > 0) HCUDA(cudaFuncSetAttribute(k_tree_up, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)up_smem_max));
-  for (int d = kappa - 1; d >= 0; d--) {
-    if (d + 1 == h->tsplit && h->nranks > 1) {   // projections g and h of all depth-t subtree roots
-      const long long Kt = dt.Kdim[d + 1];
-      double *gb = h->Vpool + dt.nodeV[d + 1];
-      hodlr_status xs = hodlr_allgather(h, gb + h->grank * Kt, gb, sizeof(double) * (Kt > 0 ? Kt : 1));
-      if (xs != HODLR_OK) return xs;
-      double *hb = h->hvec + 2 * ((1LL << (d + 1)) - 1);
-      xs = hodlr_allgather(h, hb + 2 * h->grank, hb, sizeof(double) * 2);
-      if (xs != HODLR_OK) return xs;
+  static size_t attr = 0;
+  if (dsm > attr) {
+    HCUDA(cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+    attr = dsm;
+  }
+  if (!h->bulk_checked) {     // bulk staging needs every leaf start and size and n even (16-byte segments)
+    bool ok = (h->n % 2) == 0;
+    for (long long l = 0; ok && l < h->nleaves; l++) {
+      const long long id = h->ninternal + l;
+      ok = (h->h_lo[id] % 2) == 0 && ((h->h_hi[id] - h->h_lo[id]) % 2) == 0;
     }
-    long long i0, cnt;
-    hodlr_own_nodes(h, d, &i0, &cnt);
-    const size_t q = 2 * (size_t)dt.rdep[d + 1];
-    k_tree_up<<<(int)((cnt + NWS - 1) / NWS), ST, sizeof(double) * NWS * (2 * q * q + 5 * q), h->st>>>(c, d, i0, cnt);
-    HLAUNCH(h, "k_tree_up");
+    h->bulk_ok = ok ? 1 : 0; h->bulk_checked = 1;
   }
-  if (up_only) { ph_end(h, PH_STREE); return HODLR_OK; }
-  for (int d = 0; d < kappa; d++) {
-    long long i0, cnt;
-    hodlr_own_nodes(h, d, &i0, &cnt);
-    k_tree_down<<<(int)((cnt + NWS - 1) / NWS), ST, 0, h->st>>>(c, d, i0, cnt);
-    HLAUNCH(h, "k_tree_down");
+  static int bulk_env = -1;      // bulk (TMA-engine) staging measured slower than per-thread cp.async here
+  if (bulk_env < 0) { const char *ev = getenv("HODLR_SOLVE_BULK"); bulk_env = ev && atoi(ev) ? 1 : 0; }
+  c.bulk = h->bulk_ok && bulk_env;
+  const int grid = nsm;                                   // one persistent CTA per SM
+  auto launch = [&](Phases ph) -> hodlr_status {
+    void *args[] = {(void *)&c, (void *)&ph};
+    HCUDA(cudaLaunchCooperativeKernel((const void *)k_solve, dim3(grid), dim3(LT), args, dsm, h->st));
+    HLAUNCH(h, "k_solve");
+    return HODLR_OK;
+  };
+  ph_begin(h, PH_SLEAF_UP);
+  hodlr_status st;
+  if (h->nranks > 1 && h->tsplit > 0) {
+    // leaf up + own subtree levels, exchange of the depth-t projections, then the rest
+    st = launch(Phases{1, kappa - 1, h->tsplit, 0});
+    if (st != HODLR_OK) return st;
+    const int t = h->tsplit;
+    const long long Kt = dt.Kdim[t];
+    double *gb = h->Vpool + dt.nodeV[t];
+    st = hodlr_allgather(h, gb + h->grank * Kt, gb, sizeof(double) * (Kt > 0 ? Kt : 1));
+    if (st != HODLR_OK) return st;
+    double *hb = h->hvec + 2 * ((1LL << t) - 1);
+    st = hodlr_allgather(h, hb + 2 * h->grank, hb, sizeof(double) * 2);
+    if (st != HODLR_OK) return st;
+    st = launch(Phases{0, t - 1, 0, up_only ? 0 : 1});
+  } else {
+    st = launch(Phases{1, kappa - 1, 0, up_only ? 0 : 1});
   }
-  ph_end(h, PH_STREE);
-  ph_begin(h, PH_SLEAF_DOWN);
-  k_leaf_down<<<lgrid, LT, lsm, h->st>>>(c);
-  HLAUNCH(h, "k_leaf_down");
-  if (h->nranks > 1) {            // every rank returns the full solution: allgather the sorted row slices
+  if (st != HODLR_OK) return st;
+  if (h->nranks > 1 && !up_only) {   // every rank returns the full solution: allgather the sorted row slices
     const long long id = (1LL << h->tsplit) - 1 + h->grank;
     const long long rlo = h->h_lo[id], rm = h->h_hi[id] - rlo;
     double *send = h->xshard + h->n, *recv = send + h->rows_max;
     k_pack_rows<<<(int)((rm + 255) / 256), 256, 0, h->st>>>(h->xshard, rlo, rm, send);
     HLAUNCH(h, "k_pack_rows");
-    hodlr_status xs = hodlr_allgather(h, send, recv, sizeof(double) * h->rows_max);
-    if (xs != HODLR_OK) return xs;
+    st = hodlr_allgather(h, send, recv, sizeof(double) * h->rows_max);
+    if (st != HODLR_OK) return st;
     const long long tot = (long long)h->nranks * h->rows_max;
     k_unshard<<<(int)((tot + 255) / 256), 256, 0, h->st>>>(recv, h->d_rowlo, h->nranks, h->rows_max, h->n, h->perm, x);
     HLAUNCH(h, "k_unshard");
   }
-  ph_end(h, PH_SLEAF_DOWN);
+  ph_end(h, PH_SLEAF_UP);
+  if (trace && c.stamps) {       // per-phase device times (block 0's view, after each grid barrier)
+    unsigned long long s[64];
+    HCUDA(cudaMemcpyAsync(s, c.stamps, sizeof(s), cudaMemcpyDeviceToHost, h->st));
+    HCUDA(cudaStreamSynchronize(h->st));
+    const int nst = (up_only ? 1 + kappa : 2 + 2 * kappa) + 1;
+    fprintf(stderr, "[hodlr solve phases us]");
+    for (int k = 1; k < nst && k < 64; k++) fprintf(stderr, " %.1f", 1e-3 * (double)(s[k] - s[k - 1]));
+    fprintf(stderr, "\n");
+  }
   return HODLR_OK;
 }
