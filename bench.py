@@ -151,21 +151,47 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(getattr(self, "lines", []))}
 
 
-# ------------------------------------------------------------------ algorithmic counts (DESIGN.md section 7)
+# ------------------------------------------------------------------ algorithmic counts (DESIGN.md section 6.4)
 def algorithmic(info, n, leaf):
-    """Per-launch algorithmic FLOPs / bytes of each kernel family for the formulation implemented."""
+    """Per-launch algorithmic work of each kernel family of the formulation implemented:
+    (bound, amount, unit_of_amount, kernel name)."""
     K = info["K"]
     r = info["max_rank_by_depth"]
     p = leaf
     nl = n // p
-    # leaf factor (one launch): assemble p^2/2 entries (~30 flop each), Cholesky p^3/3, Z = L^{-1}E (p^2 K),
-    # Pi = Z^T Z (p K^2, symmetric half); bytes: read E (8 n K), write L (4 n (p+1)) and Pi (8 K^2 per leaf)
-    leaf_flops = nl * (30 * p * p / 2 + p ** 3 / 3 + p * p * K + p * K * K)
-    leaf_bytes = 8 * n * K + 4 * n * (p + 1) + 4 * nl * K * (K + 1)
-    # ACA: n * K entry evaluations (~30 flop) + 2 n sum r^2 arithmetic x2 (row and column residual + dots)
-    aca_flops = n * K * 30 + 4 * n * sum(x * x for x in r)
-    aca_bytes = 8 * n * K + 4 * n * sum(x * x for x in r)
-    return {"leaf_factor": (leaf_flops, leaf_bytes), "aca": (aca_flops, aca_bytes)}
+    kap = info["kappa"]
+    Kd = [0]
+    for x in r:
+        Kd.append(Kd[-1] + x)
+    ntile_bytes = (p // 8) * (p // 8 + 1) // 2 * 64 * 8           # X = L^{-1} tiles per leaf
+    fam = {}
+    # ACA (all levels): every step streams the previous factor columns of its block side once and writes one
+    # column: sum_k 8 (k + 1) bytes per element, plus the points -- 8 n K + 4 n sum r_d^2 in total
+    fam["aca"] = ("hbm", 8 * n * K + 4 * n * sum(x * x for x in r), "bytes", "k_aca_pass/k_aca_fused")
+    # leaf Cholesky + triangular inverse (tensor pipe): p^3/3 + p^3/3 flop per leaf
+    fam["leaf_chol"] = ("tensor", nl * (2 * p ** 3 / 3), "flop", "k_leaf_chol")
+    # Z = X E (p^2 K) and Pi = Z^T Z (p K^2) per leaf (tensor pipe)
+    fam["leaf_factor"] = ("tensor", nl * (p * p * K + p * K * K), "flop", "k_leaf_zsyrk")
+    # coupling tree: per node q^3 (S^-1) + 4 q^2 K_d (T, refinement) + q K_d^2 (Schur update of Pi), FP64 ALU
+    tree = 0
+    for d in range(kap):
+        q = 2 * r[d]
+        tree += 2 ** d * (q ** 3 + 4 * q * q * Kd[d] + q * Kd[d] ** 2)
+    fam["coupling_tree"] = ("alu", 2 * tree, "flop", "k_tree_factor")
+    # solve: X tiles and the panel E read twice (up and down), y gathered twice, x written
+    fam["solve"] = ("hbm", 2 * (nl * ntile_bytes + 8 * n * K) + 3 * 8 * n, "bytes", "k_solve")
+    return fam
+
+
+def ncu_traffic():
+    """DRAM bytes per launch from the newest committed ncu summary (profiles/rNN_ncu_summary.json)."""
+    import glob
+    fs = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.json")))
+    if not fs:
+        return {}, None
+    with open(fs[-1]) as f:
+        d = json.load(f)
+    return {k: v.get("dram_bytes") for k, v in d.get("kernels", {}).items()}, os.path.basename(fs[-1])
 
 
 def load_peaks():
@@ -251,7 +277,7 @@ def run_ours(args):
     for inf in infos:
         for k, v in inf["kernel_ms"].items():
             fam_ms[k] = fam_ms.get(k, 0.0) + v
-    fam_ms = {k: v / len(infos) for k, v in fam_ms.items()}
+    fam_ms = {k: v / len(infos) for k, v in fam_ms.items() if not k.startswith("unused")}
     t_max = t_step
     if ws > 1:
         tt = torch.tensor([t_step], dtype=torch.float64, device=dev)
@@ -288,29 +314,35 @@ def run_ours(args):
     info = infos[-1]
     clocks = clk.summary()
     peaks = load_peaks()
-    # ---------------- roofline of the dominant kernel family
+    # ---------------- rooflines: algorithmic work / live event time per kernel family; dominant = longest
     alg = algorithmic(info, n, cfg.leaf)
-    dom = max(fam_ms, key=lambda k: fam_ms[k])
-    calls = info["kernel_calls"][dom] or 1
-    t_launch = fam_ms[dom] / calls / 1e3
-    if dom in alg:
-        fl, by = alg[dom]
-        if dom == "leaf_factor":
-            peak, how = fp64_peak_tflops(peaks, clocks.get("sm_mhz"))
-            achieved = fl / t_launch / 1e12
-            roof = {"kernel": "k_leaf_factor_mma", "bound": "tensor", "achieved": achieved, "peak": peak,
-                    "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None, "peak_source": how,
-                    "algorithmic_flops_per_launch": fl, "launch_ms": 1e3 * t_launch}
+    fp64_peak, fp64_how = fp64_peak_tflops(peaks, clocks.get("sm_mhz"))
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    traffic, traffic_src = ncu_traffic()
+    rows = []
+    for fam, (bound, amount, unit, kname) in alg.items():
+        ms = fam_ms.get(fam, 0.0)
+        calls = info["kernel_calls"].get(fam) or 1
+        if ms <= 0.0:
+            continue
+        t_launch = ms / calls / 1e3
+        if bound == "hbm":
+            ach, peak, u = amount / t_launch / 1e9, hbm_peak, "GB/s"
         else:
-            peak = peaks.get("hbm_gbs", 6650.0)
-            achieved = by / t_launch / 1e9
-            roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "frac": achieved / peak, "traffic": None,
-                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650",
-                    "algorithmic_bytes_per_launch": by, "launch_ms": 1e3 * t_launch}
-    else:
-        roof = {"kernel": dom, "bound": "alu", "achieved": None, "peak": None, "unit": None, "frac": None,
-                "traffic": None}
+            ach, peak, u = amount / t_launch / 1e12, fp64_peak, "TFLOP/s"
+        kk = kname.split("/")[0]
+        tr = traffic.get(kk)
+        if tr is not None and fam == "aca":
+            tr = None          # the capture is one pass of one step, not the whole ACA family
+        rows.append({"kernel": kname, "family": fam, "bound": bound, "achieved": ach, "peak": peak, "unit": u,
+                     "frac": ach / peak, "traffic": tr, "ms": ms / calls,
+                     ("algorithmic_bytes_per_launch" if bound == "hbm" else "algorithmic_flops_per_launch"): amount})
+    main = [r_ for r_ in rows if r_["family"] != "leaf_chol"]     # leaf_chol runs on a side stream under the ACA
+    dom = max(main, key=lambda r_: r_["ms"])
+    roof = dict(dom)
+    roof["peak_source"] = ("MEASURED_PEAKS.json hbm_gbs" if dom["bound"] == "hbm" else fp64_how)
+    roof["traffic_source"] = traffic_src
+    roof["all_kernels"] = rows
     cpu = None
     if not args.no_cpu_baseline and ws == 1:
         cpu = cpu_baseline_obj(cfg, args.cpu_sample)

@@ -89,8 +89,8 @@ typedef struct {
   int32_t aca_steps;            /* ACA pivot steps executed (max rank + 1) */
   int32_t gpu_launches_last;    /* kernels launched by the last API call */
   /* Device time (ms, CUDA events on the handle's stream) accumulated since build, and call counts, per
-   * kernel family: [0] sort, [1] ACA, [2] leaf factor, [3] coupling tree, [4] solve leaf up,
-   * [5] solve tree up/down, [6] solve leaf down, [7] leaf Cholesky (side stream, overlaps the ACA). */
+   * kernel family: [0] sort, [1] ACA, [2] leaf factor (Z, Pi), [3] coupling tree, [4] solve (one cooperative
+   * kernel), [5], [6] unused, [7] leaf Cholesky + inverse (side stream, overlaps the ACA). */
   double  kernel_ms[16];
   int64_t kernel_calls[16];
   int32_t rank, nranks, split_depth;   /* sharding (split_depth = log2(nranks)); ranks/means above cover the

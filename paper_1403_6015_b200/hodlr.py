@@ -48,8 +48,7 @@ class hodlr_info_t(C.Structure):
                 ("kernel_ms", C.c_double * 16), ("kernel_calls", C.c_int64 * 16),
                 ("rank", C.c_int32), ("nranks", C.c_int32), ("split_depth", C.c_int32), ("pad_", C.c_int32)]
 
-KERNEL_FAMILIES = ("sort", "aca", "leaf_factor", "coupling_tree", "solve_leaf_up", "solve_tree", "solve_leaf_down",
-                   "leaf_chol")
+KERNEL_FAMILIES = ("sort", "aca", "leaf_factor", "coupling_tree", "solve", "unused5", "unused6", "leaf_chol")
 
 
 _lib = None
