@@ -48,11 +48,6 @@ __global__ void k_aca_init(AcaCtx c, int nblocks, int cap) {
   c.rank[b] = 0;
 }
 
-__device__ __forceinline__ double warp_allsum(double v) {   // xor butterfly: every lane gets the same bits
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
 
 // Block-wide argmax (ties -> smallest index) + sum of nrm2; result broadcast to every thread.
 __device__ __forceinline__ void block_argmax_n2(double &ba, long long &bi, double &bv, double &n2,
@@ -94,7 +89,7 @@ constexpr int ACA_E = 4;                       // elements per thread per sub-ti
 constexpr int ACA_TILE = ACA_SUB * ACA_E;
 
 template <bool ROW>
-__global__ void __launch_bounds__(ACA_SUB, 3) k_aca_pass(const AcaCtx *__restrict__ pc) {
+__global__ void __launch_bounds__(ACA_SUB, 2) k_aca_pass(const AcaCtx *__restrict__ pc) {
   __shared__ AcaCtx c;                         // context in shared memory: global stores cannot alias it
   for (int i = threadIdx.x; i < (int)(sizeof(AcaCtx) / 8); i += ACA_SUB) ((long long *)&c)[i] = ((const long long *)pc)[i];
   __syncthreads();
@@ -121,42 +116,129 @@ __global__ void __launch_bounds__(ACA_SUB, 3) k_aca_pass(const AcaCtx *__restric
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   for (int l = t; l < k; l += ACA_SUB) coef[l] = slot[(long long)l * n + pg];
   __syncthreads();
-  double w0 = 0.0, w1 = 0.0;                  // lane (l & 31) owns dot l: l < 32 in w0, l >= 32 in w1
+  // dots F_l . a: for each batch of 4 columns the 4 per-lane partials are reduced over the warp by a transposed
+  // butterfly (6 shuffles); lane L then holds column l0 + ((L >> 3) & 3) and keeps it when batch l0 / 4 is
+  // congruent to L mod 8 (w0 for l < 32, w1 for l >= 32)
+  double w0 = 0.0, w1 = 0.0;
   double ba = 0.0, bv = 0.0, n2 = 0.0; long long bi = -1;
   const long long end = it.start + it.len;
+  const size_t n1 = (size_t)n, n2s = 2 * (size_t)n, n3 = 3 * (size_t)n;
+  const int hi4 = lane & 16, hi3 = lane & 8;
+  // vector path: thread t takes the 4 consecutive elements 4t..4t+3 of each 1024-element sub-tile (double2
+  // loads/stores); needs 16-byte alignment of every column segment (n and the chunk start even) -- the
+  // scalar loop below handles the rest
+  const bool vec = ((n | (lo + it.start)) & 3) == 0 && (it.len & 3) == 0;
+  if (vec) {
+    for (long long s0 = it.start; s0 < end; s0 += ACA_TILE) {
+      const long long g0 = lo + s0 + 4 * t;    // elements g0 .. g0 + 3
+      const bool ok = s0 + 4 * t < end;        // whole quad valid (len is a multiple of 4)
+      double a[4], r[4];
+      unsigned usedm = 0;
+      if (ok) {
+        const double2 x01 = *(const double2 *)(c.xs + g0), x23 = *(const double2 *)(c.xs + g0 + 2);
+        const uchar4 u4 = *(const uchar4 *)(used + g0);
+        usedm = (u4.x ? 1u : 0u) | (u4.y ? 2u : 0u) | (u4.z ? 4u : 0u) | (u4.w ? 8u : 0u);
+        const double xq[4] = {x01.x, x01.y, x23.x, x23.y};
+#pragma unroll
+        for (int q = 0; q < 4; q++) a[q] = kval(c.kp, ROW ? xp - xq[q] : xq[q] - xp);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; q++) a[q] = 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; q++) r[q] = a[q];
+      const double *colp = slot + (ok ? g0 : lo + it.start);
+      constexpr int LS = 4;
+      for (int l0 = 0; l0 < k; l0 += LS) {
+        double F[LS][4];
+#pragma unroll
+        for (int dl = 0; dl < LS; dl++) {
+          const double *cp = colp + (size_t)(l0 + dl < k ? l0 + dl : 0) * n1;
+          const double2 f01 = *(const double2 *)cp, f23 = *(const double2 *)(cp + 2);
+          const bool v = ok && l0 + dl < k;
+          F[dl][0] = v ? f01.x : 0.0; F[dl][1] = v ? f01.y : 0.0; F[dl][2] = v ? f23.x : 0.0; F[dl][3] = v ? f23.y : 0.0;
+        }
+        double pv[LS];
+#pragma unroll
+        for (int dl = 0; dl < LS; dl++) {
+          const double cf = l0 + dl < k ? coef[l0 + dl] : 0.0;
+          double p = 0.0;
+#pragma unroll
+          for (int q = 0; q < 4; q++) { r[q] = fma(-cf, F[dl][q], r[q]); p = fma(F[dl][q], a[q], p); }
+          pv[dl] = p;
+        }
+        double s0v = hi4 ? pv[0] : pv[2], s1v = hi4 ? pv[1] : pv[3];
+        double k0 = hi4 ? pv[2] : pv[0], k1 = hi4 ? pv[3] : pv[1];
+        k0 += __shfl_xor_sync(0xffffffffu, s0v, 16);
+        k1 += __shfl_xor_sync(0xffffffffu, s1v, 16);
+        const double sv = hi3 ? k0 : k1;
+        double kk = hi3 ? k1 : k0;
+        kk += __shfl_xor_sync(0xffffffffu, sv, 8);
+        kk += __shfl_xor_sync(0xffffffffu, kk, 4);
+        kk += __shfl_xor_sync(0xffffffffu, kk, 2);
+        kk += __shfl_xor_sync(0xffffffffu, kk, 1);
+        if (((l0 >> 2) & 7) == (lane & 7)) { if (l0 < 32) w0 += kk; else w1 += kk; }
+      }
+      if (ok) {
+        double v[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) v[q] = r[q] * scale;
+        double *outp = slot + (long long)k * n + g0;
+        *(double2 *)outp = make_double2(v[0], v[1]);
+        *(double2 *)(outp + 2) = make_double2(v[2], v[3]);
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          if (!((usedm >> q) & 1u) && amax_better(ba, bi, fabs(v[q]), g0 + q - lo)) { ba = fabs(v[q]); bi = g0 + q - lo; bv = v[q]; }
+          n2 += v[q] * v[q];
+        }
+      }
+    }
+  } else
   for (long long s0 = it.start; s0 < end; s0 += ACA_TILE) {
     const long long g0 = lo + s0 + t;          // element q at g0 + q * ACA_SUB
     const int nval = (int)min((long long)ACA_E, (end - s0 - t + ACA_SUB - 1) / ACA_SUB);   // valid elements
+    const double *xsp = c.xs + g0;
+    const unsigned char *up = used + g0;
     double a[ACA_E], r[ACA_E];
     unsigned usedm = 0;                        // used flags, loaded up front (char loads cannot pass the stores)
 #pragma unroll
     for (int q = 0; q < ACA_E; q++) {
-      const double xq = q < nval ? c.xs[g0 + q * ACA_SUB] : xp;
-      if (q < nval && used[g0 + q * ACA_SUB]) usedm |= 1u << q;
+      const double xq = q < nval ? xsp[q * ACA_SUB] : xp;
+      if (q < nval && up[q * ACA_SUB]) usedm |= 1u << q;
       a[q] = q < nval ? kval(c.kp, ROW ? xp - xq : xq - xp) : 0.0;
       r[q] = a[q];
     }
+    const double *colp = slot + g0;
     constexpr int LS = 4;                      // factor columns per batch of loads
     for (int l0 = 0; l0 < k; l0 += LS) {
+      const double *c0 = colp + (size_t)l0 * n1;
+      const double *cl[LS] = {c0, c0 + n1, c0 + n2s, c0 + n3};
       double F[LS][ACA_E];
 #pragma unroll
+      for (int dl = 0; dl < LS; dl++)
+#pragma unroll
+        for (int q = 0; q < ACA_E; q++) F[dl][q] = (l0 + dl < k && q < nval) ? cl[dl][q * ACA_SUB] : 0.0;
+      double pv[LS];
+#pragma unroll
       for (int dl = 0; dl < LS; dl++) {
-        const double *col = slot + (long long)(l0 + dl) * n + g0;
+        const double cf = l0 + dl < k ? coef[l0 + dl] : 0.0;
+        double p = 0.0;
 #pragma unroll
-        for (int q = 0; q < ACA_E; q++) F[dl][q] = (l0 + dl < k && q < nval) ? col[q * ACA_SUB] : 0.0;
+        for (int q = 0; q < ACA_E; q++) { r[q] = fma(-cf, F[dl][q], r[q]); p = fma(F[dl][q], a[q], p); }
+        pv[dl] = p;
       }
-#pragma unroll
-      for (int dl = 0; dl < LS; dl++) {
-        const int l = l0 + dl;
-        if (l < k) {
-          const double cf = coef[l];
-          double p = 0.0;
-#pragma unroll
-          for (int q = 0; q < ACA_E; q++) { r[q] = fma(-cf, F[dl][q], r[q]); p = fma(F[dl][q], a[q], p); }
-          p = warp_allsum(p);
-          if (lane == (l & 31)) { if (l < 32) w0 += p; else w1 += p; }
-        }
-      }
+      // transposed butterfly: 4 values x 32 lanes -> lane L holds sum of value 2*(L>>4&1) + (L>>3&1)
+      double s0v = hi4 ? pv[0] : pv[2], s1v = hi4 ? pv[1] : pv[3];
+      double k0 = hi4 ? pv[2] : pv[0], k1 = hi4 ? pv[3] : pv[1];
+      k0 += __shfl_xor_sync(0xffffffffu, s0v, 16);
+      k1 += __shfl_xor_sync(0xffffffffu, s1v, 16);
+      const double sv = hi3 ? k0 : k1;
+      double kk = hi3 ? k1 : k0;
+      kk += __shfl_xor_sync(0xffffffffu, sv, 8);
+      kk += __shfl_xor_sync(0xffffffffu, kk, 4);
+      kk += __shfl_xor_sync(0xffffffffu, kk, 2);
+      kk += __shfl_xor_sync(0xffffffffu, kk, 1);
+      if (((l0 >> 2) & 7) == (lane & 7)) { if (l0 < 32) w0 += kk; else w1 += kk; }
     }
 #pragma unroll
     for (int q = 0; q < ACA_E; q++) {
@@ -168,8 +250,11 @@ __global__ void __launch_bounds__(ACA_SUB, 3) k_aca_pass(const AcaCtx *__restric
       n2 += v * v;
     }
   }
-  if (lane < k) sdot[warp][lane] = w0;
-  if (lane + 32 < k) sdot[warp][lane + 32] = w1;
+  {
+    const int la = 4 * (lane & 7) + ((lane >> 3) & 3), lb = 32 + la;
+    if (la < k) sdot[warp][la] = w0;
+    if (lb < k) sdot[warp][lb] = w1;
+  }
   block_argmax_n2(ba, bi, bv, n2, s_abs, s_idx, s_val, s_n2);
   const int nq = c.nq[b];
   double *rec0 = c.rec + c.recbase[b] * ACA_RECW;
