@@ -97,18 +97,19 @@ __global__ void __launch_bounds__(ACA_SUB, 2) k_aca_pass(const AcaCtx *__restric
   const AcaItem it = c.items[blockIdx.x];
   const int b = it.block;
   AcaState *st = &c.st[b];
-  if (st->done) return;
-  const int k = st->k;
+  const int done = __ldcg(&st->done), k = __ldcg(&st->k);          // one round of loads for the state
+  const long long piv = ROW ? __ldcg(&st->ipiv) : __ldcg(&st->jpiv);
+  const double pivval = ROW ? 1.0 : __ldcg(&st->pivval);
+  if (done) return;
   const long long n = c.n;
-  const long long c1 = 2LL * b + 1, c2 = 2LL * b + 2;
-  const long long lo1 = c.lo[c1], m1 = c.hi[c1] - lo1, lo2 = c.lo[c2], m2 = c.hi[c2] - lo2;
-  const int e = c.bdepth[b] + 1;
-  double *slot = c.Xh + c.dt->colbase[e] * n;
+  const long long lo1 = it.lo1, m1 = it.m1, lo2 = it.lo2, m2 = it.m2;
+  const int e = it.e;
+  double *slot = c.Xh + it.slot_off;
   const unsigned char *used = c.used + (long long)(e - 1) * n;
-  const long long pg = ROW ? lo1 + st->ipiv : lo2 + st->jpiv;     // fixed row (ROW) / column (COL)
+  const long long pg = ROW ? lo1 + piv : lo2 + piv;               // fixed row (ROW) / column (COL)
   const double xp = c.xs[pg];
   const long long lo = ROW ? lo2 : lo1;
-  const double scale = ROW ? 1.0 : 1.0 / st->pivval;
+  const double scale = ROW ? 1.0 : 1.0 / pivval;
   __shared__ double coef[ACA_MAXCAP];
   __shared__ double sdot[ACA_SUB / 32][ACA_MAXCAP];
   __shared__ double s_abs[ACA_SUB / 32], s_val[ACA_SUB / 32], s_n2[ACA_SUB / 32];
@@ -301,11 +302,14 @@ __global__ void __launch_bounds__(ACA_SUB, 2) k_aca_pass(const AcaCtx *__restric
   __syncthreads();
   const long long bidx = c.bigidx[b];
   double *G = c.gram + bidx * (2LL * ACA_GSZ) + (ROW ? ACA_GSZ : 0);   // G_U then G_V
-  // dots with the new column: F_l . r = (F_l . a - sum_m coef_m G[l,m]) * scale
+  // dots with the new column: F_l . r = (F_l . a - sum_m coef_m G[l,m]) * scale; G staged in shared memory
   __shared__ double dnew[ACA_MAXCAP];
+  __shared__ double sG[ACA_GSZ];
+  for (int p = t; p < k * (k + 1) / 2; p += ACA_SUB) sG[p] = __ldcg(G + p);
+  __syncthreads();
   for (int l = t; l < k; l += ACA_SUB) {
     double s = tot[1 + l];
-    for (int m = 0; m < k; m++) s = fma(-coef[m], __ldcg(G + pk(l, m)), s);
+    for (int m = 0; m < k; m++) s = fma(-coef[m], sG[pk(l, m)], s);
     s *= scale;
     dnew[l] = s;
     G[pk(k, l)] = s;
@@ -513,7 +517,10 @@ static cudaError_t plan_create(AcaPlan *P, const hodlr_s *h) {
       if (chunk < ACA_BIG_CHUNK) chunk = ACA_BIG_CHUNK;
       int q = 0;
       for (long long s = 0; s < m; s += chunk, q++) {
-        AcaItem it; it.block = (int)b; it.q = q; it.start = s; it.len = (int)std::min(chunk, m - s); it.pad = 0;
+        AcaItem it; it.block = (int)b; it.q = q; it.start = s; it.len = (int)std::min(chunk, m - s);
+        it.e = bdepth[b] + 1;
+        it.lo1 = h->h_lo[2 * b + 1]; it.m1 = m1; it.lo2 = h->h_lo[2 * b + 2]; it.m2 = m2;
+        it.slot_off = h->dt.colbase[it.e] * h->n;
         (side == 0 ? items_r : items_c).push_back(it);
       }
       if (side == 0) { nq_r[b] = q; rb_r[b] = P->nrec_r; P->nrec_r += q; }

@@ -245,7 +245,9 @@ hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const 
   // issued now on a side stream and overlap the ACA; hodlr_factor waits for them.
   st = hodlr_leaf_alloc(h);
   if (st != HODLR_OK) goto fail;
-  {
+  static int chol_after = -1;     // HODLR_CHOL_AFTER_ACA=1: run the leaf Cholesky after the ACA (experiments)
+  if (chol_after < 0) { const char *ev = getenv("HODLR_CHOL_AFTER_ACA"); chol_after = ev && atoi(ev) ? 1 : 0; }
+  if (!chol_after) {
     bool launched = false;
     CK(cudaEventRecord(h->ev_fork, h->st));
     CK(cudaStreamWaitEvent(h->st3, h->ev_fork, 0));
@@ -260,6 +262,15 @@ hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const 
   st = hodlr_aca(h);
   hodlr_trace("build: aca returned");
   if (st != HODLR_OK) goto fail;
+  if (chol_after) {
+    bool launched = false;
+    ph_begin(h, PH_CHOL);
+    st = hodlr_leaf_chol_mma(h, h->st, &launched);
+    if (st != HODLR_OK) goto fail;
+    ph_end(h, PH_CHOL);
+    CK(cudaEventRecord(h->ev_chol, h->st));
+    h->chol_done = launched ? 1 : 0;
+  }
   {
     int f5 = 0;
     CK(cudaMemcpyAsync(&f5, h->dflags + 5, sizeof(int), cudaMemcpyDeviceToHost, h->st));

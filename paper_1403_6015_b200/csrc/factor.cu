@@ -447,6 +447,14 @@ __global__ void __launch_bounds__(TT, 3) k_tree_factor(TreeCtx c) {
   tree_node<DD>(c, c.i0 + blockIdx.x, sm);
 }
 
+// Levels with many small nodes: 128-thread CTAs (6 per SM) -- finer barrier domains, more independent nodes
+// in flight per SM.  Same device code.
+template <bool DD>
+__global__ void __launch_bounds__(TT / 2, 6) k_tree_factor_narrow(TreeCtx c) {
+  extern __shared__ double sm[];
+  tree_node<DD>(c, c.i0 + blockIdx.x, sm);
+}
+
 // log det partial = leaves (left to right), then internal nodes of depth >= tsplit by depth kappa-1..tsplit,
 // left to right; per-thread Neumaier over a contiguous segment, combined in order by thread 0.
 // out[0] = partial, out[1] = failures seen by this rank.
@@ -602,6 +610,8 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
   if (kappa > 0 && tree_smem_max > tree_attr) {
     HCUDA(cudaFuncSetAttribute(k_tree_factor<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tree_smem_max));
     HCUDA(cudaFuncSetAttribute(k_tree_factor<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tree_smem_max));
+    HCUDA(cudaFuncSetAttribute(k_tree_factor_narrow<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tree_smem_max));
+    HCUDA(cudaFuncSetAttribute(k_tree_factor_narrow<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tree_smem_max));
     tree_attr = tree_smem_max;
   }
   // debug/experiment switch: depths >= HODLR_TREE_PLAIN_FROM use plain double (default: none)
@@ -623,8 +633,14 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
     tc.Sst = h->Spool + dt.nodeS[d]; tc.BT = h->BTpool + dt.nodeBT[d];
     tc.node_ld = h->node_ld; tc.flags = h->dflags;
     const size_t smem = sizeof(double) * (size_t)tree_smem_doubles(tc.q, tc.ldk);
-    if (tc.dd) k_tree_factor<true><<<(int)cnt, TT, smem, h->st>>>(tc);
-    else k_tree_factor<false><<<(int)cnt, TT, smem, h->st>>>(tc);
+    const bool narrow = cnt >= 4 * 148 && tc.q <= 16;
+    if (narrow) {
+      if (tc.dd) k_tree_factor_narrow<true><<<(int)cnt, TT / 2, smem, h->st>>>(tc);
+      else k_tree_factor_narrow<false><<<(int)cnt, TT / 2, smem, h->st>>>(tc);
+    } else {
+      if (tc.dd) k_tree_factor<true><<<(int)cnt, TT, smem, h->st>>>(tc);
+      else k_tree_factor<false><<<(int)cnt, TT, smem, h->st>>>(tc);
+    }
     HLAUNCH(h, "k_tree_factor");
   }
   // log det: this rank's leaves and subtree nodes (others are 0), exchanged with the failure counts, then the

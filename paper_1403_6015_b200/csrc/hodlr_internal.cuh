@@ -57,7 +57,13 @@ struct AcaState {
   double dV[ACA_MAXCAP];   // V'_l . V'_k, l < k, of the current step
 };
 
-struct AcaItem { int block; int q; long long start; int len; int pad; };
+// One CTA of a big-block pass: a chunk [start, start + len) of one side of `block`, with the block geometry
+// precomputed on the host (the kernel prologue then needs no dependent loads of the tree tables).
+struct AcaItem {
+  int block; int q; long long start; int len; int e;   // e: slot depth (block depth + 1)
+  long long lo1, lo2, m1, m2;                         // child ranges: rows c1 = [lo1, lo1+m1), columns c2
+  long long slot_off;                                 // colbase[e] * n: first factor column of the slot
+};
 
 // Per-depth metadata passed by value.
 struct DepthTab {
