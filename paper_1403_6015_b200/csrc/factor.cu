@@ -157,294 +157,21 @@ __global__ void __launch_bounds__(LT) k_leaf_factor(LeafCtx c) {
   }
 }
 
-struct TreeCtx {
-  int d;                    // depth of the nodes of this launch
-  long long i0;             // first node (index within depth d) of this launch
-  int r, q, Kd, K1, ldk;    // ldk: row stride of B / T in shared memory (Kd rounded up to 4)
-  int dd;                   // compensated (double-double) T and Pi
-  const double *Pi1;        // children Pi base (depth d+1), packed K1(K1+1)/2 per node
-  double *Pic;              // this depth's Pi base, packed Kd(Kd+1)/2 per node
-  double *Sst;              // per node: S (q*q), S^{-1} (q*q), spare (q)
-  double *BT;               // per node: B, T_hi, T_lo (q*Kd each)
-  double *node_ld;
-  int *flags;
-};
+}  // namespace
+#include "tree_node.cuh"
+namespace {
 
-// Shared-memory footprint of one node (doubles), see tree_node().
-__host__ __device__ __forceinline__ long long tree_smem_doubles(int q, int ldk) {
-  return 3LL * q * q + 6LL * q + 4LL * q * ldk;
-}
-
-// Gauss-Jordan with partial pivoting on [S | I] (q <= QB rows, one row per lane, in registers): row swaps and
-// the pivot-row broadcast by shuffles, no shared-memory traffic or barriers.  Same pivots (row of max |.|,
-// first index on ties, explicit swaps) and U_kk as the LU of the coupling system.  On exit lane a < q writes
-// row a of S^{-1} to W[a][q..2q), lane 0 writes |U_kk| to ukk[k]; returns sign and zero-pivot flag.
-template <int QB>
-__device__ void gj_regs(double *W, int q, double *ukk, int &sign, int &zero) {
-  const int lane = threadIdx.x & 31, q2 = 2 * q;
-  double w[2 * QB];
-#pragma unroll
-  for (int j = 0; j < QB; j++) {
-    w[j] = (lane < q && j < q) ? W[lane * q2 + j] : 0.0;
-    w[QB + j] = (lane < q && j < q) ? W[lane * q2 + q + j] : 0.0;
-  }
-  sign = 1; zero = 0;
-#pragma unroll
-  for (int k = 0; k < QB; k++) {
-    if (k < q) {                                   // (warp-uniform; keeps the loop fully unrolled)
-      double best = (lane >= k && lane < q) ? fabs(w[k]) : -1.0;
-      int p = lane;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double b2 = __shfl_xor_sync(0xffffffffu, best, o); const int p2 = __shfl_xor_sync(0xffffffffu, p, o);
-        if (b2 > best || (b2 == best && p2 < p)) { best = b2; p = p2; }
-      }
-      if (p != k) {                                // swap rows k and p
-        sign = -sign;
-        const int src = lane == k ? p : (lane == p ? k : lane);
-#pragma unroll
-        for (int j = 0; j < 2 * QB; j++) w[j] = __shfl_sync(0xffffffffu, w[j], src);
-      }
-      const double piv = __shfl_sync(0xffffffffu, w[k], k);
-      if (piv < 0.0) sign = -sign;
-      if (!(piv != 0.0)) zero = 1;
-      if (lane == 0) ukk[k] = fabs(piv);
-      const double ip = piv != 0.0 ? 1.0 / piv : 0.0;
-      const double mlt = lane == k ? 0.0 : w[k] * ip;
-#pragma unroll
-      for (int j = 0; j < 2 * QB; j++) {
-        const double prj = __shfl_sync(0xffffffffu, w[j], k);
-        w[j] = lane == k ? w[j] * ip : fma(-mlt, prj, w[j]);
-      }
-    }
-  }
-  if (lane < q) {
-#pragma unroll
-    for (int j = 0; j < QB; j++) if (j < q) W[lane * q2 + q + j] = w[QB + j];
-  }
-}
-
-// One CTA per depth-d node c (heap index (2^d - 1) + i):
-//   S_c = [[I, Pi_c2[s,s]], [Pi_c1[s,s], I]]; Gauss-Jordan with partial pivoting (row of max |.|, first
-//   index on ties -- the same pivots and U_kk as the LU of the paper's coupling system) gives log|det S_c|,
-//   its sign and S_c^{-1};
-//   T_c = S_c^{-1} B_c, refined in compensated arithmetic (T = T_hi + T_lo);
-//   Pi_c = Pi_c1[a,a] + Pi_c2[a,a] - sum_u B_c[(u+r) mod q, a] T_c[u, b], 2x4 register tiles per thread.
-template <bool DD>
-__device__ void tree_node(const TreeCtx &c, long long i, double *sm) {
-  const int t = threadIdx.x, NT = blockDim.x;
-  const long long node = (1LL << c.d) - 1 + i;
-  const int r = c.r, q = c.q, Kd = c.Kd, ldk = c.ldk, q2 = 2 * q;
-  const long long K1 = c.K1;
-  const double *P1 = c.Pi1 + (2 * i) * (K1 * (K1 + 1) / 2);
-  const double *P2 = c.Pi1 + (2 * i + 1) * (K1 * (K1 + 1) / 2);
-  double *W = sm;                    // q x 2q  [S | I] -> [I | S^{-1}]
-  double *S0 = W + q * q2;           // q x q
-  double *rowk = S0 + q * q;         // 2q
-  double *rowold = rowk + q2;        // 2q
-  double *colk = rowold + q2;        // q: |U_kk|
-  double *mult = colk + q;           // q: elimination multipliers of the current step
-  double *B = mult + q;              // q x ldk
-  double *Th = B + (long long)q * ldk;
-  double *Tl = Th + (long long)q * ldk;
-  double *R = Tl + (long long)q * ldk;
-  __shared__ int s_zero, s_sign, s_nref, s_p;
-  for (int p = t; p < q * q2; p += NT) {
-    const int a = p / q2, b = p - a * q2;
-    double v;
-    if (b >= q) v = (b - q == a) ? 1.0 : 0.0;
-    else {
-      v = a == b ? 1.0 : 0.0;
-      if (a < r && b >= r) v = P2[pk(Kd + a, Kd + (b - r))];
-      if (a >= r && b < r) v = P1[pk(Kd + a - r, Kd + b)];
-      S0[a * q + b] = v;
-    }
-    W[p] = v;
-  }
-  for (int p = t; p < q * ldk; p += NT) {
-    const int a = p / ldk, b = p - a * ldk;
-    double v = 0.0;
-    if (b < Kd) v = a < r ? P2[pk(Kd + a, b)] : P1[pk(Kd + a - r, b)];
-    B[p] = v; Tl[p] = 0.0;
-  }
-  __syncthreads();
-  // ---------------- Gauss-Jordan with partial pivoting ----------------
-  // q <= 8: warp 0 in registers (gj_regs); larger systems: the whole CTA, 3 barriers per step.
-  if (q <= 8) {
-    if (t < 32) {
-      int sign, zero;
-      gj_regs<8>(W, q, colk, sign, zero);
-      if (t == 0) { s_sign = sign; s_zero = zero; }
-    }
-  } else {
-    int sign = 1, zero = 0;
-    for (int k = 0; k < q; k++) {
-      int p = k; double best = -1.0;
-      if (t < 32) {
-        for (int a = k + t; a < q; a += 32) { const double v = fabs(W[a * q2 + k]); if (v > best) { best = v; p = a; } }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {   // xor butterfly: every lane ends with the same (best, p)
-          const double b2 = __shfl_xor_sync(0xffffffffu, best, o); const int p2 = __shfl_xor_sync(0xffffffffu, p, o);
-          if (b2 > best || (b2 == best && p2 < p)) { best = b2; p = p2; }
-        }
-        if (t == 0) { colk[k] = best; s_p = p; }            // |U_kk| (log det below)
-      }
-      __syncthreads();
-      p = s_p;
-      const double piv = W[p * q2 + k];
-      if (p != k) sign = -sign;
-      if (piv < 0.0) sign = -sign;
-      if (!(piv != 0.0)) zero = 1;
-      for (int j = t; j < q2; j += NT) { rowk[j] = W[p * q2 + j]; rowold[j] = W[k * q2 + j]; }
-      for (int a = t; a < q; a += NT) mult[a] = a == k ? 0.0 : (a == p ? W[k * q2 + k] : W[a * q2 + k]);
-      __syncthreads();
-      const double ip = piv != 0.0 ? 1.0 / piv : 0.0;
-      for (int e = t; e < q * q2; e += NT) {
-        const int a = e / q2, j = e - a * q2;
-        if (a == k) W[e] = rowk[j] * ip;
-        else {
-          const double src = a == p ? rowold[j] : W[e];
-          W[e] = fma(-mult[a] * ip, rowk[j], src);
-        }
-      }
-      __syncthreads();
-    }
-    if (t == 0) { s_sign = sign; s_zero = zero; }
-  }
-  __syncthreads();
-  if (t < 32) {                                 // log|det S_c| = sum_k log|U_kk|, fixed-order warp reduction
-    double la = 0.0, umax = 0.0, umin = 1e300;
-    for (int k = t; k < q; k += 32) { const double u = colk[k]; la += log(u); umax = fmax(umax, u); umin = fmin(umin, u); }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      la += __shfl_xor_sync(0xffffffffu, la, o);
-      umax = fmax(umax, __shfl_xor_sync(0xffffffffu, umax, o));
-      umin = fmin(umin, __shfl_xor_sync(0xffffffffu, umin, o));
-    }
-    if (t == 0) {
-      const bool zero = s_zero != 0;
-      c.node_ld[node] = la;
-      if (zero || s_sign <= 0) { atomicAdd(&c.flags[1], 1); atomicMin(&c.flags[2], (int)node); }
-      // refinement steps: one when the pivot growth ratio is mild, two otherwise (cond(S_c) up to ~1e12)
-      s_nref = (!zero && umax < 1e6 * umin) ? 1 : 2;
-    }
-  }
-  __syncthreads();
-  const bool zero = s_zero != 0;
-  const double *Si = W + q;           // S^{-1}, row stride 2q
-  if (!zero && Kd > 0) {
-    const int qK = q * ldk;
-    for (int e = t; e < qK; e += NT) {                // T_hi = S^{-1} B
-      const int a = e / ldk, col = e - a * ldk;
-      double s = 0.0;
-      for (int j = 0; j < q; j++) s = fma(Si[a * q2 + j], B[j * ldk + col], s);
-      Th[e] = s;
-    }
-    __syncthreads();
-    const int nref = s_nref;
-    for (int it = 0; it < nref; it++) {               // iterative refinement, residual compensated
-      for (int e = t; e < qK; e += NT) {
-        const int a = e / ldk, col = e - a * ldk;
-        if (DD) {
-          Acc2 A = acc2(B[e]);
-          for (int k = 0; k < q; k++) acc_fma_dd(A, -S0[a * q + k], Th[k * ldk + col], Tl[k * ldk + col]);
-          R[e] = acc_val(A);
-        } else {
-          double s = B[e];
-          for (int k = 0; k < q; k++) s = fma(-S0[a * q + k], Th[k * ldk + col] + Tl[k * ldk + col], s);
-          R[e] = s;
-        }
-      }
-      __syncthreads();
-      for (int e = t; e < qK; e += NT) {
-        const int a = e / ldk, col = e - a * ldk;
-        double s = 0.0;
-        for (int j = 0; j < q; j++) s = fma(Si[a * q2 + j], R[j * ldk + col], s);
-        Tl[e] += s;
-      }
-      __syncthreads();
-    }
-    // ---------------- Pi_c, 2x4 register tiles over the packed lower triangle ----------------
-    // Bands of 4 rows; band P holds row tiles I = 2P, 2P+1 with column tiles J = 0..P (tile (I, J) =
-    // rows 2I, 2I+1, columns 4J..4J+3); tiles up to band P: (P+1)(P+2).
-    double *Pc = c.Pic + i * ((long long)Kd * (Kd + 1) / 2);
-    const int NB = (Kd + 3) >> 2;
-    const int ntile = NB * (NB + 1);
-    for (int tile = t; tile < ntile; tile += NT) {
-      int P = (int)((sqrt(4.0 * (double)tile + 1.0) - 1.0) * 0.5);
-      while (P * (P + 1) > tile) P--;
-      while ((P + 1) * (P + 2) <= tile) P++;
-      const int rem = tile - P * (P + 1);
-      const int I = 2 * P + rem / (P + 1), J = rem % (P + 1);
-      const int a0 = 2 * I, b0 = 4 * J;
-      double hs[2][4], ls[2][4];
-#pragma unroll
-      for (int ii = 0; ii < 2; ii++)
-#pragma unroll
-        for (int jj = 0; jj < 4; jj++) {
-          const int a = a0 + ii, b = b0 + jj;
-          double s = 0.0, e = 0.0;
-          if (a < Kd && b <= a) {
-            const long long pp = (long long)a * (a + 1) / 2 + b;   // packed (a, b): same index in both children
-            if (DD) two_sum(__ldg(P1 + pp), __ldg(P2 + pp), s, e); else s = __ldg(P1 + pp) + __ldg(P2 + pp);
-          }
-          hs[ii][jj] = s; ls[ii][jj] = e;
-        }
-      for (int u = 0; u < q; u++) {
-        const int ub = u < q - r ? u + r : u + r - q;
-        const double *bu = B + (long long)ub * ldk + a0;
-        const double *thu = Th + (long long)u * ldk + b0, *tlu = Tl + (long long)u * ldk + b0;
-        double bv[2], th[4], tl[4];
-#pragma unroll
-        for (int x = 0; x < 2; x++) bv[x] = -bu[x];
-#pragma unroll
-        for (int x = 0; x < 4; x++) { th[x] = thu[x]; tl[x] = tlu[x]; }
-#pragma unroll
-        for (int ii = 0; ii < 2; ii++)
-#pragma unroll
-          for (int jj = 0; jj < 4; jj++) {
-            if (DD) {
-              double pr, pe, s2, e2;
-              two_prod(bv[ii], th[jj], pr, pe);
-              two_sum(hs[ii][jj], pr, s2, e2);
-              hs[ii][jj] = s2;
-              ls[ii][jj] += e2 + fma(bv[ii], tl[jj], pe);
-            } else {
-              hs[ii][jj] = fma(bv[ii], th[jj] + tl[jj], hs[ii][jj]);
-            }
-          }
-      }
-#pragma unroll
-      for (int ii = 0; ii < 2; ii++)
-#pragma unroll
-        for (int jj = 0; jj < 4; jj++) {
-          const int a = a0 + ii, b = b0 + jj;
-          if (a < Kd && b <= a) Pc[(long long)a * (a + 1) / 2 + b] = hs[ii][jj] + ls[ii][jj];
-        }
-    }
-  }
-  // persist S, S^{-1}, B, T_hi, T_lo for the solve
-  double *Sg = c.Sst + i * (long long)(2 * q * q + q);
-  for (int p = t; p < q * q; p += NT) {
-    const int a = p / q, b = p - a * q;
-    Sg[p] = S0[p];
-    Sg[q * q + p] = Si[a * q2 + b];
-  }
-  const long long qKd = (long long)q * Kd;
-  double *BTg = c.BT + i * 3LL * qKd;
-  for (long long p = t; p < qKd; p += NT) {
-    const int a = (int)(p / Kd), b = (int)(p - (long long)a * Kd);
-    BTg[p] = B[a * ldk + b];
-    BTg[qKd + p] = Th[a * ldk + b];
-    BTg[2 * qKd + p] = Tl[a * ldk + b];
-  }
-  __syncthreads();
+__device__ __forceinline__ GlobalPi global_pi(const TreeCtx &c, long long i) {
+  const long long K1 = c.K1, sz = K1 * (K1 + 1) / 2;
+  GlobalPi g; g.P1 = c.Pi1 + (2 * i) * sz; g.P2 = c.Pi1 + (2 * i + 1) * sz; g.Kd = c.Kd;
+  return g;
 }
 
 template <bool DD>
 __global__ void __launch_bounds__(TT, 3) k_tree_factor(TreeCtx c) {
   extern __shared__ double sm[];
-  tree_node<DD>(c, c.i0 + blockIdx.x, sm);
+  const long long i = c.i0 + blockIdx.x;
+  tree_node<DD>(c, i, sm, global_pi(c, i));
 }
 
 // Levels with many small nodes: 128-thread CTAs (6 per SM) -- finer barrier domains, more independent nodes
@@ -452,7 +179,8 @@ __global__ void __launch_bounds__(TT, 3) k_tree_factor(TreeCtx c) {
 template <bool DD>
 __global__ void __launch_bounds__(TT / 2, 6) k_tree_factor_narrow(TreeCtx c) {
   extern __shared__ double sm[];
-  tree_node<DD>(c, c.i0 + blockIdx.x, sm);
+  const long long i = c.i0 + blockIdx.x;
+  tree_node<DD>(c, i, sm, global_pi(c, i));
 }
 
 // log det partial = leaves (left to right), then internal nodes of depth >= tsplit by depth kappa-1..tsplit,
@@ -533,6 +261,25 @@ hodlr_status hodlr_leaf_alloc(hodlr_s *h) {
   return HODLR_OK;
 }
 
+hodlr_status hodlr_leaf_pair_mma(hodlr_s *h, int K, const TreeCtx &tc, bool *used);
+
+static int tree_plain_from() {     // debug/experiment switch: depths >= HODLR_TREE_PLAIN_FROM use plain double
+  static int plain_from = -1;
+  if (plain_from < 0) { const char *ev = getenv("HODLR_TREE_PLAIN_FROM"); plain_from = ev ? atoi(ev) : 1 << 20; }
+  return plain_from;
+}
+
+static TreeCtx tree_ctx(hodlr_s *h, int d, long long i0) {
+  const DepthTab &dt = h->dt;
+  TreeCtx tc;
+  tc.d = d; tc.i0 = i0; tc.r = dt.rdep[d + 1]; tc.q = 2 * tc.r; tc.Kd = dt.Kdim[d]; tc.K1 = dt.Kdim[d + 1];
+  tc.ldk = (tc.Kd + 3) & ~3; tc.dd = d < tree_plain_from();
+  tc.Pi1 = h->Pipool + dt.piOff[d + 1]; tc.Pic = h->Pipool + dt.piOff[d];
+  tc.Sst = h->Spool + dt.nodeS[d]; tc.BT = h->BTpool + dt.nodeBT[d];
+  tc.node_ld = h->node_ld; tc.flags = h->dflags;
+  return tc;
+}
+
 hodlr_status hodlr_factor_impl(hodlr_s *h) {
   const int kappa = h->kappa;
   DepthTab &dt = h->dt;
@@ -566,8 +313,20 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
   // ---- leaves ----
   HCUDA(cudaStreamWaitEvent(h->st, h->ev_chol, 0));     // leaf Cholesky issued during the build
   ph_begin(h, PH_LEAF);
-  bool fast = false;
-  {
+  bool fast = false, paired = false;
+  // HODLR_LEAF_PAIR=1: leaves fused with the depth-(kappa-1) coupling systems (k_leaf_pair).  Measured slower
+  // at config 3 (2.52 ms vs 1.40 + 0.43 ms): at one CTA per SM the node phase cannot overlap the DMMA work.
+  static int no_pair = -1;
+  if (no_pair < 0) { const char *ev = getenv("HODLR_LEAF_PAIR"); no_pair = ev && atoi(ev) ? 0 : 1; }
+  if (kappa >= 1 && !no_pair) {     // leaves fused with the depth-(kappa-1) coupling systems
+    long long i0, cnt;
+    hodlr_own_nodes(h, kappa - 1, &i0, &cnt);
+    const TreeCtx tc = tree_ctx(h, kappa - 1, i0);
+    hodlr_status fs = hodlr_leaf_pair_mma(h, K, tc, &paired);
+    if (fs != HODLR_OK) return fs;
+    fast = paired;
+  }
+  if (!fast) {
     hodlr_status fs = hodlr_leaf_factor_mma(h, K, h->Pipool + dt.piOff[kappa], &fast);   // needs the Cholesky kernel
     if (fs != HODLR_OK) return fs;
   }
@@ -614,10 +373,7 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
     HCUDA(cudaFuncSetAttribute(k_tree_factor_narrow<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tree_smem_max));
     tree_attr = tree_smem_max;
   }
-  // debug/experiment switch: depths >= HODLR_TREE_PLAIN_FROM use plain double (default: none)
-  static int plain_from = -1;
-  if (plain_from < 0) { const char *ev = getenv("HODLR_TREE_PLAIN_FROM"); plain_from = ev ? atoi(ev) : 1 << 20; }
-  for (int d = kappa - 1; d >= 0; d--) {
+  for (int d = paired ? kappa - 2 : kappa - 1; d >= 0; d--) {
     if (d + 1 == h->tsplit && h->nranks > 1) {     // every rank gets the Pi of all depth-t subtree roots
       const long long Kt = dt.Kdim[d + 1], sz = Kt * (Kt + 1) / 2;
       double *base = h->Pipool + dt.piOff[d + 1];
@@ -626,12 +382,7 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
     }
     long long i0, cnt;
     hodlr_own_nodes(h, d, &i0, &cnt);
-    TreeCtx tc;
-    tc.d = d; tc.i0 = i0; tc.r = dt.rdep[d + 1]; tc.q = 2 * tc.r; tc.Kd = dt.Kdim[d]; tc.K1 = dt.Kdim[d + 1];
-    tc.ldk = (tc.Kd + 3) & ~3; tc.dd = d < plain_from;
-    tc.Pi1 = h->Pipool + dt.piOff[d + 1]; tc.Pic = h->Pipool + dt.piOff[d];
-    tc.Sst = h->Spool + dt.nodeS[d]; tc.BT = h->BTpool + dt.nodeBT[d];
-    tc.node_ld = h->node_ld; tc.flags = h->dflags;
+    const TreeCtx tc = tree_ctx(h, d, i0);
     const size_t smem = sizeof(double) * (size_t)tree_smem_doubles(tc.q, tc.ldk);
     const bool narrow = cnt >= 4 * 148 && tc.q <= 16;
     if (narrow) {

@@ -100,3 +100,26 @@ def test_loglik_sweep_matches_single_settings(hb):
     res = run_virtual_ranks(4, lambda r, d: hb.gp_loglik_sweep(xd, yd, cfg.kernel, th, sg, cfg.leaf, 1e-12, dist=d))
     for v in res:
         np.testing.assert_array_equal(v, vals)
+
+
+@pytest.mark.parametrize("flag", ["HODLR_LEAF_PAIR", "HODLR_CHOL_AFTER_ACA"])
+def test_alternate_paths_match(hb, flag):
+    """The opt-in variants (fused leaf pairs + deepest tree level; Cholesky after the ACA) give the same
+    factorization as the default path: run in a subprocess with the switch set."""
+    import subprocess, sys, os, json
+    code = ("import json,sys,torch; sys.path.insert(0,'.');"
+            "from paper_1403_6015_b200 import inputs; import paper_1403_6015_b200.hodlr as hb;"
+            "cfg=inputs.scaled(inputs.CONFIGS['cfg3'],1<<15); x=inputs.points(cfg); y=inputs.rhs(cfg);"
+            "g=hb.HODLR(torch.from_numpy(x).cuda(),cfg.kernel,cfg.theta,cfg.sigma2,cfg.leaf,1e-12).factor();"
+            "print(json.dumps([g.logdet(), g.solve(torch.from_numpy(y).cuda()).cpu().tolist()]))")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for env in ({}, {flag: "1"}):
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, **env}, capture_output=True,
+                           text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    (ld0, x0), (ld1, x1) = outs
+    x0 = np.array(x0); x1 = np.array(x1)
+    assert abs(ld1 - ld0) <= 1e-12 * abs(ld0)
+    assert np.linalg.norm(x1 - x0) <= 1e-10 * np.linalg.norm(x0)
