@@ -49,6 +49,7 @@ struct SolveCtx {
   int tree_warps;           // warps per CTA that take tree-up nodes (scratch must fit)
   unsigned long long *stamps;   // HODLR_TRACE: %globaltimer after each phase (block 0), or NULL
   int bulk;                 // leaf staging by bulk copies (all column segments 16-byte aligned)
+  int stage_e;              // stage the panel E_l in shared memory (else read it from global memory)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -255,7 +256,7 @@ __device__ void leaf_up_phase(const SolveCtx &c, double *sX, double *sE, LeafSme
   for (int q = t; q < K; q += LT) S.colsrc[0][q] = leaf_colsrc(c, c.ninternal + leaf, q);
   __syncthreads();
   if (BULK) { zero_e_pad(c, leaf, S.colsrc[0], sE); bulk_x(c, leaf, sX, &S.barX); bulk_e(c, leaf, S.colsrc[0], sE, &S.barE); }
-  else { issue_x(c, leaf, sX); issue_e(c, leaf, S.colsrc[0], sE); }
+  else { issue_x(c, leaf, sX); if (c.stage_e) issue_e(c, leaf, S.colsrc[0], sE); else cp_commit(); }
   for (; leaf < end; leaf += gridDim.x) {
     const long long nxt = leaf + gridDim.x;
     const long long id = c.ninternal + leaf, lo = c.lo[id];
@@ -282,9 +283,17 @@ __device__ void leaf_up_phase(const SolveCtx &c, double *sX, double *sE, LeafSme
     if (lane == 0) S.red[2 * VMAX + warp] = hs;
     double *g = c.V + c.dt->nodeV[c.kappa] + leaf * (long long)K;
     for (int q = warp; q < K; q += NWL) {      // g = E^T v: warp per column, lanes over rows
-      const double *e = sE + q * R;
       double s2 = 0.0;
-      for (int i = lane; i < R; i += 32) s2 = fma(e[i], S.red[i], s2);
+      if (c.stage_e) {
+        const double *e = sE + q * R;
+        for (int i = lane; i < R; i += 32) s2 = fma(e[i], S.red[i], s2);
+      } else {
+        const int src = S.colsrc[cur][q];
+        if (src >= 0) {
+          const double *e = c.Xh + (long long)src * c.n + lo;
+          for (int i = lane; i < m; i += 32) s2 = fma(e[i], S.red[i], s2);
+        }
+      }
       s2 = warp_sum(s2);
       if (lane == 0) g[q] = s2;
     }
@@ -294,7 +303,7 @@ __device__ void leaf_up_phase(const SolveCtx &c, double *sX, double *sE, LeafSme
       for (int w = 0; w < NWL; w++) h += S.red[2 * VMAX + w];
       c.hv[2 * id] = h; c.hv[2 * id + 1] = 0.0;
     }
-    if (nxt < end) {
+    if (nxt < end && (BULK || c.stage_e)) {
       if (BULK) { zero_e_pad(c, nxt, S.colsrc[cur ^ 1], sE); bulk_e(c, nxt, S.colsrc[cur ^ 1], sE, &S.barE); }
       else issue_e(c, nxt, S.colsrc[cur ^ 1], sE);
     } else if (!BULK) cp_commit();
@@ -316,7 +325,7 @@ __device__ void leaf_down_phase(const SolveCtx &c, double *sX, double *sE, LeafS
   for (int q = t; q < K; q += LT) S.colsrc[0][q] = leaf_colsrc(c, c.ninternal + leaf, q);
   __syncthreads();
   if (BULK) { zero_e_pad(c, leaf, S.colsrc[0], sE); bulk_e(c, leaf, S.colsrc[0], sE, &S.barE); bulk_x(c, leaf, sX, &S.barX); }
-  else { issue_e(c, leaf, S.colsrc[0], sE); issue_x(c, leaf, sX); }
+  else { if (c.stage_e) issue_e(c, leaf, S.colsrc[0], sE); else cp_commit(); issue_x(c, leaf, sX); }
   for (; leaf < end; leaf += gridDim.x) {
     const long long nxt = leaf + gridDim.x;
     const long long id = c.ninternal + leaf, lo = c.lo[id];
@@ -331,12 +340,19 @@ __device__ void leaf_down_phase(const SolveCtx &c, double *sX, double *sE, LeafS
       const int i = w4 % R, h = w4 / R;
       const int q0 = (K * h) / 4, q1 = (K * (h + 1)) / 4;
       double s2 = 0.0;
-      for (int q = q0; q < q1; q++) s2 = fma(sE[q * R + i], S.sw[q], s2);
+      if (c.stage_e) {
+        for (int q = q0; q < q1; q++) s2 = fma(sE[q * R + i], S.sw[q], s2);
+      } else if (i < m) {
+        for (int q = q0; q < q1; q++) {
+          const int src = S.colsrc[cur][q];
+          if (src >= 0) s2 = fma(c.Xh[(long long)src * c.n + lo + i], S.sw[q], s2);
+        }
+      }
       S.red[w4] = s2;
     }
     __syncthreads();
     for (int i = t; i < R; i += LT) S.sb[i] += (S.red[i] + S.red[R + i]) + (S.red[2 * R + i] + S.red[3 * R + i]);
-    if (nxt < end) {                           // E is free (barrier above)
+    if (nxt < end && (BULK || c.stage_e)) {    // E is free (barrier above)
       if (BULK) { zero_e_pad(c, nxt, S.colsrc[cur ^ 1], sE); bulk_e(c, nxt, S.colsrc[cur ^ 1], sE, &S.barE); }
       else issue_e(c, nxt, S.colsrc[cur ^ 1], sE);
     } else if (!BULK) cp_commit();
@@ -623,10 +639,13 @@ hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_on
     static_smem = (int)fa.sharedSizeBytes;
   }
   const size_t avail = ((size_t)maxsm - (size_t)static_smem - 256) / sizeof(double);
-  const size_t need = std::max(leaf_db, (size_t)c.tree_scratch);
+  const size_t x_db = 64 * (size_t)(h->ltiles * (h->ltiles + 1) / 2);
+  c.stage_e = leaf_db <= avail ? 1 : 0;      // a panel too wide for shared memory is read from global memory
+  const size_t stage_db = c.stage_e ? leaf_db : x_db;
+  const size_t need = std::max(stage_db, (size_t)c.tree_scratch);
   if (need > avail)
-    return hodlr_set_error(HODLR_EINVAL, "solve: leaf panel (%d x %d) or coupling size %zu exceeds shared memory", R, c.K, qmax);
-  const size_t dsm_d = std::min(avail, std::max(leaf_db, (size_t)NWL * (size_t)c.tree_scratch));
+    return hodlr_set_error(HODLR_EINVAL, "solve: leaf inverse (%d rows) or coupling size %zu exceeds shared memory", R, qmax);
+  const size_t dsm_d = std::min(avail, std::max(stage_db, (size_t)NWL * (size_t)c.tree_scratch));
   c.tree_warps = (int)std::min<size_t>(NWL, dsm_d / (size_t)c.tree_scratch);
   const size_t dsm = sizeof(double) * dsm_d;
   static int trace = -1;
@@ -651,7 +670,7 @@ hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_on
   }
   static int bulk_env = -1;      // bulk (TMA-engine) staging measured slower than per-thread cp.async here
   if (bulk_env < 0) { const char *ev = getenv("HODLR_SOLVE_BULK"); bulk_env = ev && atoi(ev) ? 1 : 0; }
-  c.bulk = h->bulk_ok && bulk_env;
+  c.bulk = h->bulk_ok && bulk_env && c.stage_e;
   const int grid = nsm;                                   // one persistent CTA per SM
   auto launch = [&](Phases ph) -> hodlr_status {
     void *args[] = {(void *)&c, (void *)&ph};
