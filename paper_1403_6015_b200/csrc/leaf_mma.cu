@@ -284,7 +284,9 @@ __global__ void __launch_bounds__(NTH, 2) k_leaf_chol(LeafMmaCtx c) {
 constexpr int ZTH = 512;
 constexpr int ZW = ZTH / 32;
 
-template <int P>
+// XG (wide panels, K up to ~208): X tiles are read straight from global memory (L2) as DMMA operands and
+// only Z lives in shared memory.
+template <int P, bool XG = false>
 __global__ void __launch_bounds__(ZTH, 1) k_leaf_zsyrk(LeafMmaCtx c) {
   constexpr int T = P / 8;
   constexpr int NTILE = T * (T + 1) / 2;
@@ -292,16 +294,16 @@ __global__ void __launch_bounds__(ZTH, 1) k_leaf_zsyrk(LeafMmaCtx c) {
   extern __shared__ double sm[];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int K = c.K, Kp = c.Kp, Kc = Kp / 8, Kz = c.Kz;
-  double *sX = sm;                              // NTILE * 64: tiles of X = L^{-1}
-  double *sZ = sX + NTILE * 64;                 // Kz * LDR (column-major)
-  long long *colsrc = (long long *)(sZ + (long long)Kz * LDR);   // Kz
   const long long leaf = c.leaf0 + blockIdx.x;
+  const double *sX = XG ? c.Lf + leaf * c.lstride : sm;   // NTILE * 64: tiles of X = L^{-1}
+  double *sZ = XG ? sm : sm + NTILE * 64;       // Kz * LDR (column-major)
+  long long *colsrc = (long long *)(sZ + (long long)Kz * LDR);   // Kz
   const long long id = c.ninternal + leaf, lo = c.lo[id];
   const int m = (int)(c.hi[id] - lo);
-  {
+  if (!XG) {
     const double *Lg = c.Lf + leaf * c.lstride;
     for (int p = t; p < NTILE * 32; p += ZTH) {
-      unsigned sa = (unsigned)__cvta_generic_to_shared(sX + 2 * p);
+      unsigned sa = (unsigned)__cvta_generic_to_shared(sm + 2 * p);
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(sa), "l"(Lg + 2 * p));
     }
   }
@@ -601,23 +603,28 @@ hodlr_status hodlr_leaf_factor_mma(hodlr_s *h, int K, double *Pi_leaf, bool *use
   const int P = leaf_P(h);
   if (P == 0 || !h->chol_done) return HODLR_OK;
   const int Kp = (K + 7) / 8 * 8;
-  if (Kp / 8 > ZW) return HODLR_OK;                  // one 8-column tile of Z per warp
+  if (Kp / 8 > 2 * ZW) return HODLR_OK;              // <= 2 8-column tiles of Z per warp (shared memory decides)
   const int Kz = (K + 15) / 16 * 16;
+  if (Kz / 16 > 16) return HODLR_OK;                 // SYRK block tables cover 16 x 16 blocks
   const int T = P / 8, NTILE = T * (T + 1) / 2, LDR = P + 4;
-  const size_t smem = sizeof(double) * ((size_t)NTILE * 64 + (size_t)Kz * LDR + Kz);
   int maxsm = 0;
   HCUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
+  size_t smem = sizeof(double) * ((size_t)NTILE * 64 + (size_t)Kz * LDR + Kz);
+  bool wide = false;                                 // X from global memory when X + Z do not fit
+  if (smem + 64 > (size_t)maxsm) { smem = sizeof(double) * ((size_t)Kz * LDR + Kz); wide = true; }
   if (smem + 64 > (size_t)maxsm) return HODLR_OK;
   hodlr_status ts = leaf_tables();
   if (ts != HODLR_OK) return ts;
   LeafMmaCtx c = leaf_ctx(h, K, Pi_leaf);
-  if (P == 64) {
-    HCUDA(cudaFuncSetAttribute(k_leaf_zsyrk<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_leaf_zsyrk<64><<<(int)(h->nleaves >> h->tsplit), ZTH, smem, h->st>>>(c);
-  } else {
-    HCUDA(cudaFuncSetAttribute(k_leaf_zsyrk<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_leaf_zsyrk<128><<<(int)(h->nleaves >> h->tsplit), ZTH, smem, h->st>>>(c);
-  }
+  const int grid = (int)(h->nleaves >> h->tsplit);
+#define LAUNCH_ZS(PP, XGV)                                                                                     \
+  do {                                                                                                        \
+    HCUDA(cudaFuncSetAttribute(k_leaf_zsyrk<PP, XGV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    k_leaf_zsyrk<PP, XGV><<<grid, ZTH, smem, h->st>>>(c);                                                      \
+  } while (0)
+  if (P == 64) { if (wide) LAUNCH_ZS(64, true); else LAUNCH_ZS(64, false); }
+  else { if (wide) LAUNCH_ZS(128, true); else LAUNCH_ZS(128, false); }
+#undef LAUNCH_ZS
   HLAUNCH(h, "k_leaf_zsyrk");
   *used = true;
   return HODLR_OK;
