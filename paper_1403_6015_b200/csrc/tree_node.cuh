@@ -20,7 +20,7 @@ struct TreeCtx {
 
 // Shared-memory footprint of one node (doubles), see tree_node().
 __host__ __device__ __forceinline__ long long tree_smem_doubles(int q, int ldk) {
-  return 3LL * q * q + 6LL * q + 4LL * q * ldk;
+  return 5LL * q * q + 6LL * q + 4LL * q * ldk;
 }
 
 // Gauss-Jordan with partial pivoting on [S | I] (q <= QB rows, one row per lane, in registers): row swaps and
@@ -103,11 +103,12 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
   double *rowold = rowk + q2;        // 2q
   double *colk = rowold + q2;        // q: |U_kk|
   double *mult = colk + q;           // q: elimination multipliers of the current step
-  double *B = mult + q;              // q x ldk
+  double *W2 = mult + q;             // q x 2q: Gauss-Jordan ping-pong buffer
+  double *B = W2 + q * q2;           // q x ldk
   double *Th = B + (long long)q * ldk;
   double *Tl = Th + (long long)q * ldk;
   double *R = Tl + (long long)q * ldk;
-  __shared__ int s_zero, s_sign, s_nref, s_p;
+  __shared__ int s_zero, s_sign, s_nref;
   for (int p = t; p < q * q2; p += NT) {
     const int a = p / q2, b = p - a * q2;
     double v;
@@ -136,37 +137,37 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
       if (t == 0) { s_sign = sign; s_zero = zero; }
     }
   } else {
+    // ping-pong buffers (read Wa, write Wb), one barrier per step; every warp finds the pivot itself
+    double *Wa = W, *Wb = W2;
+    const int lane = t & 31;
     int sign = 1, zero = 0;
     for (int k = 0; k < q; k++) {
       int p = k; double best = -1.0;
-      if (t < 32) {
-        for (int a = k + t; a < q; a += 32) { const double v = fabs(W[a * q2 + k]); if (v > best) { best = v; p = a; } }
+      for (int a = k + lane; a < q; a += 32) { const double v = fabs(Wa[a * q2 + k]); if (v > best) { best = v; p = a; } }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {   // xor butterfly: every lane ends with the same (best, p)
-          const double b2 = __shfl_xor_sync(0xffffffffu, best, o); const int p2 = __shfl_xor_sync(0xffffffffu, p, o);
-          if (b2 > best || (b2 == best && p2 < p)) { best = b2; p = p2; }
-        }
-        if (t == 0) { colk[k] = best; s_p = p; }            // |U_kk| (log det below)
+      for (int o = 16; o > 0; o >>= 1) {     // xor butterfly: every lane ends with the same (best, p)
+        const double b2 = __shfl_xor_sync(0xffffffffu, best, o); const int p2 = __shfl_xor_sync(0xffffffffu, p, o);
+        if (b2 > best || (b2 == best && p2 < p)) { best = b2; p = p2; }
       }
-      __syncthreads();
-      p = s_p;
-      const double piv = W[p * q2 + k];
-      if (p != k) sign = -sign;
-      if (piv < 0.0) sign = -sign;
-      if (!(piv != 0.0)) zero = 1;
-      for (int j = t; j < q2; j += NT) { rowk[j] = W[p * q2 + j]; rowold[j] = W[k * q2 + j]; }
-      for (int a = t; a < q; a += NT) mult[a] = a == k ? 0.0 : (a == p ? W[k * q2 + k] : W[a * q2 + k]);
-      __syncthreads();
+      const double piv = Wa[p * q2 + k];
+      if (t == 0) {
+        colk[k] = best;                        // |U_kk| (log det below)
+        if (p != k) sign = -sign;
+        if (piv < 0.0) sign = -sign;
+        if (!(piv != 0.0)) zero = 1;
+      }
       const double ip = piv != 0.0 ? 1.0 / piv : 0.0;
+      const double *prow = Wa + p * q2;
       for (int e = t; e < q * q2; e += NT) {
         const int a = e / q2, j = e - a * q2;
-        if (a == k) W[e] = rowk[j] * ip;
+        if (a == k) Wb[e] = prow[j] * ip;
         else {
-          const double src = a == p ? rowold[j] : W[e];
-          W[e] = fma(-mult[a] * ip, rowk[j], src);
+          const int sa = a == p ? k : a;       // rows k and p swap before the elimination
+          Wb[e] = fma(-Wa[sa * q2 + k] * ip, prow[j], Wa[sa * q2 + j]);
         }
       }
       __syncthreads();
+      double *tmp = Wa; Wa = Wb; Wb = tmp;
     }
     if (t == 0) { s_sign = sign; s_zero = zero; }
   }
@@ -190,7 +191,7 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
   }
   __syncthreads();
   const bool zero = s_zero != 0;
-  const double *Si = W + q;           // S^{-1}, row stride 2q
+  const double *Si = ((q > 8 && (q & 1)) ? W2 : W) + q;   // S^{-1} (after the last ping-pong step), row stride 2q
   if (!zero && Kd > 0) {
     const int qK = q * ldk;
     for (int e = t; e < qK; e += NT) {                // T_hi = S^{-1} B
