@@ -23,7 +23,7 @@ namespace cg = cooperative_groups;
 
 namespace {
 
-constexpr int LT = 512;           // threads per CTA
+constexpr int LT = 256;           // threads per CTA (two CTAs per SM)
 constexpr int NWL = LT / 32;      // warps per CTA
 constexpr int VMAX = 8 * 32;      // leaf rows handled (leaf_max < 2 leaf <= 256)
 
@@ -234,9 +234,10 @@ __device__ void tri_mvt(const double *X, int T, const double *in, double *out, d
   __syncthreads();
 }
 
+constexpr int KMAX_SOLVE = 512;   // ancestor columns per leaf handled by the solve
 struct LeafSmem {
-  double sb[VMAX], su[VMAX], red[4 * VMAX], sw[1024];
-  int colsrc[2][1024];
+  double sb[VMAX], su[VMAX], red[4 * VMAX], sw[KMAX_SOLVE];
+  int colsrc[2][KMAX_SOLVE];
   unsigned long long barX, barE;
 };
 
@@ -526,7 +527,7 @@ __device__ void tree_down_node(const SolveCtx &c, int d, long long i, int lane) 
 // ---------------------------------------------------------------------------------------------
 // the persistent cooperative kernel
 // ---------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(LT, 1) k_solve(SolveCtx c0, Phases ph) {
+__global__ void __launch_bounds__(LT, 2) k_solve(SolveCtx c0, Phases ph) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double sm[];
   __shared__ LeafSmem S;
@@ -596,8 +597,8 @@ __global__ void k_pack_rows(const double *xsorted, long long lo, long long m, do
 hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_only) {
   const int kappa = h->kappa;
   DepthTab &dt = h->dt;
-  if (h->leaf_max > VMAX || dt.Kdim[kappa] > 1024)
-    return hodlr_set_error(HODLR_EINVAL, "solve: leaf size %d > %d or K > 1024", h->leaf_max, VMAX);
+  if (h->leaf_max > VMAX || dt.Kdim[kappa] > KMAX_SOLVE)
+    return hodlr_set_error(HODLR_EINVAL, "solve: leaf size %d > %d or K = %d > %d", h->leaf_max, VMAX, dt.Kdim[kappa], KMAX_SOLVE);
   if (!h->Vpool) {
     long long vTot = 0, tTot = 0;
     for (int e = 0; e <= kappa; e++) { dt.nodeV[e] = vTot; vTot += (1LL << e) * (long long)dt.Kdim[e]; }
@@ -640,12 +641,17 @@ hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_on
   }
   const size_t avail = ((size_t)maxsm - (size_t)static_smem - 256) / sizeof(double);
   const size_t x_db = 64 * (size_t)(h->ltiles * (h->ltiles + 1) / 2);
-  c.stage_e = leaf_db <= avail ? 1 : 0;      // a panel too wide for shared memory is read from global memory
+  // Stage only X (68 KB at p = 128) and read E from global memory: two CTAs per SM overlap one leaf's loads with
+  // the other's arithmetic (measured faster than staging X + E at one CTA per SM).  HODLR_SOLVE_STAGE_E=1 stages E.
+  static int stage_env = -1;
+  if (stage_env < 0) { const char *ev = getenv("HODLR_SOLVE_STAGE_E"); stage_env = ev && atoi(ev) ? 1 : 0; }
+  c.stage_e = (stage_env && leaf_db <= avail) ? 1 : 0;
   const size_t stage_db = c.stage_e ? leaf_db : x_db;
   const size_t need = std::max(stage_db, (size_t)c.tree_scratch);
   if (need > avail)
     return hodlr_set_error(HODLR_EINVAL, "solve: leaf inverse (%d rows) or coupling size %zu exceeds shared memory", R, qmax);
-  const size_t dsm_d = std::min(avail, std::max(stage_db, (size_t)NWL * (size_t)c.tree_scratch));
+  const size_t half = c.stage_e ? avail : std::min(avail, (size_t)(((size_t)maxsm / 2 - (size_t)static_smem - 1024) / sizeof(double)));
+  const size_t dsm_d = std::max(stage_db, std::min(half, (size_t)NWL * (size_t)c.tree_scratch));
   c.tree_warps = (int)std::min<size_t>(NWL, dsm_d / (size_t)c.tree_scratch);
   const size_t dsm = sizeof(double) * dsm_d;
   static int trace = -1;
@@ -671,7 +677,10 @@ hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_on
   static int bulk_env = -1;      // bulk (TMA-engine) staging measured slower than per-thread cp.async here
   if (bulk_env < 0) { const char *ev = getenv("HODLR_SOLVE_BULK"); bulk_env = ev && atoi(ev) ? 1 : 0; }
   c.bulk = h->bulk_ok && bulk_env && c.stage_e;
-  const int grid = nsm;                                   // one persistent CTA per SM
+  int per_sm = 0;
+  HCUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve, LT, dsm));
+  if (per_sm < 1) return hodlr_set_error(HODLR_EINVAL, "solve: kernel does not fit on an SM");
+  const int grid = nsm * std::min(per_sm, 2);             // persistent: every CTA resident (cooperative launch)
   auto launch = [&](Phases ph) -> hodlr_status {
     void *args[] = {(void *)&c, (void *)&ph};
     HCUDA(cudaLaunchCooperativeKernel((const void *)k_solve, dim3(grid), dim3(LT), args, dsm, h->st));
