@@ -512,7 +512,7 @@ static cudaError_t plan_create(AcaPlan *P, const hodlr_s *h) {
     bigidx[b] = P->nbig++;
     for (int side = 0; side < 2; side++) {
       long long m = side == 0 ? m2 : m1;
-      long long chunk = (m + 127) / 128;
+      long long chunk = (m + ACA_CHUNKS_PER_SIDE - 1) / ACA_CHUNKS_PER_SIDE;
       chunk = ((chunk + ACA_TILE - 1) / ACA_TILE) * ACA_TILE;
       if (chunk < ACA_BIG_CHUNK) chunk = ACA_BIG_CHUNK;
       int q = 0;

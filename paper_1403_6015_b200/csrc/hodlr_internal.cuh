@@ -22,7 +22,12 @@
 #define ACA_GSZ (ACA_MAXCAP * (ACA_MAXCAP + 1) / 2)   // packed Gram matrix of one factor side
 #define ACA_SUB 256        // threads per ACA CTA == sub-tile width
 #define ACA_FUSED_MAX 4096 // blocks with both sides <= this run the fused single-CTA ACA
-#define ACA_BIG_CHUNK 2048 // minimum chunk per CTA for the step-synchronous big blocks
+#ifndef ACA_BIG_CHUNK
+#define ACA_BIG_CHUNK 8192 // minimum chunk per CTA for the step-synchronous big blocks (measured optimum)
+#endif
+#ifndef ACA_CHUNKS_PER_SIDE
+#define ACA_CHUNKS_PER_SIDE 32    // max chunks (CTAs, records) per block side
+#endif
 
 // ----------------------------------------------------------------------------------------------
 // Covariance functions, Table I; C_ij = k(x_i - x_j) + s2 [i == j]
