@@ -107,10 +107,12 @@ static void res_acquire(hodlr_s *h) {
     cudaEventCreate(&r.ev0); cudaEventCreate(&r.ev1);
     cudaEventCreateWithFlags(&r.ev_fork, cudaEventDisableTiming); cudaEventCreateWithFlags(&r.ev_join, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&r.ev_chol, cudaEventDisableTiming);
-    cudaStreamCreateWithFlags(&r.st2, cudaStreamNonBlocking);
-    cudaStreamCreateWithFlags(&r.st3, cudaStreamNonBlocking);
     int lo_pri = 0, hi_pri = 0;
     cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri);
+    static int fused_hi = -1;    // HODLR_FUSED_PRIORITY=1: the fused small-block ACA at high priority (measured slower)
+    if (fused_hi < 0) { const char *ev = getenv("HODLR_FUSED_PRIORITY"); fused_hi = ev ? atoi(ev) : 0; }
+    cudaStreamCreateWithPriority(&r.st2, cudaStreamNonBlocking, fused_hi ? hi_pri : lo_pri);
+    cudaStreamCreateWithFlags(&r.st3, cudaStreamNonBlocking);
     cudaStreamCreateWithPriority(&r.sthi, cudaStreamNonBlocking, hi_pri);
     cudaEventCreateWithFlags(&r.ev_hi, cudaEventDisableTiming);
     for (int p = 0; p < PH_N; p++) for (int j = 0; j < 2; j++) cudaEventCreate(&r.ph_ev[p][j]);

@@ -20,8 +20,12 @@
 #define ACA_MAXCAP 64      // hard ceiling on the ACA rank cap (records/state are sized by it)
 #define ACA_RECW (4 + ACA_MAXCAP)
 #define ACA_GSZ (ACA_MAXCAP * (ACA_MAXCAP + 1) / 2)   // packed Gram matrix of one factor side
+#ifndef ACA_SUB
 #define ACA_SUB 256        // threads per ACA CTA == sub-tile width
+#endif
+#ifndef ACA_FUSED_MAX
 #define ACA_FUSED_MAX 4096 // blocks with both sides <= this run the fused single-CTA ACA
+#endif
 #ifndef ACA_BIG_CHUNK
 #define ACA_BIG_CHUNK 8192 // minimum chunk per CTA for the step-synchronous big blocks (measured optimum)
 #endif

@@ -65,7 +65,7 @@ def load(build_if_missing: bool = True):
     with _lock:
         if _lib is not None:
             return _lib
-        path = os.environ.get("HODLR_LIB", _build.LIB)     # HODLR_LIB: an alternative build (experiments)
+        path = os.environ.get("HODLR_LIB") or _build.LIB   # HODLR_LIB: an alternative build (experiments)
         if not os.path.exists(path):
             if not build_if_missing:
                 raise RuntimeError(f"{path} missing; run python -m paper_1403_6015_b200.build")
