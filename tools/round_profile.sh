@@ -15,4 +15,5 @@ for spec in k_aca_pass:12 k_leaf_zsyrk:0 k_leaf_chol:0 k_tree_factor:0 k_solve:0
     -o $out/$k python tools/prof_step.py cfg3 1 > $out/$k.log 2>&1
   ncu -i $out/$k.ncu-rep --page raw --csv > $out/$k.raw.csv 2>/dev/null
 done
+python tools/ncu_summary.py $out "${2:-1}" "ncu --set full --clock-control none, one launch each (tools/round_profile.sh, cfg3 n=2^20 step)" || true
 ls $out
