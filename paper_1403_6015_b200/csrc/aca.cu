@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(ACA_SUB, 2) k_aca_pass(const AcaCtx *__restric
   const long long piv = ROW ? __ldcg(&st->ipiv) : __ldcg(&st->jpiv);
   const double pivval = ROW ? 1.0 : __ldcg(&st->pivval);
   if (done) return;
-  const long long n = c.n;
+  const long long n = c.n, ldx = c.ldx;
   const long long lo1 = it.lo1, m1 = it.m1, lo2 = it.lo2, m2 = it.m2;
   const int e = it.e;
   double *slot = c.Xh + it.slot_off;
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(ACA_SUB, 2) k_aca_pass(const AcaCtx *__restric
   __shared__ double s_abs[ACA_SUB / 32], s_val[ACA_SUB / 32], s_n2[ACA_SUB / 32];
   __shared__ long long s_idx[ACA_SUB / 32];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  for (int l = t; l < k; l += ACA_SUB) coef[l] = slot[(long long)l * n + pg];
+  for (int l = t; l < k; l += ACA_SUB) coef[l] = slot[(long long)l * ldx + pg];
   __syncthreads();
   // dots F_l . a: for each batch of 4 columns the 4 per-lane partials are reduced over the warp by a transposed
   // butterfly (6 shuffles); lane L then holds column l0 + ((L >> 3) & 3) and keeps it when batch l0 / 4 is
@@ -123,12 +123,12 @@ __global__ void __launch_bounds__(ACA_SUB, 2) k_aca_pass(const AcaCtx *__restric
   double w0 = 0.0, w1 = 0.0;
   double ba = 0.0, bv = 0.0, n2 = 0.0; long long bi = -1;
   const long long end = it.start + it.len;
-  const size_t n1 = (size_t)n, n2s = 2 * (size_t)n, n3 = 3 * (size_t)n;
+  const size_t n1 = (size_t)ldx, n2s = 2 * (size_t)ldx, n3 = 3 * (size_t)ldx;   // factor column stride
   const int hi4 = lane & 16, hi3 = lane & 8;
   // vector path: thread t takes the 4 consecutive elements 4t..4t+3 of each 1024-element sub-tile (double2
   // loads/stores); needs 16-byte alignment of every column segment (n and the chunk start even) -- the
   // scalar loop below handles the rest
-  const bool vec = ((n | (lo + it.start)) & 3) == 0 && (it.len & 3) == 0;
+  const bool vec = ((ldx | (lo + it.start)) & 3) == 0 && (it.len & 3) == 0;
   if (vec) {
     for (long long s0 = it.start; s0 < end; s0 += ACA_TILE) {
       const long long g0 = lo + s0 + 4 * t;    // elements g0 .. g0 + 3
@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(ACA_SUB, 2) k_aca_pass(const AcaCtx *__restric
         double v[4];
 #pragma unroll
         for (int q = 0; q < 4; q++) v[q] = r[q] * scale;
-        double *outp = slot + (long long)k * n + g0;
+        double *outp = slot + (long long)k * ldx + g0;
         *(double2 *)outp = make_double2(v[0], v[1]);
         *(double2 *)(outp + 2) = make_double2(v[2], v[3]);
 #pragma unroll
@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(ACA_SUB, 2) k_aca_pass(const AcaCtx *__restric
       if (q >= nval) break;
       const long long g = g0 + q * ACA_SUB;
       const double v = r[q] * scale;
-      slot[(long long)k * n + g] = v;
+      slot[(long long)k * ldx + g] = v;
       if (!((usedm >> q) & 1u) && amax_better(ba, bi, fabs(v), g - lo)) { ba = fabs(v); bi = g - lo; bv = v; }
       n2 += v * v;
     }
@@ -371,7 +371,8 @@ __global__ void __launch_bounds__(ACA_SUB) k_aca_fused(AcaCtx c, const int *bloc
   const long long mn = m1 < m2 ? m1 : m2;
   const int cap = c.st[b].cap;
   const int e = c.bdepth[b] + 1;
-  double *slot = c.Xh + c.dt->colbase[e] * n;
+  double *slot = c.Xh + c.dt->colbase[e] * c.ldx;
+  const long long ldx = c.ldx;
   for (int i = t; i < ACA_FUSED_MAX; i += ACA_SUB) { usedR[i] = 0; usedC[i] = 0; }
   __syncthreads();
   if (t == 0) {
@@ -385,15 +386,15 @@ __global__ void __launch_bounds__(ACA_SUB) k_aca_fused(AcaCtx c, const int *bloc
     // ---------------- row pass ----------------
     const long long ig = lo1 + s_ipiv;
     const double xi = c.xs[ig];
-    for (int l = t; l < k; l += ACA_SUB) Ui[l] = slot[(long long)l * n + ig];
+    for (int l = t; l < k; l += ACA_SUB) Ui[l] = slot[(long long)l * ldx + ig];
     __syncthreads();
     double ba = 0.0, bv = 0.0, n2 = 0.0; long long bi = -1;
     for (long long j = t; j < m2; j += ACA_SUB) {
       const long long gj = lo2 + j;
       double v = kval(c.kp, xi - c.xs[gj]);
 #pragma unroll 8
-      for (int l = 0; l < k; l++) v -= Ui[l] * __ldcg(slot + (long long)l * n + gj);
-      slot[(long long)k * n + gj] = v;
+      for (int l = 0; l < k; l++) v -= Ui[l] * __ldcg(slot + (long long)l * ldx + gj);
+      slot[(long long)k * ldx + gj] = v;
       vbuf[j] = v;
       if (!usedC[j] && amax_better(ba, bi, fabs(v), j)) { ba = fabs(v); bi = j; bv = v; }
       n2 += v * v;
@@ -402,7 +403,7 @@ __global__ void __launch_bounds__(ACA_SUB) k_aca_fused(AcaCtx c, const int *bloc
     for (int l = warp; l < k; l += ACA_SUB / 32) {
       double s = 0.0;
 #pragma unroll 8
-      for (long long j = lane; j < m2; j += 32) s += __ldcg(slot + (long long)l * n + lo2 + j) * vbuf[j];
+      for (long long j = lane; j < m2; j += 32) s += __ldcg(slot + (long long)l * ldx + lo2 + j) * vbuf[j];
       s = warp_sum(s);
       if (lane == 0) dV[l] = s;
     }
@@ -416,16 +417,16 @@ __global__ void __launch_bounds__(ACA_SUB) k_aca_fused(AcaCtx c, const int *bloc
     const long long jg = lo2 + s_jpiv;
     const double xj = c.xs[jg];
     const double rp = 1.0 / s_pval;
-    for (int l = t; l < k; l += ACA_SUB) Ui[l] = slot[(long long)l * n + jg];
+    for (int l = t; l < k; l += ACA_SUB) Ui[l] = slot[(long long)l * ldx + jg];
     __syncthreads();
     ba = 0.0; bv = 0.0; n2 = 0.0; bi = -1;
     for (long long i = t; i < m1; i += ACA_SUB) {
       const long long gi = lo1 + i;
       double u = kval(c.kp, c.xs[gi] - xj);
 #pragma unroll 8
-      for (int l = 0; l < k; l++) u -= Ui[l] * __ldcg(slot + (long long)l * n + gi);
+      for (int l = 0; l < k; l++) u -= Ui[l] * __ldcg(slot + (long long)l * ldx + gi);
       u *= rp;
-      slot[(long long)k * n + gi] = u;
+      slot[(long long)k * ldx + gi] = u;
       vbuf[i] = u;
       if (!usedR[i] && amax_better(ba, bi, fabs(u), i)) { ba = fabs(u); bi = i; bv = u; }
       n2 += u * u;
@@ -434,7 +435,7 @@ __global__ void __launch_bounds__(ACA_SUB) k_aca_fused(AcaCtx c, const int *bloc
     for (int l = warp; l < k; l += ACA_SUB / 32) {
       double s = 0.0;
 #pragma unroll 8
-      for (long long i = lane; i < m1; i += 32) s += __ldcg(slot + (long long)l * n + lo1 + i) * vbuf[i];
+      for (long long i = lane; i < m1; i += 32) s += __ldcg(slot + (long long)l * ldx + lo1 + i) * vbuf[i];
       s = warp_sum(s);
       if (lane == 0) dots[l] = s;
     }
@@ -520,7 +521,7 @@ static cudaError_t plan_create(AcaPlan *P, const hodlr_s *h) {
         AcaItem it; it.block = (int)b; it.q = q; it.start = s; it.len = (int)std::min(chunk, m - s);
         it.e = bdepth[b] + 1;
         it.lo1 = h->h_lo[2 * b + 1]; it.m1 = m1; it.lo2 = h->h_lo[2 * b + 2]; it.m2 = m2;
-        it.slot_off = h->dt.colbase[it.e] * h->n;
+        it.slot_off = h->dt.colbase[it.e] * h->ldx;
         (side == 0 ? items_r : items_c).push_back(it);
       }
       if (side == 0) { nq_r[b] = q; rb_r[b] = P->nrec_r; P->nrec_r += q; }
@@ -641,7 +642,7 @@ hodlr_status hodlr_aca(hodlr_s *h) {
   }
   AcaCtx c;
   memset(&c, 0, sizeof(c));
-  c.kp = h->kp; c.n = n; c.eps = h->eps; c.xs = h->xs; c.lo = h->lo; c.hi = h->hi; c.Xh = h->Xh;
+  c.kp = h->kp; c.n = n; c.ldx = h->ldx; c.eps = h->eps; c.xs = h->xs; c.lo = h->lo; c.hi = h->hi; c.Xh = h->Xh;
   c.used = h->used; c.st = h->ast; c.active = h->dflags + 4; c.rank = h->rank; c.bdepth = P->d_bdepth;
   c.dt = h->d_dt; c.bigidx = P->d_bigidx; c.gram = d_gram; c.flags = h->dflags; c.step = h->dflags + 6;
   c.maxsteps = h->cap + 1;

@@ -212,7 +212,8 @@ hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const 
   h->hi = (long long *)hodlr_dalloc(h, sizeof(long long) * h->nnodes);
   h->dflags = (int *)hodlr_dalloc(h, sizeof(int) * 16);
   h->d_dt = (DepthTab *)hodlr_dalloc(h, sizeof(DepthTab));
-  h->Xh = (double *)hodlr_dalloc(h, sizeof(double) * (size_t)n * (size_t)(cols > 0 ? cols : 1));
+  h->ldx = ((n + 31) / 32) * 32 + 32;
+  h->Xh = (double *)hodlr_dalloc(h, sizeof(double) * (size_t)h->ldx * (size_t)(cols > 0 ? cols : 1));
   if (!h->xs || !h->perm || !h->lo || !h->hi || !h->dflags || !h->d_dt || !h->Xh) {
     hodlr_free(h);
     return hodlr_set_error(HODLR_ENOMEM, "build: device allocation of %.2f GB failed",

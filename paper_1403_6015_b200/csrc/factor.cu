@@ -37,7 +37,7 @@ struct LeafCtx {
   int kappa, K, ldz, T;
   const double *xs;
   const long long *lo, *hi;
-  const double *Xh;
+  const double *Xh; long long ldx;
   const int *rank;
   const DepthTab *dt;
   double *Lf; long long lstride;
@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(LT) k_leaf_factor(LeafCtx c) {
       for (long long p = t; p < (long long)K * m; p += LT) {
         long long col = p / m, i = p - col * m;
         long long src = colsrc[col];
-        Z[i * ldz + col] = src >= 0 ? c.Xh[src * c.n + lo + i] : 0.0;
+        Z[i * ldz + col] = src >= 0 ? c.Xh[src * c.ldx + lo + i] : 0.0;
       }
       __syncthreads();
       for (int col = t; col < K; col += LT) {     // Z <- L^{-1} Z
@@ -333,7 +333,7 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
   if (!fast) {
     LeafCtx lc;
     lc.kp = h->kp; lc.n = h->n; lc.ninternal = h->ninternal; lc.nleaves = nl; lc.kappa = kappa; lc.K = K;
-    lc.ldz = K | 1; lc.T = h->ltiles; lc.xs = h->xs; lc.lo = h->lo; lc.hi = h->hi; lc.Xh = h->Xh; lc.rank = h->rank;
+    lc.ldz = K | 1; lc.T = h->ltiles; lc.xs = h->xs; lc.lo = h->lo; lc.hi = h->hi; lc.Xh = h->Xh; lc.ldx = h->ldx; lc.rank = h->rank;
     lc.dt = h->d_dt; lc.Lf = h->Lf; lc.lstride = h->lstride; lc.Pi = h->Pipool + dt.piOff[kappa];
     lc.leaf_ld = h->leaf_ld; lc.flags = h->dflags;
     lc.mmax = mmax;

@@ -90,6 +90,7 @@ struct DepthTab {
 struct AcaCtx {
   KParams kp;
   long long n;
+  long long ldx;            // column stride of Xh (n padded, see hodlr_s::ldx)
   double eps;
   const double *xs;
   const long long *lo, *hi;
@@ -156,6 +157,8 @@ struct hodlr_s {
   double *xs;
   long long *perm;
   long long *lo, *hi;
+  long long ldx;              // column stride of Xh: n rounded up to 32 plus 32 doubles, so that the columns of a
+                              // leaf panel (1 KB each) do not all fall on the same DRAM channels (stride != 2^k)
   double *Xh;
   long long xh_cols;
   unsigned char *used;

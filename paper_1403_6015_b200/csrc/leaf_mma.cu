@@ -55,7 +55,7 @@ struct LeafMmaCtx {
   int kappa, K, Kp, Kz;
   const double *xs;
   const long long *lo, *hi;
-  const double *Xh;
+  const double *Xh; long long ldx;
   const int *rank;
   const DepthTab *dt;
   double *Lf; long long lstride;
@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(ZTH, 1) k_leaf_zsyrk(LeafMmaCtx c) {
   }
   for (int q = t; q < Kz; q += ZTH) colsrc[q] = leaf_colsrc(c, id, q);
   __syncthreads();
-  const bool al16 = ((c.n | lo) & 1) == 0;      // 16-byte aligned column segments (row pairs)
+  const bool al16 = ((c.ldx | lo) & 1) == 0;      // 16-byte aligned column segments (row pairs)
   if (al16) {
     for (int p = t; p < Kz * (P / 2); p += ZTH) {
       const int col = p / (P / 2), row = 2 * (p - col * (P / 2));
@@ -317,9 +317,9 @@ __global__ void __launch_bounds__(ZTH, 1) k_leaf_zsyrk(LeafMmaCtx c) {
       double *dst = sZ + col * LDR + row;
       if (src >= 0 && row + 1 < m) {
         unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(sa), "l"(c.Xh + src * c.n + lo + row));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(sa), "l"(c.Xh + src * c.ldx + lo + row));
       } else {
-        dst[0] = (src >= 0 && row < m) ? c.Xh[src * c.n + lo + row] : 0.0;
+        dst[0] = (src >= 0 && row < m) ? c.Xh[src * c.ldx + lo + row] : 0.0;
         dst[1] = 0.0;
       }
     }
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(ZTH, 1) k_leaf_zsyrk(LeafMmaCtx c) {
       const int col = p / P, row = p - col * P;
       const long long src = colsrc[col];
       double *dst = sZ + col * LDR + row;
-      *dst = (src >= 0 && row < m) ? c.Xh[src * c.n + lo + row] : 0.0;
+      *dst = (src >= 0 && row < m) ? c.Xh[src * c.ldx + lo + row] : 0.0;
     }
   }
   asm volatile("cp.async.commit_group;\n" ::);
@@ -445,16 +445,16 @@ __global__ void __launch_bounds__(ZTH, 1) k_leaf_pair(LeafMmaCtx c, TreeCtx tc) 
     }
     for (int q = t; q < Kz; q += ZTH) colsrc[q] = leaf_colsrc(c, id, q);
     __syncthreads();
-    if (((c.n | lo) & 1) == 0) {
+    if (((c.ldx | lo) & 1) == 0) {
       for (int p = t; p < Kz * (P / 2); p += ZTH) {
         const int col = p / (P / 2), row = 2 * (p - col * (P / 2));
         const long long src = colsrc[col];
         double *dst = sZ + col * LDR + row;
         if (src >= 0 && row + 1 < m) {
           unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(sa), "l"(c.Xh + src * c.n + lo + row));
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(sa), "l"(c.Xh + src * c.ldx + lo + row));
         } else {
-          dst[0] = (src >= 0 && row < m) ? c.Xh[src * c.n + lo + row] : 0.0;
+          dst[0] = (src >= 0 && row < m) ? c.Xh[src * c.ldx + lo + row] : 0.0;
           dst[1] = 0.0;
         }
       }
@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(ZTH, 1) k_leaf_pair(LeafMmaCtx c, TreeCtx tc) 
       for (int p = t; p < Kz * P; p += ZTH) {
         const int col = p / P, row = p - col * P;
         const long long src = colsrc[col];
-        sZ[col * LDR + row] = (src >= 0 && row < m) ? c.Xh[src * c.n + lo + row] : 0.0;
+        sZ[col * LDR + row] = (src >= 0 && row < m) ? c.Xh[src * c.ldx + lo + row] : 0.0;
       }
     }
     asm volatile("cp.async.commit_group;\n" ::);
@@ -568,7 +568,7 @@ static LeafMmaCtx leaf_ctx(hodlr_s *h, int K, double *Pi_leaf) {
   LeafMmaCtx c;
   c.kp = h->kp; c.n = h->n; c.ninternal = h->ninternal; c.kappa = h->kappa; c.K = K; c.Kp = (K + 7) / 8 * 8;
   c.Kz = (K + 15) / 16 * 16;
-  c.xs = h->xs; c.lo = h->lo; c.hi = h->hi; c.Xh = h->Xh; c.rank = h->rank; c.dt = h->d_dt;
+  c.xs = h->xs; c.lo = h->lo; c.hi = h->hi; c.Xh = h->Xh; c.ldx = h->ldx; c.rank = h->rank; c.dt = h->d_dt;
   c.Lf = h->Lf; c.lstride = h->lstride; c.Pi = Pi_leaf; c.leaf_ld = h->leaf_ld; c.flags = h->dflags;
   long long cnt;
   hodlr_own_nodes(h, h->kappa, &c.leaf0, &cnt);

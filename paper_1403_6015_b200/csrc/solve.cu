@@ -26,13 +26,14 @@ namespace {
 constexpr int LT = 256;           // threads per CTA (two CTAs per SM)
 constexpr int NWL = LT / 32;      // warps per CTA
 constexpr int VMAX = 8 * 32;      // leaf rows handled (leaf_max < 2 leaf <= 256)
+static_assert(VMAX <= LT, "one leaf row per thread (y_fetch)");
 
 struct SolveCtx {
   long long n, ninternal, nleaves;
   int kappa, K, T;
   int grank, tsplit;
   const long long *lo, *hi, *perm;
-  const double *Xh;
+  const double *Xh; long long ldx;
   const int *rank;
   const DepthTab *dt;
   const double *Lf; long long lstride;
@@ -121,10 +122,10 @@ __device__ void issue_e(const SolveCtx &c, long long leaf, const int *colsrc, do
   const long long id = c.ninternal + leaf, lo = c.lo[id];
   const int m = (int)(c.hi[id] - lo), R = 8 * c.T;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (((c.n | lo) & 1) == 0) {               // warp per column, lanes over 16-byte row pairs
+  if (((c.ldx | lo) & 1) == 0) {             // warp per column, lanes over 16-byte row pairs
     for (int q = warp; q < c.K; q += NWL) {
       const int src = colsrc[q];
-      const double *g = c.Xh + (long long)src * c.n + lo;
+      const double *g = c.Xh + (long long)src * c.ldx + lo;
       double *dst = sE + q * R;
       for (int i = 2 * lane; i < R; i += 64) {
         if (src >= 0 && i + 1 < m) cp16(dst + i, g + i);
@@ -134,7 +135,7 @@ __device__ void issue_e(const SolveCtx &c, long long leaf, const int *colsrc, do
   } else {
     for (int q = warp; q < c.K; q += NWL) {
       const int src = colsrc[q];
-      const double *g = c.Xh + (long long)src * c.n + lo;
+      const double *g = c.Xh + (long long)src * c.ldx + lo;
       double *dst = sE + q * R;
       for (int i = lane; i < R; i += 32) { if (src >= 0 && i < m) cp8(dst + i, g + i); else dst[i] = 0.0; }
     }
@@ -164,7 +165,7 @@ __device__ void bulk_e(const SolveCtx &c, long long leaf, const int *colsrc, dou
   __syncwarp();
   for (int q = lane; q < c.K; q += 32) {
     const int src = colsrc[q];
-    if (src >= 0) bulk_g2s(sE + q * R, c.Xh + (long long)src * c.n + lo, (unsigned)(m * sizeof(double)), bar);
+    if (src >= 0) bulk_g2s(sE + q * R, c.Xh + (long long)src * c.ldx + lo, (unsigned)(m * sizeof(double)), bar);
   }
 }
 
@@ -234,7 +235,13 @@ __device__ void tri_mvt(const double *X, int T, const double *in, double *out, d
   __syncthreads();
 }
 
-constexpr int KMAX_SOLVE = 512;   // ancestor columns per leaf handled by the solve
+constexpr int KMAX_SOLVE = 512;
+#ifndef SOLVE_UPB
+#define SOLVE_UPB 4       // leaf up: panel columns per warp batch (multiple of 4)
+#endif
+#ifndef SOLVE_DNU
+#define SOLVE_DNU 16      // leaf down: panel columns loaded together per lane
+#endif   // ancestor columns per leaf handled by the solve
 struct LeafSmem {
   double sb[VMAX], su[VMAX], red[4 * VMAX], sw[KMAX_SOLVE];
   int colsrc[2][KMAX_SOLVE];
@@ -246,6 +253,14 @@ struct LeafSmem {
 //   wait X_i -> u = X b, v = X^T u -> issue X_{i+1} -> wait E_i -> g = E^T v, h -> issue E_{i+1}
 // BULK: bulk copies (TMA engine) completing on mbarriers; otherwise per-thread cp.async groups.
 // ---------------------------------------------------------------------------------------------
+// y entries of leaf `leaf` for this thread's row (R <= LT: at most one row per thread), gathered through perm;
+// issued one leaf ahead so the dependent loads (lo/hi -> perm -> y) overlap the current leaf.
+__device__ __forceinline__ double y_fetch(const SolveCtx &c, long long leaf) {
+  const long long id = c.ninternal + leaf, lo = c.lo[id];
+  const int m = (int)(c.hi[id] - lo);
+  return (int)threadIdx.x < m ? c.y[c.perm[lo + threadIdx.x]] : 0.0;
+}
+
 template <bool BULK>
 __device__ void leaf_up_phase(const SolveCtx &c, double *sX, double *sE, LeafSmem &S, unsigned &phX, unsigned &phE) {
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -258,22 +273,30 @@ __device__ void leaf_up_phase(const SolveCtx &c, double *sX, double *sE, LeafSme
   __syncthreads();
   if (BULK) { zero_e_pad(c, leaf, S.colsrc[0], sE); bulk_x(c, leaf, sX, &S.barX); bulk_e(c, leaf, S.colsrc[0], sE, &S.barE); }
   else { issue_x(c, leaf, sX); if (c.stage_e) issue_e(c, leaf, S.colsrc[0], sE); else cp_commit(); }
+  double ycur = y_fetch(c, leaf);
+  const bool prof = c.stamps && blockIdx.x == 0 && t == 0;
+  unsigned long long pt[6] = {0, 0, 0, 0, 0, 0}, tp = prof ? gtimer() : 0;
+#define SUBPH(k) if (prof) { const unsigned long long tn = gtimer(); pt[k] += tn - tp; tp = tn; }
   for (; leaf < end; leaf += gridDim.x) {
     const long long nxt = leaf + gridDim.x;
     const long long id = c.ninternal + leaf, lo = c.lo[id];
     const int m = (int)(c.hi[id] - lo);
-    bool bad = false;
-    for (int i = t; i < R; i += LT) {
-      const double v = i < m ? c.y[c.perm[lo + i]] : 0.0;
-      if (!isfinite(v)) bad = true;
-      S.sb[i] = v;
+    {
+      const double v = ycur;
+      if (nxt < end) ycur = y_fetch(c, nxt);
+      if (t < R) {
+        S.sb[t] = v;
+        if (!isfinite(v)) atomicOr(&c.flags[3], 1);
+      }
     }
-    if (bad) atomicOr(&c.flags[3], 1);
     if (nxt < end) for (int q = t; q < K; q += LT) S.colsrc[cur ^ 1][q] = leaf_colsrc(c, c.ninternal + nxt, q);
+    SUBPH(0)
     if (BULK) { mbar_wait(&S.barX, phX); phX ^= 1; } else cp_wait<1>();     // X_i
     __syncthreads();
+    SUBPH(1)
     tri_mv(sX, c.T, S.sb, S.su, S.red);        // u = X b
     tri_mvt(sX, c.T, S.su, S.red, nullptr);    // v = X^T u  (into red[0..R))
+    SUBPH(2)
     if (nxt < end) { if (BULK) bulk_x(c, nxt, sX, &S.barX); else issue_x(c, nxt, sX); }   // X is free
     else if (!BULK) cp_commit();               // keep the group count uniform
     double hs = 0.0;
@@ -281,24 +304,71 @@ __device__ void leaf_up_phase(const SolveCtx &c, double *sX, double *sE, LeafSme
     hs = warp_sum(hs);
     if (BULK) { mbar_wait(&S.barE, phE); phE ^= 1; } else cp_wait<1>();     // E_i
     __syncthreads();
+    SUBPH(3)
     if (lane == 0) S.red[2 * VMAX + warp] = hs;
     double *g = c.V + c.dt->nodeV[c.kappa] + leaf * (long long)K;
-    for (int q = warp; q < K; q += NWL) {      // g = E^T v: warp per column, lanes over rows
-      double s2 = 0.0;
-      if (c.stage_e) {
+    if (c.stage_e) {
+      for (int q = warp; q < K; q += NWL) {    // g = E^T v: warp per column, lanes over rows
+        double s2 = 0.0;
         const double *e = sE + q * R;
         for (int i = lane; i < R; i += 32) s2 = fma(e[i], S.red[i], s2);
-      } else {
-        const int src = S.colsrc[cur][q];
-        if (src >= 0) {
-          const double *e = c.Xh + (long long)src * c.n + lo;
-          for (int i = lane; i < m; i += 32) s2 = fma(e[i], S.red[i], s2);
+        s2 = warp_sum(s2);
+        if (lane == 0) g[q] = s2;
+      }
+    } else {
+      // g = E^T v from global memory: a warp takes 4 consecutive columns at once (all their loads in flight
+      // together), lanes over rows; the 4 partial sums are reduced by a transposed butterfly (6 shuffles), after
+      // which lanes 8j .. 8j+7 hold column q0 + j
+      const int hi4 = lane & 16, hi3 = lane & 8;
+      for (int q0 = SOLVE_UPB * warp; q0 < K; q0 += SOLVE_UPB * NWL) {
+        // every load of a row chunk is issued before any arithmetic (predicated loads, no branches)
+        constexpr int RU = 4;                  // rows per lane per chunk (128-row chunks)
+        double pv[SOLVE_UPB];
+        const double *ecol[SOLVE_UPB];
+        bool cv[SOLVE_UPB];
+#pragma unroll
+        for (int j = 0; j < SOLVE_UPB; j++) {
+          const int src = q0 + j < K ? S.colsrc[cur][q0 + j] : -1;
+          cv[j] = src >= 0;
+          ecol[j] = c.Xh + (long long)(src >= 0 ? src : 0) * c.ldx + lo;
+          pv[j] = 0.0;
+        }
+        for (int r0 = 0; r0 < R; r0 += 32 * RU) {
+          double ev[SOLVE_UPB][RU];
+#pragma unroll
+          for (int j = 0; j < SOLVE_UPB; j++)
+#pragma unroll
+            for (int u = 0; u < RU; u++) {
+              const int i = r0 + lane + 32 * u;
+              ev[j][u] = (cv[j] && i < m) ? __ldg(ecol[j] + i) : 0.0;
+            }
+#pragma unroll
+          for (int j = 0; j < SOLVE_UPB; j++)
+#pragma unroll
+            for (int u = 0; u < RU; u++) {
+              const int i = r0 + lane + 32 * u;
+              pv[j] = fma(ev[j][u], i < m ? S.red[i] : 0.0, pv[j]);
+            }
+        }
+#pragma unroll
+        for (int b4 = 0; b4 < SOLVE_UPB; b4 += 4) {
+          double s0v = hi4 ? pv[b4] : pv[b4 + 2], s1v = hi4 ? pv[b4 + 1] : pv[b4 + 3];
+          double k0 = hi4 ? pv[b4 + 2] : pv[b4], k1 = hi4 ? pv[b4 + 3] : pv[b4 + 1];
+          k0 += __shfl_xor_sync(0xffffffffu, s0v, 16);
+          k1 += __shfl_xor_sync(0xffffffffu, s1v, 16);
+          const double sv = hi3 ? k0 : k1;
+          double kk = hi3 ? k1 : k0;
+          kk += __shfl_xor_sync(0xffffffffu, sv, 8);
+          kk += __shfl_xor_sync(0xffffffffu, kk, 4);
+          kk += __shfl_xor_sync(0xffffffffu, kk, 2);
+          kk += __shfl_xor_sync(0xffffffffu, kk, 1);
+          const int j = b4 + ((lane >> 3) & 3);
+          if ((lane & 7) == 0 && q0 + j < K) g[q0 + j] = kk;
         }
       }
-      s2 = warp_sum(s2);
-      if (lane == 0) g[q] = s2;
     }
     __syncthreads();
+    SUBPH(4)
     if (t == 0) {
       double h = 0.0;
       for (int w = 0; w < NWL; w++) h += S.red[2 * VMAX + w];
@@ -309,7 +379,10 @@ __device__ void leaf_up_phase(const SolveCtx &c, double *sX, double *sE, LeafSme
       else issue_e(c, nxt, S.colsrc[cur ^ 1], sE);
     } else if (!BULK) cp_commit();
     cur ^= 1;
+    SUBPH(5)
   }
+#undef SUBPH
+  if (prof) for (int k = 0; k < 6; k++) c.stamps[64 + k] = pt[k];
   if (!BULK) cp_wait<0>();
   __syncthreads();
 }
@@ -317,7 +390,7 @@ __device__ void leaf_up_phase(const SolveCtx &c, double *sX, double *sE, LeafSme
 // leaf down: x_l = A_l^{-1} (b_l + E_l w_l):  wait E_i -> b + E w -> issue E_{i+1} -> wait X_i -> u, x -> issue X_{i+1}
 template <bool BULK>
 __device__ void leaf_down_phase(const SolveCtx &c, double *sX, double *sE, LeafSmem &S, unsigned &phX, unsigned &phE) {
-  const int t = threadIdx.x;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int R = 8 * c.T, K = c.K;
   long long leaf = c.leaf0 + blockIdx.x;
   const long long end = c.leaf0 + c.nown;
@@ -327,32 +400,65 @@ __device__ void leaf_down_phase(const SolveCtx &c, double *sX, double *sE, LeafS
   __syncthreads();
   if (BULK) { zero_e_pad(c, leaf, S.colsrc[0], sE); bulk_e(c, leaf, S.colsrc[0], sE, &S.barE); bulk_x(c, leaf, sX, &S.barX); }
   else { if (c.stage_e) issue_e(c, leaf, S.colsrc[0], sE); else cp_commit(); issue_x(c, leaf, sX); }
+  double ycur = y_fetch(c, leaf);
   for (; leaf < end; leaf += gridDim.x) {
     const long long nxt = leaf + gridDim.x;
     const long long id = c.ninternal + leaf, lo = c.lo[id];
     const int m = (int)(c.hi[id] - lo);
     const double *w = c.V + c.dt->nodeV[c.kappa] + leaf * (long long)K;
     for (int q = t; q < K; q += LT) S.sw[q] = w[q];
-    for (int i = t; i < R; i += LT) S.sb[i] = i < m ? c.y[c.perm[lo + i]] : 0.0;
+    {
+      const double v = ycur;
+      if (nxt < end) ycur = y_fetch(c, nxt);
+      if (t < R) S.sb[t] = v;
+    }
     if (nxt < end) for (int q = t; q < K; q += LT) S.colsrc[cur ^ 1][q] = leaf_colsrc(c, c.ninternal + nxt, q);
     if (BULK) { mbar_wait(&S.barE, phE); phE ^= 1; } else cp_wait<1>();     // E_i
     __syncthreads();
-    for (int w4 = t; w4 < 4 * R; w4 += LT) {   // b + E w: 4 threads per row (quarters of the columns)
-      const int i = w4 % R, h = w4 / R;
-      const int q0 = (K * h) / 4, q1 = (K * (h + 1)) / 4;
-      double s2 = 0.0;
-      if (c.stage_e) {
+    if (c.stage_e) {
+      for (int w4 = t; w4 < 4 * R; w4 += LT) { // b + E w: 4 threads per row (quarters of the columns)
+        const int i = w4 % R, h = w4 / R;
+        const int q0 = (K * h) / 4, q1 = (K * (h + 1)) / 4;
+        double s2 = 0.0;
         for (int q = q0; q < q1; q++) s2 = fma(sE[q * R + i], S.sw[q], s2);
-      } else if (i < m) {
-        for (int q = q0; q < q1; q++) {
-          const int src = S.colsrc[cur][q];
-          if (src >= 0) s2 = fma(c.Xh[(long long)src * c.n + lo + i], S.sw[q], s2);
-        }
+        S.red[w4] = s2;
       }
-      S.red[w4] = s2;
+      __syncthreads();
+      for (int i = t; i < R; i += LT) S.sb[i] += (S.red[i] + S.red[R + i]) + (S.red[2 * R + i] + S.red[3 * R + i]);
+    } else {
+      // b + E w from global memory: warp w takes row group w % RG (one row per lane) and column split w / RG;
+      // 8 columns' loads in flight per lane; the CS column-split partials are summed in a fixed order
+      const int RG = (R + 31) / 32, CS = NWL / RG;
+      const int rg = warp % RG, cs = warp / RG;
+      const int i = 32 * rg + lane;
+      double s2 = 0.0;
+      if (cs < CS) {
+        const int q0 = (K * cs) / CS, q1 = (K * (cs + 1)) / CS;
+        const double *ebase = c.Xh + lo + i;
+        int q = q0;
+        for (; q + SOLVE_DNU <= q1; q += SOLVE_DNU) {
+          double ev[SOLVE_DNU];
+#pragma unroll
+          for (int j = 0; j < SOLVE_DNU; j++) {
+            const int src = S.colsrc[cur][q + j];
+            ev[j] = (src >= 0 && i < m) ? __ldg(ebase + (long long)src * c.ldx) : 0.0;
+          }
+#pragma unroll
+          for (int j = 0; j < SOLVE_DNU; j++) s2 = fma(ev[j], S.sw[q + j], s2);
+        }
+        for (; q < q1; q++) {
+          const int src = S.colsrc[cur][q];
+          if (src >= 0 && i < m) s2 = fma(__ldg(ebase + (long long)src * c.ldx), S.sw[q], s2);
+        }
+        S.red[cs * R + i] = s2;
+      }
+      __syncthreads();
+      for (int r = t; r < R; r += LT) {
+        double acc = 0.0;
+        for (int k2 = 0; k2 < CS; k2++) acc += S.red[k2 * R + r];
+        S.sb[r] += acc;
+      }
     }
-    __syncthreads();
-    for (int i = t; i < R; i += LT) S.sb[i] += (S.red[i] + S.red[R + i]) + (S.red[2 * R + i] + S.red[3 * R + i]);
     if (nxt < end && (BULK || c.stage_e)) {    // E is free (barrier above)
       if (BULK) { zero_e_pad(c, nxt, S.colsrc[cur ^ 1], sE); bulk_e(c, nxt, S.colsrc[cur ^ 1], sE, &S.barE); }
       else issue_e(c, nxt, S.colsrc[cur ^ 1], sE);
@@ -612,7 +718,7 @@ hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_on
   SolveCtx c;
   c.n = h->n; c.ninternal = h->ninternal; c.nleaves = h->nleaves; c.kappa = kappa; c.K = dt.Kdim[kappa];
   c.T = h->ltiles; c.grank = h->grank; c.tsplit = h->tsplit;
-  c.lo = h->lo; c.hi = h->hi; c.perm = h->perm; c.Xh = h->Xh; c.rank = h->rank; c.dt = h->d_dt;
+  c.lo = h->lo; c.hi = h->hi; c.perm = h->perm; c.Xh = h->Xh; c.ldx = h->ldx; c.rank = h->rank; c.dt = h->d_dt;
   c.Lf = h->Lf; c.lstride = h->lstride; c.Spool = h->Spool; c.BTpool = h->BTpool;
   c.V = h->Vpool; c.Tv = h->Tvec; c.hv = h->hvec; c.y = y; c.x = x; c.flags = h->dflags;
   hodlr_own_nodes(h, kappa, &c.leaf0, &c.nown);
@@ -667,7 +773,7 @@ hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_on
     attr = dsm;
   }
   if (!h->bulk_checked) {     // bulk staging needs every leaf start and size and n even (16-byte segments)
-    bool ok = (h->n % 2) == 0;
+    bool ok = (h->ldx % 2) == 0;
     for (long long l = 0; ok && l < h->nleaves; l++) {
       const long long id = h->ninternal + l;
       ok = (h->h_lo[id] % 2) == 0 && ((h->h_hi[id] - h->h_lo[id]) % 2) == 0;
@@ -720,12 +826,14 @@ hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_on
   }
   ph_end(h, PH_SLEAF_UP);
   if (trace && c.stamps) {       // per-phase device times (block 0's view, after each grid barrier)
-    unsigned long long s[64];
+    unsigned long long s[72];
     HCUDA(cudaMemcpyAsync(s, c.stamps, sizeof(s), cudaMemcpyDeviceToHost, h->st));
     HCUDA(cudaStreamSynchronize(h->st));
     const int nst = (up_only ? 1 + kappa : 2 + 2 * kappa) + 1;
     fprintf(stderr, "[hodlr solve phases us]");
     for (int k = 1; k < nst && k < 64; k++) fprintf(stderr, " %.1f", 1e-3 * (double)(s[k] - s[k - 1]));
+    fprintf(stderr, "\n[hodlr solve leaf-up sub-phases us, block 0: y+colsrc, X wait, tri_mv+tri_mvt, h+E wait, E^T v, tail]");
+    for (int k = 64; k < 70; k++) fprintf(stderr, " %.1f", 1e-3 * (double)s[k]);
     fprintf(stderr, "\n");
   }
   return HODLR_OK;
