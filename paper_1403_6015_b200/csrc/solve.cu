@@ -401,20 +401,32 @@ __device__ void leaf_down_phase(const SolveCtx &c, double *sX, double *sE, LeafS
   if (BULK) { zero_e_pad(c, leaf, S.colsrc[0], sE); bulk_e(c, leaf, S.colsrc[0], sE, &S.barE); bulk_x(c, leaf, sX, &S.barX); }
   else { if (c.stage_e) issue_e(c, leaf, S.colsrc[0], sE); else cp_commit(); issue_x(c, leaf, sX); }
   double ycur = y_fetch(c, leaf);
+  static_assert(KMAX_SOLVE <= 2 * LT, "w prefetch: two columns per thread");
+  const double *wbase = c.V + c.dt->nodeV[c.kappa];
+  double w0 = t < K ? wbase[leaf * (long long)K + t] : 0.0, w1 = t + LT < K ? wbase[leaf * (long long)K + t + LT] : 0.0;
+  const bool prof = c.stamps && blockIdx.x == 0 && t == 0;
+  unsigned long long pt[6] = {0, 0, 0, 0, 0, 0}, tp = prof ? gtimer() : 0;
+#define SUBPH(k) if (prof) { const unsigned long long tn = gtimer(); pt[k] += tn - tp; tp = tn; }
   for (; leaf < end; leaf += gridDim.x) {
     const long long nxt = leaf + gridDim.x;
     const long long id = c.ninternal + leaf, lo = c.lo[id];
     const int m = (int)(c.hi[id] - lo);
-    const double *w = c.V + c.dt->nodeV[c.kappa] + leaf * (long long)K;
-    for (int q = t; q < K; q += LT) S.sw[q] = w[q];
+    if (t < K) S.sw[t] = w0;                   // w of this leaf (fetched one leaf ahead)
+    if (t + LT < K) S.sw[t + LT] = w1;
+    if (nxt < end) {
+      w0 = t < K ? wbase[nxt * (long long)K + t] : 0.0;
+      w1 = t + LT < K ? wbase[nxt * (long long)K + t + LT] : 0.0;
+    }
     {
       const double v = ycur;
       if (nxt < end) ycur = y_fetch(c, nxt);
       if (t < R) S.sb[t] = v;
     }
     if (nxt < end) for (int q = t; q < K; q += LT) S.colsrc[cur ^ 1][q] = leaf_colsrc(c, c.ninternal + nxt, q);
+    SUBPH(0)
     if (BULK) { mbar_wait(&S.barE, phE); phE ^= 1; } else cp_wait<1>();     // E_i
     __syncthreads();
+    SUBPH(1)
     if (c.stage_e) {
       for (int w4 = t; w4 < 4 * R; w4 += LT) { // b + E w: 4 threads per row (quarters of the columns)
         const int i = w4 % R, h = w4 / R;
@@ -463,16 +475,22 @@ __device__ void leaf_down_phase(const SolveCtx &c, double *sX, double *sE, LeafS
       if (BULK) { zero_e_pad(c, nxt, S.colsrc[cur ^ 1], sE); bulk_e(c, nxt, S.colsrc[cur ^ 1], sE, &S.barE); }
       else issue_e(c, nxt, S.colsrc[cur ^ 1], sE);
     } else if (!BULK) cp_commit();
+    SUBPH(2)
     if (BULK) { mbar_wait(&S.barX, phX); phX ^= 1; } else cp_wait<1>();     // X_i
     __syncthreads();
+    SUBPH(3)
     tri_mv(sX, c.T, S.sb, S.su, S.red);
     tri_mvt(sX, c.T, S.su, S.sb, S.red);
+    SUBPH(4)
     if (nxt < end) { if (BULK) bulk_x(c, nxt, sX, &S.barX); else issue_x(c, nxt, sX); }
     else if (!BULK) cp_commit();
     if (c.xsorted) for (int i = t; i < m; i += LT) c.xsorted[lo + i] = S.sb[i];
     else for (int i = t; i < m; i += LT) c.x[c.perm[lo + i]] = S.sb[i];
     cur ^= 1;
+    SUBPH(5)
   }
+#undef SUBPH
+  if (prof) for (int k = 0; k < 6; k++) c.stamps[70 + k] = pt[k];
   if (!BULK) cp_wait<0>();
   __syncthreads();
 }
@@ -630,6 +648,60 @@ __device__ void tree_down_node(const SolveCtx &c, int d, long long i, int lane) 
   for (int a = lane; a < Kd; a += 32) { const double v = wc[a]; w1[a] = v; w2[a] = v; }
 }
 
+// Down pass of node i at depth d: f_u = t_u + sum_a w_c[a] T[u, a] (compensated), w_c1 = [w_c; -f_u (u < r)],
+// w_c2 = [w_c; -f_u (u >= r)].  One warp takes the rows u = u0, u0 + ustep, ... in batches of 4 with the lanes over
+// a (all loads of a batch in flight together, then a 5-round dd butterfly per row).  Warp per node (u0 = 0,
+// ustep = 1) or, for levels with few nodes, a CTA per node (u0 = warp, ustep = warps).
+__device__ void tree_down_rows(const SolveCtx &c, int d, long long i, int lane, int u0, int ustep, bool copy_w) {
+  const int r = c.dt->rdep[d + 1], q = 2 * r, Kd = c.dt->Kdim[d], K1 = c.dt->Kdim[d + 1];
+  const double *wc = c.V + c.dt->nodeV[d] + i * (long long)Kd;
+  const long long qK = (long long)q * Kd;
+  const double *Th = c.BTpool + c.dt->nodeBT[d] + i * 3LL * qK + qK;
+  const double *Tl = Th + qK;
+  const double *tg = c.Tv + c.dt->nodeT[d] + i * 2LL * q;
+  double *w1 = c.V + c.dt->nodeV[d + 1] + (2 * i) * (long long)K1;
+  double *w2 = w1 + K1;
+  constexpr int UB = 4;
+  for (int ub = u0; ub < q; ub += UB * ustep) {
+    Acc2 A[UB];
+#pragma unroll
+    for (int x = 0; x < UB; x++) A[x] = acc2(0.0);
+    for (int a0 = 0; a0 < Kd; a0 += 64) {      // 2 entries per lane per row and chunk
+      const int aa = a0 + lane, ab = a0 + 32 + lane;
+      const double wa = aa < Kd ? wc[aa] : 0.0, wb = ab < Kd ? wc[ab] : 0.0;
+      double h[UB][2], l[UB][2];
+#pragma unroll
+      for (int x = 0; x < UB; x++) {
+        const int u = ub + x * ustep;
+        const bool ok = u < q;
+        const double *thu = Th + (long long)(ok ? u : 0) * Kd, *tlu = Tl + (long long)(ok ? u : 0) * Kd;
+        h[x][0] = (ok && aa < Kd) ? thu[aa] : 0.0; l[x][0] = (ok && aa < Kd) ? tlu[aa] : 0.0;
+        h[x][1] = (ok && ab < Kd) ? thu[ab] : 0.0; l[x][1] = (ok && ab < Kd) ? tlu[ab] : 0.0;
+      }
+#pragma unroll
+      for (int x = 0; x < UB; x++) { acc_fma_dd(A[x], wa, h[x][0], l[x][0]); acc_fma_dd(A[x], wb, h[x][1], l[x][1]); }
+    }
+#pragma unroll
+    for (int x = 0; x < UB; x++)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double s2 = __shfl_xor_sync(0xffffffffu, A[x].s, o), c2 = __shfl_xor_sync(0xffffffffu, A[x].c, o);
+        acc_add(A[x], s2); A[x].c += c2;
+      }
+    if (lane == 0) {
+#pragma unroll
+      for (int x = 0; x < UB; x++) {
+        const int u = ub + x * ustep;
+        if (u >= q) break;
+        acc_add(A[x], tg[u]); A[x].c += tg[q + u];
+        const double f = acc_val(A[x]);
+        if (u < r) w1[Kd + u] = -f; else w2[Kd + u - r] = -f;
+      }
+    }
+  }
+  if (copy_w) for (int a = lane; a < Kd; a += 32) { const double v = wc[a]; w1[a] = v; w2[a] = v; }
+}
+
 // ---------------------------------------------------------------------------------------------
 // the persistent cooperative kernel
 // ---------------------------------------------------------------------------------------------
@@ -673,7 +745,11 @@ __global__ void __launch_bounds__(LT, 2) k_solve(SolveCtx c0, Phases ph) {
   for (int d = 0; d < c.kappa; d++) {
     long long i0, cnt;
     own_range(c, d, i0, cnt);
-    for (long long j = gw; j < cnt; j += nw) tree_down_node(c, d, i0 + j, lane);
+    if (cnt >= 8 && cnt <= gridDim.x) {       // few (but not very few) nodes: one CTA each, its warps split the rows
+      if (blockIdx.x < cnt) tree_down_rows(c, d, i0 + blockIdx.x, lane, warp, NWL, warp == 0);
+    } else {
+      for (long long j = gw; j < cnt; j += nw) tree_down_node(c, d, i0 + j, lane);
+    }
     grid.sync();
     if (stamp) c.stamps[ns++] = gtimer();
   }
@@ -826,7 +902,7 @@ hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_on
   }
   ph_end(h, PH_SLEAF_UP);
   if (trace && c.stamps) {       // per-phase device times (block 0's view, after each grid barrier)
-    unsigned long long s[72];
+    unsigned long long s[80];
     HCUDA(cudaMemcpyAsync(s, c.stamps, sizeof(s), cudaMemcpyDeviceToHost, h->st));
     HCUDA(cudaStreamSynchronize(h->st));
     const int nst = (up_only ? 1 + kappa : 2 + 2 * kappa) + 1;
@@ -834,6 +910,8 @@ hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_on
     for (int k = 1; k < nst && k < 64; k++) fprintf(stderr, " %.1f", 1e-3 * (double)(s[k] - s[k - 1]));
     fprintf(stderr, "\n[hodlr solve leaf-up sub-phases us, block 0: y+colsrc, X wait, tri_mv+tri_mvt, h+E wait, E^T v, tail]");
     for (int k = 64; k < 70; k++) fprintf(stderr, " %.1f", 1e-3 * (double)s[k]);
+    fprintf(stderr, "\n[hodlr solve leaf-down sub-phases us, block 0: w+y+colsrc, E wait, E w, X wait, tri_mv+tri_mvt, x+tail]");
+    for (int k = 70; k < 76; k++) fprintf(stderr, " %.1f", 1e-3 * (double)s[k]);
     fprintf(stderr, "\n");
   }
   return HODLR_OK;
