@@ -109,10 +109,17 @@ static void res_acquire(hodlr_s *h) {
     cudaEventCreateWithFlags(&r.ev_chol, cudaEventDisableTiming);
     int lo_pri = 0, hi_pri = 0;
     cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri);
-    static int fused_hi = -1;    // HODLR_FUSED_PRIORITY=1: the fused small-block ACA at high priority (measured slower)
-    if (fused_hi < 0) { const char *ev = getenv("HODLR_FUSED_PRIORITY"); fused_hi = ev ? atoi(ev) : 0; }
-    cudaStreamCreateWithPriority(&r.st2, cudaStreamNonBlocking, fused_hi ? hi_pri : lo_pri);
-    cudaStreamCreateWithFlags(&r.st3, cudaStreamNonBlocking);
+    // Fused small-block ACA stream priority (HODLR_FUSED_PRIORITY): 0 lowest (as the leaf Cholesky), 1 the step
+    // loop's (highest), 2 (default, measured best: ACA phase 2.82 -> 2.43 ms) just below the step loop: ahead of the
+    // Cholesky's CTAs, behind the passes
+    static int fused_pri = -1;
+    if (fused_pri < 0) { const char *ev = getenv("HODLR_FUSED_PRIORITY"); fused_pri = ev ? atoi(ev) : 2; }
+    const int pf = fused_pri == 1 ? hi_pri : (fused_pri == 2 ? std::min(lo_pri, hi_pri + 1) : lo_pri);
+    cudaStreamCreateWithPriority(&r.st2, cudaStreamNonBlocking, pf);
+    static int chol_pri = -1;    // HODLR_CHOL_PRIORITY: the leaf Cholesky stream, same encoding
+    if (chol_pri < 0) { const char *ev = getenv("HODLR_CHOL_PRIORITY"); chol_pri = ev ? atoi(ev) : 0; }
+    const int pc = chol_pri == 1 ? hi_pri : (chol_pri == 2 ? std::min(lo_pri, hi_pri + 1) : lo_pri);
+    cudaStreamCreateWithPriority(&r.st3, cudaStreamNonBlocking, pc);
     cudaStreamCreateWithPriority(&r.sthi, cudaStreamNonBlocking, hi_pri);
     cudaEventCreateWithFlags(&r.ev_hi, cudaEventDisableTiming);
     for (int p = 0; p < PH_N; p++) for (int j = 0; j < 2; j++) cudaEventCreate(&r.ph_ev[p][j]);
