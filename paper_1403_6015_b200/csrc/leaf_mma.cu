@@ -17,6 +17,7 @@
 // fragment loads).  Rows m..P-1 are padded with the identity (A) and zeros (E).
 #include "hodlr_internal.cuh"
 #include "tree_node.cuh"
+#include <stdio.h>
 
 namespace {
 
@@ -136,6 +137,13 @@ __device__ __forceinline__ long long leaf_colsrc(const LeafMmaCtx &c, long long 
 //   Only X is kept: Z = X E is a GEMM and the solve's triangular solves become matrix-vector products
 //   (explicit triangular inverse: DESIGN.md R6).
 // ---------------------------------------------------------------------------------------------
+#ifdef CHOL_TRACE
+__device__ unsigned long long g_chol_stamps[2][6];
+#define CSTAMP(k) if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == 4000)) { unsigned long long v_; \
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v_)); g_chol_stamps[blockIdx.x ? 1 : 0][k] = v_; }
+#else
+#define CSTAMP(k)
+#endif
 template <int P>
 __global__ void __launch_bounds__(NTH, 2) k_leaf_chol(LeafMmaCtx c) {
   constexpr int T = P / 8;
@@ -150,6 +158,7 @@ __global__ void __launch_bounds__(NTH, 2) k_leaf_chol(LeafMmaCtx c) {
   const long long leaf = c.leaf0 + blockIdx.x;
   const long long id = c.ninternal + leaf, lo = c.lo[id];
   const int m = (int)(c.hi[id] - lo);
+  CSTAMP(0)
   if (t == 0) bad = 0;
   for (int i = t; i < P; i += NTH) sx[i] = i < m ? c.xs[lo + i] : 0.0;
   __syncthreads();
@@ -167,11 +176,88 @@ __global__ void __launch_bounds__(NTH, 2) k_leaf_chol(LeafMmaCtx c) {
     }
   }
   __syncthreads();
+  CSTAMP(1)
   // ---------------- Cholesky, left-looking over tile columns J ----------------
   // Per column: warp 0 forms the diagonal tile C(J,J) and factors it (POTRF + inverse) while warps 1-7
   // form the sub-diagonal tiles C(I,J) = A(I,J) - sum_{k<J} L(I,k) L(J,k)^T; then all warps apply
   // Linv(J)^T to the panel.
   const int cp = cpos(lane);
+#ifndef CHOL_LOOKAHEAD
+#define CHOL_LOOKAHEAD 1
+#endif
+#if CHOL_LOOKAHEAD
+  // Look-ahead schedule (one block barrier per column): in step J every warp applies Linv(J) to its panel tiles
+  // L(I,J) = C(I,J) Linv(J)^T (warp 0 takes I = J+1 first), then warp 0 -- without waiting for the others --
+  // forms the next diagonal tile C(J+1,J+1) = A - sum_{k<=J} L(J+1,k) L(J+1,k)^T and factors it (POTRF +
+  // inverse), while warps 1-7, after a named barrier that warp 0 only arrives at, form the sub-diagonal tiles
+  // C(I,J+1), I > J+1.  The factorization is the same left-looking one; only the order of independent work changes.
+  auto diag_update = [&](int J) {              // warp 0: C(J,J) -= sum_{k<J} L(J,k) L(J,k)^T, then POTRF
+    const double *tJ = sL + tix(J, 0) * 64;
+    double *tc = sL + tix(J, J) * 64;
+    double d0 = tc[cp], d1 = tc[cp + 1], e0 = 0.0, e1 = 0.0;
+    int k = 0;
+    for (; k + 1 < J; k += 2) {
+      dmma(d0, d1, -tJ[k * 64 + lane], tJ[k * 64 + lane]);
+      dmma(e0, e1, -tJ[(k + 1) * 64 + lane], tJ[(k + 1) * 64 + lane]);
+      dmma(d0, d1, -tJ[k * 64 + 32 + lane], tJ[k * 64 + 32 + lane]);
+      dmma(e0, e1, -tJ[(k + 1) * 64 + 32 + lane], tJ[(k + 1) * 64 + 32 + lane]);
+    }
+    if (k < J) {
+      dmma(d0, d1, -tJ[k * 64 + lane], tJ[k * 64 + lane]);
+      dmma(e0, e1, -tJ[k * 64 + 32 + lane], tJ[k * 64 + 32 + lane]);
+    }
+    __syncwarp();
+    tc[cp] = d0 + e0; tc[cp + 1] = d1 + e1;
+    __syncwarp();
+    potrf8(tc, sLi + J * 64, sdiag + 8 * J, &bad);
+  };
+  auto offdiag_update = [&](int I, int J) {    // C(I,J) -= sum_{k<J} L(I,k) L(J,k)^T
+    const double *tJ = sL + tix(J, 0) * 64;
+    double *tc = sL + tix(I, J) * 64;
+    double d0 = tc[cp], d1 = tc[cp + 1], e0 = 0.0, e1 = 0.0;
+    const double *tI = sL + tix(I, 0) * 64;
+    int k = 0;
+    for (; k + 1 < J; k += 2) {
+      dmma(d0, d1, -tI[k * 64 + lane], tJ[k * 64 + lane]);
+      dmma(e0, e1, -tI[(k + 1) * 64 + lane], tJ[(k + 1) * 64 + lane]);
+      dmma(d0, d1, -tI[k * 64 + 32 + lane], tJ[k * 64 + 32 + lane]);
+      dmma(e0, e1, -tI[(k + 1) * 64 + 32 + lane], tJ[(k + 1) * 64 + 32 + lane]);
+    }
+    if (k < J) {
+      dmma(d0, d1, -tI[k * 64 + lane], tJ[k * 64 + lane]);
+      dmma(e0, e1, -tI[k * 64 + 32 + lane], tJ[k * 64 + 32 + lane]);
+    }
+    __syncwarp();
+    tc[cp] = d0 + e0; tc[cp + 1] = d1 + e1;
+  };
+  auto panel = [&](int I, int J) {             // L(I,J) = C(I,J) Linv(J)^T
+    const double *Li = sLi + J * 64;
+    double *tl = sL + tix(I, J) * 64;
+    const double a0 = tl[lane], a1 = tl[32 + lane];
+    double d0 = 0.0, d1 = 0.0;
+    dmma(d0, d1, a0, Li[lane]);
+    dmma(d0, d1, a1, Li[32 + lane]);
+    __syncwarp();
+    tl[cp] = d0; tl[cp + 1] = d1;
+  };
+  if (warp == 0) diag_update(0);               // column 0: nothing to subtract
+  __syncthreads();
+  for (int J = 0; J < T; J++) {
+    if (J + 1 >= T) break;                     // the last column has no panel
+    if (warp == 0) {
+      panel(J + 1, J);
+      __syncwarp();
+      __threadfence_block();
+      asm volatile("bar.arrive 1, %0;" :: "n"(NTH) : "memory");    // L(J+1, J) is in shared memory
+      diag_update(J + 1);
+    } else {
+      for (int I = J + 1 + warp; I < T; I += NW - 1) panel(I, J);
+      asm volatile("bar.sync 1, %0;" :: "n"(NTH) : "memory");
+      for (int I = J + 1 + warp; I < T; I += NW - 1) offdiag_update(I, J + 1);
+    }
+    __syncthreads();
+  }
+#else
   for (int J = 0; J < T; J++) {
     const double *tJ = sL + tix(J, 0) * 64;
     if (warp == 0) {
@@ -225,6 +311,8 @@ __global__ void __launch_bounds__(NTH, 2) k_leaf_chol(LeafMmaCtx c) {
     }
     __syncthreads();
   }
+#endif
+  CSTAMP(2)
   if (warp == 0) {          // 2 sum log L_ii: per-lane partials, then a fixed-order warp reduction
     double s2 = 0.0;
     for (int i = lane; i < m; i += 32) s2 += log(sdiag[i]);
@@ -275,6 +363,8 @@ __global__ void __launch_bounds__(NTH, 2) k_leaf_chol(LeafMmaCtx c) {
       }
     }
   }
+  __syncthreads();
+  CSTAMP(3)
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -593,6 +683,16 @@ hodlr_status hodlr_leaf_chol_mma(hodlr_s *h, cudaStream_t stream, bool *launched
     k_leaf_chol<128><<<(int)(h->nleaves >> h->tsplit), NTH, smem, stream>>>(c);
   }
   HLAUNCH(h, "k_leaf_chol");
+#ifdef CHOL_TRACE
+  {
+    unsigned long long ts[2][6];
+    cudaStreamSynchronize(stream);
+    cudaMemcpyFromSymbol(ts, g_chol_stamps, sizeof(ts));
+    for (int b = 0; b < 2; b++)
+      fprintf(stderr, "[chol CTA %d] assemble %.2f factor %.2f logdet+X %.2f us\n", b ? 4000 : 0,
+              1e-3 * (ts[b][1] - ts[b][0]), 1e-3 * (ts[b][2] - ts[b][1]), 1e-3 * (ts[b][3] - ts[b][2]));
+  }
+#endif
   *launched = true;
   return HODLR_OK;
 }
