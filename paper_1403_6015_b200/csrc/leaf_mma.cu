@@ -101,17 +101,16 @@ __device__ void potrf8(double *tile, double *linv, double *diag8, int *bad) {
 #pragma unroll
     for (int j = 0; j < 8; j++) tile[fo(i, j)] = j <= i ? a[i][j] : 0.0;
   if (lane < 8) diag8[lane] = tile[fo(lane, lane)];
-  // L^{-1} column by column (forward substitution)
-#pragma unroll
-  for (int cc = 0; cc < 8; cc++) {
+  // L^{-1}: lane cc < 8 computes column cc by forward substitution (the 8 columns in parallel)
+  if (lane < 8) {
+    const int cc = lane;
     double y[8];
 #pragma unroll
     for (int i = 0; i < 8; i++) {
-      if (i < cc) { y[i] = 0.0; continue; }
       double s = (i == cc) ? 1.0 : 0.0;
 #pragma unroll
-      for (int k = cc; k < i; k++) s -= a[i][k] * y[k];
-      y[i] = s * inv[i];
+      for (int k = 0; k < i; k++) s = fma(-a[i][k], y[k], s);
+      y[i] = i < cc ? 0.0 : s * inv[i];
     }
 #pragma unroll
     for (int i = 0; i < 8; i++) linv[fo(i, cc)] = y[i];
