@@ -136,6 +136,9 @@ __device__ __forceinline__ long long leaf_colsrc(const LeafMmaCtx &c, long long 
 //   Only X is kept: Z = X E is a GEMM and the solve's triangular solves become matrix-vector products
 //   (explicit triangular inverse: DESIGN.md R6).
 // ---------------------------------------------------------------------------------------------
+#ifndef CHOL_LOOKAHEAD
+#define CHOL_LOOKAHEAD 1
+#endif
 #ifdef CHOL_TRACE
 __device__ unsigned long long g_chol_stamps[2][6];
 #define CSTAMP(k) if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == 4000)) { unsigned long long v_; \
@@ -161,9 +164,11 @@ __global__ void __launch_bounds__(NTH, 2) k_leaf_chol(LeafMmaCtx c) {
   if (t == 0) bad = 0;
   for (int i = t; i < P; i += NTH) sx[i] = i < m ? c.xs[lo + i] : 0.0;
   __syncthreads();
-  // assemble A_l = K[l,l] + s2 I into the lower tiles (fragment order), identity padding beyond m
-  for (int ti = warp; ti < NTILE; ti += NW) {
-    const int I = c_tileI[ti], J = c_tileJ[ti];
+  // assemble A_l = K[l,l] + s2 I into the lower tiles (fragment order), identity padding beyond m.  With the
+  // look-ahead schedule only tile columns 0 and 1 are assembled up front; column J+2 is assembled by warps 1-7
+  // during step J (while warp 0 factors the diagonal tile), hiding the kernel evaluations behind the POTRFs.
+  auto asm_tile = [&](int I, int J) {
+    const int ti = tix(I, J);
 #pragma unroll
     for (int h = 0; h < 2; h++) {
       const int r = lane >> 2, cc = (lane & 3) + 4 * h;
@@ -173,7 +178,12 @@ __global__ void __launch_bounds__(NTH, 2) k_leaf_chol(LeafMmaCtx c) {
       else v = (i == j) ? 1.0 : 0.0;
       sL[ti * 64 + 32 * h + lane] = v;
     }
-  }
+  };
+#if CHOL_LOOKAHEAD
+  for (int ti = warp; ti < 2 * T - 1; ti += NW) asm_tile(ti < T ? ti : ti - T + 1, ti < T ? 0 : 1);   // columns 0, 1
+#else
+  for (int ti = warp; ti < NTILE; ti += NW) asm_tile(c_tileI[ti], c_tileJ[ti]);
+#endif
   __syncthreads();
   CSTAMP(1)
   // ---------------- Cholesky, left-looking over tile columns J ----------------
@@ -181,9 +191,6 @@ __global__ void __launch_bounds__(NTH, 2) k_leaf_chol(LeafMmaCtx c) {
   // form the sub-diagonal tiles C(I,J) = A(I,J) - sum_{k<J} L(I,k) L(J,k)^T; then all warps apply
   // Linv(J)^T to the panel.
   const int cp = cpos(lane);
-#ifndef CHOL_LOOKAHEAD
-#define CHOL_LOOKAHEAD 1
-#endif
 #if CHOL_LOOKAHEAD
   // Look-ahead schedule (one block barrier per column): in step J every warp applies Linv(J) to its panel tiles
   // L(I,J) = C(I,J) Linv(J)^T (warp 0 takes I = J+1 first), then warp 0 -- without waiting for the others --
@@ -253,6 +260,7 @@ __global__ void __launch_bounds__(NTH, 2) k_leaf_chol(LeafMmaCtx c) {
       for (int I = J + 1 + warp; I < T; I += NW - 1) panel(I, J);
       asm volatile("bar.sync 1, %0;" :: "n"(NTH) : "memory");
       for (int I = J + 1 + warp; I < T; I += NW - 1) offdiag_update(I, J + 1);
+      for (int I = J + 1 + warp; I < T; I += NW - 1) asm_tile(I, J + 2);     // column J+2 (I >= J+2)
     }
     __syncthreads();
   }
