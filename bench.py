@@ -19,6 +19,7 @@ import math
 import os
 import statistics
 import subprocess
+import threading
 import sys
 import time
 
@@ -104,11 +105,51 @@ def run_reference(args):
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
+    """SM clock and throttle reasons sampled DURING the timed region: NVML (nvidia_ml_py) polled every 2 ms from a
+    background thread, else `nvidia-smi -lms 100`."""
+
     def __init__(self, dev):
         self.dev = dev
         self.proc = None
+        self.samples = []
 
     def __enter__(self):
+        self.samples, self.lines = [], []
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            idx = self.dev
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            if vis:
+                try:
+                    idx = int(vis.split(",")[self.dev])
+                except ValueError:
+                    pass
+            hdl = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(hdl, pynvml.NVML_CLOCK_SM)
+            bits = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                    "sw_power_cap": 0x4}
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(hdl, pynvml.NVML_CLOCK_SM)
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(hdl) \
+                            if hasattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons") \
+                            else pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(hdl)
+                        self.samples.append((float(sm), float(mx), [k for k, b in bits.items() if rs & b]))
+                    except Exception:
+                        pass
+                    self._stop.wait(0.002)
+            self.th = threading.Thread(target=run, daemon=True)
+            self.th.start()
+            while not self.samples and self.th.is_alive():      # first sample before the timed region starts
+                time.sleep(0.001)
+            self.samples.clear()
+            return self
+        except Exception:
+            self.th = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.dev), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
@@ -121,7 +162,9 @@ class ClockSampler:
         return self
 
     def __exit__(self, *a):
-        self.lines = []
+        if getattr(self, "th", None):
+            self._stop.set()
+            self.th.join(timeout=2)
         if self.proc:
             self.proc.terminate()
             try:
@@ -132,8 +175,13 @@ class ClockSampler:
 
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
+        for s, m, rs in self.samples:
+            mx = max(mx, m)
+            if s > 0.5 * m:
+                sm.append(s)
+            reasons.update(rs)
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for l in getattr(self, "lines", []):
+        for l in self.lines:
             f = [x.strip() for x in l.split(",")]
             if len(f) < 8:
                 continue
@@ -148,7 +196,8 @@ class ClockSampler:
                 if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(getattr(self, "lines", []))}
+                "reasons": sorted(reasons), "samples": len(self.samples) + len(self.lines),
+                "source": "nvml" if self.samples else "nvidia-smi"}
 
 
 # ------------------------------------------------------------------ algorithmic counts
@@ -304,7 +353,7 @@ def run_ours(args):
         h.close()
         return ld_, s_
 
-    for _ in range(1):
+    for _ in range(max(1, args.warmup)):
         step_e2e(); torch.cuda.synchronize()
     e2e_ms = []
     barrier(); torch.cuda.synchronize()
