@@ -41,7 +41,8 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--config", default="cfg3")
-    p.add_argument("--cpu-sample", type=int, default=1 << 17, help="oracle sample size (points)")
+    p.add_argument("--cpu-sample", type=int, default=1 << 19,
+                   help="oracle sample size (points): about 10 s of single-thread CPU work at config 3")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
 
