@@ -18,6 +18,8 @@
 #include "hodlr_internal.cuh"
 #include "tree_node.cuh"
 #include <stdio.h>
+#include <algorithm>
+#include <stdlib.h>
 
 namespace {
 
@@ -489,6 +491,130 @@ __global__ void __launch_bounds__(ZTH, 1) k_leaf_zsyrk(LeafMmaCtx c) {
   }
 }
 
+// Persistent form of k_leaf_zsyrk (X staged): one CTA per SM walks the leaves leaf0 + blockIdx.x + k gridDim.x;
+// the next leaf's X tiles are copied (cp.async) while this leaf's Pi = Z^T Z runs, and its panel E as soon as Z is
+// free, so only the E copy is exposed per leaf (no CTA turnaround either).
+template <int P>
+__global__ void __launch_bounds__(ZTH, 1) k_leaf_zsyrk_p(LeafMmaCtx c, long long nown) {
+  constexpr int T = P / 8;
+  constexpr int NTILE = T * (T + 1) / 2;
+  constexpr int LDR = P + 4;
+  extern __shared__ double sm[];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int K = c.K, Kp = c.Kp, Kc = Kp / 8, Kz = c.Kz;
+  double *sX = sm;                              // NTILE * 64: tiles of X = L^{-1}
+  double *sZ = sm + NTILE * 64;                 // Kz * LDR (column-major)
+  long long *colsrc = (long long *)(sZ + (long long)Kz * LDR);   // Kz
+  auto issue_x = [&](long long lf) {
+    const double *Lg = c.Lf + lf * c.lstride;
+    for (int p = t; p < NTILE * 32; p += ZTH) {
+      unsigned sa = (unsigned)__cvta_generic_to_shared(sX + 2 * p);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(sa), "l"(Lg + 2 * p));
+    }
+  };
+  auto issue_e = [&](long long lf) {            // colsrc of lf must be in shared memory (after a barrier)
+    const long long id = c.ninternal + lf, lo = c.lo[id];
+    const int m = (int)(c.hi[id] - lo);
+    const bool al16 = ((c.ldx | lo) & 1) == 0;
+    if (al16) {
+      for (int p = t; p < Kz * (P / 2); p += ZTH) {
+        const int col = p / (P / 2), row = 2 * (p - col * (P / 2));
+        const long long src = colsrc[col];
+        double *dst = sZ + col * LDR + row;
+        if (src >= 0 && row + 1 < m) {
+          unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(sa), "l"(c.Xh + src * c.ldx + lo + row));
+        } else {
+          dst[0] = (src >= 0 && row < m) ? c.Xh[src * c.ldx + lo + row] : 0.0;
+          dst[1] = 0.0;
+        }
+      }
+    } else {
+      for (int p = t; p < Kz * P; p += ZTH) {
+        const int col = p / P, row = p - col * P;
+        const long long src = colsrc[col];
+        double *dst = sZ + col * LDR + row;
+        *dst = (src >= 0 && row < m) ? c.Xh[src * c.ldx + lo + row] : 0.0;
+      }
+    }
+  };
+  long long leaf = c.leaf0 + blockIdx.x;
+  const long long end = c.leaf0 + nown;
+  if (leaf >= end) return;
+  for (int q = t; q < Kz; q += ZTH) colsrc[q] = leaf_colsrc(c, c.ninternal + leaf, q);
+  issue_x(leaf);
+  __syncthreads();
+  issue_e(leaf);
+  asm volatile("cp.async.commit_group;\n" ::);
+  for (; leaf < end; leaf += gridDim.x) {
+    const long long nxt = leaf + gridDim.x;
+    const long long id = c.ninternal + leaf;
+    const int m = (int)(c.hi[id] - c.lo[id]);
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncthreads();
+    // ---------------- Z = X E ----------------
+    {
+      const int g = lane >> 2, q2 = 2 * (lane & 3), kq = lane & 3;
+      for (int cc = warp; cc < Kc; cc += ZW) {
+        double acc[T][2];
+#pragma unroll
+        for (int i = 0; i < T; i++) { acc[i][0] = 0.0; acc[i][1] = 0.0; }
+        const double *zc = sZ + (8 * cc + g) * LDR;
+#pragma unroll
+        for (int kb = 0; kb < T; kb++) {
+          const double b0 = zc[8 * kb + kq], b1 = zc[8 * kb + 4 + kq];
+#pragma unroll
+          for (int i = kb; i < T; i++) {
+            const double *tA = sX + tix(i, kb) * 64;
+            dmma(acc[i][0], acc[i][1], tA[lane], b0);
+            dmma(acc[i][0], acc[i][1], tA[32 + lane], b1);
+          }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < T; i++) {
+          sZ[(8 * cc + q2) * LDR + 8 * i + g] = acc[i][0];
+          sZ[(8 * cc + q2 + 1) * LDR + 8 * i + g] = acc[i][1];
+        }
+      }
+    }
+    __syncthreads();
+    if (nxt < end) { issue_x(nxt); asm volatile("cp.async.commit_group;\n" ::); }   // X is free
+    if (K > 0) {
+      // ---------------- Pi_l = Z^T Z: 16x16 output blocks, DMMA m16n8k8 ----------------
+      const int Kc16 = Kz / 16;
+      const int nblk = Kc16 * (Kc16 + 1) / 2;
+      double *Pl = c.Pi + leaf * ((long long)K * (K + 1) / 2);
+      const int kend = (m + 7) & ~7;
+      const int g = lane >> 2, tq = lane & 3;
+      for (int blk = warp; blk < nblk; blk += ZW) {
+        const int BI = c_tileI[blk], BJ = c_tileJ[blk];
+        double acc0[4] = {0, 0, 0, 0}, acc1[4] = {0, 0, 0, 0};
+        const double *pa0 = sZ + (16 * BI + g) * LDR + tq;
+        const double *pa1 = pa0 + 8 * LDR;
+        const double *pb0 = sZ + (16 * BJ + g) * LDR + tq;
+        const double *pb1 = pb0 + 8 * LDR;
+        for (int k0 = 0; k0 < kend; k0 += 8) {
+          const double a0 = pa0[k0], a1 = pa1[k0], a2 = pa0[k0 + 4], a3 = pa1[k0 + 4];
+          dmma16(acc0, a0, a1, a2, a3, pb0[k0], pb0[k0 + 4]);
+          dmma16(acc1, a0, a1, a2, a3, pb1[k0], pb1[k0 + 4]);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+          const double v = q < 4 ? acc0[q] : acc1[q - 4];
+          const int row = 16 * BI + g + ((q & 2) ? 8 : 0);
+          const int col = 16 * BJ + 2 * tq + (q & 1) + (q >= 4 ? 8 : 0);
+          if (row < K && col < K && row >= col) Pl[(long long)row * (row + 1) / 2 + col] = v;
+        }
+      }
+    }
+    if (nxt < end) for (int q = t; q < Kz; q += ZTH) colsrc[q] = leaf_colsrc(c, c.ninternal + nxt, q);
+    __syncthreads();                            // Z and colsrc free / ready
+    if (nxt < end) { issue_e(nxt); asm volatile("cp.async.commit_group;\n" ::); }
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
+}
+
 // ---------------------------------------------------------------------------------------------
 // Kernel 2' (fused with the deepest tree level): one CTA per depth-(kappa-1) node c with leaves c1 = 2i,
 // c2 = 2i+1.  For each leaf: Z = X E (as k_leaf_zsyrk), the s-part rows Pi_l[s, :] = Z_s^T Z, and
@@ -729,9 +855,19 @@ hodlr_status hodlr_leaf_factor_mma(hodlr_s *h, int K, double *Pi_leaf, bool *use
     HCUDA(cudaFuncSetAttribute(k_leaf_zsyrk<PP, XGV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
     k_leaf_zsyrk<PP, XGV><<<grid, ZTH, smem, h->st>>>(c);                                                      \
   } while (0)
-  if (P == 64) { if (wide) LAUNCH_ZS(64, true); else LAUNCH_ZS(64, false); }
-  else { if (wide) LAUNCH_ZS(128, true); else LAUNCH_ZS(128, false); }
+#define LAUNCH_ZSP(PP)                                                                                         \
+  do {                                                                                                        \
+    HCUDA(cudaFuncSetAttribute(k_leaf_zsyrk_p<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));   \
+    k_leaf_zsyrk_p<PP><<<std::min(grid, nsm), ZTH, smem, h->st>>>(c, (long long)grid);                          \
+  } while (0)
+  static int persist = -1;     // HODLR_ZSYRK_PERSIST=0: one CTA per leaf (no cross-leaf prefetch)
+  if (persist < 0) { const char *ev = getenv("HODLR_ZSYRK_PERSIST"); persist = ev ? atoi(ev) : 1; }
+  int nsm = 148;
+  HCUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->dev));
+  if (P == 64) { if (wide) LAUNCH_ZS(64, true); else if (persist) LAUNCH_ZSP(64); else LAUNCH_ZS(64, false); }
+  else { if (wide) LAUNCH_ZS(128, true); else if (persist) LAUNCH_ZSP(128); else LAUNCH_ZS(128, false); }
 #undef LAUNCH_ZS
+#undef LAUNCH_ZSP
   HLAUNCH(h, "k_leaf_zsyrk");
   *used = true;
   return HODLR_OK;
