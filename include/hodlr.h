@@ -119,6 +119,13 @@ hodlr_status hodlr_logdet(hodlr_t h, double *logdet_host);
  * dimension ld >= n, original point order.  x may not alias y. */
 hodlr_status hodlr_solve(hodlr_t h, const double *y, double *x, int64_t nrhs, int64_t ld);
 
+/* Forward apply Y = C~ X of the compressed operator (NEXT-1): the leaf diagonal
+ * blocks K_ll + sigma^2 I evaluated on the fly (Table I) plus U V^T / V U^T of every ACA block
+ * (sec. 3.1) -- the operator hodlr_solve inverts, so apply(solve(y)) = y to rounding.  Legal
+ * after hodlr_build (factoring is not needed).  x, y: device, column-major n x nrhs, leading dimension ld >= n,
+ * original point order; y may not alias x.  Single-GPU handles only (HODLR_EINVAL when sharded). */
+hodlr_status hodlr_apply(hodlr_t h, const double *x, double *y, int64_t nrhs, int64_t ld);
+
 /* GP log-likelihood (eq. 1): -1/2 y^T C^{-1} y - 1/2 log det C - (n/2) log(2 pi).
  * y: device, n doubles.  out_host: host double (-INFINITY with HODLR_ENOTPD on failure). */
 hodlr_status gp_loglik(hodlr_t h, const double *y, double *out_host);

@@ -365,7 +365,6 @@ __global__ void __launch_bounds__(ACA_SUB) k_aca_fused(AcaCtx c, const int *bloc
   __shared__ int s_k, s_done;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int b = blocks[blockIdx.x];
-  const long long n = c.n;
   const long long c1 = 2LL * b + 1, c2 = 2LL * b + 2;
   const long long lo1 = c.lo[c1], m1 = c.hi[c1] - lo1, lo2 = c.lo[c2], m2 = c.hi[c2] - lo2;
   const long long mn = m1 < m2 ? m1 : m2;

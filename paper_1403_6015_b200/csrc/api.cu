@@ -379,6 +379,18 @@ static hodlr_status check_y_flag(hodlr_t h) {
   return HODLR_OK;
 }
 
+hodlr_status hodlr_apply(hodlr_t h, const double *x, double *y, int64_t nrhs, int64_t ld) {
+  if (!h || !x || !y) return hodlr_set_error(HODLR_EINVAL, "apply: NULL argument");
+  if (h->state == 0) return hodlr_set_error(HODLR_ESTATE, "apply: not built");
+  if (nrhs < 1 || ld < h->n) return hodlr_set_error(HODLR_EINVAL, "apply: nrhs = %lld, ld = %lld", (long long)nrhs, (long long)ld);
+  if (h->nranks > 1) return hodlr_set_error(HODLR_EINVAL, "apply: sharded handles are not supported (each rank holds its subtree's factors only)");
+  h->launches = 0;
+  cudaEventRecord(h->ev0, h->st);
+  hodlr_status st = HODLR_OK;
+  for (int64_t j = 0; j < nrhs && st == HODLR_OK; j++) st = hodlr_apply_impl(h, x + j * ld, y + j * ld);
+  return finish(h, st, nullptr);
+}
+
 hodlr_status hodlr_solve(hodlr_t h, const double *y, double *x, int64_t nrhs, int64_t ld) {
   if (!h || !y || !x) return hodlr_set_error(HODLR_EINVAL, "solve: NULL argument");
   if (h->state == -1) return hodlr_set_error(HODLR_ENOTPD, "solve: factorization failed");

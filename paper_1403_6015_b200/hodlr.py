@@ -18,7 +18,7 @@ HODLR_SE, HODLR_MATERN32, HODLR_MATERN52 = 0, 1, 2
 KERNELS = {"se": HODLR_SE, "matern32": HODLR_MATERN32, "matern52": HODLR_MATERN52}
 STATUS = {0: "OK", 1: "EINVAL", 2: "ENOTPD", 3: "ERANKCAP", 4: "ESTATE", 5: "ENOMEM", 6: "ECUDA", 7: "ENCCL"}
 
-EXPORTS = ("hodlr_build", "hodlr_factor", "hodlr_logdet", "hodlr_solve", "gp_loglik", "hodlr_info",
+EXPORTS = ("hodlr_build", "hodlr_factor", "hodlr_logdet", "hodlr_solve", "hodlr_apply", "gp_loglik", "hodlr_info",
            "hodlr_get_order", "hodlr_get_tree", "hodlr_get_logdet_parts", "hodlr_free", "hodlr_last_error",
            "hodlr_version", "hodlr_launch_count", "hodlr_nccl_unique_id", "hodlr_group_create",
            "hodlr_group_destroy", "hodlr_dist_plan", "gp_loglik_sweep")
@@ -76,13 +76,14 @@ def load(build_if_missing: bool = True):
         lib.hodlr_factor.argtypes = [P]
         lib.hodlr_logdet.argtypes = [P, P]
         lib.hodlr_solve.argtypes = [P, P, P, I64, I64]
+        lib.hodlr_apply.argtypes = [P, P, P, I64, I64]
         lib.gp_loglik.argtypes = [P, P, P]
         lib.hodlr_info.argtypes = [P, P]
         lib.hodlr_get_order.argtypes = [P, P, P]
         lib.hodlr_get_tree.argtypes = [P, P, P, P]
         lib.hodlr_get_logdet_parts.argtypes = [P, P, P]
-        for f in ("hodlr_build", "hodlr_factor", "hodlr_logdet", "hodlr_solve", "gp_loglik", "hodlr_info",
-                  "hodlr_get_order", "hodlr_get_tree", "hodlr_get_logdet_parts"):
+        for f in ("hodlr_build", "hodlr_factor", "hodlr_logdet", "hodlr_solve", "hodlr_apply", "gp_loglik",
+                  "hodlr_info", "hodlr_get_order", "hodlr_get_tree", "hodlr_get_logdet_parts"):
             getattr(lib, f).restype = I32
         lib.hodlr_free.argtypes = [P]; lib.hodlr_free.restype = None
         lib.hodlr_last_error.argtypes = []; lib.hodlr_last_error.restype = C.c_char_p
@@ -151,6 +152,17 @@ def hodlr_solve(h: int, y: torch.Tensor, x: torch.Tensor | None = None) -> torch
         x.copy_(out)
         return x
     return out
+
+
+def hodlr_apply(h: int, x: torch.Tensor) -> torch.Tensor:
+    """y = C~ x of the compressed operator; x: (n,) or (n, nrhs) CUDA float64."""
+    lib = load()
+    x = _dev_f64(x, "x")
+    one = x.dim() == 1
+    X = x.reshape(x.shape[0], -1).t().contiguous()          # nrhs x n rows = column-major n x nrhs
+    Y = torch.empty_like(X)
+    _check(lib.hodlr_apply(h, X.data_ptr(), Y.data_ptr(), X.shape[0], X.shape[1]))
+    return Y[0] if one else Y.t()
 
 
 def gp_loglik(h: int, y: torch.Tensor) -> float:
@@ -254,6 +266,9 @@ class HODLR:
 
     def gp_loglik(self, y: torch.Tensor) -> float:
         return gp_loglik(self._h, y)
+
+    def apply(self, x: torch.Tensor) -> torch.Tensor:
+        return hodlr_apply(self._h, x)
 
     def info(self) -> dict:
         return hodlr_info(self._h)
