@@ -126,6 +126,12 @@ hodlr_status hodlr_solve(hodlr_t h, const double *y, double *x, int64_t nrhs, in
  * original point order; y may not alias x.  Single-GPU handles only (HODLR_EINVAL when sharded). */
 hodlr_status hodlr_apply(hodlr_t h, const double *x, double *y, int64_t nrhs, int64_t ld);
 
+/* GP prediction at m test points (eq_reg1 / eq_reg2; NEXT-1): mean_j = k(xt_j, x) C^{-1} y and,
+ * if var != NULL, the latent variance var_j = k(xt_j, xt_j) - k(xt_j, x) C^{-1} k(x, xt_j) (sigma^2 not added).
+ * Cross-covariances on the fly, C^{-1} by the HODLR solve.  y: device n (original order); xt, mean, var: device m.
+ * Legal after hodlr_factor; single-GPU handles only (HODLR_EINVAL when sharded). */
+hodlr_status gp_predict(hodlr_t h, const double *y, const double *xt, int64_t m, double *mean, double *var);
+
 /* GP log-likelihood (eq. 1): -1/2 y^T C^{-1} y - 1/2 log det C - (n/2) log(2 pi).
  * y: device, n doubles.  out_host: host double (-INFINITY with HODLR_ENOTPD on failure). */
 hodlr_status gp_loglik(hodlr_t h, const double *y, double *out_host);

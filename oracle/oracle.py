@@ -120,6 +120,7 @@ class OracleHODLR:
         self._lib = _load()
         self.x = np.ascontiguousarray(x, dtype=np.float64)
         self.n = self.x.size
+        self.kernel, self.theta = int(kernel), (float(theta[0]), float(theta[1]))
         th = np.ascontiguousarray(theta, dtype=np.float64)
         h = C.c_void_p(0)
         _check(self._lib, self._lib.oracle_build(_ptr(self.x), self.n, int(kernel), _ptr(th), float(sigma2),
@@ -160,6 +161,21 @@ class OracleHODLR:
         out = np.zeros_like(v)
         _check(self._lib, self._lib.oracle_apply(self._h, _ptr(v), _ptr(out)))
         return out
+
+    def predict(self, y, xt, variance: bool = True):
+        """GP prediction at test points xt (eq_reg1 / eq_reg2) with this oracle's HODLR solve:
+        mean_j = k(xt_j, x) C^{-1} y; var_j = k(xt_j, xt_j) - k(xt_j, x) C^{-1} k(x, xt_j) (latent f, sigma^2 not
+        added).  Cross-covariances entry by entry from oracle_kernel (Table I); plain loops,
+        small cases only.  Requires factor()."""
+        xt = np.asarray(xt, dtype=np.float64)
+        alpha = self.solve(y)
+        Ks = np.array([[kernel_value(self.kernel, self.theta, float(t - xi)) for xi in self.x] for t in xt])
+        mean = Ks @ alpha
+        if not variance:
+            return mean, None
+        var = np.array([kernel_value(self.kernel, self.theta, 0.0) - Ks[j] @ self.solve(Ks[j])
+                        for j in range(xt.size)])
+        return mean, var
 
     @property
     def kappa(self) -> int:

@@ -391,6 +391,19 @@ hodlr_status hodlr_apply(hodlr_t h, const double *x, double *y, int64_t nrhs, in
   return finish(h, st, nullptr);
 }
 
+hodlr_status gp_predict(hodlr_t h, const double *y, const double *xt, int64_t m, double *mean, double *var) {
+  if (!h || !y || m < 0 || (m > 0 && (!xt || !mean))) return hodlr_set_error(HODLR_EINVAL, "predict: NULL argument or m < 0");
+  if (h->state == -1) return hodlr_set_error(HODLR_ENOTPD, "predict: factorization failed");
+  if (h->state != 2) return hodlr_set_error(HODLR_ESTATE, "predict: not factored");
+  if (h->nranks > 1) return hodlr_set_error(HODLR_EINVAL, "predict: sharded handles are not supported");
+  h->launches = 0;
+  cudaEventRecord(h->ev0, h->st);
+  hodlr_status st = hodlr_predict_impl(h, y, xt, m, mean, var);
+  st = finish(h, st, nullptr);
+  if (st != HODLR_OK) return st;
+  return check_y_flag(h);
+}
+
 hodlr_status hodlr_solve(hodlr_t h, const double *y, double *x, int64_t nrhs, int64_t ld) {
   if (!h || !y || !x) return hodlr_set_error(HODLR_EINVAL, "solve: NULL argument");
   if (h->state == -1) return hodlr_set_error(HODLR_ENOTPD, "solve: factorization failed");

@@ -188,6 +188,7 @@ struct hodlr_s {
   long long ph_calls[PH_N];
   void *allocs[64]; int nallocs;
   double *apply_ws = nullptr; size_t apply_ws_n = 0;   // hodlr_apply workspace (apply.cu)
+  double *pred_ws = nullptr; size_t pred_ws_n = 0;     // gp_predict workspace (predict.cu)
 };
 
 static inline void ph_begin(hodlr_s *h, int p, cudaStream_t s = nullptr) { cudaEventRecord(h->ph_ev[p][0], s ? s : h->st); }
@@ -208,6 +209,7 @@ hodlr_status hodlr_aca(hodlr_s *h);
 hodlr_status hodlr_factor_impl(hodlr_s *h);
 hodlr_status hodlr_leaf_factor_mma(hodlr_s *h, int K, double *Pi_leaf, bool *used);
 hodlr_status hodlr_apply_impl(hodlr_s *h, const double *x, double *y);
+hodlr_status hodlr_predict_impl(hodlr_s *h, const double *y, const double *xt, long long m, double *mean, double *var);
 hodlr_status hodlr_leaf_chol_mma(hodlr_s *h, cudaStream_t stream, bool *launched);
 hodlr_status hodlr_leaf_alloc(hodlr_s *h);
 hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_only);

@@ -18,7 +18,8 @@ HODLR_SE, HODLR_MATERN32, HODLR_MATERN52 = 0, 1, 2
 KERNELS = {"se": HODLR_SE, "matern32": HODLR_MATERN32, "matern52": HODLR_MATERN52}
 STATUS = {0: "OK", 1: "EINVAL", 2: "ENOTPD", 3: "ERANKCAP", 4: "ESTATE", 5: "ENOMEM", 6: "ECUDA", 7: "ENCCL"}
 
-EXPORTS = ("hodlr_build", "hodlr_factor", "hodlr_logdet", "hodlr_solve", "hodlr_apply", "gp_loglik", "hodlr_info",
+EXPORTS = ("hodlr_build", "hodlr_factor", "hodlr_logdet", "hodlr_solve", "hodlr_apply", "gp_predict", "gp_loglik",
+           "hodlr_info",
            "hodlr_get_order", "hodlr_get_tree", "hodlr_get_logdet_parts", "hodlr_free", "hodlr_last_error",
            "hodlr_version", "hodlr_launch_count", "hodlr_nccl_unique_id", "hodlr_group_create",
            "hodlr_group_destroy", "hodlr_dist_plan", "gp_loglik_sweep")
@@ -77,12 +78,13 @@ def load(build_if_missing: bool = True):
         lib.hodlr_logdet.argtypes = [P, P]
         lib.hodlr_solve.argtypes = [P, P, P, I64, I64]
         lib.hodlr_apply.argtypes = [P, P, P, I64, I64]
+        lib.gp_predict.argtypes = [P, P, P, I64, P, P]
         lib.gp_loglik.argtypes = [P, P, P]
         lib.hodlr_info.argtypes = [P, P]
         lib.hodlr_get_order.argtypes = [P, P, P]
         lib.hodlr_get_tree.argtypes = [P, P, P, P]
         lib.hodlr_get_logdet_parts.argtypes = [P, P, P]
-        for f in ("hodlr_build", "hodlr_factor", "hodlr_logdet", "hodlr_solve", "hodlr_apply", "gp_loglik",
+        for f in ("hodlr_build", "hodlr_factor", "hodlr_logdet", "hodlr_solve", "hodlr_apply", "gp_predict", "gp_loglik",
                   "hodlr_info", "hodlr_get_order", "hodlr_get_tree", "hodlr_get_logdet_parts"):
             getattr(lib, f).restype = I32
         lib.hodlr_free.argtypes = [P]; lib.hodlr_free.restype = None
@@ -163,6 +165,17 @@ def hodlr_apply(h: int, x: torch.Tensor) -> torch.Tensor:
     Y = torch.empty_like(X)
     _check(lib.hodlr_apply(h, X.data_ptr(), Y.data_ptr(), X.shape[0], X.shape[1]))
     return Y[0] if one else Y.t()
+
+
+def gp_predict(h: int, y: torch.Tensor, xt: torch.Tensor, variance: bool = True):
+    """Predictive mean (and latent variance) at test points xt (CUDA float64); returns (mean, var or None)."""
+    lib = load()
+    y = _dev_f64(y, "y"); xt = _dev_f64(xt, "xt")
+    mean = torch.empty_like(xt)
+    var = torch.empty_like(xt) if variance else None
+    _check(lib.gp_predict(h, y.data_ptr(), xt.data_ptr(), xt.numel(), mean.data_ptr(),
+                          var.data_ptr() if var is not None else None))
+    return mean, var
 
 
 def gp_loglik(h: int, y: torch.Tensor) -> float:
@@ -269,6 +282,9 @@ class HODLR:
 
     def apply(self, x: torch.Tensor) -> torch.Tensor:
         return hodlr_apply(self._h, x)
+
+    def predict(self, y: torch.Tensor, xt: torch.Tensor, variance: bool = True):
+        return gp_predict(self._h, y, xt, variance)
 
     def info(self) -> dict:
         return hodlr_info(self._h)

@@ -91,3 +91,12 @@ def scaled(cfg: Config, n: int) -> Config:
     """Same point density and kernel on a smaller n (interval shrunk in proportion)."""
     width = (cfg.hi - cfg.lo) * n / cfg.n
     return dataclasses.replace(cfg, n=n, hi=cfg.lo + width)
+
+
+def rmse_model(n: int = 1024, seed: int = 56):
+    """The sec. 5.6 regression data: x_j uniform in (-3, 3), y = sin(2x) + e^x / 8 + N(0, 1)
+    (sigma_eps = 1), seeded.  Returns (x, y) in generation order (unsorted)."""
+    rng = np.random.default_rng(seed)
+    x = rng.uniform(-3.0, 3.0, n)
+    y = np.sin(2.0 * x) + np.exp(x) / 8.0 + rng.standard_normal(n)
+    return x, y

@@ -362,3 +362,42 @@ def test_single_point():
     h = OracleHODLR(np.array([0.3]), MATERN52, (2.0, 1.0), 0.5, 64, 1e-12).factor()
     assert h.logdet() == pytest.approx(math.log(4.5), rel=1e-15)
     assert h.solve(np.array([9.0]))[0] == pytest.approx(2.0, rel=1e-15)
+
+
+# ---------------------------------------------------------------------------------------------------------------
+# NEXT-1: GP prediction (eq_reg1 / eq_reg2)
+def _cross(xt, x, kernel, theta):
+    """Independent numpy cross-covariance k(xt_j, x_i) (same Table I forms as dense_C)."""
+    xx = np.concatenate([np.asarray(xt, float), np.asarray(x, float)])
+    Cfull = dense_C(xx, kernel, theta, 0.0)
+    return Cfull[:len(xt), len(xt):]
+
+
+@pytest.mark.parametrize("kernel", [SE, MATERN32, MATERN52])
+def test_predict_vs_dense_gp(kernel):
+    """Oracle predict (HODLR solve + cross-covariances) against the dense GP posterior (numpy LAPACK solve on an
+    independently assembled C).  Catches: a wrong sign in the variance, sigma^2 added to the latent variance, a
+    transposed cross-covariance, alpha taken in sorted instead of original order."""
+    rng = np.random.default_rng(11 + kernel)
+    n, theta, s2 = 300, (1.3, 0.35), 1e-2
+    x = rng.uniform(0, 3, n); y = rng.standard_normal(n)
+    xt = rng.uniform(-0.2, 3.2, 17)
+    o = OracleHODLR(x, kernel, theta, s2, 16, 1e-13).factor()
+    mean, var = o.predict(y, xt)
+    C = dense_C(x, kernel, theta, s2)
+    Ks = _cross(xt, x, kernel, theta)
+    mean_d = Ks @ np.linalg.solve(C, y)
+    var_d = theta[0] ** 2 - np.einsum("ij,ji->i", Ks, np.linalg.solve(C, Ks.T))
+    np.testing.assert_allclose(mean, mean_d, rtol=1e-8, atol=1e-10)
+    np.testing.assert_allclose(var, var_d, rtol=1e-7, atol=1e-10)
+
+
+def test_predict_single_point_closed_form():
+    """n = 1: mean = k(t - x1) y / (a^2 + s2), var = a^2 - k(t - x1)^2 / (a^2 + s2) exactly (up to rounding)."""
+    a, ell, s2, x1, y1 = 1.7, 0.4, 0.3, 0.25, -1.2
+    o = OracleHODLR(np.array([x1]), SE, (a, ell), s2, 8, 1e-12).factor()
+    xt = np.array([0.25, 0.1, 1.5])
+    mean, var = o.predict(np.array([y1]), xt)
+    k = a * a * np.exp(-(xt - x1) ** 2 / (2 * ell * ell))
+    np.testing.assert_allclose(mean, k * y1 / (a * a + s2), rtol=1e-14)
+    np.testing.assert_allclose(var, a * a - k * k / (a * a + s2), rtol=1e-13, atol=1e-15)
