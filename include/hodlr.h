@@ -48,12 +48,17 @@ typedef enum {
   HODLR_ENCCL = 7      /* NCCL error (multi-GPU) */
 } hodlr_status;
 
-/* Covariance functions (Table I), theta = {a, ell}:
+/* Covariance functions (Table I), theta = {a, ell} (RQ: {a, ell, alpha}):
  *   SE:        a^2 exp(-d^2 / (2 ell^2))
  *   MATERN32:  a^2 (1 + s) exp(-s),          s = sqrt(3) |d| / ell
  *   MATERN52:  a^2 (1 + s + s^2/3) exp(-s),  s = sqrt(5) |d| / ell
+ *   EXP:       a^2 exp(-|d| / ell)            (Ornstein-Uhlenbeck, Table I; Table IV)
+ *   IMQ:       a^2 / sqrt(1 + d^2 / ell^2)    (inverse multiquadric, Table V)
+ *   RQ:        a^2 (1 + d^2 / ell^2)^-alpha   (rational quadratic, Table I), alpha = theta[2] > 0
+ * (NEXT-2 of SURVEY 8(f): the paper's other SPD 1-D kernels.)
  * C_ij = k(x_i - x_j) + sigma2 [i == j]. */
-typedef enum { HODLR_SE = 0, HODLR_MATERN32 = 1, HODLR_MATERN52 = 2 } hodlr_kernel;
+typedef enum { HODLR_SE = 0, HODLR_MATERN32 = 1, HODLR_MATERN52 = 2, HODLR_EXP = 3, HODLR_IMQ = 4,
+               HODLR_RQ = 5 } hodlr_kernel;
 
 /* Multi-GPU descriptor (subtree sharding, north_star).  NULL or nranks == 1 => one GPU.
  * nranks = P must be a power of two with P <= 2^kappa.  Rank g owns the depth-log2(P) node g (sorted rows

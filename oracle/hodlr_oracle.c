@@ -31,6 +31,9 @@ double oracle_kernel(int kernel, const double *theta, double d) {
     double t = d * d / (2.0 * ell * ell);
     return a * a * exp(-t);
   }
+  if (kernel == ORACLE_EXP) return a * a * exp(-fabs(d) / ell);              /* Table I / IV: a^2 e^{-|d|/ell} */
+  if (kernel == ORACLE_IMQ) return a * a / sqrt(1.0 + (d / ell) * (d / ell)); /* Table V */
+  if (kernel == ORACLE_RQ) return a * a * pow(1.0 + (d / ell) * (d / ell), -theta[2]);   /* Table I */
   double r = fabs(d);
   if (kernel == ORACLE_MATERN32) {                /* a^2 (1 + s) e^{-s}, s = sqrt(3) r / ell */
     double s = sqrt(3.0) * r / ell;
@@ -163,7 +166,7 @@ int oracle_aca_dense(const double *A, int64_t m1, int64_t m2, int64_t lda, doubl
 /* The handle                                                          */
 /* ------------------------------------------------------------------ */
 struct oracle_hodlr {
-  int64_t n; int kern; double theta[2]; double s2; int leaf; double eps; int cap;
+  int64_t n; int kern; double theta[3]; double s2; int leaf; double eps; int cap;
   int kappa; int64_t nnodes, ninternal, nleaves;
   double *xs; int64_t *perm;
   int64_t *lo, *hi;                 /* heap order: node (d,i) has id 2^d - 1 + i */
@@ -223,7 +226,8 @@ int oracle_build(const double *x, int64_t n, int kernel, const double *theta, do
                  int leaf, double eps, int rank_cap, oracle_hodlr **out) {
   *out = NULL;
   if (n < 1 || leaf < 1 || !(eps > 0.0 && eps < 1.0) || !(sigma2 >= 0.0) || !theta ||
-      !(theta[1] > 0.0) || !(theta[0] >= 0.0) || kernel < 0 || kernel > 2 || !isfinite(sigma2) ||
+      !(theta[1] > 0.0) || !(theta[0] >= 0.0) || kernel < 0 || kernel > 5 || (kernel == ORACLE_RQ && !(theta[2] > 0.0)) ||
+      !isfinite(sigma2) ||
       !isfinite(theta[0]) || !isfinite(theta[1]))
     return fail(ORACLE_EINVAL, "build: invalid argument");
   for (int64_t i = 0; i < n; i++)
@@ -231,6 +235,7 @@ int oracle_build(const double *x, int64_t n, int kernel, const double *theta, do
   oracle_hodlr *h = calloc(1, sizeof *h);
   if (!h) return fail(ORACLE_ENOMEM, "build: oom");
   h->n = n; h->kern = kernel; h->theta[0] = theta[0]; h->theta[1] = theta[1];
+  h->theta[2] = kernel == ORACLE_RQ ? theta[2] : 0.0;
   h->s2 = sigma2; h->leaf = leaf; h->eps = eps; h->cap = rank_cap;
   /* O1 */
   double *key = malloc(sizeof(double) * (size_t)n);

@@ -36,11 +36,11 @@ extern "C" {
 
 enum { ORACLE_OK = 0, ORACLE_EINVAL = 1, ORACLE_ENOTPD = 2, ORACLE_ERANKCAP = 3,
        ORACLE_ESTATE = 4, ORACLE_ENOMEM = 5 };
-enum { ORACLE_SE = 0, ORACLE_MATERN32 = 1, ORACLE_MATERN52 = 2 };
+enum { ORACLE_SE = 0, ORACLE_MATERN32 = 1, ORACLE_MATERN52 = 2, ORACLE_EXP = 3, ORACLE_IMQ = 4, ORACLE_RQ = 5 };
 
 typedef struct oracle_hodlr oracle_hodlr;
 
-/* O3: one kernel value k(r) for distance d = x_i - x_j (no noise term). theta = {a, ell}. */
+/* O3: one kernel value k(r) for distance d = x_i - x_j (no noise term). theta = {a, ell} ({a, ell, alpha} for RQ). */
 double oracle_kernel(int kernel, const double *theta, double d);
 
 /* O4 on an explicit dense m1 x m2 column-major block A (lda >= m1).

@@ -17,8 +17,8 @@ _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 _lock = threading.Lock()
 _lib = None
 
-SE, MATERN32, MATERN52 = 0, 1, 2
-KERNELS = {"se": SE, "matern32": MATERN32, "matern52": MATERN52}
+SE, MATERN32, MATERN52, EXP, IMQ, RQ = 0, 1, 2, 3, 4, 5
+KERNELS = {"se": SE, "matern32": MATERN32, "matern52": MATERN52, "exp": EXP, "imq": IMQ, "rq": RQ}
 STATUS = {0: "OK", 1: "EINVAL", 2: "ENOTPD", 3: "ERANKCAP", 4: "ESTATE", 5: "ENOMEM"}
 
 
@@ -120,7 +120,7 @@ class OracleHODLR:
         self._lib = _load()
         self.x = np.ascontiguousarray(x, dtype=np.float64)
         self.n = self.x.size
-        self.kernel, self.theta = int(kernel), (float(theta[0]), float(theta[1]))
+        self.kernel, self.theta = int(kernel), tuple(float(v) for v in theta)
         th = np.ascontiguousarray(theta, dtype=np.float64)
         h = C.c_void_p(0)
         _check(self._lib, self._lib.oracle_build(_ptr(self.x), self.n, int(kernel), _ptr(th), float(sigma2),

@@ -164,7 +164,9 @@ hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const 
   if (!(sigma2 >= 0.0) || !isfinite(sigma2)) return hodlr_set_error(HODLR_EINVAL, "build: sigma2 = %g", sigma2);
   if (!(theta[1] > 0.0) || !isfinite(theta[1])) return hodlr_set_error(HODLR_EINVAL, "build: ell = %g <= 0", theta[1]);
   if (!(theta[0] >= 0.0) || !isfinite(theta[0])) return hodlr_set_error(HODLR_EINVAL, "build: a = %g < 0", theta[0]);
-  if ((int)kernel < 0 || (int)kernel > 2) return hodlr_set_error(HODLR_EINVAL, "build: unknown kernel %d", (int)kernel);
+  if ((int)kernel < 0 || (int)kernel > 5) return hodlr_set_error(HODLR_EINVAL, "build: unknown kernel %d", (int)kernel);
+  if (kernel == HODLR_RQ && (!(theta[2] > 0.0) || !isfinite(theta[2])))
+    return hodlr_set_error(HODLR_EINVAL, "build: rational quadratic alpha = %g <= 0", theta[2]);
   int cap = (opts && opts->rank_cap > 0) ? opts->rank_cap : 48;
   if (cap > ACA_MAXCAP) return hodlr_set_error(HODLR_EINVAL, "build: rank_cap %d > %d", cap, ACA_MAXCAP);
   hodlr_s *h = new (std::nothrow) hodlr_s();
@@ -181,7 +183,10 @@ hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const 
   h->n = n; h->leaf = leaf; h->eps = eps; h->cap = cap; h->theta[0] = theta[0]; h->theta[1] = theta[1];
   h->kp.kern = (int)kernel; h->kp.a2 = theta[0] * theta[0]; h->kp.s2 = sigma2;
   h->kp.c = kernel == HODLR_SE ? 1.0 / (2.0 * theta[1] * theta[1])
-                               : (kernel == HODLR_MATERN32 ? sqrt(3.0) : sqrt(5.0)) / theta[1];
+          : kernel == HODLR_MATERN32 ? sqrt(3.0) / theta[1]
+          : kernel == HODLR_MATERN52 ? sqrt(5.0) / theta[1]
+          : kernel == HODLR_EXP ? 1.0 / theta[1] : 1.0 / (theta[1] * theta[1]);
+  h->kp.alpha = kernel == HODLR_RQ ? theta[2] : 0.5;
   // O2-equivalent tree: kappa = largest integer with leaf * 2^kappa <= n
   int kappa = 0;
   while (((long long)leaf << (kappa + 1)) <= n && kappa < HODLR_MAXDEPTH - 2) kappa++;

@@ -38,10 +38,15 @@
 // (PAPER.md:1251-1256).  kp = {a^2, c} with c = 1/(2 ell^2) for SE, sqrt(3)/ell or sqrt(5)/ell
 // for Matern-3/2 and -5/2.
 // ----------------------------------------------------------------------------------------------
-struct KParams { int kern; double a2; double c; double s2; };
+struct KParams { int kern; double a2; double c; double s2; double alpha; };
 
 __device__ __forceinline__ double kval(const KParams &kp, double d) {
   if (kp.kern == HODLR_SE) return kp.a2 * exp(-(d * d) * kp.c);
+  if (kp.kern >= HODLR_EXP) {                 // NEXT-2 kernels: c = 1/ell (EXP), 1/ell^2 (IMQ, RQ)
+    if (kp.kern == HODLR_EXP) return kp.a2 * exp(-fabs(d) * kp.c);
+    const double u = fma(d * d, kp.c, 1.0);
+    return kp.kern == HODLR_IMQ ? kp.a2 / sqrt(u) : kp.a2 * pow(u, -kp.alpha);
+  }
   double s = fabs(d) * kp.c;
   double e = exp(-s);
   if (kp.kern == HODLR_MATERN32) return kp.a2 * (1.0 + s) * e;

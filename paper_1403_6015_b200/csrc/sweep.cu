@@ -14,6 +14,7 @@ extern "C" hodlr_status gp_loglik_sweep(const double *x, const double *y, int64_
                                         const double *thetas, const double *sigma2s, int32_t B, int32_t leaf,
                                         double eps, const hodlr_dist *dist, void *cuda_stream, int32_t workers,
                                         double *out_host) {
+  if (kernel == HODLR_RQ) return hodlr_set_error(HODLR_EINVAL, "sweep: the rational quadratic (3 parameters) is not supported");
   if (!x || !y || !thetas || !sigma2s || !out_host || B < 1 || n < 1)
     return hodlr_set_error(HODLR_EINVAL, "gp_loglik_sweep: bad arguments");
   int dev = 0;

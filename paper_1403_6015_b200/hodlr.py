@@ -14,8 +14,9 @@ import torch
 
 from . import build as _build
 
-HODLR_SE, HODLR_MATERN32, HODLR_MATERN52 = 0, 1, 2
-KERNELS = {"se": HODLR_SE, "matern32": HODLR_MATERN32, "matern52": HODLR_MATERN52}
+HODLR_SE, HODLR_MATERN32, HODLR_MATERN52, HODLR_EXP, HODLR_IMQ, HODLR_RQ = 0, 1, 2, 3, 4, 5
+KERNELS = {"se": HODLR_SE, "matern32": HODLR_MATERN32, "matern52": HODLR_MATERN52, "exp": HODLR_EXP,
+           "imq": HODLR_IMQ, "rq": HODLR_RQ}
 STATUS = {0: "OK", 1: "EINVAL", 2: "ENOTPD", 3: "ERANKCAP", 4: "ESTATE", 5: "ENOMEM", 6: "ECUDA", 7: "ENCCL"}
 
 EXPORTS = ("hodlr_build", "hodlr_factor", "hodlr_logdet", "hodlr_solve", "hodlr_apply", "gp_predict", "gp_loglik",
@@ -122,7 +123,7 @@ def hodlr_build(x: torch.Tensor, kernel: int, theta, sigma2: float, leaf: int, e
                 rank_cap: int = 0, stream=None, dist: "hodlr_dist | None" = None) -> int:
     lib = load()
     x = _dev_f64(x, "x")
-    th = (C.c_double * 2)(float(theta[0]), float(theta[1]))
+    th = (C.c_double * 3)(float(theta[0]), float(theta[1]), float(theta[2]) if len(theta) > 2 else 0.0)
     opts = hodlr_opts(int(rank_cap))
     h = C.c_void_p(0)
     _check(lib.hodlr_build(x.data_ptr(), x.numel(), int(kernel), th, float(sigma2), int(leaf), float(eps),

@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 import scipy.special as sps
 
-from oracle import (SE, MATERN32, MATERN52, OracleHODLR, OracleError, aca_dense, dense_check,
+from oracle import (SE, MATERN32, MATERN52, EXP, IMQ, RQ, OracleHODLR, OracleError, aca_dense, dense_check,
                     kernel_value)
 
 GOLD = {}
@@ -26,10 +26,18 @@ with open(os.path.join(os.path.dirname(__file__), "golden", "closed_forms.txt"))
 
 def dense_C(x, kernel, theta, s2):
     """Independent numpy assembly of C = s2 I + K (Table I formulas)."""
-    a, ell = theta
+    a, ell = theta[0], theta[1]
     d = np.abs(x[:, None] - x[None, :])
     if kernel == SE:
         K = a * a * np.exp(-d * d / (2 * ell * ell))
+    elif kernel == EXP:      # Table I Ornstein-Uhlenbeck = Matern-1/2 (Bessel form with nu = 1/2)
+        z = d / ell
+        with np.errstate(invalid="ignore"):
+            K = a * a * (2 ** 0.5 / sps.gamma(0.5)) * z ** 0.5 * sps.kv(0.5, z)
+        K[d == 0] = a * a
+    elif kernel in (IMQ, RQ):  # rational quadratic (IMQ: alpha = 1/2) via exp(-alpha log1p(.))
+        alpha = 0.5 if kernel == IMQ else theta[2]
+        K = a * a * np.exp(-alpha * np.log1p((d / ell) ** 2))
     else:   # Table I Matern through the Bessel form -- a different formula from the oracle's closed form
         nu = 1.5 if kernel == MATERN32 else 2.5
         z = np.sqrt(2 * nu) * d / ell
@@ -261,6 +269,9 @@ CASES = [
 
 
 CASES.append(("exact-duplicates", 3000, 0.0, 12.0, SE, (1.3, 0.7), 1e-2, 64))
+CASES += [("exp-ou", 2048, 0.0, 8.0, EXP, (1.1, 0.5), 1e-2, 64),            # NEXT-2 kernels (Tables I, IV, V)
+          ("imq", 1500, -3.0, 3.0, IMQ, (1.0, 0.3), 1e-1, 40),
+          ("rq-1.5", 1800, 0.0, 5.0, RQ, (0.9, 0.4, 1.5), 1e-2, 48)]
 
 
 @pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
@@ -401,3 +412,23 @@ def test_predict_single_point_closed_form():
     k = a * a * np.exp(-(xt - x1) ** 2 / (2 * ell * ell))
     np.testing.assert_allclose(mean, k * y1 / (a * a + s2), rtol=1e-14)
     np.testing.assert_allclose(var, a * a - k * k / (a * a + s2), rtol=1e-13, atol=1e-15)
+
+
+@pytest.mark.parametrize("kernel,theta,expect", [
+    (EXP, (1.3, 0.7), 1.3 ** 2 * math.exp(-1.0)),          # d = ell: a^2 e^-1
+    (IMQ, (1.3, 0.7), 1.3 ** 2 / math.sqrt(2.0)),          # d = ell: a^2 / sqrt 2
+    (RQ, (1.3, 0.7, 1.5), 1.3 ** 2 * 2.0 ** -1.5),         # d = ell: a^2 2^-alpha
+])
+def test_next2_kernel_closed_forms(kernel, theta, expect):
+    """NEXT-2 covariance functions at d = ell and d = 0 (closed forms): a wrong scale (ell vs ell^2, 2 ell^2), a
+    missing amplitude or exponent sign fails."""
+    assert kernel_value(kernel, theta, theta[1]) == pytest.approx(expect, rel=1e-15)
+    assert kernel_value(kernel, theta, -theta[1]) == pytest.approx(expect, rel=1e-15)
+    assert kernel_value(kernel, theta, 0.0) == pytest.approx(theta[0] ** 2, rel=1e-15)
+
+
+def test_rq_alpha_half_is_imq():
+    for d in (0.0, 0.1, 1.7, -4.0):
+        assert kernel_value(RQ, (1.2, 0.6, 0.5), d) == pytest.approx(kernel_value(IMQ, (1.2, 0.6), d), rel=1e-15)
+    with pytest.raises(OracleError):
+        OracleHODLR(np.linspace(0, 1, 10), RQ, (1.0, 0.5, -1.0), 1e-2, 4, 1e-10)
