@@ -88,7 +88,7 @@ __device__ __forceinline__ void block_argmax_n2(double &ba, long long &bi, doubl
 constexpr int ACA_E = 4;                       // elements per thread per sub-tile
 constexpr int ACA_TILE = ACA_SUB * ACA_E;
 
-template <bool ROW>
+template <bool ROW, bool SEO>
 __global__ void __launch_bounds__(ACA_SUB, 2) k_aca_pass(const AcaCtx *__restrict__ pc) {
   __shared__ AcaCtx c;                         // context in shared memory: global stores cannot alias it
   for (int i = threadIdx.x; i < (int)(sizeof(AcaCtx) / 8); i += ACA_SUB) ((long long *)&c)[i] = ((const long long *)pc)[i];
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(ACA_SUB, 2) k_aca_pass(const AcaCtx *__restric
         usedm = (u4.x ? 1u : 0u) | (u4.y ? 2u : 0u) | (u4.z ? 4u : 0u) | (u4.w ? 8u : 0u);
         const double xq[4] = {x01.x, x01.y, x23.x, x23.y};
 #pragma unroll
-        for (int q = 0; q < 4; q++) a[q] = kval(c.kp, ROW ? xp - xq[q] : xq[q] - xp);
+        for (int q = 0; q < 4; q++) a[q] = kval_t<SEO>(c.kp, ROW ? xp - xq[q] : xq[q] - xp);
       } else {
 #pragma unroll
         for (int q = 0; q < 4; q++) a[q] = 0.0;
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(ACA_SUB, 2) k_aca_pass(const AcaCtx *__restric
     for (int q = 0; q < ACA_E; q++) {
       const double xq = q < nval ? xsp[q * ACA_SUB] : xp;
       if (q < nval && up[q * ACA_SUB]) usedm |= 1u << q;
-      a[q] = q < nval ? kval(c.kp, ROW ? xp - xq : xq - xp) : 0.0;
+      a[q] = q < nval ? kval_t<SEO>(c.kp, ROW ? xp - xq : xq - xp) : 0.0;
       r[q] = a[q];
     }
     const double *colp = slot + g0;
@@ -354,6 +354,7 @@ __global__ void __launch_bounds__(ACA_SUB, 2) k_aca_pass(const AcaCtx *__restric
 // block (same arithmetic and conventions as the row/column passes above, block-level reductions,
 // pivot bookkeeping in shared memory).  Runs concurrently with the step-synchronous big blocks.
 // ---------------------------------------------------------------------------------------------
+template <bool SEO>
 __global__ void __launch_bounds__(ACA_SUB) k_aca_fused(AcaCtx c, const int *blocks, int *flags) {
   __shared__ double vbuf[ACA_FUSED_MAX];
   __shared__ unsigned char usedR[ACA_FUSED_MAX], usedC[ACA_FUSED_MAX];
@@ -390,7 +391,7 @@ __global__ void __launch_bounds__(ACA_SUB) k_aca_fused(AcaCtx c, const int *bloc
     double ba = 0.0, bv = 0.0, n2 = 0.0; long long bi = -1;
     for (long long j = t; j < m2; j += ACA_SUB) {
       const long long gj = lo2 + j;
-      double v = kval(c.kp, xi - c.xs[gj]);
+      double v = kval_t<SEO>(c.kp, xi - c.xs[gj]);
 #pragma unroll 8
       for (int l = 0; l < k; l++) v -= Ui[l] * __ldcg(slot + (long long)l * ldx + gj);
       slot[(long long)k * ldx + gj] = v;
@@ -421,7 +422,7 @@ __global__ void __launch_bounds__(ACA_SUB) k_aca_fused(AcaCtx c, const int *bloc
     ba = 0.0; bv = 0.0; n2 = 0.0; bi = -1;
     for (long long i = t; i < m1; i += ACA_SUB) {
       const long long gi = lo1 + i;
-      double u = kval(c.kp, c.xs[gi] - xj);
+      double u = kval_t<SEO>(c.kp, c.xs[gi] - xj);
 #pragma unroll 8
       for (int l = 0; l < k; l++) u -= Ui[l] * __ldcg(slot + (long long)l * ldx + gi);
       u *= rp;
@@ -483,7 +484,7 @@ __global__ void k_aca_cond(cudaGraphConditionalHandle hdl, const AcaCtx *__restr
 // same shape skip the planning and the graph instantiation.  A plan in use by another build is not shared.
 // ---------------------------------------------------------------------------------------------
 struct AcaPlan {
-  long long n; int leaf; int rank, nranks;
+  long long n; int leaf; int rank, nranks; bool seo;
   long long nb; int nbig;
   std::vector<int> fused_blocks;
   size_t nitems_r = 0, nitems_c = 0;
@@ -570,12 +571,12 @@ static cudaError_t plan_create(AcaPlan *P, const hodlr_s *h) {
   if (e == cudaSuccess) {
     cudaGraph_t body = cpar.conditional.phGraph_out[0];
     cudaKernelNodeParams k1 = {};
-    k1.func = (void *)k_aca_pass<true>; k1.gridDim = dim3((unsigned)P->nitems_r); k1.blockDim = dim3(ACA_SUB);
+    k1.func = P->seo ? (void *)k_aca_pass<true, true> : (void *)k_aca_pass<true, false>; k1.gridDim = dim3((unsigned)P->nitems_r); k1.blockDim = dim3(ACA_SUB);
     k1.kernelParams = arow;
     e = cudaGraphAddKernelNode(&n1, body, nullptr, 0, &k1);
     if (e == cudaSuccess) {
       cudaKernelNodeParams k2 = {};
-      k2.func = (void *)k_aca_pass<false>; k2.gridDim = dim3((unsigned)P->nitems_c); k2.blockDim = dim3(ACA_SUB);
+      k2.func = P->seo ? (void *)k_aca_pass<false, true> : (void *)k_aca_pass<false, false>; k2.gridDim = dim3((unsigned)P->nitems_c); k2.blockDim = dim3(ACA_SUB);
       k2.kernelParams = acol;
       e = cudaGraphAddKernelNode(&n2, body, &n1, 1, &k2);
     }
@@ -594,12 +595,14 @@ static AcaPlan *plan_acquire(const hodlr_s *h, hodlr_status *st) {
   {
     std::lock_guard<std::mutex> lk(g_plan_mu);
     for (AcaPlan *P : g_plans)
-      if (!P->busy && P->n == h->n && P->leaf == h->leaf && P->rank == h->grank && P->nranks == h->nranks) {
+      if (!P->busy && P->n == h->n && P->leaf == h->leaf && P->rank == h->grank && P->nranks == h->nranks &&
+          P->seo == (h->kp.kern == HODLR_SE)) {
         P->busy = true; return P;
       }
   }
   AcaPlan *P = new AcaPlan();
   P->n = h->n; P->leaf = h->leaf; P->rank = h->grank; P->nranks = h->nranks; P->nb = h->ninternal; P->busy = true;
+  P->seo = h->kp.kern == HODLR_SE;
   cudaError_t e = plan_create(P, h);
   if (e != cudaSuccess) { *st = hodlr_cuda_check(e, "aca plan"); return nullptr; }   // (leaked on error)
   std::lock_guard<std::mutex> lk(g_plan_mu);
@@ -656,7 +659,8 @@ hodlr_status hodlr_aca(hodlr_s *h) {
   if (!P->fused_blocks.empty()) {
     HCUDA(cudaEventRecord(h->ev_fork, h->st));
     HCUDA(cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
-    k_aca_fused<<<(int)P->fused_blocks.size(), ACA_SUB, 0, h->st2>>>(c, P->d_fused, h->dflags);
+    if (P->seo) k_aca_fused<true><<<(int)P->fused_blocks.size(), ACA_SUB, 0, h->st2>>>(c, P->d_fused, h->dflags);
+    else k_aca_fused<false><<<(int)P->fused_blocks.size(), ACA_SUB, 0, h->st2>>>(c, P->d_fused, h->dflags);
     HLAUNCH(h, "k_aca_fused");
     HCUDA(cudaEventRecord(h->ev_join, h->st2));
   }
@@ -665,9 +669,11 @@ hodlr_status hodlr_aca(hodlr_s *h) {
   if (nograph < 0) { const char *ev = getenv("HODLR_ACA_NOGRAPH"); nograph = ev && atoi(ev) ? 1 : 0; }
   if (nbig > 0 && nograph) {
     for (steps = 1; steps <= h->cap + 1; steps++) {
-      k_aca_pass<true><<<(unsigned)P->nitems_r, ACA_SUB, 0, h->st>>>(P->d_ctx);
+      if (P->seo) k_aca_pass<true, true><<<(unsigned)P->nitems_r, ACA_SUB, 0, h->st>>>(P->d_ctx);
+      else k_aca_pass<true, false><<<(unsigned)P->nitems_r, ACA_SUB, 0, h->st>>>(P->d_ctx);
       HLAUNCH(h, "k_aca_pass<row>");
-      k_aca_pass<false><<<(unsigned)P->nitems_c, ACA_SUB, 0, h->st>>>(P->d_ctx + 1);
+      if (P->seo) k_aca_pass<false, true><<<(unsigned)P->nitems_c, ACA_SUB, 0, h->st>>>(P->d_ctx + 1);
+      else k_aca_pass<false, false><<<(unsigned)P->nitems_c, ACA_SUB, 0, h->st>>>(P->d_ctx + 1);
       HLAUNCH(h, "k_aca_pass<col>");
       int act = 0;
       HCUDA(cudaMemcpyAsync(&act, h->dflags + 4, sizeof(int), cudaMemcpyDeviceToHost, h->st));

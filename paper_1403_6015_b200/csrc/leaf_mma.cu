@@ -148,7 +148,7 @@ __device__ unsigned long long g_chol_stamps[2][6];
 #else
 #define CSTAMP(k)
 #endif
-template <int P>
+template <int P, bool SEO>
 __global__ void __launch_bounds__(NTH, 2) k_leaf_chol(LeafMmaCtx c) {
   constexpr int T = P / 8;
   constexpr int NTILE = T * (T + 1) / 2;
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(NTH, 2) k_leaf_chol(LeafMmaCtx c) {
       const int r = lane >> 2, cc = (lane & 3) + 4 * h;
       const int i = 8 * I + r, j = 8 * J + cc;
       double v;
-      if (i < m && j < m) { v = kval(c.kp, sx[i] - sx[j]); if (i == j) v += c.kp.s2; }
+      if (i < m && j < m) { v = kval_t<SEO>(c.kp, sx[i] - sx[j]); if (i == j) v += c.kp.s2; }
       else v = (i == j) ? 1.0 : 0.0;
       sL[ti * 64 + 32 * h + lane] = v;
     }
@@ -808,13 +808,15 @@ hodlr_status hodlr_leaf_chol_mma(hodlr_s *h, cudaStream_t stream, bool *launched
   const int T = P / 8, NTILE = T * (T + 1) / 2;
   const size_t smem = sizeof(double) * ((size_t)NTILE * 64 + T * 64 + 2 * P);
   LeafMmaCtx c = leaf_ctx(h, 0, nullptr);
-  if (P == 64) {
-    HCUDA(cudaFuncSetAttribute(k_leaf_chol<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_leaf_chol<64><<<(int)(h->nleaves >> h->tsplit), NTH, smem, stream>>>(c);
-  } else {
-    HCUDA(cudaFuncSetAttribute(k_leaf_chol<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_leaf_chol<128><<<(int)(h->nleaves >> h->tsplit), NTH, smem, stream>>>(c);
-  }
+#define LAUNCH_CHOL(PP, SE_)                                                                                    \
+  do {                                                                                                         \
+    HCUDA(cudaFuncSetAttribute(k_leaf_chol<PP, SE_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));  \
+    k_leaf_chol<PP, SE_><<<(int)(h->nleaves >> h->tsplit), NTH, smem, stream>>>(c);                           \
+  } while (0)
+  const bool seo = h->kp.kern == HODLR_SE;
+  if (P == 64) { if (seo) LAUNCH_CHOL(64, true); else LAUNCH_CHOL(64, false); }
+  else { if (seo) LAUNCH_CHOL(128, true); else LAUNCH_CHOL(128, false); }
+#undef LAUNCH_CHOL
   HLAUNCH(h, "k_leaf_chol");
 #ifdef CHOL_TRACE
   {
