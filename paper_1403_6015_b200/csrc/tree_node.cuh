@@ -158,12 +158,26 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
       }
       const double ip = piv != 0.0 ? 1.0 / piv : 0.0;
       const double *prow = Wa + p * q2;
-      for (int e = t; e < q * q2; e += NT) {
-        const int a = e / q2, j = e - a * q2;
-        if (a == k) Wb[e] = prow[j] * ip;
-        else {
-          const int sa = a == p ? k : a;       // rows k and p swap before the elimination
-          Wb[e] = fma(-Wa[sa * q2 + k] * ip, prow[j], Wa[sa * q2 + j]);
+      if (q2 <= 64) {                          // thread = (column j, every NT/64-th row): no index division
+        const int j = t & 63;
+        if (j < q2) {
+          const double pj = prow[j];
+          for (int a = t >> 6; a < q; a += NT >> 6) {
+            if (a == k) Wb[a * q2 + j] = pj * ip;
+            else {
+              const int sa = a == p ? k : a;   // rows k and p swap before the elimination
+              Wb[a * q2 + j] = fma(-Wa[sa * q2 + k] * ip, pj, Wa[sa * q2 + j]);
+            }
+          }
+        }
+      } else {
+        for (int e = t; e < q * q2; e += NT) {
+          const int a = e / q2, j = e - a * q2;
+          if (a == k) Wb[e] = prow[j] * ip;
+          else {
+            const int sa = a == p ? k : a;     // rows k and p swap before the elimination
+            Wb[e] = fma(-Wa[sa * q2 + k] * ip, prow[j], Wa[sa * q2 + j]);
+          }
         }
       }
       __syncthreads();
