@@ -266,6 +266,18 @@ def fp64_peak_tflops(peaks, sm_mhz):
         return 148 * 64 * 2 * f / 1e12, f"derived: 148 SMs x 64 FP64 FMA/clk x 2 x {f / 1e6:.0f} MHz"
 
 
+def dfma_peak_tflops(sm_mhz):
+    """Plain FP64 FMA (DFMA) peak for ALU-bound kernels: the DFMA-only microbenchmark (tools/fp64_peak.cu,
+    profiles/fp64_peak_r01.json, 33.37 TFLOP/s at 1965 MHz); else 148 SMs x 64 FP64 lanes x 2 x clock."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak_r01.json")) as f:
+            v = json.load(f)["fp64_dfma_tflops"]
+        return v, "measured DFMA peak, tools/fp64_peak.cu (profiles/fp64_peak_r01.json), 1965 MHz"
+    except (OSError, KeyError, ValueError):
+        f = (sm_mhz or 1965.0) * 1e6
+        return 148 * 64 * 2 * f / 1e12, f"derived: 148 SMs x 64 FP64 lanes x 2 x {f / 1e6:.0f} MHz"
+
+
 # ------------------------------------------------------------------ our arm
 def run_ours(args):
     import torch
@@ -384,6 +396,7 @@ def run_ours(args):
     # ---------------- rooflines: algorithmic work / live event time per kernel family; dominant = longest
     alg = algorithmic(info, n, cfg.leaf)
     fp64_peak, fp64_how = fp64_peak_tflops(peaks, clocks.get("sm_mhz"))
+    dfma_peak, dfma_how = dfma_peak_tflops(clocks.get("sm_mhz"))
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     traffic, traffic_src = ncu_traffic()
     rows = []
@@ -395,6 +408,8 @@ def run_ours(args):
         t_launch = ms / calls / 1e3
         if bound == "hbm":
             ach, peak, u = amount / t_launch / 1e9, hbm_peak, "GB/s"
+        elif bound == "alu":       # plain FP64 FMA pipe (DFMA), not the DMMA tensor path
+            ach, peak, u = amount / t_launch / 1e12, dfma_peak, "TFLOP/s"
         else:
             ach, peak, u = amount / t_launch / 1e12, fp64_peak, "TFLOP/s"
         kk = kname.split("/")[0]
@@ -407,7 +422,8 @@ def run_ours(args):
     main = [r_ for r_ in rows if r_["family"] != "leaf_chol"]     # leaf_chol runs on a side stream under the ACA
     dom = max(main, key=lambda r_: r_["ms"])
     roof = dict(dom)
-    roof["peak_source"] = ("MEASURED_PEAKS.json hbm_gbs" if dom["bound"] == "hbm" else fp64_how)
+    roof["peak_source"] = ("MEASURED_PEAKS.json hbm_gbs" if dom["bound"] == "hbm"
+                           else (dfma_how if dom["bound"] == "alu" else fp64_how))
     roof["traffic_source"] = traffic_src
     roof["all_kernels"] = rows
     cpu = None
