@@ -193,6 +193,30 @@ def test_full_size_cfg3_bench_config(hb):
     assert abs(ld_g - o.logdet()) <= LD_TOL * abs(o.logdet())
 
 
+def test_full_size_cfg5_one_gpu(hb):
+    """BASELINE.json config 5 at full size (n = 2^23, 5% clustered duplicates, eps = 1e-10) on one GPU: sampled
+    rows of the residual C x - y computed one by one on the CPU (the oracle needs minutes at this size), and the
+    log det of a shuffled copy of the input equals that of the sorted input bit for bit (the stable sort makes
+    the factorization independent of the input order, ties included)."""
+    cfg = inputs.CONFIGS["cfg5"]
+    x = inputs.points(cfg); y = inputs.rhs(cfg)
+    xd = torch.from_numpy(x).cuda()
+    g = hb.HODLR(xd, cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, cfg.eps).factor()
+    ld_g = g.logdet()
+    xg = g.solve(torch.from_numpy(y).cuda()).cpu().numpy()
+    g.close()
+    rng = np.random.default_rng(321)
+    for i in rng.choice(cfg.n, 32, replace=False):
+        ci = np.exp(-(x[i] - x) ** 2 / (2 * cfg.ell ** 2)) * cfg.a ** 2
+        ci[i] += cfg.sigma2
+        assert abs(ci @ xg - y[i]) <= 1e-6 * np.abs(y).max(), i
+    perm = rng.permutation(cfg.n)
+    g2 = hb.HODLR(xd[torch.from_numpy(perm).cuda()].contiguous(), cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf,
+                  cfg.eps).factor()
+    assert g2.logdet() == ld_g
+    g2.close()
+
+
 def test_full_size_cfg3_parity_eps12(hb):
     """Config 3 at full size (n = 2^20) at the parity epsilon 1e-12 (north_star): log det <= 1e-9 relative to the
     oracle; the solve agrees to the measured floor of the approximation (R15: both solutions have
