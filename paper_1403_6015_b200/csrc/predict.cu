@@ -10,17 +10,28 @@ namespace {
 
 constexpr int PB = 32;           // test points per variance batch
 
-// mean_j = sum_i k(xt_j - xs_i) alpha[perm[i]]: one warp per test point, lanes over the sorted points.
-__global__ void k_predict_mean(KParams kp, const double *xs, const long long *perm, long long n,
-                               const double *alpha, const double *xt, long long m, double *mean) {
-  const long long j = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (j >= m) return;
-  const double x0 = xt[j];
+// mean_j = sum_i k(xt_j - xs_i) alpha[perm[i]]: a CTA takes MT test points; the sorted points and their alpha are
+// staged in shared memory in chunks and reused by all MT test points (thread (test point, lane) over the chunk),
+// fixed-order warp reductions.
+constexpr int MT = 8;            // test points per CTA (one warp each)
+constexpr int MCH = 2048;        // points per staged chunk
+__global__ void __launch_bounds__(MT * 32) k_predict_mean(KParams kp, const double *xs, const long long *perm,
+                                                          long long n, const double *alpha, const double *xt,
+                                                          long long m, double *mean) {
+  __shared__ double sx[MCH], sa[MCH];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const long long j = (long long)blockIdx.x * MT + w;
+  const double x0 = j < m ? xt[j] : 0.0;
   double s = 0.0;
-  for (long long i = lane; i < n; i += 32) s = fma(kval(kp, x0 - xs[i]), alpha[perm[i]], s);
+  for (long long c0 = 0; c0 < n; c0 += MCH) {
+    const int len = (int)(n - c0 < MCH ? n - c0 : MCH);
+    __syncthreads();
+    for (int i = threadIdx.x; i < len; i += MT * 32) { sx[i] = xs[c0 + i]; sa[i] = alpha[perm[c0 + i]]; }
+    __syncthreads();
+    for (int i = lane; i < len; i += 32) s = fma(kval(kp, x0 - sx[i]), sa[i], s);
+  }
   s = warp_sum(s);
-  if (lane == 0) mean[j] = s;
+  if (lane == 0 && j < m) mean[j] = s;
 }
 
 // Kx[:, b] = k(x - xt_{j0 + b}) in the caller's original order (column-major, leading dimension n).
@@ -65,8 +76,7 @@ hodlr_status hodlr_predict_impl(hodlr_s *h, const double *y, const double *xt, l
   hodlr_status st = hodlr_solve_impl(h, y, alpha, false);
   if (st != HODLR_OK) return st;
   if (m > 0) {
-    const long long thr = m * 32;
-    k_predict_mean<<<(unsigned)((thr + 255) / 256), 256, 0, h->st>>>(h->kp, h->xs, h->perm, n, alpha, xt, m, mean);
+    k_predict_mean<<<(unsigned)((m + MT - 1) / MT), MT * 32, 0, h->st>>>(h->kp, h->xs, h->perm, n, alpha, xt, m, mean);
     HLAUNCH(h, "k_predict_mean");
   }
   if (var) {
