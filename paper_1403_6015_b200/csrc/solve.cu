@@ -556,14 +556,27 @@ __device__ void tree_up_node(const SolveCtx &c, int d, long long i, double *scr,
     acc_dd(A, c.hv[2 * node], c.hv[2 * node + 1]);
   }
   double *gc = c.V + c.dt->nodeV[d] + i * (long long)Kd;
-  for (int a = lane; a < Kd; a += 32) {
-    Acc2 A = acc2(g1[a]);
-    acc_add(A, g2[a]);
-#pragma unroll 4
-    for (int u = 0; u < r; u++) acc_fma_dd(A, -B[(long long)(r + u) * Kd + a], th[u], tl[u]);
-#pragma unroll 4
-    for (int u = 0; u < r; u++) acc_fma_dd(A, -B[(long long)u * Kd + a], th[r + u], tl[r + u]);
-    gc[a] = acc_val(A);
+  // 4 entries a per lane at once (a = a0 + 32 x): the B loads of all four are independent and issued together
+  for (int a0 = lane; a0 < Kd; a0 += 128) {
+    Acc2 A[4];
+#pragma unroll
+    for (int x = 0; x < 4; x++) {
+      const int a = a0 + 32 * x;
+      A[x] = acc2(a < Kd ? g1[a] : 0.0);
+      acc_add(A[x], a < Kd ? g2[a] : 0.0);
+    }
+    for (int u = 0; u < r; u++) {
+      double b1[4], b2[4];
+#pragma unroll
+      for (int x = 0; x < 4; x++) {
+        const int a = a0 + 32 * x, ac = a < Kd ? a : 0;
+        b1[x] = B[(long long)(r + u) * Kd + ac]; b2[x] = B[(long long)u * Kd + ac];
+      }
+#pragma unroll
+      for (int x = 0; x < 4; x++) { acc_fma_dd(A[x], -b1[x], th[u], tl[u]); acc_fma_dd(A[x], -b2[x], th[r + u], tl[r + u]); }
+    }
+#pragma unroll
+    for (int x = 0; x < 4; x++) if (a0 + 32 * x < Kd) gc[a0 + 32 * x] = acc_val(A[x]);
   }
   __syncwarp();
 }
