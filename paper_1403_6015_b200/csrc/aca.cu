@@ -75,6 +75,9 @@ __device__ __forceinline__ void block_argmax_n2(double &ba, long long &bi, doubl
 }
 
 // ---------------------------------------------------------------------------------------------
+// Thread-local argmax: every thread visits its elements in increasing index order, so a strict "> best" keeps the
+// smallest index among equal magnitudes (the convention of amax_better, used for the cross-thread reductions); an
+// all-zero residual leaves bi = -1, which the state update treats as the exactly-zero residual it is.
 // Step-synchronous pass over the big blocks.  ROW: elements j of c2 for the pivot row i_k,
 //   a_j = k(x_ik - x_j),  v~_j = a_j - sum_l U'[ik,l] V'[j,l]  -> V'[:,k]
 // COL: elements i of c1 for the pivot column j_k,
@@ -189,7 +192,7 @@ __global__ void __launch_bounds__(ACA_SUB, 2) k_aca_pass(const AcaCtx *__restric
         *(double2 *)(outp + 2) = make_double2(v[2], v[3]);
 #pragma unroll
         for (int q = 0; q < 4; q++) {
-          if (!((usedm >> q) & 1u) && amax_better(ba, bi, fabs(v[q]), g0 + q - lo)) { ba = fabs(v[q]); bi = g0 + q - lo; bv = v[q]; }
+          if (!((usedm >> q) & 1u) && fabs(v[q]) > ba) { ba = fabs(v[q]); bi = g0 + q - lo; bv = v[q]; }
           n2 += v[q] * v[q];
         }
       }
@@ -247,7 +250,7 @@ __global__ void __launch_bounds__(ACA_SUB, 2) k_aca_pass(const AcaCtx *__restric
       const long long g = g0 + q * ACA_SUB;
       const double v = r[q] * scale;
       slot[(long long)k * ldx + g] = v;
-      if (!((usedm >> q) & 1u) && amax_better(ba, bi, fabs(v), g - lo)) { ba = fabs(v); bi = g - lo; bv = v; }
+      if (!((usedm >> q) & 1u) && fabs(v) > ba) { ba = fabs(v); bi = g - lo; bv = v; }
       n2 += v * v;
     }
   }
@@ -396,7 +399,7 @@ __global__ void __launch_bounds__(ACA_SUB) k_aca_fused(AcaCtx c, const int *bloc
       for (int l = 0; l < k; l++) v -= Ui[l] * __ldcg(slot + (long long)l * ldx + gj);
       slot[(long long)k * ldx + gj] = v;
       vbuf[j] = v;
-      if (!usedC[j] && amax_better(ba, bi, fabs(v), j)) { ba = fabs(v); bi = j; bv = v; }
+      if (!usedC[j] && fabs(v) > ba) { ba = fabs(v); bi = j; bv = v; }
       n2 += v * v;
     }
     block_argmax_n2(ba, bi, bv, n2, s_abs, s_idx, s_val, s_n2);
@@ -428,7 +431,7 @@ __global__ void __launch_bounds__(ACA_SUB) k_aca_fused(AcaCtx c, const int *bloc
       u *= rp;
       slot[(long long)k * ldx + gi] = u;
       vbuf[i] = u;
-      if (!usedR[i] && amax_better(ba, bi, fabs(u), i)) { ba = fabs(u); bi = i; bv = u; }
+      if (!usedR[i] && fabs(u) > ba) { ba = fabs(u); bi = i; bv = u; }
       n2 += u * u;
     }
     block_argmax_n2(ba, bi, bv, n2, s_abs, s_idx, s_val, s_n2);
