@@ -118,7 +118,8 @@ __global__ void __launch_bounds__(ACA_SUB, 2) k_aca_pass(const AcaCtx *__restric
   __shared__ double s_abs[ACA_SUB / 32], s_val[ACA_SUB / 32], s_n2[ACA_SUB / 32];
   __shared__ long long s_idx[ACA_SUB / 32];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  for (int l = t; l < k; l += ACA_SUB) coef[l] = slot[(long long)l * ldx + pg];
+  // (zero-padded to a multiple of 4: the vector path runs whole batches of 4 columns without masks)
+  for (int l = t; l < ((k + 3) & ~3); l += ACA_SUB) coef[l] = l < k ? slot[(long long)l * ldx + pg] : 0.0;
   __syncthreads();
   // dots F_l . a: for each batch of 4 columns the 4 per-lane partials are reduced over the warp by a transposed
   // butterfly (6 shuffles); lane L then holds column l0 + ((L >> 3) & 3) and keeps it when batch l0 / 4 is
@@ -157,15 +158,16 @@ __global__ void __launch_bounds__(ACA_SUB, 2) k_aca_pass(const AcaCtx *__restric
         double F[LS][4];
 #pragma unroll
         for (int dl = 0; dl < LS; dl++) {
+          // no masks: a column beyond k reads column 0 (finite) with coefficient 0 and its dot is never kept; a
+          // quad beyond the chunk (!ok) has a = 0 and its residual is never stored
           const double *cp = colp + (size_t)(l0 + dl < k ? l0 + dl : 0) * n1;
           const double2 f01 = *(const double2 *)cp, f23 = *(const double2 *)(cp + 2);
-          const bool v = ok && l0 + dl < k;
-          F[dl][0] = v ? f01.x : 0.0; F[dl][1] = v ? f01.y : 0.0; F[dl][2] = v ? f23.x : 0.0; F[dl][3] = v ? f23.y : 0.0;
+          F[dl][0] = f01.x; F[dl][1] = f01.y; F[dl][2] = f23.x; F[dl][3] = f23.y;
         }
         double pv[LS];
 #pragma unroll
         for (int dl = 0; dl < LS; dl++) {
-          const double cf = l0 + dl < k ? coef[l0 + dl] : 0.0;
+          const double cf = coef[l0 + dl];
           double p = 0.0;
 #pragma unroll
           for (int q = 0; q < 4; q++) { r[q] = fma(-cf, F[dl][q], r[q]); p = fma(F[dl][q], a[q], p); }
