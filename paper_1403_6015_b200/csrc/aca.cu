@@ -50,6 +50,7 @@ __global__ void k_aca_init(AcaCtx c, int nblocks, int cap) {
 
 
 // Block-wide argmax (ties -> smallest index) + sum of nrm2; result broadcast to every thread.
+template <int NW = ACA_SUB / 32>
 __device__ __forceinline__ void block_argmax_n2(double &ba, long long &bi, double &bv, double &n2,
                                                 double *s_abs, long long *s_idx, double *s_val, double *s_n2) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -64,7 +65,7 @@ __device__ __forceinline__ void block_argmax_n2(double &ba, long long &bi, doubl
   if (lane == 0) { s_abs[warp] = ba; s_idx[warp] = bi; s_val[warp] = bv; s_n2[warp] = n2; }
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int w = 1; w < ACA_SUB / 32; w++) {
+    for (int w = 1; w < NW; w++) {
       if (amax_better(s_abs[0], s_idx[0], s_abs[w], s_idx[w])) { s_abs[0] = s_abs[w]; s_idx[0] = s_idx[w]; s_val[0] = s_val[w]; }
       s_n2[0] += s_n2[w];
     }
@@ -88,6 +89,9 @@ __device__ __forceinline__ void block_argmax_n2(double &ba, long long &bi, doubl
 // indices, ||r||^2 and F_l . a for its chunk -> one record; the last CTA of a block reduces the
 // records in a fixed order (deterministic) and advances the block state.
 // ---------------------------------------------------------------------------------------------
+#ifndef ACA_FUSED_SMALL
+#define ACA_FUSED_SMALL 128        // fused blocks with both sides <= this run in 64-thread CTAs
+#endif
 constexpr int ACA_E = 4;                       // elements per thread per sub-tile
 constexpr int ACA_TILE = ACA_SUB * ACA_E;
 
@@ -359,13 +363,15 @@ __global__ void __launch_bounds__(ACA_SUB, 2) k_aca_pass(const AcaCtx *__restric
 // block (same arithmetic and conventions as the row/column passes above, block-level reductions,
 // pivot bookkeeping in shared memory).  Runs concurrently with the step-synchronous big blocks.
 // ---------------------------------------------------------------------------------------------
-template <bool SEO>
-__global__ void __launch_bounds__(ACA_SUB) k_aca_fused(AcaCtx c, const int *blocks, int *flags) {
-  __shared__ double vbuf[ACA_FUSED_MAX];
-  __shared__ unsigned char usedR[ACA_FUSED_MAX], usedC[ACA_FUSED_MAX];
+// NT threads; MAXS >= both sides of every block of the launch (small blocks run in small CTAs: the 64- and
+// 128-point blocks of the deepest levels need neither 256 threads nor 40 KB of shared memory)
+template <bool SEO, int NT, int MAXS>
+__global__ void __launch_bounds__(NT) k_aca_fused(AcaCtx c, const int *blocks, int *flags) {
+  __shared__ double vbuf[MAXS];
+  __shared__ unsigned char usedR[MAXS], usedC[MAXS];
   __shared__ double Ui[ACA_MAXCAP], dV[ACA_MAXCAP], dots[ACA_MAXCAP];
-  __shared__ double s_abs[ACA_SUB / 32], s_val[ACA_SUB / 32], s_n2[ACA_SUB / 32];
-  __shared__ long long s_idx[ACA_SUB / 32];
+  __shared__ double s_abs[(NT / 32)], s_val[(NT / 32)], s_n2[(NT / 32)];
+  __shared__ long long s_idx[(NT / 32)];
   __shared__ long long s_ipiv, s_jpiv;
   __shared__ double s_pval, s_nv2, s_S2;
   __shared__ int s_k, s_done;
@@ -378,7 +384,7 @@ __global__ void __launch_bounds__(ACA_SUB) k_aca_fused(AcaCtx c, const int *bloc
   const int e = c.bdepth[b] + 1;
   double *slot = c.Xh + c.dt->colbase[e] * c.ldx;
   const long long ldx = c.ldx;
-  for (int i = t; i < ACA_FUSED_MAX; i += ACA_SUB) { usedR[i] = 0; usedC[i] = 0; }
+  for (int i = t; i < MAXS; i += NT) { usedR[i] = 0; usedC[i] = 0; }
   __syncthreads();
   if (t == 0) {
     s_k = 0; s_done = 0; s_S2 = 0.0; s_ipiv = m1 - 1;
@@ -391,10 +397,10 @@ __global__ void __launch_bounds__(ACA_SUB) k_aca_fused(AcaCtx c, const int *bloc
     // ---------------- row pass ----------------
     const long long ig = lo1 + s_ipiv;
     const double xi = c.xs[ig];
-    for (int l = t; l < k; l += ACA_SUB) Ui[l] = slot[(long long)l * ldx + ig];
+    for (int l = t; l < k; l += NT) Ui[l] = slot[(long long)l * ldx + ig];
     __syncthreads();
     double ba = 0.0, bv = 0.0, n2 = 0.0; long long bi = -1;
-    for (long long j = t; j < m2; j += ACA_SUB) {
+    for (long long j = t; j < m2; j += NT) {
       const long long gj = lo2 + j;
       double v = kval_t<SEO>(c.kp, xi - c.xs[gj]);
 #pragma unroll 8
@@ -404,8 +410,8 @@ __global__ void __launch_bounds__(ACA_SUB) k_aca_fused(AcaCtx c, const int *bloc
       if (!usedC[j] && fabs(v) > ba) { ba = fabs(v); bi = j; bv = v; }
       n2 += v * v;
     }
-    block_argmax_n2(ba, bi, bv, n2, s_abs, s_idx, s_val, s_n2);
-    for (int l = warp; l < k; l += ACA_SUB / 32) {
+    block_argmax_n2<NT / 32>(ba, bi, bv, n2, s_abs, s_idx, s_val, s_n2);
+    for (int l = warp; l < k; l += (NT / 32)) {
       double s = 0.0;
 #pragma unroll 8
       for (long long j = lane; j < m2; j += 32) s += __ldcg(slot + (long long)l * ldx + lo2 + j) * vbuf[j];
@@ -422,10 +428,10 @@ __global__ void __launch_bounds__(ACA_SUB) k_aca_fused(AcaCtx c, const int *bloc
     const long long jg = lo2 + s_jpiv;
     const double xj = c.xs[jg];
     const double rp = 1.0 / s_pval;
-    for (int l = t; l < k; l += ACA_SUB) Ui[l] = slot[(long long)l * ldx + jg];
+    for (int l = t; l < k; l += NT) Ui[l] = slot[(long long)l * ldx + jg];
     __syncthreads();
     ba = 0.0; bv = 0.0; n2 = 0.0; bi = -1;
-    for (long long i = t; i < m1; i += ACA_SUB) {
+    for (long long i = t; i < m1; i += NT) {
       const long long gi = lo1 + i;
       double u = kval_t<SEO>(c.kp, c.xs[gi] - xj);
 #pragma unroll 8
@@ -436,8 +442,8 @@ __global__ void __launch_bounds__(ACA_SUB) k_aca_fused(AcaCtx c, const int *bloc
       if (!usedR[i] && fabs(u) > ba) { ba = fabs(u); bi = i; bv = u; }
       n2 += u * u;
     }
-    block_argmax_n2(ba, bi, bv, n2, s_abs, s_idx, s_val, s_n2);
-    for (int l = warp; l < k; l += ACA_SUB / 32) {
+    block_argmax_n2<NT / 32>(ba, bi, bv, n2, s_abs, s_idx, s_val, s_n2);
+    for (int l = warp; l < k; l += (NT / 32)) {
       double s = 0.0;
 #pragma unroll 8
       for (long long i = lane; i < m1; i += 32) s += __ldcg(slot + (long long)l * ldx + lo1 + i) * vbuf[i];
@@ -492,6 +498,7 @@ struct AcaPlan {
   long long n; int leaf; int rank, nranks; bool seo;
   long long nb; int nbig;
   std::vector<int> fused_blocks;
+  int nfused_small = 0;                    // fused_blocks[0, nfused_small): both sides <= ACA_FUSED_SMALL
   size_t nitems_r = 0, nitems_c = 0;
   long long nrec_r = 0, nrec_c = 0;
   AcaItem *d_items_r = nullptr, *d_items_c = nullptr;
@@ -509,12 +516,16 @@ static cudaError_t plan_create(AcaPlan *P, const hodlr_s *h) {
   std::vector<AcaItem> items_r, items_c;
   std::vector<int> nq_r(nb), nq_c(nb), bdepth(nb), bigidx(nb, -1);
   std::vector<long long> rb_r(nb), rb_c(nb);
+  std::vector<int> small, large;
   P->nbig = 0;
   for (long long b = 0; b < nb; b++) {
     bdepth[b] = hodlr_depth_of(b);
     if (!hodlr_owns_block(h, b)) { nq_r[b] = nq_c[b] = 0; rb_r[b] = rb_c[b] = 0; continue; }   // another rank's subtree
     long long m1 = h->h_hi[2 * b + 1] - h->h_lo[2 * b + 1], m2 = h->h_hi[2 * b + 2] - h->h_lo[2 * b + 2];
-    if (std::max(m1, m2) <= ACA_FUSED_MAX) { P->fused_blocks.push_back((int)b); nq_r[b] = nq_c[b] = 0; rb_r[b] = rb_c[b] = 0; continue; }
+    if (std::max(m1, m2) <= ACA_FUSED_MAX) {
+      (std::max(m1, m2) <= ACA_FUSED_SMALL ? small : large).push_back((int)b);
+      nq_r[b] = nq_c[b] = 0; rb_r[b] = rb_c[b] = 0; continue;
+    }
     bigidx[b] = P->nbig++;
     for (int side = 0; side < 2; side++) {
       long long m = side == 0 ? m2 : m1;
@@ -533,6 +544,8 @@ static cudaError_t plan_create(AcaPlan *P, const hodlr_s *h) {
       else { nq_c[b] = q; rb_c[b] = P->nrec_c; P->nrec_c += q; }
     }
   }
+  P->nfused_small = (int)small.size();
+  P->fused_blocks = small; P->fused_blocks.insert(P->fused_blocks.end(), large.begin(), large.end());
   P->nitems_r = items_r.size(); P->nitems_c = items_c.size();
   std::vector<int> nq_all(nq_r); nq_all.insert(nq_all.end(), nq_c.begin(), nq_c.end());
   std::vector<long long> rb_all(rb_r); rb_all.insert(rb_all.end(), rb_c.begin(), rb_c.end());
@@ -664,8 +677,17 @@ hodlr_status hodlr_aca(hodlr_s *h) {
   if (!P->fused_blocks.empty()) {
     HCUDA(cudaEventRecord(h->ev_fork, h->st));
     HCUDA(cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
-    if (P->seo) k_aca_fused<true><<<(int)P->fused_blocks.size(), ACA_SUB, 0, h->st2>>>(c, P->d_fused, h->dflags);
-    else k_aca_fused<false><<<(int)P->fused_blocks.size(), ACA_SUB, 0, h->st2>>>(c, P->d_fused, h->dflags);
+    const int ns = P->nfused_small, nl = (int)P->fused_blocks.size() - ns;
+    if (nl > 0) {       // the large ones first (longest CTAs)
+      if (P->seo) k_aca_fused<true, ACA_SUB, ACA_FUSED_MAX><<<nl, ACA_SUB, 0, h->st2>>>(c, P->d_fused + ns, h->dflags);
+      else k_aca_fused<false, ACA_SUB, ACA_FUSED_MAX><<<nl, ACA_SUB, 0, h->st2>>>(c, P->d_fused + ns, h->dflags);
+    }
+    if (ns > 0) {       // on a second stream: not serialized behind the large blocks' long CTAs
+      HCUDA(cudaStreamWaitEvent(h->st2b, h->ev_fork, 0));
+      if (P->seo) k_aca_fused<true, 64, ACA_FUSED_SMALL><<<ns, 64, 0, h->st2b>>>(c, P->d_fused, h->dflags);
+      else k_aca_fused<false, 64, ACA_FUSED_SMALL><<<ns, 64, 0, h->st2b>>>(c, P->d_fused, h->dflags);
+      HCUDA(cudaEventRecord(h->ev_join2, h->st2b));
+    }
     HLAUNCH(h, "k_aca_fused");
     HCUDA(cudaEventRecord(h->ev_join, h->st2));
   }
@@ -690,6 +712,7 @@ hodlr_status hodlr_aca(hodlr_s *h) {
     hodlr_trace("aca: graph launched");
   }
   if (!P->fused_blocks.empty()) HCUDA(cudaStreamWaitEvent(h->st, h->ev_join, 0));
+  if (P->nfused_small > 0) HCUDA(cudaStreamWaitEvent(h->st, h->ev_join2, 0));
   HCUDA(cudaEventRecord(h->ev_hi, h->sthi));
   h->st = sm_main;
   HCUDA(cudaStreamWaitEvent(h->st, h->ev_hi, 0));

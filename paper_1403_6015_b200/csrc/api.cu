@@ -87,7 +87,8 @@ int64_t hodlr_launch_count(void) { return hodlr_global_launches; }
 // more host time than a small factorization).
 struct HRes {
   int dev;
-  cudaStream_t st2, st3, sthi;
+  cudaStream_t st2, st3, sthi, st2b;
+  cudaEvent_t ev_join2;
   cudaEvent_t ev0, ev1, ev_fork, ev_join, ev_chol, ev_hi;
   cudaEvent_t ph_ev[PH_N][2];
 };
@@ -116,6 +117,8 @@ static void res_acquire(hodlr_s *h) {
     if (fused_pri < 0) { const char *ev = getenv("HODLR_FUSED_PRIORITY"); fused_pri = ev ? atoi(ev) : 2; }
     const int pf = fused_pri == 1 ? hi_pri : (fused_pri == 2 ? std::min(lo_pri, hi_pri + 1) : lo_pri);
     cudaStreamCreateWithPriority(&r.st2, cudaStreamNonBlocking, pf);
+    cudaStreamCreateWithPriority(&r.st2b, cudaStreamNonBlocking, pf);
+    cudaEventCreateWithFlags(&r.ev_join2, cudaEventDisableTiming);
     static int chol_pri = -1;    // HODLR_CHOL_PRIORITY: the leaf Cholesky stream, same encoding
     if (chol_pri < 0) { const char *ev = getenv("HODLR_CHOL_PRIORITY"); chol_pri = ev ? atoi(ev) : 0; }
     const int pc = chol_pri == 1 ? hi_pri : (chol_pri == 2 ? std::min(lo_pri, hi_pri + 1) : lo_pri);
@@ -124,6 +127,7 @@ static void res_acquire(hodlr_s *h) {
     cudaEventCreateWithFlags(&r.ev_hi, cudaEventDisableTiming);
     for (int p = 0; p < PH_N; p++) for (int j = 0; j < 2; j++) cudaEventCreate(&r.ph_ev[p][j]);
   }
+  h->st2b = r.st2b; h->ev_join2 = r.ev_join2;
   h->st2 = r.st2; h->st3 = r.st3; h->ev0 = r.ev0; h->ev1 = r.ev1; h->ev_fork = r.ev_fork; h->ev_join = r.ev_join;
   h->ev_chol = r.ev_chol; h->sthi = r.sthi; h->ev_hi = r.ev_hi;
   for (int p = 0; p < PH_N; p++) for (int j = 0; j < 2; j++) h->ph_ev[p][j] = r.ph_ev[p][j];
@@ -132,6 +136,7 @@ static void res_acquire(hodlr_s *h) {
 static void res_release(hodlr_s *h) {
   if (!h->st2) return;
   HRes r;
+  r.st2b = h->st2b; r.ev_join2 = h->ev_join2;
   r.dev = h->dev; r.st2 = h->st2; r.st3 = h->st3; r.ev0 = h->ev0; r.ev1 = h->ev1; r.ev_fork = h->ev_fork;
   r.ev_join = h->ev_join; r.ev_chol = h->ev_chol; r.sthi = h->sthi; r.ev_hi = h->ev_hi;
   for (int p = 0; p < PH_N; p++) for (int j = 0; j < 2; j++) r.ph_ev[p][j] = h->ph_ev[p][j];
@@ -145,6 +150,7 @@ void hodlr_free(hodlr_t h) {
   for (int i = h->nallocs - 1; i >= 0; i--) cudaFreeAsync(h->allocs[i], h->st);
   if (h->st3) cudaStreamSynchronize(h->st3);
   if (h->st2) cudaStreamSynchronize(h->st2);
+  if (h->st2b) cudaStreamSynchronize(h->st2b);
   cudaStreamSynchronize(h->st);
   res_release(h);
   hodlr_dist_fini(h);

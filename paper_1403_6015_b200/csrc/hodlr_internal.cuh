@@ -132,6 +132,8 @@ enum { PH_SORT = 0, PH_ACA, PH_LEAF, PH_TREE, PH_SLEAF_UP, PH_STREE, PH_SLEAF_DO
 struct hodlr_s {
   cudaStream_t st;
   cudaStream_t st2;           // side stream (fused small-block ACA)
+  cudaStream_t st2b;          // second fused-ACA stream (the smallest blocks, 64-thread CTAs)
+  cudaEvent_t ev_join2;
   cudaStream_t st3;           // side stream (leaf Cholesky, overlapping the ACA)
   cudaStream_t sthi;          // high-priority stream (ACA step loop)
   cudaEvent_t ev_hi;
