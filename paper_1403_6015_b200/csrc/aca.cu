@@ -89,6 +89,9 @@ __device__ __forceinline__ void block_argmax_n2(double &ba, long long &bi, doubl
 // indices, ||r||^2 and F_l . a for its chunk -> one record; the last CTA of a block reduces the
 // records in a fixed order (deterministic) and advances the block state.
 // ---------------------------------------------------------------------------------------------
+#ifndef ACA_PASS_MINB
+#define ACA_PASS_MINB 2            // resident pass CTAs per SM the registers are budgeted for
+#endif
 #ifndef ACA_FUSED_SMALL
 #define ACA_FUSED_SMALL 128        // fused blocks with both sides <= this run in 64-thread CTAs
 #endif
@@ -96,7 +99,7 @@ constexpr int ACA_E = 4;                       // elements per thread per sub-ti
 constexpr int ACA_TILE = ACA_SUB * ACA_E;
 
 template <bool ROW, bool SEO>
-__global__ void __launch_bounds__(ACA_SUB, 2) k_aca_pass(const AcaCtx *__restrict__ pc) {
+__global__ void __launch_bounds__(ACA_SUB, ACA_PASS_MINB) k_aca_pass(const AcaCtx *__restrict__ pc) {
   __shared__ AcaCtx c;                         // context in shared memory: global stores cannot alias it
   for (int i = threadIdx.x; i < (int)(sizeof(AcaCtx) / 8); i += ACA_SUB) ((long long *)&c)[i] = ((const long long *)pc)[i];
   __syncthreads();
