@@ -17,6 +17,9 @@
 // The Schur updates cancel heavily (the top-level S_c reach cond ~1e11), so T_c is kept as a
 // double-double pair and Pi_c is accumulated with compensated arithmetic.
 #include "hodlr_internal.cuh"
+#ifndef TREE_NARROW_MIN
+#define TREE_NARROW_MIN (4 * 148)   // levels with at least this many nodes (and q <= 16) use the 128-thread CTAs
+#endif
 #include <limits.h>
 #include <stdlib.h>
 
@@ -384,7 +387,7 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
     hodlr_own_nodes(h, d, &i0, &cnt);
     const TreeCtx tc = tree_ctx(h, d, i0);
     const size_t smem = sizeof(double) * (size_t)tree_smem_doubles(tc.q, tc.ldk);
-    const bool narrow = cnt >= 4 * 148 && tc.q <= 16;
+    const bool narrow = cnt >= TREE_NARROW_MIN && tc.q <= 16;
     if (narrow) {
       if (tc.dd) k_tree_factor_narrow<true><<<(int)cnt, TT / 2, smem, h->st>>>(tc);
       else k_tree_factor_narrow<false><<<(int)cnt, TT / 2, smem, h->st>>>(tc);
