@@ -36,11 +36,32 @@ hodlr_status hodlr_cuda_check(cudaError_t e, const char *what) {
   return hodlr_set_error(HODLR_ECUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
+// Device blocks of freed handles are kept (per device, exact size) and handed to the next handle asking for the
+// same size: a repeated build of one shape then makes no allocation or free calls (hodlr_free synchronizes the
+// handle's streams before caching, so a reused block has no pending work).  Bounded at 16 GB per process.
+namespace {
+struct CachedBlock { int dev; size_t bytes; void *p; };
+std::mutex g_blk_mu;
+std::vector<CachedBlock> g_blk_cache;
+size_t g_blk_cached = 0;
+constexpr size_t kBlkCacheMax = (size_t)16 << 30;
+}
+
 void *hodlr_dalloc(hodlr_s *h, size_t bytes) {
   void *p = nullptr;
   if (bytes == 0) bytes = 8;
-  if (cudaMallocAsync(&p, bytes, h->st) != cudaSuccess) { cudaGetLastError(); return nullptr; }
-  if (h->nallocs >= (int)(sizeof(h->allocs) / sizeof(h->allocs[0]))) { cudaFreeAsync(p, h->st); return nullptr; }
+  if (h->nallocs >= (int)(sizeof(h->allocs) / sizeof(h->allocs[0]))) return nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_blk_mu);
+    for (size_t i = g_blk_cache.size(); i-- > 0;)
+      if (g_blk_cache[i].dev == h->dev && g_blk_cache[i].bytes == bytes) {
+        p = g_blk_cache[i].p; g_blk_cached -= bytes;
+        g_blk_cache.erase(g_blk_cache.begin() + (long)i);
+        break;
+      }
+  }
+  if (!p && cudaMallocAsync(&p, bytes, h->st) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+  h->alloc_bytes[h->nallocs] = bytes;
   h->allocs[h->nallocs++] = p;
   h->bytes += (long long)bytes;
   return p;
@@ -146,12 +167,22 @@ static void res_release(hodlr_s *h) {
 
 void hodlr_free(hodlr_t h) {
   if (!h) return;
-  if (h->st3 && h->ev_chol) { cudaEventRecord(h->ev_chol, h->st3); cudaStreamWaitEvent(h->st, h->ev_chol, 0); }
-  for (int i = h->nallocs - 1; i >= 0; i--) cudaFreeAsync(h->allocs[i], h->st);
   if (h->st3) cudaStreamSynchronize(h->st3);
   if (h->st2) cudaStreamSynchronize(h->st2);
   if (h->st2b) cudaStreamSynchronize(h->st2b);
+  if (h->sthi) cudaStreamSynchronize(h->sthi);
   cudaStreamSynchronize(h->st);
+  {
+    std::lock_guard<std::mutex> lk(g_blk_mu);
+    for (int i = h->nallocs - 1; i >= 0; i--) {
+      if (g_blk_cached + h->alloc_bytes[i] <= kBlkCacheMax) {
+        g_blk_cache.push_back({h->dev, h->alloc_bytes[i], h->allocs[i]});
+        g_blk_cached += h->alloc_bytes[i];
+      } else {
+        cudaFreeAsync(h->allocs[i], h->st);
+      }
+    }
+  }
   res_release(h);
   hodlr_dist_fini(h);
   delete[] h->h_lo; delete[] h->h_hi; delete[] h->h_rank;

@@ -197,7 +197,7 @@ struct hodlr_s {
   int ph_pending[PH_N];
   double ph_ms[PH_N];        // accumulated device ms per kernel family (since build)
   long long ph_calls[PH_N];
-  void *allocs[64]; int nallocs;
+  void *allocs[64]; size_t alloc_bytes[64]; int nallocs;
   double *apply_ws = nullptr; size_t apply_ws_n = 0;   // hodlr_apply workspace (apply.cu)
   double *pred_ws = nullptr; size_t pred_ws_n = 0;     // gp_predict workspace (predict.cu)
 };
