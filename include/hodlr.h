@@ -179,7 +179,9 @@ void         hodlr_group_destroy(void *group);
 hodlr_status hodlr_dist_plan(int64_t n, int32_t leaf, int32_t rank, int32_t nranks, int32_t *kappa, int32_t *t,
                              int64_t *row_lo, int64_t *row_hi, int64_t *leaf_lo, int64_t *leaf_hi);
 
-/* Release everything the handle owns (stream-ordered).  NULL is a no-op. */
+/* Release everything the handle owns.  NULL is a no-op.  Synchronizes the handle's streams; its device blocks are
+ * kept by the library (exact-size reuse by later handles on the same device, at most 16 GB per process) rather
+ * than returned to the CUDA pool, so repeated builds of one shape allocate nothing. */
 void hodlr_free(hodlr_t h);
 
 /* Thread-local message of the last failing call (never NULL). */
