@@ -20,8 +20,8 @@
  * Ordering: all device work is enqueued on `cuda_stream` (NULL = legacy
  * default stream); every call synchronises that stream before it returns its
  * status, so statuses are final.
- * State machine: build -> factor -> {logdet, solve, gp_loglik}*.  Any other
- * order returns HODLR_ESTATE.  After factor the handle is read-only; one
+ * State machine: build -> factor -> {logdet, solve, gp_loglik, gp_predict}*; hodlr_apply is legal from build
+ * on.  Any other order returns HODLR_ESTATE.  After factor the handle is read-only; one
  * handle must not be used from two threads at once.
  * Errors: every call returns a hodlr_status; hodlr_last_error() gives a
  * thread-local message for the last failing call.
@@ -106,7 +106,8 @@ typedef struct {
 /* "Assembly": stable sort of x (O(n), K1), balanced count-median
  * tree with kappa = floor(log2(n/leaf)) levels, and ACA compression of every
  * off-diagonal block K[c1,c2] ~ U V^T to relative eps (sec. 3.1).
- * x: device, n doubles.  theta: HOST pointer to {a, ell}.  *out receives the handle. */
+ * x: device, n doubles.  theta: HOST pointer to {a, ell} ({a, ell, alpha} for HODLR_RQ).  *out receives the
+ * handle. */
 hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const double *theta,
                          double sigma2, int32_t leaf, double eps, const hodlr_dist *dist,
                          const hodlr_opts *opts, void *cuda_stream, hodlr_t *out);
