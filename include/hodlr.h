@@ -76,10 +76,17 @@ typedef struct {
   void *group;                  /* hodlr_group_create() handle, or NULL */
 } hodlr_dist;
 
-/* Optional build options.  NULL => defaults. */
+/* Optional build options.  NULL => defaults; zero-initialise unused fields. */
 typedef struct {
   int32_t rank_cap;             /* max ACA rank per block, <= 64; 0 => 48 (always clamped to min(m1, m2)) */
-  int32_t reserved[7];
+  int32_t flags;                /* reserved, must be 0 */
+  /* Test hook (parity): HOST array of the 2^kappa - 1 internal nodes' ACA ranks in heap order, or NULL.  When set,
+   * the ACA of block b runs exactly forced_ranks[b] cross steps (it still stops early on an exactly-zero residual
+   * row) instead of applying the eps stopping test -- so the GPU can be run with the oracle's per-block ranks and
+   * a parity difference separated into compression (different ranks) and arithmetic (same ranks).  Read only
+   * during hodlr_build. */
+  const int32_t *forced_ranks;
+  int64_t reserved[6];
 } hodlr_opts;
 
 typedef struct {

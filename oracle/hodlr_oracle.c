@@ -6,6 +6,13 @@
  * no reordering beyond what the paper's algorithm states.  Ambiguities are
  * resolved by the readings listed in DESIGN.md section 3 ("R1".."R15").
  * Compile: gcc -O2 -ffp-contract=off -fPIC -shared (no BLAS, no OpenMP).
+ *
+ * -DORACLE_TWIN builds the "oracle twin" of SURVEY.md 8(c) Q15 (liboracle_twin.so): the same algorithm with a
+ * different backward-stable factorization of every small dense system -- leaf blocks by LU with partial pivoting
+ * instead of Cholesky (O5'), coupling systems S_c by Householder QR instead of LU (O7').  Same ACA, same tree,
+ * same panel and sweep.  The twin-vs-oracle difference of a solve is the FP64 conditioning floor of that
+ * problem (two correct implementations with the same pivots), which sets the parity gate of the badly
+ * conditioned config-4 settings: max(1e-9, 10 floor) (R15).
  */
 #include "hodlr_oracle.h"
 #include <math.h>
@@ -174,7 +181,8 @@ struct oracle_hodlr {
   int *rdep; int64_t *coff; int64_t K; /* per-depth column width r_e and offset, e = 1..kappa */
   double *X, *Xh;                   /* n x K row-major: processed panel and its unprocessed copy */
   double **Lleaf;                   /* per leaf: m x m lower Cholesky factor (row-major) */
-  double **Slu; int **Spiv;         /* per internal node: 2r x 2r LU (row-major) + pivots */
+  double **Slu; int **Spiv;         /* per internal node: 2r x 2r LU (row-major) + pivots; twin: Q then R */
+  int **Lpiv;                       /* twin: per-leaf LU pivots */
   double *leaf_ld, *node_ld;        /* log det partials */
   double logdet; int state;         /* 1 built, 2 factored, -1 failed */
   int fstatus;
@@ -217,6 +225,8 @@ void oracle_free(oracle_hodlr *h) {
   free(h->blk); free(h->rdep); free(h->coff); free(h->X); free(h->Xh);
   if (h->Lleaf) for (int64_t l = 0; l < h->nleaves; l++) free(h->Lleaf[l]);
   free(h->Lleaf);
+  if (h->Lpiv) for (int64_t l = 0; l < h->nleaves; l++) free(h->Lpiv[l]);
+  free(h->Lpiv);
   if (h->Slu) for (int64_t c = 0; c < h->ninternal; c++) { free(h->Slu[c]); free(h->Spiv[c]); }
   free(h->Slu); free(h->Spiv); free(h->leaf_ld); free(h->node_ld);
   free(h);
@@ -286,7 +296,7 @@ int oracle_build(const double *x, int64_t n, int kernel, const double *theta, do
 static int depth_of(int64_t id) { int d = 0; while (id >= ((int64_t)2 << d) - 1) d++; return d; }
 
 /* O5: unblocked Cholesky (Cholesky-Banachiewicz), A = L L^T, row-major m x m. */
-static int cholesky(double *A, int64_t m) {
+__attribute__((unused)) static int cholesky(double *A, int64_t m) {
   for (int64_t j = 0; j < m; j++) {
     double s = A[j * m + j];
     for (int64_t k = 0; k < j; k++) s -= A[j * m + k] * A[j * m + k];
@@ -304,7 +314,7 @@ static int cholesky(double *A, int64_t m) {
 }
 
 /* Solve L L^T w = b in place; b has stride `st`. */
-static void chol_solve(const double *L, int64_t m, double *b, int64_t st) {
+__attribute__((unused)) static void chol_solve(const double *L, int64_t m, double *b, int64_t st) {
   for (int64_t i = 0; i < m; i++) {
     double s = b[i * st];
     for (int64_t k = 0; k < i; k++) s -= L[i * m + k] * b[k * st];
@@ -346,6 +356,63 @@ static void lu_solve(const double *S, int q, const int *piv, double *b, int64_t 
   for (int i = q - 1; i >= 0; i--) { double s = b[i * st]; for (int k = i + 1; k < q; k++) s -= S[i * q + k] * b[k * st]; b[i * st] = s / S[i * q + i]; }
 }
 
+#ifdef ORACLE_TWIN
+/* Twin O7': Householder QR of the row-major q x q matrix S (overwritten), Q accumulated explicitly (row-major
+ * q x q).  Column k: x = S[k:, k], alpha = -sign(x_0) ||x||, v = x - alpha e_1, H = I - 2 v v^T / v^T v applied
+ * to S[k:, k:] from the left and to Q[:, k:] from the right.  det S = (-1)^(reflections) prod R_kk.
+ * Returns -1 on a zero R_kk (singular). */
+static int qr_factor(double *S, int q, double *Q, double *logabs, int *sign) {
+  int sg = 1; double la = 0.0;
+  double *v = malloc(sizeof(double) * (size_t)(q > 0 ? q : 1));
+  if (!v) return -2;
+  for (int i = 0; i < q; i++) for (int j = 0; j < q; j++) Q[i * q + j] = i == j ? 1.0 : 0.0;
+  for (int k = 0; k < q; k++) {
+    double nx = 0.0;
+    for (int i = k; i < q; i++) nx += S[i * q + k] * S[i * q + k];
+    nx = sqrt(nx);
+    if (nx > 0.0) {
+      double alpha = S[k * q + k] >= 0.0 ? -nx : nx;
+      double vv = 0.0;
+      for (int i = k; i < q; i++) v[i] = S[i * q + k];
+      v[k] -= alpha;
+      for (int i = k; i < q; i++) vv += v[i] * v[i];
+      if (vv > 0.0) {
+        for (int j = k; j < q; j++) {                  /* S[k:, j] -= 2 v (v . S[k:, j]) / vv */
+          double d = 0.0;
+          for (int i = k; i < q; i++) d += v[i] * S[i * q + j];
+          d = 2.0 * d / vv;
+          for (int i = k; i < q; i++) S[i * q + j] -= d * v[i];
+        }
+        for (int i = 0; i < q; i++) {                  /* Q[i, k:] -= 2 (Q[i, k:] . v) v / vv */
+          double d = 0.0;
+          for (int j = k; j < q; j++) d += Q[i * q + j] * v[j];
+          d = 2.0 * d / vv;
+          for (int j = k; j < q; j++) Q[i * q + j] -= d * v[j];
+        }
+        sg = -sg;                                     /* det H = -1 */
+      }
+    }
+    double rkk = S[k * q + k];
+    if (rkk == 0.0) { free(v); return -1; }
+    if (rkk < 0.0) sg = -sg;
+    la += log(fabs(rkk));
+  }
+  free(v);
+  *logabs = la; *sign = sg;
+  return 0;
+}
+
+/* t = R^{-1} Q^T b in place, one rhs with stride st (QR: Q row-major q x q, R upper of the row-major S). */
+static void qr_solve(const double *Q, const double *R, int q, double *b, int64_t st) {
+  double tmp[2048];
+  double *w = q <= 2048 ? tmp : malloc(sizeof(double) * (size_t)q);
+  for (int i = 0; i < q; i++) { double s = 0.0; for (int k = 0; k < q; k++) s += Q[k * q + i] * b[k * st]; w[i] = s; }
+  for (int i = q - 1; i >= 0; i--) { double s = w[i]; for (int k = i + 1; k < q; k++) s -= R[i * q + k] * w[k]; w[i] = s / R[i * q + i]; }
+  for (int i = 0; i < q; i++) b[i * st] = w[i];
+  if (w != tmp) free(w);
+}
+#endif
+
 /* Neumaier-compensated sum (R11). */
 typedef struct { double s, c; } nsum;
 static void nadd(nsum *a, double x) {
@@ -371,11 +438,12 @@ int oracle_factor(oracle_hodlr *h) {
   h->X = calloc((size_t)(n * (K ? K : 1)), sizeof(double));
   h->Xh = calloc((size_t)(n * (K ? K : 1)), sizeof(double));
   h->Lleaf = calloc((size_t)h->nleaves, sizeof(double *));
+  h->Lpiv = calloc((size_t)h->nleaves, sizeof(int *));
   h->Slu = calloc((size_t)(h->ninternal ? h->ninternal : 1), sizeof(double *));
   h->Spiv = calloc((size_t)(h->ninternal ? h->ninternal : 1), sizeof(int *));
   h->leaf_ld = calloc((size_t)h->nleaves, sizeof(double));
   h->node_ld = calloc((size_t)(h->ninternal ? h->ninternal : 1), sizeof(double));
-  if (!h->X || !h->Xh || !h->Lleaf || !h->Slu || !h->Spiv || !h->leaf_ld || !h->node_ld)
+  if (!h->X || !h->Xh || !h->Lleaf || !h->Lpiv || !h->Slu || !h->Spiv || !h->leaf_ld || !h->node_ld)
     return fail(ORACLE_ENOMEM, "factor: oom");
   /* X[a rows, cols(a)] = L_a for every non-root node a: U for a left child, V for a right child. */
   for (int64_t c = 0; c < h->ninternal; c++) {
@@ -394,6 +462,7 @@ int oracle_factor(oracle_hodlr *h) {
     double *A = malloc(sizeof(double) * (size_t)(m * m));
     if (!A) return fail(ORACLE_ENOMEM, "factor: oom");
     for (int64_t i = 0; i < m; i++) for (int64_t j = 0; j < m; j++) A[i * m + j] = entry_C(h, lo + i, lo + j);
+#ifndef ORACLE_TWIN
     if (cholesky(A, m) != 0) {
       free(A); h->logdet = -INFINITY; h->fstatus = ORACLE_ENOTPD;
       return fail(ORACLE_ENOTPD, "factor: leaf %lld not positive definite", (long long)l);
@@ -403,6 +472,18 @@ int oracle_factor(oracle_hodlr *h) {
     h->leaf_ld[l] = 2.0 * s;
     h->Lleaf[l] = A;
     for (int64_t c = 0; c < K; c++) chol_solve(A, m, &h->X[lo * K + c], K);
+#else
+    /* O5' (twin): A = P^T L U with partial pivoting; log det = sum log |U_ii|, det must be > 0 */
+    int *lp = malloc(sizeof(int) * (size_t)m);
+    double la = 0.0; int sg = 1;
+    if (!lp || lu_factor(A, (int)m, lp, &la, &sg) != 0 || sg <= 0) {
+      free(A); free(lp); h->logdet = -INFINITY; h->fstatus = ORACLE_ENOTPD;
+      return fail(ORACLE_ENOTPD, "factor: leaf %lld singular or det <= 0", (long long)l);
+    }
+    h->leaf_ld[l] = la;
+    h->Lleaf[l] = A; h->Lpiv[l] = lp;
+    for (int64_t c = 0; c < K; c++) lu_solve(A, (int)m, lp, &h->X[lo * K + c], K);
+#endif
   }
   /* O7: level sweep d = kappa-1 .. 0 (SMW on [[I, P],[Q, I]], equation_Low_Rank_Update). */
   for (int d = kappa - 1; d >= 0; d--) {
@@ -411,7 +492,7 @@ int oracle_factor(oracle_hodlr *h) {
       int64_t c = ((int64_t)1 << d) - 1 + i, c1 = 2 * c + 1, c2 = 2 * c + 2;
       int r = h->blk[c].r, q = 2 * r;
       int64_t lo1 = h->lo[c1], m1 = h->hi[c1] - lo1, lo2 = h->lo[c2], m2 = h->hi[c2] - lo2;
-      double *S = calloc((size_t)(q > 0 ? q * q : 1), sizeof(double));
+      double *S = calloc((size_t)(q > 0 ? 2 * q * q : 1), sizeof(double));   /* twin: Q in [q*q, 2 q*q) */
       int *piv = calloc((size_t)(q > 0 ? q : 1), sizeof(int));
       if (!S || !piv) return fail(ORACLE_ENOMEM, "factor: oom");
       for (int a = 0; a < q; a++) S[a * q + a] = 1.0;
@@ -423,7 +504,11 @@ int oracle_factor(oracle_hodlr *h) {
         S[(r + a) * q + b] = Q;
       }
       double la = 0.0; int sg = 1;
+#ifndef ORACLE_TWIN
       if (q > 0 && lu_factor(S, q, piv, &la, &sg) != 0) sg = 0;
+#else
+      if (q > 0 && qr_factor(S, q, S + q * q, &la, &sg) != 0) sg = 0;    /* O7' (twin) */
+#endif
       h->Slu[c] = S; h->Spiv[c] = piv;
       if (sg <= 0) {
         h->logdet = -INFINITY; h->fstatus = ORACLE_ENOTPD;
@@ -441,7 +526,11 @@ int oracle_factor(oracle_hodlr *h) {
         T[a * Kd + j] = s2;
         T[(r + a) * Kd + j] = s1;
       }
+#ifndef ORACLE_TWIN
       for (int64_t j = 0; j < Kd; j++) lu_solve(S, q, piv, &T[j], Kd);
+#else
+      for (int64_t j = 0; j < Kd; j++) qr_solve(S + q * q, S, q, &T[j], Kd);
+#endif
       /* X[c1,J] -= X[c1,cs] T_top ; X[c2,J] -= X[c2,cs] T_bot */
       for (int64_t t = 0; t < m1; t++) for (int64_t j = 0; j < Kd; j++) {
         double s = 0.0;
@@ -480,7 +569,11 @@ static void solve_sorted(const oracle_hodlr *h, double *b) {
   int64_t K = h->K;
   for (int64_t l = 0; l < h->nleaves; l++) {
     int64_t id = h->ninternal + l, lo = h->lo[id], m = h->hi[id] - lo;
+#ifndef ORACLE_TWIN
     chol_solve(h->Lleaf[l], m, &b[lo], 1);
+#else
+    lu_solve(h->Lleaf[l], (int)m, h->Lpiv[l], &b[lo], 1);
+#endif
   }
   for (int d = h->kappa - 1; d >= 0; d--) {
     int64_t cs = h->coff[d + 1];
@@ -497,7 +590,11 @@ static void solve_sorted(const oracle_hodlr *h, double *b) {
         for (int64_t u = 0; u < m1; u++) s1 += h->Xh[(lo1 + u) * K + cs + a] * b[lo1 + u];
         tt[a] = s2; tt[r + a] = s1;
       }
+#ifndef ORACLE_TWIN
       lu_solve(h->Slu[c], q, h->Spiv[c], tt, 1);
+#else
+      qr_solve(h->Slu[c] + q * q, h->Slu[c], q, tt, 1);
+#endif
       for (int64_t u = 0; u < m1; u++) { double s = 0.0; for (int a = 0; a < r; a++) s += h->X[(lo1 + u) * K + cs + a] * tt[a]; b[lo1 + u] -= s; }
       for (int64_t u = 0; u < m2; u++) { double s = 0.0; for (int a = 0; a < r; a++) s += h->X[(lo2 + u) * K + cs + a] * tt[r + a]; b[lo2 + u] -= s; }
       if (tt != t) free(tt);
@@ -566,6 +663,26 @@ int oracle_apply(oracle_hodlr *h, const double *v, double *out) {
   return ORACLE_OK;
 }
 
+/* Residual rows of a solution: out[k] = sum_j C_{r_k j} x_j - y_{r_k} for original row indices r_k, C assembled
+ * entry by entry (O3), original order; plain sequential loops.  Used by tests and the golden-file script. */
+int oracle_residual_rows(oracle_hodlr *h, const double *x, const double *y, const int64_t *rows, int64_t nr,
+                         double *out) {
+  if (!h || h->state == 0) return fail(ORACLE_ESTATE, "residual_rows: not built");
+  int64_t n = h->n;
+  int64_t *inv = malloc(sizeof(int64_t) * (size_t)n);
+  if (!inv) return fail(ORACLE_ENOMEM, "residual_rows: oom");
+  for (int64_t i = 0; i < n; i++) inv[h->perm[i]] = i;
+  for (int64_t k = 0; k < nr; k++) {
+    if (rows[k] < 0 || rows[k] >= n) { free(inv); return fail(ORACLE_EINVAL, "residual_rows: bad row"); }
+    int64_t i = inv[rows[k]];
+    double s = 0.0;
+    for (int64_t j = 0; j < n; j++) s += entry_C(h, i, j) * x[h->perm[j]];
+    out[k] = s - y[rows[k]];
+  }
+  free(inv);
+  return ORACLE_OK;
+}
+
 int oracle_kappa(oracle_hodlr *h) { return h ? h->kappa : -1; }
 int64_t oracle_num_nodes(oracle_hodlr *h) { return h ? h->nnodes : -1; }
 int oracle_get_perm(oracle_hodlr *h, int64_t *perm) { memcpy(perm, h->perm, sizeof(int64_t) * (size_t)h->n); return 0; }
@@ -606,16 +723,19 @@ int oracle_dense(const double *x, int64_t n, int kernel, const double *theta, do
       double xi = x[i] == 0.0 ? 0.0 : x[i], xj = x[j] == 0.0 ? 0.0 : x[j];
       C[i * n + j] = oracle_kernel(kernel, theta, xi - xj) + (i == j ? sigma2 : 0.0);
     }
-  /* column-oriented (Cholesky-Crout) loop order, deliberately different from O5 */
-  for (int64_t j = 0; j < n; j++) {
-    double s = C[j * n + j];
-    for (int64_t k = 0; k < j; k++) s -= C[j * n + k] * C[j * n + k];
-    if (!(s > 0.0)) { free(C); *logdet = -INFINITY; return fail(ORACLE_ENOTPD, "dense: not PD at %lld", (long long)j); }
-    C[j * n + j] = sqrt(s);
-    for (int64_t i = j + 1; i < n; i++) {
-      double t = C[i * n + j];
-      for (int64_t k = 0; k < j; k++) t -= C[i * n + k] * C[j * n + k];
-      C[i * n + j] = t / C[j * n + j];
+  /* right-looking (outer-product) Cholesky on the upper triangle, C = U^T U (U = L^T, row k of U = column k of
+   * L): after row k is scaled, its rank-1 update is applied to the whole trailing upper triangle at once -- a
+   * different operation order from O5's left-looking dot products, so the two agree only to rounding (the
+   * independent LAPACK check is numpy's, in the pins) */
+  for (int64_t k = 0; k < n; k++) {
+    double d = C[k * n + k];
+    if (!(d > 0.0)) { free(C); *logdet = -INFINITY; return fail(ORACLE_ENOTPD, "dense: not PD at %lld", (long long)k); }
+    double ukk = sqrt(d);
+    C[k * n + k] = ukk;
+    for (int64_t j = k + 1; j < n; j++) C[k * n + j] /= ukk;
+    for (int64_t i = k + 1; i < n; i++) {
+      double uki = C[k * n + i];
+      for (int64_t j = i; j < n; j++) C[i * n + j] -= uki * C[k * n + j];
     }
   }
   nsum acc = { 0.0, 0.0 };
@@ -623,8 +743,9 @@ int oracle_dense(const double *x, int64_t n, int kernel, const double *theta, do
   *logdet = acc.s + acc.c;
   if (y && xout) {
     for (int64_t i = 0; i < n; i++) xout[i] = y[i];
-    for (int64_t i = 0; i < n; i++) { double s = xout[i]; for (int64_t k = 0; k < i; k++) s -= C[i * n + k] * xout[k]; xout[i] = s / C[i * n + i]; }
-    for (int64_t i = n - 1; i >= 0; i--) { double s = xout[i]; for (int64_t k = i + 1; k < n; k++) s -= C[k * n + i] * xout[k]; xout[i] = s / C[i * n + i]; }
+    /* U^T z = y (L = U^T), then U x = z */
+    for (int64_t i = 0; i < n; i++) { double s = xout[i]; for (int64_t k = 0; k < i; k++) s -= C[k * n + i] * xout[k]; xout[i] = s / C[i * n + i]; }
+    for (int64_t i = n - 1; i >= 0; i--) { double s = xout[i]; for (int64_t k = i + 1; k < n; k++) s -= C[i * n + k] * xout[k]; xout[i] = s / C[i * n + i]; }
   }
   free(C);
   return ORACLE_OK;

@@ -64,6 +64,11 @@ int oracle_gp_loglik(oracle_hodlr *h, const double *y, double *out);
 /* HODLR matvec H v (the assembled hierarchical matrix), original order.  For pins. */
 int oracle_apply(oracle_hodlr *h, const double *v, double *out);
 
+/* Residual rows (C x - y)_r for the original row indices rows[0..nr) of a solution x (original order), C
+ * assembled entry by entry.  For tests and the golden-file script. */
+int oracle_residual_rows(oracle_hodlr *h, const double *x, const double *y, const int64_t *rows, int64_t nr,
+                         double *out);
+
 /* Introspection for tests. */
 int     oracle_kappa(oracle_hodlr *h);
 int64_t oracle_num_nodes(oracle_hodlr *h);

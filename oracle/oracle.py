@@ -1,6 +1,9 @@
-"""ctypes loader for liboracle.so (TEST INFRASTRUCTURE; see oracle/__init__.py).
+"""ctypes loader for liboracle.so and its Q15 twin liboracle_twin.so (TEST INFRASTRUCTURE; see oracle/__init__.py).
 
-Argument marshalling only: every step of the method runs in hodlr_oracle.c.
+Argument marshalling only: every step of the HODLR method (build, factor, log det, solve, log-likelihood, apply)
+runs in hodlr_oracle.c.  The one composite helper here is OracleHODLR.predict (eq_reg1 / eq_reg2), which combines
+the C solve with C kernel values and forms the final dot products with numpy; it is pinned against the dense GP
+posterior in tests/test_oracle_pins.py.
 """
 from __future__ import annotations
 
@@ -14,8 +17,9 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "hodlr_oracle.c")
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_TWIN_PATH = os.path.join(_HERE, "liboracle_twin.so")
 _lock = threading.Lock()
-_lib = None
+_libs = {}
 
 SE, MATERN32, MATERN52, EXP, IMQ, RQ = 0, 1, 2, 3, 4, 5
 KERNELS = {"se": SE, "matern32": MATERN32, "matern52": MATERN52, "exp": EXP, "imq": IMQ, "rq": RQ}
@@ -29,23 +33,24 @@ class OracleError(RuntimeError):
         self.status = STATUS.get(code, str(code))
 
 
-def build_oracle(force: bool = False) -> str:
-    """Compile hodlr_oracle.c with gcc -O2 -ffp-contract=off (no BLAS/OpenMP)."""
-    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC) \
-            or os.path.getmtime(_LIB_PATH) < os.path.getmtime(os.path.join(_HERE, "hodlr_oracle.h")):
-        tmp = _LIB_PATH + f".tmp{os.getpid()}"
+def build_oracle(force: bool = False, twin: bool = False) -> str:
+    """Compile hodlr_oracle.c with gcc -O2 -ffp-contract=off (no BLAS/OpenMP); twin=True adds -DORACLE_TWIN
+    (leaf LU + coupling-system Householder QR)."""
+    path = _TWIN_PATH if twin else _LIB_PATH
+    if force or not os.path.exists(path) or os.path.getmtime(path) < os.path.getmtime(_SRC) \
+            or os.path.getmtime(path) < os.path.getmtime(os.path.join(_HERE, "hodlr_oracle.h")):
+        tmp = path + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-Wall",
-                               "-o", tmp, _SRC, "-lm"])
-        os.replace(tmp, _LIB_PATH)
-    return _LIB_PATH
+                               *(["-DORACLE_TWIN"] if twin else []), "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, path)
+    return path
 
 
-def _load():
-    global _lib
+def _load(twin: bool = False):
     with _lock:
-        if _lib is not None:
-            return _lib
-        lib = C.CDLL(build_oracle())
+        if twin in _libs:
+            return _libs[twin]
+        lib = C.CDLL(build_oracle(twin=twin))
         P, I64, I32, D = C.c_void_p, C.c_int64, C.c_int, C.c_double
         lib.oracle_kernel.argtypes = [I32, P, D]; lib.oracle_kernel.restype = D
         lib.oracle_aca_dense.argtypes = [P, I64, I64, I64, D, I32, P, P, P]; lib.oracle_aca_dense.restype = I32
@@ -66,7 +71,8 @@ def _load():
         lib.oracle_free.argtypes = [P]; lib.oracle_free.restype = None
         lib.oracle_last_error.argtypes = []; lib.oracle_last_error.restype = C.c_char_p
         lib.oracle_dense.argtypes = [P, I64, I32, P, D, P, P, P]; lib.oracle_dense.restype = I32
-        _lib = lib
+        lib.oracle_residual_rows.argtypes = [P, P, P, P, I64, P]; lib.oracle_residual_rows.restype = I32
+        _libs[twin] = lib
         return lib
 
 
@@ -116,8 +122,10 @@ def dense_check(x, kernel: int, theta, sigma2: float, y=None):
 class OracleHODLR:
     """build -> factor -> {logdet, solve, gp_loglik}*, host memory, original point order."""
 
-    def __init__(self, x, kernel: int, theta, sigma2: float, leaf: int, eps: float, rank_cap: int = 0):
-        self._lib = _load()
+    def __init__(self, x, kernel: int, theta, sigma2: float, leaf: int, eps: float, rank_cap: int = 0,
+                 twin: bool = False):
+        self._lib = _load(twin)
+        self.twin = twin
         self.x = np.ascontiguousarray(x, dtype=np.float64)
         self.n = self.x.size
         self.kernel, self.theta = int(kernel), tuple(float(v) for v in theta)
@@ -176,6 +184,14 @@ class OracleHODLR:
         var = np.array([kernel_value(self.kernel, self.theta, 0.0) - Ks[j] @ self.solve(Ks[j])
                         for j in range(xt.size)])
         return mean, var
+
+    def residual_rows(self, xsol, y, rows):
+        """(C x - y)[rows] with C assembled entry by entry in C (original order)."""
+        xsol = np.ascontiguousarray(xsol, dtype=np.float64); y = np.ascontiguousarray(y, dtype=np.float64)
+        rows = np.ascontiguousarray(rows, dtype=np.int64)
+        out = np.zeros(rows.size)
+        _check(self._lib, self._lib.oracle_residual_rows(self._h, _ptr(xsol), _ptr(y), _ptr(rows), rows.size, _ptr(out)))
+        return out
 
     @property
     def kappa(self) -> int:

@@ -39,13 +39,27 @@ def up_to_date() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """One nvcc per translation unit, in parallel (object files under build/), then one shared link."""
     if not force and up_to_date():
         return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc(), *ARCH, *FLAGS, "-o", tmp, *sources()]
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = os.path.join(os.path.dirname(HERE), "build", "obj")
+    os.makedirs(objdir, exist_ok=True)
+    cflags = [f for f in FLAGS if f != "-shared"]
+    jobs = []
+    for src in sources():
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + f".{os.getpid()}.o")
+        jobs.append((obj, [nvcc(), *ARCH, *cflags, "-c", "-o", obj, src]))
     if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.check_call(cmd)
+        for _, cmd in jobs:
+            print(" ".join(cmd), file=sys.stderr)
+    with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as ex:
+        for f in [ex.submit(subprocess.check_call, cmd) for _, cmd in jobs]:
+            f.result()
+    tmp = LIB + f".tmp{os.getpid()}"
+    subprocess.check_call([nvcc(), *ARCH, "-shared", "-o", tmp, *[o for o, _ in jobs]])
+    for o, _ in jobs:
+        os.remove(o)
     os.replace(tmp, LIB)
     return LIB
 

@@ -351,7 +351,8 @@ __global__ void __launch_bounds__(ACA_SUB, ACA_PASS_MINB) k_aca_pass(const AcaCt
       st->k = k1;
       const long long mn = m1 < m2 ? m1 : m2;
       int done = 0;
-      if (sqrt(nu2) * sqrt(nv2) <= c.eps * sqrt(fabs(S2))) done = 1;     // stop term is kept
+      const int fr = c.forced ? c.forced[b] : -1;
+      if (fr >= 0 ? k1 >= fr : sqrt(nu2) * sqrt(nv2) <= c.eps * sqrt(fabs(S2))) done = 1;     // stop term is kept
       else if (k1 == mn) done = 1;
       else if (k1 == st->cap) { done = 2; atomicAdd(&flags[5], 1); }
       else if (bi < 0 || ba == 0.0) done = 1;
@@ -463,7 +464,8 @@ __global__ void __launch_bounds__(NT) k_aca_fused(AcaCtx c, const int *blocks, i
       const int k1 = k + 1;
       s_k = k1;
       int done = 0;
-      if (sqrt(nu2) * sqrt(nv2) <= c.eps * sqrt(fabs(S2))) done = 1;
+      const int fr = c.forced ? c.forced[b] : -1;
+      if (fr >= 0 ? k1 >= fr : sqrt(nu2) * sqrt(nv2) <= c.eps * sqrt(fabs(S2))) done = 1;
       else if (k1 == mn) done = 1;
       else if (k1 == cap) { done = 2; atomicAdd(&flags[5], 1); }
       else if (bi < 0 || ba == 0.0) done = 1;
@@ -498,7 +500,9 @@ __global__ void k_aca_cond(cudaGraphConditionalHandle hdl, const AcaCtx *__restr
 // same shape skip the planning and the graph instantiation.  A plan in use by another build is not shared.
 // ---------------------------------------------------------------------------------------------
 struct AcaPlan {
-  long long n; int leaf; int rank, nranks; bool seo;
+  // key: everything the cached device tables depend on -- the tree (n, leaf), the shard (rank, nranks), the
+  // factor slot layout (rank cap: colbase[e] = sum of min(cap, max node size)), the kernel variant and the device
+  long long n; int leaf; int rank, nranks; bool seo; int cap; int dev;
   long long nb; int nbig;
   std::vector<int> fused_blocks;
   int nfused_small = 0;                    // fused_blocks[0, nfused_small): both sides <= ACA_FUSED_SMALL
@@ -617,13 +621,13 @@ static AcaPlan *plan_acquire(const hodlr_s *h, hodlr_status *st) {
     std::lock_guard<std::mutex> lk(g_plan_mu);
     for (AcaPlan *P : g_plans)
       if (!P->busy && P->n == h->n && P->leaf == h->leaf && P->rank == h->grank && P->nranks == h->nranks &&
-          P->seo == (h->kp.kern == HODLR_SE)) {
+          P->seo == (h->kp.kern == HODLR_SE) && P->cap == h->cap && P->dev == h->dev) {
         P->busy = true; return P;
       }
   }
   AcaPlan *P = new AcaPlan();
   P->n = h->n; P->leaf = h->leaf; P->rank = h->grank; P->nranks = h->nranks; P->nb = h->ninternal; P->busy = true;
-  P->seo = h->kp.kern == HODLR_SE;
+  P->seo = h->kp.kern == HODLR_SE; P->cap = h->cap; P->dev = h->dev;
   cudaError_t e = plan_create(P, h);
   if (e != cudaSuccess) { *st = hodlr_cuda_check(e, "aca plan"); return nullptr; }   // (leaked on error)
   std::lock_guard<std::mutex> lk(g_plan_mu);
@@ -643,11 +647,11 @@ hodlr_status hodlr_aca(hodlr_s *h) {
   struct Rel { AcaPlan *p; ~Rel() { plan_release(p); } } rel{P};
   const int nbig = P->nbig;
   // ---- per-handle state ----
-  double *d_rec = (double *)hodlr_dalloc(h, sizeof(double) * ACA_RECW * (size_t)(P->nrec_r + P->nrec_c + 1));
-  h->ast = (AcaState *)hodlr_dalloc(h, sizeof(AcaState) * nb);
+  double *d_rec = (double *)hodlr_dalloc_tmp(h, sizeof(double) * ACA_RECW * (size_t)(P->nrec_r + P->nrec_c + 1));
+  h->ast = (AcaState *)hodlr_dalloc_tmp(h, sizeof(AcaState) * nb);
   h->rank = (int *)hodlr_dalloc(h, sizeof(int) * nb);
-  h->used = (unsigned char *)hodlr_dalloc(h, (size_t)h->kappa * n);
-  double *d_gram = (double *)hodlr_dalloc(h, sizeof(double) * 2 * ACA_GSZ * (size_t)(nbig > 0 ? nbig : 1));
+  h->used = (unsigned char *)hodlr_dalloc_tmp(h, (size_t)h->kappa * n);
+  double *d_gram = (double *)hodlr_dalloc_tmp(h, sizeof(double) * 2 * ACA_GSZ * (size_t)(nbig > 0 ? nbig : 1));
   if (!d_rec || !h->ast || !h->rank || !h->used || !d_gram) return hodlr_set_error(HODLR_ENOMEM, "aca: device allocation failed");
   h->bdepth = P->d_bdepth;
   // The step loop is latency-bound: everything of the ACA phase runs on a high-priority stream so that the
@@ -669,6 +673,7 @@ hodlr_status hodlr_aca(hodlr_s *h) {
   c.used = h->used; c.st = h->ast; c.active = h->dflags + 4; c.rank = h->rank; c.bdepth = P->d_bdepth;
   c.dt = h->d_dt; c.bigidx = P->d_bigidx; c.gram = d_gram; c.flags = h->dflags; c.step = h->dflags + 6;
   c.maxsteps = h->cap + 1;
+  c.forced = h->d_forced;
   AcaCtx cx[2] = {c, c};
   cx[0].items = P->d_items_r; cx[0].nq = P->d_nq; cx[0].recbase = P->d_rb; cx[0].rec = d_rec;
   cx[1].items = P->d_items_c; cx[1].nq = P->d_nq + nb; cx[1].recbase = P->d_rb + nb; cx[1].rec = d_rec + ACA_RECW * P->nrec_r;

@@ -38,16 +38,35 @@ hodlr_status hodlr_cuda_check(cudaError_t e, const char *what) {
 
 // Device blocks of freed handles are kept (per device, exact size) and handed to the next handle asking for the
 // same size: a repeated build of one shape then makes no allocation or free calls (hodlr_free synchronizes the
-// handle's streams before caching, so a reused block has no pending work).  Bounded at 16 GB per process.
+// handle's streams before caching, so a reused block has no pending work).  Bounded at 16 GB per process (or
+// HODLR_CACHE_MAX_MB); when an allocation fails the device's cached blocks are returned to the pool and the
+// allocation is retried once; hodlr_cache_trim() empties the cache on request.
 namespace {
 struct CachedBlock { int dev; size_t bytes; void *p; };
 std::mutex g_blk_mu;
 std::vector<CachedBlock> g_blk_cache;
 size_t g_blk_cached = 0;
-constexpr size_t kBlkCacheMax = (size_t)16 << 30;
+size_t blk_cache_max() {
+  static size_t mx = 0;
+  if (!mx) { const char *ev = getenv("HODLR_CACHE_MAX_MB"); mx = ev ? (size_t)atoll(ev) << 20 : (size_t)16 << 30; }
+  return mx;
+}
+// Free every cached block of `dev` (all devices if dev < 0); the caller holds g_blk_mu.
+void blk_cache_drain_locked(int dev) {
+  for (size_t i = g_blk_cache.size(); i-- > 0;) {
+    if (dev >= 0 && g_blk_cache[i].dev != dev) continue;
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != g_blk_cache[i].dev) cudaSetDevice(g_blk_cache[i].dev);
+    cudaFree(g_blk_cache[i].p);            // synchronous: the block has no pending work (see hodlr_free)
+    if (cur >= 0 && cur != g_blk_cache[i].dev) cudaSetDevice(cur);
+    g_blk_cached -= g_blk_cache[i].bytes;
+    g_blk_cache.erase(g_blk_cache.begin() + (long)i);
+  }
+}
 }
 
-void *hodlr_dalloc(hodlr_s *h, size_t bytes) {
+static void *dalloc_impl(hodlr_s *h, size_t bytes, bool transient) {
   void *p = nullptr;
   if (bytes == 0) bytes = 8;
   if (h->nallocs >= (int)(sizeof(h->allocs) / sizeof(h->allocs[0]))) return nullptr;
@@ -60,11 +79,58 @@ void *hodlr_dalloc(hodlr_s *h, size_t bytes) {
         break;
       }
   }
-  if (!p && cudaMallocAsync(&p, bytes, h->st) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+  if (!p && cudaMallocAsync(&p, bytes, h->st) != cudaSuccess) {
+    cudaGetLastError();
+    p = nullptr;
+    {   // flush this device's idle cached blocks back to the driver and retry once
+      std::lock_guard<std::mutex> lk(g_blk_mu);
+      blk_cache_drain_locked(h->dev);
+    }
+    cudaStreamSynchronize(h->st);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, h->dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+    if (cudaMallocAsync(&p, bytes, h->st) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+  }
   h->alloc_bytes[h->nallocs] = bytes;
+  h->alloc_tmp[h->nallocs] = transient ? 1 : 0;
   h->allocs[h->nallocs++] = p;
   h->bytes += (long long)bytes;
   return p;
+}
+
+void *hodlr_dalloc(hodlr_s *h, size_t bytes) { return dalloc_impl(h, bytes, false); }
+
+cudaError_t hodlr_allow_smem(const void *func, int dev) {
+  int maxsm = 0;
+  cudaError_t e = cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  cudaFuncAttributes fa;
+  e = cudaFuncGetAttributes(&fa, func);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm - (int)fa.sharedSizeBytes);
+}
+void *hodlr_dalloc_tmp(hodlr_s *h, size_t bytes) { return dalloc_impl(h, bytes, true); }
+
+// Hand the handle's transient blocks (radix-sort keys, ACA records / state) to the block cache.  Only called when
+// the handle's streams are idle.
+static void release_transient(hodlr_s *h) {
+  std::lock_guard<std::mutex> lk(g_blk_mu);
+  int w = 0;
+  for (int i = 0; i < h->nallocs; i++) {
+    if (!h->alloc_tmp[i]) {
+      h->allocs[w] = h->allocs[i]; h->alloc_bytes[w] = h->alloc_bytes[i]; h->alloc_tmp[w] = 0; w++;
+      continue;
+    }
+    h->bytes -= (long long)h->alloc_bytes[i];
+    if (g_blk_cached + h->alloc_bytes[i] <= blk_cache_max()) {
+      g_blk_cache.push_back({h->dev, h->alloc_bytes[i], h->allocs[i]});
+      g_blk_cached += h->alloc_bytes[i];
+    } else {
+      cudaFreeAsync(h->allocs[i], h->st);
+    }
+  }
+  h->nallocs = w;
+  h->used = nullptr; h->ast = nullptr; h->d_forced = nullptr;     // (ACA state: transient)
 }
 
 static void setup_pool(int dev) {
@@ -101,6 +167,11 @@ static hodlr_status finish(hodlr_s *h, hodlr_status st, double *tsec) {
 extern "C" {
 
 const char *hodlr_last_error(void) { return g_err; }
+
+void hodlr_cache_trim(void) {
+  std::lock_guard<std::mutex> lk(g_blk_mu);
+  blk_cache_drain_locked(-1);
+}
 const char *hodlr_version(void) { return "hodlr_b200 0.1 sm_100a fp64"; }
 int64_t hodlr_launch_count(void) { return hodlr_global_launches; }
 
@@ -175,7 +246,7 @@ void hodlr_free(hodlr_t h) {
   {
     std::lock_guard<std::mutex> lk(g_blk_mu);
     for (int i = h->nallocs - 1; i >= 0; i--) {
-      if (g_blk_cached + h->alloc_bytes[i] <= kBlkCacheMax) {
+      if (g_blk_cached + h->alloc_bytes[i] <= blk_cache_max()) {
         g_blk_cache.push_back({h->dev, h->alloc_bytes[i], h->allocs[i]});
         g_blk_cached += h->alloc_bytes[i];
       } else {
@@ -297,6 +368,11 @@ hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const 
   // issued now on a side stream and overlap the ACA; hodlr_factor waits for them.
   st = hodlr_leaf_alloc(h);
   if (st != HODLR_OK) goto fail;
+  if (opts && opts->forced_ranks && h->ninternal > 0) {    // parity test hook (hodlr.h)
+    h->d_forced = (int *)hodlr_dalloc_tmp(h, sizeof(int) * (size_t)h->ninternal);
+    if (!h->d_forced) { st = hodlr_set_error(HODLR_ENOMEM, "build: device allocation failed"); goto fail; }
+    CK(cudaMemcpyAsync(h->d_forced, opts->forced_ranks, sizeof(int) * (size_t)h->ninternal, cudaMemcpyHostToDevice, h->st));
+  }
   static int chol_after = -1;     // HODLR_CHOL_AFTER_ACA=1: run the leaf Cholesky after the ACA (experiments)
   if (chol_after < 0) { const char *ev = getenv("HODLR_CHOL_AFTER_ACA"); chol_after = ev && atoi(ev) ? 1 : 0; }
   if (!chol_after) {
@@ -339,7 +415,7 @@ hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const 
     loc[0] = f5;
     if (h->nranks > 1) {
       const size_t per = kappa + 2;
-      double *dbuf = (double *)hodlr_dalloc(h, sizeof(double) * per * (h->nranks + 1));
+      double *dbuf = (double *)hodlr_dalloc_tmp(h, sizeof(double) * per * (h->nranks + 1));
       if (!dbuf) { st = hodlr_set_error(HODLR_ENOMEM, "build: device allocation failed"); goto fail; }
       std::vector<double> all(per * h->nranks);
       CK(cudaMemcpyAsync(dbuf, loc.data(), sizeof(double) * per, cudaMemcpyHostToDevice, h->st));
@@ -366,6 +442,7 @@ hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const 
   st = finish(h, HODLR_OK, &h->t_build);
   hodlr_trace("build: finished");
   if (st != HODLR_OK) goto fail;
+  release_transient(h);        // h->st is idle here; the leaf Cholesky (st3) uses no transient block
   h->state = 1;
   *out = h;
   return HODLR_OK;

@@ -264,19 +264,12 @@ hodlr_status hodlr_leaf_alloc(hodlr_s *h) {
   return HODLR_OK;
 }
 
-hodlr_status hodlr_leaf_pair_mma(hodlr_s *h, int K, const TreeCtx &tc, bool *used);
-
-static int tree_plain_from() {     // debug/experiment switch: depths >= HODLR_TREE_PLAIN_FROM use plain double
-  static int plain_from = -1;
-  if (plain_from < 0) { const char *ev = getenv("HODLR_TREE_PLAIN_FROM"); plain_from = ev ? atoi(ev) : 1 << 20; }
-  return plain_from;
-}
 
 static TreeCtx tree_ctx(hodlr_s *h, int d, long long i0) {
   const DepthTab &dt = h->dt;
   TreeCtx tc;
   tc.d = d; tc.i0 = i0; tc.r = dt.rdep[d + 1]; tc.q = 2 * tc.r; tc.Kd = dt.Kdim[d]; tc.K1 = dt.Kdim[d + 1];
-  tc.ldk = (tc.Kd + 3) & ~3; tc.dd = d < tree_plain_from();
+  tc.ldk = (tc.Kd + 3) & ~3; tc.dd = 1;   // compensated at every depth
   tc.Pi1 = h->Pipool + dt.piOff[d + 1]; tc.Pic = h->Pipool + dt.piOff[d];
   tc.Sst = h->Spool + dt.nodeS[d]; tc.BT = h->BTpool + dt.nodeBT[d];
   tc.node_ld = h->node_ld; tc.flags = h->dflags;
@@ -316,20 +309,8 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
   // ---- leaves ----
   HCUDA(cudaStreamWaitEvent(h->st, h->ev_chol, 0));     // leaf Cholesky issued during the build
   ph_begin(h, PH_LEAF);
-  bool fast = false, paired = false;
-  // HODLR_LEAF_PAIR=1: leaves fused with the depth-(kappa-1) coupling systems (k_leaf_pair).  Measured slower
-  // at config 3 (2.52 ms vs 1.40 + 0.43 ms): at one CTA per SM the node phase cannot overlap the DMMA work.
-  static int no_pair = -1;
-  if (no_pair < 0) { const char *ev = getenv("HODLR_LEAF_PAIR"); no_pair = ev && atoi(ev) ? 0 : 1; }
-  if (kappa >= 1 && !no_pair) {     // leaves fused with the depth-(kappa-1) coupling systems
-    long long i0, cnt;
-    hodlr_own_nodes(h, kappa - 1, &i0, &cnt);
-    const TreeCtx tc = tree_ctx(h, kappa - 1, i0);
-    hodlr_status fs = hodlr_leaf_pair_mma(h, K, tc, &paired);
-    if (fs != HODLR_OK) return fs;
-    fast = paired;
-  }
-  if (!fast) {
+  bool fast = false;
+  {
     hodlr_status fs = hodlr_leaf_factor_mma(h, K, h->Pipool + dt.piOff[kappa], &fast);   // needs the Cholesky kernel
     if (fs != HODLR_OK) return fs;
   }
@@ -347,7 +328,7 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
     lc.scratch = nullptr; lc.scratch_per_cta = 0;
     if (need <= (size_t)maxsm - 12 * 1024) {
       lc.use_smem = 1;
-      HCUDA(cudaFuncSetAttribute(k_leaf_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
+      HCUDA(hodlr_allow_smem((const void *)k_leaf_factor, h->dev));
     } else {
       lc.use_smem = 0; need = 0;
       grid = (int)(lc.nown < 148 * 4 ? lc.nown : 148 * 4);
@@ -368,15 +349,13 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
   }
   if (tree_smem_max > (size_t)maxsm - 2048)
     return hodlr_set_error(HODLR_EINVAL, "factor: coupling system too large for shared memory");
-  static size_t tree_attr = 0;
-  if (kappa > 0 && tree_smem_max > tree_attr) {
-    HCUDA(cudaFuncSetAttribute(k_tree_factor<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tree_smem_max));
-    HCUDA(cudaFuncSetAttribute(k_tree_factor<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tree_smem_max));
-    HCUDA(cudaFuncSetAttribute(k_tree_factor_narrow<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tree_smem_max));
-    HCUDA(cudaFuncSetAttribute(k_tree_factor_narrow<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tree_smem_max));
-    tree_attr = tree_smem_max;
+  // (the device maximum, set on every call: a process-wide "already set" guard is neither per-device nor
+  // thread-safe, and concurrent handles needing different sizes would race on a per-call value)
+  if (kappa > 0) {
+    HCUDA(hodlr_allow_smem((const void *)k_tree_factor<true>, h->dev));
+    HCUDA(hodlr_allow_smem((const void *)k_tree_factor_narrow<true>, h->dev));
   }
-  for (int d = paired ? kappa - 2 : kappa - 1; d >= 0; d--) {
+  for (int d = kappa - 1; d >= 0; d--) {
     if (d + 1 == h->tsplit && h->nranks > 1) {     // every rank gets the Pi of all depth-t subtree roots
       const long long Kt = dt.Kdim[d + 1], sz = Kt * (Kt + 1) / 2;
       double *base = h->Pipool + dt.piOff[d + 1];
@@ -388,13 +367,8 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
     const TreeCtx tc = tree_ctx(h, d, i0);
     const size_t smem = sizeof(double) * (size_t)tree_smem_doubles(tc.q, tc.ldk);
     const bool narrow = cnt >= TREE_NARROW_MIN && tc.q <= 16;
-    if (narrow) {
-      if (tc.dd) k_tree_factor_narrow<true><<<(int)cnt, TT / 2, smem, h->st>>>(tc);
-      else k_tree_factor_narrow<false><<<(int)cnt, TT / 2, smem, h->st>>>(tc);
-    } else {
-      if (tc.dd) k_tree_factor<true><<<(int)cnt, TT, smem, h->st>>>(tc);
-      else k_tree_factor<false><<<(int)cnt, TT, smem, h->st>>>(tc);
-    }
+    if (narrow) k_tree_factor_narrow<true><<<(int)cnt, TT / 2, smem, h->st>>>(tc);
+    else k_tree_factor<true><<<(int)cnt, TT, smem, h->st>>>(tc);
     HLAUNCH(h, "k_tree_factor");
   }
   // log det: this rank's leaves and subtree nodes (others are 0), exchanged with the failure counts, then the

@@ -119,6 +119,7 @@ struct AcaCtx {
   int *step;                // step counter of the device loop
   int maxsteps;
   double *gram;             // per big block: packed G_U = U'^T U', then G_V = V'^T V' 
+  const int *forced;        // test hook (hodlr_opts.forced_ranks): stop block b at exactly forced[b] terms, or NULL
 };
 
 // ----------------------------------------------------------------------------------------------
@@ -176,6 +177,7 @@ struct hodlr_s {
   AcaState *ast;
   int *rank;
   int *bdepth;
+  int *d_forced;             // hodlr_opts.forced_ranks on the device (test hook), or NULL
   int *dflags;               // [0] nonfinite x, [1] notpd, [2] notpd node (min), [3] nonfinite y, [4] active big
                              // ACA blocks, [5] rank-cap hits, [6] ACA steps, [7] x not ascending
   DepthTab *d_dt;
@@ -197,7 +199,7 @@ struct hodlr_s {
   int ph_pending[PH_N];
   double ph_ms[PH_N];        // accumulated device ms per kernel family (since build)
   long long ph_calls[PH_N];
-  void *allocs[64]; size_t alloc_bytes[64]; int nallocs;
+  void *allocs[64]; size_t alloc_bytes[64]; unsigned char alloc_tmp[64]; int nallocs;
   double *apply_ws = nullptr; size_t apply_ws_n = 0;   // hodlr_apply workspace (apply.cu)
   double *pred_ws = nullptr; size_t pred_ws_n = 0;     // gp_predict workspace (predict.cu)
 };
@@ -212,6 +214,11 @@ void hodlr_trace(const char *what);
 hodlr_status hodlr_set_error(hodlr_status code, const char *fmt, ...);
 hodlr_status hodlr_cuda_check(cudaError_t e, const char *what);
 void *hodlr_dalloc(hodlr_s *h, size_t bytes);
+// Allow `func` the device's whole opt-in shared memory (minus its static shared memory).  Called before every
+// launch that needs more than 48 KB: the value is the same from every thread and handle, so concurrent handles
+// needing different sizes cannot race; occupancy follows each launch's own size.
+cudaError_t hodlr_allow_smem(const void *func, int dev);
+void *hodlr_dalloc_tmp(hodlr_s *h, size_t bytes);   // dead after the build: handed to the block cache when it ends
 extern long long hodlr_global_launches;
 
 // phase entry points (one per .cu file)

@@ -49,8 +49,10 @@ __device__ __forceinline__ void c_to_b(double c0, double c1, int lane, double &b
   b1 = sel ? y1 : y0;
 }
 
-// (I, J) of packed lower tile index ti, for T <= 16 (136 tiles)
-__constant__ unsigned char c_tileI[136], c_tileJ[136];
+// (I, J) of packed lower tile index ti, for T <= 16 (136 tiles); statically initialised (per device at module
+// load, so no host-side "tables ready" state)
+__constant__ unsigned char c_tileI[136] = {0,1,1,2,2,2,3,3,3,3,4,4,4,4,4,5,5,5,5,5,5,6,6,6,6,6,6,6,7,7,7,7,7,7,7,7,8,8,8,8,8,8,8,8,8,9,9,9,9,9,9,9,9,9,9,10,10,10,10,10,10,10,10,10,10,10,11,11,11,11,11,11,11,11,11,11,11,11,12,12,12,12,12,12,12,12,12,12,12,12,12,13,13,13,13,13,13,13,13,13,13,13,13,13,13,14,14,14,14,14,14,14,14,14,14,14,14,14,14,14,15,15,15,15,15,15,15,15,15,15,15,15,15,15,15,15};
+__constant__ unsigned char c_tileJ[136] = {0,0,1,0,1,2,0,1,2,3,0,1,2,3,4,0,1,2,3,4,5,0,1,2,3,4,5,6,0,1,2,3,4,5,6,7,0,1,2,3,4,5,6,7,8,0,1,2,3,4,5,6,7,8,9,0,1,2,3,4,5,6,7,8,9,10,0,1,2,3,4,5,6,7,8,9,10,11,0,1,2,3,4,5,6,7,8,9,10,11,12,0,1,2,3,4,5,6,7,8,9,10,11,12,13,0,1,2,3,4,5,6,7,8,9,10,11,12,13,14,0,1,2,3,4,5,6,7,8,9,10,11,12,13,14,15};
 
 struct LeafMmaCtx {
   KParams kp;
@@ -615,177 +617,10 @@ __global__ void __launch_bounds__(ZTH, 1) k_leaf_zsyrk_p(LeafMmaCtx c, long long
   asm volatile("cp.async.wait_group 0;\n" ::);
 }
 
-// ---------------------------------------------------------------------------------------------
-// Kernel 2' (fused with the deepest tree level): one CTA per depth-(kappa-1) node c with leaves c1 = 2i,
-// c2 = 2i+1.  For each leaf: Z = X E (as k_leaf_zsyrk), the s-part rows Pi_l[s, :] = Z_s^T Z, and
-// Pi_D += Z_a^T Z_a accumulated in DMMA registers across both leaves (Pi_D = Pi_c1[a,a] + Pi_c2[a,a]).
-// Then the node's coupling system and Schur update (tree_node) from shared memory.  The leaves' own Pi are
-// never written to HBM.
-// ---------------------------------------------------------------------------------------------
-struct PairPi {
-  const double *Ps0, *Ps1;  // shared: Pi_c1[s, :], Pi_c2[s, :] (r rows x K)
-  const double *D;          // shared: Pi_D rows (a >= b used), leading dimension ldD
-  int ldD, Kd, K;
-  __device__ double s21(int a, int b) const { return Ps1[a * K + Kd + b]; }
-  __device__ double s12(int a, int b) const { return Ps0[a * K + Kd + b]; }
-  __device__ double b2(int a, int col) const { return Ps1[a * K + col]; }
-  __device__ double b1(int a, int col) const { return Ps0[a * K + col]; }
-  template <bool DD> __device__ void d(int a, int b, double &hs, double &ls) const { hs = D[a * ldD + b]; ls = 0.0; }
-};
-
-template <int P>
-__global__ void __launch_bounds__(ZTH, 1) k_leaf_pair(LeafMmaCtx c, TreeCtx tc) {
-  constexpr int T = P / 8;
-  constexpr int NTILE = T * (T + 1) / 2;
-  constexpr int LDR = P + 4;
-  extern __shared__ double sm[];
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int K = c.K, Kp = c.Kp, Kc = Kp / 8, Kz = c.Kz;
-  const int Kd = tc.Kd, r = tc.r;
-  double *sX = sm;                              // NTILE * 64
-  double *sZ = sX + NTILE * 64;                 // Kz * LDR (column-major)
-  long long *colsrc = (long long *)(sZ + (long long)Kz * LDR);   // Kz
-  double *sPs = (double *)(colsrc + Kz);        // 2 * r * K
-  const long long node = tc.i0 + blockIdx.x;    // index within depth kappa - 1
-  const int KdB = (Kd + 15) / 16;               // 16x16 blocks over the a-columns
-  const int nblkD = KdB * (KdB + 1) / 2;
-  double accD[3][8];
-#pragma unroll
-  for (int s3 = 0; s3 < 3; s3++)
-#pragma unroll
-    for (int q = 0; q < 8; q++) accD[s3][q] = 0.0;
-  const int g = lane >> 2, tq = lane & 3;
-  for (int side = 0; side < 2; side++) {
-    const long long leaf = 2 * node + side;
-    const long long id = c.ninternal + leaf, lo = c.lo[id];
-    const int m = (int)(c.hi[id] - lo);
-    {
-      const double *Lg = c.Lf + leaf * c.lstride;
-      for (int p = t; p < NTILE * 32; p += ZTH) {
-        unsigned sa = (unsigned)__cvta_generic_to_shared(sX + 2 * p);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(sa), "l"(Lg + 2 * p));
-      }
-    }
-    for (int q = t; q < Kz; q += ZTH) colsrc[q] = leaf_colsrc(c, id, q);
-    __syncthreads();
-    if (((c.ldx | lo) & 1) == 0) {
-      for (int p = t; p < Kz * (P / 2); p += ZTH) {
-        const int col = p / (P / 2), row = 2 * (p - col * (P / 2));
-        const long long src = colsrc[col];
-        double *dst = sZ + col * LDR + row;
-        if (src >= 0 && row + 1 < m) {
-          unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(sa), "l"(c.Xh + src * c.ldx + lo + row));
-        } else {
-          dst[0] = (src >= 0 && row < m) ? c.Xh[src * c.ldx + lo + row] : 0.0;
-          dst[1] = 0.0;
-        }
-      }
-    } else {
-      for (int p = t; p < Kz * P; p += ZTH) {
-        const int col = p / P, row = p - col * P;
-        const long long src = colsrc[col];
-        sZ[col * LDR + row] = (src >= 0 && row < m) ? c.Xh[src * c.ldx + lo + row] : 0.0;
-      }
-    }
-    asm volatile("cp.async.commit_group;\n" ::);
-    asm volatile("cp.async.wait_group 0;\n" ::);
-    __syncthreads();
-    // Z = X E (DMMA GEMM, one 8-column tile per warp)
-    {
-      const int q2 = 2 * (lane & 3), kq = lane & 3;
-      for (int cc = warp; cc < Kc; cc += ZW) {
-        double acc[T][2];
-#pragma unroll
-        for (int i = 0; i < T; i++) { acc[i][0] = 0.0; acc[i][1] = 0.0; }
-        const double *zc = sZ + (8 * cc + g) * LDR;
-#pragma unroll
-        for (int kb = 0; kb < T; kb++) {
-          const double b0 = zc[8 * kb + kq], b1 = zc[8 * kb + 4 + kq];
-#pragma unroll
-          for (int i = kb; i < T; i++) {
-            const double *tA = sX + tix(i, kb) * 64;
-            dmma(acc[i][0], acc[i][1], tA[lane], b0);
-            dmma(acc[i][0], acc[i][1], tA[32 + lane], b1);
-          }
-        }
-        __syncwarp();
-#pragma unroll
-        for (int i = 0; i < T; i++) {
-          sZ[(8 * cc + q2) * LDR + 8 * i + g] = acc[i][0];
-          sZ[(8 * cc + q2 + 1) * LDR + 8 * i + g] = acc[i][1];
-        }
-      }
-    }
-    __syncthreads();
-    // s-part rows Pi_l[Kd + u, col] = Z[:, Kd + u] . Z[:, col]: warp per (u, col), lanes over rows
-    double *Ps = sPs + side * r * K;
-    for (int pc = warp; pc < r * K; pc += ZW) {
-      const int u = pc / K, col = pc - u * K;
-      const double *zu = sZ + (Kd + u) * LDR, *zc = sZ + col * LDR;
-      double sacc = 0.0;
-      for (int i = lane; i < P; i += 32) sacc = fma(zu[i], zc[i], sacc);
-      sacc = warp_sum(sacc);
-      if (lane == 0) Ps[pc] = sacc;
-    }
-    // Pi_D += Z_a^T Z_a over this leaf's rows: 16x16 blocks, DMMA m16n8k8 (same tiling as k_leaf_zsyrk)
-    const int kend = (m + 7) & ~7;
-#pragma unroll
-    for (int s3 = 0; s3 < 3; s3++) {
-      const int blk = warp + ZW * s3;
-      if (blk < nblkD) {
-        const int BI = c_tileI[blk], BJ = c_tileJ[blk];
-        const double *pa0 = sZ + (16 * BI + g) * LDR + tq;
-        const double *pa1 = pa0 + 8 * LDR;
-        const double *pb0 = sZ + (16 * BJ + g) * LDR + tq;
-        const double *pb1 = pb0 + 8 * LDR;
-        for (int k0 = 0; k0 < kend; k0 += 8) {
-          const double a0 = pa0[k0], a1 = pa1[k0], a2 = pa0[k0 + 4], a3 = pa1[k0 + 4];
-          dmma16(accD[s3], a0, a1, a2, a3, pb0[k0], pb0[k0 + 4]);
-          dmma16(accD[s3] + 4, a0, a1, a2, a3, pb1[k0], pb1[k0 + 4]);
-        }
-      }
-    }
-    __syncthreads();
-  }
-  // Pi_D (rows a >= b of the a-columns) into shared memory over the Z area; node scratch over the X area
-  const int ldD = 16 * KdB;
-  double *sD = sZ;
-#pragma unroll
-  for (int s3 = 0; s3 < 3; s3++) {
-    const int blk = warp + ZW * s3;
-    if (blk < nblkD) {
-      const int BI = c_tileI[blk], BJ = c_tileJ[blk];
-#pragma unroll
-      for (int q = 0; q < 8; q++) {
-        const int row = 16 * BI + g + ((q & 2) ? 8 : 0);
-        const int col = 16 * BJ + 2 * tq + (q & 1) + (q >= 4 ? 8 : 0);
-        sD[row * ldD + col] = accD[s3][q];
-      }
-    }
-  }
-  __syncthreads();
-  PairPi src;
-  src.Ps0 = sPs; src.Ps1 = sPs + r * K; src.D = sD; src.ldD = ldD; src.Kd = Kd; src.K = K;
-  if (tc.dd) tree_node<true>(tc, node, sX, src); else tree_node<false>(tc, node, sX, src);
-}
-
 }  // namespace
 
 // Leaf fast path applies for leaf <= 128 (P = 64 or 128).
 static int leaf_P(const hodlr_s *h) { return h->leaf_max <= 64 ? 64 : (h->leaf_max <= 128 ? 128 : 0); }
-
-static bool leaf_tables_ready = false;
-static hodlr_status leaf_tables() {
-  if (leaf_tables_ready) return HODLR_OK;
-  unsigned char ti[136], tj[136];
-  int q = 0;
-  for (int I = 0; I < 16; I++) for (int J = 0; J <= I; J++) { ti[q] = (unsigned char)I; tj[q] = (unsigned char)J; q++; }
-  HCUDA(cudaMemcpyToSymbol(c_tileI, ti, sizeof(ti)));
-  HCUDA(cudaMemcpyToSymbol(c_tileJ, tj, sizeof(tj)));
-  leaf_tables_ready = true;
-  return HODLR_OK;
-}
 
 static LeafMmaCtx leaf_ctx(hodlr_s *h, int K, double *Pi_leaf) {
   LeafMmaCtx c;
@@ -803,14 +638,14 @@ hodlr_status hodlr_leaf_chol_mma(hodlr_s *h, cudaStream_t stream, bool *launched
   *launched = false;
   const int P = leaf_P(h);
   if (P == 0 || h->nleaves == 0) return HODLR_OK;
-  hodlr_status ts = leaf_tables();
-  if (ts != HODLR_OK) return ts;
   const int T = P / 8, NTILE = T * (T + 1) / 2;
   const size_t smem = sizeof(double) * ((size_t)NTILE * 64 + T * 64 + 2 * P);
   LeafMmaCtx c = leaf_ctx(h, 0, nullptr);
+  int maxsm = 0;      // attributes are set to the device maximum (same value from every thread; see factor.cu)
+  HCUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
 #define LAUNCH_CHOL(PP, SE_)                                                                                    \
   do {                                                                                                         \
-    HCUDA(cudaFuncSetAttribute(k_leaf_chol<PP, SE_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));  \
+    HCUDA(hodlr_allow_smem((const void *)k_leaf_chol<PP, SE_>, h->dev));  \
     k_leaf_chol<PP, SE_><<<(int)(h->nleaves >> h->tsplit), NTH, smem, stream>>>(c);                           \
   } while (0)
   const bool seo = h->kp.kern == HODLR_SE;
@@ -848,64 +683,25 @@ hodlr_status hodlr_leaf_factor_mma(hodlr_s *h, int K, double *Pi_leaf, bool *use
   bool wide = false;                                 // X from global memory when X + Z do not fit
   if (smem + 64 > (size_t)maxsm) { smem = sizeof(double) * ((size_t)Kz * LDR + Kz); wide = true; }
   if (smem + 64 > (size_t)maxsm) return HODLR_OK;
-  hodlr_status ts = leaf_tables();
-  if (ts != HODLR_OK) return ts;
   LeafMmaCtx c = leaf_ctx(h, K, Pi_leaf);
   const int grid = (int)(h->nleaves >> h->tsplit);
 #define LAUNCH_ZS(PP, XGV)                                                                                     \
   do {                                                                                                        \
-    HCUDA(cudaFuncSetAttribute(k_leaf_zsyrk<PP, XGV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    HCUDA(hodlr_allow_smem((const void *)k_leaf_zsyrk<PP, XGV>, h->dev)); \
     k_leaf_zsyrk<PP, XGV><<<grid, ZTH, smem, h->st>>>(c);                                                      \
   } while (0)
 #define LAUNCH_ZSP(PP)                                                                                         \
   do {                                                                                                        \
-    HCUDA(cudaFuncSetAttribute(k_leaf_zsyrk_p<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));   \
+    HCUDA(hodlr_allow_smem((const void *)k_leaf_zsyrk_p<PP>, h->dev));   \
     k_leaf_zsyrk_p<PP><<<std::min(grid, nsm), ZTH, smem, h->st>>>(c, (long long)grid);                          \
   } while (0)
-  static int persist = -1;     // HODLR_ZSYRK_PERSIST=0: one CTA per leaf (no cross-leaf prefetch)
-  if (persist < 0) { const char *ev = getenv("HODLR_ZSYRK_PERSIST"); persist = ev ? atoi(ev) : 1; }
   int nsm = 148;
   HCUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->dev));
-  if (P == 64) { if (wide) LAUNCH_ZS(64, true); else if (persist) LAUNCH_ZSP(64); else LAUNCH_ZS(64, false); }
-  else { if (wide) LAUNCH_ZS(128, true); else if (persist) LAUNCH_ZSP(128); else LAUNCH_ZS(128, false); }
+  if (P == 64) { if (wide) LAUNCH_ZS(64, true); else LAUNCH_ZSP(64); }
+  else { if (wide) LAUNCH_ZS(128, true); else LAUNCH_ZSP(128); }
 #undef LAUNCH_ZS
 #undef LAUNCH_ZSP
   HLAUNCH(h, "k_leaf_zsyrk");
-  *used = true;
-  return HODLR_OK;
-}
-
-// Fused leaves + deepest tree level (kernel 2'); *used reports whether it ran.  Applies on the fast path when the
-// node scratch and Pi_D fit over the leaf staging and each depth-(kappa-1) node's two leaves belong to this rank.
-hodlr_status hodlr_leaf_pair_mma(hodlr_s *h, int K, const TreeCtx &tc, bool *used) {
-  *used = false;
-  const int P = leaf_P(h);
-  if (P == 0 || !h->chol_done || h->kappa < 1 || h->tsplit >= h->kappa) return HODLR_OK;
-  const int Kp = (K + 7) / 8 * 8;
-  if (Kp / 8 > ZW) return HODLR_OK;
-  const int Kz = (K + 15) / 16 * 16;
-  const int T = P / 8, NTILE = T * (T + 1) / 2, LDR = P + 4;
-  const int KdB = (tc.Kd + 15) / 16;
-  if (KdB * (KdB + 1) / 2 > 3 * ZW) return HODLR_OK;                 // Pi_D blocks held in registers
-  if ((long long)16 * KdB * 16 * KdB > (long long)Kz * LDR) return HODLR_OK;          // Pi_D over the Z area
-  if (tree_smem_doubles(tc.q, tc.ldk) > (long long)NTILE * 64) return HODLR_OK;      // node scratch over X
-  const size_t smem = sizeof(double) * ((size_t)NTILE * 64 + (size_t)Kz * LDR + Kz + 2 * (size_t)tc.r * K);
-  int maxsm = 0;
-  HCUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
-  if (smem + 2048 > (size_t)maxsm) return HODLR_OK;
-  hodlr_status ts = leaf_tables();
-  if (ts != HODLR_OK) return ts;
-  LeafMmaCtx c = leaf_ctx(h, K, nullptr);
-  long long i0, cnt;
-  hodlr_own_nodes(h, h->kappa - 1, &i0, &cnt);
-  if (P == 64) {
-    HCUDA(cudaFuncSetAttribute(k_leaf_pair<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_leaf_pair<64><<<(int)cnt, ZTH, smem, h->st>>>(c, tc);
-  } else {
-    HCUDA(cudaFuncSetAttribute(k_leaf_pair<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_leaf_pair<128><<<(int)cnt, ZTH, smem, h->st>>>(c, tc);
-  }
-  HLAUNCH(h, "k_leaf_pair");
   *used = true;
   return HODLR_OK;
 }

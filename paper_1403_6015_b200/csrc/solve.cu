@@ -856,10 +856,12 @@ hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_on
     if (!h->stamps) h->stamps = (unsigned long long *)hodlr_dalloc(h, sizeof(unsigned long long) * 128);
     c.stamps = h->stamps;
   }
-  static size_t attr = 0;
-  if (dsm > attr) {
-    HCUDA(cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
-    attr = dsm;
+  {   // the device's opt-in maximum on every call: the same value from every thread and handle (no race between
+      // handles that need different sizes), and it permits every launch size; occupancy follows the launch's own size
+    int maxsm = 0;
+    HCUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
+    if (dsm > (size_t)maxsm) return hodlr_set_error(HODLR_EINVAL, "solve: %zu B of shared memory needed", dsm);
+    HCUDA(hodlr_allow_smem((const void *)k_solve, h->dev));
   }
   if (!h->bulk_checked) {     // bulk staging needs every leaf start and size and n even (16-byte segments)
     bool ok = (h->ldx % 2) == 0;

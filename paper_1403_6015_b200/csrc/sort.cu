@@ -139,11 +139,11 @@ __global__ void k_finish(const unsigned long long *__restrict__ key, const long 
 hodlr_status hodlr_sort_and_tree(hodlr_s *h, const double *x) {
   const long long n = h->n;
   const int ntiles = (int)((n + TILE - 1) / TILE);
-  unsigned long long *k0 = (unsigned long long *)hodlr_dalloc(h, sizeof(unsigned long long) * n);
-  unsigned long long *k1 = (unsigned long long *)hodlr_dalloc(h, sizeof(unsigned long long) * n);
-  long long *i0 = (long long *)hodlr_dalloc(h, sizeof(long long) * n);
-  long long *i1 = (long long *)hodlr_dalloc(h, sizeof(long long) * n);
-  unsigned int *cnt = (unsigned int *)hodlr_dalloc(h, sizeof(unsigned int) * (256 * (size_t)ntiles + 256));
+  unsigned long long *k0 = (unsigned long long *)hodlr_dalloc_tmp(h, sizeof(unsigned long long) * n);
+  unsigned long long *k1 = (unsigned long long *)hodlr_dalloc_tmp(h, sizeof(unsigned long long) * n);
+  long long *i0 = (long long *)hodlr_dalloc_tmp(h, sizeof(long long) * n);
+  long long *i1 = (long long *)hodlr_dalloc_tmp(h, sizeof(long long) * n);
+  unsigned int *cnt = (unsigned int *)hodlr_dalloc_tmp(h, sizeof(unsigned int) * (256 * (size_t)ntiles + 256));
   unsigned int *tot = cnt + 256 * (size_t)ntiles;
   if (ntiles > 256 * 16) return hodlr_set_error(HODLR_EINVAL, "sort: n too large for the radix tile table");
   if (!k0 || !k1 || !i0 || !i1 || !cnt) return hodlr_set_error(HODLR_ENOMEM, "sort: device allocation failed");

@@ -38,7 +38,8 @@ class hodlr_dist(C.Structure):
 
 
 class hodlr_opts(C.Structure):
-    _fields_ = [("rank_cap", C.c_int32), ("reserved", C.c_int32 * 7)]
+    _fields_ = [("rank_cap", C.c_int32), ("flags", C.c_int32), ("forced_ranks", C.c_void_p),
+                ("reserved", C.c_int64 * 6)]
 
 
 class hodlr_info_t(C.Structure):
@@ -120,11 +121,17 @@ def _stream_ptr(stream) -> int:
 
 # ------------------------------------------------------------------ C-ABI mirrors
 def hodlr_build(x: torch.Tensor, kernel: int, theta, sigma2: float, leaf: int, eps: float,
-                rank_cap: int = 0, stream=None, dist: "hodlr_dist | None" = None) -> int:
+                rank_cap: int = 0, stream=None, dist: "hodlr_dist | None" = None, forced_ranks=None) -> int:
+    """forced_ranks: optional int32 array of the internal nodes' ACA ranks (heap order) -- the parity test hook of
+    hodlr_opts.forced_ranks."""
     lib = load()
     x = _dev_f64(x, "x")
     th = (C.c_double * 3)(float(theta[0]), float(theta[1]), float(theta[2]) if len(theta) > 2 else 0.0)
     opts = hodlr_opts(int(rank_cap))
+    if forced_ranks is not None:
+        import numpy as np
+        fr = np.ascontiguousarray(forced_ranks, dtype=np.int32)
+        opts.forced_ranks = fr.ctypes.data
     h = C.c_void_p(0)
     _check(lib.hodlr_build(x.data_ptr(), x.numel(), int(kernel), th, float(sigma2), int(leaf), float(eps),
                            C.byref(dist) if dist is not None else None, C.byref(opts), _stream_ptr(stream),
@@ -247,14 +254,15 @@ class HODLR:
     """build -> factor -> {logdet, solve, gp_loglik}* on one GPU; inputs are CUDA float64 tensors."""
 
     def __init__(self, x: torch.Tensor, kernel, theta, sigma2: float, leaf: int, eps: float,
-                 rank_cap: int = 0, stream=None, dist=None):
-        """dist: None (one GPU) or a paper_1403_6015_b200.dist.Dist (subtree sharding)."""
+                 rank_cap: int = 0, stream=None, dist=None, forced_ranks=None):
+        """dist: None (one GPU) or a paper_1403_6015_b200.dist.Dist (subtree sharding).  forced_ranks: parity test
+        hook (hodlr_opts.forced_ranks)."""
         if isinstance(kernel, str):
             kernel = KERNELS[kernel]
         self.n = x.numel()
         self._dist = dist                       # keeps the NCCL id / group alive
         self._h = hodlr_build(x, kernel, theta, sigma2, leaf, eps, rank_cap, stream,
-                              dist.struct() if dist is not None else None)
+                              dist.struct() if dist is not None else None, forced_ranks)
 
     def __del__(self):
         h = getattr(self, "_h", 0)

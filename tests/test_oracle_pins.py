@@ -204,10 +204,11 @@ def test_aca_matern_semiseparable(kernel, maxr):
 
 
 # ---------------------------------------------------------------- O5-O10: closed forms
-def test_two_by_two():
+@pytest.mark.parametrize("twin", [False, True], ids=["oracle", "twin"])
+def test_two_by_two(twin):
     """One-level example eq-two-level-1: C = [[2,.5],[.5,2]], leaf 1."""
     d = math.sqrt(2 * math.log(2.0))      # SE, a = ell = 1: exp(-d^2/2) = 1/2
-    h = OracleHODLR(np.array([0.0, d]), SE, (1.0, 1.0), 1.0, 1, 1e-12).factor()
+    h = OracleHODLR(np.array([0.0, d]), SE, (1.0, 1.0), 1.0, 1, 1e-12, twin=twin).factor()
     assert h.kappa == 1
     assert h.logdet() == pytest.approx(GOLD["twobytwo_logdet"], rel=1e-15)
     x = h.solve(np.array([1.0, -1.0]))
@@ -234,12 +235,13 @@ def test_identity_times_two():
     assert h.logdet() == pytest.approx(GOLD["eye2_logdet_n100"], rel=1e-15)
 
 
-def test_rank_one_sylvester():
+@pytest.mark.parametrize("twin", [False, True], ids=["oracle", "twin"])
+def test_rank_one_sylvester(twin):
     """SE with ell = 1e20: K = a^2 11^T exactly.  Sylvester / Sherman-Morrison closed forms."""
     rng = np.random.default_rng(7)
     n, s2 = 1024, 1e-2
     x = rng.uniform(0, 1, n); y = rng.standard_normal(n)
-    h = OracleHODLR(x, SE, (1.0, 1e20), s2, 64, 1e-12).factor()
+    h = OracleHODLR(x, SE, (1.0, 1e20), s2, 64, 1e-12, twin=twin).factor()
     assert h.logdet() == pytest.approx(GOLD["rank1_logdet_n1024"], rel=1e-13)
     xs = (y - y.sum() / (s2 + n) * np.ones(n)) / s2
     np.testing.assert_allclose(h.solve(y), xs, rtol=1e-10, atol=1e-10 * np.abs(xs).max())
@@ -274,15 +276,18 @@ CASES += [("exp-ou", 2048, 0.0, 8.0, EXP, (1.1, 0.5), 1e-2, 64),            # NE
           ("rq-1.5", 1800, 0.0, 5.0, RQ, (0.9, 0.4, 1.5), 1e-2, 48)]
 
 
+@pytest.mark.parametrize("twin", [False, True], ids=["oracle", "twin"])
 @pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
-def test_hodlr_vs_dense(case):
-    """log det <= 1e-12 rel and solve <= 1e-9 rel against numpy dense (independent LAPACK path)."""
+def test_hodlr_vs_dense(case, twin):
+    """log det <= 1e-12 rel and solve <= 1e-9 rel against numpy dense (independent LAPACK path), for the oracle and
+    for its Q15 twin (leaf LU + coupling-system QR): a wrong reflection sign, a missed pivot swap or a dropped
+    Householder update in the twin fails here."""
     _, n, lo, hi, k, th, s2, p = case
     rng = np.random.default_rng(11)
     x = rng.uniform(lo, hi, n); y = rng.standard_normal(n)
     if case[0] == "exact-duplicates":     # ~2.5 points per distinct value, plus a block of zeros (DESIGN.md R2)
         x = np.round(x, 2); x[::97] = 0.0
-    h = OracleHODLR(x, k, th, s2, p, 1e-12).factor()
+    h = OracleHODLR(x, k, th, s2, p, 1e-12, twin=twin).factor()
     C = dense_C(x, k, th, s2)
     sd, ld = np.linalg.slogdet(C)
     assert sd > 0
@@ -298,13 +303,14 @@ def test_hodlr_vs_dense(case):
     assert h.gp_loglik(y) == pytest.approx(ll, rel=1e-10)
 
 
+@pytest.mark.parametrize("twin", [False, True], ids=["oracle", "twin"])
 @pytest.mark.parametrize("n,p,k", [(256, 16, SE), (300, 7, MATERN32), (512, 32, MATERN52)])
-def test_factorization_is_exact_inverse_of_hodlr_matrix(n, p, k):
+def test_factorization_is_exact_inverse_of_hodlr_matrix(n, p, k, twin):
     """Factor-product identity: solve and log det invert the assembled HODLR matrix H
     to rounding level (not to eps), so any dropped term / wrong sign / swapped P,Q fails here."""
     rng = np.random.default_rng(12)
     x = rng.uniform(0, 3, n)
-    h = OracleHODLR(x, k, (1.0, 0.4), 1e-2, p, 1e-6).factor()   # loose eps: H differs from C
+    h = OracleHODLR(x, k, (1.0, 0.4), 1e-2, p, 1e-6, twin=twin).factor()   # loose eps: H differs from C
     H = np.stack([h.apply(e) for e in np.eye(n)], axis=1)
     assert np.array_equal(H, H.T)
     C = dense_C(x, k, (1.0, 0.4), 1e-2)
@@ -432,3 +438,37 @@ def test_rq_alpha_half_is_imq():
         assert kernel_value(RQ, (1.2, 0.6, 0.5), d) == pytest.approx(kernel_value(IMQ, (1.2, 0.6), d), rel=1e-15)
     with pytest.raises(OracleError):
         OracleHODLR(np.linspace(0, 1, 10), RQ, (1.0, 0.5, -1.0), 1e-2, 4, 1e-10)
+
+
+# ---------------------------------------------------------------------------------------------------------------
+# Q15 oracle twin: leaf LU + coupling-system Householder QR; same compression
+def test_twin_shares_compression_and_differs_only_by_rounding():
+    """The twin runs the same sort / tree / ACA (identical ranks and tree), so its log det and solve differ from
+    the oracle's only by the rounding of two backward-stable dense factorizations.  A twin that silently fell back
+    to the oracle's own Cholesky / LU would give a bitwise-equal solve: the difference must be nonzero (at this
+    conditioning) and tiny."""
+    rng = np.random.default_rng(21)
+    n = 4096
+    x = rng.uniform(0.0, 10.0 * 4096 / 131072 * 32, n); y = rng.standard_normal(n)
+    o = OracleHODLR(x, MATERN52, (1.0, 2.0), 1e-4, 64, 1e-12).factor()
+    t = OracleHODLR(x, MATERN52, (1.0, 2.0), 1e-4, 64, 1e-12, twin=True).factor()
+    np.testing.assert_array_equal(o.ranks(), t.ranks())
+    xo, xt = o.solve(y), t.solve(y)
+    d = np.linalg.norm(xo - xt) / np.linalg.norm(xo)
+    assert 0.0 < d <= 1e-8
+    assert abs(o.logdet() - t.logdet()) <= 1e-12 * abs(o.logdet())
+    la_o, nb_o = o.logdet_parts(); la_t, nb_t = t.logdet_parts()
+    np.testing.assert_allclose(la_t, la_o, rtol=1e-12)       # leaf LU log|det| = Cholesky 2 sum log L_ii
+    np.testing.assert_allclose(nb_t, nb_o, rtol=1e-9, atol=1e-10)   # S_c by QR vs LU: the same determinant
+
+
+def test_twin_qr_sign_convention():
+    """det S_c = (-1)^reflections prod R_kk: with K = 0 every S_c = I (no reflection needed or taken), log det =
+    n log s2; with a rank-1 kernel each coupling system has det > 0 (Sylvester); a sign error in the reflection
+    count makes the twin report ENOTPD on these SPD matrices."""
+    rng = np.random.default_rng(22)
+    x = rng.uniform(0, 1, 512)
+    t = OracleHODLR(x, SE, (0.0, 0.1), 1e-2, 16, 1e-12, twin=True).factor()
+    assert t.logdet() == pytest.approx(512 * math.log(1e-2), rel=1e-14)
+    t = OracleHODLR(x, SE, (1.0, 1e20), 1e-2, 16, 1e-12, twin=True).factor()
+    assert t.logdet() == pytest.approx(511 * math.log(1e-2) + math.log(1e-2 + 512), rel=1e-13)

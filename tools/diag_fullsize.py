@@ -46,3 +46,20 @@ print(f"{name} n={n} eps={eps}: oracle {t1 - t0:.1f}s; logdet rel {abs(ld_g - ld
       f"solve rel {np.linalg.norm(x_g - x_o) / np.linalg.norm(x_o):.2e}; rank mismatches {len(mism)} of {len(r_o)}"
       f" (depths {sorted(set(int(np.log2(b + 1)) for b in mism))[:10]})", flush=True)
 print(f"  residual ||Cx-y||/||y||: gpu {dense_residual(x, x_g):.2e} oracle {dense_residual(x, x_o):.2e}", flush=True)
+for b in mism[:40]:
+    print(f"    block {b} depth {int(np.log2(b + 1))}: oracle {r_o[b]} gpu {r_g[b]}")
+g.close()
+# the same GPU factorization with the oracle's per-block ranks (hodlr_opts.forced_ranks): arithmetic only
+gf = hb.HODLR(torch.from_numpy(x).cuda(), cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, eps, rank_cap=64,
+              forced_ranks=r_o).factor()
+ld_f = gf.logdet(); x_f = gf.solve(torch.from_numpy(y).cuda()).cpu().numpy()
+_, _, r_f = gf.tree()
+print(f"  forced ranks: equal {np.array_equal(r_f, r_o)}; logdet rel {abs(ld_f - ld_o) / abs(ld_o):.2e}; solve rel "
+      f"{np.linalg.norm(x_f - x_o) / np.linalg.norm(x_o):.2e}; max elementwise {np.abs(x_f - x_o).max() / np.abs(x_o).max():.2e};"
+      f" residual {dense_residual(x, x_f):.2e}", flush=True)
+gf.close()
+t2 = time.time()
+tw = OracleHODLR(x, cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, eps, twin=True).factor()
+x_t = tw.solve(y)
+print(f"  twin ({time.time() - t2:.1f}s): floor solve rel {np.linalg.norm(x_t - x_o) / np.linalg.norm(x_o):.2e}; logdet rel "
+      f"{abs(tw.logdet() - ld_o) / abs(ld_o):.2e}", flush=True)
