@@ -76,7 +76,7 @@ def oracle_sample(cfg, n_sample):
 
 def cpu_baseline_obj(cfg, n_sample):
     t, ns = oracle_sample(cfg, n_sample)
-    return {"value": ns / t, "unit": UNIT, "cores": 1, "kind": "oracle",
+    return {"value": ns / t, "unit": UNIT, "cores": 1, "kind": "oracle", "cpu_model": cpu_model(),
             "sample": f"oracle (oracle/hodlr_oracle.c, gcc -O2, 1 thread) build+factor+logdet+solve on n={ns} "
                       f"points of the {cfg.name} workload (same density: interval scaled to "
                       f"[{cfg.lo:g},{cfg.lo + (cfg.hi - cfg.lo) * ns / cfg.n:g}]), {t:.2f} s"}
@@ -97,7 +97,7 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_desc(cfg), "sample_points": ns, "parallelism": "1 CPU thread"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "cpu_model": cpu_model(),
                              "sample": f"n={ns} points of {cfg.name} (same density), per step"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -201,47 +201,87 @@ class ClockSampler:
                 "source": "nvml" if self.samples else "nvidia-smi"}
 
 
-# ------------------------------------------------------------------ algorithmic counts (DESIGN.md section 6.4)
-def algorithmic(info, n, leaf):
-    """Per-launch algorithmic work of each kernel family of the formulation implemented:
-    (bound, amount, unit_of_amount, kernel name)."""
-    K = info["K"]
-    r = info["max_rank_by_depth"]
-    p = leaf
+# ------------------------------------------------------------------ algorithmic counts (SURVEY.md App. B, 8(d))
+C_K = 30          # flops per kernel-entry evaluation (exp + ~12 FP64 ops; SE is 4 ops + exp)
+
+
+def app_b(info, n, p):
+    """SURVEY.md Appendix B per-phase algorithmic (flops, compulsory bytes) of one factor + logdet + solve, with this
+    run's per-depth max ranks r_{d+1} (depth-d blocks) and K_d = sum_{i<=d} r_i.  nrhs = 0 in D and F (the solve is
+    counted separately in G, as the App. B roofline column does)."""
+    r = list(info["max_rank_by_depth"])          # r[d] = r_{d+1}: rank of the depth-d blocks, d = 0..kappa-1
+    kap = len(r)
+    K = sum(r)
+    Kd = [sum(r[:d]) for d in range(kap)]        # K_d = columns of depths 1..d
+    ph = {
+        "B_aca": (n * K * C_K + 2 * n * sum(x * x for x in r), 8 * n + 8 * n * K),
+        "C_leaf_chol": (n * p * p / 3 + n * p * C_K / 2, 4 * n * (p + 1)),
+        "D_leaf_panel": (2 * n * p * K, 4 * n * (p + 1) + 16 * n * K),
+        "E_coupling": (sum(2 * n * r[d] ** 2 + 2 ** d * (16 / 3) * r[d] ** 3 for d in range(kap)), 16 * n * K),
+        "F_sweep": (sum(4 * n * r[d] * Kd[d] + 2 ** d * 8 * r[d] ** 2 * Kd[d] for d in range(kap)), 16 * n * K),
+        "G_solve": (2 * n * p + 4 * n * K, 4 * n * (p + 1) + 16 * n * K + 16 * n * (kap + 1)),
+    }
+    return ph
+
+
+def formulation(info, n, p):
+    """Per kernel family, the algorithmic (flops, bytes) of ONE launch of the formulation implemented (DESIGN.md 6,
+    9): what the kernel must compute and move at minimum for its job, without padding or re-reads.  The paper's
+    panel sweep (App. B phase F) is done here as the projected Gram Pi_l = Z^T Z inside the leaf kernel (half of
+    App. B's F flops) plus the small coupling-tree updates, so per-kernel counts follow this formulation while the
+    combined roofline uses App. B as SURVEY 8(d) defines it."""
+    r = list(info["max_rank_by_depth"]); kap = len(r); K = sum(r)
+    Kd = [sum(r[:d]) for d in range(kap)]
     nl = n // p
-    kap = info["kappa"]
-    Kd = [0]
-    for x in r:
-        Kd.append(Kd[-1] + x)
-    ntile_bytes = (p // 8) * (p // 8 + 1) // 2 * 64 * 8           # X = L^{-1} tiles per leaf
-    fam = {}
-    # ACA (all levels): every step streams the previous factor columns of its block side once and writes one
-    # column: sum_k 8 (k + 1) bytes per element, plus the points -- 8 n K + 4 n sum r_d^2 in total
-    fam["aca"] = ("hbm", 8 * n * K + 4 * n * sum(x * x for x in r), "bytes", "k_aca_pass/k_aca_fused")
-    # leaf Cholesky + triangular inverse (tensor pipe): p^3/3 + p^3/3 flop per leaf
-    fam["leaf_chol"] = ("tensor", nl * (2 * p ** 3 / 3), "flop", "k_leaf_chol")
-    # Z = X E (p^2 K) and Pi = Z^T Z (p K^2) per leaf (tensor pipe)
-    fam["leaf_factor"] = ("tensor", nl * (p * p * K + p * K * K), "flop", "k_leaf_zsyrk")
-    # coupling tree: per node q^3 (S^-1) + 4 q^2 K_d (T, refinement) + q K_d^2 (Schur update of Pi), FP64 ALU
-    tree = 0
-    for d in range(kap):
-        q = 2 * r[d]
-        tree += 2 ** d * (q ** 3 + 4 * q * q * Kd[d] + q * Kd[d] ** 2)
-    fam["coupling_tree"] = ("alu", 2 * tree, "flop", "k_tree_factor")
-    # solve: X tiles and the panel E read twice (up and down), y gathered twice, x written
-    fam["solve"] = ("hbm", 2 * (nl * ntile_bytes + 8 * n * K) + 3 * 8 * n, "bytes", "k_solve")
-    return fam
+    tree = sum(2 ** d * ((2 * r[d]) ** 3 + 4 * (2 * r[d]) ** 2 * (Kd[d] + 1) + 2 * r[d] * (Kd[d] + 1) ** 2)
+               for d in range(kap))
+    return {
+        # ACA: n K kernel entries + 2 n sum r^2 residual updates; x read once, the factor columns written once
+        "aca": (n * K * C_K + 2 * n * sum(x * x for x in r), 8 * n + 8 * n * K),
+        # leaf Cholesky p^3/3 + triangular inverse p^3/3 + assembly of the lower triangle; X = L^{-1} tiles written
+        "leaf_chol": (n * (2 * p * p / 3 + p * C_K / 2), 4 * n * (p + 1)),
+        # Z = X [y | E] (p^2 (K+1) per leaf, triangular) and Pi = Z^T Z ((K+1)^2 p per leaf, symmetric half);
+        # reads X tiles and the panel, writes Pi
+        "leaf_factor": (n * p * (K + 1) + n * (K + 1) ** 2, 4 * n * (p + 1) + 8 * n * K + 4 * nl * (K + 1) * (K + 2)),
+        # coupling systems: q^3 (Gauss-Jordan) + 4 q^2 K_d (T and refinement) + q K_d^2 (Schur update of Pi) per node
+        # reads both children's packed Pi, writes the node's Pi, S, S^{-1}, B, T (hi, lo)
+        "coupling_tree": (2 * tree, 8 * sum(2 ** d * ((Kd[d] + 1 + r[d]) * (Kd[d] + 2 + r[d])
+                                                       + (Kd[d] + 1) * (Kd[d] + 2) // 2
+                                                       + 2 * (2 * r[d]) ** 2 + 3 * 2 * r[d] * (Kd[d] + 1))
+                                            for d in range(kap))),
+        # solve down passes: X^T X (y + E w) per leaf; reads X tiles, the panel, y, writes x
+        "solve": (2 * n * p + 2 * n * K, 4 * n * (p + 1) + 8 * n * K + 24 * n),
+    }
+
+
+# kernel family (hodlr_info kernel_ms) -> the App. B phases whose work it performs (DESIGN.md 9)
+FAMILY_PHASES = {"aca": ["B_aca"], "leaf_chol": ["C_leaf_chol"], "leaf_factor": ["D_leaf_panel", "F_sweep"],
+                 "coupling_tree": ["E_coupling"], "solve": ["G_solve"]}
+FAMILY_KERNELS = {"aca": "k_aca_*", "leaf_chol": "k_leaf_chol", "leaf_factor": "k_leaf_zsyrk_p",
+                  "coupling_tree": "k_tree_factor*", "solve": "k_solve"}
 
 
 def ncu_traffic():
-    """DRAM bytes per launch from the newest committed ncu summary (profiles/rNN_ncu_summary.json)."""
+    """Per-build DRAM bytes of each kernel family (dram__bytes_read.sum + dram__bytes_write.sum summed over the
+    family's launches of one step) from the newest profiles/rNN_traffic.json (tools/ncu_traffic.py)."""
     import glob
-    fs = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.json")))
+    fs = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
     if not fs:
         return {}, None
     with open(fs[-1]) as f:
         d = json.load(f)
-    return {k: v.get("dram_bytes") for k, v in d.get("kernels", {}).items()}, os.path.basename(fs[-1])
+    return {k: v.get("dram_bytes") for k, v in d.get("families", {}).items()}, os.path.basename(fs[-1])
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def load_peaks():
@@ -302,11 +342,12 @@ def run_ours(args):
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)     # > 126 MB L2
     stream = torch.cuda.current_stream()
 
+    # one step = hodlr_build (sort, tree, ACA: "Assembly") + hodlr_factor_solve (leaf factors, coupling tree with y
+    # fused in, log det, the solve's down passes: "Factor", "Det.", "Solve") + hodlr_logdet -- the public C-ABI calls
     def step(xin, yin):
         h = hb.HODLR(xin, cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, cfg.eps, dist=dd)
-        h.factor()
+        sol, _ = h.factor_solve(yin)
         ld = h.logdet()
-        sol = h.solve(yin)
         info = h.info()
         h.close()
         return ld, sol, info
@@ -346,8 +387,8 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_max = float(tt.item())
     # ---------------- end-to-end through the C-ABI with host buffers: x copied first (the build needs it), y on a
-    # side stream concurrently with the build/factor (only the solve needs it), solution read back; all inside
-    # the timed region
+    # side stream concurrently with the build (only the factor needs it), solution read back; all inside the timed
+    # region
     ys = torch.cuda.Stream()
     ev_y = torch.cuda.Event()
 
@@ -358,10 +399,9 @@ def run_ours(args):
             yd.copy_(yh, non_blocking=True)
             ev_y.record(ys)
         h = hb.HODLR(xd, cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, cfg.eps, dist=dd)
-        h.factor()
-        ld_ = h.logdet()
         stream.wait_event(ev_y)
-        s_ = h.solve(yd)
+        s_, _ = h.factor_solve(yd)
+        ld_ = h.logdet()
         sol_h.copy_(s_, non_blocking=True)
         h.close()
         return ld_, s_
@@ -379,6 +419,8 @@ def run_ours(args):
         torch.cuda.synchronize()
         e2e_ms.append(a.elapsed_time(b))
     barrier()
+    print(f"[bench] device ms per step {[round(v, 3) for v in ms]}; e2e ms {[round(v, 3) for v in e2e_ms]}",
+          file=sys.stderr)
     t_e2e = sum(e2e_ms) / len(e2e_ms) / 1e3
     if ws > 1:
         tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
@@ -393,38 +435,45 @@ def run_ours(args):
     info = infos[-1]
     clocks = clk.summary()
     peaks = load_peaks()
-    # ---------------- rooflines: algorithmic work / live event time per kernel family; dominant = longest
-    alg = algorithmic(info, n, cfg.leaf)
+    # ---------------- rooflines: per phase max(F / F_peak, B / B_peak); per kernel family
+    # the algorithmic work of the phases it performs / its live event time; dominant = longest family
+    ph = app_b(info, n, cfg.leaf)
     fp64_peak, fp64_how = fp64_peak_tflops(peaks, clocks.get("sm_mhz"))
-    dfma_peak, dfma_how = dfma_peak_tflops(clocks.get("sm_mhz"))
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    t_roof = {k: max(f / (fp64_peak * 1e12), b / (hbm_peak * 1e9)) for k, (f, b) in ph.items()}
+    t_roof_s = sum(t_roof.values())
     traffic, traffic_src = ncu_traffic()
+    form = formulation(info, n, cfg.leaf)
     rows = []
-    for fam, (bound, amount, unit, kname) in alg.items():
-        ms = fam_ms.get(fam, 0.0)
-        calls = info["kernel_calls"].get(fam) or 1
-        if ms <= 0.0:
+    for fam, phases in FAMILY_PHASES.items():
+        ms_f = fam_ms.get(fam, 0.0)
+        if ms_f <= 0.0:
             continue
-        t_launch = ms / calls / 1e3
-        if bound == "hbm":
-            ach, peak, u = amount / t_launch / 1e9, hbm_peak, "GB/s"
-        elif bound == "alu":       # plain FP64 FMA pipe (DFMA), not the DMMA tensor path
-            ach, peak, u = amount / t_launch / 1e12, dfma_peak, "TFLOP/s"
+        calls = info["kernel_calls"].get(fam) or 1
+        t_launch = ms_f / calls / 1e3
+        fl, by = form[fam]
+        tr = max(fl / (fp64_peak * 1e12), by / (hbm_peak * 1e9))
+        hbm_side = by / (hbm_peak * 1e9) >= fl / (fp64_peak * 1e12)
+        if hbm_side:
+            ach, peak, u, bound = by / t_launch / 1e9, hbm_peak, "GB/s", "hbm"
         else:
-            ach, peak, u = amount / t_launch / 1e12, fp64_peak, "TFLOP/s"
-        kk = kname.split("/")[0]
-        tr = traffic.get(kk)
-        if tr is not None and fam == "aca":
-            tr = None          # the capture is one pass of one step, not the whole ACA family
-        rows.append({"kernel": kname, "family": fam, "bound": bound, "achieved": ach, "peak": peak, "unit": u,
-                     "frac": ach / peak, "traffic": tr, "ms": ms / calls,
-                     ("algorithmic_bytes_per_launch" if bound == "hbm" else "algorithmic_flops_per_launch"): amount})
-    main = [r_ for r_ in rows if r_["family"] != "leaf_chol"]     # leaf_chol runs on a side stream under the ACA
-    dom = max(main, key=lambda r_: r_["ms"])
-    roof = dict(dom)
-    roof["peak_source"] = ("MEASURED_PEAKS.json hbm_gbs" if dom["bound"] == "hbm"
-                           else (dfma_how if dom["bound"] == "alu" else fp64_how))
+            ach, peak, u, bound = fl / t_launch / 1e12, fp64_peak, "TFLOP/s", "fp64"
+        tb = traffic.get(fam)
+        rows.append({"kernel": FAMILY_KERNELS[fam], "family": fam, "app_b_phases": phases, "bound": bound,
+                     "achieved": ach, "peak": peak, "unit": u, "frac": ach / peak,
+                     "traffic": tb, "traffic_over_algorithmic": (tb / by) if tb else None,
+                     "ms": 1e3 * t_launch, "t_roof_ms": 1e3 * tr, "timing": "live CUDA events (hodlr_info)",
+                     "algorithmic_bytes_per_launch": by, "algorithmic_flops_per_launch": fl})
+    dom = max(rows, key=lambda r_: r_["ms"])
+    roof = {k: dom[k] for k in ("kernel", "family", "bound", "achieved", "peak", "unit", "frac", "traffic")}
+    roof["traffic_over_algorithmic"] = dom["traffic_over_algorithmic"]
+    roof["peak_source"] = ("MEASURED_PEAKS.json hbm_gbs (burst copy)" if dom["bound"] == "hbm" else fp64_how)
     roof["traffic_source"] = traffic_src
+    roof["counts"] = ("per kernel: the implemented formulation's algorithmic work (bench.formulation); combined: "
+                      "SURVEY.md App. B; this run's ranks, c_k = %d flop per kernel entry" % C_K)
+    roof["combined"] = {"t_roof_ms": 1e3 * t_roof_s, "t_ms": 1e3 * t_max, "frac": t_roof_s / t_max,
+                        "t_roof_ms_by_phase": {k: 1e3 * v for k, v in t_roof.items()},
+                        "fp64_peak_tflops": fp64_peak, "hbm_peak_gbs": hbm_peak}
     roof["all_kernels"] = rows
     cpu = None
     if not args.no_cpu_baseline and ws == 1:
@@ -437,9 +486,10 @@ def run_ours(args):
                        "parallelism": (f"subtree sharding over {ws} GPUs (top log2(N) levels redundant, NCCL "
                                        f"allgather of the depth-log2(N) projections)") if ws > 1 else "1 GPU",
                        "l2": "flushed between timed steps (512 MB device write, untimed)",
+                       "step": "hodlr_build + hodlr_factor_solve (y fused into the factorization) + hodlr_logdet",
                        "kappa": info["kappa"], "K": info["K"], "ranks_by_depth": info["max_rank_by_depth"],
-                       "phase_ms": {"assembly(build)": 1e3 * info["t_build"], "factor": 1e3 * info["t_factor"],
-                                    "det": 1e3 * info["t_logdet"], "solve": 1e3 * info["t_solve"]},
+                       "phase_ms": {"assembly(build)": 1e3 * info["t_build"],
+                                    "factor+det+solve(factor_solve)": 1e3 * info["t_factor"]},
                        "kernel_family_ms": fam_ms, "seconds_per_step": t_max,
                        "gpu_launches_per_step": launches / args.steps},
             "roofline": roof, "cpu_baseline": cpu,

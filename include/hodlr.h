@@ -20,8 +20,8 @@
  * Ordering: all device work is enqueued on `cuda_stream` (NULL = legacy
  * default stream); every call synchronises that stream before it returns its
  * status, so statuses are final.
- * State machine: build -> factor -> {logdet, solve, gp_loglik, gp_predict}*; hodlr_apply is legal from build
- * on.  Any other order returns HODLR_ESTATE.  After factor the handle is read-only; one
+ * State machine: build -> (factor | factor_solve) -> {logdet, solve, gp_loglik, gp_predict}*; hodlr_apply is legal
+ * from build on.  Any other order returns HODLR_ESTATE.  After factor the handle is read-only; one
  * handle must not be used from two threads at once.
  * Errors: every call returns a hodlr_status; hodlr_last_error() gives a
  * thread-local message for the last failing call.
@@ -124,6 +124,16 @@ hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const 
  * and their LU factors; accumulates log det C. */
 hodlr_status hodlr_factor(hodlr_t h);
 
+/* Factor with a right-hand side (fused factor + solve): hodlr_factor, with y carried through the
+ * factorization as an extra panel column -- leaf Z = L^{-1} [y | E] and Pi = Z^T Z give the solve's leaf
+ * projections, the coupling tree's T_c = S_c^{-1} B_c and Pi_c give its tree up pass (eq-fac, PAPER.md:1091-1100;
+ * equation_Low_Rank_Update) -- then only the solve's down passes run.
+ * y: device, n doubles (original order).  x: device, n doubles, receives C^{-1} y (original order), or NULL (no
+ * down pass).  quad_host: host double receiving y^T C^{-1} y (the root's Pi; eq. 1), or NULL.
+ * Leaves the handle factored exactly like hodlr_factor (log det, solve / gp_loglik of other right-hand sides).
+ * Errors: as hodlr_factor; HODLR_EINVAL if y has NaN/Inf (the handle is still factored). */
+hodlr_status hodlr_factor_solve(hodlr_t h, const double *y, double *x, double *quad_host);
+
 /* "Det." (sec. 4): log det C = sum_leaves 2 sum log L_ii + sum_c log det S_c.
  * logdet_host: host double.  -INFINITY with HODLR_ENOTPD if the factorization failed. */
 hodlr_status hodlr_logdet(hodlr_t h, double *logdet_host);
@@ -191,6 +201,10 @@ hodlr_status hodlr_dist_plan(int64_t n, int32_t leaf, int32_t rank, int32_t nran
  * kept by the library (exact-size reuse by later handles on the same device, at most 16 GB per process) rather
  * than returned to the CUDA pool, so repeated builds of one shape allocate nothing. */
 void hodlr_free(hodlr_t h);
+
+/* Return every device block the library keeps for reuse (see hodlr_free) to the CUDA pool.  Safe at any time (cached
+ * blocks have no pending work); live handles are unaffected. */
+void hodlr_cache_trim(void);
 
 /* Thread-local message of the last failing call (never NULL). */
 const char *hodlr_last_error(void);

@@ -456,6 +456,7 @@ fail:
 hodlr_status hodlr_factor(hodlr_t h) {
   if (!h) return hodlr_set_error(HODLR_EINVAL, "factor: NULL handle");
   if (h->state != 1) return hodlr_set_error(HODLR_ESTATE, "factor: handle is not in the built state");
+  h->aug = 0; h->y_aug = nullptr;
   h->launches = 0;
   cudaEventRecord(h->ev0, h->st);
   hodlr_trace("factor: enter");
@@ -474,6 +475,44 @@ hodlr_status hodlr_factor(hodlr_t h) {
   e = cudaMemcpy(&h->logdet, h->d_logdet, sizeof(double), cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return hodlr_cuda_check(e, "factor logdet");
   h->state = 2;
+  return HODLR_OK;
+}
+
+hodlr_status hodlr_factor_solve(hodlr_t h, const double *y, double *x, double *quad_host) {
+  if (!h || !y) return hodlr_set_error(HODLR_EINVAL, "factor_solve: NULL argument");
+  if (h->state != 1) return hodlr_set_error(HODLR_ESTATE, "factor_solve: handle is not in the built state");
+  h->launches = 0;
+  cudaEventRecord(h->ev0, h->st);
+  h->aug = 1; h->y_aug = y;                  // y is column 0 of every leaf panel (leaf_mma.cu, factor.cu)
+  hodlr_status st = HODLR_OK;
+  cudaError_t ce = cudaMemsetAsync(h->dflags + 3, 0, sizeof(int), h->st);
+  if (ce != cudaSuccess) st = hodlr_cuda_check(ce, "factor_solve flags");
+  if (st == HODLR_OK) st = hodlr_factor_impl(h);
+  if (st == HODLR_OK && x) st = hodlr_solve_impl(h, y, x, false, true);   // down passes only
+  int f[4] = {0, 0, 0, 0};
+  double quad = 0.0;
+  if (st == HODLR_OK) {
+    ce = cudaMemcpyAsync(f, h->dflags, sizeof(f), cudaMemcpyDeviceToHost, h->st);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(&h->logdet, h->d_logdet, sizeof(double), cudaMemcpyDeviceToHost, h->st);
+    // Pi at the root with the fused right-hand side is the 1 x 1 matrix y^T C^{-1} y
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(&quad, h->Pipool + h->dt.piOff[0], sizeof(double), cudaMemcpyDeviceToHost, h->st);
+    if (ce != cudaSuccess) st = hodlr_cuda_check(ce, "factor_solve results");
+  }
+  st = finish(h, st, &h->t_factor);
+  h->y_aug = nullptr;
+  if (st != HODLR_OK) { h->state = -1; h->logdet = -INFINITY; return st; }
+  if (f[1]) {
+    h->state = -1; h->logdet = -INFINITY;
+    if (quad_host) *quad_host = NAN;
+    return hodlr_set_error(HODLR_ENOTPD, "factor_solve: node %d is not positive definite (%d failures)", f[2], f[1]);
+  }
+  h->state = 2;                              // factored: logdet / solve / gp_loglik for other right-hand sides work
+  if (f[3]) {
+    int z = 0;
+    cudaMemcpy(h->dflags + 3, &z, sizeof(int), cudaMemcpyHostToDevice);
+    return hodlr_set_error(HODLR_EINVAL, "factor_solve: y contains NaN or Inf (the factorization itself is valid)");
+  }
+  if (quad_host) *quad_host = quad;
   return HODLR_OK;
 }
 

@@ -53,6 +53,8 @@ struct LeafCtx {
   int mmax;                 // max leaf size
   long long leaf0, nown;    // this rank's leaves [leaf0, leaf0 + nown)
   long long lsz;            // packed triangle capacity mmax(mmax+1)/2 + 1
+  int aug;                  // fused right-hand side: column 0 of the panel is y (gathered through perm)
+  const double *y; const long long *perm;
 };
 
 __global__ void __launch_bounds__(LT) k_leaf_factor(LeafCtx c) {
@@ -118,21 +120,25 @@ __global__ void __launch_bounds__(LT) k_leaf_factor(LeafCtx c) {
       }
     }
     if (K > 0) {
-      if (t == 0) {   // column map: leaf column order = depth 1 .. kappa; zero beyond each block's rank
+      if (t == 0) {   // column map: [rhs,] depth 1 .. kappa; zero beyond each block's rank
         long long a = id;
         for (int e = c.kappa; e >= 1; e--) {
           long long b = (a - 1) / 2;
           int rb = c.rank[b];
           for (int q = 0; q < c.dt->rdep[e]; q++)
-            colsrc[c.dt->Kdim[e - 1] + q] = q < rb ? c.dt->colbase[e] + q : -1;
+            colsrc[c.aug + c.dt->Kdim[e - 1] + q] = q < rb ? c.dt->colbase[e] + q : -1;
           a = b;
         }
+        if (c.aug) colsrc[0] = -2;
       }
       __syncthreads();
       for (long long p = t; p < (long long)K * m; p += LT) {
         long long col = p / m, i = p - col * m;
         long long src = colsrc[col];
-        Z[i * ldz + col] = src >= 0 ? c.Xh[src * c.ldx + lo + i] : 0.0;
+        double v = 0.0;
+        if (src >= 0) v = c.Xh[src * c.ldx + lo + i];
+        else if (src == -2) { v = c.y[c.perm[lo + i]]; if (!isfinite(v)) atomicOr(&c.flags[3], 1); }
+        Z[i * ldz + col] = v;
       }
       __syncthreads();
       for (int col = t; col < K; col += LT) {     // Z <- L^{-1} Z
@@ -268,7 +274,8 @@ hodlr_status hodlr_leaf_alloc(hodlr_s *h) {
 static TreeCtx tree_ctx(hodlr_s *h, int d, long long i0) {
   const DepthTab &dt = h->dt;
   TreeCtx tc;
-  tc.d = d; tc.i0 = i0; tc.r = dt.rdep[d + 1]; tc.q = 2 * tc.r; tc.Kd = dt.Kdim[d]; tc.K1 = dt.Kdim[d + 1];
+  // factor-side widths: Kf = Kdim (+ 1 with a fused right-hand side, which is then index 0 of every Pi)
+  tc.d = d; tc.i0 = i0; tc.r = dt.rdep[d + 1]; tc.q = 2 * tc.r; tc.Kd = dt.Kf[d]; tc.K1 = dt.Kf[d + 1];
   tc.ldk = (tc.Kd + 3) & ~3; tc.dd = 1;   // compensated at every depth
   tc.Pi1 = h->Pipool + dt.piOff[d + 1]; tc.Pic = h->Pipool + dt.piOff[d];
   tc.Sst = h->Spool + dt.nodeS[d]; tc.BT = h->BTpool + dt.nodeBT[d];
@@ -279,7 +286,8 @@ static TreeCtx tree_ctx(hodlr_s *h, int d, long long i0) {
 hodlr_status hodlr_factor_impl(hodlr_s *h) {
   const int kappa = h->kappa;
   DepthTab &dt = h->dt;
-  const int K = dt.Kdim[kappa];
+  for (int e = 0; e <= kappa; e++) dt.Kf[e] = dt.Kdim[e] + h->aug;
+  const int K = dt.Kf[kappa];              // panel columns per leaf (+ the fused right-hand side)
   const long long nl = h->nleaves;
   // ---- storage ----
   const int mmax = h->leaf_max;
@@ -288,12 +296,12 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
   long long piTot = 0, sTot = 0, btTot = 0;
   for (int e = kappa; e >= 0; e--) {
     dt.piOff[e] = piTot;
-    piTot += (1LL << e) * ((long long)dt.Kdim[e] * (dt.Kdim[e] + 1) / 2);
+    piTot += (1LL << e) * ((long long)dt.Kf[e] * (dt.Kf[e] + 1) / 2);
   }
   for (int d = 0; d < kappa; d++) {
     long long q = 2LL * dt.rdep[d + 1];
     dt.nodeS[d] = sTot; sTot += (1LL << d) * (2 * q * q + q);
-    dt.nodeBT[d] = btTot; btTot += (1LL << d) * 3 * q * dt.Kdim[d];
+    dt.nodeBT[d] = btTot; btTot += (1LL << d) * 3 * q * dt.Kf[d];
   }
   h->Pipool = (double *)hodlr_dalloc(h, sizeof(double) * (piTot > 0 ? piTot : 1));
   h->Spool = (double *)hodlr_dalloc(h, sizeof(double) * (sTot > 0 ? sTot : 1));
@@ -320,6 +328,7 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
     lc.ldz = K | 1; lc.T = h->ltiles; lc.xs = h->xs; lc.lo = h->lo; lc.hi = h->hi; lc.Xh = h->Xh; lc.ldx = h->ldx; lc.rank = h->rank;
     lc.dt = h->d_dt; lc.Lf = h->Lf; lc.lstride = h->lstride; lc.Pi = h->Pipool + dt.piOff[kappa];
     lc.leaf_ld = h->leaf_ld; lc.flags = h->dflags;
+    lc.aug = h->aug; lc.y = h->y_aug; lc.perm = h->perm;
     lc.mmax = mmax;
     hodlr_own_nodes(h, kappa, &lc.leaf0, &lc.nown);
     lc.lsz = (long long)mmax * (mmax + 1) / 2 + 1;
@@ -344,7 +353,7 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
   ph_begin(h, PH_TREE);
   size_t tree_smem_max = 0;
   for (int d = 0; d < kappa; d++) {
-    const int q = 2 * dt.rdep[d + 1], ldk = (dt.Kdim[d] + 3) & ~3;
+    const int q = 2 * dt.rdep[d + 1], ldk = (dt.Kf[d] + 3) & ~3;
     tree_smem_max = std::max(tree_smem_max, sizeof(double) * (size_t)tree_smem_doubles(q, ldk));
   }
   if (tree_smem_max > (size_t)maxsm - 2048)
@@ -357,7 +366,7 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
   }
   for (int d = kappa - 1; d >= 0; d--) {
     if (d + 1 == h->tsplit && h->nranks > 1) {     // every rank gets the Pi of all depth-t subtree roots
-      const long long Kt = dt.Kdim[d + 1], sz = Kt * (Kt + 1) / 2;
+      const long long Kt = dt.Kf[d + 1], sz = Kt * (Kt + 1) / 2;
       double *base = h->Pipool + dt.piOff[d + 1];
       hodlr_status xs = hodlr_allgather(h, base + h->grank * sz, base, sizeof(double) * sz);
       if (xs != HODLR_OK) return xs;

@@ -89,6 +89,8 @@ struct DepthTab {
   int capd[HODLR_MAXDEPTH + 2];            // columns allocated in slot e
   int rdep[HODLR_MAXDEPTH + 2];            // max rank of depth-(e-1) blocks (after build)
   int Kdim[HODLR_MAXDEPTH + 2];            // Kdim[e] = sum_{e'=1..e} rdep[e']
+  int Kf[HODLR_MAXDEPTH + 2];              // factor-side widths Kdim[e] + aug: with a right-hand side fused into the
+                                           // factorization (hodlr_factor_solve) it is column 0 of every panel / Pi
   long long nodeS[HODLR_MAXDEPTH + 2];     // per depth d: offset of S LU storage (doubles)
   long long nodeBT[HODLR_MAXDEPTH + 2];    // per depth d: offset of B/T storage (doubles)
   long long nodeV[HODLR_MAXDEPTH + 2];     // per depth d: offset of per-node vectors (g, w) (doubles)
@@ -157,6 +159,8 @@ struct hodlr_s {
   long long *d_rowlo;        // per rank: first sorted row of its subtree (device, nranks entries)
   long long rows_max;        // max subtree rows over the ranks (allgather slice size of the solution)
   int state;                 // 1 built, 2 factored, -1 factor failed
+  int aug;                   // right-hand sides fused into the factorization (0 or 1)
+  const double *y_aug;       // that right-hand side (device, original order) during hodlr_factor_solve
   int launches;              // kernels launched by the current call
   int aca_steps;
   int x_nonfinite;           // set by the sort: x contains NaN/Inf
@@ -230,7 +234,7 @@ hodlr_status hodlr_apply_impl(hodlr_s *h, const double *x, double *y);
 hodlr_status hodlr_predict_impl(hodlr_s *h, const double *y, const double *xt, long long m, double *mean, double *var);
 hodlr_status hodlr_leaf_chol_mma(hodlr_s *h, cudaStream_t stream, bool *launched);
 hodlr_status hodlr_leaf_alloc(hodlr_s *h);
-hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_only);
+hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_only, bool fused = false);
 
 static inline int hodlr_depth_of(long long id) { int d = 0; while (id >= ((2LL << d) - 1)) d++; return d; }
 

@@ -68,7 +68,17 @@ struct LeafMmaCtx {
   double *leaf_ld;
   int *flags;
   long long leaf0;          // first leaf of this launch (this rank's subtree)
+  int aug;                  // fused right-hand side (hodlr_factor_solve): panel column 0 is y[perm[rows]]
+  const double *y; const long long *perm;
 };
+
+// Panel entry of the fused right-hand side: y of sorted row lo + row (0 beyond the leaf); flags non-finite y.
+__device__ __forceinline__ double rhs_val(const LeafMmaCtx &c, long long lo, int row, int m) {
+  if (row >= m) return 0.0;
+  const double v = c.y[c.perm[lo + row]];
+  if (!isfinite(v)) atomicOr(&c.flags[3], 1);
+  return v;
+}
 
 // One warp, every lane computes the same 8x8 POTRF redundantly (no shuffles on the critical path),
 // then writes its fragment positions of L and of L^{-1}.
@@ -124,8 +134,11 @@ __device__ void potrf8(double *tile, double *linv, double *diag8, int *bad) {
 
 // Column map of leaf `id`: local column q (depth e block, Kdim[e-1] <= q < Kdim[e]) -> global Xh column, or -1
 // beyond the rank of that ancestor's block.  One thread per column (no serial walk).
+// With a fused right-hand side, column 0 is that vector (-2) and the ancestor columns follow.
 __device__ __forceinline__ long long leaf_colsrc(const LeafMmaCtx &c, long long id, int q) {
   if (q >= c.K) return -1;
+  if (q < c.aug) return -2;
+  q -= c.aug;
   int e = 1;
   while (c.dt->Kdim[e] <= q) e++;
   const int qq = q - c.dt->Kdim[e - 1];
@@ -419,6 +432,8 @@ __global__ void __launch_bounds__(ZTH, 1) k_leaf_zsyrk(LeafMmaCtx c) {
       if (src >= 0 && row + 1 < m) {
         unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(sa), "l"(c.Xh + src * c.ldx + lo + row));
+      } else if (src == -2) {
+        dst[0] = rhs_val(c, lo, row, m); dst[1] = rhs_val(c, lo, row + 1, m);
       } else {
         dst[0] = (src >= 0 && row < m) ? c.Xh[src * c.ldx + lo + row] : 0.0;
         dst[1] = 0.0;
@@ -429,7 +444,7 @@ __global__ void __launch_bounds__(ZTH, 1) k_leaf_zsyrk(LeafMmaCtx c) {
       const int col = p / P, row = p - col * P;
       const long long src = colsrc[col];
       double *dst = sZ + col * LDR + row;
-      *dst = (src >= 0 && row < m) ? c.Xh[src * c.ldx + lo + row] : 0.0;
+      *dst = src == -2 ? rhs_val(c, lo, row, m) : ((src >= 0 && row < m) ? c.Xh[src * c.ldx + lo + row] : 0.0);
     }
   }
   asm volatile("cp.async.commit_group;\n" ::);
@@ -526,6 +541,8 @@ __global__ void __launch_bounds__(ZTH, 1) k_leaf_zsyrk_p(LeafMmaCtx c, long long
         if (src >= 0 && row + 1 < m) {
           unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(sa), "l"(c.Xh + src * c.ldx + lo + row));
+        } else if (src == -2) {
+          dst[0] = rhs_val(c, lo, row, m); dst[1] = rhs_val(c, lo, row + 1, m);
         } else {
           dst[0] = (src >= 0 && row < m) ? c.Xh[src * c.ldx + lo + row] : 0.0;
           dst[1] = 0.0;
@@ -536,7 +553,7 @@ __global__ void __launch_bounds__(ZTH, 1) k_leaf_zsyrk_p(LeafMmaCtx c, long long
         const int col = p / P, row = p - col * P;
         const long long src = colsrc[col];
         double *dst = sZ + col * LDR + row;
-        *dst = (src >= 0 && row < m) ? c.Xh[src * c.ldx + lo + row] : 0.0;
+        *dst = src == -2 ? rhs_val(c, lo, row, m) : ((src >= 0 && row < m) ? c.Xh[src * c.ldx + lo + row] : 0.0);
       }
     }
   };
@@ -628,6 +645,7 @@ static LeafMmaCtx leaf_ctx(hodlr_s *h, int K, double *Pi_leaf) {
   c.Kz = (K + 15) / 16 * 16;
   c.xs = h->xs; c.lo = h->lo; c.hi = h->hi; c.Xh = h->Xh; c.ldx = h->ldx; c.rank = h->rank; c.dt = h->d_dt;
   c.Lf = h->Lf; c.lstride = h->lstride; c.Pi = Pi_leaf; c.leaf_ld = h->leaf_ld; c.flags = h->dflags;
+  c.aug = h->aug; c.y = h->y_aug; c.perm = h->perm;
   long long cnt;
   hodlr_own_nodes(h, h->kappa, &c.leaf0, &cnt);
   return c;

@@ -49,6 +49,9 @@ struct SolveCtx {
   long long tree_scratch;   // doubles of per-warp scratch for the tree-up nodes
   int tree_warps;           // warps per CTA that take tree-up nodes (scratch must fit)
   unsigned long long *stamps;   // HODLR_TRACE: %globaltimer after each phase (block 0), or NULL
+  int aug;                  // the factorization carries a fused right-hand side: B_c / T_c rows have Kf[d] = Kdim[d] + 1
+                            // entries with the ancestor columns at offset 1 (column 0 belongs to that right-hand side)
+  int fused;                // this solve IS that right-hand side: t_c = T_c[:, 0] from the factorization (no up pass)
   int bulk;                 // leaf staging by bulk copies (all column segments 16-byte aligned)
   int stage_e;              // stage the panel E_l in shared memory (else read it from global memory)
 };
@@ -527,10 +530,11 @@ __device__ void dd_solve_warp(const double *S0, const double *Si, int q, const d
 __device__ void tree_up_node(const SolveCtx &c, int d, long long i, double *scr, int lane) {
   const long long node = (1LL << d) - 1 + i;
   const int r = c.dt->rdep[d + 1], q = 2 * r, Kd = c.dt->Kdim[d], K1 = c.dt->Kdim[d + 1];
+  const int ldb = c.dt->Kf[d];               // B_c row stride (ancestor columns at offset c.aug)
   const double *g1 = c.V + c.dt->nodeV[d + 1] + (2 * i) * (long long)K1;
   const double *g2 = g1 + K1;
   const double *Sg = c.Spool + c.dt->nodeS[d] + i * (long long)(2 * q * q + q);
-  const double *B = c.BTpool + c.dt->nodeBT[d] + i * 3LL * q * Kd;
+  const double *B = c.BTpool + c.dt->nodeBT[d] + i * 3LL * q * ldb + c.aug;
   double *S0 = scr;
   double *Si = S0 + q * q, *rhs = Si + q * q + q, *th = rhs + q, *tl = th + q, *tmp = tl + q;
   {
@@ -570,7 +574,7 @@ __device__ void tree_up_node(const SolveCtx &c, int d, long long i, double *scr,
 #pragma unroll
       for (int x = 0; x < 4; x++) {
         const int a = a0 + 32 * x, ac = a < Kd ? a : 0;
-        b1[x] = B[(long long)(r + u) * Kd + ac]; b2[x] = B[(long long)u * Kd + ac];
+        b1[x] = B[(long long)(r + u) * ldb + ac]; b2[x] = B[(long long)u * ldb + ac];
       }
 #pragma unroll
       for (int x = 0; x < 4; x++) { acc_fma_dd(A[x], -b1[x], th[u], tl[u]); acc_fma_dd(A[x], -b2[x], th[r + u], tl[r + u]); }
@@ -587,10 +591,11 @@ __device__ void tree_up_node_cta(const SolveCtx &c, int d, long long i, double *
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const long long node = (1LL << d) - 1 + i;
   const int r = c.dt->rdep[d + 1], q = 2 * r, Kd = c.dt->Kdim[d], K1 = c.dt->Kdim[d + 1];
+  const int ldb = c.dt->Kf[d];
   const double *g1 = c.V + c.dt->nodeV[d + 1] + (2 * i) * (long long)K1;
   const double *g2 = g1 + K1;
   const double *Sg = c.Spool + c.dt->nodeS[d] + i * (long long)(2 * q * q + q);
-  const double *B = c.BTpool + c.dt->nodeBT[d] + i * 3LL * q * Kd;
+  const double *B = c.BTpool + c.dt->nodeBT[d] + i * 3LL * q * ldb + c.aug;
   double *S0 = scr;
   double *Si = S0 + q * q, *rhs = Si + q * q + q, *th = rhs + q, *tl = th + q, *tmp = tl + q;
   for (int p = t; p < 2 * q * q + q; p += LT) S0[p] = Sg[p];
@@ -614,19 +619,28 @@ __device__ void tree_up_node_cta(const SolveCtx &c, int d, long long i, double *
   for (int a = t; a < Kd; a += LT) {
     Acc2 A = acc2(g1[a]);
     acc_add(A, g2[a]);
-    for (int u = 0; u < r; u++) acc_fma_dd(A, -B[(long long)(r + u) * Kd + a], th[u], tl[u]);
-    for (int u = 0; u < r; u++) acc_fma_dd(A, -B[(long long)u * Kd + a], th[r + u], tl[r + u]);
+    for (int u = 0; u < r; u++) acc_fma_dd(A, -B[(long long)(r + u) * ldb + a], th[u], tl[u]);
+    for (int u = 0; u < r; u++) acc_fma_dd(A, -B[(long long)u * ldb + a], th[r + u], tl[r + u]);
     gc[a] = acc_val(A);
   }
   __syncthreads();
 }
 
 // f = t_c + T_c w_c with `parts` lanes per row u (interleaved a), partials combined by xor shuffles.
+// t_c (hi, lo) of row u: from the up pass, or -- for the right-hand side fused into the factorization -- column 0
+// of T_c = S_c^{-1} B_c (the factorization's compensated pair)
+__device__ __forceinline__ void t_of(const SolveCtx &c, const double *tg, const double *Th, const double *Tl, int ldb,
+                                     int q, int u, double &hi, double &lo) {
+  if (c.fused) { hi = Th[(long long)u * ldb - c.aug]; lo = Tl[(long long)u * ldb - c.aug]; }
+  else { hi = tg[u]; lo = tg[q + u]; }
+}
+
 __device__ void tree_down_node(const SolveCtx &c, int d, long long i, int lane) {
   const int r = c.dt->rdep[d + 1], q = 2 * r, Kd = c.dt->Kdim[d], K1 = c.dt->Kdim[d + 1];
+  const int ldb = c.dt->Kf[d];
   const double *wc = c.V + c.dt->nodeV[d] + i * (long long)Kd;
-  const long long qK = (long long)q * Kd;
-  const double *Th = c.BTpool + c.dt->nodeBT[d] + i * 3LL * qK + qK;
+  const long long qK = (long long)q * ldb;
+  const double *Th = c.BTpool + c.dt->nodeBT[d] + i * 3LL * qK + qK + c.aug;    // ancestor columns of T_c
   const double *Tl = Th + qK;
   const double *tg = c.Tv + c.dt->nodeT[d] + i * 2LL * q;
   double *w1 = c.V + c.dt->nodeV[d + 1] + (2 * i) * (long long)K1;
@@ -638,8 +652,8 @@ __device__ void tree_down_node(const SolveCtx &c, int d, long long i, int lane) 
     const int u = u0 + lane / parts;
     Acc2 A = acc2(0.0);
     if (u < q) {
-      if (part == 0) { A = acc2(tg[u]); A.c += tg[q + u]; }
-      const double *thu = Th + (long long)u * Kd, *tlu = Tl + (long long)u * Kd;
+      if (part == 0) { double th0, tl0; t_of(c, tg, Th, Tl, ldb, q, u, th0, tl0); A = acc2(th0); A.c += tl0; }
+      const double *thu = Th + (long long)u * ldb, *tlu = Tl + (long long)u * ldb;
       int a = part;
       for (; a + 3 * parts < Kd; a += 4 * parts) {      // 4 iterations of loads in flight
         const double w0 = wc[a], w1v = wc[a + parts], w2v = wc[a + 2 * parts], w3 = wc[a + 3 * parts];
@@ -667,9 +681,10 @@ __device__ void tree_down_node(const SolveCtx &c, int d, long long i, int lane) 
 // ustep = 1) or, for levels with few nodes, a CTA per node (u0 = warp, ustep = warps).
 __device__ void tree_down_rows(const SolveCtx &c, int d, long long i, int lane, int u0, int ustep, bool copy_w) {
   const int r = c.dt->rdep[d + 1], q = 2 * r, Kd = c.dt->Kdim[d], K1 = c.dt->Kdim[d + 1];
+  const int ldb = c.dt->Kf[d];
   const double *wc = c.V + c.dt->nodeV[d] + i * (long long)Kd;
-  const long long qK = (long long)q * Kd;
-  const double *Th = c.BTpool + c.dt->nodeBT[d] + i * 3LL * qK + qK;
+  const long long qK = (long long)q * ldb;
+  const double *Th = c.BTpool + c.dt->nodeBT[d] + i * 3LL * qK + qK + c.aug;
   const double *Tl = Th + qK;
   const double *tg = c.Tv + c.dt->nodeT[d] + i * 2LL * q;
   double *w1 = c.V + c.dt->nodeV[d + 1] + (2 * i) * (long long)K1;
@@ -687,7 +702,7 @@ __device__ void tree_down_rows(const SolveCtx &c, int d, long long i, int lane, 
       for (int x = 0; x < UB; x++) {
         const int u = ub + x * ustep;
         const bool ok = u < q;
-        const double *thu = Th + (long long)(ok ? u : 0) * Kd, *tlu = Tl + (long long)(ok ? u : 0) * Kd;
+        const double *thu = Th + (long long)(ok ? u : 0) * ldb, *tlu = Tl + (long long)(ok ? u : 0) * ldb;
         h[x][0] = (ok && aa < Kd) ? thu[aa] : 0.0; l[x][0] = (ok && aa < Kd) ? tlu[aa] : 0.0;
         h[x][1] = (ok && ab < Kd) ? thu[ab] : 0.0; l[x][1] = (ok && ab < Kd) ? tlu[ab] : 0.0;
       }
@@ -706,7 +721,9 @@ __device__ void tree_down_rows(const SolveCtx &c, int d, long long i, int lane, 
       for (int x = 0; x < UB; x++) {
         const int u = ub + x * ustep;
         if (u >= q) break;
-        acc_add(A[x], tg[u]); A[x].c += tg[q + u];
+        double th0, tl0;
+        t_of(c, tg, Th, Tl, ldb, q, u, th0, tl0);
+        acc_add(A[x], th0); A[x].c += tl0;
         const double f = acc_val(A[x]);
         if (u < r) w1[Kd + u] = -f; else w2[Kd + u - r] = -f;
       }
@@ -788,8 +805,10 @@ __global__ void k_pack_rows(const double *xsorted, long long lo, long long m, do
 
 }  // namespace
 
-// y, x: one column each (device).  up_only: stop after the up pass (h_root = y^T C^{-1} y in hvec[0]).
-hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_only) {
+// y, x: one column each (device).  up_only: stop after the up pass (h_root = y^T C^{-1} y in hvec[0]).  fused: y is
+// the right-hand side the factorization carried (hodlr_factor_solve): its leaf and tree up passes are already in the
+// factors (Pi_c[0, :] = g_c, T_c[:, 0] = t_c), so only the down passes run.
+hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_only, bool fused) {
   const int kappa = h->kappa;
   DepthTab &dt = h->dt;
   if (h->leaf_max > VMAX || dt.Kdim[kappa] > KMAX_SOLVE)
@@ -810,6 +829,7 @@ hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_on
   c.lo = h->lo; c.hi = h->hi; c.perm = h->perm; c.Xh = h->Xh; c.ldx = h->ldx; c.rank = h->rank; c.dt = h->d_dt;
   c.Lf = h->Lf; c.lstride = h->lstride; c.Spool = h->Spool; c.BTpool = h->BTpool;
   c.V = h->Vpool; c.Tv = h->Tvec; c.hv = h->hvec; c.y = y; c.x = x; c.flags = h->dflags;
+  c.aug = h->aug; c.fused = fused ? 1 : 0;
   hodlr_own_nodes(h, kappa, &c.leaf0, &c.nown);
   c.xsorted = nullptr;
   if (h->nranks > 1 && !up_only) {
@@ -886,7 +906,9 @@ hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_on
   };
   ph_begin(h, PH_SLEAF_UP);
   hodlr_status st;
-  if (h->nranks > 1 && h->tsplit > 0) {
+  if (fused) {
+    st = launch(Phases{0, -1, 0, 1});
+  } else if (h->nranks > 1 && h->tsplit > 0) {
     // leaf up + own subtree levels, exchange of the depth-t projections, then the rest
     st = launch(Phases{1, kappa - 1, h->tsplit, 0});
     if (st != HODLR_OK) return st;

@@ -23,12 +23,13 @@ __host__ __device__ __forceinline__ long long tree_smem_doubles(int q, int ldk) 
   return 5LL * q * q + 6LL * q + 4LL * q * ldk;
 }
 
-// Gauss-Jordan with partial pivoting on [S | I] (q <= QB rows, one row per lane, in registers): row swaps and
-// the pivot-row broadcast by shuffles, no shared-memory traffic or barriers.  Same pivots (row of max |.|,
-// first index on ties, explicit swaps) and U_kk as the LU of the coupling system.  On exit lane a < q writes
-// row a of S^{-1} to W[a][q..2q), lane 0 writes |U_kk| to ukk[k]; returns sign and zero-pivot flag.
+// Gauss-Jordan with partial pivoting on [S | I] (q <= QB rows, one row per lane, in registers), q <= 8.  Row
+// interchanges are logical: every lane carries the current position `pos` of its row, so a swap is two position
+// updates.  Pivot rule as the LU of the coupling system (row of max |.| among the not-yet-pivoted positions >= k,
+// the smallest position on ties), hence the same pivots, U_kk and sign.  On exit the lane at position a writes row a
+// of S^{-1} to Wout[a][q..2q); lane 0 writes |U_kk| to ukk[k]; returns sign and zero-pivot flag.
 template <int QB>
-__device__ void gj_regs(double *W, int q, double *ukk, int &sign, int &zero) {
+__device__ void gj_regs(const double *W, double *Wout, int q, double *ukk, int &sign, int &zero) {
   const int lane = threadIdx.x & 31, q2 = 2 * q;
   double w[2 * QB];
 #pragma unroll
@@ -36,40 +37,93 @@ __device__ void gj_regs(double *W, int q, double *ukk, int &sign, int &zero) {
     w[j] = (lane < q && j < q) ? W[lane * q2 + j] : 0.0;
     w[QB + j] = (lane < q && j < q) ? W[lane * q2 + q + j] : 0.0;
   }
+  int pos = lane;
   sign = 1; zero = 0;
 #pragma unroll
   for (int k = 0; k < QB; k++) {
     if (k < q) {                                   // (warp-uniform; keeps the loop fully unrolled)
-      double best = (lane >= k && lane < q) ? fabs(w[k]) : -1.0;
-      int p = lane;
+      double best = (lane < q && pos >= k) ? fabs(w[k]) : -1.0;
+      int bp = pos, bl = lane;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
-        const double b2 = __shfl_xor_sync(0xffffffffu, best, o); const int p2 = __shfl_xor_sync(0xffffffffu, p, o);
-        if (b2 > best || (b2 == best && p2 < p)) { best = b2; p = p2; }
+        const double b2 = __shfl_xor_sync(0xffffffffu, best, o);
+        const int p2 = __shfl_xor_sync(0xffffffffu, bp, o), l2 = __shfl_xor_sync(0xffffffffu, bl, o);
+        if (b2 > best || (b2 == best && p2 < bp)) { best = b2; bp = p2; bl = l2; }
       }
-      if (p != k) {                                // swap rows k and p
+      const int P = bl;                            // lane holding the pivot row (position bp >= k)
+      if (bp != k) {                               // swap positions k and bp
         sign = -sign;
-        const int src = lane == k ? p : (lane == p ? k : lane);
-#pragma unroll
-        for (int j = 0; j < 2 * QB; j++) w[j] = __shfl_sync(0xffffffffu, w[j], src);
+        if (pos == k) pos = bp;
+        else if (lane == P) pos = k;
       }
-      const double piv = __shfl_sync(0xffffffffu, w[k], k);
+      const double piv = __shfl_sync(0xffffffffu, w[k], P);
       if (piv < 0.0) sign = -sign;
       if (!(piv != 0.0)) zero = 1;
       if (lane == 0) ukk[k] = fabs(piv);
       const double ip = piv != 0.0 ? 1.0 / piv : 0.0;
-      const double mlt = lane == k ? 0.0 : w[k] * ip;
+      const double mlt = lane == P ? 0.0 : w[k] * ip;
 #pragma unroll
-      for (int j = 0; j < 2 * QB; j++) {
-        const double prj = __shfl_sync(0xffffffffu, w[j], k);
-        w[j] = lane == k ? w[j] * ip : fma(-mlt, prj, w[j]);
+      for (int j = k + 1; j < QB; j++) {
+        const double prj = __shfl_sync(0xffffffffu, w[j], P);
+        w[j] = lane == P ? w[j] * ip : fma(-mlt, prj, w[j]);
+      }
+      w[k] = lane == P ? 1.0 : 0.0;
+#pragma unroll
+      for (int j = QB; j < 2 * QB; j++) {
+        const double prj = __shfl_sync(0xffffffffu, w[j], P);
+        w[j] = lane == P ? w[j] * ip : fma(-mlt, prj, w[j]);
       }
     }
   }
   if (lane < q) {
 #pragma unroll
-    for (int j = 0; j < QB; j++) if (j < q) W[lane * q2 + q + j] = w[QB + j];
+    for (int j = 0; j < QB; j++) if (j < q) Wout[pos * q2 + q + j] = w[QB + j];
   }
+}
+
+// The same elimination for 8 < q <= 32 by one warp on [S | I] in shared memory (row a at lane a; no CTA barrier):
+// logical interchanges as above, and no pivot-row scaling during the sweep (each non-pivot row subtracts
+// (W[a][k] / W[P][k]) row_P, the pivot row is left as it is); at the end the lane of position a divides its right
+// half by its pivot and writes row a of S^{-1} to Wout[a][q..2q).  Same pivots and U_kk as the LU.
+static __device__ void gj_warp(double *W, double *Wout, int q, double *ukk, int &sign, int &zero) {
+  const int lane = threadIdx.x & 31, q2 = 2 * q;
+  int pos = lane;
+  sign = 1; zero = 0;
+  double *row = W + lane * q2;
+  for (int k = 0; k < q; k++) {
+    double best = (lane < q && pos >= k) ? fabs(row[k]) : -1.0;
+    int bp = pos, bl = lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double b2 = __shfl_xor_sync(0xffffffffu, best, o);
+      const int p2 = __shfl_xor_sync(0xffffffffu, bp, o), l2 = __shfl_xor_sync(0xffffffffu, bl, o);
+      if (b2 > best || (b2 == best && p2 < bp)) { best = b2; bp = p2; bl = l2; }
+    }
+    const int P = bl;
+    if (bp != k) {
+      sign = -sign;
+      if (pos == k) pos = bp;
+      else if (lane == P) pos = k;
+    }
+    const double *prow = W + P * q2;
+    const double piv = prow[k];
+    if (piv < 0.0) sign = -sign;
+    if (!(piv != 0.0)) zero = 1;
+    if (lane == 0) ukk[k] = fabs(piv);
+    if (lane < q && lane != P) {
+      const double mlt = piv != 0.0 ? row[k] / piv : 0.0;
+      for (int j = k + 1; j < q; j++) row[j] = fma(-mlt, prow[j], row[j]);
+      row[k] = 0.0;
+      for (int j = q; j < q2; j++) row[j] = fma(-mlt, prow[j], row[j]);
+    }
+    __syncwarp();
+  }
+  if (lane < q) {
+    const double d = row[pos];
+    const double id = d != 0.0 ? 1.0 / d : 0.0;
+    for (int j = 0; j < q; j++) Wout[pos * q2 + q + j] = row[q + j] * id;
+  }
+  __syncwarp();
 }
 
 // One CTA per depth-d node c (heap index (2^d - 1) + i):
@@ -129,11 +183,14 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
   }
   __syncthreads();
   // ---------------- Gauss-Jordan with partial pivoting ----------------
-  // q <= 8: warp 0 in registers (gj_regs); larger systems: the whole CTA, 3 barriers per step.
-  if (q <= 8) {
+  // q <= 8: warp 0 in registers (gj_regs); 8 < q <= 32: warp 0 in shared memory (gj_warp); larger systems: the
+  // whole CTA, one barrier per step.
+  // (both write S^{-1} to W2: the pre-elimination W of gj_warp is overwritten in place)
+  if (q <= 32) {
     if (t < 32) {
       int sign, zero;
-      gj_regs<8>(W, q, colk, sign, zero);
+      if (q <= 8) gj_regs<8>(W, W2, q, colk, sign, zero);
+      else gj_warp(W, W2, q, colk, sign, zero);
       if (t == 0) { s_sign = sign; s_zero = zero; }
     }
   } else {
@@ -205,7 +262,7 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
   }
   __syncthreads();
   const bool zero = s_zero != 0;
-  const double *Si = ((q > 8 && (q & 1)) ? W2 : W) + q;   // S^{-1} (after the last ping-pong step), row stride 2q
+  const double *Si = ((q <= 32 || (q & 1)) ? W2 : W) + q; // S^{-1} (gj_*, or after the last ping-pong step), stride 2q
   if (!zero && Kd > 0) {
     const int qK = q * ldk;
     for (int e = t; e < qK; e += NT) {                // T_hi = S^{-1} B

@@ -19,7 +19,7 @@ KERNELS = {"se": HODLR_SE, "matern32": HODLR_MATERN32, "matern52": HODLR_MATERN5
            "imq": HODLR_IMQ, "rq": HODLR_RQ}
 STATUS = {0: "OK", 1: "EINVAL", 2: "ENOTPD", 3: "ERANKCAP", 4: "ESTATE", 5: "ENOMEM", 6: "ECUDA", 7: "ENCCL"}
 
-EXPORTS = ("hodlr_build", "hodlr_factor", "hodlr_logdet", "hodlr_solve", "hodlr_apply", "gp_predict", "gp_loglik",
+EXPORTS = ("hodlr_build", "hodlr_factor", "hodlr_factor_solve", "hodlr_cache_trim", "hodlr_logdet", "hodlr_solve", "hodlr_apply", "gp_predict", "gp_loglik",
            "hodlr_info",
            "hodlr_get_order", "hodlr_get_tree", "hodlr_get_logdet_parts", "hodlr_free", "hodlr_last_error",
            "hodlr_version", "hodlr_launch_count", "hodlr_nccl_unique_id", "hodlr_group_create",
@@ -77,6 +77,8 @@ def load(build_if_missing: bool = True):
         P, I64, I32, D = C.c_void_p, C.c_int64, C.c_int32, C.c_double
         lib.hodlr_build.argtypes = [P, I64, I32, P, D, I32, D, P, P, P, P]
         lib.hodlr_factor.argtypes = [P]
+        lib.hodlr_factor_solve.argtypes = [P, P, P, P]; lib.hodlr_factor_solve.restype = I32
+        lib.hodlr_cache_trim.argtypes = []; lib.hodlr_cache_trim.restype = None
         lib.hodlr_logdet.argtypes = [P, P]
         lib.hodlr_solve.argtypes = [P, P, P, I64, I64]
         lib.hodlr_apply.argtypes = [P, P, P, I64, I64]
@@ -141,6 +143,20 @@ def hodlr_build(x: torch.Tensor, kernel: int, theta, sigma2: float, leaf: int, e
 
 def hodlr_factor(h: int):
     _check(load().hodlr_factor(h))
+
+
+def hodlr_factor_solve(h: int, y: torch.Tensor, solve: bool = True):
+    """Fused factor + solve of one right-hand side: returns (C^{-1} y or None, y^T C^{-1} y)."""
+    lib = load()
+    y = _dev_f64(y, "y")
+    x = torch.empty_like(y) if solve else None
+    q = C.c_double(0.0)
+    _check(lib.hodlr_factor_solve(h, y.data_ptr(), x.data_ptr() if x is not None else None, C.byref(q)))
+    return x, q.value
+
+
+def hodlr_cache_trim():
+    load().hodlr_cache_trim()
 
 
 def hodlr_logdet(h: int) -> float:
@@ -279,6 +295,10 @@ class HODLR:
     def factor(self):
         hodlr_factor(self._h)
         return self
+
+    def factor_solve(self, y: torch.Tensor, solve: bool = True):
+        """Factor with y fused in; returns (C^{-1} y or None, y^T C^{-1} y).  The handle is then factored."""
+        return hodlr_factor_solve(self._h, y, solve)
 
     def logdet(self) -> float:
         return hodlr_logdet(self._h)
