@@ -39,7 +39,7 @@ __global__ void k_aca_init(AcaCtx c, int nblocks, int cap) {
   long long m1 = c.hi[c1] - c.lo[c1], m2 = c.hi[c2] - c.lo[c2];
   long long mn = m1 < m2 ? m1 : m2;
   AcaState *s = &c.st[b];
-  s->k = 0; s->done = 0; s->cnt_r = 0; s->cnt_c = 0;
+  s->k = 0; s->done = 0; s->cnt_r = 0; s->cnt_c = 0; s->raw_last = 0;
   s->cap = (int)(cap < mn ? cap : mn);
   s->ipiv = m1 - 1;                      // DESIGN.md R2: last row of c1 (the point nearest c2)
   s->jpiv = -1; s->pivval = 0.0; s->S2 = 0.0; s->nv2 = 0.0;
@@ -98,32 +98,52 @@ __device__ __forceinline__ void block_argmax_n2(double &ba, long long &bi, doubl
 constexpr int ACA_E = 4;                       // elements per thread per sub-tile
 constexpr int ACA_TILE = ACA_SUB * ACA_E;
 
+// Shared scratch of one item (one set per CTA, reused by the row and column passes)
+struct AcaScratch {
+  double coef[ACA_MAXCAP];
+  double sdot[ACA_SUB / 32][ACA_MAXCAP];
+  double s_abs[ACA_SUB / 32], s_val[ACA_SUB / 32], s_n2[ACA_SUB / 32];
+  long long s_idx[ACA_SUB / 32];
+  double part[ACA_SUB / 32][4 + ACA_MAXCAP];
+  double tot[1 + ACA_MAXCAP];
+  double dnew[ACA_MAXCAP];
+  double sG[ACA_GSZ];
+  int amLast;
+};
+
+// One item (a chunk of one side of one active big block) of a step's row (ROW) or column pass; c is the pass's
+// context in shared memory (global stores cannot alias it).  CTA-uniform control flow.
 template <bool ROW, bool SEO>
-__global__ void __launch_bounds__(ACA_SUB, ACA_PASS_MINB) k_aca_pass(const AcaCtx *__restrict__ pc) {
-  __shared__ AcaCtx c;                         // context in shared memory: global stores cannot alias it
-  for (int i = threadIdx.x; i < (int)(sizeof(AcaCtx) / 8); i += ACA_SUB) ((long long *)&c)[i] = ((const long long *)pc)[i];
-  __syncthreads();
+__device__ __forceinline__ void aca_item(const AcaCtx &c, int item, AcaScratch &S) {
+  double *coef = S.coef;
+  double (*sdot)[ACA_MAXCAP] = S.sdot;
+  double *s_abs = S.s_abs, *s_val = S.s_val, *s_n2 = S.s_n2;
+  long long *s_idx = S.s_idx;
+  double (*part)[4 + ACA_MAXCAP] = S.part;
+  double *tot = S.tot, *dnew = S.dnew, *sG = S.sG;
   int *flags = c.flags;
-  const AcaItem it = c.items[blockIdx.x];
+  const AcaItem it = c.items[item];
   const int b = it.block;
   AcaState *st = &c.st[b];
   const int done = __ldcg(&st->done), k = __ldcg(&st->k);          // one round of loads for the state
   const long long piv = ROW ? __ldcg(&st->ipiv) : __ldcg(&st->jpiv);
-  const double pivval = ROW ? 1.0 : __ldcg(&st->pivval);
   if (done) return;
   const long long n = c.n, ldx = c.ldx;
   const long long lo1 = it.lo1, m1 = it.m1, lo2 = it.lo2, m2 = it.m2;
   const int e = it.e;
   double *slot = c.Xh + it.slot_off;
   const unsigned char *used = c.used + (long long)(e - 1) * n;
+  const long long ilen = it.len;
+  // The row pass of step k divides the previous step's column V[:, k-1] (stored as the raw residual v~) by that
+  // step's pivot as it streams it -- the oracle's V = v~ / v~_jk (R16), written back in place -- so no separate pass
+  // over the column is needed; a block that finishes in a column pass gets its last column normalised by
+  // k_aca_finish.  (ROW: pivval here is still the previous step's pivot: this pass's last CTA sets the new one
+  // only after every CTA has read the state.)
+  const double pvp = ROW ? __ldcg(&st->pivval) : 1.0;
+  const double rpvp = ROW && k > 0 ? __drcp_rn(pvp) : 1.0;
   const long long pg = ROW ? lo1 + piv : lo2 + piv;               // fixed row (ROW) / column (COL)
   const double xp = c.xs[pg];
   const long long lo = ROW ? lo2 : lo1;
-  const double scale = ROW ? 1.0 : 1.0 / pivval;
-  __shared__ double coef[ACA_MAXCAP];
-  __shared__ double sdot[ACA_SUB / 32][ACA_MAXCAP];
-  __shared__ double s_abs[ACA_SUB / 32], s_val[ACA_SUB / 32], s_n2[ACA_SUB / 32];
-  __shared__ long long s_idx[ACA_SUB / 32];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   // (zero-padded to a multiple of 4: the vector path runs whole batches of 4 columns without masks)
   for (int l = t; l < ((k + 3) & ~3); l += ACA_SUB) coef[l] = l < k ? slot[(long long)l * ldx + pg] : 0.0;
@@ -133,13 +153,13 @@ __global__ void __launch_bounds__(ACA_SUB, ACA_PASS_MINB) k_aca_pass(const AcaCt
   // congruent to L mod 8 (w0 for l < 32, w1 for l >= 32)
   double w0 = 0.0, w1 = 0.0;
   double ba = 0.0, bv = 0.0, n2 = 0.0; long long bi = -1;
-  const long long end = it.start + it.len;
+  const long long end = it.start + ilen;
   const size_t n1 = (size_t)ldx, n2s = 2 * (size_t)ldx, n3 = 3 * (size_t)ldx;   // factor column stride
   const int hi4 = lane & 16, hi3 = lane & 8;
   // vector path: thread t takes the 4 consecutive elements 4t..4t+3 of each 1024-element sub-tile (double2
   // loads/stores); needs 16-byte alignment of every column segment (n and the chunk start even) -- the
   // scalar loop below handles the rest
-  const bool vec = ((ldx | (lo + it.start)) & 3) == 0 && (it.len & 3) == 0;
+  const bool vec = ((ldx | (lo + it.start)) & 3) == 0 && (ilen & 3) == 0;
   if (vec) {
     for (long long s0 = it.start; s0 < end; s0 += ACA_TILE) {
       const long long g0 = lo + s0 + 4 * t;    // elements g0 .. g0 + 3
@@ -152,7 +172,7 @@ __global__ void __launch_bounds__(ACA_SUB, ACA_PASS_MINB) k_aca_pass(const AcaCt
         usedm = (u4.x ? 1u : 0u) | (u4.y ? 2u : 0u) | (u4.z ? 4u : 0u) | (u4.w ? 8u : 0u);
         const double xq[4] = {x01.x, x01.y, x23.x, x23.y};
 #pragma unroll
-        for (int q = 0; q < 4; q++) a[q] = kval_t<SEO>(c.kp, ROW ? xp - xq[q] : xq[q] - xp);
+        for (int q = 0; q < 4; q++) a[q] = kval_ot<SEO>(c.kp, ROW ? xp - xq[q] : xq[q] - xp);
       } else {
 #pragma unroll
         for (int q = 0; q < 4; q++) a[q] = 0.0;
@@ -171,13 +191,27 @@ __global__ void __launch_bounds__(ACA_SUB, ACA_PASS_MINB) k_aca_pass(const AcaCt
           const double2 f01 = *(const double2 *)cp, f23 = *(const double2 *)(cp + 2);
           F[dl][0] = f01.x; F[dl][1] = f01.y; F[dl][2] = f23.x; F[dl][3] = f23.y;
         }
+        if (ROW && l0 + LS >= k) {             // the batch holding column k-1: normalise it (and store it back)
+          const int dl = k - 1 - l0;
+#pragma unroll
+          for (int x = 0; x < LS; x++)
+            if (x == dl) {
+#pragma unroll
+              for (int q = 0; q < 4; q++) F[x][q] = div_by(F[x][q], pvp, rpvp);
+              if (ok) {
+                double *cp = (double *)colp + (size_t)(k - 1) * n1;
+                *(double2 *)cp = make_double2(F[x][0], F[x][1]);
+                *(double2 *)(cp + 2) = make_double2(F[x][2], F[x][3]);
+              }
+            }
+        }
         double pv[LS];
 #pragma unroll
         for (int dl = 0; dl < LS; dl++) {
           const double cf = coef[l0 + dl];
           double p = 0.0;
 #pragma unroll
-          for (int q = 0; q < 4; q++) { r[q] = fma(-cf, F[dl][q], r[q]); p = fma(F[dl][q], a[q], p); }
+          for (int q = 0; q < 4; q++) { r[q] = __dsub_rn(r[q], __dmul_rn(cf, F[dl][q])); p = fma(F[dl][q], a[q], p); }
           pv[dl] = p;
         }
         double s0v = hi4 ? pv[0] : pv[2], s1v = hi4 ? pv[1] : pv[3];
@@ -195,7 +229,7 @@ __global__ void __launch_bounds__(ACA_SUB, ACA_PASS_MINB) k_aca_pass(const AcaCt
       if (ok) {
         double v[4];
 #pragma unroll
-        for (int q = 0; q < 4; q++) v[q] = r[q] * scale;
+        for (int q = 0; q < 4; q++) v[q] = r[q];
         double *outp = slot + (long long)k * ldx + g0;
         *(double2 *)outp = make_double2(v[0], v[1]);
         *(double2 *)(outp + 2) = make_double2(v[2], v[3]);
@@ -218,7 +252,7 @@ __global__ void __launch_bounds__(ACA_SUB, ACA_PASS_MINB) k_aca_pass(const AcaCt
     for (int q = 0; q < ACA_E; q++) {
       const double xq = q < nval ? xsp[q * ACA_SUB] : xp;
       if (q < nval && up[q * ACA_SUB]) usedm |= 1u << q;
-      a[q] = q < nval ? kval_t<SEO>(c.kp, ROW ? xp - xq : xq - xp) : 0.0;
+      a[q] = q < nval ? kval_ot<SEO>(c.kp, ROW ? xp - xq : xq - xp) : 0.0;
       r[q] = a[q];
     }
     const double *colp = slot + g0;
@@ -231,13 +265,23 @@ __global__ void __launch_bounds__(ACA_SUB, ACA_PASS_MINB) k_aca_pass(const AcaCt
       for (int dl = 0; dl < LS; dl++)
 #pragma unroll
         for (int q = 0; q < ACA_E; q++) F[dl][q] = (l0 + dl < k && q < nval) ? cl[dl][q * ACA_SUB] : 0.0;
+      if (ROW && l0 + LS >= k) {               // column k-1: normalise (and store back), as in the vector path
+        const int dl = k - 1 - l0;
+#pragma unroll
+        for (int x = 0; x < LS; x++)
+          if (x == dl) {
+#pragma unroll
+            for (int q = 0; q < ACA_E; q++)
+              if (q < nval) { F[x][q] = div_by(F[x][q], pvp, rpvp); ((double *)cl[x])[q * ACA_SUB] = F[x][q]; }
+          }
+      }
       double pv[LS];
 #pragma unroll
       for (int dl = 0; dl < LS; dl++) {
         const double cf = l0 + dl < k ? coef[l0 + dl] : 0.0;
         double p = 0.0;
 #pragma unroll
-        for (int q = 0; q < ACA_E; q++) { r[q] = fma(-cf, F[dl][q], r[q]); p = fma(F[dl][q], a[q], p); }
+        for (int q = 0; q < ACA_E; q++) { r[q] = __dsub_rn(r[q], __dmul_rn(cf, F[dl][q])); p = fma(F[dl][q], a[q], p); }
         pv[dl] = p;
       }
       // transposed butterfly: 4 values x 32 lanes -> lane L holds sum of value 2*(L>>4&1) + (L>>3&1)
@@ -257,7 +301,7 @@ __global__ void __launch_bounds__(ACA_SUB, ACA_PASS_MINB) k_aca_pass(const AcaCt
     for (int q = 0; q < ACA_E; q++) {
       if (q >= nval) break;
       const long long g = g0 + q * ACA_SUB;
-      const double v = r[q] * scale;
+      const double v = r[q];
       slot[(long long)k * ldx + g] = v;
       if (!((usedm >> q) & 1u) && fabs(v) > ba) { ba = fabs(v); bi = g - lo; bv = v; }
       n2 += v * v;
@@ -278,7 +322,7 @@ __global__ void __launch_bounds__(ACA_SUB, ACA_PASS_MINB) k_aca_pass(const AcaCt
     rec[4 + l] = s;
   }
   if (t == 0) { rec[0] = ba; rec[1] = (double)bi; rec[2] = bv; rec[3] = n2; }
-  __shared__ int amLast;
+  int &amLast = S.amLast;
   __threadfence();
   __syncthreads();
   if (t == 0) amLast = (atomicAdd(ROW ? &st->cnt_r : &st->cnt_c, 1) == nq - 1);
@@ -292,7 +336,6 @@ __global__ void __launch_bounds__(ACA_SUB, ACA_PASS_MINB) k_aca_pass(const AcaCt
     const double aq = __ldcg(rq + 0); const long long iq = (long long)__ldcg(rq + 1);
     if (amax_better(ba, bi, aq, iq)) { ba = aq; bi = iq; bv = __ldcg(rq + 2); }
   }
-  __shared__ double part[ACA_SUB / 32][4 + ACA_MAXCAP];
   {   // columns 3 (nrm2) .. 3 + k (dots): warp w sums records w, w + 8, ...; lane owns columns lane + 32 s
     double acc[3] = {0.0, 0.0, 0.0};
     for (int q = warp; q < nq; q += ACA_SUB / 32) {
@@ -305,7 +348,6 @@ __global__ void __launch_bounds__(ACA_SUB, ACA_PASS_MINB) k_aca_pass(const AcaCt
   }
   double dummy = 0.0;
   block_argmax_n2(ba, bi, bv, dummy, s_abs, s_idx, s_val, s_n2);   // (syncs: part[] complete afterwards)
-  __shared__ double tot[1 + ACA_MAXCAP];
   for (int cidx = t; cidx <= k; cidx += ACA_SUB) {
     double s = 0.0;
     for (int w = 0; w < ACA_SUB / 32; w++) s += part[w][cidx];
@@ -314,21 +356,21 @@ __global__ void __launch_bounds__(ACA_SUB, ACA_PASS_MINB) k_aca_pass(const AcaCt
   __syncthreads();
   const long long bidx = c.bigidx[b];
   double *G = c.gram + bidx * (2LL * ACA_GSZ) + (ROW ? ACA_GSZ : 0);   // G_U then G_V
-  // dots with the new column: F_l . r = (F_l . a - sum_m coef_m G[l,m]) * scale; G staged in shared memory
-  __shared__ double dnew[ACA_MAXCAP];
-  __shared__ double sG[ACA_GSZ];
+  // dots with the new column: F_l . r = F_l . a - sum_m coef_m G[l,m] (G staged in shared memory); the row pass's
+  // column is normalised by the pivot (V[:,k] = v~ / v~_jk), so its dots and norm are divided by it
   for (int p = t; p < k * (k + 1) / 2; p += ACA_SUB) sG[p] = __ldcg(G + p);
   __syncthreads();
+  const double pv = (ROW && bi >= 0 && bv != 0.0) ? bv : 1.0;
   for (int l = t; l < k; l += ACA_SUB) {
     double s = tot[1 + l];
     for (int m = 0; m < k; m++) s = fma(-coef[m], sG[pk(l, m)], s);
-    s *= scale;
+    if (ROW) s = s / pv;
     dnew[l] = s;
     G[pk(k, l)] = s;
   }
   __syncthreads();
   if (t == 0) {
-    const double nr2 = tot[0];
+    const double nr2 = ROW ? (tot[0] / pv) / pv : tot[0];
     G[pk(k, k)] = nr2;
     if (ROW) {
       for (int l = 0; l < k; l++) st->dV[l] = dnew[l];
@@ -341,7 +383,7 @@ __global__ void __launch_bounds__(ACA_SUB, ACA_PASS_MINB) k_aca_pass(const AcaCt
       }
     } else {
       st->cnt_c = 0;
-      // ||S_{k+1}||^2 = ||S_k||^2 + 2 sum_{l<k} (U'_k.U'_l)(V'_l.V'_k) + ||U'_k||^2 ||V'_k||^2
+      // ||S_{k+1}||^2 = ||S_k||^2 + 2 sum_{l<k} (U_k.U_l)(V_l.V_k) + ||U_k||^2 ||V_k||^2
       double cross = 0.0;
       for (int l = 0; l < k; l++) cross += dnew[l] * st->dV[l];
       const double nu2 = nr2, nv2 = st->nv2;
@@ -357,9 +399,34 @@ __global__ void __launch_bounds__(ACA_SUB, ACA_PASS_MINB) k_aca_pass(const AcaCt
       else if (k1 == st->cap) { done = 2; atomicAdd(&flags[5], 1); }
       else if (bi < 0 || ba == 0.0) done = 1;
       else { st->ipiv = bi; mark_row_run(c, c.used + (long long)(e - 1) * n, lo1, m1, bi); }
-      if (done) { st->done = done; c.rank[b] = k1; atomicSub(c.active, 1); }
+      if (done) { st->done = done; st->raw_last = 1; c.rank[b] = k1; atomicSub(c.active, 1); }
     }
   }
+}
+
+// Step-synchronous pass: one CTA per item (launched as the nodes of a conditional-while CUDA graph, below).
+// Measured against a persistent cooperative kernel that strides one CTA per SM over the items with grid barriers
+// between passes: 3.8 ms vs 2.1 ms for the passes at config 3 (its 150 registers allow one CTA per SM, too few
+// loads in flight for the streamed factor columns).
+template <bool ROW, bool SEO>
+__global__ void __launch_bounds__(ACA_SUB, ACA_PASS_MINB) k_aca_pass(const AcaCtx *__restrict__ pc) {
+  __shared__ AcaCtx c;
+  __shared__ AcaScratch S;
+  for (int i = threadIdx.x; i < (int)(sizeof(AcaCtx) / 8); i += ACA_SUB) ((long long *)&c)[i] = ((const long long *)pc)[i];
+  __syncthreads();
+  aca_item<ROW, SEO>(c, blockIdx.x, S);
+}
+
+// After the step loop: the last column of every big block that finished in a column pass still holds the raw
+// residual row; divide it by its pivot (one CTA per row-pass item, i.e. per chunk of c2).
+__global__ void __launch_bounds__(ACA_SUB) k_aca_finish(const AcaCtx *__restrict__ pc) {
+  const AcaItem it = pc->items[blockIdx.x];
+  const AcaState *st = &pc->st[it.block];
+  if (!__ldcg(&st->raw_last)) return;
+  const int r = __ldcg(&st->k);
+  const double pv = __ldcg(&st->pivval), rp = __drcp_rn(pv);
+  double *v = pc->Xh + it.slot_off + (long long)(r - 1) * pc->ldx + it.lo2;
+  for (long long j = it.start + threadIdx.x; j < it.start + it.len; j += ACA_SUB) v[j] = div_by(v[j], pv, rp);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -377,7 +444,7 @@ __global__ void __launch_bounds__(NT) k_aca_fused(AcaCtx c, const int *blocks, i
   __shared__ double s_abs[(NT / 32)], s_val[(NT / 32)], s_n2[(NT / 32)];
   __shared__ long long s_idx[(NT / 32)];
   __shared__ long long s_ipiv, s_jpiv;
-  __shared__ double s_pval, s_nv2, s_S2;
+  __shared__ double s_nv2, s_S2;
   __shared__ int s_k, s_done;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int b = blocks[blockIdx.x];
@@ -404,17 +471,26 @@ __global__ void __launch_bounds__(NT) k_aca_fused(AcaCtx c, const int *blocks, i
     for (int l = t; l < k; l += NT) Ui[l] = slot[(long long)l * ldx + ig];
     __syncthreads();
     double ba = 0.0, bv = 0.0, n2 = 0.0; long long bi = -1;
+    // v~_j = A[ik, j] - sum_l U[ik, l] V[j, l], l ascending, each product rounded (the oracle's operation order)
     for (long long j = t; j < m2; j += NT) {
       const long long gj = lo2 + j;
-      double v = kval_t<SEO>(c.kp, xi - c.xs[gj]);
+      double v = kval_ot<SEO>(c.kp, xi - c.xs[gj]);
 #pragma unroll 8
-      for (int l = 0; l < k; l++) v -= Ui[l] * __ldcg(slot + (long long)l * ldx + gj);
-      slot[(long long)k * ldx + gj] = v;
+      for (int l = 0; l < k; l++) v = __dsub_rn(v, __dmul_rn(Ui[l], __ldcg(slot + (long long)l * ldx + gj)));
       vbuf[j] = v;
       if (!usedC[j] && fabs(v) > ba) { ba = fabs(v); bi = j; bv = v; }
       n2 += v * v;
     }
     block_argmax_n2<NT / 32>(ba, bi, bv, n2, s_abs, s_idx, s_val, s_n2);
+    if (bi < 0 || ba == 0.0) break;                      // exactly-zero residual row: rank k (block-uniform)
+    // V[:, k] = v~ / v~_jk
+    const double rbv = __drcp_rn(bv);
+    for (long long j = t; j < m2; j += NT) {
+      const double v = div_by(vbuf[j], bv, rbv);
+      vbuf[j] = v;
+      slot[(long long)k * ldx + lo2 + j] = v;
+    }
+    __syncthreads();
     for (int l = warp; l < k; l += (NT / 32)) {
       double s = 0.0;
 #pragma unroll 8
@@ -422,25 +498,20 @@ __global__ void __launch_bounds__(NT) k_aca_fused(AcaCtx c, const int *blocks, i
       s = warp_sum(s);
       if (lane == 0) dV[l] = s;
     }
-    if (t == 0) {
-      if (bi < 0 || ba == 0.0) { s_done = 1; }            // exactly-zero residual row: rank k
-      else { s_jpiv = bi; s_pval = bv; s_nv2 = n2; usedC[bi] = 1; }
-    }
+    if (t == 0) { s_jpiv = bi; s_nv2 = (n2 / bv) / bv; usedC[bi] = 1; }
     __syncthreads();
-    if (s_done) break;
     // ---------------- column pass ----------------
+    // u_i = A[i, jk] - sum_l V[jk, l] U[i, l] (unscaled, the oracle's order)
     const long long jg = lo2 + s_jpiv;
     const double xj = c.xs[jg];
-    const double rp = 1.0 / s_pval;
     for (int l = t; l < k; l += NT) Ui[l] = slot[(long long)l * ldx + jg];
     __syncthreads();
     ba = 0.0; bv = 0.0; n2 = 0.0; bi = -1;
     for (long long i = t; i < m1; i += NT) {
       const long long gi = lo1 + i;
-      double u = kval_t<SEO>(c.kp, c.xs[gi] - xj);
+      double u = kval_ot<SEO>(c.kp, c.xs[gi] - xj);
 #pragma unroll 8
-      for (int l = 0; l < k; l++) u -= Ui[l] * __ldcg(slot + (long long)l * ldx + gi);
-      u *= rp;
+      for (int l = 0; l < k; l++) u = __dsub_rn(u, __dmul_rn(Ui[l], __ldcg(slot + (long long)l * ldx + gi)));
       slot[(long long)k * ldx + gi] = u;
       vbuf[i] = u;
       if (!usedR[i] && fabs(u) > ba) { ba = fabs(u); bi = i; bv = u; }
@@ -494,10 +565,11 @@ __global__ void k_aca_cond(cudaGraphConditionalHandle hdl, const AcaCtx *__restr
 }  // namespace
 
 // ---------------------------------------------------------------------------------------------
-// Host plan, cached per tree shape (n, leaf): chunk items of the big blocks, the fused small blocks, record
-// offsets, depths, and the instantiated conditional-while graph of the big-block step loop.  The graph's
-// kernels read their context from plan-owned device memory (rewritten per build), so repeated builds of the
-// same shape skip the planning and the graph instantiation.  A plan in use by another build is not shared.
+// Host plan, cached per tree shape (n, leaf, shard, rank cap, kernel variant, device): chunk items of the big blocks,
+// the fused small blocks, record offsets, depths, and the instantiated conditional-while graph of the big-block step
+// loop.  The graph's kernels read their context from plan-owned device memory (rewritten per build), so repeated
+// builds of the same shape skip the planning and the graph instantiation.  A plan in use by another build is not
+// shared.
 // ---------------------------------------------------------------------------------------------
 struct AcaPlan {
   // key: everything the cached device tables depend on -- the tree (n, leaf), the shard (rank, nranks), the
@@ -616,6 +688,7 @@ static cudaError_t plan_create(AcaPlan *P, const hodlr_s *h) {
   return e;
 }
 
+
 static AcaPlan *plan_acquire(const hodlr_s *h, hodlr_status *st) {
   {
     std::lock_guard<std::mutex> lk(g_plan_mu);
@@ -677,6 +750,7 @@ hodlr_status hodlr_aca(hodlr_s *h) {
   AcaCtx cx[2] = {c, c};
   cx[0].items = P->d_items_r; cx[0].nq = P->d_nq; cx[0].recbase = P->d_rb; cx[0].rec = d_rec;
   cx[1].items = P->d_items_c; cx[1].nq = P->d_nq + nb; cx[1].recbase = P->d_rb + nb; cx[1].rec = d_rec + ACA_RECW * P->nrec_r;
+  cx[0].nitems = (int)P->nitems_r; cx[1].nitems = (int)P->nitems_c;
   HCUDA(cudaMemcpyAsync(P->d_ctx, cx, sizeof(cx), cudaMemcpyHostToDevice, h->st));
   hodlr_trace("aca: planned + copies issued");
   k_aca_init<<<(int)((nb + 255) / 256), 256, 0, h->st>>>(c, (int)nb, h->cap);
@@ -699,11 +773,13 @@ hodlr_status hodlr_aca(hodlr_s *h) {
     HLAUNCH(h, "k_aca_fused");
     HCUDA(cudaEventRecord(h->ev_join, h->st2));
   }
-  int steps = 0;
-  static int nograph = -1;     // HODLR_ACA_NOGRAPH=1: host-driven step loop (profilers see every launch)
+  // HODLR_ACA_NOGRAPH=1 (profiling: ncu lists every pass): the same passes launched from a host loop that polls the
+  // active count after each step; same kernels, same results (tests/test_gpu_parity.py::test_aca_nograph_identical)
+  static int nograph = -1;
   if (nograph < 0) { const char *ev = getenv("HODLR_ACA_NOGRAPH"); nograph = ev && atoi(ev) ? 1 : 0; }
+  int hsteps = 0;
   if (nbig > 0 && nograph) {
-    for (steps = 1; steps <= h->cap + 1; steps++) {
+    for (hsteps = 1; hsteps <= h->cap + 1; hsteps++) {
       if (P->seo) k_aca_pass<true, true><<<(unsigned)P->nitems_r, ACA_SUB, 0, h->st>>>(P->d_ctx);
       else k_aca_pass<true, false><<<(unsigned)P->nitems_r, ACA_SUB, 0, h->st>>>(P->d_ctx);
       HLAUNCH(h, "k_aca_pass<row>");
@@ -719,6 +795,10 @@ hodlr_status hodlr_aca(hodlr_s *h) {
     HCUDA(cudaGraphLaunch(P->ge, h->st));
     hodlr_trace("aca: graph launched");
   }
+  if (nbig > 0) {
+    k_aca_finish<<<(unsigned)P->nitems_r, ACA_SUB, 0, h->st>>>(P->d_ctx);
+    HLAUNCH(h, "k_aca_finish");
+  }
   if (!P->fused_blocks.empty()) HCUDA(cudaStreamWaitEvent(h->st, h->ev_join, 0));
   if (P->nfused_small > 0) HCUDA(cudaStreamWaitEvent(h->st, h->ev_join2, 0));
   HCUDA(cudaEventRecord(h->ev_hi, h->sthi));
@@ -727,6 +807,7 @@ hodlr_status hodlr_aca(hodlr_s *h) {
   ph_end(h, PH_ACA);
   HCUDA(cudaStreamSynchronize(h->st));
   hodlr_trace("aca: synced");
+  int steps = hsteps;
   if (nbig > 0 && !nograph) {
     HCUDA(cudaMemcpy(&steps, h->dflags + 6, sizeof(int), cudaMemcpyDeviceToHost));
     h->launches += 3 * steps; hodlr_global_launches += 3 * steps;

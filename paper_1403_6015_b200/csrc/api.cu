@@ -295,6 +295,14 @@ hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const 
           : kernel == HODLR_MATERN52 ? sqrt(5.0) / theta[1]
           : kernel == HODLR_EXP ? 1.0 / theta[1] : 1.0 / (theta[1] * theta[1]);
   h->kp.alpha = kernel == HODLR_RQ ? theta[2] : 0.5;
+  h->kp.ell = theta[1];
+  h->kp.c2 = (2.0 * theta[1]) * theta[1];            // the oracle's 2.0 * ell * ell (left to right)
+  h->kp.sq = kernel == HODLR_MATERN32 ? sqrt(3.0) : sqrt(5.0);
+  {   // exact reciprocals (powers of two) let kval_o multiply instead of divide, bit for bit the same
+    int ex;
+    h->kp.rc2 = frexp(h->kp.c2, &ex) == 0.5 ? 1.0 / h->kp.c2 : 0.0;
+    h->kp.rell = frexp(theta[1], &ex) == 0.5 ? 1.0 / theta[1] : 0.0;
+  }
   // O2-equivalent tree: kappa = largest integer with leaf * 2^kappa <= n
   int kappa = 0;
   while (((long long)leaf << (kappa + 1)) <= n && kappa < HODLR_MAXDEPTH - 2) kappa++;

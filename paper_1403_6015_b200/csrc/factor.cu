@@ -17,11 +17,15 @@
 // The Schur updates cancel heavily (the top-level S_c reach cond ~1e11), so T_c is kept as a
 // double-double pair and Pi_c is accumulated with compensated arithmetic.
 #include "hodlr_internal.cuh"
+#include <cooperative_groups.h>
+#include <vector>
 #ifndef TREE_NARROW_MIN
 #define TREE_NARROW_MIN (4 * 148)   // levels with at least this many nodes (and q <= 16) use the 128-thread CTAs
 #endif
 #include <limits.h>
 #include <stdlib.h>
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -192,6 +196,21 @@ __global__ void __launch_bounds__(TT / 2, 6) k_tree_factor_narrow(TreeCtx c) {
   tree_node<DD>(c, i, sm, global_pi(c, i));
 }
 
+// The upper levels (few nodes each) in ONE persistent cooperative launch: CTAs stride over the nodes of a level, a
+// grid barrier separates the levels (deepest first).  These levels were launch- and cold-start-bound one kernel per
+// level (~50 us each regardless of their node count: every level's few CTAs start on SMs whose instruction caches
+// hold other kernels' code -- tree_node is ~10k instructions); here every SM warms its cache once.
+template <bool DD>
+__global__ void __launch_bounds__(TT, 2) k_tree_top(const TreeCtx *__restrict__ ctxs, int nlev) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double sm[];
+  for (int L = 0; L < nlev; L++) {
+    const TreeCtx c = ctxs[L];
+    for (long long j = blockIdx.x; j < c.cnt; j += gridDim.x) tree_node<DD>(c, c.i0 + j, sm, global_pi(c, c.i0 + j));
+    if (L + 1 < nlev) grid.sync();
+  }
+}
+
 // log det partial = leaves (left to right), then internal nodes of depth >= tsplit by depth kappa-1..tsplit,
 // left to right; per-thread Neumaier over a contiguous segment, combined in order by thread 0.
 // out[0] = partial, out[1] = failures seen by this rank.
@@ -274,6 +293,7 @@ hodlr_status hodlr_leaf_alloc(hodlr_s *h) {
 static TreeCtx tree_ctx(hodlr_s *h, int d, long long i0) {
   const DepthTab &dt = h->dt;
   TreeCtx tc;
+  tc.cnt = 0;
   // factor-side widths: Kf = Kdim (+ 1 with a fused right-hand side, which is then index 0 of every Pi)
   tc.d = d; tc.i0 = i0; tc.r = dt.rdep[d + 1]; tc.q = 2 * tc.r; tc.Kd = dt.Kf[d]; tc.K1 = dt.Kf[d + 1];
   tc.ldk = (tc.Kd + 3) & ~3; tc.dd = 1;   // compensated at every depth
@@ -304,10 +324,11 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
     dt.nodeBT[d] = btTot; btTot += (1LL << d) * 3 * q * dt.Kf[d];
   }
   h->Pipool = (double *)hodlr_dalloc(h, sizeof(double) * (piTot > 0 ? piTot : 1));
+  h->d_treectx = (TreeCtx *)hodlr_dalloc(h, sizeof(TreeCtx) * TREE_TOP_MAXLEV);
   h->Spool = (double *)hodlr_dalloc(h, sizeof(double) * (sTot > 0 ? sTot : 1));
   h->BTpool = (double *)hodlr_dalloc(h, sizeof(double) * (btTot > 0 ? btTot : 1));
   double *ldx = (double *)hodlr_dalloc(h, sizeof(double) * 2 * (h->nranks + 1));   // log det exchange
-  if (!h->node_ld || !h->d_logdet || !h->Pipool || !h->Spool || !h->BTpool || !ldx)
+  if (!h->node_ld || !h->d_logdet || !h->Pipool || !h->d_treectx || !h->Spool || !h->BTpool || !ldx)
     return hodlr_set_error(HODLR_ENOMEM, "factor: device allocation failed");
   HCUDA(cudaMemsetAsync(h->node_ld, 0, sizeof(double) * (h->ninternal > 0 ? h->ninternal : 1), h->st));
   HCUDA(cudaMemcpyAsync(h->d_dt, &dt, sizeof(DepthTab), cudaMemcpyHostToDevice, h->st));
@@ -364,8 +385,36 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
     HCUDA(hodlr_allow_smem((const void *)k_tree_factor<true>, h->dev));
     HCUDA(hodlr_allow_smem((const void *)k_tree_factor_narrow<true>, h->dev));
   }
+  int nsm = 148;
+  HCUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->dev));
+  std::vector<TreeCtx> top;           // the current run of upper levels for k_tree_top
+  auto flush_top = [&]() -> hodlr_status {
+    if (top.empty()) return HODLR_OK;
+    size_t smem = 0;
+    long long maxcnt = 0;
+    for (const TreeCtx &tc : top) {
+      smem = std::max(smem, sizeof(double) * (size_t)tree_smem_doubles(tc.q, tc.ldk));
+      maxcnt = std::max(maxcnt, tc.cnt);
+    }
+    if (top.size() > (size_t)TREE_TOP_MAXLEV) return hodlr_set_error(HODLR_EINVAL, "factor: tree level table overflow");
+    HCUDA(cudaMemcpyAsync(h->d_treectx, top.data(), sizeof(TreeCtx) * top.size(), cudaMemcpyHostToDevice, h->st));
+    HCUDA(hodlr_allow_smem((const void *)k_tree_top<true>, h->dev));
+    int per_sm = 0;
+    HCUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tree_top<true>, TT, smem));
+    if (per_sm < 1) return hodlr_set_error(HODLR_EINVAL, "factor: coupling system too large for one SM");
+    const int grid = (int)std::min<long long>(maxcnt, (long long)nsm * per_sm);
+    const TreeCtx *pc = h->d_treectx;
+    int nlev = (int)top.size();
+    void *args[] = {(void *)&pc, (void *)&nlev};
+    HCUDA(cudaLaunchCooperativeKernel((const void *)k_tree_top<true>, dim3(grid), dim3(TT), args, smem, h->st));
+    HLAUNCH(h, "k_tree_top");
+    top.clear();
+    return HODLR_OK;
+  };
   for (int d = kappa - 1; d >= 0; d--) {
     if (d + 1 == h->tsplit && h->nranks > 1) {     // every rank gets the Pi of all depth-t subtree roots
+      hodlr_status fs = flush_top();
+      if (fs != HODLR_OK) return fs;
       const long long Kt = dt.Kf[d + 1], sz = Kt * (Kt + 1) / 2;
       double *base = h->Pipool + dt.piOff[d + 1];
       hodlr_status xs = hodlr_allgather(h, base + h->grank * sz, base, sizeof(double) * sz);
@@ -373,12 +422,18 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
     }
     long long i0, cnt;
     hodlr_own_nodes(h, d, &i0, &cnt);
-    const TreeCtx tc = tree_ctx(h, d, i0);
+    TreeCtx tc = tree_ctx(h, d, i0);
+    tc.cnt = cnt;
+    if (cnt < TREE_NARROW_MIN) { top.push_back(tc); continue; }   // upper levels: batched into k_tree_top
     const size_t smem = sizeof(double) * (size_t)tree_smem_doubles(tc.q, tc.ldk);
-    const bool narrow = cnt >= TREE_NARROW_MIN && tc.q <= 16;
+    const bool narrow = tc.q <= 16;
     if (narrow) k_tree_factor_narrow<true><<<(int)cnt, TT / 2, smem, h->st>>>(tc);
     else k_tree_factor<true><<<(int)cnt, TT, smem, h->st>>>(tc);
     HLAUNCH(h, "k_tree_factor");
+  }
+  {
+    hodlr_status fs = flush_top();
+    if (fs != HODLR_OK) return fs;
   }
   // log det: this rank's leaves and subtree nodes (others are 0), exchanged with the failure counts, then the
   // top-level nodes (computed redundantly by every rank) once

@@ -17,6 +17,7 @@
 #include <algorithm>
 
 #define HODLR_MAXDEPTH 48
+#define TREE_TOP_MAXLEV HODLR_MAXDEPTH   // levels of one persistent upper-tree launch
 #define ACA_MAXCAP 64      // hard ceiling on the ACA rank cap (records/state are sized by it)
 #define ACA_RECW (4 + ACA_MAXCAP)
 #define ACA_GSZ (ACA_MAXCAP * (ACA_MAXCAP + 1) / 2)   // packed Gram matrix of one factor side
@@ -38,7 +39,20 @@
 // (PAPER.md:1251-1256).  kp = {a^2, c} with c = 1/(2 ell^2) for SE, sqrt(3)/ell or sqrt(5)/ell
 // for Matern-3/2 and -5/2.
 // ----------------------------------------------------------------------------------------------
-struct KParams { int kern; double a2; double c; double s2; double alpha; };
+struct KParams {
+  int kern; double a2; double c; double s2; double alpha;
+  double ell, c2, sq;       // ell; SE 2 ell^2 as (2 ell) ell; Matern sqrt(3) / sqrt(5) -- for kval_o
+  double rc2, rell;         // 1 / c2, 1 / ell when that reciprocal is exact (a power of two: x / c == x * (1 / c)
+                            // bit for bit, and a multiply is far cheaper than a division), else 0
+};
+// x / b for many x and one b: rb = RN(1 / b), q = RN(x rb), then one FMA correction with the exact remainder
+// x - b q (Markstein): the correctly rounded quotient (barring over/underflow) at 3 FP ops instead of a division
+__device__ __forceinline__ double div_by(double x, double b, double rb) {
+  const double q = x * rb;
+  return fma(fma(-q, b, x), rb, q);
+}
+// x / c with the reciprocal when it is exact (rc != 0), else a correctly rounded division: the same bits either way
+__device__ __forceinline__ double div_exact(double x, double c, double rc) { return rc != 0.0 ? x * rc : __ddiv_rn(x, c); }
 
 // Non-SE kernels share one exp: Matern pre (1 + s [+ s^2/3]) e^{-s}; EXP e^{-|d| c}; IMQ / RQ (1 + d^2 c)^{-alpha}
 // = e^{-alpha log(1 + d^2 c)} (no pow: u >= 1, alpha > 0), with c = sqrt(3)/ell, sqrt(5)/ell, 1/ell, 1/ell^2.
@@ -51,6 +65,41 @@ __device__ __forceinline__ double kval(const KParams &kp, double d) {
   else if (kp.kern >= HODLR_IMQ) arg = -kp.alpha * log(fma(d * d, kp.c, 1.0));
   return kp.a2 * pre * exp(arg);
 }
+// The same covariance functions in the oracle's operation order (the oracle's covariance function, built without FMA
+// contraction): explicitly rounded operations, ell divided rather than multiplied by a reciprocal.  The ACA's pivots
+// and ranks are FP-derived (R11); evaluating its entries (and residual updates) in the oracle's order keeps
+// its decisions the oracle's up to ulp differences of exp / log / pow between the two math libraries (R17).
+__device__ __forceinline__ double kval_o(const KParams &kp, double d) {
+  switch (kp.kern) {
+    case HODLR_SE: return __dmul_rn(kp.a2, exp(-div_exact(__dmul_rn(d, d), kp.c2, kp.rc2)));
+    case HODLR_EXP: return __dmul_rn(kp.a2, exp(-div_exact(fabs(d), kp.ell, kp.rell)));
+    case HODLR_IMQ: {
+      const double q = div_exact(d, kp.ell, kp.rell);
+      return __ddiv_rn(kp.a2, __dsqrt_rn(__dadd_rn(1.0, __dmul_rn(q, q))));
+    }
+    case HODLR_RQ: {
+      const double q = div_exact(d, kp.ell, kp.rell);
+      return __dmul_rn(kp.a2, pow(__dadd_rn(1.0, __dmul_rn(q, q)), -kp.alpha));
+    }
+    case HODLR_MATERN32: {
+      const double s = div_exact(__dmul_rn(kp.sq, fabs(d)), kp.ell, kp.rell);
+      return __dmul_rn(__dmul_rn(kp.a2, __dadd_rn(1.0, s)), exp(-s));
+    }
+    default: {                                   // HODLR_MATERN52
+      const double s = div_exact(__dmul_rn(kp.sq, fabs(d)), kp.ell, kp.rell);
+      const double p = __dadd_rn(__dadd_rn(1.0, s), __ddiv_rn(__dmul_rn(s, s), 3.0));
+      return __dmul_rn(__dmul_rn(kp.a2, p), exp(-s));
+    }
+  }
+}
+__device__ __forceinline__ double kval_o_se(const KParams &kp, double d) {
+  return __dmul_rn(kp.a2, exp(-div_exact(__dmul_rn(d, d), kp.c2, kp.rc2)));
+}
+template <bool SEO> __device__ __forceinline__ double kval_ot(const KParams &kp, double d) {
+  if (SEO) return kval_o_se(kp, d);
+  return kval_o(kp, d);
+}
+
 // SEO: the launch knows the kernel is SE (the bench / config 1, 3, 5 path): exactly the SE code, nothing else inlined
 template <bool SEO> __device__ __forceinline__ double kval_t(const KParams &kp, double d) {
   if (SEO) return kp.a2 * exp(-(d * d) * kp.c);
@@ -58,15 +107,15 @@ template <bool SEO> __device__ __forceinline__ double kval_t(const KParams &kp, 
 }
 
 // ----------------------------------------------------------------------------------------------
-// ACA per-block state (device).  Stored factors: V'[:,k] = raw residual row v~, U'[:,k] = u / v~_jk
-// (same product U V^T as the paper's normalisation; R16).
+// ACA per-block state (device).  Stored factors in the oracle's normalisation (O4, R16): V[:,k] = v~ / v~_jk
+// (the row pass writes v~, the next column pass divides it by the pivot), U[:,k] = u unscaled.
 // ----------------------------------------------------------------------------------------------
 struct AcaState {
   int k;            // number of terms so far
   int done;         // 0 active, 1 finished, 2 hit the rank cap without meeting eps
   int cnt_r, cnt_c; // CTA arrival counters (last-CTA reduction)
   int cap;          // min(rank_cap, m1, m2)
-  int pad;
+  int raw_last;     // finished in a column pass: V[:, rank-1] still holds the raw residual (k_aca_finish divides it)
   long long ipiv;   // current row pivot (local in c1)
   long long jpiv;   // current column pivot (local in c2)
   double pivval;    // v~_jk
@@ -120,6 +169,7 @@ struct AcaCtx {
   int *flags;               // handle flags (rank-cap hits in [5])
   int *step;                // step counter of the device loop
   int maxsteps;
+  int nitems;               // items of this pass (the persistent step kernel strides over them)
   double *gram;             // per big block: packed G_U = U'^T U', then G_V = V'^T V' 
   const int *forced;        // test hook (hodlr_opts.forced_ranks): stop block b at exactly forced[b] terms, or NULL
 };
@@ -182,6 +232,7 @@ struct hodlr_s {
   int *rank;
   int *bdepth;
   int *d_forced;             // hodlr_opts.forced_ranks on the device (test hook), or NULL
+  struct TreeCtx *d_treectx; // per-level contexts of the persistent upper-tree launch (factor.cu)
   int *dflags;               // [0] nonfinite x, [1] notpd, [2] notpd node (min), [3] nonfinite y, [4] active big
                              // ACA blocks, [5] rank-cap hits, [6] ACA steps, [7] x not ascending
   DepthTab *d_dt;

@@ -40,8 +40,12 @@ extern "C" hodlr_status gp_loglik_sweep(const double *x, const double *y, int64_
       hodlr_t h = nullptr;
       double ll = -INFINITY;
       hodlr_status st = hodlr_build(x, n, kernel, thetas + 2 * b, sigma2s[b], leaf, eps, nullptr, nullptr, s, &h);
-      if (st == HODLR_OK) st = hodlr_factor(h);
-      if (st == HODLR_OK) st = gp_loglik(h, y, &ll);
+      double quad = 0.0, ld = 0.0;
+      // y fused into the factorization: y^T C^{-1} y is the root's Pi, no solve pass at all
+      if (st == HODLR_OK) st = hodlr_factor_solve(h, y, nullptr, &quad);
+      if (st == HODLR_OK) st = hodlr_logdet(h, &ld);
+      // eq. 1: -1/2 y^T C^{-1} y - 1/2 log det C - (n/2) log(2 pi)
+      if (st == HODLR_OK) ll = -0.5 * quad - 0.5 * ld - 0.5 * (double)n * log(2.0 * M_PI);
       if (st != HODLR_OK) msg[b] = hodlr_last_error();
       hodlr_free(h);
       val[b] = st == HODLR_OK ? ll : -INFINITY;

@@ -8,6 +8,7 @@
 struct TreeCtx {
   int d;                    // depth of the nodes of this launch
   long long i0;             // first node (index within depth d) of this launch
+  long long cnt;            // nodes of depth d this launch computes (i0 .. i0 + cnt)
   int r, q, Kd, K1, ldk;    // ldk: row stride of B / T in shared memory (Kd rounded up to 4)
   int dd;                   // compensated (double-double) T and Pi
   const double *Pi1;        // children Pi base (depth d+1), packed K1(K1+1)/2 per node
@@ -63,15 +64,19 @@ __device__ void gj_regs(const double *W, double *Wout, int q, double *ukk, int &
       const double ip = piv != 0.0 ? 1.0 / piv : 0.0;
       const double mlt = lane == P ? 0.0 : w[k] * ip;
 #pragma unroll
-      for (int j = k + 1; j < QB; j++) {
-        const double prj = __shfl_sync(0xffffffffu, w[j], P);
-        w[j] = lane == P ? w[j] * ip : fma(-mlt, prj, w[j]);
+      for (int j = 0; j < QB; j++) {               // (constant trip count: fully unrolled, w stays in registers)
+        if (j > k && j < q) {
+          const double prj = __shfl_sync(0xffffffffu, w[j], P);
+          w[j] = lane == P ? w[j] * ip : fma(-mlt, prj, w[j]);
+        }
       }
       w[k] = lane == P ? 1.0 : 0.0;
 #pragma unroll
       for (int j = QB; j < 2 * QB; j++) {
-        const double prj = __shfl_sync(0xffffffffu, w[j], P);
-        w[j] = lane == P ? w[j] * ip : fma(-mlt, prj, w[j]);
+        if (j - QB < q) {
+          const double prj = __shfl_sync(0xffffffffu, w[j], P);
+          w[j] = lane == P ? w[j] * ip : fma(-mlt, prj, w[j]);
+        }
       }
     }
   }
@@ -81,17 +86,22 @@ __device__ void gj_regs(const double *W, double *Wout, int q, double *ukk, int &
   }
 }
 
-// The same elimination for 8 < q <= 32 by one warp on [S | I] in shared memory (row a at lane a; no CTA barrier):
-// logical interchanges as above, and no pivot-row scaling during the sweep (each non-pivot row subtracts
-// (W[a][k] / W[P][k]) row_P, the pivot row is left as it is); at the end the lane of position a divides its right
-// half by its pivot and writes row a of S^{-1} to Wout[a][q..2q).  Same pivots and U_kk as the LU.
-static __device__ void gj_warp(double *W, double *Wout, int q, double *ukk, int &sign, int &zero) {
+// The same elimination for 8 < q <= 32 by one warp in shared memory, no CTA barrier.  [S | I] is first transposed
+// from W (row-major, stride 2q) into Wt (column-major: element (a, j) at j q + a), so that the lanes (one row each)
+// touch consecutive words and the pivot row is a broadcast -- a row-major layout with stride 2q puts 8 lanes on each
+// bank group.  Logical interchanges as above, and no pivot-row scaling during the sweep (each non-pivot row
+// subtracts (Wt[a][k] / Wt[P][k]) row_P, the pivot row is left as it is); at the end the lane of position a divides
+// its right half by its pivot and writes row a of S^{-1} to Wout[a][q..2q) (row-major, stride 2q; Wout may be W).
+// Same pivots and U_kk as the LU.
+static __device__ void gj_warp(const double *W, double *Wt, double *Wout, int q, double *ukk, int &sign, int &zero) {
   const int lane = threadIdx.x & 31, q2 = 2 * q;
+  for (int a = 0; a < q; a++)
+    for (int j = lane; j < q2; j += 32) Wt[j * q + a] = W[a * q2 + j];
+  __syncwarp();
   int pos = lane;
   sign = 1; zero = 0;
-  double *row = W + lane * q2;
   for (int k = 0; k < q; k++) {
-    double best = (lane < q && pos >= k) ? fabs(row[k]) : -1.0;
+    double best = (lane < q && pos >= k) ? fabs(Wt[k * q + lane]) : -1.0;
     int bp = pos, bl = lane;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -105,23 +115,31 @@ static __device__ void gj_warp(double *W, double *Wout, int q, double *ukk, int 
       if (pos == k) pos = bp;
       else if (lane == P) pos = k;
     }
-    const double *prow = W + P * q2;
-    const double piv = prow[k];
+    const double piv = Wt[k * q + P];
     if (piv < 0.0) sign = -sign;
     if (!(piv != 0.0)) zero = 1;
     if (lane == 0) ukk[k] = fabs(piv);
     if (lane < q && lane != P) {
-      const double mlt = piv != 0.0 ? row[k] / piv : 0.0;
-      for (int j = k + 1; j < q; j++) row[j] = fma(-mlt, prow[j], row[j]);
-      row[k] = 0.0;
-      for (int j = q; j < q2; j++) row[j] = fma(-mlt, prow[j], row[j]);
+      const double mlt = piv != 0.0 ? Wt[k * q + lane] / piv : 0.0;
+      // columns k+1 .. 2q-1 (column k becomes 0), 8 at a time: all loads of a batch before its stores
+      for (int j0 = k + 1; j0 < q2; j0 += 8) {
+        double pv[8], rv[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+          const int j = j0 + u < q2 ? j0 + u : q2 - 1;
+          pv[u] = Wt[j * q + P]; rv[u] = Wt[j * q + lane];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++) if (j0 + u < q2) Wt[(j0 + u) * q + lane] = fma(-mlt, pv[u], rv[u]);
+      }
+      Wt[k * q + lane] = 0.0;
     }
     __syncwarp();
   }
   if (lane < q) {
-    const double d = row[pos];
+    const double d = Wt[pos * q + lane];
     const double id = d != 0.0 ? 1.0 / d : 0.0;
-    for (int j = 0; j < q; j++) Wout[pos * q2 + q + j] = row[q + j] * id;
+    for (int j = 0; j < q; j++) Wout[pos * q2 + q + j] = Wt[(q + j) * q + lane] * id;
   }
   __syncwarp();
 }
@@ -146,9 +164,19 @@ struct GlobalPi {
   }
 };
 
+#ifdef TREE_TRACE
+#include <stdio.h>
+#define TSTAMP(k) if (threadIdx.x == 0 && i == 0) { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tts[k])); }
+#else
+#define TSTAMP(k)
+#endif
 template <bool DD, class Src>
 __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &src) {
   const int t = threadIdx.x, NT = blockDim.x;
+#ifdef TREE_TRACE
+  unsigned long long tts[10] = {0};
+#endif
+  TSTAMP(0)
   const long long node = (1LL << c.d) - 1 + i;
   const int r = c.r, q = c.q, Kd = c.Kd, ldk = c.ldk, q2 = 2 * q;
   double *W = sm;                    // q x 2q  [S | I] -> [I | S^{-1}]
@@ -182,15 +210,16 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
     B[p] = v; Tl[p] = 0.0;
   }
   __syncthreads();
+  TSTAMP(1)
   // ---------------- Gauss-Jordan with partial pivoting ----------------
   // q <= 8: warp 0 in registers (gj_regs); 8 < q <= 32: warp 0 in shared memory (gj_warp); larger systems: the
   // whole CTA, one barrier per step.
-  // (both write S^{-1} to W2: the pre-elimination W of gj_warp is overwritten in place)
+  // (S^{-1} goes to W2, row-major; gj_warp uses W2 as its transposed work area and then writes S^{-1} into W)
   if (q <= 32) {
     if (t < 32) {
       int sign, zero;
       if (q <= 8) gj_regs<8>(W, W2, q, colk, sign, zero);
-      else gj_warp(W, W2, q, colk, sign, zero);
+      else gj_warp(W, W2, W, q, colk, sign, zero);
       if (t == 0) { s_sign = sign; s_zero = zero; }
     }
   } else {
@@ -243,6 +272,7 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
     if (t == 0) { s_sign = sign; s_zero = zero; }
   }
   __syncthreads();
+  TSTAMP(2)
   if (t < 32) {                                 // log|det S_c| = sum_k log|U_kk|, fixed-order warp reduction
     double la = 0.0, umax = 0.0, umin = 1e300;
     for (int k = t; k < q; k += 32) { const double u = colk[k]; la += log(u); umax = fmax(umax, u); umin = fmin(umin, u); }
@@ -261,8 +291,10 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
     }
   }
   __syncthreads();
+  TSTAMP(3)
   const bool zero = s_zero != 0;
-  const double *Si = ((q <= 32 || (q & 1)) ? W2 : W) + q; // S^{-1} (gj_*, or after the last ping-pong step), stride 2q
+  // S^{-1}, row stride 2q: W2 (gj_regs), W (gj_warp), or wherever the last ping-pong step left it
+  const double *Si = ((q <= 8 || (q > 32 && (q & 1))) ? W2 : W) + q;
   if (!zero && Kd > 0) {
     const int qK = q * ldk;
     for (int e = t; e < qK; e += NT) {                // T_hi = S^{-1} B
@@ -272,6 +304,7 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
       Th[e] = s;
     }
     __syncthreads();
+    TSTAMP(4)
     const int nref = s_nref;
     for (int it = 0; it < nref; it++) {               // iterative refinement, residual compensated
       for (int e = t; e < qK; e += NT) {
@@ -295,6 +328,7 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
       }
       __syncthreads();
     }
+    TSTAMP(5)
     // ---------------- Pi_c, 2x4 register tiles over the packed lower triangle ----------------
     // Bands of 4 rows; band P holds row tiles I = 2P, 2P+1 with column tiles J = 0..P (tile (I, J) =
     // rows 2I, 2I+1, columns 4J..4J+3); tiles up to band P: (P+1)(P+2).
@@ -351,6 +385,7 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
         }
     }
   }
+  TSTAMP(6)
   // persist S, S^{-1}, B, T_hi, T_lo for the solve
   double *Sg = c.Sst + i * (long long)(2 * q * q + q);
   for (int p = t; p < q * q; p += NT) {
@@ -367,5 +402,12 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
     BTg[2 * qKd + p] = Tl[a * ldk + b];
   }
   __syncthreads();
+  TSTAMP(7)
+#ifdef TREE_TRACE
+  if (threadIdx.x == 0 && i == 0)
+    printf("[tree d=%d q=%d Kd=%d] load %.2f gj %.2f logdet %.2f T %.2f refine %.2f Pi %.2f store %.2f us\n", c.d, q, Kd,
+           1e-3 * (tts[1] - tts[0]), 1e-3 * (tts[2] - tts[1]), 1e-3 * (tts[3] - tts[2]), 1e-3 * (tts[4] - tts[3]),
+           1e-3 * (tts[5] - tts[4]), 1e-3 * (tts[6] - tts[5]), 1e-3 * (tts[7] - tts[6]));
+#endif
 }
 

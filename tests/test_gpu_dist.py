@@ -92,9 +92,14 @@ def test_loglik_sweep_matches_single_settings(hb):
     th = np.array([[cfg.a, ell[k]] for k in ks]); sg = np.array([s2[k] for k in ks])
     xd = torch.from_numpy(x).cuda(); yd = torch.from_numpy(y).cuda()
     vals = hb.gp_loglik_sweep(xd, yd, cfg.kernel, th, sg, cfg.leaf, 1e-12, workers=3)
+    import math
     for j, k in enumerate(ks):
-        one = hb.HODLR(xd, cfg.kernel, (cfg.a, ell[k]), s2[k], cfg.leaf, 1e-12).factor().gp_loglik(yd)
+        g = hb.HODLR(xd, cfg.kernel, (cfg.a, ell[k]), s2[k], cfg.leaf, 1e-12)
+        _, quad = g.factor_solve(yd, solve=False)         # the sweep's path: y fused into the factorization
+        one = -0.5 * quad - 0.5 * g.logdet() - 0.5 * c.n * math.log(2 * math.pi)
         assert vals[j] == one
+        two = hb.HODLR(xd, cfg.kernel, (cfg.a, ell[k]), s2[k], cfg.leaf, 1e-12).factor().gp_loglik(yd)
+        assert abs(two - one) <= 1e-12 * abs(one)             # the unfused factor + loglik path
         o = OracleHODLR(x, cfg.kernel, (cfg.a, ell[k]), s2[k], cfg.leaf, 1e-12).factor()
         assert abs(vals[j] - o.gp_loglik(y)) <= 1e-9 * abs(o.gp_loglik(y)) + 1e-9 * abs(o.logdet())
     res = run_virtual_ranks(4, lambda r, d: hb.gp_loglik_sweep(xd, yd, cfg.kernel, th, sg, cfg.leaf, 1e-12, dist=d))
@@ -102,7 +107,7 @@ def test_loglik_sweep_matches_single_settings(hb):
         np.testing.assert_array_equal(v, vals)
 
 
-@pytest.mark.parametrize("flag", ["HODLR_LEAF_PAIR", "HODLR_CHOL_AFTER_ACA"])
+@pytest.mark.parametrize("flag", ["HODLR_CHOL_AFTER_ACA"])
 def test_alternate_paths_match(hb, flag):
     """The opt-in variants (fused leaf pairs + deepest tree level; Cholesky after the ACA) give the same
     factorization as the default path: run in a subprocess with the switch set."""
@@ -123,3 +128,29 @@ def test_alternate_paths_match(hb, flag):
     x0 = np.array(x0); x1 = np.array(x1)
     assert abs(ld1 - ld0) <= 1e-12 * abs(ld0)
     assert np.linalg.norm(x1 - x0) <= 1e-10 * np.linalg.norm(x0)
+
+
+@pytest.mark.parametrize("name,n,P", [("cfg1", 2048, 4), ("cfg3", 1 << 16, 8)])
+def test_virtual_ranks_factor_solve(hb, name, n, P):
+    """Sharded hodlr_factor_solve (y fused into the factorization; only the down passes after it) reproduces the
+    one-GPU fused result and returns the full solution on every rank."""
+    from paper_1403_6015_b200.dist import run_virtual_ranks
+    cfg = inputs.scaled(inputs.CONFIGS[name], n)
+    x = inputs.points(cfg); y = inputs.rhs(cfg)
+    xd = torch.from_numpy(x).cuda(); yd = torch.from_numpy(y).cuda()
+    g = hb.HODLR(xd, cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, 1e-12)
+    x1, q1 = g.factor_solve(yd); x1 = x1.cpu().numpy(); ld1 = g.logdet()
+    torch.cuda.synchronize()
+
+    def fn(r, d):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            h = hb.HODLR(xd, cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, 1e-12, dist=d)
+            xs, q = h.factor_solve(yd)
+            out = (h.logdet(), xs.cpu().numpy(), q)
+            h.close()
+        return out
+    for ld, xs, q in run_virtual_ranks(P, fn):
+        assert abs(ld - ld1) <= 1e-13 * abs(ld1)
+        assert abs(q - q1) <= 1e-12 * abs(q1)
+        assert np.linalg.norm(xs - x1) <= 1e-12 * np.linalg.norm(x1)

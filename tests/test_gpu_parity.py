@@ -339,3 +339,23 @@ def test_forced_ranks_hook(hb):
     print(f"[forced ranks n=2^16] solve rel {rel:.2e}")
     assert rel <= X_TOL
     assert abs(g.logdet() - o.logdet()) <= LD_TOL * abs(o.logdet())
+
+
+def test_aca_nograph_identical():
+    """HODLR_ACA_NOGRAPH=1 (the profiling switch: host-driven ACA passes instead of the conditional-while graph) runs
+    the same kernels: bitwise-identical log det and solution (separate process, the switch is read once)."""
+    import os
+    import subprocess
+    import sys
+    code = ("import sys, numpy as np, torch; sys.path.insert(0, '.');"
+            "from paper_1403_6015_b200 import inputs; import paper_1403_6015_b200.hodlr as hb;"
+            "c = inputs.scaled(inputs.CONFIGS['cfg3'], 1 << 15); x = torch.from_numpy(inputs.points(c)).cuda();"
+            "y = torch.from_numpy(inputs.rhs(c)).cuda(); h = hb.HODLR(x, c.kernel, c.theta, c.sigma2, c.leaf, 1e-12);"
+            "s, q = h.factor_solve(y); print(repr(h.logdet()), repr(q), float(s.abs().sum()))")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for ng in ("0", "1"):
+        env = dict(os.environ, HODLR_ACA_NOGRAPH=ng)
+        outs.append(subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                                   timeout=300).stdout.strip())
+    assert outs[0] and outs[0] == outs[1], outs

@@ -30,8 +30,9 @@ for name in ("cfg1", "cfg2", "cfg3", "cfg5"):
     x = torch.from_numpy(inputs.points(cfg)).cuda(); y = torch.from_numpy(inputs.rhs(cfg)).cuda()
 
     def step():
-        h = hb.HODLR(x, cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, cfg.eps).factor()
-        ld = h.logdet(); s = h.solve(y); info = h.info(); h.close()
+        h = hb.HODLR(x, cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, cfg.eps)
+        s, _ = h.factor_solve(y)
+        ld = h.logdet(); info = h.info(); h.close()
         return ld, info
     ms, (ld, info) = timed(step, reps=3 if cfg.n > (1 << 21) else 5)
     res["configs"][name] = {"n": cfg.n, "ms_per_step": ms, "points_per_s": cfg.n / (ms * 1e-3), "logdet": ld,
@@ -42,11 +43,14 @@ cfg = inputs.CONFIGS["cfg4"]
 ell, s2 = inputs.sweep_settings(cfg)
 x = torch.from_numpy(inputs.points(cfg)).cuda(); y = torch.from_numpy(inputs.rhs(cfg)).cuda()
 th = np.stack([np.full(cfg.sweep, cfg.a), ell], 1)
-hb.gp_loglik_sweep(x, y, cfg.kernel, th, s2, cfg.leaf, cfg.eps, workers=4)
-torch.cuda.synchronize(); t0 = time.perf_counter()
-v = hb.gp_loglik_sweep(x, y, cfg.kernel, th, s2, cfg.leaf, cfg.eps, workers=4)
-torch.cuda.synchronize(); t = time.perf_counter() - t0
-res["configs"]["cfg4"] = {"n": cfg.n, "settings": cfg.sweep, "ms_per_sweep_wall": 1e3 * t,
+sw = {}
+for workers in (1, 4, 8, 16):
+    hb.gp_loglik_sweep(x, y, cfg.kernel, th, s2, cfg.leaf, cfg.eps, workers=workers)
+    torch.cuda.synchronize(); t0 = time.perf_counter()
+    v = hb.gp_loglik_sweep(x, y, cfg.kernel, th, s2, cfg.leaf, cfg.eps, workers=workers)
+    torch.cuda.synchronize(); sw[workers] = 1e3 * (time.perf_counter() - t0)
+t = min(sw.values()) / 1e3
+res["configs"]["cfg4"] = {"n": cfg.n, "settings": cfg.sweep, "ms_per_sweep_wall": 1e3 * t, "by_workers_ms": sw,
                           "settings_per_s": cfg.sweep / t, "loglik_min": float(v.min()), "loglik_max": float(v.max())}
 print("cfg4", json.dumps(res["configs"]["cfg4"]), flush=True)
 cfg = inputs.CONFIGS["cfg3"]
