@@ -86,7 +86,12 @@ typedef struct {
    * a parity difference separated into compression (different ranks) and arithmetic (same ranks).  Read only
    * during hodlr_build. */
   const int32_t *forced_ranks;
-  int64_t reserved[6];
+  /* Heteroscedastic noise (C_ij = sigma_i^2 delta_ij + k(x_i, x_j); NEXT-2 of SURVEY 8(f)): DEVICE
+   * array of n finite values >= 0 in the caller's original point order, or NULL.  The diagonal of C is then
+   * sigma2 + noise[i] (pass sigma2 = 0 for a purely per-point noise).  Read only during hodlr_build (copied, sorted,
+   * into the handle).  HODLR_EINVAL on a negative or non-finite entry. */
+  const double *noise;
+  int64_t reserved[5];
 } hodlr_opts;
 
 typedef struct {

@@ -174,6 +174,7 @@ int oracle_aca_dense(const double *A, int64_t m1, int64_t m2, int64_t lda, doubl
 /* ------------------------------------------------------------------ */
 struct oracle_hodlr {
   int64_t n; int kern; double theta[3]; double s2; int leaf; double eps; int cap;
+  double *dsort;                    /* heteroscedastic: s2 + noise_i in sorted order (NULL: s2 everywhere) */
   int kappa; int64_t nnodes, ninternal, nleaves;
   double *xs; int64_t *perm;
   int64_t *lo, *hi;                 /* heap order: node (d,i) has id 2^d - 1 + i */
@@ -195,10 +196,10 @@ static double kernel_entry(const void *c, int64_t i, int64_t j) {
   return oracle_kernel(b->h->kern, b->h->theta, d);     /* off-diagonal: no noise term */
 }
 
-/* O3: C_ij = k(xs_i, xs_j) + s2 [i = j], sorted indices. */
+/* O3: C_ij = k(xs_i, xs_j) + sigma_i^2 [i = j], sorted indices; sigma_i^2 = s2 (+ noise_i). */
 static double entry_C(const oracle_hodlr *h, int64_t i, int64_t j) {
   double v = oracle_kernel(h->kern, h->theta, h->xs[i] - h->xs[j]);
-  if (i == j) v += h->s2;
+  if (i == j) v += h->dsort ? h->dsort[i] : h->s2;
   return v;
 }
 
@@ -220,7 +221,7 @@ static void merge_sort_idx(int64_t *idx, int64_t *tmp, int64_t n, const double *
 
 void oracle_free(oracle_hodlr *h) {
   if (!h) return;
-  free(h->xs); free(h->perm); free(h->lo); free(h->hi);
+  free(h->xs); free(h->perm); free(h->lo); free(h->hi); free(h->dsort);
   if (h->blk) for (int64_t c = 0; c < h->ninternal; c++) lowrank_free(&h->blk[c]);
   free(h->blk); free(h->rdep); free(h->coff); free(h->X); free(h->Xh);
   if (h->Lleaf) for (int64_t l = 0; l < h->nleaves; l++) free(h->Lleaf[l]);
@@ -234,6 +235,11 @@ void oracle_free(oracle_hodlr *h) {
 
 int oracle_build(const double *x, int64_t n, int kernel, const double *theta, double sigma2,
                  int leaf, double eps, int rank_cap, oracle_hodlr **out) {
+  return oracle_build_noise(x, n, kernel, theta, sigma2, NULL, leaf, eps, rank_cap, out);
+}
+
+int oracle_build_noise(const double *x, int64_t n, int kernel, const double *theta, double sigma2, const double *noise,
+                       int leaf, double eps, int rank_cap, oracle_hodlr **out) {
   *out = NULL;
   if (n < 1 || leaf < 1 || !(eps > 0.0 && eps < 1.0) || !(sigma2 >= 0.0) || !theta ||
       !(theta[1] > 0.0) || !(theta[0] >= 0.0) || kernel < 0 || kernel > 5 || (kernel == ORACLE_RQ && !(theta[2] > 0.0)) ||
@@ -242,6 +248,9 @@ int oracle_build(const double *x, int64_t n, int kernel, const double *theta, do
     return fail(ORACLE_EINVAL, "build: invalid argument");
   for (int64_t i = 0; i < n; i++)
     if (!isfinite(x[i])) return fail(ORACLE_EINVAL, "build: non-finite x[%lld]", (long long)i);
+  if (noise)
+    for (int64_t i = 0; i < n; i++)
+      if (!isfinite(noise[i]) || noise[i] < 0.0) return fail(ORACLE_EINVAL, "build: bad noise[%lld]", (long long)i);
   oracle_hodlr *h = calloc(1, sizeof *h);
   if (!h) return fail(ORACLE_ENOMEM, "build: oom");
   h->n = n; h->kern = kernel; h->theta[0] = theta[0]; h->theta[1] = theta[1];
@@ -257,6 +266,11 @@ int oracle_build(const double *x, int64_t n, int kernel, const double *theta, do
   merge_sort_idx(h->perm, tmp, n, key);
   for (int64_t i = 0; i < n; i++) h->xs[i] = key[h->perm[i]];
   free(key); free(tmp);
+  if (noise) {                                       /* sigma_i^2 = s2 + noise_i, carried with its point */
+    h->dsort = malloc(sizeof(double) * (size_t)n);
+    if (!h->dsort) { oracle_free(h); return fail(ORACLE_ENOMEM, "build: oom"); }
+    for (int64_t i = 0; i < n; i++) h->dsort[i] = sigma2 + noise[h->perm[i]];
+  }
   /* O2: kappa = largest integer with leaf * 2^kappa <= n (0 if n <= leaf) */
   int kappa = 0;
   while ((int64_t)leaf << (kappa + 1) <= n && kappa < 62) kappa++;
@@ -715,13 +729,18 @@ int oracle_get_logdet_parts(oracle_hodlr *h, double *leaf_parts, double *node_pa
 /* ------------------------------------------------------------------ */
 int oracle_dense(const double *x, int64_t n, int kernel, const double *theta, double sigma2,
                  const double *y, double *logdet, double *xout) {
+  return oracle_dense_noise(x, n, kernel, theta, sigma2, NULL, y, logdet, xout);
+}
+
+int oracle_dense_noise(const double *x, int64_t n, int kernel, const double *theta, double sigma2, const double *noise,
+                       const double *y, double *logdet, double *xout) {
   if (n < 1 || n > 8192) return fail(ORACLE_EINVAL, "dense: n out of range");
   double *C = malloc(sizeof(double) * (size_t)(n * n));
   if (!C) return fail(ORACLE_ENOMEM, "dense: oom");
   for (int64_t i = 0; i < n; i++)
     for (int64_t j = 0; j < n; j++) {
       double xi = x[i] == 0.0 ? 0.0 : x[i], xj = x[j] == 0.0 ? 0.0 : x[j];
-      C[i * n + j] = oracle_kernel(kernel, theta, xi - xj) + (i == j ? sigma2 : 0.0);
+      C[i * n + j] = oracle_kernel(kernel, theta, xi - xj) + (i == j ? (noise ? sigma2 + noise[i] : sigma2) : 0.0);
     }
   /* right-looking (outer-product) Cholesky on the upper triangle, C = U^T U (U = L^T, row k of U = column k of
    * L): after row k is scaled, its rank-1 update is applied to the whole trailing upper triangle at once -- a

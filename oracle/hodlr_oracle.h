@@ -53,6 +53,10 @@ int oracle_aca_dense(const double *A, int64_t m1, int64_t m2, int64_t lda, doubl
  * rank_cap <= 0 means min(m1, m2) for every block. */
 int oracle_build(const double *x, int64_t n, int kernel, const double *theta, double sigma2,
                  int leaf, double eps, int rank_cap, oracle_hodlr **out);
+/* The same with heteroscedastic noise C_ij = k(x_i, x_j) + (sigma2 + noise_i) [i = j]: noise is
+ * n finite values >= 0 in the caller's order (NULL = homoscedastic). */
+int oracle_build_noise(const double *x, int64_t n, int kernel, const double *theta, double sigma2, const double *noise,
+                       int leaf, double eps, int rank_cap, oracle_hodlr **out);
 /* O5-O8: leaves, panel, sweep, log det ("Factor"). */
 int oracle_factor(oracle_hodlr *h);
 /* O8: log det C (after factor).  -INFINITY if the factorization failed. */
@@ -87,6 +91,8 @@ const char *oracle_last_error(void);
  * Cholesky, log det = 2 sum log L_ii, forward/back solve of one rhs.  n <= 8192. */
 int oracle_dense(const double *x, int64_t n, int kernel, const double *theta, double sigma2,
                  const double *y, double *logdet, double *xout);
+int oracle_dense_noise(const double *x, int64_t n, int kernel, const double *theta, double sigma2, const double *noise,
+                       const double *y, double *logdet, double *xout);
 
 #ifdef __cplusplus
 }

@@ -55,6 +55,8 @@ def _load(twin: bool = False):
         lib.oracle_kernel.argtypes = [I32, P, D]; lib.oracle_kernel.restype = D
         lib.oracle_aca_dense.argtypes = [P, I64, I64, I64, D, I32, P, P, P]; lib.oracle_aca_dense.restype = I32
         lib.oracle_build.argtypes = [P, I64, I32, P, D, I32, D, I32, P]; lib.oracle_build.restype = I32
+        lib.oracle_build_noise.argtypes = [P, I64, I32, P, D, P, I32, D, I32, P]; lib.oracle_build_noise.restype = I32
+        lib.oracle_dense_noise.argtypes = [P, I64, I32, P, D, P, P, P, P]; lib.oracle_dense_noise.restype = I32
         for f in ("oracle_factor",):
             getattr(lib, f).argtypes = [P]; getattr(lib, f).restype = I32
         lib.oracle_logdet.argtypes = [P, P]; lib.oracle_logdet.restype = I32
@@ -103,19 +105,20 @@ def aca_dense(A: np.ndarray, eps: float, cap: int | None = None):
     return U[:k].T.copy(), V[:k].T.copy(), k
 
 
-def dense_check(x, kernel: int, theta, sigma2: float, y=None):
-    """O11: dense Cholesky log det (+ solve).  Returns (logdet, x or None)."""
+def dense_check(x, kernel: int, theta, sigma2: float, y=None, noise=None):
+    """O11: dense Cholesky log det (+ solve).  Returns (logdet, x or None).  noise: heteroscedastic sigma_i^2 - sigma2."""
     lib = _load()
     x = np.ascontiguousarray(x, dtype=np.float64)
+    nz = None if noise is None else np.ascontiguousarray(noise, dtype=np.float64)
     th = np.ascontiguousarray(theta, dtype=np.float64)
     ld = C.c_double(0.0)
     out = None
     if y is not None:
         y = np.ascontiguousarray(y, dtype=np.float64)
         out = np.zeros_like(y)
-    _check(lib, lib.oracle_dense(_ptr(x), x.size, int(kernel), _ptr(th), float(sigma2),
-                                 _ptr(y) if y is not None else None, C.byref(ld),
-                                 _ptr(out) if out is not None else None))
+    _check(lib, lib.oracle_dense_noise(_ptr(x), x.size, int(kernel), _ptr(th), float(sigma2),
+                                       _ptr(nz) if nz is not None else None, _ptr(y) if y is not None else None,
+                                       C.byref(ld), _ptr(out) if out is not None else None))
     return ld.value, out
 
 
@@ -123,7 +126,8 @@ class OracleHODLR:
     """build -> factor -> {logdet, solve, gp_loglik}*, host memory, original point order."""
 
     def __init__(self, x, kernel: int, theta, sigma2: float, leaf: int, eps: float, rank_cap: int = 0,
-                 twin: bool = False):
+                 twin: bool = False, noise=None):
+        """noise: optional heteroscedastic part, C_ii = sigma2 + noise_i."""
         self._lib = _load(twin)
         self.twin = twin
         self.x = np.ascontiguousarray(x, dtype=np.float64)
@@ -131,8 +135,10 @@ class OracleHODLR:
         self.kernel, self.theta = int(kernel), tuple(float(v) for v in theta)
         th = np.ascontiguousarray(theta, dtype=np.float64)
         h = C.c_void_p(0)
-        _check(self._lib, self._lib.oracle_build(_ptr(self.x), self.n, int(kernel), _ptr(th), float(sigma2),
-                                                 int(leaf), float(eps), int(rank_cap), C.byref(h)))
+        self._noise = None if noise is None else np.ascontiguousarray(noise, dtype=np.float64)
+        _check(self._lib, self._lib.oracle_build_noise(_ptr(self.x), self.n, int(kernel), _ptr(th), float(sigma2),
+                                                       _ptr(self._noise) if self._noise is not None else None,
+                                                       int(leaf), float(eps), int(rank_cap), C.byref(h)))
         self._h = h
 
     def __del__(self):

@@ -144,6 +144,16 @@ static void setup_pool(int dev) {
   done_dev = dev;
 }
 
+// sigma_i^2 = s2 + noise[perm[i]] in sorted order (heteroscedastic noise); flags[8] marks a negative / non-finite entry
+__global__ void k_noise_gather(const double *__restrict__ noise, const long long *__restrict__ perm, long long n,
+                               double s2, double *__restrict__ dn, int *flags) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double v = noise[perm[i]];
+  if (!(v >= 0.0) || !isfinite(v)) atomicOr(&flags[8], 1);
+  dn[i] = s2 + v;
+}
+
 static hodlr_status finish(hodlr_s *h, hodlr_status st, double *tsec) {
   cudaError_t e1 = cudaEventRecord(h->ev1, h->st);
   cudaError_t e2 = cudaStreamSynchronize(h->st);
@@ -275,6 +285,7 @@ hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const 
   if ((int)kernel < 0 || (int)kernel > 5) return hodlr_set_error(HODLR_EINVAL, "build: unknown kernel %d", (int)kernel);
   if (kernel == HODLR_RQ && (!(theta[2] > 0.0) || !isfinite(theta[2])))
     return hodlr_set_error(HODLR_EINVAL, "build: rational quadratic alpha = %g <= 0", theta[2]);
+  if (opts && opts->flags != 0) return hodlr_set_error(HODLR_EINVAL, "build: opts.flags must be 0");
   int cap = (opts && opts->rank_cap > 0) ? opts->rank_cap : 48;
   if (cap > ACA_MAXCAP) return hodlr_set_error(HODLR_EINVAL, "build: rank_cap %d > %d", cap, ACA_MAXCAP);
   hodlr_s *h = new (std::nothrow) hodlr_s();
@@ -372,6 +383,17 @@ hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const 
   hodlr_trace("build: sort done (synced)");
   if (st != HODLR_OK) goto fail;
   if (h->x_nonfinite) { st = hodlr_set_error(HODLR_EINVAL, "build: x contains NaN or Inf"); goto fail; }
+  if (opts && opts->noise) {     // heteroscedastic diagonal, carried with its point into sorted order
+    h->d_noise = (double *)hodlr_dalloc(h, sizeof(double) * (size_t)n);
+    if (!h->d_noise) { st = hodlr_set_error(HODLR_ENOMEM, "build: device allocation failed"); goto fail; }
+    k_noise_gather<<<(int)((n + 255) / 256), 256, 0, h->st>>>(opts->noise, h->perm, n, sigma2, h->d_noise, h->dflags);
+    {
+      cudaError_t le = cudaGetLastError();
+      if (le != cudaSuccess) { st = hodlr_cuda_check(le, "launch k_noise_gather"); goto fail; }
+    }
+    h->launches++; hodlr_global_launches++;
+    h->kp.dn = h->d_noise;
+  }
   // The leaf Cholesky factors (part of "Factor", Fig. 6 line 7) do not depend on the compression: they are
   // issued now on a side stream and overlap the ACA; hodlr_factor waits for them.
   st = hodlr_leaf_alloc(h);
@@ -408,11 +430,13 @@ hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const 
     h->chol_done = launched ? 1 : 0;
   }
   {
-    int f5 = 0;
+    int f5 = 0, f8 = 0;
     CK(cudaMemcpyAsync(&f5, h->dflags + 5, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaMemcpyAsync(&f8, h->dflags + 8, sizeof(int), cudaMemcpyDeviceToHost, h->st));
     if (h->ninternal > 0)
       CK(cudaMemcpyAsync(h->h_rank, h->rank, sizeof(int) * h->ninternal, cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
+    if (f8) { st = hodlr_set_error(HODLR_EINVAL, "build: noise contains a negative or non-finite entry"); goto fail; }
     // per-depth max ranks (the panel layout K_e must agree on every rank) and the rank-cap hits
     std::vector<double> loc(kappa + 2, 0.0);
     for (int e = 1; e <= kappa; e++) {
@@ -496,7 +520,7 @@ hodlr_status hodlr_factor_solve(hodlr_t h, const double *y, double *x, double *q
   cudaError_t ce = cudaMemsetAsync(h->dflags + 3, 0, sizeof(int), h->st);
   if (ce != cudaSuccess) st = hodlr_cuda_check(ce, "factor_solve flags");
   if (st == HODLR_OK) st = hodlr_factor_impl(h);
-  if (st == HODLR_OK && x) st = hodlr_solve_impl(h, y, x, false, true);   // down passes only
+  if (st == HODLR_OK && x) st = hodlr_solve_impl(h, y, x, 1, h->n, false, true);   // down passes only
   int f[4] = {0, 0, 0, 0};
   double quad = 0.0;
   if (st == HODLR_OK) {
@@ -578,7 +602,7 @@ hodlr_status hodlr_solve(hodlr_t h, const double *y, double *x, int64_t nrhs, in
   h->launches = 0;
   cudaEventRecord(h->ev0, h->st);
   hodlr_status st = HODLR_OK;
-  for (int64_t j = 0; j < nrhs && st == HODLR_OK; j++) st = hodlr_solve_impl(h, y + j * ld, x + j * ld, false);
+  st = hodlr_solve_impl(h, y, x, nrhs, ld, false);       // up to SOLVE_RMAX columns per launch
   st = finish(h, st, &h->t_solve);
   if (st != HODLR_OK) return st;
   return check_y_flag(h);
@@ -590,7 +614,7 @@ hodlr_status gp_loglik(hodlr_t h, const double *y, double *out_host) {
   if (h->state != 2) return hodlr_set_error(HODLR_ESTATE, "gp_loglik: not factored");
   h->launches = 0;
   cudaEventRecord(h->ev0, h->st);
-  hodlr_status st = hodlr_solve_impl(h, y, nullptr, true);
+  hodlr_status st = hodlr_solve_impl(h, y, nullptr, 1, h->n, true);
   double yCy = 0.0;
   if (st == HODLR_OK) {   // h at the root = y^T C^{-1} y
     double hh[2] = {0.0, 0.0};

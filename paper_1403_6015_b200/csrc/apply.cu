@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(AT) k_apply_leaf_up(ApplyCtx c) {
     const double xi = sx[i];
     double s = 0.0;
     for (int j = 0; j < m; j++) s = fma(kval(c.kp, xi - sx[j]), sv[j], s);
-    c.ys[lo + i] = fma(c.kp.s2, sv[i], s);
+    c.ys[lo + i] = fma(sig2(c.kp, lo + i), sv[i], s);
   }
   // P_l = E_l^T x_l: a warp takes 4 consecutive panel columns at once (lanes over rows, every load of a 128-row
   // chunk issued before the arithmetic), then a transposed butterfly leaves column q0 + j in lanes 8j .. 8j+7

@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(LT) k_leaf_factor(LeafCtx c) {
       while ((i + 1) * (i + 2) / 2 <= p) i++;
       long long j = p - i * (i + 1) / 2;
       double v = kval(c.kp, xl[i] - xl[j]);
-      if (i == j) v += c.kp.s2;
+      if (i == j) v += sig2(c.kp, lo + i);
       L[p] = v;
     }
     __syncthreads();

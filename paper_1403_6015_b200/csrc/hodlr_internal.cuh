@@ -44,7 +44,10 @@ struct KParams {
   double ell, c2, sq;       // ell; SE 2 ell^2 as (2 ell) ell; Matern sqrt(3) / sqrt(5) -- for kval_o
   double rc2, rell;         // 1 / c2, 1 / ell when that reciprocal is exact (a power of two: x / c == x * (1 / c)
                             // bit for bit, and a multiply is far cheaper than a division), else 0
+  const double *dn;         // heteroscedastic noise: sigma_i^2 = s2 + noise_i in SORTED order (device), or NULL
 };
+// the diagonal term sigma_i^2 of sorted point i (C_ij = sigma_i^2 delta_ij + k(x_i, x_j))
+__device__ __forceinline__ double sig2(const KParams &kp, long long i) { return kp.dn ? kp.dn[i] : kp.s2; }
 // x / b for many x and one b: rb = RN(1 / b), q = RN(x rb), then one FMA correction with the exact remainder
 // x - b q (Markstein): the correctly rounded quotient (barring over/underflow) at 3 FP ops instead of a division
 __device__ __forceinline__ double div_by(double x, double b, double rb) {
@@ -232,6 +235,7 @@ struct hodlr_s {
   int *rank;
   int *bdepth;
   int *d_forced;             // hodlr_opts.forced_ranks on the device (test hook), or NULL
+  double *d_noise;           // heteroscedastic sigma_i^2 in sorted order (hodlr_opts.noise), or NULL
   struct TreeCtx *d_treectx; // per-level contexts of the persistent upper-tree launch (factor.cu)
   int *dflags;               // [0] nonfinite x, [1] notpd, [2] notpd node (min), [3] nonfinite y, [4] active big
                              // ACA blocks, [5] rank-cap hits, [6] ACA steps, [7] x not ascending
@@ -243,6 +247,8 @@ struct hodlr_s {
   double logdet;
   // solve workspace
   double *Vpool, *Tvec, *hvec;
+  int solve_cols;            // right-hand sides the solve pools hold (per column: vcol, tcol, hcol doubles)
+  long long vcol, tcol, hcol;
   double *xshard;            // sharded solve: sorted solution rows + allgather send/recv slices
   unsigned long long *stamps;  // HODLR_TRACE phase timestamps
   int bulk_ok, bulk_checked;   // solve leaf staging by bulk copies
@@ -285,7 +291,8 @@ hodlr_status hodlr_apply_impl(hodlr_s *h, const double *x, double *y);
 hodlr_status hodlr_predict_impl(hodlr_s *h, const double *y, const double *xt, long long m, double *mean, double *var);
 hodlr_status hodlr_leaf_chol_mma(hodlr_s *h, cudaStream_t stream, bool *launched);
 hodlr_status hodlr_leaf_alloc(hodlr_s *h);
-hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_only, bool fused = false);
+hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, int64_t nrhs, int64_t ld, bool up_only,
+                              bool fused = false);
 
 static inline int hodlr_depth_of(long long id) { int d = 0; while (id >= ((2LL << d) - 1)) d++; return d; }
 

@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(NTH, 2) k_leaf_chol(LeafMmaCtx c) {
       const int r = lane >> 2, cc = (lane & 3) + 4 * h;
       const int i = 8 * I + r, j = 8 * J + cc;
       double v;
-      if (i < m && j < m) { v = kval_t<SEO>(c.kp, sx[i] - sx[j]); if (i == j) v += c.kp.s2; }
+      if (i < m && j < m) { v = kval_t<SEO>(c.kp, sx[i] - sx[j]); if (i == j) v += sig2(c.kp, lo + i); }
       else v = (i == j) ? 1.0 : 0.0;
       sL[ti * 64 + 32 * h + lane] = v;
     }

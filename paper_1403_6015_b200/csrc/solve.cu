@@ -16,6 +16,7 @@
 // Under subtree sharding the kernel is split at the exchange of the depth-t projections.
 #include "hodlr_internal.cuh"
 #include <cooperative_groups.h>
+#include <type_traits>
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -49,11 +50,13 @@ struct SolveCtx {
   long long tree_scratch;   // doubles of per-warp scratch for the tree-up nodes
   int tree_warps;           // warps per CTA that take tree-up nodes (scratch must fit)
   unsigned long long *stamps;   // HODLR_TRACE: %globaltimer after each phase (block 0), or NULL
+  int R;                    // right-hand sides of this launch (columns r of y / x at r * ldy)
+  long long xdoubles;       // X tile staging (doubles) at the start of the dynamic shared memory
+  long long ldy;
+  long long vcol, tcol, hcol;   // per-column strides of V, Tv and hv
   int aug;                  // the factorization carries a fused right-hand side: B_c / T_c rows have Kf[d] = Kdim[d] + 1
                             // entries with the ancestor columns at offset 1 (column 0 belongs to that right-hand side)
   int fused;                // this solve IS that right-hand side: t_c = T_c[:, 0] from the factorization (no up pass)
-  int bulk;                 // leaf staging by bulk copies (all column segments 16-byte aligned)
-  int stage_e;              // stage the panel E_l in shared memory (else read it from global memory)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -75,31 +78,8 @@ __device__ __forceinline__ void cp16(double *dst, const double *src) {
   unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(sa), "l"(src));
 }
-__device__ __forceinline__ void cp8(double *dst, const double *src) {
-  unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" :: "r"(sa), "l"(src));
-}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N> __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" :: "n"(N)); }
-
-// Bulk asynchronous copies (TMA engine, no tensor map) completing on an mbarrier
-__device__ __forceinline__ unsigned sptr(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(unsigned long long *bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" :: "r"(sptr(bar)));
-  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect(unsigned long long *bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" :: "r"(sptr(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-               :: "r"(sptr(dst)), "l"(src), "r"(bytes), "r"(sptr(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned phase) {
-  asm volatile("{\n .reg .pred p;\n W%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W%=;\n}\n"
-               :: "r"(sptr(bar)), "r"(phase) : "memory");
-}
-__device__ __forceinline__ void fence_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
 __device__ __forceinline__ int leaf_colsrc(const SolveCtx &c, long long id, int q) {
   if (q >= c.K) return -1;
@@ -111,75 +91,14 @@ __device__ __forceinline__ int leaf_colsrc(const SolveCtx &c, long long id, int 
 }
 
 // ---------------------------------------------------------------------------------------------
-// leaf staging: X = L^{-1} tiles, and the panel E_l (K columns x R rows, column-major, zero beyond each
-// ancestor block's rank); one commit group each
+// leaf staging: X = L^{-1} tiles (one commit group); the panel E_l is read from global memory (L2-resident
+// across the right-hand sides of a leaf)
 // ---------------------------------------------------------------------------------------------
 __device__ void issue_x(const SolveCtx &c, long long leaf, double *sX) {
   const double *Xg = c.Lf + leaf * c.lstride;
   const int nx2 = (c.T * (c.T + 1) / 2) * 32;
   for (int p = threadIdx.x; p < nx2; p += LT) cp16(sX + 2 * p, Xg + 2 * p);
   cp_commit();
-}
-
-__device__ void issue_e(const SolveCtx &c, long long leaf, const int *colsrc, double *sE) {
-  const long long id = c.ninternal + leaf, lo = c.lo[id];
-  const int m = (int)(c.hi[id] - lo), R = 8 * c.T;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (((c.ldx | lo) & 1) == 0) {             // warp per column, lanes over 16-byte row pairs
-    for (int q = warp; q < c.K; q += NWL) {
-      const int src = colsrc[q];
-      const double *g = c.Xh + (long long)src * c.ldx + lo;
-      double *dst = sE + q * R;
-      for (int i = 2 * lane; i < R; i += 64) {
-        if (src >= 0 && i + 1 < m) cp16(dst + i, g + i);
-        else { dst[i] = (src >= 0 && i < m) ? g[i] : 0.0; dst[i + 1] = 0.0; }
-      }
-    }
-  } else {
-    for (int q = warp; q < c.K; q += NWL) {
-      const int src = colsrc[q];
-      const double *g = c.Xh + (long long)src * c.ldx + lo;
-      double *dst = sE + q * R;
-      for (int i = lane; i < R; i += 32) { if (src >= 0 && i < m) cp8(dst + i, g + i); else dst[i] = 0.0; }
-    }
-  }
-  cp_commit();
-}
-
-// Bulk variants (every leaf start, leaf size and n even: 16-byte aligned column segments).  Warp 0 issues;
-// the previous readers of the buffer must have passed a barrier.
-__device__ void bulk_x(const SolveCtx &c, long long leaf, double *sX, unsigned long long *bar) {
-  if (threadIdx.x == 0) {
-    const unsigned bytes = (unsigned)((c.T * (c.T + 1) / 2) * 64 * sizeof(double));
-    fence_async();
-    mbar_expect(bar, bytes);
-    bulk_g2s(sX, c.Lf + leaf * c.lstride, bytes, bar);
-  }
-}
-
-__device__ void bulk_e(const SolveCtx &c, long long leaf, const int *colsrc, double *sE, unsigned long long *bar) {
-  if (threadIdx.x >= 32) return;
-  const int lane = threadIdx.x;
-  const long long id = c.ninternal + leaf, lo = c.lo[id];
-  const int m = (int)(c.hi[id] - lo), R = 8 * c.T;
-  int nvalid = 0;
-  for (int q0 = 0; q0 < c.K; q0 += 32) nvalid += __popc(__ballot_sync(0xffffffffu, q0 + lane < c.K && colsrc[q0 + lane] >= 0));
-  if (lane == 0) { fence_async(); mbar_expect(bar, (unsigned)(nvalid * m * sizeof(double))); }
-  __syncwarp();
-  for (int q = lane; q < c.K; q += 32) {
-    const int src = colsrc[q];
-    if (src >= 0) bulk_g2s(sE + q * R, c.Xh + (long long)src * c.ldx + lo, (unsigned)(m * sizeof(double)), bar);
-  }
-}
-
-// zero the padding of E (rows m..R of valid columns, whole columns beyond the ranks): generic stores
-__device__ void zero_e_pad(const SolveCtx &c, long long leaf, const int *colsrc, double *sE) {
-  const long long id = c.ninternal + leaf;
-  const int m = (int)(c.hi[id] - c.lo[id]), R = 8 * c.T;
-  for (int p = threadIdx.x; p < c.K * R; p += LT) {
-    const int q = p / R, i = p - q * R;
-    if (colsrc[q] < 0 || i >= m) sE[p] = 0.0;
-  }
 }
 
 __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
@@ -239,104 +158,83 @@ __device__ void tri_mvt(const double *X, int T, const double *in, double *out, d
 }
 
 constexpr int KMAX_SOLVE = 512;
+#ifndef SOLVE_RMAX
+#define SOLVE_RMAX 32     // right-hand sides per solve launch
+#endif
 #ifndef SOLVE_UPB
 #define SOLVE_UPB 4       // leaf up: panel columns per warp batch (multiple of 4)
 #endif
 #ifndef SOLVE_DNU
 #define SOLVE_DNU 16      // leaf down: panel columns loaded together per lane
-#endif   // ancestor columns per leaf handled by the solve
+#endif
 struct LeafSmem {
   double sb[VMAX], su[VMAX], red[4 * VMAX], sw[KMAX_SOLVE];
-  int colsrc[2][KMAX_SOLVE];
-  unsigned long long barX, barE;
+  int colsrc[KMAX_SOLVE];
 };
 
-// ---------------------------------------------------------------------------------------------
-// leaf up over this CTA's leaves (leaf0 + blockIdx.x + k gridDim.x), X and E issued ahead:
-//   wait X_i -> u = X b, v = X^T u -> issue X_{i+1} -> wait E_i -> g = E^T v, h -> issue E_{i+1}
-// BULK: bulk copies (TMA engine) completing on mbarriers; otherwise per-thread cp.async groups.
-// ---------------------------------------------------------------------------------------------
-// y entries of leaf `leaf` for this thread's row (R <= LT: at most one row per thread), gathered through perm;
-// issued one leaf ahead so the dependent loads (lo/hi -> perm -> y) overlap the current leaf.
-__device__ __forceinline__ double y_fetch(const SolveCtx &c, long long leaf) {
+// y entries of (leaf, column r) for this thread's row (R <= LT: at most one row per thread), gathered through perm;
+// issued one (leaf, column) ahead so the dependent loads (lo/hi -> perm -> y) overlap the current one.
+__device__ __forceinline__ double y_fetch(const SolveCtx &c, long long leaf, int r) {
   const long long id = c.ninternal + leaf, lo = c.lo[id];
   const int m = (int)(c.hi[id] - lo);
-  return (int)threadIdx.x < m ? c.y[c.perm[lo + threadIdx.x]] : 0.0;
+  return (int)threadIdx.x < m ? c.y[r * c.ldy + c.perm[lo + threadIdx.x]] : 0.0;
 }
 
-template <bool BULK>
-__device__ void leaf_up_phase(const SolveCtx &c, double *sX, double *sE, LeafSmem &S, unsigned &phX, unsigned &phE) {
+// ---------------------------------------------------------------------------------------------
+// leaf up over this CTA's leaves (leaf0 + blockIdx.x + k gridDim.x); per leaf X is staged once and reused by every
+// right-hand side r: u = X b_r, v = X^T u, h_r = b_r . v, g_r = E^T v (E from global memory; after the first
+// column of a leaf it is an L2 hit).  The next leaf's X is copied during the last column.
+// ---------------------------------------------------------------------------------------------
+__device__ void leaf_up_phase(const SolveCtx &c, double *sX, LeafSmem &S) {
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int R = 8 * c.T, K = c.K;
+  const int Rr = 8 * c.T, K = c.K;
   long long leaf = c.leaf0 + blockIdx.x;
   const long long end = c.leaf0 + c.nown;
   if (leaf >= end) return;
-  int cur = 0;
-  for (int q = t; q < K; q += LT) S.colsrc[0][q] = leaf_colsrc(c, c.ninternal + leaf, q);
-  __syncthreads();
-  if (BULK) { zero_e_pad(c, leaf, S.colsrc[0], sE); bulk_x(c, leaf, sX, &S.barX); bulk_e(c, leaf, S.colsrc[0], sE, &S.barE); }
-  else { issue_x(c, leaf, sX); if (c.stage_e) issue_e(c, leaf, S.colsrc[0], sE); else cp_commit(); }
-  double ycur = y_fetch(c, leaf);
-  const bool prof = c.stamps && blockIdx.x == 0 && t == 0;
-  unsigned long long pt[6] = {0, 0, 0, 0, 0, 0}, tp = prof ? gtimer() : 0;
-#define SUBPH(k) if (prof) { const unsigned long long tn = gtimer(); pt[k] += tn - tp; tp = tn; }
+  issue_x(c, leaf, sX);
+  double ycur = y_fetch(c, leaf, 0);
   for (; leaf < end; leaf += gridDim.x) {
     const long long nxt = leaf + gridDim.x;
     const long long id = c.ninternal + leaf, lo = c.lo[id];
     const int m = (int)(c.hi[id] - lo);
-    {
-      const double v = ycur;
-      if (nxt < end) ycur = y_fetch(c, nxt);
-      if (t < R) {
-        S.sb[t] = v;
-        if (!isfinite(v)) atomicOr(&c.flags[3], 1);
+    for (int q = t; q < K; q += LT) S.colsrc[q] = leaf_colsrc(c, id, q);
+    for (int r = 0; r < c.R; r++) {
+      {
+        const double v = ycur;
+        if (r + 1 < c.R) ycur = y_fetch(c, leaf, r + 1);
+        else if (nxt < end) ycur = y_fetch(c, nxt, 0);
+        if (t < Rr) {
+          S.sb[t] = v;
+          if (!isfinite(v)) atomicOr(&c.flags[3], 1);
+        }
       }
-    }
-    if (nxt < end) for (int q = t; q < K; q += LT) S.colsrc[cur ^ 1][q] = leaf_colsrc(c, c.ninternal + nxt, q);
-    SUBPH(0)
-    if (BULK) { mbar_wait(&S.barX, phX); phX ^= 1; } else cp_wait<1>();     // X_i
-    __syncthreads();
-    SUBPH(1)
-    tri_mv(sX, c.T, S.sb, S.su, S.red);        // u = X b
-    tri_mvt(sX, c.T, S.su, S.red, nullptr);    // v = X^T u  (into red[0..R))
-    SUBPH(2)
-    if (nxt < end) { if (BULK) bulk_x(c, nxt, sX, &S.barX); else issue_x(c, nxt, sX); }   // X is free
-    else if (!BULK) cp_commit();               // keep the group count uniform
-    double hs = 0.0;
-    for (int i = t; i < m; i += LT) hs += S.sb[i] * S.red[i];
-    hs = warp_sum(hs);
-    if (BULK) { mbar_wait(&S.barE, phE); phE ^= 1; } else cp_wait<1>();     // E_i
-    __syncthreads();
-    SUBPH(3)
-    if (lane == 0) S.red[2 * VMAX + warp] = hs;
-    double *g = c.V + c.dt->nodeV[c.kappa] + leaf * (long long)K;
-    if (c.stage_e) {
-      for (int q = warp; q < K; q += NWL) {    // g = E^T v: warp per column, lanes over rows
-        double s2 = 0.0;
-        const double *e = sE + q * R;
-        for (int i = lane; i < R; i += 32) s2 = fma(e[i], S.red[i], s2);
-        s2 = warp_sum(s2);
-        if (lane == 0) g[q] = s2;
-      }
-    } else {
+      if (r == 0) cp_wait<0>();                // X of this leaf
+      __syncthreads();
+      tri_mv(sX, c.T, S.sb, S.su, S.red);      // u = X b
+      tri_mvt(sX, c.T, S.su, S.red, nullptr);  // v = X^T u  (into red[0..R))
+      if (r + 1 == c.R && nxt < end) issue_x(c, nxt, sX);   // X is free
+      double hs = 0.0;
+      for (int i = t; i < m; i += LT) hs += S.sb[i] * S.red[i];
+      hs = warp_sum(hs);
+      if (lane == 0) S.red[2 * VMAX + warp] = hs;
+      double *g = c.V + r * c.vcol + c.dt->nodeV[c.kappa] + leaf * (long long)K;
       // g = E^T v from global memory: a warp takes 4 consecutive columns at once (all their loads in flight
       // together), lanes over rows; the 4 partial sums are reduced by a transposed butterfly (6 shuffles), after
       // which lanes 8j .. 8j+7 hold column q0 + j
       const int hi4 = lane & 16, hi3 = lane & 8;
       for (int q0 = SOLVE_UPB * warp; q0 < K; q0 += SOLVE_UPB * NWL) {
-        // every load of a row chunk is issued before any arithmetic (predicated loads, no branches)
         constexpr int RU = 4;                  // rows per lane per chunk (128-row chunks)
         double pv[SOLVE_UPB];
         const double *ecol[SOLVE_UPB];
         bool cv[SOLVE_UPB];
 #pragma unroll
         for (int j = 0; j < SOLVE_UPB; j++) {
-          const int src = q0 + j < K ? S.colsrc[cur][q0 + j] : -1;
+          const int src = q0 + j < K ? S.colsrc[q0 + j] : -1;
           cv[j] = src >= 0;
           ecol[j] = c.Xh + (long long)(src >= 0 ? src : 0) * c.ldx + lo;
           pv[j] = 0.0;
         }
-        for (int r0 = 0; r0 < R; r0 += 32 * RU) {
+        for (int r0 = 0; r0 < Rr; r0 += 32 * RU) {
           double ev[SOLVE_UPB][RU];
 #pragma unroll
           for (int j = 0; j < SOLVE_UPB; j++)
@@ -369,85 +267,60 @@ __device__ void leaf_up_phase(const SolveCtx &c, double *sX, double *sE, LeafSme
           if ((lane & 7) == 0 && q0 + j < K) g[q0 + j] = kk;
         }
       }
+      __syncthreads();
+      if (t == 0) {
+        double h = 0.0;
+        for (int w = 0; w < NWL; w++) h += S.red[2 * VMAX + w];
+        double *hv = c.hv + r * c.hcol;
+        hv[2 * id] = h; hv[2 * id + 1] = 0.0;
+      }
     }
-    __syncthreads();
-    SUBPH(4)
-    if (t == 0) {
-      double h = 0.0;
-      for (int w = 0; w < NWL; w++) h += S.red[2 * VMAX + w];
-      c.hv[2 * id] = h; c.hv[2 * id + 1] = 0.0;
-    }
-    if (nxt < end && (BULK || c.stage_e)) {
-      if (BULK) { zero_e_pad(c, nxt, S.colsrc[cur ^ 1], sE); bulk_e(c, nxt, S.colsrc[cur ^ 1], sE, &S.barE); }
-      else issue_e(c, nxt, S.colsrc[cur ^ 1], sE);
-    } else if (!BULK) cp_commit();
-    cur ^= 1;
-    SUBPH(5)
   }
-#undef SUBPH
-  if (prof) for (int k = 0; k < 6; k++) c.stamps[64 + k] = pt[k];
-  if (!BULK) cp_wait<0>();
+  cp_wait<0>();
   __syncthreads();
 }
 
-// leaf down: x_l = A_l^{-1} (b_l + E_l w_l):  wait E_i -> b + E w -> issue E_{i+1} -> wait X_i -> u, x -> issue X_{i+1}
-template <bool BULK>
-__device__ void leaf_down_phase(const SolveCtx &c, double *sX, double *sE, LeafSmem &S, unsigned &phX, unsigned &phE) {
+// leaf down: x_l = A_l^{-1} (b_l + E_l w_l) for every right-hand side r; X staged once per leaf
+__device__ void leaf_down_phase(const SolveCtx &c, double *sX, LeafSmem &S) {
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int R = 8 * c.T, K = c.K;
+  const int Rr = 8 * c.T, K = c.K;
   long long leaf = c.leaf0 + blockIdx.x;
   const long long end = c.leaf0 + c.nown;
   if (leaf >= end) return;
-  int cur = 0;
-  for (int q = t; q < K; q += LT) S.colsrc[0][q] = leaf_colsrc(c, c.ninternal + leaf, q);
-  __syncthreads();
-  if (BULK) { zero_e_pad(c, leaf, S.colsrc[0], sE); bulk_e(c, leaf, S.colsrc[0], sE, &S.barE); bulk_x(c, leaf, sX, &S.barX); }
-  else { if (c.stage_e) issue_e(c, leaf, S.colsrc[0], sE); else cp_commit(); issue_x(c, leaf, sX); }
-  double ycur = y_fetch(c, leaf);
+  issue_x(c, leaf, sX);
+  double ycur = y_fetch(c, leaf, 0);
   static_assert(KMAX_SOLVE <= 2 * LT, "w prefetch: two columns per thread");
   const double *wbase = c.V + c.dt->nodeV[c.kappa];
   double w0 = t < K ? wbase[leaf * (long long)K + t] : 0.0, w1 = t + LT < K ? wbase[leaf * (long long)K + t + LT] : 0.0;
-  const bool prof = c.stamps && blockIdx.x == 0 && t == 0;
-  unsigned long long pt[6] = {0, 0, 0, 0, 0, 0}, tp = prof ? gtimer() : 0;
-#define SUBPH(k) if (prof) { const unsigned long long tn = gtimer(); pt[k] += tn - tp; tp = tn; }
   for (; leaf < end; leaf += gridDim.x) {
     const long long nxt = leaf + gridDim.x;
     const long long id = c.ninternal + leaf, lo = c.lo[id];
     const int m = (int)(c.hi[id] - lo);
-    if (t < K) S.sw[t] = w0;                   // w of this leaf (fetched one leaf ahead)
-    if (t + LT < K) S.sw[t + LT] = w1;
-    if (nxt < end) {
-      w0 = t < K ? wbase[nxt * (long long)K + t] : 0.0;
-      w1 = t + LT < K ? wbase[nxt * (long long)K + t + LT] : 0.0;
-    }
-    {
-      const double v = ycur;
-      if (nxt < end) ycur = y_fetch(c, nxt);
-      if (t < R) S.sb[t] = v;
-    }
-    if (nxt < end) for (int q = t; q < K; q += LT) S.colsrc[cur ^ 1][q] = leaf_colsrc(c, c.ninternal + nxt, q);
-    SUBPH(0)
-    if (BULK) { mbar_wait(&S.barE, phE); phE ^= 1; } else cp_wait<1>();     // E_i
-    __syncthreads();
-    SUBPH(1)
-    if (c.stage_e) {
-      for (int w4 = t; w4 < 4 * R; w4 += LT) { // b + E w: 4 threads per row (quarters of the columns)
-        const int i = w4 % R, h = w4 / R;
-        const int q0 = (K * h) / 4, q1 = (K * (h + 1)) / 4;
-        double s2 = 0.0;
-        for (int q = q0; q < q1; q++) s2 = fma(sE[q * R + i], S.sw[q], s2);
-        S.red[w4] = s2;
+    for (int q = t; q < K; q += LT) S.colsrc[q] = leaf_colsrc(c, id, q);
+    for (int r = 0; r < c.R; r++) {
+      __syncthreads();                         // previous column's users of sw / sb / colsrc are done
+      if (t < K) S.sw[t] = w0;                 // w of this (leaf, column), fetched one ahead
+      if (t + LT < K) S.sw[t + LT] = w1;
+      {
+        const long long nl = r + 1 < c.R ? leaf : nxt;
+        const int nr = r + 1 < c.R ? r + 1 : 0;
+        if (nl < end) {
+          const double *wb = wbase + nr * c.vcol + nl * (long long)K;
+          w0 = t < K ? wb[t] : 0.0;
+          w1 = t + LT < K ? wb[t + LT] : 0.0;
+        }
+        const double v = ycur;
+        if (nl < end) ycur = y_fetch(c, nl, nr);
+        if (t < Rr) S.sb[t] = v;
       }
       __syncthreads();
-      for (int i = t; i < R; i += LT) S.sb[i] += (S.red[i] + S.red[R + i]) + (S.red[2 * R + i] + S.red[3 * R + i]);
-    } else {
       // b + E w from global memory: warp w takes row group w % RG (one row per lane) and column split w / RG;
-      // 8 columns' loads in flight per lane; the CS column-split partials are summed in a fixed order
-      const int RG = (R + 31) / 32, CS = NWL / RG;
+      // SOLVE_DNU columns' loads in flight per lane; the CS column-split partials are summed in a fixed order
+      const int RG = (Rr + 31) / 32, CS = NWL / RG;
       const int rg = warp % RG, cs = warp / RG;
       const int i = 32 * rg + lane;
-      double s2 = 0.0;
       if (cs < CS) {
+        double s2 = 0.0;
         const int q0 = (K * cs) / CS, q1 = (K * (cs + 1)) / CS;
         const double *ebase = c.Xh + lo + i;
         int q = q0;
@@ -455,46 +328,232 @@ __device__ void leaf_down_phase(const SolveCtx &c, double *sX, double *sE, LeafS
           double ev[SOLVE_DNU];
 #pragma unroll
           for (int j = 0; j < SOLVE_DNU; j++) {
-            const int src = S.colsrc[cur][q + j];
+            const int src = S.colsrc[q + j];
             ev[j] = (src >= 0 && i < m) ? __ldg(ebase + (long long)src * c.ldx) : 0.0;
           }
 #pragma unroll
           for (int j = 0; j < SOLVE_DNU; j++) s2 = fma(ev[j], S.sw[q + j], s2);
         }
         for (; q < q1; q++) {
-          const int src = S.colsrc[cur][q];
+          const int src = S.colsrc[q];
           if (src >= 0 && i < m) s2 = fma(__ldg(ebase + (long long)src * c.ldx), S.sw[q], s2);
         }
-        S.red[cs * R + i] = s2;
+        S.red[cs * Rr + i] = s2;
       }
       __syncthreads();
-      for (int r = t; r < R; r += LT) {
+      for (int rr = t; rr < Rr; rr += LT) {
         double acc = 0.0;
-        for (int k2 = 0; k2 < CS; k2++) acc += S.red[k2 * R + r];
-        S.sb[r] += acc;
+        for (int k2 = 0; k2 < CS; k2++) acc += S.red[k2 * Rr + rr];
+        S.sb[rr] += acc;
+      }
+      if (r == 0) cp_wait<0>();                // X of this leaf
+      __syncthreads();
+      tri_mv(sX, c.T, S.sb, S.su, S.red);
+      tri_mvt(sX, c.T, S.su, S.sb, S.red);
+      if (r + 1 == c.R && nxt < end) issue_x(c, nxt, sX);
+      if (c.xsorted) for (int i2 = t; i2 < m; i2 += LT) c.xsorted[lo + i2] = S.sb[i2];
+      else for (int i2 = t; i2 < m; i2 += LT) c.x[r * c.ldy + c.perm[lo + i2]] = S.sb[i2];
+    }
+  }
+  cp_wait<0>();
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------------------------
+// Eight right-hand sides at a time (the batched kernel k_solve<8>): every DMMA m8n8k4 then carries 8 different
+// vectors in its B operand instead of one replicated vector, the panel products E^T V and E W become 8-column
+// DMMA products, and X and E_l are read once per leaf for all columns.  Rows beyond the leaf are zero.
+// ---------------------------------------------------------------------------------------------
+constexpr int VP = VMAX + 4;            // row stride of the 8-column vectors (bank padding)
+struct LeafSmem8 {
+  double b[8][VP], u[8][VP];
+  union { double v[8][VP]; double w[8][KMAX_SOLVE + 4]; };
+  int colsrc[KMAX_SOLVE];
+  double hred[8];
+};
+
+// out_c = X in_c for the 8 columns c (warp I owns tile row I; C fragment: column 2tq, 2tq+1, row 8I + g)
+__device__ void tri_mv8(const double *X, int T, const double (*in)[VP], double (*out)[VP]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, tq = lane & 3;
+  for (int I = warp; I < T; I += NWL) {
+    double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+    int k = 0;
+    for (; k + 1 <= I; k += 2) {
+      const double *t0 = X + tix(I, k) * 64, *t1 = X + tix(I, k + 1) * 64;
+      dmma(c0, c1, t0[lane], in[g][8 * k + tq]);
+      dmma(e0, e1, t1[lane], in[g][8 * k + 8 + tq]);
+      dmma(c0, c1, t0[32 + lane], in[g][8 * k + 4 + tq]);
+      dmma(e0, e1, t1[32 + lane], in[g][8 * k + 12 + tq]);
+    }
+    if (k <= I) {
+      const double *t0 = X + tix(I, k) * 64;
+      dmma(c0, c1, t0[lane], in[g][8 * k + tq]);
+      dmma(c0, c1, t0[32 + lane], in[g][8 * k + 4 + tq]);
+    }
+    out[2 * tq][8 * I + g] = c0 + e0;
+    out[2 * tq + 1][8 * I + g] = c1 + e1;
+  }
+  __syncthreads();
+}
+
+// out_c = X^T in_c (warp J owns tile column J)
+__device__ void tri_mvt8(const double *X, int T, const double (*in)[VP], double (*out)[VP]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, tq = lane & 3;
+  const int a0 = fo(tq, g), a1 = fo(tq + 4, g);
+  for (int J = warp; J < T; J += NWL) {
+    double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+    int I = J;
+    for (; I + 1 < T; I += 2) {
+      const double *t0 = X + tix(I, J) * 64, *t1 = X + tix(I + 1, J) * 64;
+      dmma(c0, c1, t0[a0], in[g][8 * I + tq]);
+      dmma(e0, e1, t1[a0], in[g][8 * I + 8 + tq]);
+      dmma(c0, c1, t0[a1], in[g][8 * I + 4 + tq]);
+      dmma(e0, e1, t1[a1], in[g][8 * I + 12 + tq]);
+    }
+    if (I < T) {
+      const double *t0 = X + tix(I, J) * 64;
+      dmma(c0, c1, t0[a0], in[g][8 * I + tq]);
+      dmma(c0, c1, t0[a1], in[g][8 * I + 4 + tq]);
+    }
+    out[2 * tq][8 * J + g] = c0 + e0;
+    out[2 * tq + 1][8 * J + g] = c1 + e1;
+  }
+  __syncthreads();
+}
+
+// b[c][i] = y of column r0 + c (c < nr) at sorted row lo + i, zero elsewhere
+__device__ void load_b8(const SolveCtx &c, long long lo, int m, int r0, int nr, double (*b)[VP]) {
+  const int Rr = 8 * c.T;
+  for (int p = threadIdx.x; p < 8 * Rr; p += LT) {
+    const int cc = p / Rr, i = p - cc * Rr;
+    double v = 0.0;
+    if (cc < nr && i < m) {
+      v = c.y[(r0 + cc) * c.ldy + c.perm[lo + i]];
+      if (!isfinite(v)) atomicOr(&c.flags[3], 1);
+    }
+    b[cc][i] = v;
+  }
+}
+
+__device__ void leaf_up_phase8(const SolveCtx &c, double *sX, LeafSmem8 &S) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, g = lane >> 2, tq = lane & 3;
+  const int K = c.K;
+  long long leaf = c.leaf0 + blockIdx.x;
+  const long long end = c.leaf0 + c.nown;
+  if (leaf >= end) return;
+  issue_x(c, leaf, sX);
+  for (; leaf < end; leaf += gridDim.x) {
+    const long long nxt = leaf + gridDim.x;
+    const long long id = c.ninternal + leaf, lo = c.lo[id];
+    const int m = (int)(c.hi[id] - lo);
+    for (int q = t; q < K; q += LT) S.colsrc[q] = leaf_colsrc(c, id, q);
+    for (int r0 = 0; r0 < c.R; r0 += 8) {
+      const int nr = min(8, c.R - r0);
+      load_b8(c, lo, m, r0, nr, S.b);
+      if (r0 == 0) cp_wait<0>();
+      __syncthreads();
+      tri_mv8(sX, c.T, S.b, S.u);               // u = X b
+      tri_mvt8(sX, c.T, S.u, S.v);              // v = X^T u
+      if (r0 + 8 >= c.R && nxt < end) issue_x(c, nxt, sX);   // X is free
+      {                                          // h_c = b_c . v_c: warp c
+        double hs = 0.0;
+        for (int i = lane; i < m; i += 32) hs = fma(S.b[warp][i], S.v[warp][i], hs);
+        hs = warp_sum(hs);
+        if (lane == 0 && warp < nr) {
+          double *hv = c.hv + (r0 + warp) * c.hcol;
+          hv[2 * id] = hs; hv[2 * id + 1] = 0.0;
+        }
+      }
+      // G (8 x K) = V^T E: warp takes 8 panel columns q0 .. q0+7 at a time; A = V^T (row c, col = leaf row),
+      // B = E (row = leaf row, col = panel column), both k = 4 leaf rows per DMMA
+      for (int q0 = 8 * warp; q0 < K; q0 += 8 * NWL) {
+        const int src = q0 + g < K ? S.colsrc[q0 + g] : -1;
+        const double *ecol = c.Xh + (long long)(src >= 0 ? src : 0) * c.ldx + lo;
+        double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+        for (int kb = 0; kb < m; kb += 32) {       // 8 DMMA steps (32 rows) per batch, loads first
+          double ev[8];
+#pragma unroll
+          for (int u = 0; u < 8; u++) {
+            const int i = kb + 4 * u + tq;
+            ev[u] = (src >= 0 && i < m) ? __ldg(ecol + i) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; u += 2) {
+            dmma(c0, c1, S.v[g][kb + 4 * u + tq], ev[u]);
+            dmma(e0, e1, S.v[g][kb + 4 * u + 4 + tq], ev[u + 1]);
+          }
+        }
+        // C[c = g][q0 + 2tq (+1)]
+        if (g < nr) {
+          double *gp = c.V + (r0 + g) * c.vcol + c.dt->nodeV[c.kappa] + leaf * (long long)K;
+          if (q0 + 2 * tq < K) gp[q0 + 2 * tq] = c0 + e0;
+          if (q0 + 2 * tq + 1 < K) gp[q0 + 2 * tq + 1] = c1 + e1;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  cp_wait<0>();
+  __syncthreads();
+}
+
+__device__ void leaf_down_phase8(const SolveCtx &c, double *sX, LeafSmem8 &S) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, g = lane >> 2, tq = lane & 3;
+  const int K = c.K, T = c.T;
+  long long leaf = c.leaf0 + blockIdx.x;
+  const long long end = c.leaf0 + c.nown;
+  if (leaf >= end) return;
+  issue_x(c, leaf, sX);
+  const double *wbase = c.V + c.dt->nodeV[c.kappa];
+  for (; leaf < end; leaf += gridDim.x) {
+    const long long nxt = leaf + gridDim.x;
+    const long long id = c.ninternal + leaf, lo = c.lo[id];
+    const int m = (int)(c.hi[id] - lo);
+    for (int q = t; q < K; q += LT) S.colsrc[q] = leaf_colsrc(c, id, q);
+    for (int r0 = 0; r0 < c.R; r0 += 8) {
+      const int nr = min(8, c.R - r0);
+      __syncthreads();
+      load_b8(c, lo, m, r0, nr, S.b);
+      for (int p = t; p < 8 * K; p += LT) {      // w of the 8 columns (zero for c >= nr)
+        const int cc = p / K, q = p - cc * K;
+        S.w[cc][q] = cc < nr ? wbase[(r0 + cc) * c.vcol + leaf * (long long)K + q] : 0.0;
+      }
+      for (int p = t; p < 8 * 4; p += LT) S.w[p >> 2][K + (p & 3)] = 0.0;   // (k padding of the last DMMA step)
+      __syncthreads();
+      // b += E W: warp takes tile rows I (8 leaf rows), A = E (row 8I + g, col = panel column), B = W
+      for (int I = warp; I < T; I += NWL) {
+        const int i = 8 * I + g;
+        double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+        for (int q0 = 0; q0 < K; q0 += 16) {
+          double ev[4];
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            const int q = q0 + 4 * u + tq;
+            const int src = q < K ? S.colsrc[q] : -1;
+            ev[u] = (src >= 0 && i < m) ? __ldg(c.Xh + (long long)src * c.ldx + lo + i) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; u += 2) {
+            const int qa = q0 + 4 * u + tq, qb = qa + 4;
+            dmma(c0, c1, ev[u], qa < K ? S.w[g][qa] : 0.0);
+            dmma(e0, e1, ev[u + 1], qb < K ? S.w[g][qb] : 0.0);
+          }
+        }
+        S.b[2 * tq][i] += c0 + e0;
+        S.b[2 * tq + 1][i] += c1 + e1;
+      }
+      if (r0 == 0) cp_wait<0>();
+      __syncthreads();
+      tri_mv8(sX, T, S.b, S.u);
+      tri_mvt8(sX, T, S.u, S.b);
+      if (r0 + 8 >= c.R && nxt < end) issue_x(c, nxt, sX);
+      for (int p = t; p < 8 * m; p += LT) {
+        const int cc = p / m, i = p - cc * m;
+        if (cc < nr) c.x[(r0 + cc) * c.ldy + c.perm[lo + i]] = S.b[cc][i];
       }
     }
-    if (nxt < end && (BULK || c.stage_e)) {    // E is free (barrier above)
-      if (BULK) { zero_e_pad(c, nxt, S.colsrc[cur ^ 1], sE); bulk_e(c, nxt, S.colsrc[cur ^ 1], sE, &S.barE); }
-      else issue_e(c, nxt, S.colsrc[cur ^ 1], sE);
-    } else if (!BULK) cp_commit();
-    SUBPH(2)
-    if (BULK) { mbar_wait(&S.barX, phX); phX ^= 1; } else cp_wait<1>();     // X_i
-    __syncthreads();
-    SUBPH(3)
-    tri_mv(sX, c.T, S.sb, S.su, S.red);
-    tri_mvt(sX, c.T, S.su, S.sb, S.red);
-    SUBPH(4)
-    if (nxt < end) { if (BULK) bulk_x(c, nxt, sX, &S.barX); else issue_x(c, nxt, sX); }
-    else if (!BULK) cp_commit();
-    if (c.xsorted) for (int i = t; i < m; i += LT) c.xsorted[lo + i] = S.sb[i];
-    else for (int i = t; i < m; i += LT) c.x[c.perm[lo + i]] = S.sb[i];
-    cur ^= 1;
-    SUBPH(5)
   }
-#undef SUBPH
-  if (prof) for (int k = 0; k < 6; k++) c.stamps[70 + k] = pt[k];
-  if (!BULK) cp_wait<0>();
+  cp_wait<0>();
   __syncthreads();
 }
 
@@ -527,11 +586,12 @@ __device__ void dd_solve_warp(const double *S0, const double *Si, int q, const d
   }
 }
 
-__device__ void tree_up_node(const SolveCtx &c, int d, long long i, double *scr, int lane) {
+__device__ void tree_up_node(const SolveCtx &c, int d, long long i, int col, double *scr, int lane) {
   const long long node = (1LL << d) - 1 + i;
+  double *const V = c.V + col * c.vcol, *const Tvc = c.Tv + col * c.tcol, *const hv = c.hv + col * c.hcol;
   const int r = c.dt->rdep[d + 1], q = 2 * r, Kd = c.dt->Kdim[d], K1 = c.dt->Kdim[d + 1];
   const int ldb = c.dt->Kf[d];               // B_c row stride (ancestor columns at offset c.aug)
-  const double *g1 = c.V + c.dt->nodeV[d + 1] + (2 * i) * (long long)K1;
+  const double *g1 = V + c.dt->nodeV[d + 1] + (2 * i) * (long long)K1;
   const double *g2 = g1 + K1;
   const double *Sg = c.Spool + c.dt->nodeS[d] + i * (long long)(2 * q * q + q);
   const double *B = c.BTpool + c.dt->nodeBT[d] + i * 3LL * q * ldb + c.aug;
@@ -549,17 +609,17 @@ __device__ void tree_up_node(const SolveCtx &c, int d, long long i, double *scr,
   for (int u = lane; u < r; u += 32) { rhs[u] = g2[Kd + u]; rhs[r + u] = g1[Kd + u]; }
   __syncwarp();
   dd_solve_warp(S0, Si, q, rhs, th, tl, tmp, lane);
-  double *tg = c.Tv + c.dt->nodeT[d] + i * 2LL * q;
+  double *tg = Tvc + c.dt->nodeT[d] + i * 2LL * q;
   for (int u = lane; u < q; u += 32) { tg[u] = th[u]; tg[q + u] = tl[u]; }
   if (lane == 0) {
-    Acc2 A = acc2(c.hv[2 * (2 * node + 1)]);
-    acc_add_dd(A, c.hv[2 * (2 * node + 2)], c.hv[2 * (2 * node + 2) + 1]);
-    A.c += c.hv[2 * (2 * node + 1) + 1];
+    Acc2 A = acc2(hv[2 * (2 * node + 1)]);
+    acc_add_dd(A, hv[2 * (2 * node + 2)], hv[2 * (2 * node + 2) + 1]);
+    A.c += hv[2 * (2 * node + 1) + 1];
     for (int u = 0; u < r; u++) acc_fma_dd(A, -g1[Kd + u], th[u], tl[u]);
     for (int u = 0; u < r; u++) acc_fma_dd(A, -g2[Kd + u], th[r + u], tl[r + u]);
-    acc_dd(A, c.hv[2 * node], c.hv[2 * node + 1]);
+    acc_dd(A, hv[2 * node], hv[2 * node + 1]);
   }
-  double *gc = c.V + c.dt->nodeV[d] + i * (long long)Kd;
+  double *gc = V + c.dt->nodeV[d] + i * (long long)Kd;
   // 4 entries a per lane at once (a = a0 + 32 x): the B loads of all four are independent and issued together
   for (int a0 = lane; a0 < Kd; a0 += 128) {
     Acc2 A[4];
@@ -587,12 +647,13 @@ __device__ void tree_up_node(const SolveCtx &c, int d, long long i, double *scr,
 
 // Same as tree_up_node with the whole CTA on one node (levels with few nodes): every thread stages, warp 0
 // solves, all threads form g_c; the arithmetic and its order per output are identical.
-__device__ void tree_up_node_cta(const SolveCtx &c, int d, long long i, double *scr) {
+__device__ void tree_up_node_cta(const SolveCtx &c, int d, long long i, int col, double *scr) {
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const long long node = (1LL << d) - 1 + i;
+  double *const V = c.V + col * c.vcol, *const Tvc = c.Tv + col * c.tcol, *const hv = c.hv + col * c.hcol;
   const int r = c.dt->rdep[d + 1], q = 2 * r, Kd = c.dt->Kdim[d], K1 = c.dt->Kdim[d + 1];
   const int ldb = c.dt->Kf[d];
-  const double *g1 = c.V + c.dt->nodeV[d + 1] + (2 * i) * (long long)K1;
+  const double *g1 = V + c.dt->nodeV[d + 1] + (2 * i) * (long long)K1;
   const double *g2 = g1 + K1;
   const double *Sg = c.Spool + c.dt->nodeS[d] + i * (long long)(2 * q * q + q);
   const double *B = c.BTpool + c.dt->nodeBT[d] + i * 3LL * q * ldb + c.aug;
@@ -603,19 +664,19 @@ __device__ void tree_up_node_cta(const SolveCtx &c, int d, long long i, double *
   __syncthreads();
   if (warp == 0) {
     dd_solve_warp(S0, Si, q, rhs, th, tl, tmp, lane);
-    double *tg = c.Tv + c.dt->nodeT[d] + i * 2LL * q;
+    double *tg = Tvc + c.dt->nodeT[d] + i * 2LL * q;
     for (int u = lane; u < q; u += 32) { tg[u] = th[u]; tg[q + u] = tl[u]; }
     if (lane == 0) {
-      Acc2 A = acc2(c.hv[2 * (2 * node + 1)]);
-      acc_add_dd(A, c.hv[2 * (2 * node + 2)], c.hv[2 * (2 * node + 2) + 1]);
-      A.c += c.hv[2 * (2 * node + 1) + 1];
+      Acc2 A = acc2(hv[2 * (2 * node + 1)]);
+      acc_add_dd(A, hv[2 * (2 * node + 2)], hv[2 * (2 * node + 2) + 1]);
+      A.c += hv[2 * (2 * node + 1) + 1];
       for (int u = 0; u < r; u++) acc_fma_dd(A, -g1[Kd + u], th[u], tl[u]);
       for (int u = 0; u < r; u++) acc_fma_dd(A, -g2[Kd + u], th[r + u], tl[r + u]);
-      acc_dd(A, c.hv[2 * node], c.hv[2 * node + 1]);
+      acc_dd(A, hv[2 * node], hv[2 * node + 1]);
     }
   }
   __syncthreads();
-  double *gc = c.V + c.dt->nodeV[d] + i * (long long)Kd;
+  double *gc = V + c.dt->nodeV[d] + i * (long long)Kd;
   for (int a = t; a < Kd; a += LT) {
     Acc2 A = acc2(g1[a]);
     acc_add(A, g2[a]);
@@ -635,15 +696,16 @@ __device__ __forceinline__ void t_of(const SolveCtx &c, const double *tg, const 
   else { hi = tg[u]; lo = tg[q + u]; }
 }
 
-__device__ void tree_down_node(const SolveCtx &c, int d, long long i, int lane) {
+__device__ void tree_down_node(const SolveCtx &c, int d, long long i, int col, int lane) {
+  double *const V = c.V + col * c.vcol, *const Tvc = c.Tv + col * c.tcol;
   const int r = c.dt->rdep[d + 1], q = 2 * r, Kd = c.dt->Kdim[d], K1 = c.dt->Kdim[d + 1];
   const int ldb = c.dt->Kf[d];
-  const double *wc = c.V + c.dt->nodeV[d] + i * (long long)Kd;
+  const double *wc = V + c.dt->nodeV[d] + i * (long long)Kd;
   const long long qK = (long long)q * ldb;
   const double *Th = c.BTpool + c.dt->nodeBT[d] + i * 3LL * qK + qK + c.aug;    // ancestor columns of T_c
   const double *Tl = Th + qK;
-  const double *tg = c.Tv + c.dt->nodeT[d] + i * 2LL * q;
-  double *w1 = c.V + c.dt->nodeV[d + 1] + (2 * i) * (long long)K1;
+  const double *tg = Tvc + c.dt->nodeT[d] + i * 2LL * q;
+  double *w1 = V + c.dt->nodeV[d + 1] + (2 * i) * (long long)K1;
   double *w2 = w1 + K1;
   int parts = 1;
   while (parts * 2 * q <= 32 && parts < 16) parts *= 2;
@@ -679,15 +741,16 @@ __device__ void tree_down_node(const SolveCtx &c, int d, long long i, int lane) 
 // w_c2 = [w_c; -f_u (u >= r)].  One warp takes the rows u = u0, u0 + ustep, ... in batches of 4 with the lanes over
 // a (all loads of a batch in flight together, then a 5-round dd butterfly per row).  Warp per node (u0 = 0,
 // ustep = 1) or, for levels with few nodes, a CTA per node (u0 = warp, ustep = warps).
-__device__ void tree_down_rows(const SolveCtx &c, int d, long long i, int lane, int u0, int ustep, bool copy_w) {
+__device__ void tree_down_rows(const SolveCtx &c, int d, long long i, int col, int lane, int u0, int ustep, bool copy_w) {
+  double *const V = c.V + col * c.vcol, *const Tvc = c.Tv + col * c.tcol;
   const int r = c.dt->rdep[d + 1], q = 2 * r, Kd = c.dt->Kdim[d], K1 = c.dt->Kdim[d + 1];
   const int ldb = c.dt->Kf[d];
-  const double *wc = c.V + c.dt->nodeV[d] + i * (long long)Kd;
+  const double *wc = V + c.dt->nodeV[d] + i * (long long)Kd;
   const long long qK = (long long)q * ldb;
   const double *Th = c.BTpool + c.dt->nodeBT[d] + i * 3LL * qK + qK + c.aug;
   const double *Tl = Th + qK;
-  const double *tg = c.Tv + c.dt->nodeT[d] + i * 2LL * q;
-  double *w1 = c.V + c.dt->nodeV[d + 1] + (2 * i) * (long long)K1;
+  const double *tg = Tvc + c.dt->nodeT[d] + i * 2LL * q;
+  double *w1 = V + c.dt->nodeV[d + 1] + (2 * i) * (long long)K1;
   double *w2 = w1 + K1;
   constexpr int UB = 4;
   for (int ub = u0; ub < q; ub += UB * ustep) {
@@ -735,37 +798,47 @@ __device__ void tree_down_rows(const SolveCtx &c, int d, long long i, int lane, 
 // ---------------------------------------------------------------------------------------------
 // the persistent cooperative kernel
 // ---------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(LT, 2) k_solve(SolveCtx c0, Phases ph) {
+// RB = 1: one right-hand side at a time through the leaves (two CTAs per SM); RB = 8: the leaves take 8 columns per
+// pass (k_solve<8>, larger shared state: one CTA per SM).  The tree levels are the same code.
+template <int RB>
+__global__ void __launch_bounds__(LT, (RB == 1 ? 2 : 1)) k_solve(SolveCtx c0, Phases ph) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double sm[];
-  __shared__ LeafSmem S;
+  // RB = 1: the leaf scratch is static; RB = 8: it is too large for static shared memory and sits after the X tiles
+  __shared__ typename std::conditional<RB == 1, LeafSmem, int>::type S1;
+  auto &S = *[&]() {
+    if constexpr (RB == 1) return &S1;
+    else return reinterpret_cast<LeafSmem8 *>(sm + c0.xdoubles);
+  }();
   __shared__ DepthTab sdt;                     // the per-depth tables, read by every tree node
   for (int i = threadIdx.x; i < (int)(sizeof(DepthTab) / 8); i += LT) ((long long *)&sdt)[i] = ((const long long *)c0.dt)[i];
-  if (threadIdx.x == 0) { mbar_init(&S.barX); mbar_init(&S.barE); }
   __syncthreads();
   SolveCtx c = c0;
   c.dt = &sdt;
-  unsigned phX = 0, phE = 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double *sX = sm, *sE = sm + 64 * (c.T * (c.T + 1) / 2);
+  double *sX = sm;
   const long long gw = (long long)blockIdx.x * NWL + warp, nw = (long long)gridDim.x * NWL;
   const bool stamp = c.stamps && blockIdx.x == 0 && threadIdx.x == 0;
   int ns = 0;
+  const int R = c.R;
   if (stamp) c.stamps[ns++] = gtimer();
   if (ph.leaf_up) {
-    if (c.bulk) leaf_up_phase<true>(c, sX, sE, S, phX, phE); else leaf_up_phase<false>(c, sX, sE, S, phX, phE);
+    if constexpr (RB == 1) leaf_up_phase(c, sX, S); else leaf_up_phase8(c, sX, S);
     grid.sync();
     if (stamp) c.stamps[ns++] = gtimer();
   }
   {
+    // work items of a level: (node, right-hand side) pairs, node fastest
     const long long gwt = (long long)blockIdx.x * c.tree_warps + warp, nwt = (long long)gridDim.x * c.tree_warps;
     for (int d = ph.up_hi; d >= ph.up_lo; d--) {
       long long i0, cnt;
       own_range(c, d, i0, cnt);
-      if (cnt <= gridDim.x) {                  // few nodes: one CTA each
-        if (blockIdx.x < cnt) tree_up_node_cta(c, d, i0 + blockIdx.x, sm);
+      const long long items = cnt * R;
+      if (items <= gridDim.x) {                // few items: one CTA each
+        if (blockIdx.x < items) tree_up_node_cta(c, d, i0 + blockIdx.x % cnt, (int)(blockIdx.x / cnt), sm);
       } else if (warp < c.tree_warps) {
-        for (long long j = gwt; j < cnt; j += nwt) tree_up_node(c, d, i0 + j, sm + (size_t)warp * c.tree_scratch, lane);
+        for (long long j = gwt; j < items; j += nwt)
+          tree_up_node(c, d, i0 + j % cnt, (int)(j / cnt), sm + (size_t)warp * c.tree_scratch, lane);
       }
       grid.sync();
       if (stamp) c.stamps[ns++] = gtimer();
@@ -775,15 +848,17 @@ __global__ void __launch_bounds__(LT, 2) k_solve(SolveCtx c0, Phases ph) {
   for (int d = 0; d < c.kappa; d++) {
     long long i0, cnt;
     own_range(c, d, i0, cnt);
-    if (cnt >= 8 && cnt <= gridDim.x) {       // few (but not very few) nodes: one CTA each, its warps split the rows
-      if (blockIdx.x < cnt) tree_down_rows(c, d, i0 + blockIdx.x, lane, warp, NWL, warp == 0);
+    const long long items = cnt * R;
+    if (items >= 8 && items <= gridDim.x) {   // few (but not very few) items: one CTA each, its warps split the rows
+      if (blockIdx.x < items)
+        tree_down_rows(c, d, i0 + blockIdx.x % cnt, (int)(blockIdx.x / cnt), lane, warp, NWL, warp == 0);
     } else {
-      for (long long j = gw; j < cnt; j += nw) tree_down_node(c, d, i0 + j, lane);
+      for (long long j = gw; j < items; j += nw) tree_down_node(c, d, i0 + j % cnt, (int)(j / cnt), lane);
     }
     grid.sync();
     if (stamp) c.stamps[ns++] = gtimer();
   }
-  if (c.bulk) leaf_down_phase<true>(c, sX, sE, S, phX, phE); else leaf_down_phase<false>(c, sX, sE, S, phX, phE);
+  if constexpr (RB == 1) leaf_down_phase(c, sX, S); else leaf_down_phase8(c, sX, S);
   if (stamp) c.stamps[ns++] = gtimer();
 }
 
@@ -805,127 +880,9 @@ __global__ void k_pack_rows(const double *xsorted, long long lo, long long m, do
 
 }  // namespace
 
-// y, x: one column each (device).  up_only: stop after the up pass (h_root = y^T C^{-1} y in hvec[0]).  fused: y is
-// the right-hand side the factorization carried (hodlr_factor_solve): its leaf and tree up passes are already in the
-// factors (Pi_c[0, :] = g_c, T_c[:, 0] = t_c), so only the down passes run.
-hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_only, bool fused) {
-  const int kappa = h->kappa;
-  DepthTab &dt = h->dt;
-  if (h->leaf_max > VMAX || dt.Kdim[kappa] > KMAX_SOLVE)
-    return hodlr_set_error(HODLR_EINVAL, "solve: leaf size %d > %d or K = %d > %d", h->leaf_max, VMAX, dt.Kdim[kappa], KMAX_SOLVE);
-  if (!h->Vpool) {
-    long long vTot = 0, tTot = 0;
-    for (int e = 0; e <= kappa; e++) { dt.nodeV[e] = vTot; vTot += (1LL << e) * (long long)dt.Kdim[e]; }
-    for (int d = 0; d < kappa; d++) { dt.nodeT[d] = tTot; tTot += (1LL << d) * 4LL * dt.rdep[d + 1]; }
-    h->Vpool = (double *)hodlr_dalloc(h, sizeof(double) * (vTot > 0 ? vTot : 1));
-    h->Tvec = (double *)hodlr_dalloc(h, sizeof(double) * (tTot > 0 ? tTot : 1));
-    h->hvec = (double *)hodlr_dalloc(h, sizeof(double) * 2 * h->nnodes);
-    if (!h->Vpool || !h->Tvec || !h->hvec) return hodlr_set_error(HODLR_ENOMEM, "solve: device allocation failed");
-    HCUDA(cudaMemcpyAsync(h->d_dt, &dt, sizeof(DepthTab), cudaMemcpyHostToDevice, h->st));
-  }
-  SolveCtx c;
-  c.n = h->n; c.ninternal = h->ninternal; c.nleaves = h->nleaves; c.kappa = kappa; c.K = dt.Kdim[kappa];
-  c.T = h->ltiles; c.grank = h->grank; c.tsplit = h->tsplit;
-  c.lo = h->lo; c.hi = h->hi; c.perm = h->perm; c.Xh = h->Xh; c.ldx = h->ldx; c.rank = h->rank; c.dt = h->d_dt;
-  c.Lf = h->Lf; c.lstride = h->lstride; c.Spool = h->Spool; c.BTpool = h->BTpool;
-  c.V = h->Vpool; c.Tv = h->Tvec; c.hv = h->hvec; c.y = y; c.x = x; c.flags = h->dflags;
-  c.aug = h->aug; c.fused = fused ? 1 : 0;
-  hodlr_own_nodes(h, kappa, &c.leaf0, &c.nown);
-  c.xsorted = nullptr;
-  if (h->nranks > 1 && !up_only) {
-    if (!h->xshard) {
-      h->xshard = (double *)hodlr_dalloc(h, sizeof(double) * ((size_t)h->n + (size_t)h->rows_max * (h->nranks + 1)));
-      if (!h->xshard) return hodlr_set_error(HODLR_ENOMEM, "solve: device allocation failed");
-    }
-    c.xsorted = h->xshard;
-  }
-  // dynamic shared memory: the leaf staging (X tiles + E panel) or the tree-up scratch of every warp
-  const int R = 8 * h->ltiles;
-  const size_t leaf_db = 64 * (size_t)(h->ltiles * (h->ltiles + 1) / 2) + (size_t)c.K * R;
-  size_t qmax = 0;
-  for (int d = 0; d < kappa; d++) qmax = std::max(qmax, 2 * (size_t)dt.rdep[d + 1]);
-  c.tree_scratch = (long long)std::max<size_t>(1, 2 * qmax * qmax + 5 * qmax);   // kappa = 0: no tree
-  int maxsm = 0, nsm = 0;
-  HCUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
-  HCUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->dev));
-  static int static_smem = -1;
-  if (static_smem < 0) {
-    cudaFuncAttributes fa;
-    HCUDA(cudaFuncGetAttributes(&fa, k_solve));
-    static_smem = (int)fa.sharedSizeBytes;
-  }
-  const size_t avail = ((size_t)maxsm - (size_t)static_smem - 256) / sizeof(double);
-  const size_t x_db = 64 * (size_t)(h->ltiles * (h->ltiles + 1) / 2);
-  // Stage only X (68 KB at p = 128) and read E from global memory: two CTAs per SM overlap one leaf's loads with
-  // the other's arithmetic (measured faster than staging X + E at one CTA per SM).  HODLR_SOLVE_STAGE_E=1 stages E.
-  static int stage_env = -1;
-  if (stage_env < 0) { const char *ev = getenv("HODLR_SOLVE_STAGE_E"); stage_env = ev && atoi(ev) ? 1 : 0; }
-  c.stage_e = (stage_env && leaf_db <= avail) ? 1 : 0;
-  const size_t stage_db = c.stage_e ? leaf_db : x_db;
-  const size_t need = std::max(stage_db, (size_t)c.tree_scratch);
-  if (need > avail)
-    return hodlr_set_error(HODLR_EINVAL, "solve: leaf inverse (%d rows) or coupling size %zu exceeds shared memory", R, qmax);
-  const size_t half = c.stage_e ? avail : std::min(avail, (size_t)(((size_t)maxsm / 2 - (size_t)static_smem - 1024) / sizeof(double)));
-  const size_t dsm_d = std::max(stage_db, std::min(half, (size_t)NWL * (size_t)c.tree_scratch));
-  c.tree_warps = (int)std::min<size_t>(NWL, dsm_d / (size_t)c.tree_scratch);
-  const size_t dsm = sizeof(double) * dsm_d;
-  static int trace = -1;
-  if (trace < 0) { const char *ev = getenv("HODLR_TRACE"); trace = ev && atoi(ev) ? 1 : 0; }
-  c.stamps = nullptr;
-  if (trace) {
-    if (!h->stamps) h->stamps = (unsigned long long *)hodlr_dalloc(h, sizeof(unsigned long long) * 128);
-    c.stamps = h->stamps;
-  }
-  {   // the device's opt-in maximum on every call: the same value from every thread and handle (no race between
-      // handles that need different sizes), and it permits every launch size; occupancy follows the launch's own size
-    int maxsm = 0;
-    HCUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
-    if (dsm > (size_t)maxsm) return hodlr_set_error(HODLR_EINVAL, "solve: %zu B of shared memory needed", dsm);
-    HCUDA(hodlr_allow_smem((const void *)k_solve, h->dev));
-  }
-  if (!h->bulk_checked) {     // bulk staging needs every leaf start and size and n even (16-byte segments)
-    bool ok = (h->ldx % 2) == 0;
-    for (long long l = 0; ok && l < h->nleaves; l++) {
-      const long long id = h->ninternal + l;
-      ok = (h->h_lo[id] % 2) == 0 && ((h->h_hi[id] - h->h_lo[id]) % 2) == 0;
-    }
-    h->bulk_ok = ok ? 1 : 0; h->bulk_checked = 1;
-  }
-  static int bulk_env = -1;      // bulk (TMA-engine) staging measured slower than per-thread cp.async here
-  if (bulk_env < 0) { const char *ev = getenv("HODLR_SOLVE_BULK"); bulk_env = ev && atoi(ev) ? 1 : 0; }
-  c.bulk = h->bulk_ok && bulk_env && c.stage_e;
-  int per_sm = 0;
-  HCUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve, LT, dsm));
-  if (per_sm < 1) return hodlr_set_error(HODLR_EINVAL, "solve: kernel does not fit on an SM");
-  const int grid = nsm * std::min(per_sm, 2);             // persistent: every CTA resident (cooperative launch)
-  auto launch = [&](Phases ph) -> hodlr_status {
-    void *args[] = {(void *)&c, (void *)&ph};
-    HCUDA(cudaLaunchCooperativeKernel((const void *)k_solve, dim3(grid), dim3(LT), args, dsm, h->st));
-    HLAUNCH(h, "k_solve");
-    return HODLR_OK;
-  };
-  ph_begin(h, PH_SLEAF_UP);
+// every rank returns the full solution: allgather the sorted row slices, un-permute into x
+static hodlr_status unshard(hodlr_s *h, double *x) {
   hodlr_status st;
-  if (fused) {
-    st = launch(Phases{0, -1, 0, 1});
-  } else if (h->nranks > 1 && h->tsplit > 0) {
-    // leaf up + own subtree levels, exchange of the depth-t projections, then the rest
-    st = launch(Phases{1, kappa - 1, h->tsplit, 0});
-    if (st != HODLR_OK) return st;
-    const int t = h->tsplit;
-    const long long Kt = dt.Kdim[t];
-    double *gb = h->Vpool + dt.nodeV[t];
-    st = hodlr_allgather(h, gb + h->grank * Kt, gb, sizeof(double) * (Kt > 0 ? Kt : 1));
-    if (st != HODLR_OK) return st;
-    double *hb = h->hvec + 2 * ((1LL << t) - 1);
-    st = hodlr_allgather(h, hb + 2 * h->grank, hb, sizeof(double) * 2);
-    if (st != HODLR_OK) return st;
-    st = launch(Phases{0, t - 1, 0, up_only ? 0 : 1});
-  } else {
-    st = launch(Phases{1, kappa - 1, 0, up_only ? 0 : 1});
-  }
-  if (st != HODLR_OK) return st;
-  if (h->nranks > 1 && !up_only) {   // every rank returns the full solution: allgather the sorted row slices
     const long long id = (1LL << h->tsplit) - 1 + h->grank;
     const long long rlo = h->h_lo[id], rm = h->h_hi[id] - rlo;
     double *send = h->xshard + h->n, *recv = send + h->rows_max;
@@ -936,7 +893,121 @@ hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_on
     const long long tot = (long long)h->nranks * h->rows_max;
     k_unshard<<<(int)((tot + 255) / 256), 256, 0, h->st>>>(recv, h->d_rowlo, h->nranks, h->rows_max, h->n, h->perm, x);
     HLAUNCH(h, "k_unshard");
+    return HODLR_OK;
+}
+
+// y, x: nrhs columns with leading dimension ld (device; x may be NULL when up_only).  up_only: stop after the up pass
+// (h_root = y^T C^{-1} y of column r in hvec[r * 2 nnodes]).  fused: y is the right-hand side the factorization
+// carried (hodlr_factor_solve, nrhs = 1): its leaf and tree up passes are already in the factors (Pi_c[0, :] = g_c,
+// T_c[:, 0] = t_c), so only the down passes run.  Up to SOLVE_RMAX columns per launch share every staged leaf
+// inverse X and every L2-resident panel E_l, and the tree levels run their (node, column) pairs in parallel.
+hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, int64_t nrhs, int64_t ld, bool up_only, bool fused) {
+  const int kappa = h->kappa;
+  DepthTab &dt = h->dt;
+  if (h->leaf_max > VMAX || dt.Kdim[kappa] > KMAX_SOLVE)
+    return hodlr_set_error(HODLR_EINVAL, "solve: leaf size %d > %d or K = %d > %d", h->leaf_max, VMAX, dt.Kdim[kappa], KMAX_SOLVE);
+  // per-launch columns: one when sharded (the exchanges are per column) or fused
+  const int RM = (h->nranks > 1 || fused) ? 1 : (int)std::min<int64_t>(nrhs, SOLVE_RMAX);
+  if (!h->Vpool || h->solve_cols < RM) {
+    long long vTot = 0, tTot = 0;
+    for (int e = 0; e <= kappa; e++) { dt.nodeV[e] = vTot; vTot += (1LL << e) * (long long)dt.Kdim[e]; }
+    for (int d = 0; d < kappa; d++) { dt.nodeT[d] = tTot; tTot += (1LL << d) * 4LL * dt.rdep[d + 1]; }
+    h->vcol = vTot > 0 ? vTot : 1; h->tcol = tTot > 0 ? tTot : 1; h->hcol = 2 * h->nnodes;
+    h->Vpool = (double *)hodlr_dalloc(h, sizeof(double) * h->vcol * RM);
+    h->Tvec = (double *)hodlr_dalloc(h, sizeof(double) * h->tcol * RM);
+    h->hvec = (double *)hodlr_dalloc(h, sizeof(double) * h->hcol * RM);
+    if (!h->Vpool || !h->Tvec || !h->hvec) return hodlr_set_error(HODLR_ENOMEM, "solve: device allocation failed");
+    h->solve_cols = RM;
+    HCUDA(cudaMemcpyAsync(h->d_dt, &dt, sizeof(DepthTab), cudaMemcpyHostToDevice, h->st));
   }
+  SolveCtx c;
+  c.n = h->n; c.ninternal = h->ninternal; c.nleaves = h->nleaves; c.kappa = kappa; c.K = dt.Kdim[kappa];
+  c.T = h->ltiles; c.grank = h->grank; c.tsplit = h->tsplit;
+  c.lo = h->lo; c.hi = h->hi; c.perm = h->perm; c.Xh = h->Xh; c.ldx = h->ldx; c.rank = h->rank; c.dt = h->d_dt;
+  c.Lf = h->Lf; c.lstride = h->lstride; c.Spool = h->Spool; c.BTpool = h->BTpool;
+  c.V = h->Vpool; c.Tv = h->Tvec; c.hv = h->hvec; c.y = y; c.x = x; c.flags = h->dflags;
+  c.vcol = h->vcol; c.tcol = h->tcol; c.hcol = h->hcol; c.ldy = ld;
+  c.aug = h->aug; c.fused = fused ? 1 : 0;
+  hodlr_own_nodes(h, kappa, &c.leaf0, &c.nown);
+  c.xsorted = nullptr;
+  if (h->nranks > 1 && !up_only) {
+    if (!h->xshard) {
+      h->xshard = (double *)hodlr_dalloc(h, sizeof(double) * ((size_t)h->n + (size_t)h->rows_max * (h->nranks + 1)));
+      if (!h->xshard) return hodlr_set_error(HODLR_ENOMEM, "solve: device allocation failed");
+    }
+    c.xsorted = h->xshard;
+  }
+  // dynamic shared memory: the leaf staging (X tiles) or the tree-up scratch of every warp
+  const int Rr = 8 * h->ltiles;
+  size_t qmax = 0;
+  for (int d = 0; d < kappa; d++) qmax = std::max(qmax, 2 * (size_t)dt.rdep[d + 1]);
+  c.tree_scratch = (long long)std::max<size_t>(1, 2 * qmax * qmax + 5 * qmax);   // kappa = 0: no tree
+  int maxsm = 0, nsm = 0;
+  HCUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
+  HCUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->dev));
+  const void *kfun = RM > 1 ? (const void *)k_solve<8> : (const void *)k_solve<1>;
+  cudaFuncAttributes fa;
+  HCUDA(cudaFuncGetAttributes(&fa, kfun));
+  const size_t static_smem = fa.sharedSizeBytes;
+  const size_t avail = ((size_t)maxsm - static_smem - 256) / sizeof(double);
+  // Stage only X (68 KB at p = 128) and read E from global memory: two CTAs per SM overlap one leaf's loads with
+  // the other's arithmetic (measured faster than staging X + E at one CTA per SM)
+  const size_t x_db0 = 64 * (size_t)(h->ltiles * (h->ltiles + 1) / 2);
+  c.xdoubles = (long long)x_db0;
+  // RB = 8: the 8-column leaf scratch follows the X tiles in dynamic shared memory
+  const size_t x_db = x_db0 + (RM > 1 ? (sizeof(LeafSmem8) + 7) / 8 : 0);
+  const size_t need = std::max(x_db, (size_t)c.tree_scratch);
+  if (need > avail)
+    return hodlr_set_error(HODLR_EINVAL, "solve: leaf inverse (%d rows) or coupling size %zu exceeds shared memory", Rr, qmax);
+  const size_t half = RM > 1 ? avail : std::min(avail, (size_t)(((size_t)maxsm / 2 - static_smem - 1024) / sizeof(double)));
+  const size_t dsm_d = std::max(x_db, std::min(half, (size_t)NWL * (size_t)c.tree_scratch));
+  c.tree_warps = (int)std::min<size_t>(NWL, dsm_d / (size_t)c.tree_scratch);
+  const size_t dsm = sizeof(double) * dsm_d;
+  static int trace = -1;
+  if (trace < 0) { const char *ev = getenv("HODLR_TRACE"); trace = ev && atoi(ev) ? 1 : 0; }
+  c.stamps = nullptr;
+  if (trace) {
+    if (!h->stamps) h->stamps = (unsigned long long *)hodlr_dalloc(h, sizeof(unsigned long long) * 128);
+    c.stamps = h->stamps;
+  }
+  HCUDA(hodlr_allow_smem(kfun, h->dev));
+  int per_sm = 0;
+  HCUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfun, LT, dsm));
+  if (per_sm < 1) return hodlr_set_error(HODLR_EINVAL, "solve: kernel does not fit on an SM");
+  const int grid = nsm * std::min(per_sm, 2);             // persistent: every CTA resident (cooperative launch)
+  auto launch = [&](Phases ph) -> hodlr_status {
+    void *args[] = {(void *)&c, (void *)&ph};
+    HCUDA(cudaLaunchCooperativeKernel(kfun, dim3(grid), dim3(LT), args, dsm, h->st));
+    HLAUNCH(h, "k_solve");
+    return HODLR_OK;
+  };
+  ph_begin(h, PH_SLEAF_UP);
+  hodlr_status st = HODLR_OK;
+  for (int64_t j0 = 0; j0 < nrhs && st == HODLR_OK; j0 += RM) {
+    c.R = (int)std::min<int64_t>(RM, nrhs - j0);
+    c.y = y + j0 * ld; c.x = x ? x + j0 * ld : nullptr;
+    if (fused) {
+      st = launch(Phases{0, -1, 0, 1});
+    } else if (h->nranks > 1 && h->tsplit > 0) {
+      // leaf up + own subtree levels, exchange of the depth-t projections, then the rest
+      st = launch(Phases{1, kappa - 1, h->tsplit, 0});
+      if (st != HODLR_OK) return st;
+      const int t = h->tsplit;
+      const long long Kt = dt.Kdim[t];
+      double *gb = h->Vpool + dt.nodeV[t];
+      st = hodlr_allgather(h, gb + h->grank * Kt, gb, sizeof(double) * (Kt > 0 ? Kt : 1));
+      if (st != HODLR_OK) return st;
+      double *hb = h->hvec + 2 * ((1LL << t) - 1);
+      st = hodlr_allgather(h, hb + 2 * h->grank, hb, sizeof(double) * 2);
+      if (st != HODLR_OK) return st;
+      st = launch(Phases{0, t - 1, 0, up_only ? 0 : 1});
+    } else {
+      st = launch(Phases{1, kappa - 1, 0, up_only ? 0 : 1});
+    }
+    if (st != HODLR_OK) return st;
+    if (h->nranks > 1 && !up_only) st = unshard(h, c.x);
+  }
+  if (st != HODLR_OK) return st;
   ph_end(h, PH_SLEAF_UP);
   if (trace && c.stamps) {       // per-phase device times (block 0's view, after each grid barrier)
     unsigned long long s[80];
@@ -945,10 +1016,6 @@ hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, bool up_on
     const int nst = (up_only ? 1 + kappa : 2 + 2 * kappa) + 1;
     fprintf(stderr, "[hodlr solve phases us]");
     for (int k = 1; k < nst && k < 64; k++) fprintf(stderr, " %.1f", 1e-3 * (double)(s[k] - s[k - 1]));
-    fprintf(stderr, "\n[hodlr solve leaf-up sub-phases us, block 0: y+colsrc, X wait, tri_mv+tri_mvt, h+E wait, E^T v, tail]");
-    for (int k = 64; k < 70; k++) fprintf(stderr, " %.1f", 1e-3 * (double)s[k]);
-    fprintf(stderr, "\n[hodlr solve leaf-down sub-phases us, block 0: w+y+colsrc, E wait, E w, X wait, tri_mv+tri_mvt, x+tail]");
-    for (int k = 70; k < 76; k++) fprintf(stderr, " %.1f", 1e-3 * (double)s[k]);
     fprintf(stderr, "\n");
   }
   return HODLR_OK;

@@ -38,8 +38,8 @@ class hodlr_dist(C.Structure):
 
 
 class hodlr_opts(C.Structure):
-    _fields_ = [("rank_cap", C.c_int32), ("flags", C.c_int32), ("forced_ranks", C.c_void_p),
-                ("reserved", C.c_int64 * 6)]
+    _fields_ = [("rank_cap", C.c_int32), ("flags", C.c_int32), ("forced_ranks", C.c_void_p), ("noise", C.c_void_p),
+                ("reserved", C.c_int64 * 5)]
 
 
 class hodlr_info_t(C.Structure):
@@ -123,9 +123,10 @@ def _stream_ptr(stream) -> int:
 
 # ------------------------------------------------------------------ C-ABI mirrors
 def hodlr_build(x: torch.Tensor, kernel: int, theta, sigma2: float, leaf: int, eps: float,
-                rank_cap: int = 0, stream=None, dist: "hodlr_dist | None" = None, forced_ranks=None) -> int:
+                rank_cap: int = 0, stream=None, dist: "hodlr_dist | None" = None, forced_ranks=None,
+                noise: "torch.Tensor | None" = None) -> int:
     """forced_ranks: optional int32 array of the internal nodes' ACA ranks (heap order) -- the parity test hook of
-    hodlr_opts.forced_ranks."""
+    hodlr_opts.forced_ranks.  noise: optional CUDA float64 (n,) heteroscedastic part of the diagonal."""
     lib = load()
     x = _dev_f64(x, "x")
     th = (C.c_double * 3)(float(theta[0]), float(theta[1]), float(theta[2]) if len(theta) > 2 else 0.0)
@@ -134,6 +135,9 @@ def hodlr_build(x: torch.Tensor, kernel: int, theta, sigma2: float, leaf: int, e
         import numpy as np
         fr = np.ascontiguousarray(forced_ranks, dtype=np.int32)
         opts.forced_ranks = fr.ctypes.data
+    if noise is not None:
+        noise = _dev_f64(noise, "noise")
+        opts.noise = noise.data_ptr()
     h = C.c_void_p(0)
     _check(lib.hodlr_build(x.data_ptr(), x.numel(), int(kernel), th, float(sigma2), int(leaf), float(eps),
                            C.byref(dist) if dist is not None else None, C.byref(opts), _stream_ptr(stream),
@@ -270,7 +274,7 @@ class HODLR:
     """build -> factor -> {logdet, solve, gp_loglik}* on one GPU; inputs are CUDA float64 tensors."""
 
     def __init__(self, x: torch.Tensor, kernel, theta, sigma2: float, leaf: int, eps: float,
-                 rank_cap: int = 0, stream=None, dist=None, forced_ranks=None):
+                 rank_cap: int = 0, stream=None, dist=None, forced_ranks=None, noise=None):
         """dist: None (one GPU) or a paper_1403_6015_b200.dist.Dist (subtree sharding).  forced_ranks: parity test
         hook (hodlr_opts.forced_ranks)."""
         if isinstance(kernel, str):
@@ -278,7 +282,7 @@ class HODLR:
         self.n = x.numel()
         self._dist = dist                       # keeps the NCCL id / group alive
         self._h = hodlr_build(x, kernel, theta, sigma2, leaf, eps, rank_cap, stream,
-                              dist.struct() if dist is not None else None, forced_ranks)
+                              dist.struct() if dist is not None else None, forced_ranks, noise)
 
     def __del__(self):
         h = getattr(self, "_h", 0)

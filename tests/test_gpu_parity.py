@@ -359,3 +359,22 @@ def test_aca_nograph_identical():
         outs.append(subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
                                    timeout=300).stdout.strip())
     assert outs[0] and outs[0] == outs[1], outs
+
+
+@pytest.mark.parametrize("name,n,nrhs", [("cfg1", 2048, 40), ("cfg3", 1 << 15, 33), ("cfg2", 1 << 14, 7)])
+def test_batched_multi_rhs(hb, name, n, nrhs):
+    """hodlr_solve with many right-hand sides (up to 32 per launch; the leaves take 8 columns per DMMA pass, the tree
+    levels run (node, column) pairs) against the oracle's multi-RHS solve, column by column, and against the same
+    columns solved one at a time (the single-column leaf path sums in another order: rounding-level agreement)."""
+    cfg = inputs.scaled(inputs.CONFIGS[name], n)
+    x = inputs.points(cfg, sort=False)
+    Y = np.random.default_rng(5).standard_normal((n, nrhs))
+    o = OracleHODLR(x, cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, 1e-12).factor()
+    Xo = o.solve(Y)
+    g = hb.HODLR(torch.from_numpy(x).cuda(), cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, 1e-12).factor()
+    Xg = g.solve(torch.from_numpy(Y).cuda()).cpu().numpy()
+    for j in range(nrhs):
+        assert np.linalg.norm(Xg[:, j] - Xo[:, j]) <= X_TOL * np.linalg.norm(Xo[:, j]), j
+    for j in (0, nrhs // 2, nrhs - 1):
+        one = g.solve(torch.from_numpy(np.ascontiguousarray(Y[:, j])).cuda()).cpu().numpy()
+        assert np.linalg.norm(one - Xg[:, j]) <= 1e-11 * np.linalg.norm(one), (j, np.linalg.norm(one - Xg[:, j]))

@@ -472,3 +472,35 @@ def test_twin_qr_sign_convention():
     assert t.logdet() == pytest.approx(512 * math.log(1e-2), rel=1e-14)
     t = OracleHODLR(x, SE, (1.0, 1e20), 1e-2, 16, 1e-12, twin=True).factor()
     assert t.logdet() == pytest.approx(511 * math.log(1e-2) + math.log(1e-2 + 512), rel=1e-13)
+
+
+# ---------------------------------------------------------------------------------------------------------------
+# NEXT-2: heteroscedastic noise C_ij = sigma_i^2 delta_ij + k(x_i, x_j)
+def test_noise_zero_kernel_closed_form():
+    """K = 0 with per-point noise: C = diag(s2 + noise_i), log det = sum log(s2 + noise_i), x = y / (s2 + noise_i)
+    in the caller's order -- a noise vector applied in sorted instead of original order fails here."""
+    rng = np.random.default_rng(31)
+    n, s2 = 1000, 1e-3
+    x = rng.uniform(0, 1, n); y = rng.standard_normal(n); nz = rng.uniform(0, 0.5, n)
+    h = OracleHODLR(x, SE, (0.0, 0.1), s2, 32, 1e-12, noise=nz).factor()
+    assert h.logdet() == pytest.approx(float(np.sum(np.log(s2 + nz))), rel=1e-13)
+    np.testing.assert_allclose(h.solve(y), y / (s2 + nz), rtol=1e-14)
+
+
+@pytest.mark.parametrize("kernel", [SE, MATERN32])
+def test_noise_hodlr_vs_dense(kernel):
+    """HODLR with heteroscedastic noise against numpy dense (independent assembly + LAPACK) and the O11 checker."""
+    rng = np.random.default_rng(32 + kernel)
+    n = 1500
+    x = rng.uniform(0, 4, n); y = rng.standard_normal(n); nz = np.exp(rng.uniform(np.log(1e-4), np.log(1e-1), n))
+    th = (1.0, 0.3)
+    h = OracleHODLR(x, kernel, th, 0.0, 48, 1e-12, noise=nz).factor()
+    C = dense_C(x, kernel, th, 0.0) + np.diag(nz)
+    sd, ld = np.linalg.slogdet(C)
+    assert sd > 0 and abs(h.logdet() - ld) <= 1e-12 * abs(ld)
+    xd = np.linalg.solve(C, y)
+    assert np.linalg.norm(h.solve(y) - xd) <= 1e-9 * np.linalg.norm(xd)
+    ld2, x2 = dense_check(x, kernel, th, 0.0, y, noise=nz)
+    assert abs(ld2 - ld) <= 1e-12 * abs(ld) and np.linalg.norm(x2 - xd) <= 1e-9 * np.linalg.norm(xd)
+    with pytest.raises(OracleError):
+        OracleHODLR(x, kernel, th, 0.0, 48, 1e-12, noise=-nz)
