@@ -394,18 +394,25 @@ def run_ours(args):
     ys = torch.cuda.Stream()
     ev_y = torch.cuda.Event()
 
+    host_t = []
+
     def step_e2e():
+        t0 = time.perf_counter()
         xd.copy_(xh, non_blocking=True)
         ys.wait_stream(stream)
         with torch.cuda.stream(ys):
             yd.copy_(yh, non_blocking=True)
             ev_y.record(ys)
+        t1 = time.perf_counter()
         h = hb.HODLR(xd, cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, cfg.eps, dist=dd)
+        t2 = time.perf_counter()
         stream.wait_event(ev_y)
         s_, _ = h.factor_solve(yd)
+        t3 = time.perf_counter()
         ld_ = h.logdet()
         sol_h.copy_(s_, non_blocking=True)
         h.close()
+        host_t.append([round(1e3 * (b_ - a_), 3) for a_, b_ in ((t0, t1), (t1, t2), (t2, t3), (t3, time.perf_counter()))])
         return ld_, s_
 
     for _ in range(max(1, args.warmup)):
@@ -422,8 +429,8 @@ def run_ours(args):
         e2e_ms.append(a.elapsed_time(b))
     barrier()
     gc.enable()
-    print(f"[bench] device ms per step {[round(v, 3) for v in ms]}; e2e ms {[round(v, 3) for v in e2e_ms]}",
-          file=sys.stderr)
+    print(f"[bench] device ms per step {[round(v, 3) for v in ms]}; e2e ms {[round(v, 3) for v in e2e_ms]}; "
+          f"e2e host ms (copies, build, factor_solve, rest) {host_t[-args.steps:]}", file=sys.stderr)
     t_e2e = sum(e2e_ms) / len(e2e_ms) / 1e3
     if ws > 1:
         tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)

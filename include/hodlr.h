@@ -167,7 +167,9 @@ hodlr_status gp_loglik(hodlr_t h, const double *y, double *out_host);
 /* Config 4 (BASELINE.json): log-likelihoods (eq. 1) of B independent hyper-parameter settings on the same
  * x, y (device, n doubles).  thetas: HOST B x 2 {a, ell}; sigma2s: HOST B; out_host: HOST B doubles (-INFINITY
  * for a setting that failed).  One GPU runs `workers` settings concurrently (host threads, one stream each;
- * <= 0 => 4).  With dist (nranks > 1) rank g computes settings g, g + P, ... and the values are allgathered, so
+ * <= 0 => 8; each setting's persistent upper-tree launch then takes ~1/workers of the SMs so that the settings'
+ * latency-bound phases overlap).  Every setting is one hodlr_factor_solve with y fused (y^T C^{-1} y from the
+ * factorization, no solve pass).  With dist (nranks > 1) rank g computes settings g, g + P, ... and the values are allgathered, so
  * every rank returns all B (replicas; the settings share nothing).  Returns the first failing setting's status
  * (message names it), HODLR_OK if all succeeded. */
 hodlr_status gp_loglik_sweep(const double *x, const double *y, int64_t n, hodlr_kernel kernel, const double *thetas,
@@ -196,6 +198,13 @@ hodlr_status hodlr_nccl_unique_id(void *out128);
  * after every handle that uses it has been freed. */
 hodlr_status hodlr_group_create(int32_t nranks, void **group);
 void         hodlr_group_destroy(void *group);
+
+/* Scaling projection on one GPU: mode 1 records every exchange of the next sharded run (all virtual
+ * ranks running, rank 0's gathered buffers kept on the device); mode 2 replays: only rank 0 runs, and each exchange
+ * returns the recorded buffer with rank 0's own slot replaced by its live data -- rank 0's critical path without the
+ * other ranks' work on the shared GPU (replay must repeat the recorded call sequence; HODLR_EINVAL otherwise);
+ * mode 0 = normal.  HODLR_ESTATE for mode 2 with nothing recorded. */
+hodlr_status hodlr_group_mode(void *group, int32_t mode);
 
 /* Host-side shard plan (no device work): tree depth kappa, split depth t = log2(nranks), the sorted row range
  * [row_lo, row_hi) and leaf range [leaf_lo, leaf_hi) owned by `rank`.  HODLR_EINVAL for an invalid split. */

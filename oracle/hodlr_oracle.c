@@ -81,6 +81,9 @@ static void mark_row_run(char *used_r, const double *rowkey, int64_t m1, int64_t
   for (int64_t i = ik + 1; i < m1 && rowkey[i] == rowkey[ik]; i++) used_r[i] = 1;
 }
 
+#ifdef ORACLE_TRACE_ACA
+static int g_trace_aca = 0;     /* diagnostic build only: per-step stop statistics of block ORACLE_TRACE_ACA */
+#endif
 static int aca(entry_fn f, const void *ctx, int64_t m1, int64_t m2, double eps, int cap, lowrank *B,
                const double *rowkey) {
   memset(B, 0, sizeof *B);
@@ -133,6 +136,10 @@ static int aca(entry_fn f, const void *ctx, int64_t m1, int64_t m2, double eps, 
     S2 += 2.0 * cross + nu2 * nv2;
     B->U[k] = u; B->V[k] = v; k++; B->r = k;
     /* step 5: stop when ||u_k|| ||v_k|| <= eps ||S_k||_F (term kept, R1/R4) */
+#ifdef ORACLE_TRACE_ACA
+    if (g_trace_aca) fprintf(stderr, "[oracle aca] k=%d ik=%lld jk=%lld nu2=%.17g nv2=%.17g S2=%.17g ratio=%.17g\n", k,
+                             (long long)ik, (long long)jk, nu2, nv2, S2, sqrt(nu2) * sqrt(nv2) / (eps * sqrt(fabs(S2))));
+#endif
     if (sqrt(nu2) * sqrt(nv2) <= eps * sqrt(fabs(S2))) break;
     /* step 6 */
     if (k == mn) break;
@@ -293,6 +300,9 @@ int oracle_build_noise(const double *x, int64_t n, int kernel, const double *the
   for (int64_t c = 0; c < h->ninternal; c++) {
     int64_t c1 = 2 * c + 1, c2 = 2 * c + 2;
     blk_ctx ctx = { h, h->lo[c1], h->lo[c2] };
+#ifdef ORACLE_TRACE_ACA
+    g_trace_aca = c == ORACLE_TRACE_ACA;
+#endif
     int st = aca(kernel_entry, &ctx, h->hi[c1] - h->lo[c1], h->hi[c2] - h->lo[c2], eps, rank_cap, &h->blk[c],
                  h->xs + h->lo[c1]);
     if (st != ORACLE_OK) {

@@ -11,10 +11,11 @@
 //              argmax |u_i| over unused rows; dots U'_l . u ; ||u||^2
 // The last CTA of each block to finish a pass reduces the per-CTA records in a fixed order
 // (deterministic) and advances the block state (pivot, ||S||_F^2 update, stop test).
-// The previous factor columns are streamed once; the dot products come from F_l . a and the
-// running Gram matrix of the factor columns (see k_aca_pass).
+// The previous factor columns are streamed once from HBM; the dot products with the new column are formed from
+// the residual itself (a second sweep over the same columns, served by L1).
 #include "hodlr_internal.cuh"
 #include <vector>
+#include <stdio.h>
 #include <algorithm>
 #include <stdlib.h>
 #include <string.h>
@@ -80,14 +81,13 @@ __device__ __forceinline__ void block_argmax_n2(double &ba, long long &bi, doubl
 // smallest index among equal magnitudes (the convention of amax_better, used for the cross-thread reductions); an
 // all-zero residual leaves bi = -1, which the state update treats as the exactly-zero residual it is.
 // Step-synchronous pass over the big blocks.  ROW: elements j of c2 for the pivot row i_k,
-//   a_j = k(x_ik - x_j),  v~_j = a_j - sum_l U'[ik,l] V'[j,l]  -> V'[:,k]
+//   a_j = k(x_ik - x_j),  v~_j = a_j - sum_l U[ik,l] V[j,l]  -> column k (normalised by the next row pass)
 // COL: elements i of c1 for the pivot column j_k,
-//   a_i = k(x_i - x_jk), u_i = (a_i - sum_l V'[jk,l] U'[i,l]) / v~_jk  -> U'[:,k]
-// Each factor value is streamed once: the dot products F_l . r needed by the ||S_k||_F update are
-// formed as F_l . a - sum_m coef_m G[l,m] with the running Gram matrix G = F^T F of the previous
-// columns (kept per block), so no column has to be staged or re-read.  Per CTA: argmax over unused
-// indices, ||r||^2 and F_l . a for its chunk -> one record; the last CTA of a block reduces the
-// records in a fixed order (deterministic) and advances the block state.
+//   a_i = k(x_i - x_jk), u_i = a_i - sum_l V[jk,l] U[i,l]  -> U[:,k]
+// (entries and updates in the oracle's operation order, R17).  Per thread: the residual over the streamed factor
+// columns, then the dots F_l . r needed by the ||S_k||_F update over the same columns again (L1-resident).  Per
+// CTA: argmax over unused indices, ||r||^2 and F_l . r for its chunk -> one record; the last CTA of a block
+// reduces the records in a fixed order (deterministic) and advances the block state.
 // ---------------------------------------------------------------------------------------------
 #ifndef ACA_PASS_MINB
 #define ACA_PASS_MINB 2            // resident pass CTAs per SM the registers are budgeted for
@@ -95,8 +95,26 @@ __device__ __forceinline__ void block_argmax_n2(double &ba, long long &bi, doubl
 #ifndef ACA_FUSED_SMALL
 #define ACA_FUSED_SMALL 128        // fused blocks with both sides <= this run in 64-thread CTAs
 #endif
-constexpr int ACA_E = 4;                       // elements per thread per sub-tile
+constexpr int ACA_E = 4;                       // elements per thread per sub-tile (measured: 2 with three CTAs per
+                                               // SM is slower)
 constexpr int ACA_TILE = ACA_SUB * ACA_E;
+
+// Warp sum of 4 per-lane partial dots (columns l0 .. l0+3) by a transposed butterfly (6 shuffles); lane L then holds
+// column l0 + ((L >> 3) & 3) and keeps it when batch l0 / 4 is congruent to L mod 8 (w0 for l < 32, w1 for l >= 32)
+__device__ __forceinline__ void dot_butterfly(const double *pv, int l0, int lane, double &w0, double &w1) {
+  const int hi4 = lane & 16, hi3 = lane & 8;
+  double s0v = hi4 ? pv[0] : pv[2], s1v = hi4 ? pv[1] : pv[3];
+  double k0 = hi4 ? pv[2] : pv[0], k1 = hi4 ? pv[3] : pv[1];
+  k0 += __shfl_xor_sync(0xffffffffu, s0v, 16);
+  k1 += __shfl_xor_sync(0xffffffffu, s1v, 16);
+  const double sv = hi3 ? k0 : k1;
+  double kk = hi3 ? k1 : k0;
+  kk += __shfl_xor_sync(0xffffffffu, sv, 8);
+  kk += __shfl_xor_sync(0xffffffffu, kk, 4);
+  kk += __shfl_xor_sync(0xffffffffu, kk, 2);
+  kk += __shfl_xor_sync(0xffffffffu, kk, 1);
+  if (((l0 >> 2) & 7) == (lane & 7)) { if (l0 < 32) w0 += kk; else w1 += kk; }
+}
 
 // Shared scratch of one item (one set per CTA, reused by the row and column passes)
 struct AcaScratch {
@@ -107,7 +125,6 @@ struct AcaScratch {
   double part[ACA_SUB / 32][4 + ACA_MAXCAP];
   double tot[1 + ACA_MAXCAP];
   double dnew[ACA_MAXCAP];
-  double sG[ACA_GSZ];
   int amLast;
 };
 
@@ -120,7 +137,7 @@ __device__ __forceinline__ void aca_item(const AcaCtx &c, int item, AcaScratch &
   double *s_abs = S.s_abs, *s_val = S.s_val, *s_n2 = S.s_n2;
   long long *s_idx = S.s_idx;
   double (*part)[4 + ACA_MAXCAP] = S.part;
-  double *tot = S.tot, *dnew = S.dnew, *sG = S.sG;
+  double *tot = S.tot, *dnew = S.dnew;
   int *flags = c.flags;
   const AcaItem it = c.items[item];
   const int b = it.block;
@@ -155,41 +172,46 @@ __device__ __forceinline__ void aca_item(const AcaCtx &c, int item, AcaScratch &
   double ba = 0.0, bv = 0.0, n2 = 0.0; long long bi = -1;
   const long long end = it.start + ilen;
   const size_t n1 = (size_t)ldx, n2s = 2 * (size_t)ldx, n3 = 3 * (size_t)ldx;   // factor column stride
-  const int hi4 = lane & 16, hi3 = lane & 8;
-  // vector path: thread t takes the 4 consecutive elements 4t..4t+3 of each 1024-element sub-tile (double2
+  // vector path: thread t takes the ACA_E consecutive elements of each ACA_TILE-element sub-tile (double2
   // loads/stores); needs 16-byte alignment of every column segment (n and the chunk start even) -- the
   // scalar loop below handles the rest
-  const bool vec = ((ldx | (lo + it.start)) & 3) == 0 && (ilen & 3) == 0;
+  const bool vec = ((ldx | (lo + it.start)) & 1) == 0 && (ilen % ACA_E) == 0;
+  constexpr int NP = ACA_E / 2;                  // double2 pairs per thread
   if (vec) {
     for (long long s0 = it.start; s0 < end; s0 += ACA_TILE) {
-      const long long g0 = lo + s0 + 4 * t;    // elements g0 .. g0 + 3
-      const bool ok = s0 + 4 * t < end;        // whole quad valid (len is a multiple of 4)
-      double a[4], r[4];
+      const long long g0 = lo + s0 + ACA_E * t;        // elements g0 .. g0 + ACA_E - 1
+      const bool ok = s0 + ACA_E * t < end;            // whole group valid (len is a multiple of ACA_E)
+      double a[ACA_E], r[ACA_E];
       unsigned usedm = 0;
       if (ok) {
-        const double2 x01 = *(const double2 *)(c.xs + g0), x23 = *(const double2 *)(c.xs + g0 + 2);
-        const uchar4 u4 = *(const uchar4 *)(used + g0);
-        usedm = (u4.x ? 1u : 0u) | (u4.y ? 2u : 0u) | (u4.z ? 4u : 0u) | (u4.w ? 8u : 0u);
-        const double xq[4] = {x01.x, x01.y, x23.x, x23.y};
 #pragma unroll
-        for (int q = 0; q < 4; q++) a[q] = kval_ot<SEO>(c.kp, ROW ? xp - xq[q] : xq[q] - xp);
+        for (int pp = 0; pp < NP; pp++) {
+          const double2 xx = *(const double2 *)(c.xs + g0 + 2 * pp);
+          const uchar2 uu = *(const uchar2 *)(used + g0 + 2 * pp);
+          usedm |= ((uu.x ? 1u : 0u) | (uu.y ? 2u : 0u)) << (2 * pp);
+          a[2 * pp] = kval_ot<SEO>(c.kp, ROW ? xp - xx.x : xx.x - xp);
+          a[2 * pp + 1] = kval_ot<SEO>(c.kp, ROW ? xp - xx.y : xx.y - xp);
+        }
       } else {
 #pragma unroll
-        for (int q = 0; q < 4; q++) a[q] = 0.0;
+        for (int q = 0; q < ACA_E; q++) a[q] = 0.0;
       }
 #pragma unroll
-      for (int q = 0; q < 4; q++) r[q] = a[q];
+      for (int q = 0; q < ACA_E; q++) r[q] = a[q];
       const double *colp = slot + (ok ? g0 : lo + it.start);
       constexpr int LS = 4;
       for (int l0 = 0; l0 < k; l0 += LS) {
-        double F[LS][4];
+        double F[LS][ACA_E];
 #pragma unroll
         for (int dl = 0; dl < LS; dl++) {
-          // no masks: a column beyond k reads column 0 (finite) with coefficient 0 and its dot is never kept; a
-          // quad beyond the chunk (!ok) has a = 0 and its residual is never stored
+          // no masks: a column beyond k reads column 0 (finite) with coefficient 0; a group beyond the chunk (!ok)
+          // has a = 0 and its residual is never stored
           const double *cp = colp + (size_t)(l0 + dl < k ? l0 + dl : 0) * n1;
-          const double2 f01 = *(const double2 *)cp, f23 = *(const double2 *)(cp + 2);
-          F[dl][0] = f01.x; F[dl][1] = f01.y; F[dl][2] = f23.x; F[dl][3] = f23.y;
+#pragma unroll
+          for (int pp = 0; pp < NP; pp++) {
+            const double2 f = *(const double2 *)(cp + 2 * pp);
+            F[dl][2 * pp] = f.x; F[dl][2 * pp + 1] = f.y;
+          }
         }
         if (ROW && l0 + LS >= k) {             // the batch holding column k-1: normalise it (and store it back)
           const int dl = k - 1 - l0;
@@ -197,46 +219,46 @@ __device__ __forceinline__ void aca_item(const AcaCtx &c, int item, AcaScratch &
           for (int x = 0; x < LS; x++)
             if (x == dl) {
 #pragma unroll
-              for (int q = 0; q < 4; q++) F[x][q] = div_by(F[x][q], pvp, rpvp);
+              for (int q = 0; q < ACA_E; q++) F[x][q] = div_by(F[x][q], pvp, rpvp);
               if (ok) {
                 double *cp = (double *)colp + (size_t)(k - 1) * n1;
-                *(double2 *)cp = make_double2(F[x][0], F[x][1]);
-                *(double2 *)(cp + 2) = make_double2(F[x][2], F[x][3]);
+#pragma unroll
+                for (int pp = 0; pp < NP; pp++) *(double2 *)(cp + 2 * pp) = make_double2(F[x][2 * pp], F[x][2 * pp + 1]);
               }
             }
         }
-        double pv[LS];
 #pragma unroll
         for (int dl = 0; dl < LS; dl++) {
           const double cf = coef[l0 + dl];
+#pragma unroll
+          for (int q = 0; q < ACA_E; q++) r[q] = __dsub_rn(r[q], __dmul_rn(cf, F[dl][q]));
+        }
+      }
+      // dots F_l . r with the residual as computed, re-reading this group's factor columns newest first (the most
+      // recently streamed columns are the likeliest to still be in L1)
+      for (int l0 = ((k - 1) & ~(LS - 1)); l0 >= 0; l0 -= LS) {
+        double pv[LS];
+#pragma unroll
+        for (int dl = 0; dl < LS; dl++) {
+          const double *cp = colp + (size_t)(l0 + dl < k ? l0 + dl : 0) * n1;
           double p = 0.0;
 #pragma unroll
-          for (int q = 0; q < 4; q++) { r[q] = __dsub_rn(r[q], __dmul_rn(cf, F[dl][q])); p = fma(F[dl][q], a[q], p); }
+          for (int pp = 0; pp < NP; pp++) {
+            const double2 f = *(const double2 *)(cp + 2 * pp);
+            p = fma(f.x, r[2 * pp], fma(f.y, r[2 * pp + 1], p));
+          }
           pv[dl] = p;
         }
-        double s0v = hi4 ? pv[0] : pv[2], s1v = hi4 ? pv[1] : pv[3];
-        double k0 = hi4 ? pv[2] : pv[0], k1 = hi4 ? pv[3] : pv[1];
-        k0 += __shfl_xor_sync(0xffffffffu, s0v, 16);
-        k1 += __shfl_xor_sync(0xffffffffu, s1v, 16);
-        const double sv = hi3 ? k0 : k1;
-        double kk = hi3 ? k1 : k0;
-        kk += __shfl_xor_sync(0xffffffffu, sv, 8);
-        kk += __shfl_xor_sync(0xffffffffu, kk, 4);
-        kk += __shfl_xor_sync(0xffffffffu, kk, 2);
-        kk += __shfl_xor_sync(0xffffffffu, kk, 1);
-        if (((l0 >> 2) & 7) == (lane & 7)) { if (l0 < 32) w0 += kk; else w1 += kk; }
+        dot_butterfly(pv, l0, lane, w0, w1);
       }
       if (ok) {
-        double v[4];
-#pragma unroll
-        for (int q = 0; q < 4; q++) v[q] = r[q];
         double *outp = slot + (long long)k * ldx + g0;
-        *(double2 *)outp = make_double2(v[0], v[1]);
-        *(double2 *)(outp + 2) = make_double2(v[2], v[3]);
 #pragma unroll
-        for (int q = 0; q < 4; q++) {
-          if (!((usedm >> q) & 1u) && fabs(v[q]) > ba) { ba = fabs(v[q]); bi = g0 + q - lo; bv = v[q]; }
-          n2 += v[q] * v[q];
+        for (int pp = 0; pp < NP; pp++) *(double2 *)(outp + 2 * pp) = make_double2(r[2 * pp], r[2 * pp + 1]);
+#pragma unroll
+        for (int q = 0; q < ACA_E; q++) {
+          if (!((usedm >> q) & 1u) && fabs(r[q]) > ba) { ba = fabs(r[q]); bi = g0 + q - lo; bv = r[q]; }
+          n2 += r[q] * r[q];
         }
       }
     }
@@ -275,27 +297,25 @@ __device__ __forceinline__ void aca_item(const AcaCtx &c, int item, AcaScratch &
               if (q < nval) { F[x][q] = div_by(F[x][q], pvp, rpvp); ((double *)cl[x])[q * ACA_SUB] = F[x][q]; }
           }
       }
-      double pv[LS];
 #pragma unroll
       for (int dl = 0; dl < LS; dl++) {
         const double cf = l0 + dl < k ? coef[l0 + dl] : 0.0;
+#pragma unroll
+        for (int q = 0; q < ACA_E; q++) r[q] = __dsub_rn(r[q], __dmul_rn(cf, F[dl][q]));
+      }
+    }
+    for (int l0 = 0; l0 < k; l0 += LS) {       // dots F_l . r with the residual as computed
+      const double *c0 = colp + (size_t)l0 * n1;
+      double pv[LS];
+#pragma unroll
+      for (int dl = 0; dl < LS; dl++) {
         double p = 0.0;
 #pragma unroll
-        for (int q = 0; q < ACA_E; q++) { r[q] = __dsub_rn(r[q], __dmul_rn(cf, F[dl][q])); p = fma(F[dl][q], a[q], p); }
+        for (int q = 0; q < ACA_E; q++)
+          if (l0 + dl < k && q < nval) p = fma(c0[(size_t)dl * n1 + q * ACA_SUB], r[q], p);
         pv[dl] = p;
       }
-      // transposed butterfly: 4 values x 32 lanes -> lane L holds sum of value 2*(L>>4&1) + (L>>3&1)
-      double s0v = hi4 ? pv[0] : pv[2], s1v = hi4 ? pv[1] : pv[3];
-      double k0 = hi4 ? pv[2] : pv[0], k1 = hi4 ? pv[3] : pv[1];
-      k0 += __shfl_xor_sync(0xffffffffu, s0v, 16);
-      k1 += __shfl_xor_sync(0xffffffffu, s1v, 16);
-      const double sv = hi3 ? k0 : k1;
-      double kk = hi3 ? k1 : k0;
-      kk += __shfl_xor_sync(0xffffffffu, sv, 8);
-      kk += __shfl_xor_sync(0xffffffffu, kk, 4);
-      kk += __shfl_xor_sync(0xffffffffu, kk, 2);
-      kk += __shfl_xor_sync(0xffffffffu, kk, 1);
-      if (((l0 >> 2) & 7) == (lane & 7)) { if (l0 < 32) w0 += kk; else w1 += kk; }
+      dot_butterfly(pv, l0, lane, w0, w1);
     }
 #pragma unroll
     for (int q = 0; q < ACA_E; q++) {
@@ -354,24 +374,16 @@ __device__ __forceinline__ void aca_item(const AcaCtx &c, int item, AcaScratch &
     tot[cidx] = s;
   }
   __syncthreads();
-  const long long bidx = c.bigidx[b];
-  double *G = c.gram + bidx * (2LL * ACA_GSZ) + (ROW ? ACA_GSZ : 0);   // G_U then G_V
-  // dots with the new column: F_l . r = F_l . a - sum_m coef_m G[l,m] (G staged in shared memory); the row pass's
-  // column is normalised by the pivot (V[:,k] = v~ / v~_jk), so its dots and norm are divided by it
-  for (int p = t; p < k * (k + 1) / 2; p += ACA_SUB) sG[p] = __ldcg(G + p);
-  __syncthreads();
+  // dots with the new column, F_l . r, formed from the residual as computed (the oracle's dot(u, U_l) and
+  // dot(V_l, v)); the row pass's column is normalised by the pivot (V[:,k] = v~ / v~_jk), so its dots and norm are
+  // divided by it.  (Forming them as F_l . a - sum_m coef_m (F_l . F_m) from a running Gram matrix, as before, is
+  // unstable once the residual is rounding noise: at eps = 1e-12 that estimate of ||S||_F drifted by 40% within two
+  // steps and flipped whole blocks' stopping decisions -- DESIGN.md R17.)
   const double pv = (ROW && bi >= 0 && bv != 0.0) ? bv : 1.0;
-  for (int l = t; l < k; l += ACA_SUB) {
-    double s = tot[1 + l];
-    for (int m = 0; m < k; m++) s = fma(-coef[m], sG[pk(l, m)], s);
-    if (ROW) s = s / pv;
-    dnew[l] = s;
-    G[pk(k, l)] = s;
-  }
+  for (int l = t; l < k; l += ACA_SUB) dnew[l] = ROW ? tot[1 + l] / pv : tot[1 + l];
   __syncthreads();
   if (t == 0) {
     const double nr2 = ROW ? (tot[0] / pv) / pv : tot[0];
-    G[pk(k, k)] = nr2;
     if (ROW) {
       for (int l = 0; l < k; l++) st->dV[l] = dnew[l];
       st->cnt_r = 0;
@@ -394,6 +406,11 @@ __device__ __forceinline__ void aca_item(const AcaCtx &c, int item, AcaScratch &
       const long long mn = m1 < m2 ? m1 : m2;
       int done = 0;
       const int fr = c.forced ? c.forced[b] : -1;
+#ifdef ACA_TRACE_BLOCK
+      if (b == ACA_TRACE_BLOCK)      // diagnostic build only: the oracle's ORACLE_TRACE_ACA line for the same block
+        printf("[gpu aca] k=%d ik=%lld jk=%lld nu2=%.17g nv2=%.17g S2=%.17g ratio=%.17g\n", k, st->ipiv, st->jpiv, nu2,
+               nv2, S2, sqrt(nu2) * sqrt(nv2) / (c.eps * sqrt(fabs(S2))));
+#endif
       if (fr >= 0 ? k1 >= fr : sqrt(nu2) * sqrt(nv2) <= c.eps * sqrt(fabs(S2))) done = 1;     // stop term is kept
       else if (k1 == mn) done = 1;
       else if (k1 == st->cap) { done = 2; atomicAdd(&flags[5], 1); }
@@ -724,8 +741,7 @@ hodlr_status hodlr_aca(hodlr_s *h) {
   h->ast = (AcaState *)hodlr_dalloc_tmp(h, sizeof(AcaState) * nb);
   h->rank = (int *)hodlr_dalloc(h, sizeof(int) * nb);
   h->used = (unsigned char *)hodlr_dalloc_tmp(h, (size_t)h->kappa * n);
-  double *d_gram = (double *)hodlr_dalloc_tmp(h, sizeof(double) * 2 * ACA_GSZ * (size_t)(nbig > 0 ? nbig : 1));
-  if (!d_rec || !h->ast || !h->rank || !h->used || !d_gram) return hodlr_set_error(HODLR_ENOMEM, "aca: device allocation failed");
+  if (!d_rec || !h->ast || !h->rank || !h->used) return hodlr_set_error(HODLR_ENOMEM, "aca: device allocation failed");
   h->bdepth = P->d_bdepth;
   // The step loop is latency-bound: everything of the ACA phase runs on a high-priority stream so that the
   // leaf Cholesky (side stream, issued earlier) only fills the SM slots it leaves free.
@@ -744,7 +760,7 @@ hodlr_status hodlr_aca(hodlr_s *h) {
   memset(&c, 0, sizeof(c));
   c.kp = h->kp; c.n = n; c.ldx = h->ldx; c.eps = h->eps; c.xs = h->xs; c.lo = h->lo; c.hi = h->hi; c.Xh = h->Xh;
   c.used = h->used; c.st = h->ast; c.active = h->dflags + 4; c.rank = h->rank; c.bdepth = P->d_bdepth;
-  c.dt = h->d_dt; c.bigidx = P->d_bigidx; c.gram = d_gram; c.flags = h->dflags; c.step = h->dflags + 6;
+  c.dt = h->d_dt; c.bigidx = P->d_bigidx; c.flags = h->dflags; c.step = h->dflags + 6;
   c.maxsteps = h->cap + 1;
   c.forced = h->d_forced;
   AcaCtx cx[2] = {c, c};

@@ -58,6 +58,14 @@ struct HodlrGroup {
   int arrived = 0;
   long long gen = 0;
   const void *send[256];
+  // scaling projection (hodlr_group_mode): 1 = record every gathered buffer (rank 0's view, device copies);
+  // 2 = solo replay: only rank 0 runs, each exchange copies the recorded buffer and overwrites rank 0's slot with
+  // its live send (the other ranks' parts are what they computed in the recorded run: same inputs, deterministic
+  // kernels), so rank 0's critical path is timed without the other ranks' work on the same GPU
+  int mode = 0;
+  size_t replay_next = 0;
+  std::vector<void *> rec;
+  std::vector<size_t> rec_bytes;
 };
 
 static void group_barrier(HodlrGroup *g) {
@@ -79,11 +87,25 @@ hodlr_status hodlr_allgather(hodlr_s *h, const void *send, void *recv, size_t by
     return HODLR_OK;
   }
   HodlrGroup *g = (HodlrGroup *)h->group;
+  if (g->mode == 2) {                       // solo replay (rank 0 only)
+    if (g->replay_next >= g->rec.size() || g->rec_bytes[g->replay_next] != bytes * g->n)
+      return hodlr_set_error(HODLR_EINVAL, "group replay: exchange %zu does not match the recorded run", g->replay_next);
+    HCUDA(cudaMemcpyAsync(recv, g->rec[g->replay_next++], bytes * g->n, cudaMemcpyDeviceToDevice, h->st));
+    HCUDA(cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, h->st));
+    return HODLR_OK;
+  }
   HCUDA(cudaStreamSynchronize(h->st));
   { std::lock_guard<std::mutex> lk(g->mu); g->send[h->grank] = send; }
   group_barrier(g);
   for (int j = 0; j < g->n; j++)
     HCUDA(cudaMemcpyAsync((char *)recv + (size_t)j * bytes, g->send[j], bytes, cudaMemcpyDeviceToDevice, h->st));
+  if (g->mode == 1 && h->grank == 0) {      // record rank 0's gathered buffer
+    void *p = nullptr;
+    HCUDA(cudaMalloc(&p, bytes * g->n));
+    HCUDA(cudaMemcpyAsync(p, recv, bytes * g->n, cudaMemcpyDeviceToDevice, h->st));
+    std::lock_guard<std::mutex> lk(g->mu);
+    g->rec.push_back(p); g->rec_bytes.push_back(bytes * g->n);
+  }
   HCUDA(cudaStreamSynchronize(h->st));
   group_barrier(g);
   return HODLR_OK;
@@ -149,7 +171,21 @@ hodlr_status hodlr_group_create(int32_t nranks, void **group) {
   return HODLR_OK;
 }
 
-void hodlr_group_destroy(void *group) { delete (HodlrGroup *)group; }
+void hodlr_group_destroy(void *group) {
+  HodlrGroup *g = (HodlrGroup *)group;
+  if (!g) return;
+  for (void *p : g->rec) cudaFree(p);
+  delete g;
+}
+
+hodlr_status hodlr_group_mode(void *group, int32_t mode) {
+  HodlrGroup *g = (HodlrGroup *)group;
+  if (!g || mode < 0 || mode > 2) return hodlr_set_error(HODLR_EINVAL, "group_mode: bad arguments");
+  if (mode == 2 && g->rec.empty()) return hodlr_set_error(HODLR_ESTATE, "group_mode: nothing recorded");
+  if (mode == 1) { for (void *p : g->rec) cudaFree(p); g->rec.clear(); g->rec_bytes.clear(); }
+  g->mode = mode; g->replay_next = 0;
+  return HODLR_OK;
+}
 
 hodlr_status hodlr_dist_plan(int64_t n, int32_t leaf, int32_t rank, int32_t nranks, int32_t *kappa, int32_t *t,
                              int64_t *row_lo, int64_t *row_hi, int64_t *leaf_lo, int64_t *leaf_hi) {

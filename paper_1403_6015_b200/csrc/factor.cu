@@ -402,7 +402,9 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
     int per_sm = 0;
     HCUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tree_top<true>, TT, smem));
     if (per_sm < 1) return hodlr_set_error(HODLR_EINVAL, "factor: coupling system too large for one SM");
-    const int grid = (int)std::min<long long>(maxcnt, (long long)nsm * per_sm);
+    long long gmax = (long long)nsm * per_sm;
+    if (h->coop_ctas > 0) gmax = std::min<long long>(gmax, h->coop_ctas);
+    const int grid = (int)std::min<long long>(maxcnt, gmax);
     const TreeCtx *pc = h->d_treectx;
     int nlev = (int)top.size();
     void *args[] = {(void *)&pc, (void *)&nlev};

@@ -20,7 +20,6 @@
 #define TREE_TOP_MAXLEV HODLR_MAXDEPTH   // levels of one persistent upper-tree launch
 #define ACA_MAXCAP 64      // hard ceiling on the ACA rank cap (records/state are sized by it)
 #define ACA_RECW (4 + ACA_MAXCAP)
-#define ACA_GSZ (ACA_MAXCAP * (ACA_MAXCAP + 1) / 2)   // packed Gram matrix of one factor side
 #ifndef ACA_SUB
 #define ACA_SUB 256        // threads per ACA CTA == sub-tile width
 #endif
@@ -68,41 +67,6 @@ __device__ __forceinline__ double kval(const KParams &kp, double d) {
   else if (kp.kern >= HODLR_IMQ) arg = -kp.alpha * log(fma(d * d, kp.c, 1.0));
   return kp.a2 * pre * exp(arg);
 }
-// The same covariance functions in the oracle's operation order (the oracle's covariance function, built without FMA
-// contraction): explicitly rounded operations, ell divided rather than multiplied by a reciprocal.  The ACA's pivots
-// and ranks are FP-derived (DESIGN.md R11); evaluating its entries (and residual updates) in the oracle's order keeps
-// its decisions the oracle's up to ulp differences of exp / log / pow between the two math libraries (R17).
-__device__ __forceinline__ double kval_o(const KParams &kp, double d) {
-  switch (kp.kern) {
-    case HODLR_SE: return __dmul_rn(kp.a2, exp(-div_exact(__dmul_rn(d, d), kp.c2, kp.rc2)));
-    case HODLR_EXP: return __dmul_rn(kp.a2, exp(-div_exact(fabs(d), kp.ell, kp.rell)));
-    case HODLR_IMQ: {
-      const double q = div_exact(d, kp.ell, kp.rell);
-      return __ddiv_rn(kp.a2, __dsqrt_rn(__dadd_rn(1.0, __dmul_rn(q, q))));
-    }
-    case HODLR_RQ: {
-      const double q = div_exact(d, kp.ell, kp.rell);
-      return __dmul_rn(kp.a2, pow(__dadd_rn(1.0, __dmul_rn(q, q)), -kp.alpha));
-    }
-    case HODLR_MATERN32: {
-      const double s = div_exact(__dmul_rn(kp.sq, fabs(d)), kp.ell, kp.rell);
-      return __dmul_rn(__dmul_rn(kp.a2, __dadd_rn(1.0, s)), exp(-s));
-    }
-    default: {                                   // HODLR_MATERN52
-      const double s = div_exact(__dmul_rn(kp.sq, fabs(d)), kp.ell, kp.rell);
-      const double p = __dadd_rn(__dadd_rn(1.0, s), __ddiv_rn(__dmul_rn(s, s), 3.0));
-      return __dmul_rn(__dmul_rn(kp.a2, p), exp(-s));
-    }
-  }
-}
-__device__ __forceinline__ double kval_o_se(const KParams &kp, double d) {
-  return __dmul_rn(kp.a2, exp(-div_exact(__dmul_rn(d, d), kp.c2, kp.rc2)));
-}
-template <bool SEO> __device__ __forceinline__ double kval_ot(const KParams &kp, double d) {
-  if (SEO) return kval_o_se(kp, d);
-  return kval_o(kp, d);
-}
-
 // SEO: the launch knows the kernel is SE (the bench / config 1, 3, 5 path): exactly the SE code, nothing else inlined
 template <bool SEO> __device__ __forceinline__ double kval_t(const KParams &kp, double d) {
   if (SEO) return kp.a2 * exp(-(d * d) * kp.c);
@@ -173,7 +137,6 @@ struct AcaCtx {
   int *step;                // step counter of the device loop
   int maxsteps;
   int nitems;               // items of this pass (the persistent step kernel strides over them)
-  double *gram;             // per big block: packed G_U = U'^T U', then G_V = V'^T V' 
   const int *forced;        // test hook (hodlr_opts.forced_ranks): stop block b at exactly forced[b] terms, or NULL
 };
 
@@ -213,6 +176,8 @@ struct hodlr_s {
   long long rows_max;        // max subtree rows over the ranks (allgather slice size of the solution)
   int state;                 // 1 built, 2 factored, -1 factor failed
   int aug;                   // right-hand sides fused into the factorization (0 or 1)
+  int coop_ctas;             // cap on the CTAs of the persistent (cooperative) launches, 0 = the whole GPU: concurrent
+                             // problems (the config-4 sweep) leave each other room instead of serialising
   const double *y_aug;       // that right-hand side (device, original order) during hodlr_factor_solve
   int launches;              // kernels launched by the current call
   int aca_steps;
@@ -346,6 +311,67 @@ __device__ __forceinline__ void acc_fma_dd(Acc2 &A, double a, double bh, double 
 }
 __device__ __forceinline__ double acc_val(const Acc2 &A) { return A.s + A.c; }
 __device__ __forceinline__ void acc_dd(const Acc2 &A, double &hi, double &lo) { two_sum(A.s, A.c, hi, lo); }
+
+// exp(x) correctly rounded for x in (-708, 0] (outside: the library exp), for the ACA entries (R17): the
+// host libm's exp is correctly rounded in all but ~0.1% of arguments while CUDA's exp differs from it in ~6%; at
+// eps = 1e-12 the ACA residuals are rounding noise near the stopping threshold, so entry-level differences flip
+// rank decisions.  x = k ln2/512 + r (Cody-Waite in three parts, r as a double-double), exp(r) - 1 by a degree-5
+// polynomial (|r| <= ln2/1024, truncation 2^-72 relative), 2^(j/512) from a double-double table, one final rounding.
+#include "exp_table.cuh"
+__device__ __forceinline__ double exp_cr(double x) {
+  if (!(x > -708.0) || x > 0.0) return exp(x);
+  const double kd = rint(x * INV_LN2_512);
+  const int k = (int)kd;
+  const double t = fma(-kd, LN2_512_HI, x);             // exact: k * LN2_512_HI has <= 53 bits
+  double p_hi, p_lo; two_prod(kd, LN2_512_LO, p_hi, p_lo);
+  double r_hi, r_lo; two_sum(t, -p_hi, r_hi, r_lo);
+  r_lo = r_lo - p_lo - kd * LN2_512_LO2;
+  const double q = r_hi * r_hi * (0.5 + r_hi * (1.0 / 6.0 + r_hi * (1.0 / 24.0 + r_hi * (1.0 / 120.0))));
+  double a_hi, a_lo; two_sum(r_hi, q, a_hi, a_lo);
+  a_lo += r_lo + r_lo * r_hi;                          // exp(r) - 1 = a_hi + a_lo
+  const int j = k & 511, m = k >> 9;                   // k = 512 m + j
+  const double Th = EXP2_HI[j], Tl = EXP2_LO[j];
+  double pp_hi, pp_lo, s_hi, s_lo;
+  two_prod(Th, a_hi, pp_hi, pp_lo);
+  two_sum(Th, pp_hi, s_hi, s_lo);
+  const double lo = s_lo + pp_lo + Tl + Th * a_lo + Tl * a_hi;
+  return scalbn(s_hi + lo, m);
+}
+
+// The same covariance functions in the oracle's operation order (the oracle's covariance function, built without FMA
+// contraction): explicitly rounded operations, ell divided rather than multiplied by a reciprocal.  The ACA's pivots
+// and ranks are FP-derived (DESIGN.md R11); evaluating its entries (and residual updates) in the oracle's order keeps
+// its decisions the oracle's up to ulp differences of exp / log / pow between the two math libraries (R17).
+__device__ __forceinline__ double kval_o(const KParams &kp, double d) {
+  switch (kp.kern) {
+    case HODLR_SE: return __dmul_rn(kp.a2, exp_cr(-div_exact(__dmul_rn(d, d), kp.c2, kp.rc2)));
+    case HODLR_EXP: return __dmul_rn(kp.a2, exp_cr(-div_exact(fabs(d), kp.ell, kp.rell)));
+    case HODLR_IMQ: {
+      const double q = div_exact(d, kp.ell, kp.rell);
+      return __ddiv_rn(kp.a2, __dsqrt_rn(__dadd_rn(1.0, __dmul_rn(q, q))));
+    }
+    case HODLR_RQ: {
+      const double q = div_exact(d, kp.ell, kp.rell);
+      return __dmul_rn(kp.a2, pow(__dadd_rn(1.0, __dmul_rn(q, q)), -kp.alpha));
+    }
+    case HODLR_MATERN32: {
+      const double s = div_exact(__dmul_rn(kp.sq, fabs(d)), kp.ell, kp.rell);
+      return __dmul_rn(__dmul_rn(kp.a2, __dadd_rn(1.0, s)), exp_cr(-s));
+    }
+    default: {                                   // HODLR_MATERN52
+      const double s = div_exact(__dmul_rn(kp.sq, fabs(d)), kp.ell, kp.rell);
+      const double p = __dadd_rn(__dadd_rn(1.0, s), __ddiv_rn(__dmul_rn(s, s), 3.0));
+      return __dmul_rn(__dmul_rn(kp.a2, p), exp_cr(-s));
+    }
+  }
+}
+__device__ __forceinline__ double kval_o_se(const KParams &kp, double d) {
+  return __dmul_rn(kp.a2, exp_cr(-div_exact(__dmul_rn(d, d), kp.c2, kp.rc2)));
+}
+template <bool SEO> __device__ __forceinline__ double kval_ot(const KParams &kp, double d) {
+  if (SEO) return kval_o_se(kp, d);
+  return kval_o(kp, d);
+}
 
 // ----------------------------------------------------------------------------------------------
 // Storage helpers shared by the factor and solve kernels.

@@ -28,7 +28,10 @@ extern "C" hodlr_status gp_loglik_sweep(const double *x, const double *y, int64_
   std::vector<hodlr_status> stat(B, HODLR_OK);
   std::vector<std::string> msg(B);
   std::atomic<int> next(0);
-  const int W = std::max(1, std::min<int>(workers > 0 ? workers : 4, (int)mine.size()));
+  const int W = std::max(1, std::min<int>(workers > 0 ? workers : 8, (int)mine.size()));
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int coop = W > 1 ? std::max(16, 2 * nsm / W) : 0;
   auto work = [&]() {
     cudaSetDevice(dev);
     cudaStream_t s;
@@ -40,6 +43,7 @@ extern "C" hodlr_status gp_loglik_sweep(const double *x, const double *y, int64_
       hodlr_t h = nullptr;
       double ll = -INFINITY;
       hodlr_status st = hodlr_build(x, n, kernel, thetas + 2 * b, sigma2s[b], leaf, eps, nullptr, nullptr, s, &h);
+      if (st == HODLR_OK) h->coop_ctas = coop;  // W problems in flight: each upper-tree launch takes ~1/W of the GPU
       double quad = 0.0, ld = 0.0;
       // y fused into the factorization: y^T C^{-1} y is the root's Pi, no solve pass at all
       if (st == HODLR_OK) st = hodlr_factor_solve(h, y, nullptr, &quad);

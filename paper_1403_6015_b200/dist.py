@@ -23,6 +23,10 @@ class Group:
         hb._check(hb.load().hodlr_group_create(self.nranks, C.byref(p)))
         self.ptr = p.value
 
+    def mode(self, m: int):
+        """0 normal, 1 record the next sharded run's exchanges, 2 solo replay of rank 0 (scaling projection)."""
+        hb._check(hb.load().hodlr_group_mode(self.ptr, int(m)))
+
     def close(self):
         if self.ptr:
             hb.load().hodlr_group_destroy(self.ptr)
@@ -59,10 +63,10 @@ class Dist:
         return cls(rank, ws, nccl_id=obj[0])
 
 
-def run_virtual_ranks(nranks: int, fn):
-    """Run fn(rank, Dist) for every virtual rank on its own host thread (one shared Group); returns the list of
-    results in rank order and re-raises the first exception."""
-    g = Group(nranks)
+def run_virtual_ranks(nranks: int, fn, group: Group | None = None):
+    """Run fn(rank, Dist) for every virtual rank on its own host thread (one shared Group, created here unless
+    given); returns the list of results in rank order and re-raises the first exception."""
+    g = group or Group(nranks)
     out, errs = [None] * nranks, [None] * nranks
 
     def body(r):
@@ -76,7 +80,8 @@ def run_virtual_ranks(nranks: int, fn):
         t.start()
     for t in th:
         t.join()
-    g.close()
+    if group is None:
+        g.close()
     for e in errs:
         if e is not None:
             raise e

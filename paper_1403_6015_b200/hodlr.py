@@ -23,7 +23,7 @@ EXPORTS = ("hodlr_build", "hodlr_factor", "hodlr_factor_solve", "hodlr_cache_tri
            "hodlr_info",
            "hodlr_get_order", "hodlr_get_tree", "hodlr_get_logdet_parts", "hodlr_free", "hodlr_last_error",
            "hodlr_version", "hodlr_launch_count", "hodlr_nccl_unique_id", "hodlr_group_create",
-           "hodlr_group_destroy", "hodlr_dist_plan", "gp_loglik_sweep")
+           "hodlr_group_destroy", "hodlr_group_mode", "hodlr_dist_plan", "gp_loglik_sweep")
 
 
 class HodlrError(RuntimeError):
@@ -98,6 +98,7 @@ def load(build_if_missing: bool = True):
         lib.hodlr_nccl_unique_id.argtypes = [P]; lib.hodlr_nccl_unique_id.restype = I32
         lib.hodlr_group_create.argtypes = [I32, P]; lib.hodlr_group_create.restype = I32
         lib.hodlr_group_destroy.argtypes = [P]; lib.hodlr_group_destroy.restype = None
+        lib.hodlr_group_mode.argtypes = [P, I32]; lib.hodlr_group_mode.restype = I32
         lib.hodlr_dist_plan.argtypes = [I64, I32, I32, I32, P, P, P, P, P, P]; lib.hodlr_dist_plan.restype = I32
         lib.gp_loglik_sweep.argtypes = [P, P, I64, I32, P, P, I32, I32, D, P, P, I32, P]
         lib.gp_loglik_sweep.restype = I32

@@ -154,3 +154,26 @@ def test_virtual_ranks_factor_solve(hb, name, n, P):
         assert abs(ld - ld1) <= 1e-13 * abs(ld1)
         assert abs(q - q1) <= 1e-12 * abs(q1)
         assert np.linalg.norm(xs - x1) <= 1e-12 * np.linalg.norm(x1)
+
+
+def test_group_record_replay(hb):
+    """hodlr_group_mode (the scaling projection of tools/project_scaling.py): rank 0 replayed alone against the
+    recorded exchanges of a full P-rank run computes the same log det and solution as in that run."""
+    from paper_1403_6015_b200.dist import Group, Dist, run_virtual_ranks
+    cfg = inputs.scaled(inputs.CONFIGS["cfg3"], 1 << 15)
+    xd = torch.from_numpy(inputs.points(cfg)).cuda(); yd = torch.from_numpy(inputs.rhs(cfg)).cuda()
+
+    def step(d):
+        h = hb.HODLR(xd, cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, 1e-12, dist=d)
+        s, q = h.factor_solve(yd)
+        out = (h.logdet(), q, s.cpu().numpy())
+        h.close()
+        return out
+    g = Group(4)
+    g.mode(1)
+    rec = run_virtual_ranks(4, lambda r, d: step(d), g)
+    g.mode(2)
+    ld, q, s = step(Dist(0, 4, group=g))
+    g.close()
+    assert ld == rec[0][0] and q == rec[0][1]
+    np.testing.assert_array_equal(s, rec[0][2])

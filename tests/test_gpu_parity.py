@@ -262,12 +262,13 @@ def test_full_size_cfg5_vs_oracle_golden(hb):
         xg, _ = g.factor_solve(yd)
         xg = xg.cpu().numpy()
         ld_g = g.logdet()
+        r_g = g.tree()[2]
         if mode == "forced":
-            np.testing.assert_array_equal(g.tree()[2], gold["ranks"])
+            np.testing.assert_array_equal(r_g, gold["ranks"])
         g.close()
         rel = np.linalg.norm(xg[idx] - xo) / np.linalg.norm(xo)
         res[mode] = (abs(ld_g - ld_o) / abs(ld_o), rel, xg)
-        print(f"[cfg5 full {mode} ranks] logdet rel {res[mode][0]:.2e} sampled solve rel {rel:.2e}")
+        print(f"[cfg5 full {mode} ranks] logdet rel {res[mode][0]:.2e} sampled solve rel {rel:.2e} rank mismatches {int(np.sum(r_g != gold['ranks']))}")
         assert abs(ld_g - ld_o) <= LD_TOL * abs(ld_o)
     assert res["forced"][1] <= X_TOL
     assert res["free"][1] <= 2 * X_TOL

@@ -44,7 +44,7 @@ ell, s2 = inputs.sweep_settings(cfg)
 x = torch.from_numpy(inputs.points(cfg)).cuda(); y = torch.from_numpy(inputs.rhs(cfg)).cuda()
 th = np.stack([np.full(cfg.sweep, cfg.a), ell], 1)
 sw = {}
-for workers in (1, 4, 8, 16):
+for workers in (1, 4, 8, 16, 32):
     hb.gp_loglik_sweep(x, y, cfg.kernel, th, s2, cfg.leaf, cfg.eps, workers=workers)
     torch.cuda.synchronize(); t0 = time.perf_counter()
     v = hb.gp_loglik_sweep(x, y, cfg.kernel, th, s2, cfg.leaf, cfg.eps, workers=workers)

@@ -1,0 +1,2 @@
+out=gpurun_out/r2p; mkdir -p $out
+timeout 3000 python -m pytest tests -m gpu -q 2>&1 | tail -15
