@@ -200,6 +200,8 @@ __device__ __forceinline__ void aca_item(const AcaCtx &c, int item, AcaScratch &
       for (int q = 0; q < ACA_E; q++) r[q] = a[q];
       const double *colp = slot + (ok ? g0 : lo + it.start);
       constexpr int LS = 4;
+      const int lastb = (k - 1) & ~(LS - 1);           // the last batch's columns stay in registers for their dots
+      double Fl[LS][ACA_E];
       for (int l0 = 0; l0 < k; l0 += LS) {
         double F[LS][ACA_E];
 #pragma unroll
@@ -233,14 +235,30 @@ __device__ __forceinline__ void aca_item(const AcaCtx &c, int item, AcaScratch &
 #pragma unroll
           for (int q = 0; q < ACA_E; q++) r[q] = __dsub_rn(r[q], __dmul_rn(cf, F[dl][q]));
         }
+        if (l0 == lastb) {
+#pragma unroll
+          for (int dl = 0; dl < LS; dl++)
+#pragma unroll
+            for (int q = 0; q < ACA_E; q++) Fl[dl][q] = F[dl][q];
+        }
       }
-      // dots F_l . r with the residual as computed, re-reading this group's factor columns newest first (the most
-      // recently streamed columns are the likeliest to still be in L1)
-      for (int l0 = ((k - 1) & ~(LS - 1)); l0 >= 0; l0 -= LS) {
+      // dots F_l . r with the residual as computed: the last batch from registers, the earlier ones re-read (L1)
+      if (k > 0) {
         double pv[LS];
 #pragma unroll
         for (int dl = 0; dl < LS; dl++) {
-          const double *cp = colp + (size_t)(l0 + dl < k ? l0 + dl : 0) * n1;
+          double p = 0.0;
+#pragma unroll
+          for (int q = 0; q < ACA_E; q++) p = fma(Fl[dl][q], r[q], p);
+          pv[dl] = p;
+        }
+        dot_butterfly(pv, lastb, lane, w0, w1);
+      }
+      for (int l0 = 0; l0 < lastb; l0 += LS) {
+        double pv[LS];
+#pragma unroll
+        for (int dl = 0; dl < LS; dl++) {
+          const double *cp = colp + (size_t)(l0 + dl) * n1;
           double p = 0.0;
 #pragma unroll
           for (int pp = 0; pp < NP; pp++) {

@@ -59,7 +59,7 @@ def test_apply_inverts_solve(hb, name, cfg, eps):
     r = g.apply(g.solve(yd)) - yd
     rel = (torch.linalg.norm(r) / torch.linalg.norm(yd)).item()
     print(f"[apply] {name} ||apply(solve(y)) - y|| / ||y|| = {rel:.2e}")
-    assert rel <= 1e-8, rel
+    assert rel <= 2e-10, rel                # ~cond(C) x 1e-16 at these configs (cfg2: 1.2e-10)
     g.close()
 
 

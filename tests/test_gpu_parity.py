@@ -208,21 +208,25 @@ def test_errors(hb):
 
 
 def test_full_size_cfg3_bench_config(hb):
-    """BASELINE.json config 3 at full size in the bench's configuration (n = 2^20, eps = 1e-10):
-    sampled rows of the residual C x - y computed one by one on the CPU, and the oracle's log det."""
+    """BASELINE.json config 3 at full size in the bench's configuration (n = 2^20, eps = 1e-10, the fused
+    factor_solve the bench times): log det <= 1e-9 and solve <= 1e-9 against the oracle at the same eps, and the
+    exact residual C x - y on 64 sampled rows (assembled row by row) within 2x the oracle's on the same rows."""
     cfg = inputs.CONFIGS["cfg3"]
     x = inputs.points(cfg); y = inputs.rhs(cfg)
-    g = hb.HODLR(torch.from_numpy(x).cuda(), cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, cfg.eps).factor()
+    g = hb.HODLR(torch.from_numpy(x).cuda(), cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, cfg.eps)
+    xg, _ = g.factor_solve(torch.from_numpy(y).cuda())
+    xg = xg.cpu().numpy()
     ld_g = g.logdet()
-    xg = g.solve(torch.from_numpy(y).cuda()).cpu().numpy()
-    rng = np.random.default_rng(123)
-    rows = rng.choice(cfg.n, 64, replace=False)
-    for i in rows:
-        ci = np.exp(-(x[i] - x) ** 2 / (2 * cfg.ell ** 2)) * cfg.a ** 2
-        ci[i] += cfg.sigma2
-        assert abs(ci @ xg - y[i]) <= 1e-6 * np.abs(y).max()
     o = OracleHODLR(x, cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, cfg.eps).factor()
+    xo = o.solve(y)
+    rel = np.linalg.norm(xg - xo) / np.linalg.norm(xo)
+    print(f"[full cfg3 eps=1e-10 fused] logdet rel {abs(ld_g - o.logdet()) / abs(o.logdet()):.2e} solve rel {rel:.2e}")
     assert abs(ld_g - o.logdet()) <= LD_TOL * abs(o.logdet())
+    assert rel <= X_TOL
+    rows = np.random.default_rng(123).choice(cfg.n, 64, replace=False)
+    r_g = residual_rows_torch(x, y, xg, rows, cfg.kernel, cfg.a, cfg.ell, cfg.sigma2)
+    r_o = residual_rows_torch(x, y, xo, rows, cfg.kernel, cfg.a, cfg.ell, cfg.sigma2)
+    assert np.linalg.norm(r_g) <= 2 * np.linalg.norm(r_o)
 
 
 def residual_rows_torch(x, y, sol, rows, kernel, a, ell, s2):
@@ -244,8 +248,8 @@ def test_full_size_cfg5_vs_oracle_golden(hb):
     eps = 1e-12, via tests/golden/cfg5_eps1e-12.npz (written by tools/make_golden.py, which calls only oracle/: the
     oracle needs ~17 min and ~45 GB here).  (a) With the oracle's per-block ranks (hodlr_opts.forced_ranks): log det
     <= 1e-9 and the 4096 sampled solution entries <= 1e-9 relative (arithmetic parity).  (b) With the GPU's own ACA
-    ranks: log det <= 1e-9, sampled entries at the compression floor, and the exact residual on 128 sampled rows
-    within 10x the oracle's own residual on the same rows."""
+    ranks (a handful of the 65535 blocks differ, R17): the same gates, and the exact residual on 128
+    sampled rows within 2x the oracle's own residual on the same rows."""
     import hashlib
     import os
     gold = np.load(os.path.join(os.path.dirname(__file__), "golden", "cfg5_eps1e-12.npz"))
@@ -271,18 +275,35 @@ def test_full_size_cfg5_vs_oracle_golden(hb):
         print(f"[cfg5 full {mode} ranks] logdet rel {res[mode][0]:.2e} sampled solve rel {rel:.2e} rank mismatches {int(np.sum(r_g != gold['ranks']))}")
         assert abs(ld_g - ld_o) <= LD_TOL * abs(ld_o)
     assert res["forced"][1] <= X_TOL
-    assert res["free"][1] <= 2 * X_TOL
+    assert res["free"][1] <= X_TOL
     r_g = residual_rows_torch(x, y, res["free"][2], gold["res_idx"], cfg.kernel, cfg.a, cfg.ell, cfg.sigma2)
     r_o = gold["res_oracle"]
     print(f"[cfg5 full] residual rows: gpu {np.linalg.norm(r_g):.3e} oracle {np.linalg.norm(r_o):.3e}")
-    assert np.linalg.norm(r_g) <= 10 * np.linalg.norm(r_o)
+    assert np.linalg.norm(r_g) <= 2 * np.linalg.norm(r_o)
+
+
+def test_full_size_cfg5_shuffled_input_bitwise(hb):
+    """Config 5 at full size (n = 2^23, eps = 1e-10): a shuffled copy of the input gives a bitwise-identical log
+    det and the same solution permuted (the stable sort makes the factorization independent of the input order,
+    ties included)."""
+    cfg = inputs.CONFIGS["cfg5"]
+    x = inputs.points(cfg); y = inputs.rhs(cfg)
+    xd = torch.from_numpy(x).cuda(); yd = torch.from_numpy(y).cuda()
+    g = hb.HODLR(xd, cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, cfg.eps)
+    s1, _ = g.factor_solve(yd); ld1 = g.logdet(); s1 = s1.cpu().numpy(); g.close()
+    perm = np.random.default_rng(321).permutation(cfg.n)
+    pd = torch.from_numpy(perm).cuda()
+    g2 = hb.HODLR(xd[pd].contiguous(), cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, cfg.eps)
+    s2, _ = g2.factor_solve(yd[pd].contiguous()); ld2 = g2.logdet(); s2 = s2.cpu().numpy(); g2.close()
+    assert ld2 == ld1
+    np.testing.assert_array_equal(s2, s1[perm])
 
 
 def test_full_size_cfg3_parity_eps12(hb):
-    """Config 3 at full size (n = 2^20) at the parity epsilon 1e-12 (north_star): log det <= 1e-9 relative to the
-    oracle; the solve agrees to the measured floor of the approximation (R15: both solutions have
-    exact relative residuals ~1e-9 at cond(C) ~ 2.6e6), gated at 2e-9, and the GPU solution's exact residual on
-    sampled rows (computed one by one on the CPU) is no worse than 3x the oracle's on the same rows."""
+    """Config 3 at full size (n = 2^20) at the parity epsilon 1e-12 (north_star): log det and solve <= 1e-9 relative to
+    the oracle (measured 2e-14 and 1.8e-10, every per-block ACA rank equal to the oracle's; the twin floor is
+    2.4e-10, R15), and the GPU solution's exact residual on sampled rows (computed one by one on the CPU)
+    within 2x the oracle's on the same rows."""
     cfg = inputs.CONFIGS["cfg3"]
     x = inputs.points(cfg); y = inputs.rhs(cfg)
     o, g, ro, rg = run_both(hb, x, y, cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, 1e-12)
@@ -291,14 +312,14 @@ def test_full_size_cfg3_parity_eps12(hb):
     assert abs(ld_g - ld_o) <= LD_TOL * abs(ld_o)
     rel = np.linalg.norm(x_g - x_o) / np.linalg.norm(x_o)
     print(f"[full cfg3 eps=1e-12] logdet rel {abs(ld_g - ld_o) / abs(ld_o):.2e} solve rel {rel:.2e}")
-    assert rel <= 2e-9
+    assert rel <= X_TOL
     rows = np.random.default_rng(7).choice(cfg.n, 48, replace=False)
     rg_, ro_ = [], []
     for i in rows:
         ci = np.exp(-(x[i] - x) ** 2 / (2 * cfg.ell ** 2)) * cfg.a ** 2
         ci[i] += cfg.sigma2
         rg_.append(ci @ x_g - y[i]); ro_.append(ci @ x_o - y[i])
-    assert np.linalg.norm(rg_) <= 3 * np.linalg.norm(ro_) + 1e-12 * np.linalg.norm(y[rows])
+    assert np.linalg.norm(rg_) <= 2 * np.linalg.norm(ro_) + 1e-12 * np.linalg.norm(y[rows])
 
 
 def test_cfg5_duplicates_2e18(hb):
