@@ -40,7 +40,7 @@ __global__ void k_aca_init(AcaCtx c, int nblocks, int cap) {
   long long m1 = c.hi[c1] - c.lo[c1], m2 = c.hi[c2] - c.lo[c2];
   long long mn = m1 < m2 ? m1 : m2;
   AcaState *s = &c.st[b];
-  s->k = 0; s->done = 0; s->cnt_r = 0; s->cnt_c = 0; s->raw_last = 0;
+  s->k = 0; s->done = 0; s->cnt_r = 0; s->cnt_c = 0; s->raw_last = 0; s->donly = 0;
   s->cap = (int)(cap < mn ? cap : mn);
   s->ipiv = m1 - 1;                      // DESIGN.md R2: last row of c1 (the point nearest c2)
   s->jpiv = -1; s->pivval = 0.0; s->S2 = 0.0; s->nv2 = 0.0;
@@ -95,7 +95,10 @@ __device__ __forceinline__ void block_argmax_n2(double &ba, long long &bi, doubl
 #ifndef ACA_FUSED_SMALL
 #define ACA_FUSED_SMALL 128        // fused blocks with both sides <= this run in 64-thread CTAs
 #endif
-constexpr int ACA_E = 4;                       // elements per thread per sub-tile (measured: 2 with three CTAs per
+#ifndef ACA_E_DEF
+#define ACA_E_DEF 4
+#endif
+constexpr int ACA_E = ACA_E_DEF;                       // elements per thread per sub-tile (measured: 2 with three CTAs per
                                                // SM is slower)
 constexpr int ACA_TILE = ACA_SUB * ACA_E;
 
@@ -123,13 +126,21 @@ struct AcaScratch {
   double s_abs[ACA_SUB / 32], s_val[ACA_SUB / 32], s_n2[ACA_SUB / 32];
   long long s_idx[ACA_SUB / 32];
   double part[ACA_SUB / 32][4 + ACA_MAXCAP];
-  double tot[1 + ACA_MAXCAP];
-  double dnew[ACA_MAXCAP];
+  double tot[ACA_MAXCAP];
   int amLast;
 };
 
 // One item (a chunk of one side of one active big block) of a step's row (ROW) or column pass; c is the pass's
 // context in shared memory (global stores cannot alias it).  CTA-uniform control flow.
+//
+// Lagged stop test.  The ||S||_F update of term k-1 needs the dots F_{k-1} . F_l (l <= k-1) of its new columns
+// (U'_{k-1} with the U'_l, V'_{k-1} with the V'_l).  Step k's passes stream every one of those columns anyway for
+// the residual, with F_{k-1} among them, so they form the dots in the same sweep -- one read of the factor columns
+// per pass -- and the stop test of term k-1 runs at the end of step k's column pass.  A block that stops there
+// keeps k terms (term k, computed by the same step, is discarded): the oracle's ranks, for one extra step per
+// block.  The cases that end the oracle's loop without the test (k + 1 == min(m1, m2), no unused nonzero pivot
+// row, forced ranks) end immediately; at the rank cap (k + 1 == cap, where the test decides between rank cap and
+// ERANKCAP) one more step runs in dots-only mode (no new column is stored).
 template <bool ROW, bool SEO>
 __device__ __forceinline__ void aca_item(const AcaCtx &c, int item, AcaScratch &S) {
   double *coef = S.coef;
@@ -137,12 +148,12 @@ __device__ __forceinline__ void aca_item(const AcaCtx &c, int item, AcaScratch &
   double *s_abs = S.s_abs, *s_val = S.s_val, *s_n2 = S.s_n2;
   long long *s_idx = S.s_idx;
   double (*part)[4 + ACA_MAXCAP] = S.part;
-  double *tot = S.tot, *dnew = S.dnew;
+  double *tot = S.tot;
   int *flags = c.flags;
   const AcaItem it = c.items[item];
   const int b = it.block;
   AcaState *st = &c.st[b];
-  const int done = __ldcg(&st->done), k = __ldcg(&st->k);          // one round of loads for the state
+  const int done = __ldcg(&st->done), k = __ldcg(&st->k), donly = __ldcg(&st->donly);   // one round of loads
   const long long piv = ROW ? __ldcg(&st->ipiv) : __ldcg(&st->jpiv);
   if (done) return;
   const long long n = c.n, ldx = c.ldx;
@@ -153,131 +164,115 @@ __device__ __forceinline__ void aca_item(const AcaCtx &c, int item, AcaScratch &
   const long long ilen = it.len;
   // The row pass of step k divides the previous step's column V[:, k-1] (stored as the raw residual v~) by that
   // step's pivot as it streams it -- the oracle's V = v~ / v~_jk (R16), written back in place -- so no separate pass
-  // over the column is needed; a block that finishes in a column pass gets its last column normalised by
-  // k_aca_finish.  (ROW: pivval here is still the previous step's pivot: this pass's last CTA sets the new one
-  // only after every CTA has read the state.)
+  // over the column is needed; a block that finishes in a column pass without a further step gets its last column
+  // normalised by k_aca_finish.  (ROW: pivval here is still the previous step's pivot: this pass's last CTA sets the
+  // new one only after every CTA has read the state.)
   const double pvp = ROW ? __ldcg(&st->pivval) : 1.0;
   const double rpvp = ROW && k > 0 ? __drcp_rn(pvp) : 1.0;
   const long long pg = ROW ? lo1 + piv : lo2 + piv;               // fixed row (ROW) / column (COL)
   const double xp = c.xs[pg];
   const long long lo = ROW ? lo2 : lo1;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const bool store = !donly;                                       // dots-only step: column k does not exist
   // (zero-padded to a multiple of 4: the vector path runs whole batches of 4 columns without masks)
   for (int l = t; l < ((k + 3) & ~3); l += ACA_SUB) coef[l] = l < k ? slot[(long long)l * ldx + pg] : 0.0;
   __syncthreads();
-  // dots F_l . a: for each batch of 4 columns the 4 per-lane partials are reduced over the warp by a transposed
-  // butterfly (6 shuffles); lane L then holds column l0 + ((L >> 3) & 3) and keeps it when batch l0 / 4 is
-  // congruent to L mod 8 (w0 for l < 32, w1 for l >= 32)
+  // dots F_{k-1} . F_l: for each batch of 4 columns the 4 per-lane partials are reduced over the warp by a
+  // transposed butterfly (6 shuffles); lane L then holds column l0 + ((L >> 3) & 3) and keeps it when batch l0 / 4
+  // is congruent to L mod 8 (w0 for l < 32, w1 for l >= 32)
   double w0 = 0.0, w1 = 0.0;
-  double ba = 0.0, bv = 0.0, n2 = 0.0; long long bi = -1;
+  double ba = 0.0, bv = 0.0; long long bi = -1;
   const long long end = it.start + ilen;
-  const size_t n1 = (size_t)ldx, n2s = 2 * (size_t)ldx, n3 = 3 * (size_t)ldx;   // factor column stride
+  const size_t n1 = (size_t)ldx;                   // factor column stride
   // vector path: thread t takes the ACA_E consecutive elements of each ACA_TILE-element sub-tile (double2
   // loads/stores); needs 16-byte alignment of every column segment (n and the chunk start even) -- the
   // scalar loop below handles the rest
   const bool vec = ((ldx | (lo + it.start)) & 1) == 0 && (ilen % ACA_E) == 0;
   constexpr int NP = ACA_E / 2;                  // double2 pairs per thread
+  constexpr int LS = 4;                          // factor columns per batch of loads
   if (vec) {
+    // the coordinates and used flags of the next tile are loaded one tile ahead (their latency overlaps this tile)
+    double2 xn[NP]; uchar2 un[NP];
+    auto load_xu = [&](long long s0) {
+      const long long g = s0 + ACA_E * t < end ? lo + s0 + ACA_E * t : lo + it.start;
+#pragma unroll
+      for (int pp = 0; pp < NP; pp++) { xn[pp] = *(const double2 *)(c.xs + g + 2 * pp); un[pp] = *(const uchar2 *)(used + g + 2 * pp); }
+    };
+    load_xu(it.start);
     for (long long s0 = it.start; s0 < end; s0 += ACA_TILE) {
       const long long g0 = lo + s0 + ACA_E * t;        // elements g0 .. g0 + ACA_E - 1
       const bool ok = s0 + ACA_E * t < end;            // whole group valid (len is a multiple of ACA_E)
-      double a[ACA_E], r[ACA_E];
+      const double *colp = slot + (ok ? g0 : lo + it.start);
+      double r[ACA_E], Fk[ACA_E];
       unsigned usedm = 0;
-      if (ok) {
+      {
+        double2 xx[NP]; uchar2 uu[NP];
+#pragma unroll
+        for (int pp = 0; pp < NP; pp++) { xx[pp] = xn[pp]; uu[pp] = un[pp]; }
+        if (s0 + ACA_TILE < end) load_xu(s0 + ACA_TILE);
 #pragma unroll
         for (int pp = 0; pp < NP; pp++) {
-          const double2 xx = *(const double2 *)(c.xs + g0 + 2 * pp);
-          const uchar2 uu = *(const uchar2 *)(used + g0 + 2 * pp);
-          usedm |= ((uu.x ? 1u : 0u) | (uu.y ? 2u : 0u)) << (2 * pp);
-          a[2 * pp] = kval_ot<SEO>(c.kp, ROW ? xp - xx.x : xx.x - xp);
-          a[2 * pp + 1] = kval_ot<SEO>(c.kp, ROW ? xp - xx.y : xx.y - xp);
+          usedm |= ((uu[pp].x ? 1u : 0u) | (uu[pp].y ? 2u : 0u)) << (2 * pp);
+          r[2 * pp] = ok ? kval_ot<SEO>(c.kp, ROW ? xp - xx[pp].x : xx[pp].x - xp) : 0.0;
+          r[2 * pp + 1] = ok ? kval_ot<SEO>(c.kp, ROW ? xp - xx[pp].y : xx[pp].y - xp) : 0.0;
         }
-      } else {
-#pragma unroll
-        for (int q = 0; q < ACA_E; q++) a[q] = 0.0;
       }
+      // the newest column F_{k-1} first (normalised and stored back by the row pass)
+      if (k > 0) {
+        const double *cp = colp + (size_t)(k - 1) * n1;
 #pragma unroll
-      for (int q = 0; q < ACA_E; q++) r[q] = a[q];
-      const double *colp = slot + (ok ? g0 : lo + it.start);
-      constexpr int LS = 4;
-      const int lastb = (k - 1) & ~(LS - 1);           // the last batch's columns stay in registers for their dots
-      double Fl[LS][ACA_E];
+        for (int pp = 0; pp < NP; pp++) {
+          const double2 f = *(const double2 *)(cp + 2 * pp);
+          Fk[2 * pp] = f.x; Fk[2 * pp + 1] = f.y;
+        }
+        if (ROW) {
+#pragma unroll
+          for (int q = 0; q < ACA_E; q++) Fk[q] = div_by(Fk[q], pvp, rpvp);
+          if (ok) {
+#pragma unroll
+            for (int pp = 0; pp < NP; pp++) *(double2 *)((double *)cp + 2 * pp) = make_double2(Fk[2 * pp], Fk[2 * pp + 1]);
+          }
+        }
+      }
       for (int l0 = 0; l0 < k; l0 += LS) {
         double F[LS][ACA_E];
 #pragma unroll
         for (int dl = 0; dl < LS; dl++) {
-          // no masks: a column beyond k reads column 0 (finite) with coefficient 0; a group beyond the chunk (!ok)
-          // has a = 0 and its residual is never stored
-          const double *cp = colp + (size_t)(l0 + dl < k ? l0 + dl : 0) * n1;
+          // no masks: a column beyond k reads column 0 (finite) with coefficient 0 and its dot is never kept; a
+          // group beyond the chunk (!ok) has r = 0 and its residual is never stored
+          const int l = l0 + dl;
+          const double *cp = colp + (size_t)(l < k - 1 ? l : 0) * n1;
 #pragma unroll
           for (int pp = 0; pp < NP; pp++) {
             const double2 f = *(const double2 *)(cp + 2 * pp);
             F[dl][2 * pp] = f.x; F[dl][2 * pp + 1] = f.y;
           }
+          if (l == k - 1) {
+#pragma unroll
+            for (int q = 0; q < ACA_E; q++) F[dl][q] = Fk[q];
+          }
         }
-        if (ROW && l0 + LS >= k) {             // the batch holding column k-1: normalise it (and store it back)
-          const int dl = k - 1 - l0;
-#pragma unroll
-          for (int x = 0; x < LS; x++)
-            if (x == dl) {
-#pragma unroll
-              for (int q = 0; q < ACA_E; q++) F[x][q] = div_by(F[x][q], pvp, rpvp);
-              if (ok) {
-                double *cp = (double *)colp + (size_t)(k - 1) * n1;
-#pragma unroll
-                for (int pp = 0; pp < NP; pp++) *(double2 *)(cp + 2 * pp) = make_double2(F[x][2 * pp], F[x][2 * pp + 1]);
-              }
-            }
-        }
+        double pv[LS];
 #pragma unroll
         for (int dl = 0; dl < LS; dl++) {
           const double cf = coef[l0 + dl];
-#pragma unroll
-          for (int q = 0; q < ACA_E; q++) r[q] = __dsub_rn(r[q], __dmul_rn(cf, F[dl][q]));
-        }
-        if (l0 == lastb) {
-#pragma unroll
-          for (int dl = 0; dl < LS; dl++)
-#pragma unroll
-            for (int q = 0; q < ACA_E; q++) Fl[dl][q] = F[dl][q];
-        }
-      }
-      // dots F_l . r with the residual as computed: the last batch from registers, the earlier ones re-read (L1)
-      if (k > 0) {
-        double pv[LS];
-#pragma unroll
-        for (int dl = 0; dl < LS; dl++) {
           double p = 0.0;
 #pragma unroll
-          for (int q = 0; q < ACA_E; q++) p = fma(Fl[dl][q], r[q], p);
-          pv[dl] = p;
-        }
-        dot_butterfly(pv, lastb, lane, w0, w1);
-      }
-      for (int l0 = 0; l0 < lastb; l0 += LS) {
-        double pv[LS];
-#pragma unroll
-        for (int dl = 0; dl < LS; dl++) {
-          const double *cp = colp + (size_t)(l0 + dl) * n1;
-          double p = 0.0;
-#pragma unroll
-          for (int pp = 0; pp < NP; pp++) {
-            const double2 f = *(const double2 *)(cp + 2 * pp);
-            p = fma(f.x, r[2 * pp], fma(f.y, r[2 * pp + 1], p));
+          for (int q = 0; q < ACA_E; q++) {
+            r[q] = __dsub_rn(r[q], __dmul_rn(cf, F[dl][q]));     // the oracle's operation order (R17)
+            p = fma(Fk[q], F[dl][q], p);
           }
           pv[dl] = p;
         }
         dot_butterfly(pv, l0, lane, w0, w1);
       }
-      if (ok) {
+      if (ok && store) {
         double *outp = slot + (long long)k * ldx + g0;
 #pragma unroll
         for (int pp = 0; pp < NP; pp++) *(double2 *)(outp + 2 * pp) = make_double2(r[2 * pp], r[2 * pp + 1]);
 #pragma unroll
-        for (int q = 0; q < ACA_E; q++) {
+        for (int q = 0; q < ACA_E; q++)
           if (!((usedm >> q) & 1u) && fabs(r[q]) > ba) { ba = fabs(r[q]); bi = g0 + q - lo; bv = r[q]; }
-          n2 += r[q] * r[q];
-        }
       }
     }
   } else
@@ -286,63 +281,55 @@ __device__ __forceinline__ void aca_item(const AcaCtx &c, int item, AcaScratch &
     const int nval = (int)min((long long)ACA_E, (end - s0 - t + ACA_SUB - 1) / ACA_SUB);   // valid elements
     const double *xsp = c.xs + g0;
     const unsigned char *up = used + g0;
-    double a[ACA_E], r[ACA_E];
+    const double *colp = slot + g0;
+    double r[ACA_E], Fk[ACA_E];
     unsigned usedm = 0;                        // used flags, loaded up front (char loads cannot pass the stores)
 #pragma unroll
     for (int q = 0; q < ACA_E; q++) {
       const double xq = q < nval ? xsp[q * ACA_SUB] : xp;
       if (q < nval && up[q * ACA_SUB]) usedm |= 1u << q;
-      a[q] = q < nval ? kval_ot<SEO>(c.kp, ROW ? xp - xq : xq - xp) : 0.0;
-      r[q] = a[q];
+      r[q] = q < nval ? kval_ot<SEO>(c.kp, ROW ? xp - xq : xq - xp) : 0.0;
+      Fk[q] = 0.0;
     }
-    const double *colp = slot + g0;
-    constexpr int LS = 4;                      // factor columns per batch of loads
+    if (k > 0) {                               // the newest column, normalised and stored back by the row pass
+      double *cp = (double *)colp + (size_t)(k - 1) * n1;
+#pragma unroll
+      for (int q = 0; q < ACA_E; q++)
+        if (q < nval) {
+          Fk[q] = cp[q * ACA_SUB];
+          if (ROW) { Fk[q] = div_by(Fk[q], pvp, rpvp); cp[q * ACA_SUB] = Fk[q]; }
+        }
+    }
     for (int l0 = 0; l0 < k; l0 += LS) {
-      const double *c0 = colp + (size_t)l0 * n1;
-      const double *cl[LS] = {c0, c0 + n1, c0 + n2s, c0 + n3};
       double F[LS][ACA_E];
 #pragma unroll
-      for (int dl = 0; dl < LS; dl++)
-#pragma unroll
-        for (int q = 0; q < ACA_E; q++) F[dl][q] = (l0 + dl < k && q < nval) ? cl[dl][q * ACA_SUB] : 0.0;
-      if (ROW && l0 + LS >= k) {               // column k-1: normalise (and store back), as in the vector path
-        const int dl = k - 1 - l0;
-#pragma unroll
-        for (int x = 0; x < LS; x++)
-          if (x == dl) {
-#pragma unroll
-            for (int q = 0; q < ACA_E; q++)
-              if (q < nval) { F[x][q] = div_by(F[x][q], pvp, rpvp); ((double *)cl[x])[q * ACA_SUB] = F[x][q]; }
-          }
-      }
-#pragma unroll
       for (int dl = 0; dl < LS; dl++) {
-        const double cf = l0 + dl < k ? coef[l0 + dl] : 0.0;
+        const int l = l0 + dl;
 #pragma unroll
-        for (int q = 0; q < ACA_E; q++) r[q] = __dsub_rn(r[q], __dmul_rn(cf, F[dl][q]));
+        for (int q = 0; q < ACA_E; q++)
+          F[dl][q] = l == k - 1 ? Fk[q] : (l < k && q < nval) ? colp[(size_t)l * n1 + q * ACA_SUB] : 0.0;
       }
-    }
-    for (int l0 = 0; l0 < k; l0 += LS) {       // dots F_l . r with the residual as computed
-      const double *c0 = colp + (size_t)l0 * n1;
       double pv[LS];
 #pragma unroll
       for (int dl = 0; dl < LS; dl++) {
+        const double cf = l0 + dl < k ? coef[l0 + dl] : 0.0;
         double p = 0.0;
 #pragma unroll
-        for (int q = 0; q < ACA_E; q++)
-          if (l0 + dl < k && q < nval) p = fma(c0[(size_t)dl * n1 + q * ACA_SUB], r[q], p);
+        for (int q = 0; q < ACA_E; q++) {
+          r[q] = __dsub_rn(r[q], __dmul_rn(cf, F[dl][q]));
+          p = fma(Fk[q], F[dl][q], p);
+        }
         pv[dl] = p;
       }
       dot_butterfly(pv, l0, lane, w0, w1);
     }
 #pragma unroll
     for (int q = 0; q < ACA_E; q++) {
-      if (q >= nval) break;
+      if (q >= nval || !store) break;
       const long long g = g0 + q * ACA_SUB;
       const double v = r[q];
       slot[(long long)k * ldx + g] = v;
       if (!((usedm >> q) & 1u) && fabs(v) > ba) { ba = fabs(v); bi = g - lo; bv = v; }
-      n2 += v * v;
     }
   }
   {
@@ -350,6 +337,7 @@ __device__ __forceinline__ void aca_item(const AcaCtx &c, int item, AcaScratch &
     if (la < k) sdot[warp][la] = w0;
     if (lb < k) sdot[warp][lb] = w1;
   }
+  double n2 = 0.0;
   block_argmax_n2(ba, bi, bv, n2, s_abs, s_idx, s_val, s_n2);
   const int nq = c.nq[b];
   double *rec0 = c.rec + c.recbase[b] * ACA_RECW;
@@ -359,7 +347,7 @@ __device__ __forceinline__ void aca_item(const AcaCtx &c, int item, AcaScratch &
     for (int w = 0; w < ACA_SUB / 32; w++) s += sdot[w][l];
     rec[4 + l] = s;
   }
-  if (t == 0) { rec[0] = ba; rec[1] = (double)bi; rec[2] = bv; rec[3] = n2; }
+  if (t == 0) { rec[0] = ba; rec[1] = (double)bi; rec[2] = bv; rec[3] = 0.0; }
   int &amLast = S.amLast;
   __threadfence();
   __syncthreads();
@@ -368,73 +356,77 @@ __device__ __forceinline__ void aca_item(const AcaCtx &c, int item, AcaScratch &
   if (!amLast) return;
   __threadfence();
   // ---- last CTA: reduce the nq records in a fixed order ----
-  ba = 0.0; bv = 0.0; bi = -1; n2 = 0.0;
+  ba = 0.0; bv = 0.0; bi = -1;
   for (int q = t; q < nq; q += ACA_SUB) {
     const double *rq = rec0 + (long long)q * ACA_RECW;
     const double aq = __ldcg(rq + 0); const long long iq = (long long)__ldcg(rq + 1);
     if (amax_better(ba, bi, aq, iq)) { ba = aq; bi = iq; bv = __ldcg(rq + 2); }
   }
-  {   // columns 3 (nrm2) .. 3 + k (dots): warp w sums records w, w + 8, ...; lane owns columns lane + 32 s
-    double acc[3] = {0.0, 0.0, 0.0};
+  {   // record columns 4 .. 3 + k (dots): warp w sums records w, w + 8, ...; lane owns columns lane + 32 s
+    double acc[2] = {0.0, 0.0};
     for (int q = warp; q < nq; q += ACA_SUB / 32) {
-      const double *rq = rec0 + (long long)q * ACA_RECW + 3;
+      const double *rq = rec0 + (long long)q * ACA_RECW + 4;
 #pragma unroll
-      for (int s = 0; s < 3; s++) if (lane + 32 * s <= k) acc[s] += __ldcg(rq + lane + 32 * s);
+      for (int s = 0; s < 2; s++) if (lane + 32 * s < k) acc[s] += __ldcg(rq + lane + 32 * s);
     }
 #pragma unroll
-    for (int s = 0; s < 3; s++) if (lane + 32 * s <= k) part[warp][lane + 32 * s] = acc[s];
+    for (int s = 0; s < 2; s++) if (lane + 32 * s < k) part[warp][lane + 32 * s] = acc[s];
   }
   double dummy = 0.0;
   block_argmax_n2(ba, bi, bv, dummy, s_abs, s_idx, s_val, s_n2);   // (syncs: part[] complete afterwards)
-  for (int cidx = t; cidx <= k; cidx += ACA_SUB) {
+  // tot[l] = F_{k-1} . F_l, l < k (tot[k-1] = ||F_{k-1}||^2): the oracle's dot(u, U_l), dot(V_l, v), dot(u, u),
+  // dot(v, v) of term k-1, from the stored (normalised) columns.  (Forming them from a running Gram matrix instead
+  // is unstable once the residual is rounding noise: at eps = 1e-12 that estimate of ||S||_F drifted by 40% within
+  // two steps and flipped whole blocks' stopping decisions -- DESIGN.md R17.)
+  for (int cidx = t; cidx < k; cidx += ACA_SUB) {
     double s = 0.0;
     for (int w = 0; w < ACA_SUB / 32; w++) s += part[w][cidx];
     tot[cidx] = s;
   }
   __syncthreads();
-  // dots with the new column, F_l . r, formed from the residual as computed (the oracle's dot(u, U_l) and
-  // dot(V_l, v)); the row pass's column is normalised by the pivot (V[:,k] = v~ / v~_jk), so its dots and norm are
-  // divided by it.  (Forming them as F_l . a - sum_m coef_m (F_l . F_m) from a running Gram matrix, as before, is
-  // unstable once the residual is rounding noise: at eps = 1e-12 that estimate of ||S||_F drifted by 40% within two
-  // steps and flipped whole blocks' stopping decisions -- DESIGN.md R17.)
-  const double pv = (ROW && bi >= 0 && bv != 0.0) ? bv : 1.0;
-  for (int l = t; l < k; l += ACA_SUB) dnew[l] = ROW ? tot[1 + l] / pv : tot[1 + l];
-  __syncthreads();
   if (t == 0) {
-    const double nr2 = ROW ? (tot[0] / pv) / pv : tot[0];
+    const int fr = c.forced ? c.forced[b] : -1;
+    const long long mn = m1 < m2 ? m1 : m2;
     if (ROW) {
-      for (int l = 0; l < k; l++) st->dV[l] = dnew[l];
+      for (int l = 0; l + 1 < k; l++) st->dV[l] = tot[l];
+      if (k > 0) st->nv2 = tot[k - 1];
       st->cnt_r = 0;
-      if (bi < 0 || ba == 0.0) {                          // exactly-zero residual row: rank k
-        st->done = 1; c.rank[b] = k; atomicSub(c.active, 1);
-      } else {
-        st->jpiv = bi; st->pivval = bv; st->nv2 = nr2;
-        c.used[(long long)(e - 1) * n + lo2 + bi] = 1;
+      if (!donly) {
+        if (bi < 0 || ba == 0.0) {                 // exactly-zero residual row: rank k whatever term k-1's test says
+          st->done = 1; c.rank[b] = k; atomicSub(c.active, 1);
+        } else {
+          st->jpiv = bi; st->pivval = bv;
+          c.used[(long long)(e - 1) * n + lo2 + bi] = 1;
+        }
       }
     } else {
       st->cnt_c = 0;
-      // ||S_{k+1}||^2 = ||S_k||^2 + 2 sum_{l<k} (U_k.U_l)(V_l.V_k) + ||U_k||^2 ||V_k||^2
-      double cross = 0.0;
-      for (int l = 0; l < k; l++) cross += dnew[l] * st->dV[l];
-      const double nu2 = nr2, nv2 = st->nv2;
-      const double S2 = st->S2 + 2.0 * cross + nu2 * nv2;
-      st->S2 = S2;
-      const int k1 = k + 1;
-      st->k = k1;
-      const long long mn = m1 < m2 ? m1 : m2;
-      int done = 0;
-      const int fr = c.forced ? c.forced[b] : -1;
+      int done = 0, rank = 0;
+      if (k > 0) {
+        // term k-1: ||S_k||^2 = ||S_{k-1}||^2 + 2 sum_{l<k-1} (U_{k-1}.U_l)(V_l.V_{k-1}) + ||U_{k-1}||^2 ||V_{k-1}||^2
+        double cross = 0.0;
+        for (int l = 0; l + 1 < k; l++) cross += tot[l] * st->dV[l];
+        const double nu2 = tot[k - 1], nv2 = st->nv2;
+        const double S2 = st->S2 + 2.0 * cross + nu2 * nv2;
+        st->S2 = S2;
 #ifdef ACA_TRACE_BLOCK
-      if (b == ACA_TRACE_BLOCK)      // diagnostic build only: the oracle's ORACLE_TRACE_ACA line for the same block
-        printf("[gpu aca] k=%d ik=%lld jk=%lld nu2=%.17g nv2=%.17g S2=%.17g ratio=%.17g\n", k, st->ipiv, st->jpiv, nu2,
-               nv2, S2, sqrt(nu2) * sqrt(nv2) / (c.eps * sqrt(fabs(S2))));
+        if (b == ACA_TRACE_BLOCK)      // diagnostic build only: the oracle's ORACLE_TRACE_ACA line for the same block
+          printf("[gpu aca] k=%d nu2=%.17g nv2=%.17g S2=%.17g ratio=%.17g\n", k, nu2, nv2, S2,
+                 sqrt(nu2) * sqrt(nv2) / (c.eps * sqrt(fabs(S2))));
 #endif
-      if (fr >= 0 ? k1 >= fr : sqrt(nu2) * sqrt(nv2) <= c.eps * sqrt(fabs(S2))) done = 1;     // stop term is kept
-      else if (k1 == mn) done = 1;
-      else if (k1 == st->cap) { done = 2; atomicAdd(&flags[5], 1); }
-      else if (bi < 0 || ba == 0.0) done = 1;
-      else { st->ipiv = bi; mark_row_run(c, c.used + (long long)(e - 1) * n, lo1, m1, bi); }
-      if (done) { st->done = done; st->raw_last = 1; c.rank[b] = k1; atomicSub(c.active, 1); }
+        if (fr < 0 && sqrt(nu2) * sqrt(nv2) <= c.eps * sqrt(fabs(S2))) { done = 1; rank = k; }   // stop term kept
+        else if (donly) { done = 2; rank = k; atomicAdd(&flags[5], 1); }                        // rank cap, eps unmet
+      }
+      if (!done) {                                   // term k stands; can a step k + 1 follow?
+        const int k1 = k + 1;
+        st->k = k1;
+        // (the oracle's order after its stop test: forced rank / min(m1, m2), rank cap, no pivot row)
+        if ((fr >= 0 && k1 >= fr) || k1 == mn) { done = 1; rank = k1; st->raw_last = 1; }
+        else if (k1 == st->cap) st->donly = 1;       // the test of term k decides: one dots-only step
+        else if (bi < 0 || ba == 0.0) { done = 1; rank = k1; st->raw_last = 1; }
+        else { st->ipiv = bi; mark_row_run(c, c.used + (long long)(e - 1) * n, lo1, m1, bi); }
+      }
+      if (done) { st->done = done; st->k = rank; c.rank[b] = rank; atomicSub(c.active, 1); }
     }
   }
 }
@@ -779,7 +771,7 @@ hodlr_status hodlr_aca(hodlr_s *h) {
   c.kp = h->kp; c.n = n; c.ldx = h->ldx; c.eps = h->eps; c.xs = h->xs; c.lo = h->lo; c.hi = h->hi; c.Xh = h->Xh;
   c.used = h->used; c.st = h->ast; c.active = h->dflags + 4; c.rank = h->rank; c.bdepth = P->d_bdepth;
   c.dt = h->d_dt; c.bigidx = P->d_bigidx; c.flags = h->dflags; c.step = h->dflags + 6;
-  c.maxsteps = h->cap + 1;
+  c.maxsteps = h->cap + 2;                 // + the dots-only step of the lagged stop test
   c.forced = h->d_forced;
   AcaCtx cx[2] = {c, c};
   cx[0].items = P->d_items_r; cx[0].nq = P->d_nq; cx[0].recbase = P->d_rb; cx[0].rec = d_rec;
@@ -813,7 +805,7 @@ hodlr_status hodlr_aca(hodlr_s *h) {
   if (nograph < 0) { const char *ev = getenv("HODLR_ACA_NOGRAPH"); nograph = ev && atoi(ev) ? 1 : 0; }
   int hsteps = 0;
   if (nbig > 0 && nograph) {
-    for (hsteps = 1; hsteps <= h->cap + 1; hsteps++) {
+    for (hsteps = 1; hsteps <= h->cap + 2; hsteps++) {
       if (P->seo) k_aca_pass<true, true><<<(unsigned)P->nitems_r, ACA_SUB, 0, h->st>>>(P->d_ctx);
       else k_aca_pass<true, false><<<(unsigned)P->nitems_r, ACA_SUB, 0, h->st>>>(P->d_ctx);
       HLAUNCH(h, "k_aca_pass<row>");

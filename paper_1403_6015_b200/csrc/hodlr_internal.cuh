@@ -27,10 +27,10 @@
 #define ACA_FUSED_MAX 4096 // blocks with both sides <= this run the fused single-CTA ACA
 #endif
 #ifndef ACA_BIG_CHUNK
-#define ACA_BIG_CHUNK 8192 // minimum chunk per CTA for the step-synchronous big blocks (measured optimum)
+#define ACA_BIG_CHUNK 4096 // minimum chunk per CTA for the step-synchronous big blocks (measured: 8192 0.2 ms slower)
 #endif
 #ifndef ACA_CHUNKS_PER_SIDE
-#define ACA_CHUNKS_PER_SIDE 32    // max chunks (CTAs, records) per block side
+#define ACA_CHUNKS_PER_SIDE 64    // max chunks (CTAs, records) per block side
 #endif
 
 // ----------------------------------------------------------------------------------------------
@@ -83,12 +83,13 @@ struct AcaState {
   int cnt_r, cnt_c; // CTA arrival counters (last-CTA reduction)
   int cap;          // min(rank_cap, m1, m2)
   int raw_last;     // finished in a column pass: V[:, rank-1] still holds the raw residual (k_aca_finish divides it)
+  int donly;        // the step after the rank cap: passes form the last column's dots only (lagged stop test)
   long long ipiv;   // current row pivot (local in c1)
   long long jpiv;   // current column pivot (local in c2)
   double pivval;    // v~_jk
   double S2;        // ||S_k||_F^2 estimate
-  double nv2;       // ||V'[:,k]||^2 of the current step
-  double dV[ACA_MAXCAP];   // V'_l . V'_k, l < k, of the current step
+  double nv2;       // ||V'[:,k-1]||^2, formed by the row pass of step k (lagged stop test)
+  double dV[ACA_MAXCAP];   // V'_l . V'_{k-1}, l < k - 1, formed by the row pass of step k
 };
 
 // One CTA of a big-block pass: a chunk [start, start + len) of one side of `block`, with the block geometry

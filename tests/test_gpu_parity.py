@@ -346,6 +346,30 @@ def test_rank_cap_change_same_shape(hb):
         assert np.linalg.norm(x_g - x_o) <= X_TOL * np.linalg.norm(x_o), cap
 
 
+def test_rank_cap_boundary_big_blocks(hb):
+    """Lagged stop test of the big-block passes at the rank cap (the dots-only step): with the cap equal to the
+    largest oracle rank (held by a big block, sides > ACA_FUSED_MAX) the build succeeds with the oracle's ranks; one
+    below it, both the oracle and the GPU return ERANKCAP (the oracle's step 6 after its stop test)."""
+    from oracle import OracleError
+    cfg = inputs.scaled(inputs.CONFIGS["cfg3"], 1 << 15)
+    x = inputs.points(cfg); y = inputs.rhs(cfg)
+    o = OracleHODLR(x, cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, 1e-12).factor()
+    r_o = o.ranks()
+    R = int(r_o.max())
+    assert int(r_o[:3].max()) == R            # blocks 0..2 (sides 16384, 8192, 8192) run in the passes
+    xd = torch.from_numpy(x).cuda()
+    g = hb.HODLR(xd, cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, 1e-12, R).factor()
+    np.testing.assert_array_equal(g.tree()[2][:3], r_o[:3])
+    assert abs(g.logdet() - o.logdet()) <= LD_TOL * abs(o.logdet())
+    g.close()
+    with pytest.raises(OracleError) as eo:
+        OracleHODLR(x, cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, 1e-12, R - 1)
+    assert eo.value.status == "ERANKCAP"
+    with pytest.raises(hb.HodlrError) as e:
+        hb.HODLR(xd, cfg.kernel, cfg.theta, cfg.sigma2, cfg.leaf, 1e-12, R - 1)
+    assert e.value.status == "ERANKCAP"
+
+
 def test_forced_ranks_hook(hb):
     """hodlr_opts.forced_ranks: the GPU reproduces the oracle's per-block ranks exactly, and with them the solve
     difference is the arithmetic alone (far below the 1e-9 gate)."""
