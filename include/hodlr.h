@@ -164,12 +164,36 @@ hodlr_status gp_predict(hodlr_t h, const double *y, const double *xt, int64_t m,
  * y: device, n doubles.  out_host: host double (-INFINITY with HODLR_ENOTPD on failure). */
 hodlr_status gp_loglik(hodlr_t h, const double *y, double *out_host);
 
+/* Batched factorizations (NEXT-4: the marginalisation / hyper-parameter loops of PAPER.md:399-446
+ * evaluate many settings on the same points): B = 2^t independent problems C_s = sigma2s[s] I + K(x; thetas[s]) on
+ * the same n points x (device, original order), held in ONE handle as the block-diagonal matrix
+ * diag(C_0, ..., C_{B-1}) of order B n.  Problem s occupies rows [s n, (s + 1) n) of every vector argument of the
+ * handle (y, x of hodlr_solve / hodlr_factor_solve / hodlr_apply: device, B n doubles, problem-major, each problem in
+ * the original point order).  The tree is the B-fold tree whose top t levels split exactly between problems (n B
+ * halves evenly) -- their off-diagonal blocks are zero and skipped (rank 0) -- and whose subtree s below is problem
+ * s's own tree; every kernel launch of the path then covers all B problems (one ACA step loop, one leaf Cholesky
+ * launch, one zsyrk, one pass per tree level).  thetas: HOST B x 2 {a, ell} (B x 3 for HODLR_RQ); sigma2s: HOST
+ * B.  Requires n >= leaf; no dist, no noise.  The handle then follows the usual state machine; hodlr_logdet /
+ * gp_loglik report the whole block-diagonal matrix (the sum over problems), hodlr_batch_results each problem's.
+ * gp_predict refuses batched handles (HODLR_EINVAL).  A failure (HODLR_ENOTPD, HODLR_ERANKCAP) in any problem fails
+ * the handle. */
+hodlr_status hodlr_build_batch(const double *x, int64_t n, hodlr_kernel kernel, const double *thetas,
+                               const double *sigma2s, int32_t B, int32_t leaf, double eps, const hodlr_opts *opts,
+                               void *cuda_stream, hodlr_t *out);
+
+/* Per-problem results of a factored batched handle (HOST arrays of B doubles): log det C_s (its subtree's leaf and
+ * node partials, fixed compensated order) and, if quad_host != NULL, y_s^T C_s^{-1} y_s of the right-hand side fused
+ * by hodlr_factor_solve (HODLR_ESTATE if none was).  Synchronizes the handle's stream.  On a B = 1 handle: the
+ * handle's own log det and y^T C^{-1} y. */
+hodlr_status hodlr_batch_results(hodlr_t h, double *logdet_host, double *quad_host);
+
 /* Config 4 (BASELINE.json): log-likelihoods (eq. 1) of B independent hyper-parameter settings on the same
  * x, y (device, n doubles).  thetas: HOST B x 2 {a, ell}; sigma2s: HOST B; out_host: HOST B doubles (-INFINITY
- * for a setting that failed).  One GPU runs `workers` settings concurrently (host threads, one stream each;
- * <= 0 => 8; each setting's persistent upper-tree launch then takes ~1/workers of the SMs so that the settings'
- * latency-bound phases overlap).  Every setting is one hodlr_factor_solve with y fused (y^T C^{-1} y from the
- * factorization, no solve pass).  With dist (nranks > 1) rank g computes settings g, g + P, ... and the values are allgathered, so
+ * for a setting that failed).  The settings are factored in batches (hodlr_build_batch): the largest powers of two
+ * that fit (at most 2^23 / n problems per batch), each one hodlr_factor_solve with y fused into all problems
+ * (y^T C_s^{-1} y from the factorization, no solve pass) and hodlr_batch_results.  A batch that fails is redone
+ * setting by setting (`workers` host threads, one stream each; <= 0 => 8) so that every setting gets its own status
+ * and value.  With dist (nranks > 1) rank g computes settings g, g + P, ... and the values are allgathered, so
  * every rank returns all B (replicas; the settings share nothing).  Returns the first failing setting's status
  * (message names it), HODLR_OK if all succeeded. */
 hodlr_status gp_loglik_sweep(const double *x, const double *y, int64_t n, hodlr_kernel kernel, const double *thetas,

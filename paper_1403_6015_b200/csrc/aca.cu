@@ -95,6 +95,10 @@ __device__ __forceinline__ void block_argmax_n2(double &ba, long long &bi, doubl
 #ifndef ACA_FUSED_SMALL
 #define ACA_FUSED_SMALL 128        // fused blocks with both sides <= this run in 64-thread CTAs
 #endif
+#ifndef ACA_FUSED_MID
+#define ACA_FUSED_MID 512          // ... <= this in 128-thread CTAs with 512-entry buffers (7 KB of shared memory
+                                   // instead of 42 KB: more blocks in flight per SM)
+#endif
 #ifndef ACA_E_DEF
 #define ACA_E_DEF 4
 #endif
@@ -162,6 +166,7 @@ __device__ __forceinline__ void aca_item(const AcaCtx &c, int item, AcaScratch &
   double *slot = c.Xh + it.slot_off;
   const unsigned char *used = c.used + (long long)(e - 1) * n;
   const long long ilen = it.len;
+  const KParams &kp = kp_of(c.kp, c.kps, c.nseg, lo1);
   // The row pass of step k divides the previous step's column V[:, k-1] (stored as the raw residual v~) by that
   // step's pivot as it streams it -- the oracle's V = v~ / v~_jk (R16), written back in place -- so no separate pass
   // over the column is needed; a block that finishes in a column pass without a further step gets its last column
@@ -213,8 +218,8 @@ __device__ __forceinline__ void aca_item(const AcaCtx &c, int item, AcaScratch &
 #pragma unroll
         for (int pp = 0; pp < NP; pp++) {
           usedm |= ((uu[pp].x ? 1u : 0u) | (uu[pp].y ? 2u : 0u)) << (2 * pp);
-          r[2 * pp] = ok ? kval_ot<SEO>(c.kp, ROW ? xp - xx[pp].x : xx[pp].x - xp) : 0.0;
-          r[2 * pp + 1] = ok ? kval_ot<SEO>(c.kp, ROW ? xp - xx[pp].y : xx[pp].y - xp) : 0.0;
+          r[2 * pp] = ok ? kval_ot<SEO>(kp, ROW ? xp - xx[pp].x : xx[pp].x - xp) : 0.0;
+          r[2 * pp + 1] = ok ? kval_ot<SEO>(kp, ROW ? xp - xx[pp].y : xx[pp].y - xp) : 0.0;
         }
       }
       // the newest column F_{k-1} first (normalised and stored back by the row pass)
@@ -288,7 +293,7 @@ __device__ __forceinline__ void aca_item(const AcaCtx &c, int item, AcaScratch &
     for (int q = 0; q < ACA_E; q++) {
       const double xq = q < nval ? xsp[q * ACA_SUB] : xp;
       if (q < nval && up[q * ACA_SUB]) usedm |= 1u << q;
-      r[q] = q < nval ? kval_ot<SEO>(c.kp, ROW ? xp - xq : xq - xp) : 0.0;
+      r[q] = q < nval ? kval_ot<SEO>(kp, ROW ? xp - xq : xq - xp) : 0.0;
       Fk[q] = 0.0;
     }
     if (k > 0) {                               // the newest column, normalised and stored back by the row pass
@@ -480,6 +485,7 @@ __global__ void __launch_bounds__(NT) k_aca_fused(AcaCtx c, const int *blocks, i
   const long long mn = m1 < m2 ? m1 : m2;
   const int cap = c.st[b].cap;
   const int e = c.bdepth[b] + 1;
+  const KParams &kp = kp_of(c.kp, c.kps, c.nseg, lo1);
   double *slot = c.Xh + c.dt->colbase[e] * c.ldx;
   const long long ldx = c.ldx;
   for (int i = t; i < MAXS; i += NT) { usedR[i] = 0; usedC[i] = 0; }
@@ -501,7 +507,7 @@ __global__ void __launch_bounds__(NT) k_aca_fused(AcaCtx c, const int *blocks, i
     // v~_j = A[ik, j] - sum_l U[ik, l] V[j, l], l ascending, each product rounded (the oracle's operation order)
     for (long long j = t; j < m2; j += NT) {
       const long long gj = lo2 + j;
-      double v = kval_ot<SEO>(c.kp, xi - c.xs[gj]);
+      double v = kval_ot<SEO>(kp, xi - c.xs[gj]);
 #pragma unroll 8
       for (int l = 0; l < k; l++) v = __dsub_rn(v, __dmul_rn(Ui[l], __ldcg(slot + (long long)l * ldx + gj)));
       vbuf[j] = v;
@@ -536,7 +542,7 @@ __global__ void __launch_bounds__(NT) k_aca_fused(AcaCtx c, const int *blocks, i
     ba = 0.0; bv = 0.0; n2 = 0.0; bi = -1;
     for (long long i = t; i < m1; i += NT) {
       const long long gi = lo1 + i;
-      double u = kval_ot<SEO>(c.kp, c.xs[gi] - xj);
+      double u = kval_ot<SEO>(kp, c.xs[gi] - xj);
 #pragma unroll 8
       for (int l = 0; l < k; l++) u = __dsub_rn(u, __dmul_rn(Ui[l], __ldcg(slot + (long long)l * ldx + gi)));
       slot[(long long)k * ldx + gi] = u;
@@ -599,12 +605,13 @@ __global__ void k_aca_cond(cudaGraphConditionalHandle hdl, const AcaCtx *__restr
 // shared.
 // ---------------------------------------------------------------------------------------------
 struct AcaPlan {
-  // key: everything the cached device tables depend on -- the tree (n, leaf), the shard (rank, nranks), the
+  // key: everything the cached device tables depend on -- the tree (n, leaf, batch depth), the shard (rank, nranks), the
   // factor slot layout (rank cap: colbase[e] = sum of min(cap, max node size)), the kernel variant and the device
-  long long n; int leaf; int rank, nranks; bool seo; int cap; int dev;
+  long long n; int leaf; int rank, nranks; bool seo; int cap; int dev; int tbatch;
   long long nb; int nbig;
   std::vector<int> fused_blocks;
   int nfused_small = 0;                    // fused_blocks[0, nfused_small): both sides <= ACA_FUSED_SMALL
+  int nfused_mid = 0;                      // then nfused_mid blocks with both sides <= ACA_FUSED_MID
   size_t nitems_r = 0, nitems_c = 0;
   long long nrec_r = 0, nrec_c = 0;
   AcaItem *d_items_r = nullptr, *d_items_c = nullptr;
@@ -622,14 +629,17 @@ static cudaError_t plan_create(AcaPlan *P, const hodlr_s *h) {
   std::vector<AcaItem> items_r, items_c;
   std::vector<int> nq_r(nb), nq_c(nb), bdepth(nb), bigidx(nb, -1);
   std::vector<long long> rb_r(nb), rb_c(nb);
-  std::vector<int> small, large;
+  std::vector<int> small, mid, large;
   P->nbig = 0;
   for (long long b = 0; b < nb; b++) {
     bdepth[b] = hodlr_depth_of(b);
     if (!hodlr_owns_block(h, b)) { nq_r[b] = nq_c[b] = 0; rb_r[b] = rb_c[b] = 0; continue; }   // another rank's subtree
+    // batched handle: the blocks of the top log2 B levels couple different problems and are exactly zero (rank 0)
+    if (bdepth[b] < h->tbatch) { nq_r[b] = nq_c[b] = 0; rb_r[b] = rb_c[b] = 0; continue; }
     long long m1 = h->h_hi[2 * b + 1] - h->h_lo[2 * b + 1], m2 = h->h_hi[2 * b + 2] - h->h_lo[2 * b + 2];
     if (std::max(m1, m2) <= ACA_FUSED_MAX) {
-      (std::max(m1, m2) <= ACA_FUSED_SMALL ? small : large).push_back((int)b);
+      const long long mx = std::max(m1, m2);
+      (mx <= ACA_FUSED_SMALL ? small : mx <= ACA_FUSED_MID ? mid : large).push_back((int)b);
       nq_r[b] = nq_c[b] = 0; rb_r[b] = rb_c[b] = 0; continue;
     }
     bigidx[b] = P->nbig++;
@@ -650,8 +660,10 @@ static cudaError_t plan_create(AcaPlan *P, const hodlr_s *h) {
       else { nq_c[b] = q; rb_c[b] = P->nrec_c; P->nrec_c += q; }
     }
   }
-  P->nfused_small = (int)small.size();
-  P->fused_blocks = small; P->fused_blocks.insert(P->fused_blocks.end(), large.begin(), large.end());
+  P->nfused_small = (int)small.size(); P->nfused_mid = (int)mid.size();
+  P->fused_blocks = small;
+  P->fused_blocks.insert(P->fused_blocks.end(), mid.begin(), mid.end());
+  P->fused_blocks.insert(P->fused_blocks.end(), large.begin(), large.end());
   P->nitems_r = items_r.size(); P->nitems_c = items_c.size();
   std::vector<int> nq_all(nq_r); nq_all.insert(nq_all.end(), nq_c.begin(), nq_c.end());
   std::vector<long long> rb_all(rb_r); rb_all.insert(rb_all.end(), rb_c.begin(), rb_c.end());
@@ -721,13 +733,13 @@ static AcaPlan *plan_acquire(const hodlr_s *h, hodlr_status *st) {
     std::lock_guard<std::mutex> lk(g_plan_mu);
     for (AcaPlan *P : g_plans)
       if (!P->busy && P->n == h->n && P->leaf == h->leaf && P->rank == h->grank && P->nranks == h->nranks &&
-          P->seo == (h->kp.kern == HODLR_SE) && P->cap == h->cap && P->dev == h->dev) {
+          P->seo == (h->kp.kern == HODLR_SE) && P->cap == h->cap && P->dev == h->dev && P->tbatch == h->tbatch) {
         P->busy = true; return P;
       }
   }
   AcaPlan *P = new AcaPlan();
   P->n = h->n; P->leaf = h->leaf; P->rank = h->grank; P->nranks = h->nranks; P->nb = h->ninternal; P->busy = true;
-  P->seo = h->kp.kern == HODLR_SE; P->cap = h->cap; P->dev = h->dev;
+  P->seo = h->kp.kern == HODLR_SE; P->cap = h->cap; P->dev = h->dev; P->tbatch = h->tbatch;
   cudaError_t e = plan_create(P, h);
   if (e != cudaSuccess) { *st = hodlr_cuda_check(e, "aca plan"); return nullptr; }   // (leaked on error)
   std::lock_guard<std::mutex> lk(g_plan_mu);
@@ -773,6 +785,7 @@ hodlr_status hodlr_aca(hodlr_s *h) {
   c.dt = h->d_dt; c.bigidx = P->d_bigidx; c.flags = h->dflags; c.step = h->dflags + 6;
   c.maxsteps = h->cap + 2;                 // + the dots-only step of the lagged stop test
   c.forced = h->d_forced;
+  c.kps = h->d_kps; c.nseg = h->nseg;
   AcaCtx cx[2] = {c, c};
   cx[0].items = P->d_items_r; cx[0].nq = P->d_nq; cx[0].recbase = P->d_rb; cx[0].rec = d_rec;
   cx[1].items = P->d_items_c; cx[1].nq = P->d_nq + nb; cx[1].recbase = P->d_rb + nb; cx[1].rec = d_rec + ACA_RECW * P->nrec_r;
@@ -785,15 +798,21 @@ hodlr_status hodlr_aca(hodlr_s *h) {
   if (!P->fused_blocks.empty()) {
     HCUDA(cudaEventRecord(h->ev_fork, h->st));
     HCUDA(cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
-    const int ns = P->nfused_small, nl = (int)P->fused_blocks.size() - ns;
+    const int ns = P->nfused_small, nm = P->nfused_mid, nl = (int)P->fused_blocks.size() - ns - nm;
     if (nl > 0) {       // the large ones first (longest CTAs)
-      if (P->seo) k_aca_fused<true, ACA_SUB, ACA_FUSED_MAX><<<nl, ACA_SUB, 0, h->st2>>>(c, P->d_fused + ns, h->dflags);
-      else k_aca_fused<false, ACA_SUB, ACA_FUSED_MAX><<<nl, ACA_SUB, 0, h->st2>>>(c, P->d_fused + ns, h->dflags);
+      if (P->seo) k_aca_fused<true, ACA_SUB, ACA_FUSED_MAX><<<nl, ACA_SUB, 0, h->st2>>>(c, P->d_fused + ns + nm, h->dflags);
+      else k_aca_fused<false, ACA_SUB, ACA_FUSED_MAX><<<nl, ACA_SUB, 0, h->st2>>>(c, P->d_fused + ns + nm, h->dflags);
     }
-    if (ns > 0) {       // on a second stream: not serialized behind the large blocks' long CTAs
+    if (ns + nm > 0) {  // on a second stream: not serialized behind the large blocks' long CTAs
       HCUDA(cudaStreamWaitEvent(h->st2b, h->ev_fork, 0));
-      if (P->seo) k_aca_fused<true, 64, ACA_FUSED_SMALL><<<ns, 64, 0, h->st2b>>>(c, P->d_fused, h->dflags);
-      else k_aca_fused<false, 64, ACA_FUSED_SMALL><<<ns, 64, 0, h->st2b>>>(c, P->d_fused, h->dflags);
+      if (nm > 0) {
+        if (P->seo) k_aca_fused<true, 128, ACA_FUSED_MID><<<nm, 128, 0, h->st2b>>>(c, P->d_fused + ns, h->dflags);
+        else k_aca_fused<false, 128, ACA_FUSED_MID><<<nm, 128, 0, h->st2b>>>(c, P->d_fused + ns, h->dflags);
+      }
+      if (ns > 0) {
+        if (P->seo) k_aca_fused<true, 64, ACA_FUSED_SMALL><<<ns, 64, 0, h->st2b>>>(c, P->d_fused, h->dflags);
+        else k_aca_fused<false, 64, ACA_FUSED_SMALL><<<ns, 64, 0, h->st2b>>>(c, P->d_fused, h->dflags);
+      }
       HCUDA(cudaEventRecord(h->ev_join2, h->st2b));
     }
     HLAUNCH(h, "k_aca_fused");
@@ -826,7 +845,7 @@ hodlr_status hodlr_aca(hodlr_s *h) {
     HLAUNCH(h, "k_aca_finish");
   }
   if (!P->fused_blocks.empty()) HCUDA(cudaStreamWaitEvent(h->st, h->ev_join, 0));
-  if (P->nfused_small > 0) HCUDA(cudaStreamWaitEvent(h->st, h->ev_join2, 0));
+  if (P->nfused_small + P->nfused_mid > 0) HCUDA(cudaStreamWaitEvent(h->st, h->ev_join2, 0));
   HCUDA(cudaEventRecord(h->ev_hi, h->sthi));
   h->st = sm_main;
   HCUDA(cudaStreamWaitEvent(h->st, h->ev_hi, 0));

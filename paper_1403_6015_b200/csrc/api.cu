@@ -270,21 +270,68 @@ void hodlr_free(hodlr_t h) {
   delete h;
 }
 
-hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const double *theta, double sigma2,
-                         int32_t leaf, double eps, const hodlr_dist *dist, const hodlr_opts *opts, void *cuda_stream,
-                         hodlr_t *out) {
+// Validate one setting's parameters (theta = {a, ell[, alpha]})
+static hodlr_status check_setting(hodlr_kernel kernel, const double *theta, double sigma2, int b) {
+  if (!(sigma2 >= 0.0) || !isfinite(sigma2)) return hodlr_set_error(HODLR_EINVAL, "build: setting %d: sigma2 = %g", b, sigma2);
+  if (!(theta[1] > 0.0) || !isfinite(theta[1])) return hodlr_set_error(HODLR_EINVAL, "build: setting %d: ell = %g <= 0", b, theta[1]);
+  if (!(theta[0] >= 0.0) || !isfinite(theta[0])) return hodlr_set_error(HODLR_EINVAL, "build: setting %d: a = %g < 0", b, theta[0]);
+  if (kernel == HODLR_RQ && (!(theta[2] > 0.0) || !isfinite(theta[2])))
+    return hodlr_set_error(HODLR_EINVAL, "build: setting %d: rational quadratic alpha = %g <= 0", b, theta[2]);
+  return HODLR_OK;
+}
+
+// Covariance parameters of one setting (Table I)
+static KParams make_kp(hodlr_kernel kernel, const double *theta, double sigma2) {
+  KParams kp;
+  memset(&kp, 0, sizeof(kp));
+  kp.kern = (int)kernel; kp.a2 = theta[0] * theta[0]; kp.s2 = sigma2;
+  kp.c = kernel == HODLR_SE ? 1.0 / (2.0 * theta[1] * theta[1])
+       : kernel == HODLR_MATERN32 ? sqrt(3.0) / theta[1]
+       : kernel == HODLR_MATERN52 ? sqrt(5.0) / theta[1]
+       : kernel == HODLR_EXP ? 1.0 / theta[1] : 1.0 / (theta[1] * theta[1]);
+  kp.alpha = kernel == HODLR_RQ ? theta[2] : 0.5;
+  kp.ell = theta[1];
+  kp.c2 = (2.0 * theta[1]) * theta[1];            // the oracle's 2.0 * ell * ell (left to right)
+  kp.sq = kernel == HODLR_MATERN32 ? sqrt(3.0) : sqrt(5.0);
+  int ex;   // exact reciprocals (powers of two) let kval_o multiply instead of divide, bit for bit the same
+  kp.rc2 = frexp(kp.c2, &ex) == 0.5 ? 1.0 / kp.c2 : 0.0;
+  kp.rell = frexp(theta[1], &ex) == 0.5 ? 1.0 / theta[1] : 0.0;
+  kp.dn = nullptr;
+  return kp;
+}
+
+// Problem s of a batched handle: sorted rows and permutation of problem 0 shifted by s * nseg
+__global__ void k_replicate_order(double *xs, long long *perm, long long nseg, int B) {
+  const long long N = nseg * B;
+  for (long long i = nseg + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
+    const long long s = i / nseg, j = i - s * nseg;
+    xs[i] = xs[j];
+    perm[i] = perm[j] + s * nseg;
+  }
+}
+
+// hodlr_build (B = 1) and hodlr_build_batch (B = 2^t problems on the same points): one implementation.
+static hodlr_status build_impl(const double *x, int64_t nseg, int32_t B, hodlr_kernel kernel, const double *thetas,
+                               int tstride, const double *sigma2s, int32_t leaf, double eps, const hodlr_dist *dist,
+                               const hodlr_opts *opts, void *cuda_stream, hodlr_t *out) {
   if (!out) return hodlr_set_error(HODLR_EINVAL, "build: out is NULL");
   *out = nullptr;
-  if (!x || !theta) return hodlr_set_error(HODLR_EINVAL, "build: NULL x or theta");
-  if (n < 1) return hodlr_set_error(HODLR_EINVAL, "build: n = %lld < 1", (long long)n);
+  if (!x || !thetas || !sigma2s) return hodlr_set_error(HODLR_EINVAL, "build: NULL x or theta");
+  if (nseg < 1) return hodlr_set_error(HODLR_EINVAL, "build: n = %lld < 1", (long long)nseg);
   if (leaf < 1) return hodlr_set_error(HODLR_EINVAL, "build: leaf = %d < 1", leaf);
   if (!(eps > 0.0 && eps < 1.0)) return hodlr_set_error(HODLR_EINVAL, "build: eps = %g not in (0, 1)", eps);
-  if (!(sigma2 >= 0.0) || !isfinite(sigma2)) return hodlr_set_error(HODLR_EINVAL, "build: sigma2 = %g", sigma2);
-  if (!(theta[1] > 0.0) || !isfinite(theta[1])) return hodlr_set_error(HODLR_EINVAL, "build: ell = %g <= 0", theta[1]);
-  if (!(theta[0] >= 0.0) || !isfinite(theta[0])) return hodlr_set_error(HODLR_EINVAL, "build: a = %g < 0", theta[0]);
   if ((int)kernel < 0 || (int)kernel > 5) return hodlr_set_error(HODLR_EINVAL, "build: unknown kernel %d", (int)kernel);
-  if (kernel == HODLR_RQ && (!(theta[2] > 0.0) || !isfinite(theta[2])))
-    return hodlr_set_error(HODLR_EINVAL, "build: rational quadratic alpha = %g <= 0", theta[2]);
+  if (B < 1 || (B & (B - 1))) return hodlr_set_error(HODLR_EINVAL, "build_batch: B = %d is not a power of two", B);
+  if (B > 1 && nseg < leaf) return hodlr_set_error(HODLR_EINVAL, "build_batch: n = %lld < leaf = %d", (long long)nseg, leaf);
+  if (B > 1 && ((dist && dist->nranks > 1) || (opts && opts->noise)))
+    return hodlr_set_error(HODLR_EINVAL, "build_batch: no dist or noise on batched handles");
+  for (int b = 0; b < B; b++) {
+    hodlr_status cs = check_setting(kernel, thetas + (size_t)b * tstride, sigma2s[b], b);
+    if (cs != HODLR_OK) return cs;
+  }
+  const long long n = nseg * (long long)B;
+  const double *theta = thetas;
+  const double sigma2 = sigma2s[0];
   if (opts && opts->flags != 0) return hodlr_set_error(HODLR_EINVAL, "build: opts.flags must be 0");
   int cap = (opts && opts->rank_cap > 0) ? opts->rank_cap : 48;
   if (cap > ACA_MAXCAP) return hodlr_set_error(HODLR_EINVAL, "build: rank_cap %d > %d", cap, ACA_MAXCAP);
@@ -300,20 +347,10 @@ hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const 
   cudaEventRecord(h->ev0, h->st);
   h->launches = 0;
   h->n = n; h->leaf = leaf; h->eps = eps; h->cap = cap; h->theta[0] = theta[0]; h->theta[1] = theta[1];
-  h->kp.kern = (int)kernel; h->kp.a2 = theta[0] * theta[0]; h->kp.s2 = sigma2;
-  h->kp.c = kernel == HODLR_SE ? 1.0 / (2.0 * theta[1] * theta[1])
-          : kernel == HODLR_MATERN32 ? sqrt(3.0) / theta[1]
-          : kernel == HODLR_MATERN52 ? sqrt(5.0) / theta[1]
-          : kernel == HODLR_EXP ? 1.0 / theta[1] : 1.0 / (theta[1] * theta[1]);
-  h->kp.alpha = kernel == HODLR_RQ ? theta[2] : 0.5;
-  h->kp.ell = theta[1];
-  h->kp.c2 = (2.0 * theta[1]) * theta[1];            // the oracle's 2.0 * ell * ell (left to right)
-  h->kp.sq = kernel == HODLR_MATERN32 ? sqrt(3.0) : sqrt(5.0);
-  {   // exact reciprocals (powers of two) let kval_o multiply instead of divide, bit for bit the same
-    int ex;
-    h->kp.rc2 = frexp(h->kp.c2, &ex) == 0.5 ? 1.0 / h->kp.c2 : 0.0;
-    h->kp.rell = frexp(theta[1], &ex) == 0.5 ? 1.0 / theta[1] : 0.0;
-  }
+  h->kp = make_kp(kernel, theta, sigma2);
+  h->nbatch = B; h->nseg = nseg;
+  h->tbatch = 0;
+  while ((1 << h->tbatch) < B) h->tbatch++;
   // O2-equivalent tree: kappa = largest integer with leaf * 2^kappa <= n
   int kappa = 0;
   while (((long long)leaf << (kappa + 1)) <= n && kappa < HODLR_MAXDEPTH - 2) kappa++;
@@ -340,7 +377,7 @@ hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const 
   for (int e = 1; e <= kappa; e++) {
     long long mmax = 0;
     for (long long id = (1LL << e) - 1; id < (2LL << e) - 1; id++) mmax = std::max(mmax, h->h_hi[id] - h->h_lo[id]);
-    h->dt.capd[e] = (int)std::min<long long>(cap, mmax);
+    h->dt.capd[e] = e <= h->tbatch ? 0 : (int)std::min<long long>(cap, mmax);   // (batched: top blocks are zero)
     h->dt.colbase[e] = cols;
     cols += h->dt.capd[e];
   }
@@ -379,10 +416,24 @@ hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const 
   CK(cudaMemcpyAsync(h->hi, h->h_hi, sizeof(long long) * h->nnodes, cudaMemcpyHostToDevice, h->st));
   CK(cudaMemcpyAsync(h->d_dt, &h->dt, sizeof(DepthTab), cudaMemcpyHostToDevice, h->st));
   hodlr_trace("build: enter");
-  st = hodlr_sort_and_tree(h, x);
+  st = hodlr_sort_and_tree(h, x, nseg);
   hodlr_trace("build: sort done (synced)");
   if (st != HODLR_OK) goto fail;
   if (h->x_nonfinite) { st = hodlr_set_error(HODLR_EINVAL, "build: x contains NaN or Inf"); goto fail; }
+  if (B > 1) {     // batched: every problem has problem 0's order; per-problem parameters on the device
+    k_replicate_order<<<592, 256, 0, h->st>>>(h->xs, h->perm, nseg, B);
+    {
+      cudaError_t le = cudaGetLastError();
+      if (le != cudaSuccess) { st = hodlr_cuda_check(le, "launch k_replicate_order"); goto fail; }
+    }
+    h->launches++; hodlr_global_launches++;
+    std::vector<KParams> kps(B);
+    for (int b = 0; b < B; b++) kps[b] = make_kp(kernel, thetas + (size_t)b * tstride, sigma2s[b]);
+    h->d_kps = (KParams *)hodlr_dalloc(h, sizeof(KParams) * B);
+    if (!h->d_kps) { st = hodlr_set_error(HODLR_ENOMEM, "build: device allocation failed"); goto fail; }
+    CK(cudaMemcpyAsync(h->d_kps, kps.data(), sizeof(KParams) * B, cudaMemcpyHostToDevice, h->st));
+    CK(cudaStreamSynchronize(h->st));      // (kps is a host temporary)
+  }
   if (opts && opts->noise) {     // heteroscedastic diagonal, carried with its point into sorted order
     h->d_noise = (double *)hodlr_dalloc(h, sizeof(double) * (size_t)n);
     if (!h->d_noise) { st = hodlr_set_error(HODLR_ENOMEM, "build: device allocation failed"); goto fail; }
@@ -483,6 +534,43 @@ fail:
   hodlr_free(h);
   return st;
 #undef CK
+}
+
+hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const double *theta, double sigma2,
+                         int32_t leaf, double eps, const hodlr_dist *dist, const hodlr_opts *opts, void *cuda_stream,
+                         hodlr_t *out) {
+  return build_impl(x, n, 1, kernel, theta, 0, &sigma2, leaf, eps, dist, opts, cuda_stream, out);
+}
+
+hodlr_status hodlr_build_batch(const double *x, int64_t n, hodlr_kernel kernel, const double *thetas,
+                               const double *sigma2s, int32_t B, int32_t leaf, double eps, const hodlr_opts *opts,
+                               void *cuda_stream, hodlr_t *out) {
+  return build_impl(x, n, B, kernel, thetas, kernel == HODLR_RQ ? 3 : 2, sigma2s, leaf, eps, nullptr, opts,
+                    cuda_stream, out);
+}
+
+hodlr_status hodlr_batch_results(hodlr_t h, double *logdet_host, double *quad_host) {
+  if (!h || !logdet_host) return hodlr_set_error(HODLR_EINVAL, "batch_results: NULL argument");
+  if (h->state == -1) return hodlr_set_error(HODLR_ENOTPD, "batch_results: factorization failed");
+  if (h->state != 2) return hodlr_set_error(HODLR_ESTATE, "batch_results: not factored");
+  if (quad_host && !h->aug) return hodlr_set_error(HODLR_ESTATE, "batch_results: no right-hand side was fused (hodlr_factor_solve)");
+  if (h->nranks > 1) return hodlr_set_error(HODLR_EINVAL, "batch_results: sharded handle");
+  const int B = h->nbatch;
+  double *d = (double *)hodlr_dalloc_tmp(h, sizeof(double) * 2 * B);
+  if (!d) return hodlr_set_error(HODLR_ENOMEM, "batch_results: device allocation failed");
+  hodlr_status st = hodlr_batch_parts(h, d);
+  std::vector<double> v(2 * (size_t)B);
+  cudaError_t e = cudaSuccess;
+  if (st == HODLR_OK) e = cudaMemcpyAsync(v.data(), d, sizeof(double) * 2 * B, cudaMemcpyDeviceToHost, h->st);
+  if (st == HODLR_OK && e == cudaSuccess) e = cudaStreamSynchronize(h->st);
+  release_transient(h);
+  if (st != HODLR_OK) return st;
+  if (e != cudaSuccess) return hodlr_cuda_check(e, "batch_results");
+  for (int b = 0; b < B; b++) {
+    logdet_host[b] = v[b];
+    if (quad_host) quad_host[b] = v[B + b];
+  }
+  return HODLR_OK;
 }
 
 hodlr_status hodlr_factor(hodlr_t h) {

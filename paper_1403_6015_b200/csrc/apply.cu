@@ -35,6 +35,7 @@ struct ApplyCtx {
   double *P;                // nleaves x K
   double *R;                // tree levels: depth d at Roff[d], 2^d x Kdim[d]
   long long Roff[HODLR_MAXDEPTH + 2];
+  const KParams *kps; long long nseg;     // batched handle (kp_of), or NULL
 };
 
 // Leaf-local panel column q -> global Xh column (slot e = 1..kappa, qq-th factor of the depth-(e-1) ancestor
@@ -58,11 +59,12 @@ __global__ void __launch_bounds__(AT) k_apply_leaf_up(ApplyCtx c) {
   for (int i = t; i < m; i += AT) { sx[i] = c.xs[lo + i]; sv[i] = c.x[c.perm[lo + i]]; }
   __syncthreads();
   // dense diagonal block, on the fly (Table I + σ² on the diagonal)
+  const KParams kp = kp_of(c.kp, c.kps, c.nseg, lo);
   for (int i = t; i < m; i += AT) {
     const double xi = sx[i];
     double s = 0.0;
-    for (int j = 0; j < m; j++) s = fma(kval(c.kp, xi - sx[j]), sv[j], s);
-    c.ys[lo + i] = fma(sig2(c.kp, lo + i), sv[i], s);
+    for (int j = 0; j < m; j++) s = fma(kval(kp, xi - sx[j]), sv[j], s);
+    c.ys[lo + i] = fma(sig2(kp, lo + i), sv[i], s);
   }
   // P_l = E_l^T x_l: a warp takes 4 consecutive panel columns at once (lanes over rows, every load of a 128-row
   // chunk issued before the arithmetic), then a transposed butterfly leaves column q0 + j in lanes 8j .. 8j+7
@@ -173,6 +175,7 @@ hodlr_status hodlr_apply_impl(hodlr_s *h, const double *x, double *y) {
   c.kp = h->kp; c.n = n; c.ninternal = h->ninternal; c.nleaves = nl; c.ldx = h->ldx; c.kappa = kappa; c.K = K;
   c.xs = h->xs; c.lo = h->lo; c.hi = h->hi; c.perm = h->perm; c.Xh = h->Xh; c.rank = h->rank; c.dt = h->d_dt;
   c.x = x; c.y = y;
+  c.kps = h->d_kps; c.nseg = h->nseg;
   long long rtot = 0;
   for (int d = 0; d <= kappa && d < HODLR_MAXDEPTH + 2; d++) {
     c.Roff[d] = rtot;

@@ -59,6 +59,7 @@ struct LeafCtx {
   long long lsz;            // packed triangle capacity mmax(mmax+1)/2 + 1
   int aug;                  // fused right-hand side: column 0 of the panel is y (gathered through perm)
   const double *y; const long long *perm;
+  const KParams *kps; long long nseg;     // batched handle (kp_of), or NULL
 };
 
 __global__ void __launch_bounds__(LT) k_leaf_factor(LeafCtx c) {
@@ -70,6 +71,7 @@ __global__ void __launch_bounds__(LT) k_leaf_factor(LeafCtx c) {
   double *base = c.use_smem ? sm : c.scratch + (long long)blockIdx.x * c.scratch_per_cta;
   for (long long leaf = c.leaf0 + blockIdx.x; leaf < c.leaf0 + c.nown; leaf += gridDim.x) {
     const long long id = c.ninternal + leaf, lo = c.lo[id], m = c.hi[id] - lo;
+    const KParams kp = kp_of(c.kp, c.kps, c.nseg, lo);
     double *xl = base;                       // m
     double *L = base + c.mmax;               // packed lower m(m+1)/2
     double *Z = L + c.lsz;                   // m x ldz
@@ -82,8 +84,8 @@ __global__ void __launch_bounds__(LT) k_leaf_factor(LeafCtx c) {
       while (i * (i + 1) / 2 > p) i--;
       while ((i + 1) * (i + 2) / 2 <= p) i++;
       long long j = p - i * (i + 1) / 2;
-      double v = kval(c.kp, xl[i] - xl[j]);
-      if (i == j) v += sig2(c.kp, lo + i);
+      double v = kval(kp, xl[i] - xl[j]);
+      if (i == j) v += sig2(kp, lo + i);
       L[p] = v;
     }
     __syncthreads();
@@ -189,8 +191,11 @@ __global__ void __launch_bounds__(TT, 3) k_tree_factor(TreeCtx c) {
 
 // Levels with many small nodes: 128-thread CTAs (6 per SM) -- finer barrier domains, more independent nodes
 // in flight per SM.  Same device code.
+#ifndef TREE_NARROW_MINB
+#define TREE_NARROW_MINB 6
+#endif
 template <bool DD>
-__global__ void __launch_bounds__(TT / 2, 6) k_tree_factor_narrow(TreeCtx c) {
+__global__ void __launch_bounds__(TT / 2, TREE_NARROW_MINB) k_tree_factor_narrow(TreeCtx c) {
   extern __shared__ double sm[];
   const long long i = c.i0 + blockIdx.x;
   tree_node<DD>(c, i, sm, global_pi(c, i));
@@ -222,14 +227,14 @@ __global__ void k_logdet_reduce(const double *leaf_ld, const double *node_ld, lo
   const int t = threadIdx.x;
   long long per = (N + 255) / 256, v0 = t * per, v1 = v0 + per < N ? v0 + per : N;
   double s = 0.0, comp = 0.0;
+  int d = kappa - 1; long long u = 0;     // (depth, index) of internal value v (depth kappa-1 first), advanced in step
+  if (v0 > nleaves && v0 < v1) { u = v0 - nleaves; while (u >= (1LL << d)) { u -= (1LL << d); d--; } }
   for (long long v = v0; v < v1; v++) {
     double x;
     if (v < nleaves) x = leaf_ld[v];
     else {
-      long long u = v - nleaves;       // depth kappa-1 first
-      int d = kappa - 1;
-      while (u >= (1LL << d)) { u -= (1LL << d); d--; }
       x = node_ld[(1LL << d) - 1 + u];
+      if (++u == (1LL << d)) { u = 0; d--; }
     }
     double tt = s + x;
     if (fabs(s) >= fabs(x)) comp += (s - tt) + x; else comp += (x - tt) + s;
@@ -272,7 +277,56 @@ __global__ void k_logdet_final(const double *gathered, int nranks, const double 
   }
 }
 
+// Batched handle: per-problem log det (problem s = blockIdx.x: its leaves left to right, then its internal nodes by
+// depth kappa-1 .. tbatch, left to right -- k_logdet_reduce's order on its subtree) and y^T C_s^-1 y from the fused
+// right-hand side (the aug entry of the problem root's Pi; NaN without one).  out[s], out[B + s].
+__global__ void k_logdet_segments(const double *leaf_ld, const double *node_ld, int kappa, int t, const double *Pi_t,
+                                  long long pi_sz, int aug, double *out) {
+  __shared__ double ss[256], cc[256];
+  const int s = blockIdx.x, B = gridDim.x;
+  const long long Ls = 1LL << (kappa - t);               // leaves per problem
+  const long long N = Ls + (Ls - 1);
+  const int th = threadIdx.x;
+  const long long per = (N + 255) / 256, v0 = th * per, v1 = v0 + per < N ? v0 + per : N;
+  double S = 0.0, comp = 0.0;
+  int dl = kappa - t - 1; long long u = 0;                // (local depth, index) of internal value v, advanced in step
+  if (v0 > Ls && v0 < v1) { u = v0 - Ls; while (u >= (1LL << dl)) { u -= (1LL << dl); dl--; } }
+  for (long long v = v0; v < v1; v++) {
+    double x;
+    if (v < Ls) x = leaf_ld[s * Ls + v];
+    else {
+      x = node_ld[(1LL << (t + dl)) - 1 + (long long)s * (1LL << dl) + u];
+      if (++u == (1LL << dl)) { u = 0; dl--; }
+    }
+    const double tt = S + x;
+    if (fabs(S) >= fabs(x)) comp += (S - tt) + x; else comp += (x - tt) + S;
+    S = tt;
+  }
+  ss[th] = S; cc[th] = comp;
+  __syncthreads();
+  if (th == 0) {
+    double T = 0.0, C = 0.0;
+    for (int j = 0; j < 256; j++) {
+      const double x = ss[j], tt = T + x;
+      if (fabs(T) >= fabs(x)) C += (T - tt) + x; else C += (x - tt) + T;
+      T = tt;
+      C += cc[j];
+    }
+    out[s] = T + C;
+    out[B + s] = aug ? Pi_t[(long long)s * pi_sz] : NAN;
+  }
+}
+
 }  // namespace
+
+hodlr_status hodlr_batch_parts(hodlr_s *h, double *d_out) {
+  const int t = h->tbatch, kappa = h->kappa;
+  const long long Kt = h->dt.Kf[t];
+  k_logdet_segments<<<h->nbatch, 256, 0, h->st>>>(h->leaf_ld, h->node_ld, kappa, t, h->Pipool + h->dt.piOff[t],
+                                                  Kt * (Kt + 1) / 2, h->aug, d_out);
+  HLAUNCH(h, "k_logdet_segments");
+  return HODLR_OK;
+}
 
 // Leaf factor storage (T = ceil(leaf_max / 8) tile rows, or 8 / 16 on the fast path): allocated at build time
 // because the leaf Cholesky runs during the build.
@@ -350,6 +404,7 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
     lc.dt = h->d_dt; lc.Lf = h->Lf; lc.lstride = h->lstride; lc.Pi = h->Pipool + dt.piOff[kappa];
     lc.leaf_ld = h->leaf_ld; lc.flags = h->dflags;
     lc.aug = h->aug; lc.y = h->y_aug; lc.perm = h->perm;
+    lc.kps = h->d_kps; lc.nseg = h->nseg;
     lc.mmax = mmax;
     hodlr_own_nodes(h, kappa, &lc.leaf0, &lc.nown);
     lc.lsz = (long long)mmax * (mmax + 1) / 2 + 1;

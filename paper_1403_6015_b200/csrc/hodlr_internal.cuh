@@ -47,6 +47,13 @@ struct KParams {
 };
 // the diagonal term sigma_i^2 of sorted point i (C_ij = sigma_i^2 delta_ij + k(x_i, x_j))
 __device__ __forceinline__ double sig2(const KParams &kp, long long i) { return kp.dn ? kp.dn[i] : kp.s2; }
+// Batched handles (hodlr_build_batch, NEXT-4): B problems on the same points, problem s on the sorted rows
+// [s nseg, (s + 1) nseg) with its own covariance parameters kps[s].  Every covariance entry the path evaluates lies
+// inside one problem's rows (the blocks of the top log2 B levels are exactly zero and skipped, and leaves never
+// straddle problems), so one lookup per block or leaf selects the parameters.
+__device__ __forceinline__ const KParams &kp_of(const KParams &kp, const KParams *kps, long long nseg, long long row) {
+  return kps ? kps[row / nseg] : kp;
+}
 // x / b for many x and one b: rb = RN(1 / b), q = RN(x rb), then one FMA correction with the exact remainder
 // x - b q (Markstein): the correctly rounded quotient (barring over/underflow) at 3 FP ops instead of a division
 __device__ __forceinline__ double div_by(double x, double b, double rb) {
@@ -139,6 +146,8 @@ struct AcaCtx {
   int maxsteps;
   int nitems;               // items of this pass (the persistent step kernel strides over them)
   const int *forced;        // test hook (hodlr_opts.forced_ranks): stop block b at exactly forced[b] terms, or NULL
+  const KParams *kps;       // batched handle: per-problem parameters (kp_of), or NULL
+  long long nseg;           // batched handle: rows per problem
 };
 
 // ----------------------------------------------------------------------------------------------
@@ -162,6 +171,11 @@ struct hodlr_s {
   int dev;
   long long n;
   KParams kp;
+  // batched handle (hodlr_build_batch): nbatch = 2^tbatch problems of nseg points each (n = nbatch * nseg); the
+  // per-problem parameters on the device; nbatch = 1, d_kps = NULL otherwise
+  int nbatch, tbatch;
+  long long nseg;
+  KParams *d_kps;
   double theta[2];
   int leaf;
   double eps;
@@ -249,9 +263,10 @@ void *hodlr_dalloc_tmp(hodlr_s *h, size_t bytes);   // dead after the build: han
 extern long long hodlr_global_launches;
 
 // phase entry points (one per .cu file)
-hodlr_status hodlr_sort_and_tree(hodlr_s *h, const double *x);
+hodlr_status hodlr_sort_and_tree(hodlr_s *h, const double *x, long long n);   // sorts n <= h->n points
 hodlr_status hodlr_aca(hodlr_s *h);
 hodlr_status hodlr_factor_impl(hodlr_s *h);
+hodlr_status hodlr_batch_parts(hodlr_s *h, double *d_out);   // batched: per-problem log det [B] and y^T C^-1 y [B]
 hodlr_status hodlr_leaf_factor_mma(hodlr_s *h, int K, double *Pi_leaf, bool *used);
 hodlr_status hodlr_apply_impl(hodlr_s *h, const double *x, double *y);
 hodlr_status hodlr_predict_impl(hodlr_s *h, const double *y, const double *xt, long long m, double *mean, double *var);

@@ -23,8 +23,6 @@
 
 namespace {
 
-constexpr int NTH = 256;   // 8 warps
-constexpr int NW = NTH / 32;
 
 __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -70,6 +68,7 @@ struct LeafMmaCtx {
   long long leaf0;          // first leaf of this launch (this rank's subtree)
   int aug;                  // fused right-hand side (hodlr_factor_solve): panel column 0 is y[perm[rows]]
   const double *y; const long long *perm;
+  const KParams *kps; long long nseg;     // batched handle (kp_of), or NULL
 };
 
 // Panel entry of the fused right-hand side: y of sorted row lo + row (0 beyond the leaf); flags non-finite y.
@@ -163,8 +162,13 @@ __device__ unsigned long long g_chol_stamps[2][6];
 #else
 #define CSTAMP(k)
 #endif
+// CTA size: 8 warps for 128-point leaves (2 CTAs per SM); 4 warps for 64-point leaves (the X = L^{-1} sweep needs
+// NW >= T / 2), 4 CTAs per SM -- a 64-point leaf's chain of 8 diagonal steps is latency, so more leaves in flight.
+template <int P> struct CholCfg { static constexpr int NT = P == 64 ? 128 : 256, MINB = P == 64 ? 4 : 2; };
 template <int P, bool SEO>
-__global__ void __launch_bounds__(NTH, 2) k_leaf_chol(LeafMmaCtx c) {
+__global__ void __launch_bounds__(CholCfg<P>::NT, CholCfg<P>::MINB) k_leaf_chol(LeafMmaCtx c) {
+  constexpr int NTH = CholCfg<P>::NT, NW = NTH / 32;
+  static_assert(2 * NW >= P / 8, "X sweep: every tile column needs a warp");
   constexpr int T = P / 8;
   constexpr int NTILE = T * (T + 1) / 2;
   extern __shared__ double sm[];
@@ -176,6 +180,7 @@ __global__ void __launch_bounds__(NTH, 2) k_leaf_chol(LeafMmaCtx c) {
   double *sdiag = sx + P;                       // P
   const long long leaf = c.leaf0 + blockIdx.x;
   const long long id = c.ninternal + leaf, lo = c.lo[id];
+  const KParams kp = kp_of(c.kp, c.kps, c.nseg, lo);
   const int m = (int)(c.hi[id] - lo);
   CSTAMP(0)
   if (t == 0) bad = 0;
@@ -191,7 +196,7 @@ __global__ void __launch_bounds__(NTH, 2) k_leaf_chol(LeafMmaCtx c) {
       const int r = lane >> 2, cc = (lane & 3) + 4 * h;
       const int i = 8 * I + r, j = 8 * J + cc;
       double v;
-      if (i < m && j < m) { v = kval_t<SEO>(c.kp, sx[i] - sx[j]); if (i == j) v += sig2(c.kp, lo + i); }
+      if (i < m && j < m) { v = kval_t<SEO>(kp, sx[i] - sx[j]); if (i == j) v += sig2(kp, lo + i); }
       else v = (i == j) ? 1.0 : 0.0;
       sL[ti * 64 + 32 * h + lane] = v;
     }
@@ -511,8 +516,12 @@ __global__ void __launch_bounds__(ZTH, 1) k_leaf_zsyrk(LeafMmaCtx c) {
 // Persistent form of k_leaf_zsyrk (X staged): one CTA per SM walks the leaves leaf0 + blockIdx.x + k gridDim.x;
 // the next leaf's X tiles are copied (cp.async) while this leaf's Pi = Z^T Z runs, and its panel E as soon as Z is
 // free, so only the E copy is exposed per leaf (no CTA turnaround either).
-template <int P>
-__global__ void __launch_bounds__(ZTH, 1) k_leaf_zsyrk_p(LeafMmaCtx c, long long nown) {
+// NT threads: 512 (16 warps, one CTA per SM) in general; 256 (8 warps, 4 CTAs per SM) for 64-point leaves with at
+// most 64 panel columns -- there a leaf has too few Z tiles for 16 warps and the per-leaf barriers dominate, so
+// four leaves per SM are in flight instead of one (the batched config-4 factorization: 131072 such leaves).
+template <int P, int NT>
+__global__ void __launch_bounds__(NT, NT == 512 ? 1 : 4) k_leaf_zsyrk_p(LeafMmaCtx c, long long nown) {
+  constexpr int ZTH = NT, ZW = NT / 32;
   constexpr int T = P / 8;
   constexpr int NTILE = T * (T + 1) / 2;
   constexpr int LDR = P + 4;
@@ -646,6 +655,7 @@ static LeafMmaCtx leaf_ctx(hodlr_s *h, int K, double *Pi_leaf) {
   c.xs = h->xs; c.lo = h->lo; c.hi = h->hi; c.Xh = h->Xh; c.ldx = h->ldx; c.rank = h->rank; c.dt = h->d_dt;
   c.Lf = h->Lf; c.lstride = h->lstride; c.Pi = Pi_leaf; c.leaf_ld = h->leaf_ld; c.flags = h->dflags;
   c.aug = h->aug; c.y = h->y_aug; c.perm = h->perm;
+  c.kps = h->d_kps; c.nseg = h->nseg;
   long long cnt;
   hodlr_own_nodes(h, h->kappa, &c.leaf0, &cnt);
   return c;
@@ -664,7 +674,7 @@ hodlr_status hodlr_leaf_chol_mma(hodlr_s *h, cudaStream_t stream, bool *launched
 #define LAUNCH_CHOL(PP, SE_)                                                                                    \
   do {                                                                                                         \
     HCUDA(hodlr_allow_smem((const void *)k_leaf_chol<PP, SE_>, h->dev));  \
-    k_leaf_chol<PP, SE_><<<(int)(h->nleaves >> h->tsplit), NTH, smem, stream>>>(c);                           \
+    k_leaf_chol<PP, SE_><<<(int)(h->nleaves >> h->tsplit), CholCfg<PP>::NT, smem, stream>>>(c);                           \
   } while (0)
   const bool seo = h->kp.kern == HODLR_SE;
   if (P == 64) { if (seo) LAUNCH_CHOL(64, true); else LAUNCH_CHOL(64, false); }
@@ -708,15 +718,17 @@ hodlr_status hodlr_leaf_factor_mma(hodlr_s *h, int K, double *Pi_leaf, bool *use
     HCUDA(hodlr_allow_smem((const void *)k_leaf_zsyrk<PP, XGV>, h->dev)); \
     k_leaf_zsyrk<PP, XGV><<<grid, ZTH, smem, h->st>>>(c);                                                      \
   } while (0)
-#define LAUNCH_ZSP(PP)                                                                                         \
+#define LAUNCH_ZSP(PP, NT, PER_SM)                                                                             \
   do {                                                                                                        \
-    HCUDA(hodlr_allow_smem((const void *)k_leaf_zsyrk_p<PP>, h->dev));   \
-    k_leaf_zsyrk_p<PP><<<std::min(grid, nsm), ZTH, smem, h->st>>>(c, (long long)grid);                          \
+    HCUDA(hodlr_allow_smem((const void *)k_leaf_zsyrk_p<PP, NT>, h->dev));   \
+    k_leaf_zsyrk_p<PP, NT><<<std::min(grid, (PER_SM) * nsm), NT, smem, h->st>>>(c, (long long)grid);            \
   } while (0)
-  int nsm = 148;
+  int nsm = 148, maxsm_sm = 0;
   HCUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->dev));
-  if (P == 64) { if (wide) LAUNCH_ZS(64, true); else LAUNCH_ZSP(64); }
-  else { if (wide) LAUNCH_ZS(128, true); else LAUNCH_ZSP(128); }
+  HCUDA(cudaDeviceGetAttribute(&maxsm_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, h->dev));
+  const bool small = P == 64 && Kp <= 64 && 4 * (smem + 1024) <= (size_t)maxsm_sm;
+  if (P == 64) { if (wide) LAUNCH_ZS(64, true); else if (small) LAUNCH_ZSP(64, 256, 4); else LAUNCH_ZSP(64, 512, 1); }
+  else { if (wide) LAUNCH_ZS(128, true); else LAUNCH_ZSP(128, 512, 1); }
 #undef LAUNCH_ZS
 #undef LAUNCH_ZSP
   HLAUNCH(h, "k_leaf_zsyrk");

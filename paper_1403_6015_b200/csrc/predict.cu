@@ -66,6 +66,7 @@ __global__ void k_predict_var_h(KParams kp, const double *hv, long long hcol, in
 }  // namespace
 
 hodlr_status hodlr_predict_impl(hodlr_s *h, const double *y, const double *xt, long long m, double *mean, double *var) {
+  if (h->nbatch > 1) return hodlr_set_error(HODLR_EINVAL, "predict: not supported on batched handles");
   const long long n = h->n;
   const int nsl = (int)((n + MSL - 1) / MSL);
   const size_t need = (size_t)n * (1 + PB) + (size_t)(m > 0 ? m : 1) * nsl;

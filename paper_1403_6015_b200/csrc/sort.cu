@@ -136,8 +136,7 @@ __global__ void k_finish(const unsigned long long *__restrict__ key, const long 
 
 }  // namespace
 
-hodlr_status hodlr_sort_and_tree(hodlr_s *h, const double *x) {
-  const long long n = h->n;
+hodlr_status hodlr_sort_and_tree(hodlr_s *h, const double *x, long long n) {
   const int ntiles = (int)((n + TILE - 1) / TILE);
   unsigned long long *k0 = (unsigned long long *)hodlr_dalloc_tmp(h, sizeof(unsigned long long) * n);
   unsigned long long *k1 = (unsigned long long *)hodlr_dalloc_tmp(h, sizeof(unsigned long long) * n);

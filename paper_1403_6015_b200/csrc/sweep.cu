@@ -1,14 +1,27 @@
 // sweep.cu -- config 4 (BASELINE.json): GP log-likelihood (eq. 1) of B hyper-parameter
-// settings (a, ell, sigma2) on the same points and observations.  The settings are independent problems:
-// on one GPU up to `workers` of them run concurrently (host threads, one stream each, so the small top-level
-// kernels of different settings overlap); with dist (nranks > 1) rank g takes settings g, g + P, ... and the
-// values are allgathered ("replicas only").
+// settings (a, ell, sigma2) on the same points and observations.  The settings are independent problems; they are
+// factored in batches (hodlr_build_batch: every kernel launch of the path covers a whole batch), and a batch that
+// fails is redone setting by setting (up to `workers` concurrently: host threads, one stream each) so that each
+// setting reports its own status.  With dist (nranks > 1) rank g takes settings g, g + P, ... and the values are
+// allgathered ("replicas only").
 #include "hodlr_internal.cuh"
 #include <thread>
 #include <vector>
 #include <atomic>
 #include <string.h>
 #include <string>
+
+#ifndef SWEEP_MAX_POINTS
+#define SWEEP_MAX_POINTS (1LL << 23)   // points (B n) per batched handle
+#endif
+
+namespace {
+__global__ void k_tile_rhs(const double *y, long long n, int B, double *yb) {
+  const long long N = n * B;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x)
+    yb[i] = y[i % n];
+}
+}  // namespace
 
 extern "C" hodlr_status gp_loglik_sweep(const double *x, const double *y, int64_t n, hodlr_kernel kernel,
                                         const double *thetas, const double *sigma2s, int32_t B, int32_t leaf,
@@ -27,8 +40,63 @@ extern "C" hodlr_status gp_loglik_sweep(const double *x, const double *y, int64_
   std::vector<double> val(B, 0.0);
   std::vector<hodlr_status> stat(B, HODLR_OK);
   std::vector<std::string> msg(B);
+  // the caller's stream orders our reads of x and y after its prior work
+  ce = cudaStreamSynchronize((cudaStream_t)cuda_stream);
+  if (ce != cudaSuccess) return hodlr_cuda_check(ce, "gp_loglik_sweep: stream");
+  const double half_log2pi_n = 0.5 * (double)n * log(2.0 * M_PI);
+  // ---- batches: the largest powers of two of this rank's settings that fit ----
+  std::vector<int> redo;
+  {
+    const int tw = 2;                              // (the rational quadratic is refused above)
+    long long bmax = 1;
+    while (bmax * 2 * n <= SWEEP_MAX_POINTS) bmax *= 2;
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    size_t k0 = 0;
+    double *yb = nullptr; long long yb_n = 0;
+    while (k0 < mine.size()) {
+      long long nb = 1;
+      while (nb * 2 <= bmax && k0 + nb * 2 <= mine.size()) nb *= 2;
+      if (nb == 1 || n < leaf) {                   // single settings: the per-setting path below
+        for (size_t k = k0; k < k0 + nb; k++) redo.push_back(mine[k]);
+        k0 += nb; continue;
+      }
+      std::vector<double> th((size_t)nb * tw), s2((size_t)nb);
+      for (long long j = 0; j < nb; j++) {
+        const int b = mine[k0 + j];
+        for (int q = 0; q < 2; q++) th[j * tw + q] = thetas[2 * b + q];
+        s2[j] = sigma2s[b];
+      }
+      hodlr_status st = HODLR_OK;
+      if (yb_n < nb * n) {
+        if (yb) cudaFree(yb);
+        yb = nullptr; yb_n = 0;
+        if (cudaMalloc(&yb, sizeof(double) * nb * n) != cudaSuccess) st = hodlr_set_error(HODLR_ENOMEM, "sweep: rhs");
+        else yb_n = nb * n;
+      }
+      hodlr_t h = nullptr;
+      if (st == HODLR_OK) {
+        k_tile_rhs<<<592, 256, 0, s>>>(y, n, (int)nb, yb);
+        hodlr_global_launches++;
+        st = hodlr_build_batch(x, n, kernel, th.data(), s2.data(), (int)nb, leaf, eps, nullptr, s, &h);
+      }
+      double qtot = 0.0;
+      std::vector<double> ld(nb), qd(nb);
+      // y fused into the factorization: y^T C_s^{-1} y is problem s's root Pi, no solve pass
+      if (st == HODLR_OK) st = hodlr_factor_solve(h, yb, nullptr, &qtot);
+      if (st == HODLR_OK) st = hodlr_batch_results(h, ld.data(), qd.data());
+      hodlr_free(h);
+      if (st == HODLR_OK) {
+        // eq. 1: -1/2 y^T C^{-1} y - 1/2 log det C - (n/2) log(2 pi)
+        for (long long j = 0; j < nb; j++) val[mine[k0 + j]] = -0.5 * qd[j] - 0.5 * ld[j] - half_log2pi_n;
+      } else {
+        for (long long j = 0; j < nb; j++) redo.push_back(mine[k0 + j]);   // find the failing setting(s)
+      }
+      k0 += nb;
+    }
+    if (yb) { cudaStreamSynchronize(s); cudaFree(yb); }
+  }
   std::atomic<int> next(0);
-  const int W = std::max(1, std::min<int>(workers > 0 ? workers : 8, (int)mine.size()));
+  const int W = std::max(1, std::min<int>(workers > 0 ? workers : 8, (int)redo.size()));
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int coop = W > 1 ? std::max(16, 2 * nsm / W) : 0;
@@ -38,8 +106,8 @@ extern "C" hodlr_status gp_loglik_sweep(const double *x, const double *y, int64_
     cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
     for (;;) {
       const int k = next.fetch_add(1);
-      if (k >= (int)mine.size()) break;
-      const int b = mine[k];
+      if (k >= (int)redo.size()) break;
+      const int b = redo[k];
       hodlr_t h = nullptr;
       double ll = -INFINITY;
       hodlr_status st = hodlr_build(x, n, kernel, thetas + 2 * b, sigma2s[b], leaf, eps, nullptr, nullptr, s, &h);
@@ -49,7 +117,7 @@ extern "C" hodlr_status gp_loglik_sweep(const double *x, const double *y, int64_
       if (st == HODLR_OK) st = hodlr_factor_solve(h, y, nullptr, &quad);
       if (st == HODLR_OK) st = hodlr_logdet(h, &ld);
       // eq. 1: -1/2 y^T C^{-1} y - 1/2 log det C - (n/2) log(2 pi)
-      if (st == HODLR_OK) ll = -0.5 * quad - 0.5 * ld - 0.5 * (double)n * log(2.0 * M_PI);
+      if (st == HODLR_OK) ll = -0.5 * quad - 0.5 * ld - half_log2pi_n;
       if (st != HODLR_OK) msg[b] = hodlr_last_error();
       hodlr_free(h);
       val[b] = st == HODLR_OK ? ll : -INFINITY;
@@ -58,11 +126,9 @@ extern "C" hodlr_status gp_loglik_sweep(const double *x, const double *y, int64_
     cudaStreamSynchronize(s);
     cudaStreamDestroy(s);
   };
-  // the caller's stream orders our reads of x and y after its prior work
-  ce = cudaStreamSynchronize((cudaStream_t)cuda_stream);
-  if (ce != cudaSuccess) return hodlr_cuda_check(ce, "gp_loglik_sweep: stream");
   std::vector<std::thread> th;
-  for (int w = 0; w < W; w++) th.emplace_back(work);
+  if (!redo.empty())
+    for (int w = 0; w < W; w++) th.emplace_back(work);
   for (auto &t : th) t.join();
   if (P > 1) {     // allgather (value, status) of every rank's settings (slot k of rank r = setting r + k P)
     hodlr_s ex;

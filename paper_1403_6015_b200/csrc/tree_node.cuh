@@ -4,6 +4,9 @@
 // T_c = S_c^{-1} B_c refined in compensated arithmetic, Pi_c = Pi_c1 + Pi_c2 - B^T T (compensated).
 #pragma once
 #include "hodlr_internal.cuh"
+#ifndef TREE_GJ_REGS
+#define TREE_GJ_REGS 8           // largest q of the register Gauss-Jordan (8; 16 measured slower: spills)
+#endif
 
 struct TreeCtx {
   int d;                    // depth of the nodes of this launch
@@ -24,7 +27,7 @@ __host__ __device__ __forceinline__ long long tree_smem_doubles(int q, int ldk) 
   return 5LL * q * q + 6LL * q + 4LL * q * ldk;
 }
 
-// Gauss-Jordan with partial pivoting on [S | I] (q <= QB rows, one row per lane, in registers), q <= 8.  Row
+// Gauss-Jordan with partial pivoting on [S | I] (q <= QB rows, one row per lane, in registers), q <= 16.  Row
 // interchanges are logical: every lane carries the current position `pos` of its row, so a swap is two position
 // updates.  Pivot rule as the LU of the coupling system (row of max |.| among the not-yet-pivoted positions >= k,
 // the smallest position on ties), hence the same pivots, U_kk and sign.  On exit the lane at position a writes row a
@@ -212,13 +215,14 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
   __syncthreads();
   TSTAMP(1)
   // ---------------- Gauss-Jordan with partial pivoting ----------------
-  // q <= 8: warp 0 in registers (gj_regs); 8 < q <= 32: warp 0 in shared memory (gj_warp); larger systems: the
+  // q <= 16: warp 0 in registers (gj_regs); 16 < q <= 32: warp 0 in shared memory (gj_warp); larger systems: the
   // whole CTA, one barrier per step.
   // (S^{-1} goes to W2, row-major; gj_warp uses W2 as its transposed work area and then writes S^{-1} into W)
   if (q <= 32) {
     if (t < 32) {
       int sign, zero;
       if (q <= 8) gj_regs<8>(W, W2, q, colk, sign, zero);
+      else if (q <= TREE_GJ_REGS) gj_regs<16>(W, W2, q, colk, sign, zero);
       else gj_warp(W, W2, W, q, colk, sign, zero);
       if (t == 0) { s_sign = sign; s_zero = zero; }
     }
@@ -294,7 +298,7 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
   TSTAMP(3)
   const bool zero = s_zero != 0;
   // S^{-1}, row stride 2q: W2 (gj_regs), W (gj_warp), or wherever the last ping-pong step left it
-  const double *Si = ((q <= 8 || (q > 32 && (q & 1))) ? W2 : W) + q;
+  const double *Si = ((q <= TREE_GJ_REGS || (q > 32 && (q & 1))) ? W2 : W) + q;
   if (!zero && Kd > 0) {
     const int qK = q * ldk;
     for (int e = t; e < qK; e += NT) {                // T_hi = S^{-1} B

@@ -23,7 +23,8 @@ EXPORTS = ("hodlr_build", "hodlr_factor", "hodlr_factor_solve", "hodlr_cache_tri
            "hodlr_info",
            "hodlr_get_order", "hodlr_get_tree", "hodlr_get_logdet_parts", "hodlr_free", "hodlr_last_error",
            "hodlr_version", "hodlr_launch_count", "hodlr_nccl_unique_id", "hodlr_group_create",
-           "hodlr_group_destroy", "hodlr_group_mode", "hodlr_dist_plan", "gp_loglik_sweep")
+           "hodlr_group_destroy", "hodlr_group_mode", "hodlr_dist_plan", "gp_loglik_sweep", "hodlr_build_batch",
+           "hodlr_batch_results")
 
 
 class HodlrError(RuntimeError):
@@ -101,6 +102,8 @@ def load(build_if_missing: bool = True):
         lib.hodlr_group_mode.argtypes = [P, I32]; lib.hodlr_group_mode.restype = I32
         lib.hodlr_dist_plan.argtypes = [I64, I32, I32, I32, P, P, P, P, P, P]; lib.hodlr_dist_plan.restype = I32
         lib.gp_loglik_sweep.argtypes = [P, P, I64, I32, P, P, I32, I32, D, P, P, I32, P]
+        lib.hodlr_build_batch.argtypes = [P, I64, I32, P, P, I32, I32, D, P, P, P]
+        lib.hodlr_batch_results.argtypes = [P, P, P]
         lib.gp_loglik_sweep.restype = I32
         _lib = lib
         return lib
@@ -144,6 +147,32 @@ def hodlr_build(x: torch.Tensor, kernel: int, theta, sigma2: float, leaf: int, e
                            C.byref(dist) if dist is not None else None, C.byref(opts), _stream_ptr(stream),
                            C.byref(h)))
     return h.value
+
+
+def hodlr_build_batch(x: torch.Tensor, kernel: int, thetas, sigma2s, leaf: int, eps: float, rank_cap: int = 0,
+                      stream=None, forced_ranks=None) -> int:
+    """B = 2^t problems on the same points (hodlr_build_batch): thetas (B, 2) {a, ell} ((B, 3) for RQ), sigma2s (B,)."""
+    import numpy as np
+    lib = load()
+    x = _dev_f64(x, "x")
+    s2 = np.ascontiguousarray(np.asarray(sigma2s, dtype=np.float64).reshape(-1))
+    th = np.ascontiguousarray(np.asarray(thetas, dtype=np.float64).reshape(s2.size, -1))
+    opts = hodlr_opts(int(rank_cap))
+    if forced_ranks is not None:
+        fr = np.ascontiguousarray(forced_ranks, dtype=np.int32)
+        opts.forced_ranks = fr.ctypes.data
+    h = C.c_void_p(0)
+    _check(lib.hodlr_build_batch(x.data_ptr(), x.numel(), int(kernel), th.ctypes.data, s2.ctypes.data, s2.size,
+                                 int(leaf), float(eps), C.byref(opts), _stream_ptr(stream), C.byref(h)))
+    return h.value
+
+
+def hodlr_batch_results(h: int, nbatch: int, quad: bool = True):
+    """Per-problem log det (and y_s^T C_s^{-1} y_s of the fused right-hand side): numpy arrays."""
+    import numpy as np
+    ld = np.zeros(nbatch); q = np.zeros(nbatch)
+    _check(load().hodlr_batch_results(h, ld.ctypes.data, q.ctypes.data if quad else None))
+    return (ld, q) if quad else ld
 
 
 def hodlr_factor(h: int):
@@ -343,3 +372,21 @@ class HODLR:
         a = np.zeros(1 << k); b = np.zeros(max((1 << k) - 1, 1))
         _check(load().hodlr_get_logdet_parts(self._h, a.ctypes.data, b.ctypes.data))
         return a, b[:(1 << k) - 1]
+
+
+class HODLRBatch(HODLR):
+    """B = 2^t problems (thetas[s], sigma2s[s]) on the same points x, held as one block-diagonal handle of order
+    B n (hodlr_build_batch); vectors are problem-major (B n,)."""
+
+    def __init__(self, x: torch.Tensor, kernel, thetas, sigma2s, leaf: int, eps: float, rank_cap: int = 0,
+                 stream=None, forced_ranks=None):
+        if isinstance(kernel, str):
+            kernel = KERNELS[kernel]
+        import numpy as np
+        self.nbatch = int(np.asarray(sigma2s).size)
+        self.n = x.numel() * self.nbatch
+        self._dist = None
+        self._h = hodlr_build_batch(x, kernel, thetas, sigma2s, leaf, eps, rank_cap, stream, forced_ranks)
+
+    def results(self, quad: bool = True):
+        return hodlr_batch_results(self._h, self.nbatch, quad)
