@@ -850,13 +850,8 @@ hodlr_status hodlr_aca(hodlr_s *h) {
   h->st = sm_main;
   HCUDA(cudaStreamWaitEvent(h->st, h->ev_hi, 0));
   ph_end(h, PH_ACA);
-  HCUDA(cudaStreamSynchronize(h->st));
-  hodlr_trace("aca: synced");
-  int steps = hsteps;
-  if (nbig > 0 && !nograph) {
-    HCUDA(cudaMemcpy(&steps, h->dflags + 6, sizeof(int), cudaMemcpyDeviceToHost));
-    h->launches += 3 * steps; hodlr_global_launches += 3 * steps;
-  }
-  h->aca_steps = steps;
+  // no host round trip here: the graph's step counter (dflags[6]) comes back with the build's rank readback
+  // (api.cu), which also accounts the graph's launches
+  h->aca_steps = (nbig > 0 && !nograph) ? -1 : hsteps;
   return HODLR_OK;
 }

@@ -193,6 +193,7 @@ struct HRes {
   cudaEvent_t ev_join2;
   cudaEvent_t ev0, ev1, ev_fork, ev_join, ev_chol, ev_hi;
   cudaEvent_t ph_ev[PH_N][2];
+  void *pin;                 // pinned host staging for the handle's device-to-host reads (HODLR_PIN_BYTES)
 };
 static std::mutex g_res_mu;
 static std::vector<HRes> g_res_pool;
@@ -228,11 +229,13 @@ static void res_acquire(hodlr_s *h) {
     cudaStreamCreateWithPriority(&r.sthi, cudaStreamNonBlocking, hi_pri);
     cudaEventCreateWithFlags(&r.ev_hi, cudaEventDisableTiming);
     for (int p = 0; p < PH_N; p++) for (int j = 0; j < 2; j++) cudaEventCreate(&r.ph_ev[p][j]);
+    if (cudaHostAlloc(&r.pin, HODLR_PIN_BYTES, cudaHostAllocDefault) != cudaSuccess) { cudaGetLastError(); r.pin = nullptr; }
   }
   h->st2b = r.st2b; h->ev_join2 = r.ev_join2;
   h->st2 = r.st2; h->st3 = r.st3; h->ev0 = r.ev0; h->ev1 = r.ev1; h->ev_fork = r.ev_fork; h->ev_join = r.ev_join;
   h->ev_chol = r.ev_chol; h->sthi = r.sthi; h->ev_hi = r.ev_hi;
   for (int p = 0; p < PH_N; p++) for (int j = 0; j < 2; j++) h->ph_ev[p][j] = r.ph_ev[p][j];
+  h->pin = r.pin;
 }
 
 static void res_release(hodlr_s *h) {
@@ -242,6 +245,7 @@ static void res_release(hodlr_s *h) {
   r.dev = h->dev; r.st2 = h->st2; r.st3 = h->st3; r.ev0 = h->ev0; r.ev1 = h->ev1; r.ev_fork = h->ev_fork;
   r.ev_join = h->ev_join; r.ev_chol = h->ev_chol; r.sthi = h->sthi; r.ev_hi = h->ev_hi;
   for (int p = 0; p < PH_N; p++) for (int j = 0; j < 2; j++) r.ph_ev[p][j] = h->ph_ev[p][j];
+  r.pin = h->pin;
   std::lock_guard<std::mutex> lk(g_res_mu);
   g_res_pool.push_back(r);
 }
@@ -481,12 +485,23 @@ static hodlr_status build_impl(const double *x, int64_t nseg, int32_t B, hodlr_k
     h->chol_done = launched ? 1 : 0;
   }
   {
-    int f5 = 0, f8 = 0;
-    CK(cudaMemcpyAsync(&f5, h->dflags + 5, sizeof(int), cudaMemcpyDeviceToHost, h->st));
-    CK(cudaMemcpyAsync(&f8, h->dflags + 8, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+    // one round trip: the flags and the per-block ranks through the pinned staging buffer (pageable
+    // destinations would each block the host on their own)
+    int *pf = (int *)h->pin;
+    const bool pin_ranks = pf && sizeof(int) * (16 + (size_t)h->ninternal) <= HODLR_PIN_BYTES;
+    if (pf) CK(cudaMemcpyAsync(pf, h->dflags, sizeof(int) * 16, cudaMemcpyDeviceToHost, h->st));
     if (h->ninternal > 0)
-      CK(cudaMemcpyAsync(h->h_rank, h->rank, sizeof(int) * h->ninternal, cudaMemcpyDeviceToHost, h->st));
+      CK(cudaMemcpyAsync(pin_ranks ? pf + 16 : h->h_rank, h->rank, sizeof(int) * h->ninternal, cudaMemcpyDeviceToHost, h->st));
+    int fl16[16];
+    if (!pf) CK(cudaMemcpyAsync(fl16, h->dflags, sizeof(fl16), cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
+    if (pf) memcpy(fl16, pf, sizeof(fl16));
+    if (pin_ranks && h->ninternal > 0) memcpy(h->h_rank, pf + 16, sizeof(int) * h->ninternal);
+    int f5 = fl16[5], f8 = fl16[8];
+    if (h->aca_steps < 0) {                             // the graph's step counter (hodlr_aca): 3 launches per step
+      h->aca_steps = fl16[6];
+      h->launches += 3 * fl16[6]; hodlr_global_launches += 3 * fl16[6];
+    }
     if (f8) { st = hodlr_set_error(HODLR_EINVAL, "build: noise contains a negative or non-finite entry"); goto fail; }
     // per-depth max ranks (the panel layout K_e must agree on every rank) and the rank-cap hits
     std::vector<double> loc(kappa + 2, 0.0);
@@ -611,14 +626,23 @@ hodlr_status hodlr_factor_solve(hodlr_t h, const double *y, double *x, double *q
   if (st == HODLR_OK && x) st = hodlr_solve_impl(h, y, x, 1, h->n, false, true);   // down passes only
   int f[4] = {0, 0, 0, 0};
   double quad = 0.0;
+  // results through the pinned staging buffer: [0, 2) log det, y^T C^{-1} y; then the flags (one round trip)
+  double *pd = (double *)h->pin;
   if (st == HODLR_OK) {
-    ce = cudaMemcpyAsync(f, h->dflags, sizeof(f), cudaMemcpyDeviceToHost, h->st);
-    if (ce == cudaSuccess) ce = cudaMemcpyAsync(&h->logdet, h->d_logdet, sizeof(double), cudaMemcpyDeviceToHost, h->st);
-    // Pi at the root with the fused right-hand side is the 1 x 1 matrix y^T C^{-1} y
-    if (ce == cudaSuccess) ce = cudaMemcpyAsync(&quad, h->Pipool + h->dt.piOff[0], sizeof(double), cudaMemcpyDeviceToHost, h->st);
+    if (pd) {
+      ce = cudaMemcpyAsync(pd, h->d_logdet, sizeof(double), cudaMemcpyDeviceToHost, h->st);
+      // Pi at the root with the fused right-hand side is the 1 x 1 matrix y^T C^{-1} y
+      if (ce == cudaSuccess) ce = cudaMemcpyAsync(pd + 1, h->Pipool + h->dt.piOff[0], sizeof(double), cudaMemcpyDeviceToHost, h->st);
+      if (ce == cudaSuccess) ce = cudaMemcpyAsync(pd + 2, h->dflags, sizeof(f), cudaMemcpyDeviceToHost, h->st);
+    } else {
+      ce = cudaMemcpyAsync(f, h->dflags, sizeof(f), cudaMemcpyDeviceToHost, h->st);
+      if (ce == cudaSuccess) ce = cudaMemcpyAsync(&h->logdet, h->d_logdet, sizeof(double), cudaMemcpyDeviceToHost, h->st);
+      if (ce == cudaSuccess) ce = cudaMemcpyAsync(&quad, h->Pipool + h->dt.piOff[0], sizeof(double), cudaMemcpyDeviceToHost, h->st);
+    }
     if (ce != cudaSuccess) st = hodlr_cuda_check(ce, "factor_solve results");
   }
   st = finish(h, st, &h->t_factor);
+  if (st == HODLR_OK && pd) { h->logdet = pd[0]; quad = pd[1]; memcpy(f, pd + 2, sizeof(f)); }
   h->y_aug = nullptr;
   if (st != HODLR_OK) { h->state = -1; h->logdet = -INFINITY; return st; }
   if (f[1]) {

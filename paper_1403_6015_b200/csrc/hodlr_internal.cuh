@@ -17,6 +17,7 @@
 #include <algorithm>
 
 #define HODLR_MAXDEPTH 48
+#define HODLR_PIN_BYTES (1 << 20)  // pinned host staging per pooled stream set (flags, ranks, scalars)
 #define TREE_TOP_MAXLEV HODLR_MAXDEPTH   // levels of one persistent upper-tree launch
 #define ACA_MAXCAP 64      // hard ceiling on the ACA rank cap (records/state are sized by it)
 #define ACA_RECW (4 + ACA_MAXCAP)
@@ -194,6 +195,7 @@ struct hodlr_s {
   int coop_ctas;             // cap on the CTAs of the persistent (cooperative) launches, 0 = the whole GPU: concurrent
                              // problems (the config-4 sweep) leave each other room instead of serialising
   const double *y_aug;       // that right-hand side (device, original order) during hodlr_factor_solve
+  void *pin;                 // pinned host staging (HODLR_PIN_BYTES, from the per-device pool), or NULL
   int launches;              // kernels launched by the current call
   int aca_steps;
   int x_nonfinite;           // set by the sort: x contains NaN/Inf

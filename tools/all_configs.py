@@ -43,14 +43,15 @@ cfg = inputs.CONFIGS["cfg4"]
 ell, s2 = inputs.sweep_settings(cfg)
 x = torch.from_numpy(inputs.points(cfg)).cuda(); y = torch.from_numpy(inputs.rhs(cfg)).cuda()
 th = np.stack([np.full(cfg.sweep, cfg.a), ell], 1)
-sw = {}
-for workers in (1, 4, 8, 16, 32):
-    hb.gp_loglik_sweep(x, y, cfg.kernel, th, s2, cfg.leaf, cfg.eps, workers=workers)
+hb.gp_loglik_sweep(x, y, cfg.kernel, th, s2, cfg.leaf, cfg.eps)          # warm-up (allocations, plans)
+ts = []
+for _ in range(5):
     torch.cuda.synchronize(); t0 = time.perf_counter()
-    v = hb.gp_loglik_sweep(x, y, cfg.kernel, th, s2, cfg.leaf, cfg.eps, workers=workers)
-    torch.cuda.synchronize(); sw[workers] = 1e3 * (time.perf_counter() - t0)
-t = min(sw.values()) / 1e3
-res["configs"]["cfg4"] = {"n": cfg.n, "settings": cfg.sweep, "ms_per_sweep_wall": 1e3 * t, "by_workers_ms": sw,
+    v = hb.gp_loglik_sweep(x, y, cfg.kernel, th, s2, cfg.leaf, cfg.eps)
+    torch.cuda.synchronize(); ts.append(1e3 * (time.perf_counter() - t0))
+t = float(np.median(ts)) / 1e3
+res["configs"]["cfg4"] = {"n": cfg.n, "settings": cfg.sweep, "ms_per_sweep_wall": 1e3 * t, "samples_ms": ts,
+                          "path": "batched handles (hodlr_build_batch, 64 settings in one handle)",
                           "settings_per_s": cfg.sweep / t, "loglik_min": float(v.min()), "loglik_max": float(v.max())}
 print("cfg4", json.dumps(res["configs"]["cfg4"]), flush=True)
 cfg = inputs.CONFIGS["cfg3"]
