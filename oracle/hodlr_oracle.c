@@ -51,6 +51,22 @@ double oracle_kernel(int kernel, const double *theta, double d) {
   return a * a * (1.0 + s + s * s / 3.0) * exp(-s);
 }
 
+/* O3 for d >= 2 (NEXT-3): the same Table I functions of the Euclidean distance r = |x_i - x_j|, given its square
+ * r2 = sum_k (x_ik - x_jk)^2 (summed over k in order): SE uses r2 directly, the others r = sqrt(r2) in place of |d|.
+ * (1-D points use oracle_kernel(d) -- bit for bit the same definition as before.) */
+double oracle_kernel_r2(int kernel, const double *theta, double r2) {
+  double a = theta[0], ell = theta[1];
+  if (kernel == ORACLE_SE) return a * a * exp(-(r2 / (2.0 * ell * ell)));
+  return oracle_kernel(kernel, theta, sqrt(r2));
+}
+
+/* squared distance of points p, q (dim coordinates each), summed in coordinate order */
+static double dist2(const double *p, const double *q, int dim) {
+  double r2 = 0.0;
+  for (int k = 0; k < dim; k++) { double d = p[k] - q[k]; r2 += d * d; }
+  return r2;
+}
+
 /* ------------------------------------------------------------------ */
 /* O4: adaptive cross approximation (partial-pivoted LU). */
 /* Entry source is a callback so the same routine serves kernel blocks and  */
@@ -74,18 +90,24 @@ static double dot(const double *a, const double *b, int64_t m) {
 /* Returns ORACLE_OK or ORACLE_ERANKCAP/ENOMEM; B->r is the rank. */
 /* rowkey (may be NULL): coordinates of the rows (sorted).  Rows with a key equal to a used pivot row
  * have identical residual rows and are treated as used as well (R2). */
-static void mark_row_run(char *used_r, const double *rowkey, int64_t m1, int64_t ik) {
+/* (d-dimensional points: rowkey holds m1 points of `dim` coordinates; "equal" = every coordinate equal -- the
+ * kd ordering keeps identical points adjacent, as the 1-D sort does) */
+static int same_point(const double *key, int dim, int64_t a, int64_t b) {
+  for (int k = 0; k < dim; k++) if (key[a * dim + k] != key[b * dim + k]) return 0;
+  return 1;
+}
+static void mark_row_run(char *used_r, const double *rowkey, int dim, int64_t m1, int64_t ik) {
   used_r[ik] = 1;
   if (!rowkey) return;
-  for (int64_t i = ik - 1; i >= 0 && rowkey[i] == rowkey[ik]; i--) used_r[i] = 1;
-  for (int64_t i = ik + 1; i < m1 && rowkey[i] == rowkey[ik]; i++) used_r[i] = 1;
+  for (int64_t i = ik - 1; i >= 0 && same_point(rowkey, dim, i, ik); i--) used_r[i] = 1;
+  for (int64_t i = ik + 1; i < m1 && same_point(rowkey, dim, i, ik); i++) used_r[i] = 1;
 }
 
 #ifdef ORACLE_TRACE_ACA
 static int g_trace_aca = 0;     /* diagnostic build only: per-step stop statistics of block ORACLE_TRACE_ACA */
 #endif
 static int aca(entry_fn f, const void *ctx, int64_t m1, int64_t m2, double eps, int cap, lowrank *B,
-               const double *rowkey) {
+               const double *rowkey, int dim) {
   memset(B, 0, sizeof *B);
   B->m1 = m1; B->m2 = m2;
   int64_t mn = m1 < m2 ? m1 : m2;
@@ -103,7 +125,7 @@ static int aca(entry_fn f, const void *ctx, int64_t m1, int64_t m2, double eps, 
       for (int l = 0; l < k; l++) v -= B->U[l][ik] * B->V[l][j];
       vt[j] = v;
     }
-    mark_row_run(used_r, rowkey, m1, ik);
+    mark_row_run(used_r, rowkey, dim, m1, ik);
     /* step 2: jk = smallest unused column maximising |v~_j| */
     int64_t jk = -1; double best = -1.0;
     for (int64_t j = 0; j < m2; j++)
@@ -166,7 +188,7 @@ int oracle_aca_dense(const double *A, int64_t m1, int64_t m2, int64_t lda, doubl
     return fail(ORACLE_EINVAL, "aca_dense: bad arguments");
   dense_ctx ctx = { A, lda };
   lowrank B;
-  int st = aca(dense_entry, &ctx, m1, m2, eps, cap, &B, NULL);
+  int st = aca(dense_entry, &ctx, m1, m2, eps, cap, &B, NULL, 1);
   *rank = B.r;
   for (int l = 0; l < B.r; l++) {
     memcpy(U + (int64_t)l * m1, B.U[l], sizeof(double) * (size_t)m1);
@@ -181,6 +203,7 @@ int oracle_aca_dense(const double *A, int64_t m1, int64_t m2, int64_t lda, doubl
 /* ------------------------------------------------------------------ */
 struct oracle_hodlr {
   int64_t n; int kern; double theta[3]; double s2; int leaf; double eps; int cap;
+  int dim;                          /* coordinates per point (xs: n x dim, point-major, sorted order) */
   double *dsort;                    /* heteroscedastic: s2 + noise_i in sorted order (NULL: s2 everywhere) */
   int kappa; int64_t nnodes, ninternal, nleaves;
   double *xs; int64_t *perm;
@@ -197,28 +220,34 @@ struct oracle_hodlr {
 };
 
 typedef struct { const struct oracle_hodlr *h; int64_t r0, c0; } blk_ctx;
+/* O3: k(xs_i, xs_j) of sorted points i, j: 1-D as a function of d = x_i - x_j, d-D of r2 = |x_i - x_j|^2 */
+static double kval_sorted(const oracle_hodlr *h, int64_t i, int64_t j) {
+  if (h->dim == 1) return oracle_kernel(h->kern, h->theta, h->xs[i] - h->xs[j]);
+  return oracle_kernel_r2(h->kern, h->theta, dist2(h->xs + i * h->dim, h->xs + j * h->dim, h->dim));
+}
+
 static double kernel_entry(const void *c, int64_t i, int64_t j) {
   const blk_ctx *b = c;
-  double d = b->h->xs[b->r0 + i] - b->h->xs[b->c0 + j];
-  return oracle_kernel(b->h->kern, b->h->theta, d);     /* off-diagonal: no noise term */
+  return kval_sorted(b->h, b->r0 + i, b->c0 + j);       /* off-diagonal: no noise term */
 }
 
 /* O3: C_ij = k(xs_i, xs_j) + sigma_i^2 [i = j], sorted indices; sigma_i^2 = s2 (+ noise_i). */
 static double entry_C(const oracle_hodlr *h, int64_t i, int64_t j) {
-  double v = oracle_kernel(h->kern, h->theta, h->xs[i] - h->xs[j]);
+  double v = kval_sorted(h, i, j);
   if (i == j) v += h->dsort ? h->dsort[i] : h->s2;
   return v;
 }
 
-/* O1: stable ascending argsort (ties -> lower original index), merge sort. */
-static void merge_sort_idx(int64_t *idx, int64_t *tmp, int64_t n, const double *key) {
+/* O1: stable ascending argsort (equal keys keep their current relative order), merge sort; the key of index v is
+ * key[v * stride] (stride = dim, key = one coordinate of point-major data). */
+static void merge_sort_idx(int64_t *idx, int64_t *tmp, int64_t n, const double *key, int stride) {
   if (n < 2) return;
   int64_t h = n / 2;
-  merge_sort_idx(idx, tmp, h, key);
-  merge_sort_idx(idx + h, tmp, n - h, key);
+  merge_sort_idx(idx, tmp, h, key, stride);
+  merge_sort_idx(idx + h, tmp, n - h, key, stride);
   int64_t i = 0, j = h, k = 0;
   while (i < h && j < n) {
-    if (key[idx[j]] < key[idx[i]]) tmp[k++] = idx[j++];   /* strict: equal keys keep left first */
+    if (key[idx[j] * stride] < key[idx[i] * stride]) tmp[k++] = idx[j++];   /* strict: equal keys keep left first */
     else tmp[k++] = idx[i++];
   }
   while (i < h) tmp[k++] = idx[i++];
@@ -247,38 +276,28 @@ int oracle_build(const double *x, int64_t n, int kernel, const double *theta, do
 
 int oracle_build_noise(const double *x, int64_t n, int kernel, const double *theta, double sigma2, const double *noise,
                        int leaf, double eps, int rank_cap, oracle_hodlr **out) {
+  return oracle_build_nd(x, n, 1, kernel, theta, sigma2, noise, leaf, eps, rank_cap, out);
+}
+
+int oracle_build_nd(const double *x, int64_t n, int dim, int kernel, const double *theta, double sigma2,
+                    const double *noise, int leaf, double eps, int rank_cap, oracle_hodlr **out) {
   *out = NULL;
-  if (n < 1 || leaf < 1 || !(eps > 0.0 && eps < 1.0) || !(sigma2 >= 0.0) || !theta ||
+  if (n < 1 || dim < 1 || dim > 64 || leaf < 1 || !(eps > 0.0 && eps < 1.0) || !(sigma2 >= 0.0) || !theta ||
       !(theta[1] > 0.0) || !(theta[0] >= 0.0) || kernel < 0 || kernel > 5 || (kernel == ORACLE_RQ && !(theta[2] > 0.0)) ||
       !isfinite(sigma2) ||
       !isfinite(theta[0]) || !isfinite(theta[1]))
     return fail(ORACLE_EINVAL, "build: invalid argument");
-  for (int64_t i = 0; i < n; i++)
+  for (int64_t i = 0; i < n * dim; i++)
     if (!isfinite(x[i])) return fail(ORACLE_EINVAL, "build: non-finite x[%lld]", (long long)i);
   if (noise)
     for (int64_t i = 0; i < n; i++)
       if (!isfinite(noise[i]) || noise[i] < 0.0) return fail(ORACLE_EINVAL, "build: bad noise[%lld]", (long long)i);
   oracle_hodlr *h = calloc(1, sizeof *h);
   if (!h) return fail(ORACLE_ENOMEM, "build: oom");
-  h->n = n; h->kern = kernel; h->theta[0] = theta[0]; h->theta[1] = theta[1];
+  h->n = n; h->dim = dim; h->kern = kernel; h->theta[0] = theta[0]; h->theta[1] = theta[1];
   h->theta[2] = kernel == ORACLE_RQ ? theta[2] : 0.0;
   h->s2 = sigma2; h->leaf = leaf; h->eps = eps; h->cap = rank_cap;
-  /* O1 */
-  double *key = malloc(sizeof(double) * (size_t)n);
-  int64_t *tmp = malloc(sizeof(int64_t) * (size_t)n);
-  h->perm = malloc(sizeof(int64_t) * (size_t)n);
-  h->xs = malloc(sizeof(double) * (size_t)n);
-  if (!key || !tmp || !h->perm || !h->xs) { free(key); free(tmp); oracle_free(h); return fail(ORACLE_ENOMEM, "build: oom"); }
-  for (int64_t i = 0; i < n; i++) { key[i] = x[i] == 0.0 ? 0.0 : x[i]; h->perm[i] = i; } /* -0.0 -> +0.0 */
-  merge_sort_idx(h->perm, tmp, n, key);
-  for (int64_t i = 0; i < n; i++) h->xs[i] = key[h->perm[i]];
-  free(key); free(tmp);
-  if (noise) {                                       /* sigma_i^2 = s2 + noise_i, carried with its point */
-    h->dsort = malloc(sizeof(double) * (size_t)n);
-    if (!h->dsort) { oracle_free(h); return fail(ORACLE_ENOMEM, "build: oom"); }
-    for (int64_t i = 0; i < n; i++) h->dsort[i] = sigma2 + noise[h->perm[i]];
-  }
-  /* O2: kappa = largest integer with leaf * 2^kappa <= n (0 if n <= leaf) */
+  /* O2: kappa = largest integer with leaf * 2^kappa <= n (0 if n <= leaf); count-median split, left = ceil(m/2) */
   int kappa = 0;
   while ((int64_t)leaf << (kappa + 1) <= n && kappa < 62) kappa++;
   h->kappa = kappa;
@@ -294,6 +313,31 @@ int oracle_build_noise(const double *x, int64_t n, int kernel, const double *the
     h->lo[2 * c + 1] = h->lo[c]; h->hi[2 * c + 1] = h->lo[c] + half;
     h->lo[2 * c + 2] = h->lo[c] + half; h->hi[2 * c + 2] = h->hi[c];
   }
+  /* O1: 1-D: one stable ascending sort.  d >= 2: the kd-tree ordering -- each node of depth
+   * L < max(kappa, 1), top down, stably sorts its points by coordinate L mod d; the count-median split above then
+   * halves it (R19).  For d = 1 this is the same order as the single sort. */
+  double *key = malloc(sizeof(double) * (size_t)(n * dim));
+  int64_t *tmp = malloc(sizeof(int64_t) * (size_t)n);
+  h->perm = malloc(sizeof(int64_t) * (size_t)n);
+  h->xs = malloc(sizeof(double) * (size_t)(n * dim));
+  if (!key || !tmp || !h->perm || !h->xs) { free(key); free(tmp); oracle_free(h); return fail(ORACLE_ENOMEM, "build: oom"); }
+  for (int64_t i = 0; i < n * dim; i++) key[i] = x[i] == 0.0 ? 0.0 : x[i];     /* -0.0 -> +0.0 */
+  for (int64_t i = 0; i < n; i++) h->perm[i] = i;
+  if (dim == 1) merge_sort_idx(h->perm, tmp, n, key, 1);
+  else {
+    int levels = kappa > 0 ? kappa : 1;
+    for (int L = 0; L < levels; L++)
+      for (int64_t c = ((int64_t)1 << L) - 1; c < ((int64_t)2 << L) - 1; c++)
+        merge_sort_idx(h->perm + h->lo[c], tmp, h->hi[c] - h->lo[c], key + (L % dim), dim);
+  }
+  for (int64_t i = 0; i < n; i++)
+    for (int k = 0; k < dim; k++) h->xs[i * dim + k] = key[h->perm[i] * dim + k];
+  free(key); free(tmp);
+  if (noise) {                                       /* sigma_i^2 = s2 + noise_i, carried with its point */
+    h->dsort = malloc(sizeof(double) * (size_t)n);
+    if (!h->dsort) { oracle_free(h); return fail(ORACLE_ENOMEM, "build: oom"); }
+    for (int64_t i = 0; i < n; i++) h->dsort[i] = sigma2 + noise[h->perm[i]];
+  }
   /* O4: compress K[c1, c2] of every internal node c */
   h->blk = calloc((size_t)(h->ninternal ? h->ninternal : 1), sizeof(lowrank));
   if (!h->blk) { oracle_free(h); return fail(ORACLE_ENOMEM, "build: oom"); }
@@ -304,7 +348,7 @@ int oracle_build_noise(const double *x, int64_t n, int kernel, const double *the
     g_trace_aca = c == ORACLE_TRACE_ACA;
 #endif
     int st = aca(kernel_entry, &ctx, h->hi[c1] - h->lo[c1], h->hi[c2] - h->lo[c2], eps, rank_cap, &h->blk[c],
-                 h->xs + h->lo[c1]);
+                 h->xs + h->lo[c1] * dim, dim);
     if (st != ORACLE_OK) {
       int code = st;
       char msg[400]; snprintf(msg, sizeof msg, "%.360s", g_err);
@@ -710,7 +754,8 @@ int oracle_residual_rows(oracle_hodlr *h, const double *x, const double *y, cons
 int oracle_kappa(oracle_hodlr *h) { return h ? h->kappa : -1; }
 int64_t oracle_num_nodes(oracle_hodlr *h) { return h ? h->nnodes : -1; }
 int oracle_get_perm(oracle_hodlr *h, int64_t *perm) { memcpy(perm, h->perm, sizeof(int64_t) * (size_t)h->n); return 0; }
-int oracle_get_sorted(oracle_hodlr *h, double *xs) { memcpy(xs, h->xs, sizeof(double) * (size_t)h->n); return 0; }
+int oracle_get_sorted(oracle_hodlr *h, double *xs) { memcpy(xs, h->xs, sizeof(double) * (size_t)(h->n * h->dim)); return 0; }
+int oracle_dim(oracle_hodlr *h) { return h ? h->dim : -1; }
 int oracle_get_tree(oracle_hodlr *h, int64_t *lo, int64_t *hi) {
   memcpy(lo, h->lo, sizeof(int64_t) * (size_t)h->nnodes); memcpy(hi, h->hi, sizeof(int64_t) * (size_t)h->nnodes); return 0;
 }
@@ -744,13 +789,26 @@ int oracle_dense(const double *x, int64_t n, int kernel, const double *theta, do
 
 int oracle_dense_noise(const double *x, int64_t n, int kernel, const double *theta, double sigma2, const double *noise,
                        const double *y, double *logdet, double *xout) {
-  if (n < 1 || n > 8192) return fail(ORACLE_EINVAL, "dense: n out of range");
+  return oracle_dense_nd(x, n, 1, kernel, theta, sigma2, noise, y, logdet, xout);
+}
+
+int oracle_dense_nd(const double *x, int64_t n, int dim, int kernel, const double *theta, double sigma2,
+                    const double *noise, const double *y, double *logdet, double *xout) {
+  if (n < 1 || n > 8192 || dim < 1) return fail(ORACLE_EINVAL, "dense: n out of range");
   double *C = malloc(sizeof(double) * (size_t)(n * n));
   if (!C) return fail(ORACLE_ENOMEM, "dense: oom");
   for (int64_t i = 0; i < n; i++)
     for (int64_t j = 0; j < n; j++) {
-      double xi = x[i] == 0.0 ? 0.0 : x[i], xj = x[j] == 0.0 ? 0.0 : x[j];
-      C[i * n + j] = oracle_kernel(kernel, theta, xi - xj) + (i == j ? (noise ? sigma2 + noise[i] : sigma2) : 0.0);
+      double v;
+      if (dim == 1) {
+        double xi = x[i] == 0.0 ? 0.0 : x[i], xj = x[j] == 0.0 ? 0.0 : x[j];
+        v = oracle_kernel(kernel, theta, xi - xj);
+      } else {
+        double r2 = 0.0;                               /* (x_i - x_j) . (x_i - x_j), coordinates in order */
+        for (int k = 0; k < dim; k++) { double d = x[i * dim + k] - x[j * dim + k]; r2 += d * d; }
+        v = oracle_kernel_r2(kernel, theta, r2);
+      }
+      C[i * n + j] = v + (i == j ? (noise ? sigma2 + noise[i] : sigma2) : 0.0);
     }
   /* right-looking (outer-product) Cholesky on the upper triangle, C = U^T U (U = L^T, row k of U = column k of
    * L): after row k is scaled, its rank-1 update is applied to the whole trailing upper triangle at once -- a

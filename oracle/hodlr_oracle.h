@@ -11,7 +11,7 @@
  *
  * The oracle follows the paper's algorithm step by step, in the paper's
  * order:
- *   O1 sort              PAPER.md:666-677 (sec. 3, kd-tree ordering; 1-D = stable sort)
+ *   O1 sort              PAPER.md:666-677 (sec. 3, kd-tree ordering; 1-D = stable sort; d-D: per-level sorts)
  *   O2 tree              PAPER.md:1063 (Fig. 6 line 1, kappa = floor(log2 n/p_max))
  *   O3 entries           PAPER.md:281-308 (Table I), PAPER.md:1251-1256 (C_ij = s2 d_ij + k)
  *   O4 ACA               PAPER.md:837-864 (sec. 3.1, partial-pivoted LU / ACA)
@@ -42,6 +42,9 @@ typedef struct oracle_hodlr oracle_hodlr;
 
 /* O3: one kernel value k(r) for distance d = x_i - x_j (no noise term). theta = {a, ell} ({a, ell, alpha} for RQ). */
 double oracle_kernel(int kernel, const double *theta, double d);
+/* O3 for d-dimensional points (NEXT-3): the same function of r = |x_i - x_j| given r2 = r^2 (SE from r2, the others
+ * from sqrt(r2)). */
+double oracle_kernel_r2(int kernel, const double *theta, double r2);
 
 /* O4 on an explicit dense m1 x m2 column-major block A (lda >= m1).
  * U (m1 x cap) and V (m2 x cap) column-major, caller-allocated.
@@ -57,6 +60,11 @@ int oracle_build(const double *x, int64_t n, int kernel, const double *theta, do
  * n finite values >= 0 in the caller's order (NULL = homoscedastic). */
 int oracle_build_noise(const double *x, int64_t n, int kernel, const double *theta, double sigma2, const double *noise,
                        int leaf, double eps, int rank_cap, oracle_hodlr **out);
+/* d-dimensional points (NEXT-3): x is n x dim, point-major (point i at x[i dim .. i dim + dim)); O1 is the kd-tree
+ * ordering of PAPER.md:666-677 (each node of depth L sorts its points stably by coordinate L mod dim, then the
+ * count-median split halves it).  dim = 1 is oracle_build_noise. */
+int oracle_build_nd(const double *x, int64_t n, int dim, int kernel, const double *theta, double sigma2,
+                    const double *noise, int leaf, double eps, int rank_cap, oracle_hodlr **out);
 /* O5-O8: leaves, panel, sweep, log det ("Factor"). */
 int oracle_factor(oracle_hodlr *h);
 /* O8: log det C (after factor).  -INFINITY if the factorization failed. */
@@ -77,7 +85,8 @@ int oracle_residual_rows(oracle_hodlr *h, const double *x, const double *y, cons
 int     oracle_kappa(oracle_hodlr *h);
 int64_t oracle_num_nodes(oracle_hodlr *h);
 int     oracle_get_perm(oracle_hodlr *h, int64_t *perm);          /* n */
-int     oracle_get_sorted(oracle_hodlr *h, double *xs);           /* n */
+int     oracle_get_sorted(oracle_hodlr *h, double *xs);           /* n x dim, point-major */
+int     oracle_dim(oracle_hodlr *h);
 int     oracle_get_tree(oracle_hodlr *h, int64_t *lo, int64_t *hi); /* num_nodes each, heap order */
 int     oracle_get_ranks(oracle_hodlr *h, int32_t *ranks);        /* 2^kappa - 1 internal nodes */
 /* Copy U (m1 x r) and V (m2 x r) of internal node `node` (heap id), column-major. */
@@ -93,6 +102,8 @@ int oracle_dense(const double *x, int64_t n, int kernel, const double *theta, do
                  const double *y, double *logdet, double *xout);
 int oracle_dense_noise(const double *x, int64_t n, int kernel, const double *theta, double sigma2, const double *noise,
                        const double *y, double *logdet, double *xout);
+int oracle_dense_nd(const double *x, int64_t n, int dim, int kernel, const double *theta, double sigma2,
+                    const double *noise, const double *y, double *logdet, double *xout);
 
 #ifdef __cplusplus
 }

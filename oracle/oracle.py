@@ -53,6 +53,10 @@ def _load(twin: bool = False):
         lib = C.CDLL(build_oracle(twin=twin))
         P, I64, I32, D = C.c_void_p, C.c_int64, C.c_int, C.c_double
         lib.oracle_kernel.argtypes = [I32, P, D]; lib.oracle_kernel.restype = D
+        lib.oracle_kernel_r2.argtypes = [I32, P, D]; lib.oracle_kernel_r2.restype = D
+        lib.oracle_build_nd.argtypes = [P, I64, I32, I32, P, D, P, I32, D, I32, P]; lib.oracle_build_nd.restype = I32
+        lib.oracle_dense_nd.argtypes = [P, I64, I32, I32, P, D, P, P, P, P]; lib.oracle_dense_nd.restype = I32
+        lib.oracle_dim.argtypes = [P]; lib.oracle_dim.restype = I32
         lib.oracle_aca_dense.argtypes = [P, I64, I64, I64, D, I32, P, P, P]; lib.oracle_aca_dense.restype = I32
         lib.oracle_build.argtypes = [P, I64, I32, P, D, I32, D, I32, P]; lib.oracle_build.restype = I32
         lib.oracle_build_noise.argtypes = [P, I64, I32, P, D, P, I32, D, I32, P]; lib.oracle_build_noise.restype = I32
@@ -105,10 +109,26 @@ def aca_dense(A: np.ndarray, eps: float, cap: int | None = None):
     return U[:k].T.copy(), V[:k].T.copy(), k
 
 
-def dense_check(x, kernel: int, theta, sigma2: float, y=None, noise=None):
-    """O11: dense Cholesky log det (+ solve).  Returns (logdet, x or None).  noise: heteroscedastic sigma_i^2 - sigma2."""
+def kernel_value_r2(kernel: int, theta, r2: float) -> float:
+    """O3 for d-dimensional points: k as a function of the squared distance r2 (NEXT-3)."""
     lib = _load()
+    th = np.ascontiguousarray(theta, dtype=np.float64)
+    return lib.oracle_kernel_r2(int(kernel), _ptr(th), float(r2))
+
+
+def _points(x):
+    """(n,) or (n, d) -> contiguous float64 (n, d) array and d."""
     x = np.ascontiguousarray(x, dtype=np.float64)
+    if x.ndim == 1:
+        return x, 1
+    return x, int(x.shape[1])
+
+
+def dense_check(x, kernel: int, theta, sigma2: float, y=None, noise=None):
+    """O11: dense Cholesky log det (+ solve).  Returns (logdet, x or None).  noise: heteroscedastic sigma_i^2 - sigma2.
+    x: (n,) or (n, d) points."""
+    lib = _load()
+    x, dim = _points(x)
     nz = None if noise is None else np.ascontiguousarray(noise, dtype=np.float64)
     th = np.ascontiguousarray(theta, dtype=np.float64)
     ld = C.c_double(0.0)
@@ -116,9 +136,9 @@ def dense_check(x, kernel: int, theta, sigma2: float, y=None, noise=None):
     if y is not None:
         y = np.ascontiguousarray(y, dtype=np.float64)
         out = np.zeros_like(y)
-    _check(lib, lib.oracle_dense_noise(_ptr(x), x.size, int(kernel), _ptr(th), float(sigma2),
-                                       _ptr(nz) if nz is not None else None, _ptr(y) if y is not None else None,
-                                       C.byref(ld), _ptr(out) if out is not None else None))
+    _check(lib, lib.oracle_dense_nd(_ptr(x), x.shape[0], dim, int(kernel), _ptr(th), float(sigma2),
+                                    _ptr(nz) if nz is not None else None, _ptr(y) if y is not None else None,
+                                    C.byref(ld), _ptr(out) if out is not None else None))
     return ld.value, out
 
 
@@ -127,18 +147,19 @@ class OracleHODLR:
 
     def __init__(self, x, kernel: int, theta, sigma2: float, leaf: int, eps: float, rank_cap: int = 0,
                  twin: bool = False, noise=None):
-        """noise: optional heteroscedastic part, C_ii = sigma2 + noise_i."""
+        """x: (n,) points, or (n, d) for d-dimensional inputs (kd ordering, NEXT-3).  noise: optional heteroscedastic
+        part, C_ii = sigma2 + noise_i (PAPER.md:1251-1256)."""
         self._lib = _load(twin)
         self.twin = twin
-        self.x = np.ascontiguousarray(x, dtype=np.float64)
-        self.n = self.x.size
+        self.x, self.dim = _points(x)
+        self.n = self.x.shape[0]
         self.kernel, self.theta = int(kernel), tuple(float(v) for v in theta)
         th = np.ascontiguousarray(theta, dtype=np.float64)
         h = C.c_void_p(0)
         self._noise = None if noise is None else np.ascontiguousarray(noise, dtype=np.float64)
-        _check(self._lib, self._lib.oracle_build_noise(_ptr(self.x), self.n, int(kernel), _ptr(th), float(sigma2),
-                                                       _ptr(self._noise) if self._noise is not None else None,
-                                                       int(leaf), float(eps), int(rank_cap), C.byref(h)))
+        _check(self._lib, self._lib.oracle_build_nd(_ptr(self.x), self.n, self.dim, int(kernel), _ptr(th),
+                                                    float(sigma2), _ptr(self._noise) if self._noise is not None else None,
+                                                    int(leaf), float(eps), int(rank_cap), C.byref(h)))
         self._h = h
 
     def __del__(self):
@@ -183,12 +204,18 @@ class OracleHODLR:
         small cases only.  Requires factor()."""
         xt = np.asarray(xt, dtype=np.float64)
         alpha = self.solve(y)
-        Ks = np.array([[kernel_value(self.kernel, self.theta, float(t - xi)) for xi in self.x] for t in xt])
+        if self.dim == 1:
+            Ks = np.array([[kernel_value(self.kernel, self.theta, float(t - xi)) for xi in self.x] for t in xt])
+        else:
+            xt = xt.reshape(-1, self.dim)
+            Ks = np.array([[kernel_value_r2(self.kernel, self.theta, float(sum((t[k] - xi[k]) * (t[k] - xi[k])
+                                                                                for k in range(self.dim))))
+                            for xi in self.x] for t in xt])
         mean = Ks @ alpha
         if not variance:
             return mean, None
         var = np.array([kernel_value(self.kernel, self.theta, 0.0) - Ks[j] @ self.solve(Ks[j])
-                        for j in range(xt.size)])
+                        for j in range(Ks.shape[0])])
         return mean, var
 
     def residual_rows(self, xsol, y, rows):
@@ -209,9 +236,9 @@ class OracleHODLR:
         return p
 
     def sorted_x(self):
-        p = np.zeros(self.n)
+        p = np.zeros(self.n * self.dim)
         self._lib.oracle_get_sorted(self._h, _ptr(p))
-        return p
+        return p if self.dim == 1 else p.reshape(self.n, self.dim)
 
     def tree(self):
         nn = self._lib.oracle_num_nodes(self._h)

@@ -468,8 +468,12 @@ __global__ void __launch_bounds__(ACA_SUB) k_aca_finish(const AcaCtx *__restrict
 // ---------------------------------------------------------------------------------------------
 // NT threads; MAXS >= both sides of every block of the launch (small blocks run in small CTAs: the 64- and
 // 128-point blocks of the deepest levels need neither 256 threads nor 40 KB of shared memory)
+#ifndef ACA_FUSED_FU
+#define ACA_FUSED_FU 4
+#endif
 template <bool SEO, int NT, int MAXS>
 __global__ void __launch_bounds__(NT) k_aca_fused(AcaCtx c, const int *blocks, int *flags) {
+  constexpr int FU = ACA_FUSED_FU;
   __shared__ double vbuf[MAXS];
   __shared__ unsigned char usedR[MAXS], usedC[MAXS];
   __shared__ double Ui[ACA_MAXCAP], dV[ACA_MAXCAP], dots[ACA_MAXCAP];
@@ -504,15 +508,34 @@ __global__ void __launch_bounds__(NT) k_aca_fused(AcaCtx c, const int *blocks, i
     for (int l = t; l < k; l += NT) Ui[l] = slot[(long long)l * ldx + ig];
     __syncthreads();
     double ba = 0.0, bv = 0.0, n2 = 0.0; long long bi = -1;
-    // v~_j = A[ik, j] - sum_l U[ik, l] V[j, l], l ascending, each product rounded (the oracle's operation order)
-    for (long long j = t; j < m2; j += NT) {
-      const long long gj = lo2 + j;
-      double v = kval_ot<SEO>(kp, xi - c.xs[gj]);
-#pragma unroll 8
-      for (int l = 0; l < k; l++) v = __dsub_rn(v, __dmul_rn(Ui[l], __ldcg(slot + (long long)l * ldx + gj)));
-      vbuf[j] = v;
-      if (!usedC[j] && fabs(v) > ba) { ba = fabs(v); bi = j; bv = v; }
-      n2 += v * v;
+    // v~_j = A[ik, j] - sum_l U[ik, l] V[j, l], l ascending, each product rounded (the oracle's operation order);
+    // FU elements per thread at a time (independent chains: the kernel entries' exp and the column loads overlap),
+    // visited in increasing index order (the argmax tie rule)
+    for (long long j0 = t; j0 < m2; j0 += FU * NT) {
+      double v[FU];
+#pragma unroll
+      for (int u = 0; u < FU; u++) {
+        const long long j = j0 + u * NT;
+        v[u] = j < m2 ? kval_ot<SEO>(kp, xi - c.xs[lo2 + j]) : 0.0;
+      }
+      for (int l = 0; l < k; l++) {
+        const double ul = Ui[l];
+        const double *col = slot + (long long)l * ldx + lo2;
+#pragma unroll
+        for (int u = 0; u < FU; u++) {
+          const long long j = j0 + u * NT;
+          if (j < m2) v[u] = __dsub_rn(v[u], __dmul_rn(ul, __ldcg(col + j)));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < FU; u++) {
+        const long long j = j0 + u * NT;
+        if (j < m2) {
+          vbuf[j] = v[u];
+          if (!usedC[j] && fabs(v[u]) > ba) { ba = fabs(v[u]); bi = j; bv = v[u]; }
+          n2 += v[u] * v[u];
+        }
+      }
     }
     block_argmax_n2<NT / 32>(ba, bi, bv, n2, s_abs, s_idx, s_val, s_n2);
     if (bi < 0 || ba == 0.0) break;                      // exactly-zero residual row: rank k (block-uniform)
@@ -540,15 +563,32 @@ __global__ void __launch_bounds__(NT) k_aca_fused(AcaCtx c, const int *blocks, i
     for (int l = t; l < k; l += NT) Ui[l] = slot[(long long)l * ldx + jg];
     __syncthreads();
     ba = 0.0; bv = 0.0; n2 = 0.0; bi = -1;
-    for (long long i = t; i < m1; i += NT) {
-      const long long gi = lo1 + i;
-      double u = kval_ot<SEO>(kp, c.xs[gi] - xj);
-#pragma unroll 8
-      for (int l = 0; l < k; l++) u = __dsub_rn(u, __dmul_rn(Ui[l], __ldcg(slot + (long long)l * ldx + gi)));
-      slot[(long long)k * ldx + gi] = u;
-      vbuf[i] = u;
-      if (!usedR[i] && fabs(u) > ba) { ba = fabs(u); bi = i; bv = u; }
-      n2 += u * u;
+    for (long long i0 = t; i0 < m1; i0 += FU * NT) {           // (FU elements per thread at a time, as above)
+      double w[FU];
+#pragma unroll
+      for (int u = 0; u < FU; u++) {
+        const long long i = i0 + u * NT;
+        w[u] = i < m1 ? kval_ot<SEO>(kp, c.xs[lo1 + i] - xj) : 0.0;
+      }
+      for (int l = 0; l < k; l++) {
+        const double ul = Ui[l];
+        const double *col = slot + (long long)l * ldx + lo1;
+#pragma unroll
+        for (int u = 0; u < FU; u++) {
+          const long long i = i0 + u * NT;
+          if (i < m1) w[u] = __dsub_rn(w[u], __dmul_rn(ul, __ldcg(col + i)));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < FU; u++) {
+        const long long i = i0 + u * NT;
+        if (i < m1) {
+          slot[(long long)k * ldx + lo1 + i] = w[u];
+          vbuf[i] = w[u];
+          if (!usedR[i] && fabs(w[u]) > ba) { ba = fabs(w[u]); bi = i; bv = w[u]; }
+          n2 += w[u] * w[u];
+        }
+      }
     }
     block_argmax_n2<NT / 32>(ba, bi, bv, n2, s_abs, s_idx, s_val, s_n2);
     for (int l = warp; l < k; l += (NT / 32)) {

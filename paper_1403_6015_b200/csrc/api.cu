@@ -79,9 +79,15 @@ static void *dalloc_impl(hodlr_s *h, size_t bytes, bool transient) {
         break;
       }
   }
+  if (!p) {
+    char msg[96];
+    snprintf(msg, sizeof msg, "dalloc: cache miss, cudaMallocAsync %.1f MB", bytes / 1048576.0);
+    hodlr_trace(msg);
+  }
   if (!p && cudaMallocAsync(&p, bytes, h->st) != cudaSuccess) {
     cudaGetLastError();
     p = nullptr;
+    hodlr_trace("dalloc: allocation failed: draining the cache and trimming the pool");
     {   // flush this device's idle cached blocks back to the driver and retry once
       std::lock_guard<std::mutex> lk(g_blk_mu);
       blk_cache_drain_locked(h->dev);

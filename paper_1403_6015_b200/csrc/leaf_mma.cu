@@ -162,13 +162,18 @@ __device__ unsigned long long g_chol_stamps[2][6];
 #else
 #define CSTAMP(k)
 #endif
-// CTA size: 8 warps for 128-point leaves (2 CTAs per SM); 4 warps for 64-point leaves (the X = L^{-1} sweep needs
-// NW >= T / 2), 4 CTAs per SM -- a 64-point leaf's chain of 8 diagonal steps is latency, so more leaves in flight.
-template <int P> struct CholCfg { static constexpr int NT = P == 64 ? 128 : 256, MINB = P == 64 ? 4 : 2; };
+// CTA size: 8 warps for 128-point leaves (2 CTAs per SM); 2 warps for 64-point leaves, 8 CTAs per SM -- a 64-point
+// leaf's chain of 8 diagonal steps is latency, so more leaves in flight (the batched config-4 factorization:
+// 131072 such leaves).
+#ifndef CHOL64_NT
+#define CHOL64_NT 64
+#endif
+template <int P> struct CholCfg {
+  static constexpr int NT = P == 64 ? CHOL64_NT : 256, MINB = P == 64 ? 512 / CHOL64_NT : 2;
+};
 template <int P, bool SEO>
 __global__ void __launch_bounds__(CholCfg<P>::NT, CholCfg<P>::MINB) k_leaf_chol(LeafMmaCtx c) {
   constexpr int NTH = CholCfg<P>::NT, NW = NTH / 32;
-  static_assert(2 * NW >= P / 8, "X sweep: every tile column needs a warp");
   constexpr int T = P / 8;
   constexpr int NTILE = T * (T + 1) / 2;
   extern __shared__ double sm[];
@@ -357,9 +362,17 @@ __global__ void __launch_bounds__(CholCfg<P>::NT, CholCfg<P>::MINB) k_leaf_chol(
   {
     const int g = lane >> 2, q2 = 2 * (lane & 3);
     const int cp = cpos(lane);
-    for (int pass = 0; pass < 2; pass++) {
-      const int J = pass ? T - 1 - warp : warp;
-      if (J >= T || (pass && J < NW)) break;
+    for (int pass = 0;; pass++) {
+      // 2 NW >= T: columns J = warp, then T-1-warp (balanced: column J costs T - J tiles); else J = warp + pass NW
+      int J;
+      if (2 * NW >= T) {
+        if (pass >= 2) break;
+        J = pass ? T - 1 - warp : warp;
+        if (J >= T || (pass && J < NW)) break;
+      } else {
+        J = warp + pass * NW;
+        if (J >= T) break;
+      }
       double z[T][2];
 #pragma unroll
       for (int i = 0; i < T; i++) {

@@ -67,10 +67,10 @@ extern "C" hodlr_status gp_loglik_sweep(const double *x, const double *y, int64_
         s2[j] = sigma2s[b];
       }
       hodlr_status st = HODLR_OK;
-      if (yb_n < nb * n) {
-        if (yb) cudaFree(yb);
+      if (yb_n < nb * n) {                          // (stream-ordered pool allocations: no device-wide sync)
+        if (yb) cudaFreeAsync(yb, s);
         yb = nullptr; yb_n = 0;
-        if (cudaMalloc(&yb, sizeof(double) * nb * n) != cudaSuccess) st = hodlr_set_error(HODLR_ENOMEM, "sweep: rhs");
+        if (cudaMallocAsync(&yb, sizeof(double) * nb * n, s) != cudaSuccess) { cudaGetLastError(); st = hodlr_set_error(HODLR_ENOMEM, "sweep: rhs"); }
         else yb_n = nb * n;
       }
       hodlr_t h = nullptr;
@@ -93,7 +93,7 @@ extern "C" hodlr_status gp_loglik_sweep(const double *x, const double *y, int64_
       }
       k0 += nb;
     }
-    if (yb) { cudaStreamSynchronize(s); cudaFree(yb); }
+    if (yb) { cudaFreeAsync(yb, s); cudaStreamSynchronize(s); }
   }
   std::atomic<int> next(0);
   const int W = std::max(1, std::min<int>(workers > 0 ? workers : 8, (int)redo.size()));
