@@ -5,7 +5,7 @@
 #pragma once
 #include "hodlr_internal.cuh"
 #ifndef TREE_GJ_REGS
-#define TREE_GJ_REGS 8           // largest q of the register Gauss-Jordan (8; 16 measured slower: spills)
+#define TREE_GJ_REGS 16          // largest q of the register Gauss-Jordan (gj_regs up to 8, gj_cols up to 16)
 #endif
 
 struct TreeCtx {
@@ -86,6 +86,64 @@ __device__ void gj_regs(const double *W, double *Wout, int q, double *ukk, int &
   if (lane < q) {
 #pragma unroll
     for (int j = 0; j < QB; j++) if (j < q) Wout[pos * q2 + q + j] = w[QB + j];
+  }
+}
+
+// The same elimination with one COLUMN of [S | I] per lane (2q <= 32 columns, q <= QB rows in registers), for
+// 8 < q <= 16: per step the pivot column's lane scans its own q entries for the pivot, and every lane updates its
+// column with the multipliers broadcast from that lane -- q shuffles per step instead of the row layout's 2q, and
+// no per-lane 2q-register rows.  Logical interchanges (every lane carries the same position table), the row layout's
+// exact arithmetic (multiplier W[a][k] * (1 / piv), one FMA per entry, pivot row scaled), hence bitwise its result.
+template <int QB>
+__device__ void gj_cols(const double *W, double *Wout, int q, double *ukk, int &sign, int &zero) {
+  const int lane = threadIdx.x & 31, q2 = 2 * q;
+  const bool act = lane < q2;
+  double cl[QB];
+  int pos[QB];
+#pragma unroll
+  for (int a = 0; a < QB; a++) { cl[a] = (act && a < q) ? W[a * q2 + lane] : 0.0; pos[a] = a; }
+  sign = 1; zero = 0;
+  for (int k = 0; k < q; k++) {
+    // pivot: physical row of max |W[., k]| among positions >= k, smallest position on ties (lane k's column)
+    double best = -1.0; int bp = 1 << 30, P = 0;
+#pragma unroll
+    for (int a = 0; a < QB; a++)
+      if (a < q && pos[a] >= k) {
+        const double v = fabs(cl[a]);
+        if (v > best || (v == best && pos[a] < bp)) { best = v; bp = pos[a]; P = a; }
+      }
+    P = __shfl_sync(0xffffffffu, P, k);
+    double pj = 0.0;                               // this lane's entry of the pivot row
+#pragma unroll
+    for (int a = 0; a < QB; a++) if (a == P) pj = cl[a];
+    const double piv = __shfl_sync(0xffffffffu, pj, k);
+    int posP = 0;
+#pragma unroll
+    for (int a = 0; a < QB; a++) if (a == P) posP = pos[a];
+    if (posP != k) {                               // swap positions k and posP
+      sign = -sign;
+#pragma unroll
+      for (int a = 0; a < QB; a++) { if (pos[a] == k) pos[a] = posP; else if (a == P) pos[a] = k; }
+    }
+    if (piv < 0.0) sign = -sign;
+    if (!(piv != 0.0)) zero = 1;
+    if (lane == 0) ukk[k] = fabs(piv);
+    const double ip = piv != 0.0 ? 1.0 / piv : 0.0;
+#pragma unroll
+    for (int a = 0; a < QB; a++) {
+      if (a < q) {
+        const double mlt = __shfl_sync(0xffffffffu, cl[a], k) * ip;     // (lane k's column: W[a][k])
+        cl[a] = a == P ? cl[a] * ip : fma(-mlt, pj, cl[a]);
+      }
+    }
+    if (lane == k) {
+#pragma unroll
+      for (int a = 0; a < QB; a++) cl[a] = a == P ? 1.0 : 0.0;
+    }
+  }
+  if (act && lane >= q) {
+#pragma unroll
+    for (int a = 0; a < QB; a++) if (a < q) Wout[pos[a] * q2 + lane] = cl[a];
   }
 }
 
@@ -222,7 +280,7 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
     if (t < 32) {
       int sign, zero;
       if (q <= 8) gj_regs<8>(W, W2, q, colk, sign, zero);
-      else if (q <= TREE_GJ_REGS) gj_regs<16>(W, W2, q, colk, sign, zero);
+      else if (q <= TREE_GJ_REGS) gj_cols<16>(W, W2, q, colk, sign, zero);
       else gj_warp(W, W2, W, q, colk, sign, zero);
       if (t == 0) { s_sign = sign; s_zero = zero; }
     }

@@ -504,3 +504,87 @@ def test_noise_hodlr_vs_dense(kernel):
     assert abs(ld2 - ld) <= 1e-12 * abs(ld) and np.linalg.norm(x2 - xd) <= 1e-9 * np.linalg.norm(xd)
     with pytest.raises(OracleError):
         OracleHODLR(x, kernel, th, 0.0, 48, 1e-12, noise=-nz)
+
+
+# ---------------------------------------------------------------------------------------------------------------
+# NEXT-3 groundwork (oracle only): d-dimensional points with the kd-tree ordering of PAPER.md:666-677 (R19)
+def _dense_C_nd(X, kernel, theta, s2):
+    """Independent numpy assembly for d-dimensional points: Euclidean distances (scipy), Table I of r."""
+    from scipy.spatial.distance import cdist
+    r = cdist(X, X)
+    a, ell = theta[0], theta[1]
+    if kernel == SE:
+        K = a * a * np.exp(-r * r / (2 * ell * ell))
+    else:
+        s = (3.0 ** 0.5 if kernel == MATERN32 else 5.0 ** 0.5) * r / ell
+        K = a * a * ((1 + s) if kernel == MATERN32 else (1 + s + s * s / 3)) * np.exp(-s)
+    return K + s2 * np.eye(len(X))
+
+
+def test_kd_order_spec_square():
+    """SPEC.md geometry example: the 2-D unit square with leaf size 1 -- the first split (on x) puts (0,0), (0,1)
+    before (1,0), (1,1); the second level sorts each half by y."""
+    X = np.array([[0.0, 0.0], [1.0, 0.0], [0.0, 1.0], [1.0, 1.0]])
+    o = OracleHODLR(X, SE, (1.0, 1.0), 1e-2, 1, 1e-12)
+    assert o.kappa == 2
+    np.testing.assert_array_equal(o.perm(), [0, 2, 1, 3])
+    np.testing.assert_array_equal(o.sorted_x(), X[[0, 2, 1, 3]])
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_kd_order_invariants(d):
+    """perm is a permutation; every internal node of depth L splits its points by coordinate L mod d (all of the
+    left child's coordinates <= all of the right child's); ties in the split coordinate keep their relative
+    order from the level above (checked by a plain re-implementation in Python: per-level stable sorts)."""
+    rng = np.random.default_rng(40 + d)
+    n = 1000
+    X = np.round(rng.uniform(0, 4, (n, d)), 1)          # many ties
+    o = OracleHODLR(X, SE, (1.0, 1.0), 1e-2, 16, 1e-12)
+    p = o.perm()
+    assert np.array_equal(np.sort(p), np.arange(n))
+    lo, hi = o.tree()
+    k = o.kappa
+    Xs = X[p]
+    for c in range((1 << k) - 1):
+        L = int(np.floor(np.log2(c + 1)))
+        cl, cr = 2 * c + 1, 2 * c + 2
+        ax = L % d
+        assert Xs[lo[cl]:hi[cl], ax].max() <= Xs[lo[cr]:hi[cr], ax].min()
+    ref = np.arange(n)
+    for L in range(k):
+        for c in range((1 << L) - 1, (2 << L) - 1):
+            seg = ref[lo[c]:hi[c]]
+            ref[lo[c]:hi[c]] = seg[np.argsort(X[seg, L % d], kind="stable")]
+    np.testing.assert_array_equal(p, ref)
+
+
+def test_kd_order_one_dim_is_the_sort():
+    """d = 1 given as an (n, 1) array: the same permutation and factorization as the 1-D input."""
+    rng = np.random.default_rng(44)
+    x = np.round(rng.uniform(0, 1, 777), 2); y = rng.standard_normal(777)
+    a = OracleHODLR(x, MATERN32, (1.0, 0.2), 1e-2, 20, 1e-12).factor()
+    b = OracleHODLR(x[:, None], MATERN32, (1.0, 0.2), 1e-2, 20, 1e-12).factor()
+    np.testing.assert_array_equal(a.perm(), b.perm())
+    assert a.logdet() == b.logdet()
+    np.testing.assert_array_equal(a.solve(y), b.solve(y))
+
+
+@pytest.mark.parametrize("d,kernel", [(2, SE), (2, MATERN32), (3, MATERN52)])
+def test_kd_hodlr_vs_dense(d, kernel):
+    """d-dimensional HODLR (kd ordering, Euclidean kernel entries) against numpy dense (scipy distances, LAPACK) and
+    the O11 checker; a shuffled input gives the same log det."""
+    rng = np.random.default_rng(50 + d + kernel)
+    n = 1200
+    X = rng.uniform(0, 1, (n, d)); y = rng.standard_normal(n)
+    th = (1.0, 0.5)
+    h = OracleHODLR(X, kernel, th, 1e-2, 32, 1e-12).factor()
+    C = _dense_C_nd(X, kernel, th, 1e-2)
+    sd, ld = np.linalg.slogdet(C)
+    assert sd > 0 and abs(h.logdet() - ld) <= 1e-11 * abs(ld)
+    xd = np.linalg.solve(C, y)
+    assert np.linalg.norm(h.solve(y) - xd) <= 1e-8 * np.linalg.norm(xd)
+    ld11, x11 = dense_check(X, kernel, th, 1e-2, y)
+    assert abs(ld11 - ld) <= 1e-11 * abs(ld)
+    q = rng.permutation(n)
+    h2 = OracleHODLR(X[q], kernel, th, 1e-2, 32, 1e-12).factor()
+    assert h2.logdet() == h.logdet()
