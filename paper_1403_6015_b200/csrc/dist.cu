@@ -9,6 +9,8 @@
 #include <string.h>
 #include <mutex>
 #include <condition_variable>
+#include <chrono>
+#include <stdlib.h>
 #include <vector>
 
 // ---------------------------------------------------------------------------------------------
@@ -68,11 +70,17 @@ struct HodlrGroup {
   std::vector<size_t> rec_bytes;
 };
 
-static void group_barrier(HodlrGroup *g) {
+// Returns false when the other ranks do not arrive within HODLR_GROUP_TIMEOUT_S seconds (default 300): a rank that
+// failed before an exchange then makes the waiting ranks fail instead of blocking forever.
+static bool group_barrier(HodlrGroup *g) {
+  static int tmo = -1;
+  if (tmo < 0) { const char *ev = getenv("HODLR_GROUP_TIMEOUT_S"); tmo = ev ? atoi(ev) : 300; }
   std::unique_lock<std::mutex> lk(g->mu);
   const long long my = g->gen;
-  if (++g->arrived == g->n) { g->arrived = 0; g->gen++; g->cv.notify_all(); }
-  else g->cv.wait(lk, [&] { return g->gen != my; });
+  if (++g->arrived == g->n) { g->arrived = 0; g->gen++; g->cv.notify_all(); return true; }
+  if (g->cv.wait_for(lk, std::chrono::seconds(tmo), [&] { return g->gen != my; })) return true;
+  g->arrived--;                              // withdraw: this rank gives up on the exchange
+  return false;
 }
 
 hodlr_status hodlr_allgather(hodlr_s *h, const void *send, void *recv, size_t bytes) {
@@ -96,7 +104,7 @@ hodlr_status hodlr_allgather(hodlr_s *h, const void *send, void *recv, size_t by
   }
   HCUDA(cudaStreamSynchronize(h->st));
   { std::lock_guard<std::mutex> lk(g->mu); g->send[h->grank] = send; }
-  group_barrier(g);
+  if (!group_barrier(g)) return hodlr_set_error(HODLR_ECUDA, "group exchange: the other ranks did not arrive (failed?)");
   for (int j = 0; j < g->n; j++)
     HCUDA(cudaMemcpyAsync((char *)recv + (size_t)j * bytes, g->send[j], bytes, cudaMemcpyDeviceToDevice, h->st));
   if (g->mode == 1 && h->grank == 0) {      // record rank 0's gathered buffer
@@ -107,7 +115,7 @@ hodlr_status hodlr_allgather(hodlr_s *h, const void *send, void *recv, size_t by
     g->rec.push_back(p); g->rec_bytes.push_back(bytes * g->n);
   }
   HCUDA(cudaStreamSynchronize(h->st));
-  group_barrier(g);
+  if (!group_barrier(g)) return hodlr_set_error(HODLR_ECUDA, "group exchange: the other ranks did not arrive (failed?)");
   return HODLR_OK;
 }
 

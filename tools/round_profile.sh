@@ -8,7 +8,7 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $out/gpu.txt
 lscpu | grep -E "Model name|^CPU\(s\)" > $out/cpu.txt
 HODLR_ACA_NOGRAPH=1 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
   --clock-control none --csv --log-file $out/traffic.csv python tools/prof_step.py cfg3 1 > /dev/null 2>&1
-python tools/ncu_traffic.py $out/traffic.csv $out/traffic.json
+python tools/ncu_traffic.py $out/traffic.csv $out/traffic.json && cp $out/traffic.json profiles/${tag}_traffic.json
 timeout 600 python bench.py --steps 5 --warmup 3 > $out/bench.json 2> $out/bench.err || tail -20 $out/bench.err
 timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > $out/bench_reference.json 2>> $out/bench.err
 HODLR_ACA_NOGRAPH=1 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
