@@ -41,6 +41,13 @@ double oracle_kernel(int kernel, const double *theta, double d) {
   if (kernel == ORACLE_EXP) return a * a * exp(-fabs(d) / ell);              /* Table I / IV: a^2 e^{-|d|/ell} */
   if (kernel == ORACLE_IMQ) return a * a / sqrt(1.0 + (d / ell) * (d / ell)); /* Table V */
   if (kernel == ORACLE_RQ) return a * a * pow(1.0 + (d / ell) * (d / ell), -theta[2]);   /* Table I */
+  /* NEXT-2, not positive definite (R20): multiquadric a^2 sqrt(1 + (d/ell)^2) (sec. 5.2 eq., Table III) and
+   * biharmonic / thin-plate a^2 (d/ell)^2 log|d/ell|, 0 at d = 0 (sec. 5.4, Table VI) */
+  if (kernel == ORACLE_MQ) return a * a * sqrt(1.0 + (d / ell) * (d / ell));
+  if (kernel == ORACLE_BIHARM) {
+    double q = fabs(d) / ell;
+    return q == 0.0 ? 0.0 : a * a * (q * q) * log(q);
+  }
   double r = fabs(d);
   if (kernel == ORACLE_MATERN32) {                /* a^2 (1 + s) e^{-s}, s = sqrt(3) r / ell */
     double s = sqrt(3.0) * r / ell;
@@ -204,6 +211,9 @@ int oracle_aca_dense(const double *A, int64_t m1, int64_t m2, int64_t lda, doubl
 struct oracle_hodlr {
   int64_t n; int kern; double theta[3]; double s2; int leaf; double eps; int cap;
   int dim;                          /* coordinates per point (xs: n x dim, point-major, sorted order) */
+  int leaf_lu;                      /* leaves by LU with partial pivoting: the twin, or a kernel that is not SPD */
+  int nonspd;                       /* kernel not positive definite: det C may be negative (signed log det) */
+  int sign;                         /* sign of det C after factor */
   double *dsort;                    /* heteroscedastic: s2 + noise_i in sorted order (NULL: s2 everywhere) */
   int kappa; int64_t nnodes, ninternal, nleaves;
   double *xs; int64_t *perm;
@@ -283,7 +293,7 @@ int oracle_build_nd(const double *x, int64_t n, int dim, int kernel, const doubl
                     const double *noise, int leaf, double eps, int rank_cap, oracle_hodlr **out) {
   *out = NULL;
   if (n < 1 || dim < 1 || dim > 64 || leaf < 1 || !(eps > 0.0 && eps < 1.0) || !(sigma2 >= 0.0) || !theta ||
-      !(theta[1] > 0.0) || !(theta[0] >= 0.0) || kernel < 0 || kernel > 5 || (kernel == ORACLE_RQ && !(theta[2] > 0.0)) ||
+      !(theta[1] > 0.0) || !(theta[0] >= 0.0) || kernel < 0 || kernel > 7 || (kernel == ORACLE_RQ && !(theta[2] > 0.0)) ||
       !isfinite(sigma2) ||
       !isfinite(theta[0]) || !isfinite(theta[1]))
     return fail(ORACLE_EINVAL, "build: invalid argument");
@@ -295,6 +305,12 @@ int oracle_build_nd(const double *x, int64_t n, int dim, int kernel, const doubl
   oracle_hodlr *h = calloc(1, sizeof *h);
   if (!h) return fail(ORACLE_ENOMEM, "build: oom");
   h->n = n; h->dim = dim; h->kern = kernel; h->theta[0] = theta[0]; h->theta[1] = theta[1];
+  h->nonspd = kernel == ORACLE_MQ || kernel == ORACLE_BIHARM;
+#ifdef ORACLE_TWIN
+  h->leaf_lu = 1;
+#else
+  h->leaf_lu = h->nonspd;
+#endif
   h->theta[2] = kernel == ORACLE_RQ ? theta[2] : 0.0;
   h->s2 = sigma2; h->leaf = leaf; h->eps = eps; h->cap = rank_cap;
   /* O2: kappa = largest integer with leaf * 2^kappa <= n (0 if n <= leaf); count-median split, left = ceil(m/2) */
@@ -524,34 +540,37 @@ int oracle_factor(oracle_hodlr *h) {
   }
   memcpy(h->Xh, h->X, sizeof(double) * (size_t)(n * K));
   h->state = -1;   /* until success */
+  int sign = 1;    /* sign of det C (R20): product of the leaves' and coupling systems' determinant signs */
   /* O5 + O6: leaves -- Cholesky, log det partial, solve the panel rows (all ancestor columns). */
   for (int64_t l = 0; l < h->nleaves; l++) {
     int64_t id = h->ninternal + l, lo = h->lo[id], m = h->hi[id] - lo;
     double *A = malloc(sizeof(double) * (size_t)(m * m));
     if (!A) return fail(ORACLE_ENOMEM, "factor: oom");
     for (int64_t i = 0; i < m; i++) for (int64_t j = 0; j < m; j++) A[i * m + j] = entry_C(h, lo + i, lo + j);
-#ifndef ORACLE_TWIN
-    if (cholesky(A, m) != 0) {
-      free(A); h->logdet = -INFINITY; h->fstatus = ORACLE_ENOTPD;
-      return fail(ORACLE_ENOTPD, "factor: leaf %lld not positive definite", (long long)l);
+    if (!h->leaf_lu) {
+      if (cholesky(A, m) != 0) {
+        free(A); h->logdet = -INFINITY; h->fstatus = ORACLE_ENOTPD;
+        return fail(ORACLE_ENOTPD, "factor: leaf %lld not positive definite", (long long)l);
+      }
+      double s = 0.0;
+      for (int64_t i = 0; i < m; i++) s += log(A[i * m + i]);
+      h->leaf_ld[l] = 2.0 * s;
+      h->Lleaf[l] = A;
+      for (int64_t c = 0; c < K; c++) chol_solve(A, m, &h->X[lo * K + c], K);
+    } else {
+      /* O5' (twin, or a kernel that is not SPD): A = P^T L U with partial pivoting; log|det| = sum log |U_ii|, sign
+       * from the pivots and U_ii: must be > 0 for a covariance, may be < 0 otherwise (zero = singular) */
+      int *lp = malloc(sizeof(int) * (size_t)m);
+      double la = 0.0; int sg = 1;
+      if (!lp || lu_factor(A, (int)m, lp, &la, &sg) != 0 || sg == 0 || (sg < 0 && !h->nonspd)) {
+        free(A); free(lp); h->logdet = -INFINITY; h->fstatus = ORACLE_ENOTPD;
+        return fail(ORACLE_ENOTPD, "factor: leaf %lld singular or det <= 0", (long long)l);
+      }
+      h->leaf_ld[l] = la;
+      if (sg < 0) sign = -sign;
+      h->Lleaf[l] = A; h->Lpiv[l] = lp;
+      for (int64_t c = 0; c < K; c++) lu_solve(A, (int)m, lp, &h->X[lo * K + c], K);
     }
-    double s = 0.0;
-    for (int64_t i = 0; i < m; i++) s += log(A[i * m + i]);
-    h->leaf_ld[l] = 2.0 * s;
-    h->Lleaf[l] = A;
-    for (int64_t c = 0; c < K; c++) chol_solve(A, m, &h->X[lo * K + c], K);
-#else
-    /* O5' (twin): A = P^T L U with partial pivoting; log det = sum log |U_ii|, det must be > 0 */
-    int *lp = malloc(sizeof(int) * (size_t)m);
-    double la = 0.0; int sg = 1;
-    if (!lp || lu_factor(A, (int)m, lp, &la, &sg) != 0 || sg <= 0) {
-      free(A); free(lp); h->logdet = -INFINITY; h->fstatus = ORACLE_ENOTPD;
-      return fail(ORACLE_ENOTPD, "factor: leaf %lld singular or det <= 0", (long long)l);
-    }
-    h->leaf_ld[l] = la;
-    h->Lleaf[l] = A; h->Lpiv[l] = lp;
-    for (int64_t c = 0; c < K; c++) lu_solve(A, (int)m, lp, &h->X[lo * K + c], K);
-#endif
   }
   /* O7: level sweep d = kappa-1 .. 0 (SMW on [[I, P],[Q, I]], equation_Low_Rank_Update). */
   for (int d = kappa - 1; d >= 0; d--) {
@@ -578,10 +597,11 @@ int oracle_factor(oracle_hodlr *h) {
       if (q > 0 && qr_factor(S, q, S + q * q, &la, &sg) != 0) sg = 0;    /* O7' (twin) */
 #endif
       h->Slu[c] = S; h->Spiv[c] = piv;
-      if (sg <= 0) {
+      if (sg == 0 || (sg < 0 && !h->nonspd)) {
         h->logdet = -INFINITY; h->fstatus = ORACLE_ENOTPD;
         return fail(ORACLE_ENOTPD, "factor: coupling system of node %lld singular or det <= 0", (long long)c);
       }
+      if (sg < 0) sign = -sign;
       h->node_ld[c] = la;
       if (Kd == 0 || r == 0) continue;
       /* B = [Xh[c2,cs]^T X[c2,J]; Xh[c1,cs]^T X[c1,J]],  T = S^{-1} B */
@@ -619,8 +639,18 @@ int oracle_factor(oracle_hodlr *h) {
   for (int d = kappa - 1; d >= 0; d--)
     for (int64_t i = 0; i < ((int64_t)1 << d); i++) nadd(&acc, h->node_ld[((int64_t)1 << d) - 1 + i]);
   h->logdet = acc.s + acc.c;
+  h->sign = sign;
   h->fstatus = ORACLE_OK;
   h->state = 2;
+  return ORACLE_OK;
+}
+
+/* O8 for kernels that are not SPD: log |det C| and the sign of det C. */
+int oracle_logdet_sign(oracle_hodlr *h, double *logabs, int *sign) {
+  if (!h) return fail(ORACLE_EINVAL, "logdet: null handle");
+  if (h->state == -1) { *logabs = -INFINITY; *sign = 0; return fail(ORACLE_ENOTPD, "logdet: factorization failed"); }
+  if (h->state != 2) return fail(ORACLE_ESTATE, "logdet: not factored");
+  *logabs = h->logdet; *sign = h->sign;
   return ORACLE_OK;
 }
 
@@ -637,11 +667,8 @@ static void solve_sorted(const oracle_hodlr *h, double *b) {
   int64_t K = h->K;
   for (int64_t l = 0; l < h->nleaves; l++) {
     int64_t id = h->ninternal + l, lo = h->lo[id], m = h->hi[id] - lo;
-#ifndef ORACLE_TWIN
-    chol_solve(h->Lleaf[l], m, &b[lo], 1);
-#else
-    lu_solve(h->Lleaf[l], (int)m, h->Lpiv[l], &b[lo], 1);
-#endif
+    if (!h->leaf_lu) chol_solve(h->Lleaf[l], m, &b[lo], 1);
+    else lu_solve(h->Lleaf[l], (int)m, h->Lpiv[l], &b[lo], 1);
   }
   for (int d = h->kappa - 1; d >= 0; d--) {
     int64_t cs = h->coff[d + 1];
@@ -691,6 +718,7 @@ int oracle_solve(oracle_hodlr *h, const double *y, double *x, int64_t nrhs, int6
 
 int oracle_gp_loglik(oracle_hodlr *h, const double *y, double *out) {
   if (!h) return fail(ORACLE_EINVAL, "loglik: null handle");
+  if (h->nonspd) return fail(ORACLE_EINVAL, "loglik: the kernel is not positive definite (not a covariance)");
   if (h->state == -1) { *out = -INFINITY; return fail(ORACLE_ENOTPD, "loglik: factorization failed"); }
   if (h->state != 2) return fail(ORACLE_ESTATE, "loglik: not factored");
   int64_t n = h->n;

@@ -36,7 +36,8 @@ extern "C" {
 
 enum { ORACLE_OK = 0, ORACLE_EINVAL = 1, ORACLE_ENOTPD = 2, ORACLE_ERANKCAP = 3,
        ORACLE_ESTATE = 4, ORACLE_ENOMEM = 5 };
-enum { ORACLE_SE = 0, ORACLE_MATERN32 = 1, ORACLE_MATERN52 = 2, ORACLE_EXP = 3, ORACLE_IMQ = 4, ORACLE_RQ = 5 };
+enum { ORACLE_SE = 0, ORACLE_MATERN32 = 1, ORACLE_MATERN52 = 2, ORACLE_EXP = 3, ORACLE_IMQ = 4, ORACLE_RQ = 5,
+       ORACLE_MQ = 6, ORACLE_BIHARM = 7 };   /* MQ, BIHARM: not positive definite (NEXT-2) */
 
 typedef struct oracle_hodlr oracle_hodlr;
 
@@ -67,8 +68,10 @@ int oracle_build_nd(const double *x, int64_t n, int dim, int kernel, const doubl
                     const double *noise, int leaf, double eps, int rank_cap, oracle_hodlr **out);
 /* O5-O8: leaves, panel, sweep, log det ("Factor"). */
 int oracle_factor(oracle_hodlr *h);
-/* O8: log det C (after factor).  -INFINITY if the factorization failed. */
+/* O8: log det C (after factor).  -INFINITY if the factorization failed.  (log |det C| for MQ / BIHARM.) */
 int oracle_logdet(oracle_hodlr *h, double *logdet);
+/* O8 with the sign of det C (kernels that are not SPD: leaves by LU, det S_c of either sign; +1 for SPD kernels). */
+int oracle_logdet_sign(oracle_hodlr *h, double *logabs, int *sign);
 /* O9: x = C^{-1} y in the caller's original point order; nrhs columns, leading dim ld. */
 int oracle_solve(oracle_hodlr *h, const double *y, double *x, int64_t nrhs, int64_t ld);
 /* O10: -1/2 y^T C^{-1} y - 1/2 log det C - n/2 log(2 pi). */

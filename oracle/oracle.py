@@ -21,8 +21,9 @@ _TWIN_PATH = os.path.join(_HERE, "liboracle_twin.so")
 _lock = threading.Lock()
 _libs = {}
 
-SE, MATERN32, MATERN52, EXP, IMQ, RQ = 0, 1, 2, 3, 4, 5
-KERNELS = {"se": SE, "matern32": MATERN32, "matern52": MATERN52, "exp": EXP, "imq": IMQ, "rq": RQ}
+SE, MATERN32, MATERN52, EXP, IMQ, RQ, MQ, BIHARM = 0, 1, 2, 3, 4, 5, 6, 7
+KERNELS = {"se": SE, "matern32": MATERN32, "matern52": MATERN52, "exp": EXP, "imq": IMQ, "rq": RQ, "mq": MQ,
+           "biharm": BIHARM}
 STATUS = {0: "OK", 1: "EINVAL", 2: "ENOTPD", 3: "ERANKCAP", 4: "ESTATE", 5: "ENOMEM"}
 
 
@@ -64,6 +65,7 @@ def _load(twin: bool = False):
         for f in ("oracle_factor",):
             getattr(lib, f).argtypes = [P]; getattr(lib, f).restype = I32
         lib.oracle_logdet.argtypes = [P, P]; lib.oracle_logdet.restype = I32
+        lib.oracle_logdet_sign.argtypes = [P, P, P]; lib.oracle_logdet_sign.restype = I32
         lib.oracle_solve.argtypes = [P, P, P, I64, I64]; lib.oracle_solve.restype = I32
         lib.oracle_gp_loglik.argtypes = [P, P, P]; lib.oracle_gp_loglik.restype = I32
         lib.oracle_apply.argtypes = [P, P, P]; lib.oracle_apply.restype = I32
@@ -176,6 +178,12 @@ class OracleHODLR:
         v = C.c_double(0.0)
         _check(self._lib, self._lib.oracle_logdet(self._h, C.byref(v)))
         return v.value
+
+    def logdet_sign(self):
+        """(log |det C|, sign of det C) -- the kernels that are not SPD (MQ, BIHARM) may have det C < 0."""
+        v = C.c_double(0.0); sg = C.c_int(0)
+        _check(self._lib, self._lib.oracle_logdet_sign(self._h, C.byref(v), C.byref(sg)))
+        return v.value, sg.value
 
     def solve(self, y):
         y = np.asarray(y, dtype=np.float64)

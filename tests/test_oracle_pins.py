@@ -588,3 +588,59 @@ def test_kd_hodlr_vs_dense(d, kernel):
     q = rng.permutation(n)
     h2 = OracleHODLR(X[q], kernel, th, 1e-2, 32, 1e-12).factor()
     assert h2.logdet() == h.logdet()
+
+
+# ---------------------------------------------------------------------------------------------------------------
+# NEXT-2 (not positive definite): multiquadric (Table III) and biharmonic (Table VI), signed log det (R20)
+from oracle import MQ, BIHARM  # noqa: E402
+
+
+def test_nonspd_kernel_closed_forms():
+    """MQ a^2 sqrt(1 + (d/ell)^2) and biharmonic a^2 (d/ell)^2 log|d/ell| at hand-checked points."""
+    assert kernel_value(MQ, (2.0, 0.5), 0.5) == pytest.approx(4.0 * math.sqrt(2.0), rel=1e-15)
+    assert kernel_value(MQ, (1.0, 1.0), 0.0) == 1.0
+    assert kernel_value(BIHARM, (1.0, 1.0), math.e) == pytest.approx(math.e ** 2, rel=1e-15)
+    assert kernel_value(BIHARM, (3.0, 2.0), 2.0) == 0.0           # log 1 = 0
+    assert kernel_value(BIHARM, (1.0, 1.0), 0.0) == 0.0           # removable singularity
+    assert kernel_value(BIHARM, (1.0, 1.0), -0.5) == pytest.approx(0.25 * math.log(0.5), rel=1e-15)
+
+
+@pytest.mark.parametrize("kernel,s2,n", [(MQ, 1.0, 1500), (BIHARM, 2.0, 1500), (MQ, 1.0, 3000)])
+def test_nonspd_hodlr_vs_dense(kernel, s2, n):
+    """The paper's Table III / VI matrices C = s2 I + K on U[-3, 3] (1-D): HODLR (leaf LU, coupling systems of either
+    sign) against numpy slogdet / LAPACK solve -- log |det| and sign -- and the unfactorable-as-covariance guard."""
+    rng = np.random.default_rng(60 + kernel + n)
+    x = rng.uniform(-3, 3, n); y = rng.standard_normal(n)
+    d = np.abs(x[:, None] - x[None, :])
+    if kernel == MQ:
+        K = np.sqrt(1 + d * d)
+    else:
+        with np.errstate(divide="ignore", invalid="ignore"):
+            K = np.where(d > 0, d * d * np.log(d), 0.0)
+    Cm = K + s2 * np.eye(n)
+    sd, ld = np.linalg.slogdet(Cm)
+    h = OracleHODLR(x, kernel, (1.0, 1.0), s2, 64, 1e-12).factor()
+    la, sg = h.logdet_sign()
+    assert sg == int(sd) and abs(la - ld) <= 1e-11 * abs(ld)
+    xs = h.solve(y)
+    xd = np.linalg.solve(Cm, y)
+    assert np.linalg.norm(xs - xd) <= 1e-8 * np.linalg.norm(xd)
+    with pytest.raises(OracleError) as e:
+        h.gp_loglik(y)
+    assert e.value.status == "EINVAL"
+
+
+def test_nonspd_sign_both_ways():
+    """C = s2 I + MQ on U[-3, 3] has a handful of negative eigenvalues (7..10 here), so det C takes either sign with
+    the shift: both signs and log |det| against numpy on well-conditioned cases (cond ~1e4)."""
+    rng = np.random.default_rng(0)
+    seen = set()
+    for n, s2 in ((500, 1.0), (500, 0.5), (1000, 0.5), (1000, 1.0)):
+        x = rng.uniform(-3, 3, n)
+        d = np.abs(x[:, None] - x[None, :])
+        sd, ld = np.linalg.slogdet(np.sqrt(1 + d * d) + s2 * np.eye(n))
+        h = OracleHODLR(x, MQ, (1.0, 1.0), s2, 32, 1e-12).factor()
+        la, sg = h.logdet_sign()
+        assert sg == int(sd) and abs(la - ld) <= 1e-11 * abs(ld), (n, s2)
+        seen.add(sg)
+    assert seen == {1, -1}
