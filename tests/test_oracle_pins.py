@@ -355,7 +355,7 @@ def test_multi_rhs():
 def test_errors():
     x = np.linspace(0, 1, 100)
     for bad in [dict(n_x=np.array([])), dict(leaf=0), dict(eps=0.0), dict(eps=1.0), dict(s2=-1.0),
-                dict(theta=(1.0, 0.0)), dict(theta=(-1.0, 1.0)), dict(kernel=7),
+                dict(theta=(1.0, 0.0)), dict(theta=(-1.0, 1.0)), dict(kernel=8),
                 dict(n_x=np.array([0.0, np.nan])), dict(n_x=np.array([np.inf, 1.0]))]:
         args = dict(n_x=x, kernel=SE, theta=(1.0, 0.1), s2=1e-2, leaf=16, eps=1e-12)
         args.update(bad)
