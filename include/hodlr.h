@@ -55,10 +55,15 @@ typedef enum {
  *   EXP:       a^2 exp(-|d| / ell)            (Ornstein-Uhlenbeck, Table I; Table IV)
  *   IMQ:       a^2 / sqrt(1 + d^2 / ell^2)    (inverse multiquadric, Table V)
  *   RQ:        a^2 (1 + d^2 / ell^2)^-alpha   (rational quadratic, Table I), alpha = theta[2] > 0
- * (NEXT-2 of SURVEY 8(f): the paper's other SPD 1-D kernels.)
+ *   MQ:        a^2 sqrt(1 + d^2 / ell^2)    (multiquadric, sec. 5.2 / Table III)
+ *   BIHARM:    a^2 q^2 log q, q = |d| / ell, 0 at d = 0 (biharmonic, sec. 5.4 / Table VI)
+ * (NEXT-2 of SURVEY 8(f): the paper's other 1-D kernels.)  MQ and BIHARM are NOT positive definite (R20):
+ * their leaves are factored by LU with partial pivoting, coupling systems of either sign are accepted, det C may be
+ * negative (hodlr_logdet_sign), gp_loglik and the predictive variance refuse them (HODLR_EINVAL: not a covariance),
+ * and they run on one GPU, unbatched (dist / hodlr_build_batch / gp_loglik_sweep: HODLR_EINVAL).
  * C_ij = k(x_i - x_j) + sigma2 [i == j]. */
 typedef enum { HODLR_SE = 0, HODLR_MATERN32 = 1, HODLR_MATERN52 = 2, HODLR_EXP = 3, HODLR_IMQ = 4,
-               HODLR_RQ = 5 } hodlr_kernel;
+               HODLR_RQ = 5, HODLR_MQ = 6, HODLR_BIHARM = 7 } hodlr_kernel;
 
 /* Multi-GPU descriptor (subtree sharding, north_star).  NULL or nranks == 1 => one GPU.
  * nranks = P must be a power of two with P <= 2^kappa.  Rank g owns the depth-log2(P) node g (sorted rows
@@ -142,6 +147,12 @@ hodlr_status hodlr_factor_solve(hodlr_t h, const double *y, double *x, double *q
 /* "Det." (sec. 4): log det C = sum_leaves 2 sum log L_ii + sum_c log det S_c.
  * logdet_host: host double.  -INFINITY with HODLR_ENOTPD if the factorization failed. */
 hodlr_status hodlr_logdet(hodlr_t h, double *logdet_host);
+
+/* log |det C| and the sign of det C (O8, R20): the product of the leaves' LU
+ * determinant signs and the coupling systems' signs; +1 for every SPD kernel (whose factorization refuses any other
+ * sign with HODLR_ENOTPD).  logabs_host: host double (hodlr_logdet's value); sign_host: host int32 in {-1, +1}
+ * (0 with HODLR_ENOTPD when the factorization failed: a zero pivot). */
+hodlr_status hodlr_logdet_sign(hodlr_t h, double *logabs_host, int32_t *sign_host);
 
 /* Solve C X = Y (eq-fac).  y, x: device, column-major n x nrhs with leading
  * dimension ld >= n, original point order.  x may not alias y. */

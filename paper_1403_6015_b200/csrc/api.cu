@@ -13,10 +13,14 @@
 #include <chrono>
 static thread_local char g_err[1024] = "";
 
-void hodlr_trace(const char *what) {
+int hodlr_trace_on() {
   static int on = -1;
   if (on < 0) { const char *ev = getenv("HODLR_TRACE"); on = ev && atoi(ev) ? 1 : 0; }
-  if (!on) return;
+  return on;
+}
+
+void hodlr_trace(const char *what) {
+  if (!hodlr_trace_on()) return;
   static auto t0 = std::chrono::steady_clock::now();
   static auto tl = t0;
   auto now = std::chrono::steady_clock::now();
@@ -298,7 +302,7 @@ static KParams make_kp(hodlr_kernel kernel, const double *theta, double sigma2) 
   kp.c = kernel == HODLR_SE ? 1.0 / (2.0 * theta[1] * theta[1])
        : kernel == HODLR_MATERN32 ? sqrt(3.0) / theta[1]
        : kernel == HODLR_MATERN52 ? sqrt(5.0) / theta[1]
-       : kernel == HODLR_EXP ? 1.0 / theta[1] : 1.0 / (theta[1] * theta[1]);
+       : (kernel == HODLR_EXP || kernel == HODLR_BIHARM) ? 1.0 / theta[1] : 1.0 / (theta[1] * theta[1]);
   kp.alpha = kernel == HODLR_RQ ? theta[2] : 0.5;
   kp.ell = theta[1];
   kp.c2 = (2.0 * theta[1]) * theta[1];            // the oracle's 2.0 * ell * ell (left to right)
@@ -330,7 +334,10 @@ static hodlr_status build_impl(const double *x, int64_t nseg, int32_t B, hodlr_k
   if (nseg < 1) return hodlr_set_error(HODLR_EINVAL, "build: n = %lld < 1", (long long)nseg);
   if (leaf < 1) return hodlr_set_error(HODLR_EINVAL, "build: leaf = %d < 1", leaf);
   if (!(eps > 0.0 && eps < 1.0)) return hodlr_set_error(HODLR_EINVAL, "build: eps = %g not in (0, 1)", eps);
-  if ((int)kernel < 0 || (int)kernel > 5) return hodlr_set_error(HODLR_EINVAL, "build: unknown kernel %d", (int)kernel);
+  if ((int)kernel < 0 || (int)kernel > 7) return hodlr_set_error(HODLR_EINVAL, "build: unknown kernel %d", (int)kernel);
+  const bool nonspd = kernel == HODLR_MQ || kernel == HODLR_BIHARM;     // DESIGN.md R20
+  if (nonspd && (B > 1 || (dist && dist->nranks > 1)))
+    return hodlr_set_error(HODLR_EINVAL, "build: MQ / BIHARM (not positive definite) run on one GPU, unbatched");
   if (B < 1 || (B & (B - 1))) return hodlr_set_error(HODLR_EINVAL, "build_batch: B = %d is not a power of two", B);
   if (B > 1 && nseg < leaf) return hodlr_set_error(HODLR_EINVAL, "build_batch: n = %lld < leaf = %d", (long long)nseg, leaf);
   if (B > 1 && ((dist && dist->nranks > 1) || (opts && opts->noise)))
@@ -358,6 +365,7 @@ static hodlr_status build_impl(const double *x, int64_t nseg, int32_t B, hodlr_k
   h->launches = 0;
   h->n = n; h->leaf = leaf; h->eps = eps; h->cap = cap; h->theta[0] = theta[0]; h->theta[1] = theta[1];
   h->kp = make_kp(kernel, theta, sigma2);
+  h->nonspd = nonspd ? 1 : 0;
   h->nbatch = B; h->nseg = nseg;
   h->tbatch = 0;
   while ((1 << h->tbatch) < B) h->tbatch++;
@@ -466,7 +474,9 @@ static hodlr_status build_impl(const double *x, int64_t nseg, int32_t B, hodlr_k
   }
   static int chol_after = -1;     // HODLR_CHOL_AFTER_ACA=1: run the leaf Cholesky after the ACA (experiments)
   if (chol_after < 0) { const char *ev = getenv("HODLR_CHOL_AFTER_ACA"); chol_after = ev && atoi(ev) ? 1 : 0; }
-  if (!chol_after) {
+  if (h->nonspd) {
+    h->chol_done = 0;              // LU leaves in hodlr_factor (factor.cu)
+  } else if (!chol_after) {
     bool launched = false;
     CK(cudaEventRecord(h->ev_fork, h->st));
     CK(cudaStreamWaitEvent(h->st3, h->ev_fork, 0));
@@ -481,7 +491,7 @@ static hodlr_status build_impl(const double *x, int64_t nseg, int32_t B, hodlr_k
   st = hodlr_aca(h);
   hodlr_trace("build: aca returned");
   if (st != HODLR_OK) goto fail;
-  if (chol_after) {
+  if (chol_after && !h->nonspd) {
     bool launched = false;
     ph_begin(h, PH_CHOL);
     st = hodlr_leaf_chol_mma(h, h->st, &launched);
@@ -606,9 +616,10 @@ hodlr_status hodlr_factor(hodlr_t h) {
   st = finish(h, st, &h->t_factor);
   hodlr_trace("factor: finished");
   if (st != HODLR_OK) { h->state = -1; h->logdet = -INFINITY; return st; }
-  int f[3];
+  int f[11];
   cudaError_t e = cudaMemcpy(f, h->dflags, sizeof(f), cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return hodlr_cuda_check(e, "factor flags");
+  h->det_sign = (f[10] & 1) ? -1 : 1;
   if (f[1]) {
     h->state = -1; h->logdet = -INFINITY;
     return hodlr_set_error(HODLR_ENOTPD, "factor: node %d is not positive definite (%d failures)", f[2], f[1]);
@@ -630,7 +641,7 @@ hodlr_status hodlr_factor_solve(hodlr_t h, const double *y, double *x, double *q
   if (ce != cudaSuccess) st = hodlr_cuda_check(ce, "factor_solve flags");
   if (st == HODLR_OK) st = hodlr_factor_impl(h);
   if (st == HODLR_OK && x) st = hodlr_solve_impl(h, y, x, 1, h->n, false, true);   // down passes only
-  int f[4] = {0, 0, 0, 0};
+  int f[11] = {0};
   double quad = 0.0;
   // results through the pinned staging buffer: [0, 2) log det, y^T C^{-1} y; then the flags (one round trip)
   double *pd = (double *)h->pin;
@@ -656,6 +667,7 @@ hodlr_status hodlr_factor_solve(hodlr_t h, const double *y, double *x, double *q
     if (quad_host) *quad_host = NAN;
     return hodlr_set_error(HODLR_ENOTPD, "factor_solve: node %d is not positive definite (%d failures)", f[2], f[1]);
   }
+  h->det_sign = (f[10] & 1) ? -1 : 1;
   h->state = 2;                              // factored: logdet / solve / gp_loglik for other right-hand sides work
   if (f[3]) {
     int z = 0;
@@ -672,6 +684,17 @@ hodlr_status hodlr_logdet(hodlr_t h, double *logdet_host) {
   if (h->state != 2) return hodlr_set_error(HODLR_ESTATE, "logdet: not factored");
   *logdet_host = h->logdet;
   h->t_logdet = 0.0;
+  return HODLR_OK;
+}
+
+hodlr_status hodlr_logdet_sign(hodlr_t h, double *logabs_host, int32_t *sign_host) {
+  if (!h || !logabs_host || !sign_host) return hodlr_set_error(HODLR_EINVAL, "logdet_sign: NULL argument");
+  if (h->state == -1) {
+    *logabs_host = -INFINITY; *sign_host = 0;
+    return hodlr_set_error(HODLR_ENOTPD, "logdet_sign: factorization failed");
+  }
+  if (h->state != 2) return hodlr_set_error(HODLR_ESTATE, "logdet_sign: not factored");
+  *logabs_host = h->logdet; *sign_host = h->det_sign;
   return HODLR_OK;
 }
 
@@ -704,6 +727,7 @@ hodlr_status gp_predict(hodlr_t h, const double *y, const double *xt, int64_t m,
   if (h->state == -1) return hodlr_set_error(HODLR_ENOTPD, "predict: factorization failed");
   if (h->state != 2) return hodlr_set_error(HODLR_ESTATE, "predict: not factored");
   if (h->nranks > 1) return hodlr_set_error(HODLR_EINVAL, "predict: sharded handles are not supported");
+  if (h->nonspd && var) return hodlr_set_error(HODLR_EINVAL, "predict: no variance for a kernel that is not positive definite");
   h->launches = 0;
   cudaEventRecord(h->ev0, h->st);
   hodlr_status st = hodlr_predict_impl(h, y, xt, m, mean, var);
@@ -730,6 +754,7 @@ hodlr_status gp_loglik(hodlr_t h, const double *y, double *out_host) {
   if (!h || !y || !out_host) return hodlr_set_error(HODLR_EINVAL, "gp_loglik: NULL argument");
   if (h->state == -1) { *out_host = -INFINITY; return hodlr_set_error(HODLR_ENOTPD, "gp_loglik: factorization failed"); }
   if (h->state != 2) return hodlr_set_error(HODLR_ESTATE, "gp_loglik: not factored");
+  if (h->nonspd) return hodlr_set_error(HODLR_EINVAL, "gp_loglik: the kernel is not positive definite (not a covariance)");
   h->launches = 0;
   cudaEventRecord(h->ev0, h->st);
   hodlr_status st = hodlr_solve_impl(h, y, nullptr, 1, h->n, true);

@@ -23,6 +23,7 @@
 #define TREE_NARROW_MIN (4 * 148)   // levels with at least this many nodes (and q <= 16) use the 128-thread CTAs
 #endif
 #include <limits.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 namespace cg = cooperative_groups;
@@ -172,6 +173,159 @@ __global__ void __launch_bounds__(LT) k_leaf_factor(LeafCtx c) {
   }
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// Leaves of a kernel that is not positive definite (MQ, BIHARM; NEXT-2, R20): A_l = P^T L U by LU with
+// partial pivoting (the oracle's O5': row of max |.|, first index on ties), log|det A_l| = sum log|U_ii|, the sign of
+// det A_l counted into flags[10] when negative.  Stored for the solve: XL = L^{-1} (unit lower) in Lf, XU = U^{-T}
+// (lower) in Uf, both as fragment-order tiles (identity padding), and the row order lperm (P b = b[lperm]), so that
+// A_l^{-1} b = XU^T (XL (P b)).  Pi_l = E^T W with W = A_l^{-1} E by the LU substitutions (packed lower: row index a
+// = the E side, column b = the W side, as the oracle's B entries E_s^T X_J).  One CTA per leaf; A in shared memory
+// when it fits, W and the unpermuted panel E in the CTA's global scratch (L2-resident).
+// ---------------------------------------------------------------------------------------------
+struct LuCtx {
+  LeafCtx b;
+  double *Uf;              // XU tiles (lstride doubles per leaf)
+  int *lperm;              // 8T ints per leaf
+  int a_smem;              // A in shared memory
+  double *scr; long long scr_per_cta;
+};
+
+__global__ void __launch_bounds__(LT) k_leaf_factor_lu(LuCtx lc) {
+  extern __shared__ double sm[];
+  __shared__ long long colsrc[1024];
+  __shared__ int prm[256];
+  __shared__ int s_bad, s_neg, s_p;
+  const LeafCtx &c = lc.b;
+  const int t = threadIdx.x, lane = t & 31;
+  const int K = c.K, ldz = c.ldz, T = c.T, R8 = 8 * T;
+  double *scr = lc.scr + (long long)blockIdx.x * lc.scr_per_cta;
+  for (long long leaf = c.leaf0 + blockIdx.x; leaf < c.leaf0 + c.nown; leaf += gridDim.x) {
+    const long long id = c.ninternal + leaf, lo = c.lo[id];
+    const int m = (int)(c.hi[id] - lo);
+    const KParams kp = kp_of(c.kp, c.kps, c.nseg, lo);
+    double *A = lc.a_smem ? sm : scr;                          // m x m, row-major
+    double *W = scr + (lc.a_smem ? 0 : (long long)m * m);      // m x ldz: P E, then A^{-1} E
+    double *Eg = W + (long long)m * ldz;                      // m x ldz: E (sorted row order)
+    for (int p = t; p < m * m; p += LT) {
+      const int i = p / m, j = p - i * m;
+      double v = kval(kp, c.xs[lo + i] - c.xs[lo + j]);
+      if (i == j) v += sig2(kp, lo + i);
+      A[p] = v;
+    }
+    for (int i = t; i < 256; i += LT) prm[i] = i;
+    if (t == 0) { s_bad = 0; s_neg = 0; }
+    __syncthreads();
+    for (int k = 0; k < m; k++) {
+      if (t < 32) {                                            // pivot: first max |A[i][k]|, i >= k
+        double best = -1.0; int p = m;
+        for (int i = k + lane; i < m; i += 32) { const double v = fabs(A[i * m + k]); if (v > best) { best = v; p = i; } }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double b2 = __shfl_xor_sync(0xffffffffu, best, o); const int p2 = __shfl_xor_sync(0xffffffffu, p, o);
+          if (b2 > best || (b2 == best && p2 < p)) { best = b2; p = p2; }
+        }
+        if (lane == 0) {
+          s_p = p;
+          if (p != k) { const int tq = prm[k]; prm[k] = prm[p]; prm[p] = tq; s_neg ^= 1; }
+        }
+      }
+      __syncthreads();
+      const int p = s_p;
+      if (p != k) for (int j = t; j < m; j += LT) { const double tq = A[k * m + j]; A[k * m + j] = A[p * m + j]; A[p * m + j] = tq; }
+      __syncthreads();
+      const double ukk = A[k * m + k];
+      if (t == 0) { if (ukk == 0.0) s_bad = 1; if (ukk < 0.0) s_neg ^= 1; }
+      const double iu = ukk != 0.0 ? ukk : 1.0;
+      for (int i = k + 1 + t; i < m; i += LT) A[i * m + k] = A[i * m + k] / iu;
+      __syncthreads();
+      const int w = m - k - 1;
+      for (int e = t; e < w * w; e += LT) {
+        const int i = k + 1 + e / w, j = k + 1 + e % w;
+        A[i * m + j] = fma(-A[i * m + k], A[k * m + j], A[i * m + j]);
+      }
+      __syncthreads();
+    }
+    if (t == 0) {
+      double s = 0.0;
+      for (int i = 0; i < m; i++) s += log(fabs(A[i * m + i]));
+      c.leaf_ld[leaf] = s;
+      if (s_bad) { atomicAdd(&c.flags[1], 1); atomicMin(&c.flags[2], (int)id); }
+      else if (s_neg) atomicAdd(&c.flags[10], 1);
+    }
+    // XL = L^{-1} and XU = U^{-T} as fragment-order tiles (identity beyond m), one thread per column j
+    const int NT = T * (T + 1) / 2;
+    double *Lg = c.Lf + leaf * c.lstride, *Ug = lc.Uf + leaf * c.lstride;
+    for (long long p = t; p < (long long)NT * 64; p += LT) { Lg[p] = 0.0; Ug[p] = 0.0; }
+    for (int i = t; i < R8; i += LT) lc.lperm[leaf * R8 + i] = i < m ? prm[i] : i;
+    __syncthreads();
+    for (int j = t; j < R8; j += LT) {
+      if (j >= m) {
+        Lg[tix(j >> 3, j >> 3) * 64 + fo(j & 7, j & 7)] = 1.0;
+        Ug[tix(j >> 3, j >> 3) * 64 + fo(j & 7, j & 7)] = 1.0;
+        continue;
+      }
+      for (int i = j; i < m; i++) {                            // L x = e_j (unit diagonal)
+        double s = i == j ? 1.0 : 0.0;
+        for (int k = j; k < i; k++) s -= A[i * m + k] * Lg[tix(k >> 3, j >> 3) * 64 + fo(k & 7, j & 7)];
+        Lg[tix(i >> 3, j >> 3) * 64 + fo(i & 7, j & 7)] = s;
+      }
+      for (int i = j; i < m; i++) {                            // U^T z = e_j: z_i = (d_ij - sum_k U[k][i] z_k) / U_ii
+        double s = i == j ? 1.0 : 0.0;
+        for (int k = j; k < i; k++) s -= A[k * m + i] * Ug[tix(k >> 3, j >> 3) * 64 + fo(k & 7, j & 7)];
+        Ug[tix(i >> 3, j >> 3) * 64 + fo(i & 7, j & 7)] = s / A[i * m + i];
+      }
+    }
+    if (K > 0) {
+      if (t == 0) {   // column map: [rhs,] depth 1 .. kappa; zero beyond each block's rank
+        long long a = id;
+        for (int e = c.kappa; e >= 1; e--) {
+          long long b = (a - 1) / 2;
+          int rb = c.rank[b];
+          for (int q = 0; q < c.dt->rdep[e]; q++)
+            colsrc[c.aug + c.dt->Kdim[e - 1] + q] = q < rb ? c.dt->colbase[e] + q : -1;
+          a = b;
+        }
+        if (c.aug) colsrc[0] = -2;
+      }
+      __syncthreads();
+      for (long long p = t; p < (long long)K * m; p += LT) {
+        const long long col = p / m, i = p - col * m, src = colsrc[col];
+        double v = 0.0;
+        if (src >= 0) v = c.Xh[src * c.ldx + lo + i];
+        else if (src == -2) { v = c.y[c.perm[lo + i]]; if (!isfinite(v)) atomicOr(&c.flags[3], 1); }
+        Eg[i * ldz + col] = v;
+      }
+      __syncthreads();
+      for (int col = t; col < K; col += LT) {                  // W = U^{-1} L^{-1} P E
+        for (int i = 0; i < m; i++) {
+          double s = Eg[(long long)prm[i] * ldz + col];
+          for (int k = 0; k < i; k++) s -= A[i * m + k] * W[(long long)k * ldz + col];
+          W[(long long)i * ldz + col] = s;
+        }
+        for (int i = m - 1; i >= 0; i--) {
+          double s = W[(long long)i * ldz + col];
+          for (int k = i + 1; k < m; k++) s -= A[i * m + k] * W[(long long)k * ldz + col];
+          W[(long long)i * ldz + col] = s / A[i * m + i];
+        }
+      }
+      __syncthreads();
+      double *Pl = c.Pi + leaf * ((long long)K * (K + 1) / 2);   // Pi_l = E^T W, packed lower
+      const long long npk = (long long)K * (K + 1) / 2;
+      for (long long p = t; p < npk; p += LT) {
+        long long a = (long long)((sqrt(8.0 * (double)p + 1.0) - 1.0) * 0.5);
+        while (a * (a + 1) / 2 > p) a--;
+        while ((a + 1) * (a + 2) / 2 <= p) a++;
+        const long long b = p - a * (a + 1) / 2;
+        double s = 0.0;
+        for (int i = 0; i < m; i++) s = fma(Eg[(long long)i * ldz + a], W[(long long)i * ldz + b], s);
+        Pl[p] = s;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
 #include "tree_node.cuh"
 namespace {
@@ -198,7 +352,7 @@ template <bool DD>
 __global__ void __launch_bounds__(TT / 2, TREE_NARROW_MINB) k_tree_factor_narrow(TreeCtx c) {
   extern __shared__ double sm[];
   const long long i = c.i0 + blockIdx.x;
-  tree_node<DD>(c, i, sm, global_pi(c, i));
+  tree_node<DD, GlobalPi, 16>(c, i, sm, global_pi(c, i));      // (q <= 16 only)
 }
 
 // The upper levels (few nodes each) in ONE persistent cooperative launch: CTAs stride over the nodes of a level, a
@@ -337,6 +491,11 @@ hodlr_status hodlr_leaf_alloc(hodlr_s *h) {
   h->ltiles = Pfast ? Pfast / 8 : (mmax + 7) / 8;
   h->lstride = (long long)(h->ltiles * (h->ltiles + 1) / 2) * 64;      // tiles of X = L^{-1}
   h->Lf = (double *)hodlr_dalloc(h, sizeof(double) * h->lstride * nl);
+  if (h->nonspd) {                 // LU leaves: U^{-T} tiles and the row order (R20)
+    h->Uf = (double *)hodlr_dalloc(h, sizeof(double) * h->lstride * nl);
+    h->lperm = (int *)hodlr_dalloc(h, sizeof(int) * 8 * (size_t)h->ltiles * nl);
+    if (!h->Uf || !h->lperm) return hodlr_set_error(HODLR_ENOMEM, "leaf factor allocation failed");
+  }
   h->leaf_ld = (double *)hodlr_dalloc(h, sizeof(double) * nl);
   if (!h->Lf || !h->leaf_ld) return hodlr_set_error(HODLR_ENOMEM, "leaf factor allocation failed");
   HCUDA(cudaMemsetAsync(h->leaf_ld, 0, sizeof(double) * nl, h->st));      // other ranks' leaves count 0
@@ -353,7 +512,7 @@ static TreeCtx tree_ctx(hodlr_s *h, int d, long long i0) {
   tc.ldk = (tc.Kd + 3) & ~3; tc.dd = 1;   // compensated at every depth
   tc.Pi1 = h->Pipool + dt.piOff[d + 1]; tc.Pic = h->Pipool + dt.piOff[d];
   tc.Sst = h->Spool + dt.nodeS[d]; tc.BT = h->BTpool + dt.nodeBT[d];
-  tc.node_ld = h->node_ld; tc.flags = h->dflags;
+  tc.node_ld = h->node_ld; tc.flags = h->dflags; tc.nonspd = h->nonspd;
   return tc;
 }
 
@@ -393,9 +552,31 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
   HCUDA(cudaStreamWaitEvent(h->st, h->ev_chol, 0));     // leaf Cholesky issued during the build
   ph_begin(h, PH_LEAF);
   bool fast = false;
-  {
+  if (!h->nonspd) {
     hodlr_status fs = hodlr_leaf_factor_mma(h, K, h->Pipool + dt.piOff[kappa], &fast);   // needs the Cholesky kernel
     if (fs != HODLR_OK) return fs;
+  }
+  if (h->nonspd) {                 // LU leaves (R20)
+    LuCtx lu;
+    LeafCtx &lc = lu.b;
+    lc.kp = h->kp; lc.n = h->n; lc.ninternal = h->ninternal; lc.nleaves = nl; lc.kappa = kappa; lc.K = K;
+    lc.ldz = K | 1; lc.T = h->ltiles; lc.xs = h->xs; lc.lo = h->lo; lc.hi = h->hi; lc.Xh = h->Xh; lc.ldx = h->ldx;
+    lc.rank = h->rank; lc.dt = h->d_dt; lc.Lf = h->Lf; lc.lstride = h->lstride; lc.Pi = h->Pipool + dt.piOff[kappa];
+    lc.leaf_ld = h->leaf_ld; lc.flags = h->dflags; lc.aug = h->aug; lc.y = h->y_aug; lc.perm = h->perm;
+    lc.kps = h->d_kps; lc.nseg = h->nseg; lc.mmax = mmax;
+    hodlr_own_nodes(h, kappa, &lc.leaf0, &lc.nown);
+    lu.Uf = h->Uf; lu.lperm = h->lperm;
+    if (mmax > 256 || K > 1024) return hodlr_set_error(HODLR_EINVAL, "factor: LU leaves need leaf size <= 256, K <= 1024");
+    const size_t a_bytes = sizeof(double) * (size_t)mmax * mmax;
+    lu.a_smem = a_bytes <= (size_t)maxsm - 16 * 1024 ? 1 : 0;
+    const int grid = (int)std::min<long long>(lc.nown, 148 * 2);
+    lu.scr_per_cta = (lu.a_smem ? 0 : (long long)mmax * mmax) + 2LL * mmax * lc.ldz;
+    lu.scr = (double *)hodlr_dalloc_tmp(h, sizeof(double) * (size_t)lu.scr_per_cta * grid);
+    if (!lu.scr) return hodlr_set_error(HODLR_ENOMEM, "factor: scratch allocation failed");
+    if (lu.a_smem) HCUDA(hodlr_allow_smem((const void *)k_leaf_factor_lu, h->dev));
+    k_leaf_factor_lu<<<grid, LT, lu.a_smem ? a_bytes : 0, h->st>>>(lu);
+    HLAUNCH(h, "k_leaf_factor_lu");
+    fast = true;
   }
   if (!fast) {
     LeafCtx lc;

@@ -66,8 +66,11 @@ __device__ __forceinline__ double div_exact(double x, double c, double rc) { ret
 
 // Non-SE kernels share one exp: Matern pre (1 + s [+ s^2/3]) e^{-s}; EXP e^{-|d| c}; IMQ / RQ (1 + d^2 c)^{-alpha}
 // = e^{-alpha log(1 + d^2 c)} (no pow: u >= 1, alpha > 0), with c = sqrt(3)/ell, sqrt(5)/ell, 1/ell, 1/ell^2.
+// MQ a^2 sqrt(1 + d^2 c), BIHARM a^2 s^2 log s with s = |d| c (c = 1/ell^2, 1/ell): DESIGN.md R20.
 __device__ __forceinline__ double kval(const KParams &kp, double d) {
   if (kp.kern == HODLR_SE) return kp.a2 * exp(-(d * d) * kp.c);
+  if (kp.kern == HODLR_MQ) return kp.a2 * sqrt(fma(d * d, kp.c, 1.0));
+  if (kp.kern == HODLR_BIHARM) { const double q = fabs(d) * kp.c; return q == 0.0 ? 0.0 : kp.a2 * (q * q) * log(q); }
   const double s = fabs(d) * kp.c;
   double pre = 1.0, arg = -s;
   if (kp.kern == HODLR_MATERN32) pre = 1.0 + s;
@@ -220,10 +223,14 @@ struct hodlr_s {
   double *d_noise;           // heteroscedastic sigma_i^2 in sorted order (hodlr_opts.noise), or NULL
   struct TreeCtx *d_treectx; // per-level contexts of the persistent upper-tree launch (factor.cu)
   int *dflags;               // [0] nonfinite x, [1] notpd, [2] notpd node (min), [3] nonfinite y, [4] active big
-                             // ACA blocks, [5] rank-cap hits, [6] ACA steps, [7] x not ascending
+                             // ACA blocks, [5] rank-cap hits, [6] ACA steps, [7] x not ascending, [10] negative
+                             // determinants (LU leaves, coupling systems) of a kernel that is not SPD
   DepthTab *d_dt;
   // factor storage
   double *Lf; long long lstride; int ltiles;   // leaf factor tiles (see storage helpers)
+  int nonspd;                // MQ / BIHARM: LU leaves, either sign (R20)
+  int det_sign;              // sign of det C after the factorization (+1 for the SPD kernels)
+  double *Uf; int *lperm;    // LU leaves: U^{-T} tiles (as Lf) and the row order P (8 ltiles ints per leaf)
   double *Spool;  int *Piv;  double *BTpool; double *Pipool;
   double *leaf_ld, *node_ld, *d_logdet;
   double logdet;
@@ -252,6 +259,7 @@ static inline void ph_end(hodlr_s *h, int p, cudaStream_t s = nullptr) { cudaEve
 
 // HODLR_TRACE=1: host timestamps of the orchestration steps on stderr (development aid)
 void hodlr_trace(const char *what);
+int hodlr_trace_on();
 
 // helpers implemented in api.cu
 hodlr_status hodlr_set_error(hodlr_status code, const char *fmt, ...);
@@ -371,6 +379,14 @@ __device__ __forceinline__ double kval_o(const KParams &kp, double d) {
     case HODLR_RQ: {
       const double q = div_exact(d, kp.ell, kp.rell);
       return __dmul_rn(kp.a2, pow(__dadd_rn(1.0, __dmul_rn(q, q)), -kp.alpha));
+    }
+    case HODLR_MQ: {
+      const double q = div_exact(d, kp.ell, kp.rell);
+      return __dmul_rn(kp.a2, __dsqrt_rn(__dadd_rn(1.0, __dmul_rn(q, q))));
+    }
+    case HODLR_BIHARM: {
+      const double q = div_exact(fabs(d), kp.ell, kp.rell);
+      return q == 0.0 ? 0.0 : __dmul_rn(__dmul_rn(kp.a2, __dmul_rn(q, q)), log(q));
     }
     case HODLR_MATERN32: {
       const double s = div_exact(__dmul_rn(kp.sq, fabs(d)), kp.ell, kp.rell);

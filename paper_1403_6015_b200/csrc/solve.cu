@@ -38,6 +38,8 @@ struct SolveCtx {
   const int *rank;
   const DepthTab *dt;
   const double *Lf; long long lstride;
+  const double *Uf; const int *lperm;   // LU leaves (kernel not SPD, R20): A^{-1} b = XU^T (XL (P b)), XU = Uf tiles
+                                        // read from global memory, P b = b[lperm]; NULL for Cholesky leaves
   const double *Spool, *BTpool;
   double *V;        // per-level node vectors (g on the way up, w on the way down)
   double *Tv;       // per-node t_c (q hi, q lo doubles; depth-d offset nodeT[d])
@@ -210,8 +212,16 @@ __device__ void leaf_up_phase(const SolveCtx &c, double *sX, LeafSmem &S) {
       }
       if (r == 0) cp_wait<0>();                // X of this leaf
       __syncthreads();
-      tri_mv(sX, c.T, S.sb, S.su, S.red);      // u = X b
-      tri_mvt(sX, c.T, S.su, S.red, nullptr);  // v = X^T u  (into red[0..R))
+      if (c.Uf) {                              // LU leaves: u = XL (P b), v = XU^T u
+        const int *lp = c.lperm + leaf * Rr;
+        for (int i = t; i < Rr; i += LT) S.red[VMAX + i] = S.sb[lp[i]];
+        __syncthreads();
+        tri_mv(sX, c.T, S.red + VMAX, S.su, nullptr);
+        tri_mvt(c.Uf + leaf * c.lstride, c.T, S.su, S.red, nullptr);
+      } else {
+        tri_mv(sX, c.T, S.sb, S.su, S.red);      // u = X b
+        tri_mvt(sX, c.T, S.su, S.red, nullptr);  // v = X^T u  (into red[0..R))
+      }
       if (r + 1 == c.R && nxt < end) issue_x(c, nxt, sX);   // X is free
       double hs = 0.0;
       for (int i = t; i < m; i += LT) hs += S.sb[i] * S.red[i];
@@ -348,8 +358,16 @@ __device__ void leaf_down_phase(const SolveCtx &c, double *sX, LeafSmem &S) {
       }
       if (r == 0) cp_wait<0>();                // X of this leaf
       __syncthreads();
-      tri_mv(sX, c.T, S.sb, S.su, S.red);
-      tri_mvt(sX, c.T, S.su, S.sb, S.red);
+      if (c.Uf) {                              // LU leaves (R20)
+        const int *lp = c.lperm + leaf * Rr;
+        for (int i = t; i < Rr; i += LT) S.red[VMAX + i] = S.sb[lp[i]];
+        __syncthreads();
+        tri_mv(sX, c.T, S.red + VMAX, S.su, nullptr);
+        tri_mvt(c.Uf + leaf * c.lstride, c.T, S.su, S.sb, nullptr);
+      } else {
+        tri_mv(sX, c.T, S.sb, S.su, S.red);
+        tri_mvt(sX, c.T, S.su, S.sb, S.red);
+      }
       if (r + 1 == c.R && nxt < end) issue_x(c, nxt, sX);
       if (c.xsorted) for (int i2 = t; i2 < m; i2 += LT) c.xsorted[lo + i2] = S.sb[i2];
       else for (int i2 = t; i2 < m; i2 += LT) c.x[r * c.ldy + c.perm[lo + i2]] = S.sb[i2];
@@ -925,6 +943,7 @@ hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, int64_t nr
   c.T = h->ltiles; c.grank = h->grank; c.tsplit = h->tsplit;
   c.lo = h->lo; c.hi = h->hi; c.perm = h->perm; c.Xh = h->Xh; c.ldx = h->ldx; c.rank = h->rank; c.dt = h->d_dt;
   c.Lf = h->Lf; c.lstride = h->lstride; c.Spool = h->Spool; c.BTpool = h->BTpool;
+  c.Uf = h->nonspd ? h->Uf : nullptr; c.lperm = h->nonspd ? h->lperm : nullptr;
   c.V = h->Vpool; c.Tv = h->Tvec; c.hv = h->hvec; c.y = y; c.x = x; c.flags = h->dflags;
   c.vcol = h->vcol; c.tcol = h->tcol; c.hcol = h->hcol; c.ldy = ld;
   c.aug = h->aug; c.fused = fused ? 1 : 0;
@@ -945,7 +964,8 @@ hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, int64_t nr
   int maxsm = 0, nsm = 0;
   HCUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
   HCUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->dev));
-  const void *kfun = RM > 1 ? (const void *)k_solve<8> : (const void *)k_solve<1>;
+  const bool rb8 = RM > 1 && !h->nonspd;         // LU leaves: the one-column leaf phases (R20)
+  const void *kfun = rb8 ? (const void *)k_solve<8> : (const void *)k_solve<1>;
   cudaFuncAttributes fa;
   HCUDA(cudaFuncGetAttributes(&fa, kfun));
   const size_t static_smem = fa.sharedSizeBytes;
@@ -955,11 +975,11 @@ hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, int64_t nr
   const size_t x_db0 = 64 * (size_t)(h->ltiles * (h->ltiles + 1) / 2);
   c.xdoubles = (long long)x_db0;
   // RB = 8: the 8-column leaf scratch follows the X tiles in dynamic shared memory
-  const size_t x_db = x_db0 + (RM > 1 ? (sizeof(LeafSmem8) + 7) / 8 : 0);
+  const size_t x_db = x_db0 + (rb8 ? (sizeof(LeafSmem8) + 7) / 8 : 0);
   const size_t need = std::max(x_db, (size_t)c.tree_scratch);
   if (need > avail)
     return hodlr_set_error(HODLR_EINVAL, "solve: leaf inverse (%d rows) or coupling size %zu exceeds shared memory", Rr, qmax);
-  const size_t half = RM > 1 ? avail : std::min(avail, (size_t)(((size_t)maxsm / 2 - static_smem - 1024) / sizeof(double)));
+  const size_t half = rb8 ? avail : std::min(avail, (size_t)(((size_t)maxsm / 2 - static_smem - 1024) / sizeof(double)));
   const size_t dsm_d = std::max(x_db, std::min(half, (size_t)NWL * (size_t)c.tree_scratch));
   c.tree_warps = (int)std::min<size_t>(NWL, dsm_d / (size_t)c.tree_scratch);
   const size_t dsm = sizeof(double) * dsm_d;

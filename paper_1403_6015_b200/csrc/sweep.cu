@@ -28,6 +28,8 @@ extern "C" hodlr_status gp_loglik_sweep(const double *x, const double *y, int64_
                                         double eps, const hodlr_dist *dist, void *cuda_stream, int32_t workers,
                                         double *out_host) {
   if (kernel == HODLR_RQ) return hodlr_set_error(HODLR_EINVAL, "sweep: the rational quadratic (3 parameters) is not supported");
+  if (kernel == HODLR_MQ || kernel == HODLR_BIHARM)
+    return hodlr_set_error(HODLR_EINVAL, "sweep: the kernel is not positive definite (no log-likelihood)");
   if (!x || !y || !thetas || !sigma2s || !out_host || B < 1 || n < 1)
     return hodlr_set_error(HODLR_EINVAL, "gp_loglik_sweep: bad arguments");
   int dev = 0;

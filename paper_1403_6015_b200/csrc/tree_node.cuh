@@ -14,6 +14,7 @@ struct TreeCtx {
   long long cnt;            // nodes of depth d this launch computes (i0 .. i0 + cnt)
   int r, q, Kd, K1, ldk;    // ldk: row stride of B / T in shared memory (Kd rounded up to 4)
   int dd;                   // compensated (double-double) T and Pi
+  int nonspd;               // kernel not positive definite: det S_c < 0 is counted, not a failure (R20)
   const double *Pi1;        // children Pi base (depth d+1), packed K1(K1+1)/2 per node
   double *Pic;              // this depth's Pi base, packed Kd(Kd+1)/2 per node
   double *Sst;              // per node: S (q*q), S^{-1} (q*q), spare (q)
@@ -210,7 +211,7 @@ static __device__ void gj_warp(const double *W, double *Wt, double *Wout, int q,
 //   index on ties -- the same pivots and U_kk as the LU of the paper's coupling system) gives log|det S_c|,
 //   its sign and S_c^{-1};
 //   T_c = S_c^{-1} B_c, refined in compensated arithmetic (T = T_hi + T_lo);
-//   Pi_c = Pi_c1[a,a] + Pi_c2[a,a] - sum_u B_c[(u+r) mod q, a] T_c[u, b], 2x4 register tiles per thread.
+//   Pi_c = Pi_c1[a,a] + Pi_c2[a,a] - sum_u B_c[(u+r) mod q, a] T_c[u, b], 4x2 register tiles per thread.
 // Children's projected Gram matrices from global memory (packed, one per child at depth d+1).
 struct GlobalPi {
   const double *P1, *P2;    // Pi_c1, Pi_c2 (packed lower triangles)
@@ -231,7 +232,7 @@ struct GlobalPi {
 #else
 #define TSTAMP(k)
 #endif
-template <bool DD, class Src>
+template <bool DD, class Src, int QMAX = 32>
 __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &src) {
   const int t = threadIdx.x, NT = blockDim.x;
 #ifdef TREE_TRACE
@@ -273,15 +274,17 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
   __syncthreads();
   TSTAMP(1)
   // ---------------- Gauss-Jordan with partial pivoting ----------------
-  // q <= 16: warp 0 in registers (gj_regs); 16 < q <= 32: warp 0 in shared memory (gj_warp); larger systems: the
-  // whole CTA, one barrier per step.
-  // (S^{-1} goes to W2, row-major; gj_warp uses W2 as its transposed work area and then writes S^{-1} into W)
+  // q <= 16: warp 0 in registers (gj_regs, gj_cols); 16 < q <= 32: warp 0 in shared memory (gj_warp); larger systems:
+  // the whole CTA, one barrier per step.  (S^{-1} goes to W2, row-major; gj_warp uses W2 as its transposed work area
+  // and then writes S^{-1} into W.)  Measured per system (tools/micro/gj_bench.cu): ~1000 cycles per elimination step
+  // at q = 8, ~2700 at q = 26 -- a latency chain (pivot reduction, reciprocal, broadcast) that neither a CTA-wide
+  // elimination (one barrier per step) nor a two-warp column layout shortens.
   if (q <= 32) {
     if (t < 32) {
       int sign, zero;
       if (q <= 8) gj_regs<8>(W, W2, q, colk, sign, zero);
       else if (q <= TREE_GJ_REGS) gj_cols<16>(W, W2, q, colk, sign, zero);
-      else gj_warp(W, W2, W, q, colk, sign, zero);
+      else if (QMAX > 16) gj_warp(W, W2, W, q, colk, sign, zero);
       if (t == 0) { s_sign = sign; s_zero = zero; }
     }
   } else {
@@ -347,7 +350,8 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
     if (t == 0) {
       const bool zero = s_zero != 0;
       c.node_ld[node] = la;
-      if (zero || s_sign <= 0) { atomicAdd(&c.flags[1], 1); atomicMin(&c.flags[2], (int)node); }
+      if (zero || (s_sign <= 0 && !c.nonspd)) { atomicAdd(&c.flags[1], 1); atomicMin(&c.flags[2], (int)node); }
+      else if (s_sign < 0) atomicAdd(&c.flags[10], 1);          // det S_c < 0: allowed when not SPD (R20)
       // refinement steps: one when the pivot growth ratio is mild, two otherwise (cond(S_c) up to ~1e12)
       s_nref = (!zero && umax < 1e6 * umin) ? 1 : 2;
     }
@@ -391,9 +395,11 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
       __syncthreads();
     }
     TSTAMP(5)
-    // ---------------- Pi_c, 2x4 register tiles over the packed lower triangle ----------------
-    // Bands of 4 rows; band P holds row tiles I = 2P, 2P+1 with column tiles J = 0..P (tile (I, J) =
-    // rows 2I, 2I+1, columns 4J..4J+3); tiles up to band P: (P+1)(P+2).
+    // ---------------- Pi_c, 4x2 register tiles over the packed lower triangle ----------------
+    // Bands of 4 rows; band P (rows 4P .. 4P+3) holds column tiles J = 0 .. 2P+1 (columns 2J, 2J+1); tiles up to
+    // band P: (P+1)(P+2).  Consecutive threads take consecutive column pairs of a band: their T reads are
+    // consecutive 16-byte words (conflict-free double2 loads) and their B reads one broadcast -- a 2x4 tile with
+    // 4-column strides per lane had made every T load an 8-way bank conflict (the deep levels' bottleneck).
     double *Pc = c.Pic + i * ((long long)Kd * (Kd + 1) / 2);
     const int NB = (Kd + 3) >> 2;
     const int ntile = NB * (NB + 1);
@@ -401,14 +407,12 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
       int P = (int)((sqrt(4.0 * (double)tile + 1.0) - 1.0) * 0.5);
       while (P * (P + 1) > tile) P--;
       while ((P + 1) * (P + 2) <= tile) P++;
-      const int rem = tile - P * (P + 1);
-      const int I = 2 * P + rem / (P + 1), J = rem % (P + 1);
-      const int a0 = 2 * I, b0 = 4 * J;
-      double hs[2][4], ls[2][4];
+      const int a0 = 4 * P, b0 = 2 * (tile - P * (P + 1));
+      double hs[4][2], ls[4][2];
 #pragma unroll
-      for (int ii = 0; ii < 2; ii++)
+      for (int ii = 0; ii < 4; ii++)
 #pragma unroll
-        for (int jj = 0; jj < 4; jj++) {
+        for (int jj = 0; jj < 2; jj++) {
           const int a = a0 + ii, b = b0 + jj;
           double s = 0.0, e = 0.0;
           if (a < Kd && b <= a) src.template d<DD>(a, b, s, e);   // packed (a, b): same index in both children
@@ -417,16 +421,16 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
       for (int u = 0; u < q; u++) {
         const int ub = u < q - r ? u + r : u + r - q;
         const double *bu = B + (long long)ub * ldk + a0;
-        const double *thu = Th + (long long)u * ldk + b0, *tlu = Tl + (long long)u * ldk + b0;
-        double bv[2], th[4], tl[4];
+        const double2 th2 = *(const double2 *)(Th + (long long)u * ldk + b0);
+        const double2 tl2 = *(const double2 *)(Tl + (long long)u * ldk + b0);
+        const double th[2] = {th2.x, th2.y}, tl[2] = {tl2.x, tl2.y};
+        double bv[4];
 #pragma unroll
-        for (int x = 0; x < 2; x++) bv[x] = -bu[x];
+        for (int x = 0; x < 4; x++) bv[x] = -bu[x];
 #pragma unroll
-        for (int x = 0; x < 4; x++) { th[x] = thu[x]; tl[x] = tlu[x]; }
+        for (int ii = 0; ii < 4; ii++)
 #pragma unroll
-        for (int ii = 0; ii < 2; ii++)
-#pragma unroll
-          for (int jj = 0; jj < 4; jj++) {
+          for (int jj = 0; jj < 2; jj++) {
             if (DD) {
               double pr, pe, s2, e2;
               two_prod(bv[ii], th[jj], pr, pe);
@@ -439,9 +443,9 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
           }
       }
 #pragma unroll
-      for (int ii = 0; ii < 2; ii++)
+      for (int ii = 0; ii < 4; ii++)
 #pragma unroll
-        for (int jj = 0; jj < 4; jj++) {
+        for (int jj = 0; jj < 2; jj++) {
           const int a = a0 + ii, b = b0 + jj;
           if (a < Kd && b <= a) Pc[(long long)a * (a + 1) / 2 + b] = hs[ii][jj] + ls[ii][jj];
         }

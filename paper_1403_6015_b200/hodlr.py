@@ -15,11 +15,13 @@ import torch
 from . import build as _build
 
 HODLR_SE, HODLR_MATERN32, HODLR_MATERN52, HODLR_EXP, HODLR_IMQ, HODLR_RQ = 0, 1, 2, 3, 4, 5
+HODLR_MQ, HODLR_BIHARM = 6, 7      # not positive definite (hodlr.h, R20)
 KERNELS = {"se": HODLR_SE, "matern32": HODLR_MATERN32, "matern52": HODLR_MATERN52, "exp": HODLR_EXP,
-           "imq": HODLR_IMQ, "rq": HODLR_RQ}
+           "imq": HODLR_IMQ, "rq": HODLR_RQ, "mq": HODLR_MQ, "biharm": HODLR_BIHARM}
 STATUS = {0: "OK", 1: "EINVAL", 2: "ENOTPD", 3: "ERANKCAP", 4: "ESTATE", 5: "ENOMEM", 6: "ECUDA", 7: "ENCCL"}
 
-EXPORTS = ("hodlr_build", "hodlr_factor", "hodlr_factor_solve", "hodlr_cache_trim", "hodlr_logdet", "hodlr_solve", "hodlr_apply", "gp_predict", "gp_loglik",
+EXPORTS = ("hodlr_build", "hodlr_factor", "hodlr_factor_solve", "hodlr_cache_trim", "hodlr_logdet",
+           "hodlr_logdet_sign", "hodlr_solve", "hodlr_apply", "gp_predict", "gp_loglik",
            "hodlr_info",
            "hodlr_get_order", "hodlr_get_tree", "hodlr_get_logdet_parts", "hodlr_free", "hodlr_last_error",
            "hodlr_version", "hodlr_launch_count", "hodlr_nccl_unique_id", "hodlr_group_create",
@@ -81,6 +83,7 @@ def load(build_if_missing: bool = True):
         lib.hodlr_factor_solve.argtypes = [P, P, P, P]; lib.hodlr_factor_solve.restype = I32
         lib.hodlr_cache_trim.argtypes = []; lib.hodlr_cache_trim.restype = None
         lib.hodlr_logdet.argtypes = [P, P]
+        lib.hodlr_logdet_sign.argtypes = [P, P, P]
         lib.hodlr_solve.argtypes = [P, P, P, I64, I64]
         lib.hodlr_apply.argtypes = [P, P, P, I64, I64]
         lib.gp_predict.argtypes = [P, P, P, I64, P, P]
@@ -89,7 +92,7 @@ def load(build_if_missing: bool = True):
         lib.hodlr_get_order.argtypes = [P, P, P]
         lib.hodlr_get_tree.argtypes = [P, P, P, P]
         lib.hodlr_get_logdet_parts.argtypes = [P, P, P]
-        for f in ("hodlr_build", "hodlr_factor", "hodlr_logdet", "hodlr_solve", "hodlr_apply", "gp_predict", "gp_loglik",
+        for f in ("hodlr_build", "hodlr_factor", "hodlr_logdet", "hodlr_logdet_sign", "hodlr_solve", "hodlr_apply", "gp_predict", "gp_loglik",
                   "hodlr_info", "hodlr_get_order", "hodlr_get_tree", "hodlr_get_logdet_parts"):
             getattr(lib, f).restype = I32
         lib.hodlr_free.argtypes = [P]; lib.hodlr_free.restype = None
@@ -197,6 +200,13 @@ def hodlr_logdet(h: int) -> float:
     v = C.c_double(0.0)
     _check(load().hodlr_logdet(h, C.byref(v)))
     return v.value
+
+
+def hodlr_logdet_sign(h: int):
+    """(log |det C|, sign of det C) -- the sign is -1 only for a kernel that is not positive definite."""
+    v = C.c_double(0.0); sg = C.c_int32(0)
+    _check(load().hodlr_logdet_sign(h, C.byref(v), C.byref(sg)))
+    return v.value, sg.value
 
 
 def hodlr_solve(h: int, y: torch.Tensor, x: torch.Tensor | None = None) -> torch.Tensor:
@@ -336,6 +346,9 @@ class HODLR:
 
     def logdet(self) -> float:
         return hodlr_logdet(self._h)
+
+    def logdet_sign(self):
+        return hodlr_logdet_sign(self._h)
 
     def solve(self, y: torch.Tensor) -> torch.Tensor:
         return hodlr_solve(self._h, y)
