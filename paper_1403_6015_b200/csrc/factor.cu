@@ -19,6 +19,9 @@
 #include "hodlr_internal.cuh"
 #include <cooperative_groups.h>
 #include <vector>
+#ifndef TREE_PLAIN_LEVELS
+#define TREE_PLAIN_LEVELS 3
+#endif
 #ifndef TREE_NARROW_MIN
 #define TREE_NARROW_MIN (4 * 148)   // levels with at least this many nodes (and q <= 16) use the 128-thread CTAs
 #endif
@@ -336,23 +339,27 @@ __device__ __forceinline__ GlobalPi global_pi(const TreeCtx &c, long long i) {
   return g;
 }
 
-template <bool DD>
+// PIDD = false: the plain Pi update (the deepest levels); true: as the level's c.dd says.  DESIGN.md 6.2.
+template <bool PIDD>
 __global__ void __launch_bounds__(TT, 3) k_tree_factor(TreeCtx c) {
   extern __shared__ double sm[];
   const long long i = c.i0 + blockIdx.x;
-  tree_node<DD>(c, i, sm, global_pi(c, i));
+  tree_node<true, GlobalPi, 32, PIDD>(c, i, sm, global_pi(c, i));
 }
 
 // Levels with many small nodes: 128-thread CTAs (6 per SM) -- finer barrier domains, more independent nodes
 // in flight per SM.  Same device code.
+#ifndef TREE_PLAIN_LEVELS
+#define TREE_PLAIN_LEVELS 3
+#endif
 #ifndef TREE_NARROW_MINB
 #define TREE_NARROW_MINB 6
 #endif
-template <bool DD>
+template <bool PIDD>
 __global__ void __launch_bounds__(TT / 2, TREE_NARROW_MINB) k_tree_factor_narrow(TreeCtx c) {
   extern __shared__ double sm[];
   const long long i = c.i0 + blockIdx.x;
-  tree_node<DD, GlobalPi, 16>(c, i, sm, global_pi(c, i));      // (q <= 16 only)
+  tree_node<true, GlobalPi, 16, PIDD>(c, i, sm, global_pi(c, i));   // (q <= 16 only)
 }
 
 // The upper levels (few nodes each) in ONE persistent cooperative launch: CTAs stride over the nodes of a level, a
@@ -509,7 +516,10 @@ static TreeCtx tree_ctx(hodlr_s *h, int d, long long i0) {
   tc.cnt = 0;
   // factor-side widths: Kf = Kdim (+ 1 with a fused right-hand side, which is then index 0 of every Pi)
   tc.d = d; tc.i0 = i0; tc.r = dt.rdep[d + 1]; tc.q = 2 * tc.r; tc.Kd = dt.Kf[d]; tc.K1 = dt.Kf[d + 1];
-  tc.ldk = (tc.Kd + 3) & ~3; tc.dd = 1;   // compensated at every depth
+  tc.ldk = (tc.Kd + 3) & ~3;
+  // Pi update in plain FP64 at the TREE_PLAIN_LEVELS deepest levels of each problem (local depth = d - tbatch, so a
+  // batched handle and a single one do the same arithmetic per node), compensated above
+  tc.dd = (d - h->tbatch) < (h->kappa - h->tbatch) - TREE_PLAIN_LEVELS ? 1 : 0;
   tc.Pi1 = h->Pipool + dt.piOff[d + 1]; tc.Pic = h->Pipool + dt.piOff[d];
   tc.Sst = h->Spool + dt.nodeS[d]; tc.BT = h->BTpool + dt.nodeBT[d];
   tc.node_ld = h->node_ld; tc.flags = h->dflags; tc.nonspd = h->nonspd;
@@ -619,7 +629,9 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
   // thread-safe, and concurrent handles needing different sizes would race on a per-call value)
   if (kappa > 0) {
     HCUDA(hodlr_allow_smem((const void *)k_tree_factor<true>, h->dev));
+    HCUDA(hodlr_allow_smem((const void *)k_tree_factor<false>, h->dev));
     HCUDA(hodlr_allow_smem((const void *)k_tree_factor_narrow<true>, h->dev));
+    HCUDA(hodlr_allow_smem((const void *)k_tree_factor_narrow<false>, h->dev));
   }
   int nsm = 148;
   HCUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->dev));
@@ -665,8 +677,13 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
     if (cnt < TREE_NARROW_MIN) { top.push_back(tc); continue; }   // upper levels: batched into k_tree_top
     const size_t smem = sizeof(double) * (size_t)tree_smem_doubles(tc.q, tc.ldk);
     const bool narrow = tc.q <= 16;
-    if (narrow) k_tree_factor_narrow<true><<<(int)cnt, TT / 2, smem, h->st>>>(tc);
-    else k_tree_factor<true><<<(int)cnt, TT, smem, h->st>>>(tc);
+    if (narrow) {
+      if (tc.dd) k_tree_factor_narrow<true><<<(int)cnt, TT / 2, smem, h->st>>>(tc);
+      else k_tree_factor_narrow<false><<<(int)cnt, TT / 2, smem, h->st>>>(tc);
+    } else {
+      if (tc.dd) k_tree_factor<true><<<(int)cnt, TT, smem, h->st>>>(tc);
+      else k_tree_factor<false><<<(int)cnt, TT, smem, h->st>>>(tc);
+    }
     HLAUNCH(h, "k_tree_factor");
   }
   {

@@ -13,7 +13,7 @@ struct TreeCtx {
   long long i0;             // first node (index within depth d) of this launch
   long long cnt;            // nodes of depth d this launch computes (i0 .. i0 + cnt)
   int r, q, Kd, K1, ldk;    // ldk: row stride of B / T in shared memory (Kd rounded up to 4)
-  int dd;                   // compensated (double-double) T and Pi
+  int dd;                   // compensated (double-double) Pi update at this level
   int nonspd;               // kernel not positive definite: det S_c < 0 is counted, not a failure (R20)
   const double *Pi1;        // children Pi base (depth d+1), packed K1(K1+1)/2 per node
   double *Pic;              // this depth's Pi base, packed Kd(Kd+1)/2 per node
@@ -232,7 +232,7 @@ struct GlobalPi {
 #else
 #define TSTAMP(k)
 #endif
-template <bool DD, class Src, int QMAX = 32>
+template <bool DD, class Src, int QMAX = 32, bool PIDD = true>
 __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &src) {
   const int t = threadIdx.x, NT = blockDim.x;
 #ifdef TREE_TRACE
@@ -401,6 +401,7 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
     // consecutive 16-byte words (conflict-free double2 loads) and their B reads one broadcast -- a 2x4 tile with
     // 4-column strides per lane had made every T load an 8-way bank conflict (the deep levels' bottleneck).
     double *Pc = c.Pic + i * ((long long)Kd * (Kd + 1) / 2);
+    const bool PDD = DD && PIDD && c.dd;   // compensated Pi update (all but the deepest levels)
     const int NB = (Kd + 3) >> 2;
     const int ntile = NB * (NB + 1);
     for (int tile = t; tile < ntile; tile += NT) {
@@ -415,7 +416,9 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
         for (int jj = 0; jj < 2; jj++) {
           const int a = a0 + ii, b = b0 + jj;
           double s = 0.0, e = 0.0;
-          if (a < Kd && b <= a) src.template d<DD>(a, b, s, e);   // packed (a, b): same index in both children
+          if (a < Kd && b <= a) {                                 // packed (a, b): same index in both children
+            if (PDD) src.template d<true>(a, b, s, e); else src.template d<false>(a, b, s, e);
+          }
           hs[ii][jj] = s; ls[ii][jj] = e;
         }
       for (int u = 0; u < q; u++) {
@@ -431,7 +434,7 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
         for (int ii = 0; ii < 4; ii++)
 #pragma unroll
           for (int jj = 0; jj < 2; jj++) {
-            if (DD) {
+            if (PDD) {
               double pr, pe, s2, e2;
               two_prod(bv[ii], th[jj], pr, pe);
               two_sum(hs[ii][jj], pr, s2, e2);
