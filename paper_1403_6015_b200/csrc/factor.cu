@@ -366,14 +366,15 @@ __global__ void __launch_bounds__(TT / 2, TREE_NARROW_MINB) k_tree_factor_narrow
 // grid barrier separates the levels (deepest first).  These levels were launch- and cold-start-bound one kernel per
 // level (~50 us each regardless of their node count: every level's few CTAs start on SMs whose instruction caches
 // hold other kernels' code -- tree_node is ~10k instructions); here every SM warms its cache once.
+// Levels are not separated by grid barriers: a node waits (tree_node) for its children's progress flags, so a parent's
+// Gauss-Jordan overlaps the children's Pi updates.  Deadlock-free: every CTA takes its nodes deepest level first, and
+// the cooperative launch keeps every CTA resident.
 template <bool DD>
 __global__ void __launch_bounds__(TT, 2) k_tree_top(const TreeCtx *__restrict__ ctxs, int nlev) {
-  cg::grid_group grid = cg::this_grid();
   extern __shared__ double sm[];
   for (int L = 0; L < nlev; L++) {
     const TreeCtx c = ctxs[L];
     for (long long j = blockIdx.x; j < c.cnt; j += gridDim.x) tree_node<DD>(c, c.i0 + j, sm, global_pi(c, c.i0 + j));
-    if (L + 1 < nlev) grid.sync();
   }
 }
 
@@ -523,6 +524,7 @@ static TreeCtx tree_ctx(hodlr_s *h, int d, long long i0) {
   tc.Pi1 = h->Pipool + dt.piOff[d + 1]; tc.Pic = h->Pipool + dt.piOff[d];
   tc.Sst = h->Spool + dt.nodeS[d]; tc.BT = h->BTpool + dt.nodeBT[d];
   tc.node_ld = h->node_ld; tc.flags = h->dflags; tc.nonspd = h->nonspd;
+  tc.ready = nullptr; tc.wait = 0; tc.r_up = d > 0 ? dt.rdep[d] : 0;
   return tc;
 }
 
@@ -535,6 +537,8 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
   // ---- storage ----
   const int mmax = h->leaf_max;
   h->node_ld = (double *)hodlr_dalloc(h, sizeof(double) * (h->ninternal > 0 ? h->ninternal : 1));
+  if (!h->d_ready) h->d_ready = (int *)hodlr_dalloc(h, sizeof(int) * (h->ninternal > 0 ? h->ninternal : 1));
+  if (!h->d_ready) return hodlr_set_error(HODLR_ENOMEM, "factor: device allocation failed");
   h->d_logdet = (double *)hodlr_dalloc(h, sizeof(double));
   long long piTot = 0, sTot = 0, btTot = 0;
   for (int e = kappa; e >= 0; e--) {
@@ -645,6 +649,8 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
       maxcnt = std::max(maxcnt, tc.cnt);
     }
     if (top.size() > (size_t)TREE_TOP_MAXLEV) return hodlr_set_error(HODLR_EINVAL, "factor: tree level table overflow");
+    for (size_t L = 0; L < top.size(); L++) { top[L].ready = h->d_ready; top[L].wait = L > 0 ? 1 : 0; }
+    HCUDA(cudaMemsetAsync(h->d_ready, 0, sizeof(int) * (size_t)(h->ninternal > 0 ? h->ninternal : 1), h->st));
     HCUDA(cudaMemcpyAsync(h->d_treectx, top.data(), sizeof(TreeCtx) * top.size(), cudaMemcpyHostToDevice, h->st));
     HCUDA(hodlr_allow_smem((const void *)k_tree_top<true>, h->dev));
     int per_sm = 0;

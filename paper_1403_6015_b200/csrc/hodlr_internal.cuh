@@ -222,6 +222,7 @@ struct hodlr_s {
   int *d_forced;             // hodlr_opts.forced_ranks on the device (test hook), or NULL
   double *d_noise;           // heteroscedastic sigma_i^2 in sorted order (hodlr_opts.noise), or NULL
   struct TreeCtx *d_treectx; // per-level contexts of the persistent upper-tree launch (factor.cu)
+  int *d_ready;              // k_tree_top per-node progress flags (factor.cu, tree_node.cuh)
   int *dflags;               // [0] nonfinite x, [1] notpd, [2] notpd node (min), [3] nonfinite y, [4] active big
                              // ACA blocks, [5] rank-cap hits, [6] ACA steps, [7] x not ascending, [10] negative
                              // determinants (LU leaves, coupling systems) of a kernel that is not SPD

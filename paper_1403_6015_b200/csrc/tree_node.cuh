@@ -15,6 +15,10 @@ struct TreeCtx {
   int r, q, Kd, K1, ldk;    // ldk: row stride of B / T in shared memory (Kd rounded up to 4)
   int dd;                   // compensated (double-double) Pi update at this level
   int nonspd;               // kernel not positive definite: det S_c < 0 is counted, not a failure (R20)
+  int *ready;               // k_tree_top: per-node progress flags (heap id; 1 = the parent's rows of Pi_c written,
+                            // 2 = node done), or NULL (levels separated by kernel boundaries)
+  int wait;                 // wait for the children's flags (their level ran in the same k_tree_top launch)
+  int r_up;                 // rows of Pi_c the parent's coupling system and B read first: its rank r (= rdep[d])
   const double *Pi1;        // children Pi base (depth d+1), packed K1(K1+1)/2 per node
   double *Pic;              // this depth's Pi base, packed Kd(Kd+1)/2 per node
   double *Sst;              // per node: S (q*q), S^{-1} (q*q), spare (q)
@@ -232,6 +236,27 @@ struct GlobalPi {
 #else
 #define TSTAMP(k)
 #endif
+// Node-level dependencies inside k_tree_top (instead of a grid barrier per level): a parent starts as soon as its
+// children have written the bottom rows of their Pi (the ones its S_c and B_c read) and runs its Gauss-Jordan,
+// T and refinement while the children finish the rest of their Pi.
+__device__ __forceinline__ void tree_wait(const int *f, int v) {
+  int x;
+  while (true) {
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(x) : "l"(f) : "memory");
+    if (x >= v) break;
+    __nanosleep(100);
+  }
+}
+__device__ __forceinline__ void tree_signal(int *f, int v) {    // after a CTA barrier that follows the writes
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" :: "l"(f), "r"(v) : "memory");
+}
+__device__ __forceinline__ void tree_wait_children(const TreeCtx &c, long long node, int v) {
+  if (c.ready && c.wait) {
+    if (threadIdx.x == 0) { tree_wait(c.ready + 2 * node + 1, v); tree_wait(c.ready + 2 * node + 2, v); }
+    __syncthreads();
+  }
+}
+
 template <bool DD, class Src, int QMAX = 32, bool PIDD = true>
 __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &src) {
   const int t = threadIdx.x, NT = blockDim.x;
@@ -253,6 +278,7 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
   double *Tl = Th + (long long)q * ldk;
   double *R = Tl + (long long)q * ldk;
   __shared__ int s_zero, s_sign, s_nref;
+  tree_wait_children(c, node, 1);              // (k_tree_top) the children's bottom rows of Pi
   for (int p = t; p < q * q2; p += NT) {
     const int a = p / q2, b = p - a * q2;
     double v;
@@ -404,7 +430,8 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
     const bool PDD = DD && PIDD && c.dd;   // compensated Pi update (all but the deepest levels)
     const int NB = (Kd + 3) >> 2;
     const int ntile = NB * (NB + 1);
-    for (int tile = t; tile < ntile; tile += NT) {
+    tree_wait_children(c, node, 2);            // (k_tree_top) the children's whole Pi
+    auto pi_tile = [&](int tile) {
       int P = (int)((sqrt(4.0 * (double)tile + 1.0) - 1.0) * 0.5);
       while (P * (P + 1) > tile) P--;
       while ((P + 1) * (P + 2) <= tile) P++;
@@ -452,7 +479,16 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
           const int a = a0 + ii, b = b0 + jj;
           if (a < Kd && b <= a) Pc[(long long)a * (a + 1) / 2 + b] = hs[ii][jj] + ls[ii][jj];
         }
+    };
+    // (k_tree_top) the bands holding the parent's rows first, then the flag, then the rest
+    const int Pb = c.ready ? max(0, (Kd - c.r_up) >> 2) : 0, tb = Pb * (Pb + 1);
+    for (int tile = tb + t; tile < ntile; tile += NT) pi_tile(tile);
+    if (c.ready) {
+      __threadfence();
+      __syncthreads();
+      if (t == 0) tree_signal(c.ready + node, 1);
     }
+    for (int tile = t; tile < tb; tile += NT) pi_tile(tile);
   }
   TSTAMP(6)
   // persist S, S^{-1}, B, T_hi, T_lo for the solve
@@ -470,7 +506,9 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
     BTg[qKd + p] = Th[a * ldk + b];
     BTg[2 * qKd + p] = Tl[a * ldk + b];
   }
+  if (c.ready) __threadfence();
   __syncthreads();
+  if (c.ready && t == 0) tree_signal(c.ready + node, 2);
   TSTAMP(7)
 #ifdef TREE_TRACE
   if (threadIdx.x == 0 && i == 0)
