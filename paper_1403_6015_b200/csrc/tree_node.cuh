@@ -4,6 +4,10 @@
 // T_c = S_c^{-1} B_c refined in compensated arithmetic, Pi_c = Pi_c1 + Pi_c2 - B^T T (compensated).
 #pragma once
 #include "hodlr_internal.cuh"
+#ifndef TREE_GJ_WARP_MAX
+#define TREE_GJ_WARP_MAX 8       // largest q eliminated by one warp in registers (larger: the whole CTA, one barrier
+                                 // per step -- measured 66 us faster over cfg3's tree than one warp for 8 < q <= 32)
+#endif
 #ifndef TREE_GJ_REGS
 #define TREE_GJ_REGS 16          // largest q of the register Gauss-Jordan (gj_regs up to 8, gj_cols up to 16)
 #endif
@@ -300,12 +304,12 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
   __syncthreads();
   TSTAMP(1)
   // ---------------- Gauss-Jordan with partial pivoting ----------------
-  // q <= 16: warp 0 in registers (gj_regs, gj_cols); 16 < q <= 32: warp 0 in shared memory (gj_warp); larger systems:
-  // the whole CTA, one barrier per step.  (S^{-1} goes to W2, row-major; gj_warp uses W2 as its transposed work area
-  // and then writes S^{-1} into W.)  Measured per system (tools/micro/gj_bench.cu): ~1000 cycles per elimination step
-  // at q = 8, ~2700 at q = 26 -- a latency chain (pivot reduction, reciprocal, broadcast) that neither a CTA-wide
-  // elimination (one barrier per step) nor a two-warp column layout shortens.
-  if (q <= 32) {
+  // q <= TREE_GJ_WARP_MAX (8): warp 0 in registers (gj_regs); larger systems: the whole CTA, one barrier per step
+  // (gj_cols / gj_warp, one warp for q <= 16 / 32, measured slower).  (S^{-1} goes to W2, row-major, or wherever the
+  // last ping-pong step left it; gj_warp uses W2 as its transposed work area and then writes S^{-1} into W.)
+  // One warp needs ~1000 cycles per elimination step at q = 8 and ~2700 at q = 26 (tools/micro/gj_bench.cu); a
+  // two-warp column layout and a software-pipelined row sweep were no faster.
+  if (q <= TREE_GJ_WARP_MAX) {
     if (t < 32) {
       int sign, zero;
       if (q <= 8) gj_regs<8>(W, W2, q, colk, sign, zero);
@@ -386,7 +390,7 @@ __device__ void tree_node(const TreeCtx &c, long long i, double *sm, const Src &
   TSTAMP(3)
   const bool zero = s_zero != 0;
   // S^{-1}, row stride 2q: W2 (gj_regs), W (gj_warp), or wherever the last ping-pong step left it
-  const double *Si = ((q <= TREE_GJ_REGS || (q > 32 && (q & 1))) ? W2 : W) + q;
+  const double *Si = (q <= TREE_GJ_WARP_MAX ? (q <= TREE_GJ_REGS ? W2 : W) : ((q & 1) ? W2 : W)) + q;
   if (!zero && Kd > 0) {
     const int qK = q * ldk;
     for (int e = t; e < qK; e += NT) {                // T_hi = S^{-1} B
