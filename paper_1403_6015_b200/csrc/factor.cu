@@ -22,6 +22,9 @@
 #ifndef TREE_PLAIN_LEVELS
 #define TREE_PLAIN_LEVELS 3
 #endif
+#ifndef TREE_DEEP_SMEM
+#define TREE_DEEP_SMEM (36 * 1024)  // deep-run levels keep 6 CTAs per SM (their shared memory per node at most this)
+#endif
 #ifndef TREE_NARROW_MIN
 #define TREE_NARROW_MIN (4 * 148)   // levels with at least this many nodes (and q <= 16) use the 128-thread CTAs
 #endif
@@ -352,6 +355,9 @@ __global__ void __launch_bounds__(TT, 3) k_tree_factor(TreeCtx c) {
 #ifndef TREE_PLAIN_LEVELS
 #define TREE_PLAIN_LEVELS 3
 #endif
+#ifndef TREE_DEEP_SMEM
+#define TREE_DEEP_SMEM (36 * 1024)  // deep-run levels keep 6 CTAs per SM (their shared memory per node at most this)
+#endif
 #ifndef TREE_NARROW_MINB
 #define TREE_NARROW_MINB 6
 #endif
@@ -366,6 +372,33 @@ __global__ void __launch_bounds__(TT / 2, TREE_NARROW_MINB) k_tree_factor_narrow
 // grid barrier separates the levels (deepest first).  These levels were launch- and cold-start-bound one kernel per
 // level (~50 us each regardless of their node count: every level's few CTAs start on SMs whose instruction caches
 // hold other kernels' code -- tree_node is ~10k instructions); here every SM warms its cache once.
+// The deep levels (many nodes, q <= 16) in ONE persistent launch of 128-thread CTAs: nodes are handed out by an atomic
+// counter, deepest level first, and a node waits (tree_node) for its children's progress flags, so the partial last
+// wave of one level is filled by the next level's nodes instead of each level's launch ending in a tail.  Deadlock-free:
+// a node only waits for nodes handed out before it (to resident CTAs of the cooperative launch).
+template <bool PIDD>
+__global__ void __launch_bounds__(TT / 2, TREE_NARROW_MINB) k_tree_deep(const TreeCtx *__restrict__ ctxs, int nlev,
+                                                                      unsigned *next) {
+  extern __shared__ double sm[];
+  __shared__ long long s_j;
+  __shared__ int s_L;
+  for (;;) {
+    if (threadIdx.x == 0) {
+      long long j = (long long)atomicAdd(next, 1u);
+      int L = 0;
+      while (L < nlev && j >= ctxs[L].cnt) { j -= ctxs[L].cnt; L++; }
+      s_j = j; s_L = L;
+    }
+    __syncthreads();
+    const int L = s_L;
+    const long long j = s_j;
+    __syncthreads();
+    if (L >= nlev) return;
+    const TreeCtx c = ctxs[L];
+    tree_node<true, GlobalPi, 16, PIDD>(c, c.i0 + j, sm, global_pi(c, c.i0 + j));
+  }
+}
+
 // Levels are not separated by grid barriers: a node waits (tree_node) for its children's progress flags, so a parent's
 // Gauss-Jordan overlaps the children's Pi updates.  Deadlock-free: every CTA takes its nodes deepest level first, and
 // the cooperative launch keeps every CTA resident.
@@ -537,7 +570,7 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
   // ---- storage ----
   const int mmax = h->leaf_max;
   h->node_ld = (double *)hodlr_dalloc(h, sizeof(double) * (h->ninternal > 0 ? h->ninternal : 1));
-  if (!h->d_ready) h->d_ready = (int *)hodlr_dalloc(h, sizeof(int) * (h->ninternal > 0 ? h->ninternal : 1));
+  if (!h->d_ready) h->d_ready = (int *)hodlr_dalloc(h, sizeof(int) * (size_t)(h->ninternal + 2));   // + k_tree_deep's counter
   if (!h->d_ready) return hodlr_set_error(HODLR_ENOMEM, "factor: device allocation failed");
   h->d_logdet = (double *)hodlr_dalloc(h, sizeof(double));
   long long piTot = 0, sTot = 0, btTot = 0;
@@ -650,7 +683,7 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
     }
     if (top.size() > (size_t)TREE_TOP_MAXLEV) return hodlr_set_error(HODLR_EINVAL, "factor: tree level table overflow");
     for (size_t L = 0; L < top.size(); L++) { top[L].ready = h->d_ready; top[L].wait = L > 0 ? 1 : 0; }
-    HCUDA(cudaMemsetAsync(h->d_ready, 0, sizeof(int) * (size_t)(h->ninternal > 0 ? h->ninternal : 1), h->st));
+    HCUDA(cudaMemsetAsync(h->d_ready, 0, sizeof(int) * (size_t)(h->ninternal + 2), h->st));
     HCUDA(cudaMemcpyAsync(h->d_treectx, top.data(), sizeof(TreeCtx) * top.size(), cudaMemcpyHostToDevice, h->st));
     HCUDA(hodlr_allow_smem((const void *)k_tree_top<true>, h->dev));
     int per_sm = 0;
@@ -667,9 +700,43 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
     top.clear();
     return HODLR_OK;
   };
+  std::vector<TreeCtx> deep;          // the current run of deep levels for k_tree_deep
+  auto flush_deep = [&]() -> hodlr_status {
+    if (deep.empty()) return HODLR_OK;
+    if (deep.size() > (size_t)TREE_TOP_MAXLEV) return hodlr_set_error(HODLR_EINVAL, "factor: tree level table overflow");
+    size_t smem = 0;
+    long long tot = 0;
+    bool anydd = false;
+    for (size_t L = 0; L < deep.size(); L++) {
+      deep[L].ready = h->d_ready; deep[L].wait = L > 0 ? 1 : 0;
+      smem = std::max(smem, sizeof(double) * (size_t)tree_smem_doubles(deep[L].q, deep[L].ldk));
+      tot += deep[L].cnt;
+      anydd = anydd || deep[L].dd;
+    }
+    const void *kf = anydd ? (const void *)k_tree_deep<true> : (const void *)k_tree_deep<false>;
+    HCUDA(cudaMemsetAsync(h->d_ready, 0, sizeof(int) * (size_t)(h->ninternal + 2), h->st));
+    HCUDA(cudaMemcpyAsync(h->d_treectx, deep.data(), sizeof(TreeCtx) * deep.size(), cudaMemcpyHostToDevice, h->st));
+    HCUDA(hodlr_allow_smem(kf, h->dev));
+    int per_sm = 0;
+    HCUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, TT / 2, smem));
+    if (per_sm < 1) return hodlr_set_error(HODLR_EINVAL, "factor: coupling system too large for one SM");
+    long long gmax = (long long)nsm * per_sm;
+    if (h->coop_ctas > 0) gmax = std::min<long long>(gmax, h->coop_ctas);
+    const int grid = (int)std::min<long long>(tot, gmax);
+    const TreeCtx *pc = h->d_treectx;
+    int nlev = (int)deep.size();
+    unsigned *nx = (unsigned *)(h->d_ready + h->ninternal);
+    void *args[] = {(void *)&pc, (void *)&nlev, (void *)&nx};
+    HCUDA(cudaLaunchCooperativeKernel(kf, dim3(grid), dim3(TT / 2), args, smem, h->st));
+    HLAUNCH(h, "k_tree_deep");
+    deep.clear();
+    return HODLR_OK;
+  };
   for (int d = kappa - 1; d >= 0; d--) {
     if (d + 1 == h->tsplit && h->nranks > 1) {     // every rank gets the Pi of all depth-t subtree roots
-      hodlr_status fs = flush_top();
+      hodlr_status fs = flush_deep();
+      if (fs != HODLR_OK) return fs;
+      fs = flush_top();
       if (fs != HODLR_OK) return fs;
       const long long Kt = dt.Kf[d + 1], sz = Kt * (Kt + 1) / 2;
       double *base = h->Pipool + dt.piOff[d + 1];
@@ -680,9 +747,19 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
     hodlr_own_nodes(h, d, &i0, &cnt);
     TreeCtx tc = tree_ctx(h, d, i0);
     tc.cnt = cnt;
-    if (cnt < TREE_NARROW_MIN) { top.push_back(tc); continue; }   // upper levels: batched into k_tree_top
+    if (cnt < TREE_NARROW_MIN) {                  // upper levels: batched into k_tree_top
+      hodlr_status fs = flush_deep();
+      if (fs != HODLR_OK) return fs;
+      top.push_back(tc);
+      continue;
+    }
     const size_t smem = sizeof(double) * (size_t)tree_smem_doubles(tc.q, tc.ldk);
     const bool narrow = tc.q <= 16;
+    if (narrow && smem <= TREE_DEEP_SMEM) { deep.push_back(tc); continue; }   // deep run: k_tree_deep
+    {
+      hodlr_status fs = flush_deep();
+      if (fs != HODLR_OK) return fs;
+    }
     if (narrow) {
       if (tc.dd) k_tree_factor_narrow<true><<<(int)cnt, TT / 2, smem, h->st>>>(tc);
       else k_tree_factor_narrow<false><<<(int)cnt, TT / 2, smem, h->st>>>(tc);
@@ -693,7 +770,9 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
     HLAUNCH(h, "k_tree_factor");
   }
   {
-    hodlr_status fs = flush_top();
+    hodlr_status fs = flush_deep();
+    if (fs != HODLR_OK) return fs;
+    fs = flush_top();
     if (fs != HODLR_OK) return fs;
   }
   // log det: this rank's leaves and subtree nodes (others are 0), exchanged with the failure counts, then the
