@@ -435,9 +435,8 @@ static hodlr_status build_impl(const double *x, int64_t nseg, int32_t B, hodlr_k
   CK(cudaMemcpyAsync(h->d_dt, &h->dt, sizeof(DepthTab), cudaMemcpyHostToDevice, h->st));
   hodlr_trace("build: enter");
   st = hodlr_sort_and_tree(h, x, nseg);
-  hodlr_trace("build: sort done (synced)");
+  hodlr_trace("build: sort issued");
   if (st != HODLR_OK) goto fail;
-  if (h->x_nonfinite) { st = hodlr_set_error(HODLR_EINVAL, "build: x contains NaN or Inf"); goto fail; }
   if (B > 1) {     // batched: every problem has problem 0's order; per-problem parameters on the device
     k_replicate_order<<<592, 256, 0, h->st>>>(h->xs, h->perm, nseg, B);
     {
@@ -518,6 +517,7 @@ static hodlr_status build_impl(const double *x, int64_t nseg, int32_t B, hodlr_k
       h->aca_steps = fl16[6];
       h->launches += 3 * fl16[6]; hodlr_global_launches += 3 * fl16[6];
     }
+    if (fl16[0]) { st = hodlr_set_error(HODLR_EINVAL, "build: x contains NaN or Inf"); goto fail; }   // (k_make_keys)
     if (f8) { st = hodlr_set_error(HODLR_EINVAL, "build: noise contains a negative or non-finite entry"); goto fail; }
     // per-depth max ranks (the panel layout K_e must agree on every rank) and the rank-cap hits
     std::vector<double> loc(kappa + 2, 0.0);
