@@ -755,7 +755,14 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
     }
     const size_t smem = sizeof(double) * (size_t)tree_smem_doubles(tc.q, tc.ldk);
     const bool narrow = tc.q <= 16;
-    if (narrow && smem <= TREE_DEEP_SMEM) { deep.push_back(tc); continue; }   // deep run: k_tree_deep
+    if (narrow && smem <= TREE_DEEP_SMEM) {      // deep run (k_tree_deep): levels of one Pi precision per launch
+      if (!deep.empty() && deep.back().dd != tc.dd) {
+        hodlr_status fs = flush_deep();
+        if (fs != HODLR_OK) return fs;
+      }
+      deep.push_back(tc);
+      continue;
+    }
     {
       hodlr_status fs = flush_deep();
       if (fs != HODLR_OK) return fs;

@@ -123,3 +123,13 @@ def test_nonspd_refusals(hb):
     g.close()
     with pytest.raises(hb.HodlrError):
         hb.HODLRBatch(x, BIHARM, [(1.0, 1.0), (1.0, 1.0)], [2.0, 2.0], 32, 1e-10)
+
+
+def test_logdet_sign_spd_is_plus_one(hb):
+    """hodlr_logdet_sign on an SPD kernel: sign +1 and log |det| = hodlr_logdet (the same factorization)."""
+    rng = np.random.default_rng(3)
+    x = torch.from_numpy(rng.uniform(0, 10, 4096)).cuda()
+    g = hb.HODLR(x, 0, (1.0, 0.5), 1e-2, 64, 1e-10).factor()
+    la, sg = g.logdet_sign()
+    assert sg == 1 and la == g.logdet()
+    g.close()
