@@ -414,13 +414,19 @@ __global__ void __launch_bounds__(TT, 2) k_tree_top(const TreeCtx *__restrict__ 
 // log det partial = leaves (left to right), then internal nodes of depth >= tsplit by depth kappa-1..tsplit,
 // left to right; per-thread Neumaier over a contiguous segment, combined in order by thread 0.
 // out[0] = partial, out[1] = failures seen by this rank.
-__global__ void k_logdet_reduce(const double *leaf_ld, const double *node_ld, long long nleaves, int kappa, int tsplit,
-                                const int *flags, double *out) {
-  __shared__ double ss[256], cc[256];
+constexpr int LDR_T = 1024;      // k_logdet_reduce threads
+__device__ __forceinline__ void neu_add(double &S, double &C, double x) {   // Neumaier: S + C += x
+  const double tt = S + x;
+  if (fabs(S) >= fabs(x)) C += (S - tt) + x; else C += (x - tt) + S;
+  S = tt;
+}
+__global__ void __launch_bounds__(LDR_T) k_logdet_reduce(const double *leaf_ld, const double *node_ld, long long nleaves,
+                                                         int kappa, int tsplit, const int *flags, double *out) {
+  __shared__ double ss[LDR_T], cc[LDR_T], s2[32], c2[32];
   const long long nnode = nleaves - (1LL << tsplit);     // internal nodes of depth >= tsplit
   const long long N = nleaves + nnode;
   const int t = threadIdx.x;
-  long long per = (N + 255) / 256, v0 = t * per, v1 = v0 + per < N ? v0 + per : N;
+  long long per = (N + LDR_T - 1) / LDR_T, v0 = t * per, v1 = v0 + per < N ? v0 + per : N;
   double s = 0.0, comp = 0.0;
   int d = kappa - 1; long long u = 0;     // (depth, index) of internal value v (depth kappa-1 first), advanced in step
   if (v0 > nleaves && v0 < v1) { u = v0 - nleaves; while (u >= (1LL << d)) { u -= (1LL << d); d--; } }
@@ -431,23 +437,21 @@ __global__ void k_logdet_reduce(const double *leaf_ld, const double *node_ld, lo
       x = node_ld[(1LL << d) - 1 + u];
       if (++u == (1LL << d)) { u = 0; d--; }
     }
-    double tt = s + x;
-    if (fabs(s) >= fabs(x)) comp += (s - tt) + x; else comp += (x - tt) + s;
-    s = tt;
+    neu_add(s, comp, x);
   }
   ss[t] = s; cc[t] = comp;
   __syncthreads();
-  if (t == 0) {
+  if (t < 32) {                          // fixed order: lane l folds partials 32l .. 32l+31, lane 0 folds the lanes
     double S = 0.0, Cc = 0.0;
-    for (int j = 0; j < 256; j++) {
-      double x = ss[j];
-      double tt = S + x;
-      if (fabs(S) >= fabs(x)) Cc += (S - tt) + x; else Cc += (x - tt) + S;
-      S = tt;
-      Cc += cc[j];
+    for (int j = 32 * t; j < 32 * t + 32; j++) { neu_add(S, Cc, ss[j]); Cc += cc[j]; }
+    s2[t] = S; c2[t] = Cc;
+    __syncwarp();
+    if (t == 0) {
+      double S2 = 0.0, C2 = 0.0;
+      for (int j = 0; j < 32; j++) { neu_add(S2, C2, s2[j]); C2 += c2[j]; }
+      out[0] = S2 + C2;
+      out[1] = (double)flags[1];
     }
-    out[0] = S + Cc;
-    out[1] = (double)flags[1];
   }
 }
 
@@ -784,7 +788,7 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
   }
   // log det: this rank's leaves and subtree nodes (others are 0), exchanged with the failure counts, then the
   // top-level nodes (computed redundantly by every rank) once
-  k_logdet_reduce<<<1, 256, 0, h->st>>>(h->leaf_ld, h->node_ld, nl, kappa, h->tsplit, h->dflags, ldx + 2 * h->nranks);
+  k_logdet_reduce<<<1, LDR_T, 0, h->st>>>(h->leaf_ld, h->node_ld, nl, kappa, h->tsplit, h->dflags, ldx + 2 * h->nranks);
   HLAUNCH(h, "k_logdet_reduce");
   {
     hodlr_status xs = hodlr_allgather(h, ldx + 2 * h->nranks, ldx, sizeof(double) * 2);
