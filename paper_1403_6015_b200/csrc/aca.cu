@@ -145,7 +145,7 @@ struct AcaScratch {
 // block.  The cases that end the oracle's loop without the test (k + 1 == min(m1, m2), no unused nonzero pivot
 // row, forced ranks) end immediately; at the rank cap (k + 1 == cap, where the test decides between rank cap and
 // ERANKCAP) one more step runs in dots-only mode (no new column is stored).
-template <bool ROW, bool SEO>
+template <bool ROW, int SEO>
 __device__ __forceinline__ void aca_item(const AcaCtx &c, int item, AcaScratch &S) {
   double *coef = S.coef;
   double (*sdot)[ACA_MAXCAP] = S.sdot;
@@ -440,7 +440,7 @@ __device__ __forceinline__ void aca_item(const AcaCtx &c, int item, AcaScratch &
 // Measured against a persistent cooperative kernel that strides one CTA per SM over the items with grid barriers
 // between passes: 3.8 ms vs 2.1 ms for the passes at config 3 (its 150 registers allow one CTA per SM, too few
 // loads in flight for the streamed factor columns).
-template <bool ROW, bool SEO>
+template <bool ROW, int SEO>
 __global__ void __launch_bounds__(ACA_SUB, ACA_PASS_MINB) k_aca_pass(const AcaCtx *__restrict__ pc) {
   __shared__ AcaCtx c;
   __shared__ AcaScratch S;
@@ -471,7 +471,7 @@ __global__ void __launch_bounds__(ACA_SUB) k_aca_finish(const AcaCtx *__restrict
 #ifndef ACA_FUSED_FU
 #define ACA_FUSED_FU 4
 #endif
-template <bool SEO, int NT, int MAXS>
+template <int SEO, int NT, int MAXS>
 __global__ void __launch_bounds__(NT) k_aca_fused(AcaCtx c, const int *blocks, int *flags) {
   constexpr int FU = ACA_FUSED_FU;
   __shared__ double vbuf[MAXS];
@@ -647,7 +647,7 @@ __global__ void k_aca_cond(cudaGraphConditionalHandle hdl, const AcaCtx *__restr
 struct AcaPlan {
   // key: everything the cached device tables depend on -- the tree (n, leaf, batch depth), the shard (rank, nranks), the
   // factor slot layout (rank cap: colbase[e] = sum of min(cap, max node size)), the kernel variant and the device
-  long long n; int leaf; int rank, nranks; bool seo; int cap; int dev; int tbatch;
+  long long n; int leaf; int rank, nranks; int seo; int cap; int dev; int tbatch;   // seo: kv_of(kernel)
   long long nb; int nbig;
   std::vector<int> fused_blocks;
   int nfused_small = 0;                    // fused_blocks[0, nfused_small): both sides <= ACA_FUSED_SMALL
@@ -747,12 +747,12 @@ static cudaError_t plan_create(AcaPlan *P, const hodlr_s *h) {
   if (e == cudaSuccess) {
     cudaGraph_t body = cpar.conditional.phGraph_out[0];
     cudaKernelNodeParams k1 = {};
-    k1.func = P->seo ? (void *)k_aca_pass<true, true> : (void *)k_aca_pass<true, false>; k1.gridDim = dim3((unsigned)P->nitems_r); k1.blockDim = dim3(ACA_SUB);
+    k1.func = P->seo == KV_SE ? (void *)k_aca_pass<true, KV_SE> : P->seo == KV_M52 ? (void *)k_aca_pass<true, KV_M52> : (void *)k_aca_pass<true, KV_ANY>; k1.gridDim = dim3((unsigned)P->nitems_r); k1.blockDim = dim3(ACA_SUB);
     k1.kernelParams = arow;
     e = cudaGraphAddKernelNode(&n1, body, nullptr, 0, &k1);
     if (e == cudaSuccess) {
       cudaKernelNodeParams k2 = {};
-      k2.func = P->seo ? (void *)k_aca_pass<false, true> : (void *)k_aca_pass<false, false>; k2.gridDim = dim3((unsigned)P->nitems_c); k2.blockDim = dim3(ACA_SUB);
+      k2.func = P->seo == KV_SE ? (void *)k_aca_pass<false, KV_SE> : P->seo == KV_M52 ? (void *)k_aca_pass<false, KV_M52> : (void *)k_aca_pass<false, KV_ANY>; k2.gridDim = dim3((unsigned)P->nitems_c); k2.blockDim = dim3(ACA_SUB);
       k2.kernelParams = acol;
       e = cudaGraphAddKernelNode(&n2, body, &n1, 1, &k2);
     }
@@ -773,13 +773,13 @@ static AcaPlan *plan_acquire(const hodlr_s *h, hodlr_status *st) {
     std::lock_guard<std::mutex> lk(g_plan_mu);
     for (AcaPlan *P : g_plans)
       if (!P->busy && P->n == h->n && P->leaf == h->leaf && P->rank == h->grank && P->nranks == h->nranks &&
-          P->seo == (h->kp.kern == HODLR_SE) && P->cap == h->cap && P->dev == h->dev && P->tbatch == h->tbatch) {
+          P->seo == kv_of(h->kp.kern) && P->cap == h->cap && P->dev == h->dev && P->tbatch == h->tbatch) {
         P->busy = true; return P;
       }
   }
   AcaPlan *P = new AcaPlan();
   P->n = h->n; P->leaf = h->leaf; P->rank = h->grank; P->nranks = h->nranks; P->nb = h->ninternal; P->busy = true;
-  P->seo = h->kp.kern == HODLR_SE; P->cap = h->cap; P->dev = h->dev; P->tbatch = h->tbatch;
+  P->seo = kv_of(h->kp.kern); P->cap = h->cap; P->dev = h->dev; P->tbatch = h->tbatch;
   cudaError_t e = plan_create(P, h);
   if (e != cudaSuccess) { *st = hodlr_cuda_check(e, "aca plan"); return nullptr; }   // (leaked on error)
   std::lock_guard<std::mutex> lk(g_plan_mu);
@@ -840,18 +840,21 @@ hodlr_status hodlr_aca(hodlr_s *h) {
     HCUDA(cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
     const int ns = P->nfused_small, nm = P->nfused_mid, nl = (int)P->fused_blocks.size() - ns - nm;
     if (nl > 0) {       // the large ones first (longest CTAs)
-      if (P->seo) k_aca_fused<true, ACA_SUB, ACA_FUSED_MAX><<<nl, ACA_SUB, 0, h->st2>>>(c, P->d_fused + ns + nm, h->dflags);
-      else k_aca_fused<false, ACA_SUB, ACA_FUSED_MAX><<<nl, ACA_SUB, 0, h->st2>>>(c, P->d_fused + ns + nm, h->dflags);
+      if (P->seo == KV_SE) k_aca_fused<KV_SE, ACA_SUB, ACA_FUSED_MAX><<<nl, ACA_SUB, 0, h->st2>>>(c, P->d_fused + ns + nm, h->dflags);
+      else if (P->seo == KV_M52) k_aca_fused<KV_M52, ACA_SUB, ACA_FUSED_MAX><<<nl, ACA_SUB, 0, h->st2>>>(c, P->d_fused + ns + nm, h->dflags);
+      else k_aca_fused<KV_ANY, ACA_SUB, ACA_FUSED_MAX><<<nl, ACA_SUB, 0, h->st2>>>(c, P->d_fused + ns + nm, h->dflags);
     }
     if (ns + nm > 0) {  // on a second stream: not serialized behind the large blocks' long CTAs
       HCUDA(cudaStreamWaitEvent(h->st2b, h->ev_fork, 0));
       if (nm > 0) {
-        if (P->seo) k_aca_fused<true, 128, ACA_FUSED_MID><<<nm, 128, 0, h->st2b>>>(c, P->d_fused + ns, h->dflags);
-        else k_aca_fused<false, 128, ACA_FUSED_MID><<<nm, 128, 0, h->st2b>>>(c, P->d_fused + ns, h->dflags);
+        if (P->seo == KV_SE) k_aca_fused<KV_SE, 128, ACA_FUSED_MID><<<nm, 128, 0, h->st2b>>>(c, P->d_fused + ns, h->dflags);
+        else if (P->seo == KV_M52) k_aca_fused<KV_M52, 128, ACA_FUSED_MID><<<nm, 128, 0, h->st2b>>>(c, P->d_fused + ns, h->dflags);
+        else k_aca_fused<KV_ANY, 128, ACA_FUSED_MID><<<nm, 128, 0, h->st2b>>>(c, P->d_fused + ns, h->dflags);
       }
       if (ns > 0) {
-        if (P->seo) k_aca_fused<true, 64, ACA_FUSED_SMALL><<<ns, 64, 0, h->st2b>>>(c, P->d_fused, h->dflags);
-        else k_aca_fused<false, 64, ACA_FUSED_SMALL><<<ns, 64, 0, h->st2b>>>(c, P->d_fused, h->dflags);
+        if (P->seo == KV_SE) k_aca_fused<KV_SE, 64, ACA_FUSED_SMALL><<<ns, 64, 0, h->st2b>>>(c, P->d_fused, h->dflags);
+        else if (P->seo == KV_M52) k_aca_fused<KV_M52, 64, ACA_FUSED_SMALL><<<ns, 64, 0, h->st2b>>>(c, P->d_fused, h->dflags);
+        else k_aca_fused<KV_ANY, 64, ACA_FUSED_SMALL><<<ns, 64, 0, h->st2b>>>(c, P->d_fused, h->dflags);
       }
       HCUDA(cudaEventRecord(h->ev_join2, h->st2b));
     }
@@ -865,11 +868,13 @@ hodlr_status hodlr_aca(hodlr_s *h) {
   int hsteps = 0;
   if (nbig > 0 && nograph) {
     for (hsteps = 1; hsteps <= h->cap + 2; hsteps++) {
-      if (P->seo) k_aca_pass<true, true><<<(unsigned)P->nitems_r, ACA_SUB, 0, h->st>>>(P->d_ctx);
-      else k_aca_pass<true, false><<<(unsigned)P->nitems_r, ACA_SUB, 0, h->st>>>(P->d_ctx);
+      if (P->seo == KV_SE) k_aca_pass<true, KV_SE><<<(unsigned)P->nitems_r, ACA_SUB, 0, h->st>>>(P->d_ctx);
+      else if (P->seo == KV_M52) k_aca_pass<true, KV_M52><<<(unsigned)P->nitems_r, ACA_SUB, 0, h->st>>>(P->d_ctx);
+      else k_aca_pass<true, KV_ANY><<<(unsigned)P->nitems_r, ACA_SUB, 0, h->st>>>(P->d_ctx);
       HLAUNCH(h, "k_aca_pass<row>");
-      if (P->seo) k_aca_pass<false, true><<<(unsigned)P->nitems_c, ACA_SUB, 0, h->st>>>(P->d_ctx + 1);
-      else k_aca_pass<false, false><<<(unsigned)P->nitems_c, ACA_SUB, 0, h->st>>>(P->d_ctx + 1);
+      if (P->seo == KV_SE) k_aca_pass<false, KV_SE><<<(unsigned)P->nitems_c, ACA_SUB, 0, h->st>>>(P->d_ctx + 1);
+      else if (P->seo == KV_M52) k_aca_pass<false, KV_M52><<<(unsigned)P->nitems_c, ACA_SUB, 0, h->st>>>(P->d_ctx + 1);
+      else k_aca_pass<false, KV_ANY><<<(unsigned)P->nitems_c, ACA_SUB, 0, h->st>>>(P->d_ctx + 1);
       HLAUNCH(h, "k_aca_pass<col>");
       int act = 0;
       HCUDA(cudaMemcpyAsync(&act, h->dflags + 4, sizeof(int), cudaMemcpyDeviceToHost, h->st));

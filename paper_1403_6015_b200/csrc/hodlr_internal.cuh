@@ -78,9 +78,13 @@ __device__ __forceinline__ double kval(const KParams &kp, double d) {
   else if (kp.kern >= HODLR_IMQ) arg = -kp.alpha * log(fma(d * d, kp.c, 1.0));
   return kp.a2 * pre * exp(arg);
 }
-// SEO: the launch knows the kernel is SE (the bench / config 1, 3, 5 path): exactly the SE code, nothing else inlined
-template <bool SEO> __device__ __forceinline__ double kval_t(const KParams &kp, double d) {
-  if (SEO) return kp.a2 * exp(-(d * d) * kp.c);
+// KV: the kernel family when the launch knows it (KV_SE: the bench / config 1, 3, 5 path; KV_M52: config 4): exactly
+// that code, nothing else inlined; KV_ANY: the run-time switch
+constexpr int KV_ANY = -1, KV_SE = HODLR_SE, KV_M52 = HODLR_MATERN52;
+static inline int kv_of(int kern) { return kern == HODLR_SE ? KV_SE : (kern == HODLR_MATERN52 ? KV_M52 : KV_ANY); }
+template <int KV> __device__ __forceinline__ double kval_t(const KParams &kp, double d) {
+  if (KV == KV_SE) return kp.a2 * exp(-(d * d) * kp.c);
+  if (KV == KV_M52) { const double s = fabs(d) * kp.c; return kp.a2 * (1.0 + s + s * s * (1.0 / 3.0)) * exp(-s); }
   return kval(kp, d);
 }
 
@@ -403,8 +407,14 @@ __device__ __forceinline__ double kval_o(const KParams &kp, double d) {
 __device__ __forceinline__ double kval_o_se(const KParams &kp, double d) {
   return __dmul_rn(kp.a2, exp_cr(-div_exact(__dmul_rn(d, d), kp.c2, kp.rc2)));
 }
-template <bool SEO> __device__ __forceinline__ double kval_ot(const KParams &kp, double d) {
-  if (SEO) return kval_o_se(kp, d);
+__device__ __forceinline__ double kval_o_m52(const KParams &kp, double d) {   // kval_o's Matern-5/2 branch
+  const double s = div_exact(__dmul_rn(kp.sq, fabs(d)), kp.ell, kp.rell);
+  const double p = __dadd_rn(__dadd_rn(1.0, s), __ddiv_rn(__dmul_rn(s, s), 3.0));
+  return __dmul_rn(__dmul_rn(kp.a2, p), exp_cr(-s));
+}
+template <int KV> __device__ __forceinline__ double kval_ot(const KParams &kp, double d) {
+  if (KV == KV_SE) return kval_o_se(kp, d);
+  if (KV == KV_M52) return kval_o_m52(kp, d);
   return kval_o(kp, d);
 }
 

@@ -171,7 +171,7 @@ __device__ unsigned long long g_chol_stamps[2][6];
 template <int P> struct CholCfg {
   static constexpr int NT = P == 64 ? CHOL64_NT : 256, MINB = P == 64 ? 512 / CHOL64_NT : 2;
 };
-template <int P, bool SEO>
+template <int P, int SEO>
 __global__ void __launch_bounds__(CholCfg<P>::NT, CholCfg<P>::MINB) k_leaf_chol(LeafMmaCtx c) {
   constexpr int NTH = CholCfg<P>::NT, NW = NTH / 32;
   constexpr int T = P / 8;
@@ -689,9 +689,9 @@ hodlr_status hodlr_leaf_chol_mma(hodlr_s *h, cudaStream_t stream, bool *launched
     HCUDA(hodlr_allow_smem((const void *)k_leaf_chol<PP, SE_>, h->dev));  \
     k_leaf_chol<PP, SE_><<<(int)(h->nleaves >> h->tsplit), CholCfg<PP>::NT, smem, stream>>>(c);                           \
   } while (0)
-  const bool seo = h->kp.kern == HODLR_SE;
-  if (P == 64) { if (seo) LAUNCH_CHOL(64, true); else LAUNCH_CHOL(64, false); }
-  else { if (seo) LAUNCH_CHOL(128, true); else LAUNCH_CHOL(128, false); }
+  const int kv = kv_of(h->kp.kern);
+  if (P == 64) { if (kv == KV_SE) LAUNCH_CHOL(64, KV_SE); else if (kv == KV_M52) LAUNCH_CHOL(64, KV_M52); else LAUNCH_CHOL(64, KV_ANY); }
+  else { if (kv == KV_SE) LAUNCH_CHOL(128, KV_SE); else if (kv == KV_M52) LAUNCH_CHOL(128, KV_M52); else LAUNCH_CHOL(128, KV_ANY); }
 #undef LAUNCH_CHOL
   HLAUNCH(h, "k_leaf_chol");
 #ifdef CHOL_TRACE
