@@ -15,7 +15,7 @@ HODLR_ACA_NOGRAPH=1 timeout 300 ncu --metrics gpu__time_duration.sum --clock-con
   --log-file $out/launches.csv python tools/prof_step.py cfg3 1 > /dev/null 2>&1
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file $out/launches_graph.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
-for spec in k_aca_pass:24 k_leaf_zsyrk:0 k_leaf_chol:0 k_tree_factor:0 k_solve:0 k_aca_fused:0; do
+for spec in k_aca_pass:24 k_leaf_zsyrk:0 k_leaf_chol:0 k_tree_deep:0 k_tree_top:0 k_solve:0 k_aca_fused:0; do
   k=${spec%%:*}; skip=${spec#*:}
   HODLR_ACA_NOGRAPH=1 timeout 400 ncu --set full --import-source on --clock-control none -k regex:$k --launch-skip $skip -c 1 \
     -o $out/$k python tools/prof_step.py cfg3 1 > $out/$k.log 2>&1
