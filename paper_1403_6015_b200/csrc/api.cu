@@ -223,18 +223,12 @@ static void res_acquire(hodlr_s *h) {
     cudaEventCreateWithFlags(&r.ev_chol, cudaEventDisableTiming);
     int lo_pri = 0, hi_pri = 0;
     cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri);
-    // Fused small-block ACA stream priority (HODLR_FUSED_PRIORITY): 0 lowest (as the leaf Cholesky), 1 the step
-    // loop's (highest), 2 (default, measured best: ACA phase 2.82 -> 2.43 ms) just below the step loop: ahead of the
-    // Cholesky's CTAs, behind the passes
-    static int fused_pri = -1;
-    if (fused_pri < 0) { const char *ev = getenv("HODLR_FUSED_PRIORITY"); fused_pri = ev ? atoi(ev) : 2; }
-    const int pf = fused_pri == 1 ? hi_pri : (fused_pri == 2 ? std::min(lo_pri, hi_pri + 1) : lo_pri);
+    // Stream priorities (measured): the step loop highest; the fused small-block ACA just below it (ahead
+    // of the leaf Cholesky's CTAs, behind the passes: ACA phase 2.82 -> 2.43 ms); the leaf Cholesky lowest
+    const int pf = std::min(lo_pri, hi_pri + 1), pc = lo_pri;
     cudaStreamCreateWithPriority(&r.st2, cudaStreamNonBlocking, pf);
     cudaStreamCreateWithPriority(&r.st2b, cudaStreamNonBlocking, pf);
     cudaEventCreateWithFlags(&r.ev_join2, cudaEventDisableTiming);
-    static int chol_pri = -1;    // HODLR_CHOL_PRIORITY: the leaf Cholesky stream, same encoding
-    if (chol_pri < 0) { const char *ev = getenv("HODLR_CHOL_PRIORITY"); chol_pri = ev ? atoi(ev) : 0; }
-    const int pc = chol_pri == 1 ? hi_pri : (chol_pri == 2 ? std::min(lo_pri, hi_pri + 1) : lo_pri);
     cudaStreamCreateWithPriority(&r.st3, cudaStreamNonBlocking, pc);
     cudaStreamCreateWithPriority(&r.sthi, cudaStreamNonBlocking, hi_pri);
     cudaEventCreateWithFlags(&r.ev_hi, cudaEventDisableTiming);
