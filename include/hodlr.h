@@ -138,8 +138,10 @@ hodlr_status hodlr_factor(hodlr_t h);
  * factorization as an extra panel column -- leaf Z = L^{-1} [y | E] and Pi = Z^T Z give the solve's leaf
  * projections, the coupling tree's T_c = S_c^{-1} B_c and Pi_c give its tree up pass (eq-fac, PAPER.md:1091-1100;
  * equation_Low_Rank_Update) -- then only the solve's down passes run.
- * y: device, n doubles (original order).  x: device, n doubles, receives C^{-1} y (original order), or NULL (no
- * down pass).  quad_host: host double receiving y^T C^{-1} y (the root's Pi; eq. 1), or NULL.
+ * y: device, n doubles (original order).  x: n doubles, receives C^{-1} y (original order), or NULL (no down pass):
+ * device memory, or page-locked host memory (cudaHostAlloc / cudaMallocHost / cudaHostRegister: the solve kernel
+ * writes it through the unified address, so the device-to-host transfer overlaps the leaf phase; pageable host
+ * memory is HODLR_EINVAL).  quad_host: host double receiving y^T C^{-1} y (the root's Pi; eq. 1), or NULL.
  * Leaves the handle factored exactly like hodlr_factor (log det, solve / gp_loglik of other right-hand sides).
  * Errors: as hodlr_factor; HODLR_EINVAL if y has NaN/Inf (the handle is still factored). */
 hodlr_status hodlr_factor_solve(hodlr_t h, const double *y, double *x, double *quad_host);

@@ -629,6 +629,14 @@ hodlr_status hodlr_factor_solve(hodlr_t h, const double *y, double *x, double *q
   if (h->state != 1) return hodlr_set_error(HODLR_ESTATE, "factor_solve: handle is not in the built state");
   h->launches = 0;
   cudaEventRecord(h->ev0, h->st);
+  if (x) {                                   // device or page-locked host memory (written by the solve kernel)
+    cudaPointerAttributes pa;
+    if (cudaPointerGetAttributes(&pa, x) != cudaSuccess || pa.type == cudaMemoryTypeUnregistered || !pa.devicePointer) {
+      cudaGetLastError();
+      return hodlr_set_error(HODLR_EINVAL, "factor_solve: x is neither device nor page-locked host memory");
+    }
+    x = (double *)pa.devicePointer;
+  }
   h->aug = 1; h->y_aug = y;                  // y is column 0 of every leaf panel (leaf_mma.cu, factor.cu)
   hodlr_status st = HODLR_OK;
   cudaError_t ce = cudaMemsetAsync(h->dflags + 3, 0, sizeof(int), h->st);

@@ -182,11 +182,19 @@ def hodlr_factor(h: int):
     _check(load().hodlr_factor(h))
 
 
-def hodlr_factor_solve(h: int, y: torch.Tensor, solve: bool = True):
-    """Fused factor + solve of one right-hand side: returns (C^{-1} y or None, y^T C^{-1} y)."""
+def hodlr_factor_solve(h: int, y: torch.Tensor, solve: bool = True, out: "torch.Tensor | None" = None):
+    """Fused factor + solve of one right-hand side: returns (C^{-1} y or None, y^T C^{-1} y).  out: optional
+    contiguous float64 tensor of n entries for C^{-1} y -- on the device or in pinned host memory (then the solve
+    kernel writes it directly: the device-to-host transfer overlaps the solve)."""
     lib = load()
     y = _dev_f64(y, "y")
-    x = torch.empty_like(y) if solve else None
+    if out is not None:
+        if out.dtype != torch.float64 or not out.is_contiguous() or out.numel() != y.numel() or \
+                (out.device.type != "cuda" and not out.is_pinned()):
+            raise TypeError("out must be a contiguous float64 CUDA or pinned CPU tensor of n entries")
+        x = out
+    else:
+        x = torch.empty_like(y) if solve else None
     q = C.c_double(0.0)
     _check(lib.hodlr_factor_solve(h, y.data_ptr(), x.data_ptr() if x is not None else None, C.byref(q)))
     return x, q.value
@@ -340,9 +348,10 @@ class HODLR:
         hodlr_factor(self._h)
         return self
 
-    def factor_solve(self, y: torch.Tensor, solve: bool = True):
-        """Factor with y fused in; returns (C^{-1} y or None, y^T C^{-1} y).  The handle is then factored."""
-        return hodlr_factor_solve(self._h, y, solve)
+    def factor_solve(self, y: torch.Tensor, solve: bool = True, out: "torch.Tensor | None" = None):
+        """Factor with y fused in; returns (C^{-1} y or None, y^T C^{-1} y).  The handle is then factored.
+        out: optional destination of C^{-1} y (CUDA or pinned CPU tensor)."""
+        return hodlr_factor_solve(self._h, y, solve, out)
 
     def logdet(self) -> float:
         return hodlr_logdet(self._h)

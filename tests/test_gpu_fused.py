@@ -85,3 +85,28 @@ def test_fused_quad_only_and_errors(hb):
         g2.factor_solve(torch.from_numpy(yb).cuda())
     assert e.value.status == "EINVAL"
     assert abs(g2.logdet() - o.logdet()) <= TOL * abs(o.logdet())   # the factorization itself is valid
+
+
+def test_factor_solve_into_pinned_host(hb):
+    """x of hodlr_factor_solve in page-locked host memory (written by the solve kernel through the unified address)
+    equals the device result bit for bit; pageable host memory is refused (include/hodlr.h)."""
+    import numpy as np
+    rng = np.random.default_rng(11)
+    n = 20000
+    x = torch.from_numpy(np.sort(rng.uniform(0, 50, n))).cuda()
+    y = torch.from_numpy(rng.standard_normal(n)).cuda()
+    g = hb.HODLR(x, 0, (1.0, 1.0), 1e-2, 128, 1e-10)
+    sd, qd = g.factor_solve(y)
+    g.close()
+    pin = torch.empty(n, dtype=torch.float64).pin_memory()
+    g = hb.HODLR(x, 0, (1.0, 1.0), 1e-2, 128, 1e-10)
+    sp, qp = g.factor_solve(y, out=pin)
+    g.close()
+    assert sp.data_ptr() == pin.data_ptr() and qp == qd
+    assert torch.equal(pin, sd.cpu())
+    g = hb.HODLR(x, 0, (1.0, 1.0), 1e-2, 128, 1e-10)
+    with pytest.raises(TypeError):
+        g.factor_solve(y, out=torch.empty(n, dtype=torch.float64))          # pageable: refused by the binding
+    arr = np.zeros(n)                                                       # ... and by the C-ABI (HODLR_EINVAL)
+    assert hb.load().hodlr_factor_solve(g._h, y.data_ptr(), arr.ctypes.data, None) == 1
+    g.close()
