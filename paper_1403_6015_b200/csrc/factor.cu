@@ -22,6 +22,9 @@
 #ifndef TREE_PLAIN_LEVELS
 #define TREE_PLAIN_LEVELS 3
 #endif
+#ifndef TREE_DEEP64_SMEM
+#define TREE_DEEP64_SMEM (20 * 1024)   // deep runs whose nodes need at most this run 64-thread CTAs, 11-12 per SM
+#endif
 #ifndef TREE_DEEP_SMEM
 #define TREE_DEEP_SMEM (36 * 1024)  // deep-run levels keep 6 CTAs per SM (their shared memory per node at most this)
 #endif
@@ -355,6 +358,9 @@ __global__ void __launch_bounds__(TT, 3) k_tree_factor(TreeCtx c) {
 #ifndef TREE_PLAIN_LEVELS
 #define TREE_PLAIN_LEVELS 3
 #endif
+#ifndef TREE_DEEP64_SMEM
+#define TREE_DEEP64_SMEM (20 * 1024)   // deep runs whose nodes need at most this run 64-thread CTAs, 11-12 per SM
+#endif
 #ifndef TREE_DEEP_SMEM
 #define TREE_DEEP_SMEM (36 * 1024)  // deep-run levels keep 6 CTAs per SM (their shared memory per node at most this)
 #endif
@@ -376,9 +382,10 @@ __global__ void __launch_bounds__(TT / 2, TREE_NARROW_MINB) k_tree_factor_narrow
 // counter, deepest level first, and a node waits (tree_node) for its children's progress flags, so the partial last
 // wave of one level is filled by the next level's nodes instead of each level's launch ending in a tail.  Deadlock-free:
 // a node only waits for nodes handed out before it (to resident CTAs of the cooperative launch).
-template <bool PIDD>
-__global__ void __launch_bounds__(TT / 2, TREE_NARROW_MINB) k_tree_deep(const TreeCtx *__restrict__ ctxs, int nlev,
-                                                                      unsigned *next) {
+// NTD threads per node: 128, or 64 for runs of small nodes (12 per SM instead of 6: the per-node phases are latency)
+template <bool PIDD, int NTD>
+__global__ void __launch_bounds__(NTD, 768 / NTD) k_tree_deep(const TreeCtx *__restrict__ ctxs, int nlev,
+                                                              unsigned *next) {
   extern __shared__ double sm[];
   __shared__ long long s_j;
   __shared__ int s_L;
@@ -428,17 +435,23 @@ __global__ void __launch_bounds__(LDR_T) k_logdet_reduce(const double *leaf_ld, 
   const int t = threadIdx.x;
   long long per = (N + LDR_T - 1) / LDR_T, v0 = t * per, v1 = v0 + per < N ? v0 + per : N;
   double s = 0.0, comp = 0.0;
-  int d = kappa - 1; long long u = 0;     // (depth, index) of internal value v (depth kappa-1 first), advanced in step
-  if (v0 > nleaves && v0 < v1) { u = v0 - nleaves; while (u >= (1LL << d)) { u -= (1LL << d); d--; } }
-  for (long long v = v0; v < v1; v++) {
-    double x;
-    if (v < nleaves) x = leaf_ld[v];
-    else {
-      x = node_ld[(1LL << d) - 1 + u];
-      if (++u == (1LL << d)) { u = 0; d--; }
-    }
-    neu_add(s, comp, x);
+  // value v: leaf v, then the internal nodes of depth kappa-1 .. tsplit left to right (offset o = v - nleaves lies
+  // in depth d when 2^kappa - 2^(d+1) <= o < 2^kappa - 2^d); 8 loads in flight, folded in order
+  auto val = [&](long long v) -> double {
+    if (v < nleaves) return leaf_ld[v];
+    const long long o = v - nleaves, w = (1LL << kappa) - o;           // 2^d < w <= 2^(d+1)
+    const int d = 63 - __clzll(w - 1);                                // floor(log2(w - 1))
+    return node_ld[(1LL << d) - 1 + (o - ((1LL << kappa) - (2LL << d)))];
+  };
+  long long v = v0;
+  for (; v + 8 <= v1; v += 8) {
+    double x[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) x[k] = val(v + k);
+#pragma unroll
+    for (int k = 0; k < 8; k++) neu_add(s, comp, x[k]);
   }
+  for (; v < v1; v++) neu_add(s, comp, val(v));
   ss[t] = s; cc[t] = comp;
   __syncthreads();
   if (t < 32) {                          // fixed order: lane l folds partials 32l .. 32l+31, lane 0 folds the lanes
@@ -717,12 +730,15 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
       tot += deep[L].cnt;
       anydd = anydd || deep[L].dd;
     }
-    const void *kf = anydd ? (const void *)k_tree_deep<true> : (const void *)k_tree_deep<false>;
+    const bool small = smem <= TREE_DEEP64_SMEM;
+    const int ntd = small ? 64 : TT / 2;
+    const void *kf = small ? (anydd ? (const void *)k_tree_deep<true, 64> : (const void *)k_tree_deep<false, 64>)
+                           : (anydd ? (const void *)k_tree_deep<true, TT / 2> : (const void *)k_tree_deep<false, TT / 2>);
     HCUDA(cudaMemsetAsync(h->d_ready, 0, sizeof(int) * (size_t)(h->ninternal + 2), h->st));
     HCUDA(cudaMemcpyAsync(h->d_treectx, deep.data(), sizeof(TreeCtx) * deep.size(), cudaMemcpyHostToDevice, h->st));
     HCUDA(hodlr_allow_smem(kf, h->dev));
     int per_sm = 0;
-    HCUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, TT / 2, smem));
+    HCUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, ntd, smem));
     if (per_sm < 1) return hodlr_set_error(HODLR_EINVAL, "factor: coupling system too large for one SM");
     long long gmax = (long long)nsm * per_sm;
     if (h->coop_ctas > 0) gmax = std::min<long long>(gmax, h->coop_ctas);
@@ -731,7 +747,7 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
     int nlev = (int)deep.size();
     unsigned *nx = (unsigned *)(h->d_ready + h->ninternal);
     void *args[] = {(void *)&pc, (void *)&nlev, (void *)&nx};
-    HCUDA(cudaLaunchCooperativeKernel(kf, dim3(grid), dim3(TT / 2), args, smem, h->st));
+    HCUDA(cudaLaunchCooperativeKernel(kf, dim3(grid), dim3(ntd), args, smem, h->st));
     HLAUNCH(h, "k_tree_deep");
     deep.clear();
     return HODLR_OK;

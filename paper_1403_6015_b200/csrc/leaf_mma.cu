@@ -168,8 +168,11 @@ __device__ unsigned long long g_chol_stamps[2][6];
 #ifndef CHOL64_NT
 #define CHOL64_NT 64
 #endif
+#ifndef CHOL64_MINB
+#define CHOL64_MINB (512 / CHOL64_NT)
+#endif
 template <int P> struct CholCfg {
-  static constexpr int NT = P == 64 ? CHOL64_NT : 256, MINB = P == 64 ? 512 / CHOL64_NT : 2;
+  static constexpr int NT = P == 64 ? CHOL64_NT : 256, MINB = P == 64 ? CHOL64_MINB : 2;
 };
 template <int P, int SEO>
 __global__ void __launch_bounds__(CholCfg<P>::NT, CholCfg<P>::MINB) k_leaf_chol(LeafMmaCtx c) {
