@@ -129,6 +129,22 @@ hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const 
                          double sigma2, int32_t leaf, double eps, const hodlr_dist *dist,
                          const hodlr_opts *opts, void *cuda_stream, hodlr_t *out);
 
+/* NEXT-3, d-dimensional points ("points in one, two, or three dimensions", Table II
+ * PAPER.md:1302-1351).  Same "Assembly" as hodlr_build with the kd ordering of PAPER.md:666-677 ("sorted
+ * recursively, one dimension at a time") as DESIGN.md R19 reads it: every depth-L node (L < max(kappa, 1), top
+ * down) sorts its points stably by coordinate L mod dim before the count-median split; kernel entries are the
+ * Table I functions of the Euclidean distance |x_i - x_j| (SE from its square).  x: device, n x dim row-major
+ * (point i at x[i * dim .. i * dim + dim)).  1 <= dim <= 64 (dim = 1 is hodlr_build, bit for bit).  One GPU,
+ * unbatched (no dist); noise, forced_ranks and rank_cap in opts as for hodlr_build.  The rest of the path (factor,
+ * logdet, solve, factor_solve, gp_loglik, apply) is unchanged; gp_predict refuses d > 1 (HODLR_EINVAL).
+ * hodlr_get_order returns the sorted points coordinate-major (dim x n: coordinate k of sorted point i at
+ * xs[k * n + i]).  Limits: the ranks must meet eps within the rank cap (<= 64, else HODLR_ERANKCAP) and each
+ * coupling system's on-chip working set must fit one SM (else HODLR_EINVAL at factor) -- 2-D problems of moderate
+ * smoothness do; the paper's Table II 2-D/3-D settings, with ranks in the hundreds, do not. */
+hodlr_status hodlr_build_nd(const double *x, int64_t n, int32_t dim, hodlr_kernel kernel, const double *theta,
+                            double sigma2, int32_t leaf, double eps, const hodlr_opts *opts, void *cuda_stream,
+                            hodlr_t *out);
+
 /* "Factor" (Fig. 6): leaf Cholesky of K_kappa, bottom-up SMW coupling systems
  * S_c = [[I, V^T K_c2^{-1} V], [U^T K_c1^{-1} U, I]] (equation_Low_Rank_Update)
  * and their LU factors; accumulates log det C. */
@@ -216,7 +232,7 @@ hodlr_status gp_loglik_sweep(const double *x, const double *y, int64_t n, hodlr_
 /* Sizes, ranks and phase times.  info: host struct. */
 hodlr_status hodlr_info(hodlr_t h, hodlr_info_t *info);
 
-/* Copy the sorted points (n doubles) and the permutation perm[i] = original index of sorted
+/* Copy the sorted points (n doubles; dim x n coordinate-major for a hodlr_build_nd handle) and the permutation perm[i] = original index of sorted
  * position i (n int64) to DEVICE buffers; either may be NULL.  For parity tests (bit-exact). */
 hodlr_status hodlr_get_order(hodlr_t h, double *xs_dev, int64_t *perm_dev);
 

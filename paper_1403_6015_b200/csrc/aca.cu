@@ -27,10 +27,10 @@ namespace {
 // Rows with the same coordinate as a used pivot row have identical residual rows: mark the whole
 // run of equal sorted coordinates inside c1 as used (R2).  Single thread.
 __device__ void mark_row_run(const AcaCtx &c, unsigned char *used, long long lo1, long long m1, long long ik) {
-  const double v = c.xs[lo1 + ik];
-  used[lo1 + ik] = 1;
-  for (long long i = ik - 1; i >= 0 && c.xs[lo1 + i] == v; i--) used[lo1 + i] = 1;
-  for (long long i = ik + 1; i < m1 && c.xs[lo1 + i] == v; i++) used[lo1 + i] = 1;
+  const long long p = lo1 + ik;
+  used[p] = 1;
+  for (long long i = ik - 1; i >= 0 && pt_eq(c.kp, c.xs, lo1 + i, p); i--) used[lo1 + i] = 1;
+  for (long long i = ik + 1; i < m1 && pt_eq(c.kp, c.xs, lo1 + i, p); i++) used[lo1 + i] = 1;
 }
 
 __global__ void k_aca_init(AcaCtx c, int nblocks, int cap) {
@@ -192,7 +192,7 @@ __device__ __forceinline__ void aca_item(const AcaCtx &c, int item, AcaScratch &
   // vector path: thread t takes the ACA_E consecutive elements of each ACA_TILE-element sub-tile (double2
   // loads/stores); needs 16-byte alignment of every column segment (n and the chunk start even) -- the
   // scalar loop below handles the rest
-  const bool vec = ((ldx | (lo + it.start)) & 1) == 0 && (ilen % ACA_E) == 0;
+  const bool vec = SEO != KV_ND && ((ldx | (lo + it.start)) & 1) == 0 && (ilen % ACA_E) == 0;
   constexpr int NP = ACA_E / 2;                  // double2 pairs per thread
   constexpr int LS = 4;                          // factor columns per batch of loads
   if (vec) {
@@ -293,7 +293,8 @@ __device__ __forceinline__ void aca_item(const AcaCtx &c, int item, AcaScratch &
     for (int q = 0; q < ACA_E; q++) {
       const double xq = q < nval ? xsp[q * ACA_SUB] : xp;
       if (q < nval && up[q * ACA_SUB]) usedm |= 1u << q;
-      r[q] = q < nval ? kval_ot<SEO>(kp, ROW ? xp - xq : xq - xp) : 0.0;
+      r[q] = q < nval ? (SEO == KV_ND ? kval_nd(kp, c.xs, pg, g0 + q * ACA_SUB) : kval_ot<SEO>(kp, ROW ? xp - xq : xq - xp))
+                      : 0.0;
       Fk[q] = 0.0;
     }
     if (k > 0) {                               // the newest column, normalised and stored back by the row pass
@@ -496,8 +497,10 @@ __global__ void __launch_bounds__(NT) k_aca_fused(AcaCtx c, const int *blocks, i
   __syncthreads();
   if (t == 0) {
     s_k = 0; s_done = 0; s_S2 = 0.0; s_ipiv = m1 - 1;
-    const double v = c.xs[lo1 + m1 - 1];          // mark the run of the first pivot row (R2)
-    for (long long i = m1 - 1; i >= 0 && c.xs[lo1 + i] == v; i--) usedR[i] = 1;
+    // mark the run of the first pivot row (R2)
+    const double v = c.xs[lo1 + m1 - 1];
+    for (long long i = m1 - 1; i >= 0 && (SEO == KV_ND ? pt_eq(c.kp, c.xs, lo1 + i, lo1 + m1 - 1) : c.xs[lo1 + i] == v); i--)
+      usedR[i] = 1;
   }
   __syncthreads();
   for (;;) {
@@ -516,7 +519,7 @@ __global__ void __launch_bounds__(NT) k_aca_fused(AcaCtx c, const int *blocks, i
 #pragma unroll
       for (int u = 0; u < FU; u++) {
         const long long j = j0 + u * NT;
-        v[u] = j < m2 ? kval_ot<SEO>(kp, xi - c.xs[lo2 + j]) : 0.0;
+        v[u] = j < m2 ? (SEO == KV_ND ? kval_nd(kp, c.xs, ig, lo2 + j) : kval_ot<SEO>(kp, xi - c.xs[lo2 + j])) : 0.0;
       }
       for (int l = 0; l < k; l++) {
         const double ul = Ui[l];
@@ -568,7 +571,7 @@ __global__ void __launch_bounds__(NT) k_aca_fused(AcaCtx c, const int *blocks, i
 #pragma unroll
       for (int u = 0; u < FU; u++) {
         const long long i = i0 + u * NT;
-        w[u] = i < m1 ? kval_ot<SEO>(kp, c.xs[lo1 + i] - xj) : 0.0;
+        w[u] = i < m1 ? (SEO == KV_ND ? kval_nd(kp, c.xs, lo1 + i, jg) : kval_ot<SEO>(kp, c.xs[lo1 + i] - xj)) : 0.0;
       }
       for (int l = 0; l < k; l++) {
         const double ul = Ui[l];
@@ -617,8 +620,13 @@ __global__ void __launch_bounds__(NT) k_aca_fused(AcaCtx c, const int *blocks, i
         s_ipiv = bi;
         const double v = c.xs[lo1 + bi];
         usedR[bi] = 1;
-        for (long long i = bi - 1; i >= 0 && c.xs[lo1 + i] == v; i--) usedR[i] = 1;
-        for (long long i = bi + 1; i < m1 && c.xs[lo1 + i] == v; i++) usedR[i] = 1;
+        if (SEO == KV_ND) {
+          for (long long i = bi - 1; i >= 0 && pt_eq(c.kp, c.xs, lo1 + i, lo1 + bi); i--) usedR[i] = 1;
+          for (long long i = bi + 1; i < m1 && pt_eq(c.kp, c.xs, lo1 + i, lo1 + bi); i++) usedR[i] = 1;
+        } else {
+          for (long long i = bi - 1; i >= 0 && c.xs[lo1 + i] == v; i--) usedR[i] = 1;
+          for (long long i = bi + 1; i < m1 && c.xs[lo1 + i] == v; i++) usedR[i] = 1;
+        }
       }
       s_done = done;
     }
@@ -626,6 +634,16 @@ __global__ void __launch_bounds__(NT) k_aca_fused(AcaCtx c, const int *blocks, i
     if (s_done) break;
   }
   if (t == 0) c.rank[b] = s_k;
+}
+
+// Launch families (kv_of_kp): SE / Matern-5/2 specialisations, any 1-D kernel, d-dimensional points (NEXT-3)
+template <bool ROW> static void *pass_fn(int seo) {
+  return seo == KV_SE ? (void *)k_aca_pass<ROW, KV_SE> : seo == KV_M52 ? (void *)k_aca_pass<ROW, KV_M52>
+       : seo == KV_ND ? (void *)k_aca_pass<ROW, KV_ND> : (void *)k_aca_pass<ROW, KV_ANY>;
+}
+template <int NT, int MAXS> static void (*fused_fn(int seo))(AcaCtx, const int *, int *) {
+  return seo == KV_SE ? k_aca_fused<KV_SE, NT, MAXS> : seo == KV_M52 ? k_aca_fused<KV_M52, NT, MAXS>
+       : seo == KV_ND ? k_aca_fused<KV_ND, NT, MAXS> : k_aca_fused<KV_ANY, NT, MAXS>;
 }
 
 // Device-side loop control for the conditional-while CUDA graph: keep iterating while big blocks are
@@ -747,12 +765,12 @@ static cudaError_t plan_create(AcaPlan *P, const hodlr_s *h) {
   if (e == cudaSuccess) {
     cudaGraph_t body = cpar.conditional.phGraph_out[0];
     cudaKernelNodeParams k1 = {};
-    k1.func = P->seo == KV_SE ? (void *)k_aca_pass<true, KV_SE> : P->seo == KV_M52 ? (void *)k_aca_pass<true, KV_M52> : (void *)k_aca_pass<true, KV_ANY>; k1.gridDim = dim3((unsigned)P->nitems_r); k1.blockDim = dim3(ACA_SUB);
+    k1.func = pass_fn<true>(P->seo); k1.gridDim = dim3((unsigned)P->nitems_r); k1.blockDim = dim3(ACA_SUB);
     k1.kernelParams = arow;
     e = cudaGraphAddKernelNode(&n1, body, nullptr, 0, &k1);
     if (e == cudaSuccess) {
       cudaKernelNodeParams k2 = {};
-      k2.func = P->seo == KV_SE ? (void *)k_aca_pass<false, KV_SE> : P->seo == KV_M52 ? (void *)k_aca_pass<false, KV_M52> : (void *)k_aca_pass<false, KV_ANY>; k2.gridDim = dim3((unsigned)P->nitems_c); k2.blockDim = dim3(ACA_SUB);
+      k2.func = pass_fn<false>(P->seo); k2.gridDim = dim3((unsigned)P->nitems_c); k2.blockDim = dim3(ACA_SUB);
       k2.kernelParams = acol;
       e = cudaGraphAddKernelNode(&n2, body, &n1, 1, &k2);
     }
@@ -773,13 +791,13 @@ static AcaPlan *plan_acquire(const hodlr_s *h, hodlr_status *st) {
     std::lock_guard<std::mutex> lk(g_plan_mu);
     for (AcaPlan *P : g_plans)
       if (!P->busy && P->n == h->n && P->leaf == h->leaf && P->rank == h->grank && P->nranks == h->nranks &&
-          P->seo == kv_of(h->kp.kern) && P->cap == h->cap && P->dev == h->dev && P->tbatch == h->tbatch) {
+          P->seo == kv_of_kp(h->kp) && P->cap == h->cap && P->dev == h->dev && P->tbatch == h->tbatch) {
         P->busy = true; return P;
       }
   }
   AcaPlan *P = new AcaPlan();
   P->n = h->n; P->leaf = h->leaf; P->rank = h->grank; P->nranks = h->nranks; P->nb = h->ninternal; P->busy = true;
-  P->seo = kv_of(h->kp.kern); P->cap = h->cap; P->dev = h->dev; P->tbatch = h->tbatch;
+  P->seo = kv_of_kp(h->kp); P->cap = h->cap; P->dev = h->dev; P->tbatch = h->tbatch;
   cudaError_t e = plan_create(P, h);
   if (e != cudaSuccess) { *st = hodlr_cuda_check(e, "aca plan"); return nullptr; }   // (leaked on error)
   std::lock_guard<std::mutex> lk(g_plan_mu);
@@ -840,21 +858,24 @@ hodlr_status hodlr_aca(hodlr_s *h) {
     HCUDA(cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
     const int ns = P->nfused_small, nm = P->nfused_mid, nl = (int)P->fused_blocks.size() - ns - nm;
     if (nl > 0) {       // the large ones first (longest CTAs)
-      if (P->seo == KV_SE) k_aca_fused<KV_SE, ACA_SUB, ACA_FUSED_MAX><<<nl, ACA_SUB, 0, h->st2>>>(c, P->d_fused + ns + nm, h->dflags);
-      else if (P->seo == KV_M52) k_aca_fused<KV_M52, ACA_SUB, ACA_FUSED_MAX><<<nl, ACA_SUB, 0, h->st2>>>(c, P->d_fused + ns + nm, h->dflags);
-      else k_aca_fused<KV_ANY, ACA_SUB, ACA_FUSED_MAX><<<nl, ACA_SUB, 0, h->st2>>>(c, P->d_fused + ns + nm, h->dflags);
+      {
+        void (*f)(AcaCtx, const int *, int *) = fused_fn<ACA_SUB, ACA_FUSED_MAX>(P->seo);
+        f<<<nl, ACA_SUB, 0, h->st2>>>(c, P->d_fused + ns + nm, h->dflags);
+      }
     }
     if (ns + nm > 0) {  // on a second stream: not serialized behind the large blocks' long CTAs
       HCUDA(cudaStreamWaitEvent(h->st2b, h->ev_fork, 0));
       if (nm > 0) {
-        if (P->seo == KV_SE) k_aca_fused<KV_SE, 128, ACA_FUSED_MID><<<nm, 128, 0, h->st2b>>>(c, P->d_fused + ns, h->dflags);
-        else if (P->seo == KV_M52) k_aca_fused<KV_M52, 128, ACA_FUSED_MID><<<nm, 128, 0, h->st2b>>>(c, P->d_fused + ns, h->dflags);
-        else k_aca_fused<KV_ANY, 128, ACA_FUSED_MID><<<nm, 128, 0, h->st2b>>>(c, P->d_fused + ns, h->dflags);
+        {
+          void (*f)(AcaCtx, const int *, int *) = fused_fn<128, ACA_FUSED_MID>(P->seo);
+          f<<<nm, 128, 0, h->st2b>>>(c, P->d_fused + ns, h->dflags);
+        }
       }
       if (ns > 0) {
-        if (P->seo == KV_SE) k_aca_fused<KV_SE, 64, ACA_FUSED_SMALL><<<ns, 64, 0, h->st2b>>>(c, P->d_fused, h->dflags);
-        else if (P->seo == KV_M52) k_aca_fused<KV_M52, 64, ACA_FUSED_SMALL><<<ns, 64, 0, h->st2b>>>(c, P->d_fused, h->dflags);
-        else k_aca_fused<KV_ANY, 64, ACA_FUSED_SMALL><<<ns, 64, 0, h->st2b>>>(c, P->d_fused, h->dflags);
+        {
+          void (*f)(AcaCtx, const int *, int *) = fused_fn<64, ACA_FUSED_SMALL>(P->seo);
+          f<<<ns, 64, 0, h->st2b>>>(c, P->d_fused, h->dflags);
+        }
       }
       HCUDA(cudaEventRecord(h->ev_join2, h->st2b));
     }
@@ -868,13 +889,9 @@ hodlr_status hodlr_aca(hodlr_s *h) {
   int hsteps = 0;
   if (nbig > 0 && nograph) {
     for (hsteps = 1; hsteps <= h->cap + 2; hsteps++) {
-      if (P->seo == KV_SE) k_aca_pass<true, KV_SE><<<(unsigned)P->nitems_r, ACA_SUB, 0, h->st>>>(P->d_ctx);
-      else if (P->seo == KV_M52) k_aca_pass<true, KV_M52><<<(unsigned)P->nitems_r, ACA_SUB, 0, h->st>>>(P->d_ctx);
-      else k_aca_pass<true, KV_ANY><<<(unsigned)P->nitems_r, ACA_SUB, 0, h->st>>>(P->d_ctx);
+      ((void (*)(const AcaCtx *))pass_fn<true>(P->seo))<<<(unsigned)P->nitems_r, ACA_SUB, 0, h->st>>>(P->d_ctx);
       HLAUNCH(h, "k_aca_pass<row>");
-      if (P->seo == KV_SE) k_aca_pass<false, KV_SE><<<(unsigned)P->nitems_c, ACA_SUB, 0, h->st>>>(P->d_ctx + 1);
-      else if (P->seo == KV_M52) k_aca_pass<false, KV_M52><<<(unsigned)P->nitems_c, ACA_SUB, 0, h->st>>>(P->d_ctx + 1);
-      else k_aca_pass<false, KV_ANY><<<(unsigned)P->nitems_c, ACA_SUB, 0, h->st>>>(P->d_ctx + 1);
+      ((void (*)(const AcaCtx *))pass_fn<false>(P->seo))<<<(unsigned)P->nitems_c, ACA_SUB, 0, h->st>>>(P->d_ctx + 1);
       HLAUNCH(h, "k_aca_pass<col>");
       int act = 0;
       HCUDA(cudaMemcpyAsync(&act, h->dflags + 4, sizeof(int), cudaMemcpyDeviceToHost, h->st));

@@ -319,7 +319,7 @@ __global__ void k_replicate_order(double *xs, long long *perm, long long nseg, i
 }
 
 // hodlr_build (B = 1) and hodlr_build_batch (B = 2^t problems on the same points): one implementation.
-static hodlr_status build_impl(const double *x, int64_t nseg, int32_t B, hodlr_kernel kernel, const double *thetas,
+static hodlr_status build_impl(const double *x, int64_t nseg, int32_t dim, int32_t B, hodlr_kernel kernel, const double *thetas,
                                int tstride, const double *sigma2s, int32_t leaf, double eps, const hodlr_dist *dist,
                                const hodlr_opts *opts, void *cuda_stream, hodlr_t *out) {
   if (!out) return hodlr_set_error(HODLR_EINVAL, "build: out is NULL");
@@ -333,6 +333,9 @@ static hodlr_status build_impl(const double *x, int64_t nseg, int32_t B, hodlr_k
   if (nonspd && (B > 1 || (dist && dist->nranks > 1)))
     return hodlr_set_error(HODLR_EINVAL, "build: MQ / BIHARM (not positive definite) run on one GPU, unbatched");
   if (B < 1 || (B & (B - 1))) return hodlr_set_error(HODLR_EINVAL, "build_batch: B = %d is not a power of two", B);
+  if (dim < 1 || dim > 64) return hodlr_set_error(HODLR_EINVAL, "build_nd: dim = %d not in [1, 64]", dim);
+  if (dim > 1 && (B > 1 || (dist && dist->nranks > 1)))
+    return hodlr_set_error(HODLR_EINVAL, "build_nd: d-dimensional points run on one GPU, unbatched (NEXT-3)");
   if (B > 1 && nseg < leaf) return hodlr_set_error(HODLR_EINVAL, "build_batch: n = %lld < leaf = %d", (long long)nseg, leaf);
   if (B > 1 && ((dist && dist->nranks > 1) || (opts && opts->noise)))
     return hodlr_set_error(HODLR_EINVAL, "build_batch: no dist or noise on batched handles");
@@ -359,6 +362,8 @@ static hodlr_status build_impl(const double *x, int64_t nseg, int32_t B, hodlr_k
   h->launches = 0;
   h->n = n; h->leaf = leaf; h->eps = eps; h->cap = cap; h->theta[0] = theta[0]; h->theta[1] = theta[1];
   h->kp = make_kp(kernel, theta, sigma2);
+  h->kp.dim = dim; h->kp.ldp = n;             // coordinate-major points (NEXT-3; 1-D: one row)
+  h->dim = dim;
   h->nonspd = nonspd ? 1 : 0;
   h->nbatch = B; h->nseg = nseg;
   h->tbatch = 0;
@@ -394,7 +399,7 @@ static hodlr_status build_impl(const double *x, int64_t nseg, int32_t B, hodlr_k
     cols += h->dt.capd[e];
   }
   h->xh_cols = cols;
-  h->xs = (double *)hodlr_dalloc(h, sizeof(double) * n);
+  h->xs = (double *)hodlr_dalloc(h, sizeof(double) * n * dim);
   h->perm = (long long *)hodlr_dalloc(h, sizeof(long long) * n);
   h->lo = (long long *)hodlr_dalloc(h, sizeof(long long) * h->nnodes);
   h->hi = (long long *)hodlr_dalloc(h, sizeof(long long) * h->nnodes);
@@ -428,7 +433,7 @@ static hodlr_status build_impl(const double *x, int64_t nseg, int32_t B, hodlr_k
   CK(cudaMemcpyAsync(h->hi, h->h_hi, sizeof(long long) * h->nnodes, cudaMemcpyHostToDevice, h->st));
   CK(cudaMemcpyAsync(h->d_dt, &h->dt, sizeof(DepthTab), cudaMemcpyHostToDevice, h->st));
   hodlr_trace("build: enter");
-  st = hodlr_sort_and_tree(h, x, nseg);
+  st = dim > 1 ? hodlr_kd_sort(h, x, nseg, dim) : hodlr_sort_and_tree(h, x, nseg);
   hodlr_trace("build: sort issued");
   if (st != HODLR_OK) goto fail;
   if (B > 1) {     // batched: every problem has problem 0's order; per-problem parameters on the device
@@ -439,7 +444,10 @@ static hodlr_status build_impl(const double *x, int64_t nseg, int32_t B, hodlr_k
     }
     h->launches++; hodlr_global_launches++;
     std::vector<KParams> kps(B);
-    for (int b = 0; b < B; b++) kps[b] = make_kp(kernel, thetas + (size_t)b * tstride, sigma2s[b]);
+    for (int b = 0; b < B; b++) {
+      kps[b] = make_kp(kernel, thetas + (size_t)b * tstride, sigma2s[b]);
+      kps[b].dim = 1; kps[b].ldp = n;
+    }
     h->d_kps = (KParams *)hodlr_dalloc(h, sizeof(KParams) * B);
     if (!h->d_kps) { st = hodlr_set_error(HODLR_ENOMEM, "build: device allocation failed"); goto fail; }
     CK(cudaMemcpyAsync(h->d_kps, kps.data(), sizeof(KParams) * B, cudaMemcpyHostToDevice, h->st));
@@ -564,13 +572,19 @@ fail:
 hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const double *theta, double sigma2,
                          int32_t leaf, double eps, const hodlr_dist *dist, const hodlr_opts *opts, void *cuda_stream,
                          hodlr_t *out) {
-  return build_impl(x, n, 1, kernel, theta, 0, &sigma2, leaf, eps, dist, opts, cuda_stream, out);
+  return build_impl(x, n, 1, 1, kernel, theta, 0, &sigma2, leaf, eps, dist, opts, cuda_stream, out);
+}
+
+hodlr_status hodlr_build_nd(const double *x, int64_t n, int32_t dim, hodlr_kernel kernel, const double *theta,
+                            double sigma2, int32_t leaf, double eps, const hodlr_opts *opts, void *cuda_stream,
+                            hodlr_t *out) {
+  return build_impl(x, n, dim, 1, kernel, theta, 0, &sigma2, leaf, eps, nullptr, opts, cuda_stream, out);
 }
 
 hodlr_status hodlr_build_batch(const double *x, int64_t n, hodlr_kernel kernel, const double *thetas,
                                const double *sigma2s, int32_t B, int32_t leaf, double eps, const hodlr_opts *opts,
                                void *cuda_stream, hodlr_t *out) {
-  return build_impl(x, n, B, kernel, thetas, kernel == HODLR_RQ ? 3 : 2, sigma2s, leaf, eps, nullptr, opts,
+  return build_impl(x, n, 1, B, kernel, thetas, kernel == HODLR_RQ ? 3 : 2, sigma2s, leaf, eps, nullptr, opts,
                     cuda_stream, out);
 }
 
@@ -730,6 +744,7 @@ hodlr_status gp_predict(hodlr_t h, const double *y, const double *xt, int64_t m,
   if (h->state != 2) return hodlr_set_error(HODLR_ESTATE, "predict: not factored");
   if (h->nranks > 1) return hodlr_set_error(HODLR_EINVAL, "predict: sharded handles are not supported");
   if (h->nonspd && var) return hodlr_set_error(HODLR_EINVAL, "predict: no variance for a kernel that is not positive definite");
+  if (h->dim > 1) return hodlr_set_error(HODLR_EINVAL, "predict: 1-D handles only (NEXT-3 covers build / factor / solve / apply)");
   h->launches = 0;
   cudaEventRecord(h->ev0, h->st);
   hodlr_status st = hodlr_predict_impl(h, y, xt, m, mean, var);
@@ -802,7 +817,7 @@ hodlr_status hodlr_info(hodlr_t h, hodlr_info_t *info) {
 
 hodlr_status hodlr_get_order(hodlr_t h, double *xs_dev, int64_t *perm_dev) {
   if (!h) return hodlr_set_error(HODLR_EINVAL, "get_order: NULL handle");
-  if (xs_dev) { cudaError_t e = cudaMemcpyAsync(xs_dev, h->xs, sizeof(double) * h->n, cudaMemcpyDeviceToDevice, h->st); if (e) return hodlr_cuda_check(e, "get_order"); }
+  if (xs_dev) { cudaError_t e = cudaMemcpyAsync(xs_dev, h->xs, sizeof(double) * h->n * h->dim, cudaMemcpyDeviceToDevice, h->st); if (e) return hodlr_cuda_check(e, "get_order"); }
   if (perm_dev) { cudaError_t e = cudaMemcpyAsync(perm_dev, h->perm, sizeof(long long) * h->n, cudaMemcpyDeviceToDevice, h->st); if (e) return hodlr_cuda_check(e, "get_order"); }
   cudaError_t e = cudaStreamSynchronize(h->st);
   return e == cudaSuccess ? HODLR_OK : hodlr_cuda_check(e, "get_order");

@@ -63,7 +63,8 @@ __global__ void __launch_bounds__(AT) k_apply_leaf_up(ApplyCtx c) {
   for (int i = t; i < m; i += AT) {
     const double xi = sx[i];
     double s = 0.0;
-    for (int j = 0; j < m; j++) s = fma(kval(kp, xi - sx[j]), sv[j], s);
+    if (kp.dim > 1) for (int j = 0; j < m; j++) s = fma(kval_nd(kp, c.xs, lo + i, lo + j), sv[j], s);   // NEXT-3
+    else for (int j = 0; j < m; j++) s = fma(kval(kp, xi - sx[j]), sv[j], s);
     c.ys[lo + i] = fma(sig2(kp, lo + i), sv[i], s);
   }
   // P_l = E_l^T x_l: a warp takes 4 consecutive panel columns at once (lanes over rows, every load of a 128-row

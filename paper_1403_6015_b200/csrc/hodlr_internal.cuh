@@ -45,6 +45,8 @@ struct KParams {
   double rc2, rell;         // 1 / c2, 1 / ell when that reciprocal is exact (a power of two: x / c == x * (1 / c)
                             // bit for bit, and a multiply is far cheaper than a division), else 0
   const double *dn;         // heteroscedastic noise: sigma_i^2 = s2 + noise_i in SORTED order (device), or NULL
+  int dim;                  // point dimension d (NEXT-3): xs holds coordinate k of sorted point i at xs[k * ldp + i]
+  long long ldp;            // coordinate stride of xs (= n; 1-D: the single coordinate row)
 };
 // the diagonal term sigma_i^2 of sorted point i (C_ij = sigma_i^2 delta_ij + k(x_i, x_j))
 __device__ __forceinline__ double sig2(const KParams &kp, long long i) { return kp.dn ? kp.dn[i] : kp.s2; }
@@ -233,6 +235,7 @@ struct hodlr_s {
   DepthTab *d_dt;
   // factor storage
   double *Lf; long long lstride; int ltiles;   // leaf factor tiles (see storage helpers)
+  int dim;                   // point dimension (NEXT-3; xs is coordinate-major, dim x n)
   int nonspd;                // MQ / BIHARM: LU leaves, either sign (R20)
   int det_sign;              // sign of det C after the factorization (+1 for the SPD kernels)
   double *Uf; int *lperm;    // LU leaves: U^{-T} tiles (as Lf) and the row order P (8 ltiles ints per leaf)
@@ -279,6 +282,7 @@ extern long long hodlr_global_launches;
 
 // phase entry points (one per .cu file)
 hodlr_status hodlr_sort_and_tree(hodlr_s *h, const double *x, long long n);   // sorts n <= h->n points
+hodlr_status hodlr_kd_sort(hodlr_s *h, const double *x, long long n, int dim);   // NEXT-3: kd ordering, d > 1
 hodlr_status hodlr_aca(hodlr_s *h);
 hodlr_status hodlr_factor_impl(hodlr_s *h);
 hodlr_status hodlr_batch_parts(hodlr_s *h, double *d_out);   // batched: per-problem log det [B] and y^T C^-1 y [B]
@@ -416,6 +420,36 @@ template <int KV> __device__ __forceinline__ double kval_ot(const KParams &kp, d
   if (KV == KV_SE) return kval_o_se(kp, d);
   if (KV == KV_M52) return kval_o_m52(kp, d);
   return kval_o(kp, d);
+}
+
+// ----------------------------------------------------------------------------------------------
+// NEXT-3: d-dimensional points ("points in one, two, or three dimensions", Table II; DESIGN.md
+// R19).  Launches on such a handle are the KV_ND instantiations: entries are the Table I functions of the Euclidean
+// distance, from the squared distance r2 = sum_k (x_ik - x_jk)^2 summed in coordinate order (SE uses r2 directly,
+// the others r = sqrt(r2)), in the oracle's operation order (its oracle_kernel_r2).  Coordinate-major points:
+// a warp reading consecutive sorted points reads consecutive addresses of each coordinate row.
+// ----------------------------------------------------------------------------------------------
+constexpr int KV_ND = -2;
+__device__ __forceinline__ double pt_r2(const KParams &kp, const double *xs, long long i, long long j) {
+  double r2 = 0.0;
+  for (int k = 0; k < kp.dim; k++) {
+    const double d = __dsub_rn(xs[k * kp.ldp + i], xs[k * kp.ldp + j]);
+    r2 = __dadd_rn(r2, __dmul_rn(d, d));
+  }
+  return r2;
+}
+__device__ __forceinline__ double kval_nd(const KParams &kp, const double *xs, long long i, long long j) {
+  const double r2 = pt_r2(kp, xs, i, j);
+  if (kp.kern == HODLR_SE) return __dmul_rn(kp.a2, exp_cr(-div_exact(r2, kp.c2, kp.rc2)));
+  return kval_o(kp, __dsqrt_rn(r2));
+}
+// the launch family of a handle: KV_ND for d > 1, else the kernel family's specialisation
+static inline int kv_of_kp(const KParams &kp) { return kp.dim > 1 ? KV_ND : kv_of(kp.kern); }
+// sorted points i and j coincide (every coordinate equal; 1-D: xs[i] == xs[j]) -- the duplicate-row rule (R2)
+__device__ __forceinline__ bool pt_eq(const KParams &kp, const double *xs, long long i, long long j) {
+  for (int k = 0; k < kp.dim; k++)
+    if (xs[k * kp.ldp + i] != xs[k * kp.ldp + j]) return false;
+  return true;
 }
 
 // ----------------------------------------------------------------------------------------------

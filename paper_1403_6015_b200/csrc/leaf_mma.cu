@@ -204,7 +204,10 @@ __global__ void __launch_bounds__(CholCfg<P>::NT, CholCfg<P>::MINB) k_leaf_chol(
       const int r = lane >> 2, cc = (lane & 3) + 4 * h;
       const int i = 8 * I + r, j = 8 * J + cc;
       double v;
-      if (i < m && j < m) { v = kval_t<SEO>(kp, sx[i] - sx[j]); if (i == j) v += sig2(kp, lo + i); }
+      if (i < m && j < m) {
+        v = SEO == KV_ND ? kval_nd(kp, c.xs, lo + i, lo + j) : kval_t<SEO>(kp, sx[i] - sx[j]);
+        if (i == j) v += sig2(kp, lo + i);
+      }
       else v = (i == j) ? 1.0 : 0.0;
       sL[ti * 64 + 32 * h + lane] = v;
     }
@@ -692,9 +695,14 @@ hodlr_status hodlr_leaf_chol_mma(hodlr_s *h, cudaStream_t stream, bool *launched
     HCUDA(hodlr_allow_smem((const void *)k_leaf_chol<PP, SE_>, h->dev));  \
     k_leaf_chol<PP, SE_><<<(int)(h->nleaves >> h->tsplit), CholCfg<PP>::NT, smem, stream>>>(c);                           \
   } while (0)
-  const int kv = kv_of(h->kp.kern);
-  if (P == 64) { if (kv == KV_SE) LAUNCH_CHOL(64, KV_SE); else if (kv == KV_M52) LAUNCH_CHOL(64, KV_M52); else LAUNCH_CHOL(64, KV_ANY); }
-  else { if (kv == KV_SE) LAUNCH_CHOL(128, KV_SE); else if (kv == KV_M52) LAUNCH_CHOL(128, KV_M52); else LAUNCH_CHOL(128, KV_ANY); }
+  const int kv = kv_of_kp(h->kp);
+  if (P == 64) {
+    if (kv == KV_SE) LAUNCH_CHOL(64, KV_SE); else if (kv == KV_M52) LAUNCH_CHOL(64, KV_M52);
+    else if (kv == KV_ND) LAUNCH_CHOL(64, KV_ND); else LAUNCH_CHOL(64, KV_ANY);
+  } else {
+    if (kv == KV_SE) LAUNCH_CHOL(128, KV_SE); else if (kv == KV_M52) LAUNCH_CHOL(128, KV_M52);
+    else if (kv == KV_ND) LAUNCH_CHOL(128, KV_ND); else LAUNCH_CHOL(128, KV_ANY);
+  }
 #undef LAUNCH_CHOL
   HLAUNCH(h, "k_leaf_chol");
 #ifdef CHOL_TRACE

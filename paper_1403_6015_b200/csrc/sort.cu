@@ -222,7 +222,121 @@ static cudaError_t sort_graph(SortPlan *P, int ntiles, int nb) {
   return e;
 }
 
+// ---------------------------------------------------------------------------------------------------------------
+// NEXT-3: the kd ordering of d-dimensional points ("sorted recursively, one dimension at a time";
+// DESIGN.md R19): for L = 0 .. max(kappa, 1) - 1, top down, every depth-L node sorts its points stably by
+// coordinate L mod d, and the count-median split halves it.  One level is one stable LSD radix sort of the whole
+// array by (node, coordinate): 8 digit passes on the coordinate's order-preserving key, then ceil(L / 8) passes on
+// the depth-L node index -- equal nodes keep the coordinate order, equal coordinates the previous order, which is
+// each node's stable sort -- then one gather of the coordinate rows and the permutation.
+// ---------------------------------------------------------------------------------------------------------------
+__global__ void k_kd_init(const double *__restrict__ x, long long n, int dim, double *__restrict__ xs,
+                          long long *__restrict__ perm, int *__restrict__ flags) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int k = 0; k < dim; k++) {
+    double v = x[i * dim + k];
+    if (!isfinite(v)) atomicOr(&flags[0], 1);
+    if (v == 0.0) v = 0.0;                      // -0.0 -> +0.0
+    xs[k * n + i] = v;
+  }
+  perm[i] = i;
+}
+__global__ void k_kd_keys(const double *__restrict__ xa, long long n, unsigned long long *__restrict__ key,
+                          long long *__restrict__ idx) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  unsigned long long b = __double_as_longlong(xa[i]);
+  b ^= (b >> 63) ? 0xffffffffffffffffULL : 0x8000000000000000ULL;
+  key[i] = b;
+  idx[i] = i;
+}
+// node key of the element that came from position idx[i]: the depth-L node whose rows contain that position
+__global__ void k_kd_nodekeys(const long long *__restrict__ idx, long long n, const long long *__restrict__ lo, int L,
+                              unsigned long long *__restrict__ key) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const long long p = idx[i], base = (1LL << L) - 1;
+  long long a = 0, b = (1LL << L) - 1;            // largest j in [a, b] with lo[base + j] <= p
+  while (a < b) { const long long m = (a + b + 1) >> 1; if (lo[base + m] <= p) a = m; else b = m - 1; }
+  key[i] = (unsigned long long)a;
+}
+__global__ void k_kd_gather(const long long *__restrict__ idx, long long n, int dim, const double *__restrict__ xin,
+                            const long long *__restrict__ pin, double *__restrict__ xout, long long *__restrict__ pout) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const long long j = idx[i];
+  for (int k = 0; k < dim; k++) xout[k * n + i] = xin[k * n + j];
+  pout[i] = pin[j];
+}
+__global__ void __launch_bounds__(STHREADS) k_hist_p(const unsigned long long *key, long long n, int shift, int ntiles,
+                                                     unsigned int *cnt) {
+  hist_body(key, n, shift, ntiles, cnt);
+}
+__global__ void __launch_bounds__(256) k_scan_p(unsigned int *cnt, int ntiles, unsigned int *tot) {
+  scan_digit_body(cnt, ntiles, tot);
+}
+__global__ void __launch_bounds__(STHREADS) k_scatter_p(const unsigned long long *kin, const long long *iin, long long n,
+                                                        int shift, int ntiles, const unsigned int *cnt,
+                                                        const unsigned int *tot, unsigned long long *kout,
+                                                        long long *iout) {
+  scatter_body(kin, iin, n, shift, ntiles, cnt, tot, kout, iout);
+}
+
 }  // namespace
+
+hodlr_status hodlr_kd_sort(hodlr_s *h, const double *x, long long n, int dim) {
+  const int ntiles = (int)((n + TILE - 1) / TILE);
+  if (ntiles > 256 * 16) return hodlr_set_error(HODLR_EINVAL, "sort: n too large for the radix tile table");
+  unsigned long long *k[2] = {(unsigned long long *)hodlr_dalloc_tmp(h, sizeof(unsigned long long) * n),
+                              (unsigned long long *)hodlr_dalloc_tmp(h, sizeof(unsigned long long) * n)};
+  long long *id[2] = {(long long *)hodlr_dalloc_tmp(h, sizeof(long long) * n),
+                      (long long *)hodlr_dalloc_tmp(h, sizeof(long long) * n)};
+  unsigned int *cnt = (unsigned int *)hodlr_dalloc_tmp(h, sizeof(unsigned int) * (256 * (size_t)ntiles + 256));
+  double *xs2 = (double *)hodlr_dalloc_tmp(h, sizeof(double) * (size_t)n * dim);
+  long long *perm2 = (long long *)hodlr_dalloc_tmp(h, sizeof(long long) * n);
+  if (!k[0] || !k[1] || !id[0] || !id[1] || !cnt || !xs2 || !perm2)
+    return hodlr_set_error(HODLR_ENOMEM, "sort: device allocation failed");
+  unsigned int *tot = cnt + 256 * (size_t)ntiles;
+  const int nb = (int)((n + 255) / 256);
+  double *xa[2] = {h->xs, xs2};
+  long long *pa[2] = {h->perm, perm2};
+  int cur = 0;                 // xa[cur], pa[cur]: the current order
+  ph_begin(h, PH_SORT);
+  k_kd_init<<<nb, 256, 0, h->st>>>(x, n, dim, h->xs, h->perm, h->dflags);
+  HLAUNCH(h, "k_kd_init");
+  const int levels = h->kappa > 0 ? h->kappa : 1;
+  for (int L = 0; L < levels; L++) {
+    k_kd_keys<<<nb, 256, 0, h->st>>>(xa[cur] + (size_t)(L % dim) * n, n, k[0], id[0]);
+    HLAUNCH(h, "k_kd_keys");
+    int b = 0;                 // k[b], id[b]: the pass input
+    auto pass = [&](int shift) -> hodlr_status {
+      k_hist_p<<<ntiles, STHREADS, 0, h->st>>>(k[b], n, shift, ntiles, cnt);
+      HLAUNCH(h, "k_hist_p");
+      k_scan_p<<<256, 256, 0, h->st>>>(cnt, ntiles, tot);
+      HLAUNCH(h, "k_scan_p");
+      k_scatter_p<<<ntiles, STHREADS, 0, h->st>>>(k[b], id[b], n, shift, ntiles, cnt, tot, k[b ^ 1], id[b ^ 1]);
+      HLAUNCH(h, "k_scatter_p");
+      b ^= 1;
+      return HODLR_OK;
+    };
+    for (int p = 0; p < 8; p++) { hodlr_status s = pass(8 * p); if (s != HODLR_OK) return s; }
+    if (L > 0) {
+      k_kd_nodekeys<<<nb, 256, 0, h->st>>>(id[b], n, h->lo, L, k[b]);
+      HLAUNCH(h, "k_kd_nodekeys");
+      for (int p = 0; p < (L + 7) / 8; p++) { hodlr_status s = pass(8 * p); if (s != HODLR_OK) return s; }
+    }
+    k_kd_gather<<<nb, 256, 0, h->st>>>(id[b], n, dim, xa[cur], pa[cur], xa[cur ^ 1], pa[cur ^ 1]);
+    HLAUNCH(h, "k_kd_gather");
+    cur ^= 1;
+  }
+  if (cur) {
+    HCUDA(cudaMemcpyAsync(h->xs, xs2, sizeof(double) * (size_t)n * dim, cudaMemcpyDeviceToDevice, h->st));
+    HCUDA(cudaMemcpyAsync(h->perm, perm2, sizeof(long long) * n, cudaMemcpyDeviceToDevice, h->st));
+  }
+  ph_end(h, PH_SORT);
+  return HODLR_OK;
+}
 
 hodlr_status hodlr_sort_and_tree(hodlr_s *h, const double *x, long long n) {
   const int ntiles = (int)((n + TILE - 1) / TILE);

@@ -26,7 +26,7 @@ EXPORTS = ("hodlr_build", "hodlr_factor", "hodlr_factor_solve", "hodlr_cache_tri
            "hodlr_get_order", "hodlr_get_tree", "hodlr_get_logdet_parts", "hodlr_free", "hodlr_last_error",
            "hodlr_version", "hodlr_launch_count", "hodlr_nccl_unique_id", "hodlr_group_create",
            "hodlr_group_destroy", "hodlr_group_mode", "hodlr_dist_plan", "gp_loglik_sweep", "hodlr_build_batch",
-           "hodlr_batch_results")
+           "hodlr_batch_results", "hodlr_build_nd")
 
 
 class HodlrError(RuntimeError):
@@ -107,6 +107,7 @@ def load(build_if_missing: bool = True):
         lib.gp_loglik_sweep.argtypes = [P, P, I64, I32, P, P, I32, I32, D, P, P, I32, P]
         lib.hodlr_build_batch.argtypes = [P, I64, I32, P, P, I32, I32, D, P, P, P]
         lib.hodlr_batch_results.argtypes = [P, P, P]
+        lib.hodlr_build_nd.argtypes = [P, I64, I32, I32, P, D, I32, D, P, P, P]; lib.hodlr_build_nd.restype = I32
         lib.gp_loglik_sweep.restype = I32
         _lib = lib
         return lib
@@ -149,6 +150,28 @@ def hodlr_build(x: torch.Tensor, kernel: int, theta, sigma2: float, leaf: int, e
     _check(lib.hodlr_build(x.data_ptr(), x.numel(), int(kernel), th, float(sigma2), int(leaf), float(eps),
                            C.byref(dist) if dist is not None else None, C.byref(opts), _stream_ptr(stream),
                            C.byref(h)))
+    return h.value
+
+
+def hodlr_build_nd(x: torch.Tensor, kernel: int, theta, sigma2: float, leaf: int, eps: float,
+                   rank_cap: int = 0, stream=None, forced_ranks=None, noise: "torch.Tensor | None" = None) -> int:
+    """NEXT-3: x is a CUDA float64 (n, d) tensor of d-dimensional points (row-major), kd ordering (hodlr.h)."""
+    lib = load()
+    x = _dev_f64(x, "x")
+    if x.dim() != 2:
+        raise ValueError("hodlr_build_nd: x must be (n, d)")
+    th = (C.c_double * 3)(float(theta[0]), float(theta[1]), float(theta[2]) if len(theta) > 2 else 0.0)
+    opts = hodlr_opts(int(rank_cap))
+    if forced_ranks is not None:
+        import numpy as np
+        fr = np.ascontiguousarray(forced_ranks, dtype=np.int32)
+        opts.forced_ranks = fr.ctypes.data
+    if noise is not None:
+        noise = _dev_f64(noise, "noise")
+        opts.noise = noise.data_ptr()
+    h = C.c_void_p(0)
+    _check(lib.hodlr_build_nd(x.data_ptr(), x.shape[0], x.shape[1], int(kernel), th, float(sigma2), int(leaf),
+                              float(eps), C.byref(opts), _stream_ptr(stream), C.byref(h)))
     return h.value
 
 
@@ -327,8 +350,14 @@ class HODLR:
         hook (hodlr_opts.forced_ranks)."""
         if isinstance(kernel, str):
             kernel = KERNELS[kernel]
-        self.n = x.numel()
         self._dist = dist                       # keeps the NCCL id / group alive
+        if x.dim() == 2:                        # (n, d) points: hodlr_build_nd (NEXT-3, one GPU)
+            if dist is not None:
+                raise ValueError("HODLR: d-dimensional points run on one GPU (no dist)")
+            self.n, self.dim = x.shape[0], x.shape[1]
+            self._h = hodlr_build_nd(x, kernel, theta, sigma2, leaf, eps, rank_cap, stream, forced_ranks, noise)
+            return
+        self.n, self.dim = x.numel(), 1
         self._h = hodlr_build(x, kernel, theta, sigma2, leaf, eps, rank_cap, stream,
                               dist.struct() if dist is not None else None, forced_ranks, noise)
 
@@ -375,9 +404,13 @@ class HODLR:
         return hodlr_info(self._h)
 
     def order(self):
-        xs = torch.empty(self.n, dtype=torch.float64, device="cuda")
+        """(sorted points, perm): points (n,) for 1-D, (n, d) for a d-dimensional handle."""
+        dim = getattr(self, "dim", 1)
+        xs = torch.empty(self.n * dim, dtype=torch.float64, device="cuda")
         perm = torch.empty(self.n, dtype=torch.int64, device="cuda")
         _check(load().hodlr_get_order(self._h, xs.data_ptr(), perm.data_ptr()))
+        if dim > 1:
+            xs = xs.view(dim, self.n).t().contiguous()     # coordinate-major on the device -> (n, d)
         return xs, perm
 
     def tree(self):

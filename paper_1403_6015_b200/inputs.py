@@ -100,3 +100,25 @@ def rmse_model(n: int = 1024, seed: int = 56):
     x = rng.uniform(-3.0, 3.0, n)
     y = np.sin(2.0 * x) + np.exp(x) / 8.0 + rng.standard_normal(n)
     return x, y
+
+
+# NEXT-3 workloads (DESIGN.md section 4 / 9f): the shape of Table II's multi-dimensional columns -- "random uniformly
+# distributed points" in a cube -- with the cube and length scale chosen so that the ranks meet
+# eps within this build's rank cap (the paper's [-3, 3]^d with exp(-r^2) has ranks in the hundreds).
+ND_CONFIGS = {
+    #        d, half-side, kernel, (a, ell), sigma2, leaf, eps
+    "nd2": (2, 0.5, SE, (1.0, 1.0), 1e-2, 128, 1e-10),
+    "nd3": (3, 0.5, SE, (1.0, 4.0), 1e-2, 128, 1e-10),
+}
+
+
+def points_nd(n: int, d: int, seed: int, half: float = 0.5, grid: int = 0):
+    """(x, y): n points uniform in [-half, half]^d (row-major (n, d)), then y ~ N(0, 1).  grid > 0 rounds every
+    coordinate to a multiple of 1/grid (exact coordinate ties and duplicate points: the kd sort's tie rule and the
+    ACA's duplicate-row rule)."""
+    rng = np.random.default_rng(seed)
+    x = rng.uniform(-half, half, (n, d))
+    if grid > 0:
+        x = np.round(x * grid) / grid
+    y = rng.standard_normal(n)
+    return x, y
