@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(AT) k_apply_leaf_up(ApplyCtx c) {
   for (int i = t; i < m; i += AT) {
     const double xi = sx[i];
     double s = 0.0;
-    if (kp.dim > 1) for (int j = 0; j < m; j++) s = fma(kval_nd(kp, c.xs, lo + i, lo + j), sv[j], s);   // NEXT-3
+    if (kp.dim > 1) for (int j = 0; j < m; j++) s = fma(kval_nd_fast(kp, c.xs, lo + i, lo + j), sv[j], s);   // NEXT-3
     else for (int j = 0; j < m; j++) s = fma(kval(kp, xi - sx[j]), sv[j], s);
     c.ys[lo + i] = fma(sig2(kp, lo + i), sv[i], s);
   }

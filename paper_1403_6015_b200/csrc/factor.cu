@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(LT) k_leaf_factor(LeafCtx c) {
       while (i * (i + 1) / 2 > p) i--;
       while ((i + 1) * (i + 2) / 2 <= p) i++;
       long long j = p - i * (i + 1) / 2;
-      double v = kp.dim > 1 ? kval_nd(kp, c.xs, lo + i, lo + j) : kval(kp, xl[i] - xl[j]);
+      double v = kp.dim > 1 ? kval_nd_fast(kp, c.xs, lo + i, lo + j) : kval(kp, xl[i] - xl[j]);
       if (i == j) v += sig2(kp, lo + i);
       L[p] = v;
     }
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(LT) k_leaf_factor_lu(LuCtx lc) {
     double *Eg = W + (long long)m * ldz;                      // m x ldz: E (sorted row order)
     for (int p = t; p < m * m; p += LT) {
       const int i = p / m, j = p - i * m;
-      double v = kp.dim > 1 ? kval_nd(kp, c.xs, lo + i, lo + j) : kval(kp, c.xs[lo + i] - c.xs[lo + j]);
+      double v = kp.dim > 1 ? kval_nd_fast(kp, c.xs, lo + i, lo + j) : kval(kp, c.xs[lo + i] - c.xs[lo + j]);
       if (i == j) v += sig2(kp, lo + i);
       A[p] = v;
     }

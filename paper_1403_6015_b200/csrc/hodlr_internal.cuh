@@ -443,6 +443,13 @@ __device__ __forceinline__ double kval_nd(const KParams &kp, const double *xs, l
   if (kp.kern == HODLR_SE) return __dmul_rn(kp.a2, exp_cr(-div_exact(r2, kp.c2, kp.rc2)));
   return kval_o(kp, __dsqrt_rn(r2));
 }
+// the same entry for the leaf blocks and the forward apply (no pivot decision depends on it): kval's fast exp / log
+__device__ __forceinline__ double kval_nd_fast(const KParams &kp, const double *xs, long long i, long long j) {
+  double r2 = 0.0;
+  for (int k = 0; k < kp.dim; k++) { const double d = xs[k * kp.ldp + i] - xs[k * kp.ldp + j]; r2 = fma(d, d, r2); }
+  if (kp.kern == HODLR_SE) return kp.a2 * exp(-r2 * kp.c);
+  return kval(kp, sqrt(r2));
+}
 // the launch family of a handle: KV_ND for d > 1, else the kernel family's specialisation
 static inline int kv_of_kp(const KParams &kp) { return kp.dim > 1 ? KV_ND : kv_of(kp.kern); }
 // sorted points i and j coincide (every coordinate equal; 1-D: xs[i] == xs[j]) -- the duplicate-row rule (R2)

@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(CholCfg<P>::NT, CholCfg<P>::MINB) k_leaf_chol(
       const int i = 8 * I + r, j = 8 * J + cc;
       double v;
       if (i < m && j < m) {
-        v = SEO == KV_ND ? kval_nd(kp, c.xs, lo + i, lo + j) : kval_t<SEO>(kp, sx[i] - sx[j]);
+        v = SEO == KV_ND ? kval_nd_fast(kp, c.xs, lo + i, lo + j) : kval_t<SEO>(kp, sx[i] - sx[j]);
         if (i == j) v += sig2(kp, lo + i);
       }
       else v = (i == j) ? 1.0 : 0.0;

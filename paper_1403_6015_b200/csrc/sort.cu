@@ -269,6 +269,71 @@ __global__ void k_kd_gather(const long long *__restrict__ idx, long long n, int 
   for (int k = 0; k < dim; k++) xout[k * n + i] = xin[k * n + j];
   pout[i] = pin[j];
 }
+// The deep levels in one launch: CTA b takes the depth-L0 node b (m <= KD_LOCAL points) and runs levels L0 .. levels-1
+// in shared memory.  At level L each depth-L sub-node is sorted by (coordinate key, position) with its own bitonic
+// network over S = 2^ceil(log2(largest sub-node)) slots (padding slots sort last): the tuples are distinct, so the
+// result is each sub-node's stable sort by that coordinate (the global passes' result).  Points are read through the
+// running order cur[] (coordinate-major input, L1/L2-cached).
+constexpr int KD_LOCAL = 4096, KD_LT = 512;
+constexpr size_t KD_LOCAL_SMEM = 2 * KD_LOCAL * (8 + 4) + KD_LOCAL * (2 + 2);
+__global__ void __launch_bounds__(KD_LT) k_kd_local(const double *__restrict__ xin, const long long *__restrict__ pin,
+                                                    long long n, int dim, int L0, int levels,
+                                                    const long long *__restrict__ lo, const long long *__restrict__ hi,
+                                                    double *__restrict__ xout, long long *__restrict__ pout) {
+  extern __shared__ unsigned long long kd_sm[];    // KD_LOCAL_SMEM bytes
+  unsigned long long *key = kd_sm;                 // 2 KD_LOCAL slots
+  unsigned int *tag = (unsigned int *)(key + 2 * KD_LOCAL);        // position in the node (padding: ~0)
+  unsigned short *cur = (unsigned short *)(tag + 2 * KD_LOCAL), *nxt = cur + KD_LOCAL;
+  const int t = threadIdx.x;
+  const long long root = (1LL << L0) - 1 + blockIdx.x, base = lo[root];
+  const int m = (int)(hi[root] - base);
+  for (int i = t; i < m; i += KD_LT) cur[i] = (unsigned short)i;
+  __syncthreads();
+  for (int L = L0; L < levels; L++) {
+    const int ax = L % dim;
+    const long long first = ((root + 1) << (L - L0)) - 1;   // depth-L descendants of root: ids first .. first + nsub - 1
+    const int nsub = 1 << (L - L0);
+    int S = 1, sh = 0;                             // count-median: the first sub-node is the largest
+    while (S < (int)(hi[first] - lo[first])) { S <<= 1; sh++; }
+    const int V = nsub << sh;
+    for (int v = t; v < V; v += KD_LT) {
+      const int sb = v >> sh, li = v & (S - 1);
+      const int p0 = (int)(lo[first + sb] - base), sz = (int)(hi[first + sb] - lo[first + sb]);
+      if (li < sz) {
+        unsigned long long b = __double_as_longlong(xin[(long long)ax * n + base + cur[p0 + li]]);
+        b ^= (b >> 63) ? 0xffffffffffffffffULL : 0x8000000000000000ULL;
+        key[v] = b; tag[v] = (unsigned)(p0 + li);
+      } else { key[v] = ~0ULL; tag[v] = ~0u; }
+    }
+    __syncthreads();
+    for (int k = 2; k <= S; k <<= 1)
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = t; i < V; i += KD_LT) {
+          const int l = i ^ j;
+          if (l > i) {
+            const unsigned ta = tag[i], tb = tag[l];
+            const unsigned long long ka = key[i], kb = key[l];
+            const bool gt = ka != kb ? ka > kb : ta > tb;
+            if (gt == (k == S || (i & k) == 0)) { key[i] = kb; key[l] = ka; tag[i] = tb; tag[l] = ta; }
+          }
+        }
+        __syncthreads();
+      }
+    for (int v = t; v < V; v += KD_LT) {
+      const int sb = v >> sh, li = v & (S - 1);
+      const int p0 = (int)(lo[first + sb] - base), sz = (int)(hi[first + sb] - lo[first + sb]);
+      if (li < sz) nxt[p0 + li] = cur[tag[v]];
+    }
+    __syncthreads();
+    for (int i = t; i < m; i += KD_LT) cur[i] = nxt[i];
+    __syncthreads();
+  }
+  for (int i = t; i < m; i += KD_LT) {
+    const long long src = base + cur[i];
+    for (int k = 0; k < dim; k++) xout[(long long)k * n + base + i] = xin[(long long)k * n + src];
+    pout[base + i] = pin[src];
+  }
+}
 __global__ void __launch_bounds__(STHREADS) k_hist_p(const unsigned long long *key, long long n, int shift, int ntiles,
                                                      unsigned int *cnt) {
   hist_body(key, n, shift, ntiles, cnt);
@@ -306,7 +371,9 @@ hodlr_status hodlr_kd_sort(hodlr_s *h, const double *x, long long n, int dim) {
   k_kd_init<<<nb, 256, 0, h->st>>>(x, n, dim, h->xs, h->perm, h->dflags);
   HLAUNCH(h, "k_kd_init");
   const int levels = h->kappa > 0 ? h->kappa : 1;
-  for (int L = 0; L < levels; L++) {
+  int L0 = 0;                  // first level whose nodes all fit one CTA's shared memory (count-median: sizes differ by <= 1)
+  while (L0 < levels && (n + (1LL << L0) - 1) >> L0 > KD_LOCAL) L0++;
+  for (int L = 0; L < L0; L++) {
     k_kd_keys<<<nb, 256, 0, h->st>>>(xa[cur] + (size_t)(L % dim) * n, n, k[0], id[0]);
     HLAUNCH(h, "k_kd_keys");
     int b = 0;                 // k[b], id[b]: the pass input
@@ -328,6 +395,13 @@ hodlr_status hodlr_kd_sort(hodlr_s *h, const double *x, long long n, int dim) {
     }
     k_kd_gather<<<nb, 256, 0, h->st>>>(id[b], n, dim, xa[cur], pa[cur], xa[cur ^ 1], pa[cur ^ 1]);
     HLAUNCH(h, "k_kd_gather");
+    cur ^= 1;
+  }
+  if (L0 < levels) {
+    HCUDA(hodlr_allow_smem((const void *)k_kd_local, h->dev));
+    k_kd_local<<<(int)(1LL << L0), KD_LT, KD_LOCAL_SMEM, h->st>>>(xa[cur], pa[cur], n, dim, L0, levels, h->lo, h->hi, xa[cur ^ 1],
+                                                       pa[cur ^ 1]);
+    HLAUNCH(h, "k_kd_local");
     cur ^= 1;
   }
   if (cur) {

@@ -56,6 +56,9 @@ def run(name, n, warm=3, reps=7):
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "once":     # profiling: python tools/nd_bench.py once nd2 20
+        print(json.dumps(run(sys.argv[2], 1 << int(sys.argv[3]), warm=1, reps=1)))
+        sys.exit(0)
     res = {"device": torch.cuda.get_device_name(0), "l2": "flushed between timed steps (512 MB write, untimed)",
            "runs": []}
     for name, n in (("nd2", 1 << 16), ("nd2", 1 << 18), ("nd2", 1 << 20), ("nd3", 1 << 16), ("nd3", 1 << 18)):
