@@ -644,3 +644,17 @@ def test_nonspd_sign_both_ways():
         assert sg == int(sd) and abs(la - ld) <= 1e-11 * abs(ld), (n, s2)
         seen.add(sg)
     assert seen == {1, -1}
+
+
+def test_points_nd_recipe():
+    """NEXT-3 input recipe: seeded, inside the cube, y drawn after x; the lattice option gives
+    exact coordinate ties and duplicate points (the cases the kd sort's tie rule and the duplicate-row rule cover)."""
+    from paper_1403_6015_b200 import inputs
+    x, y = inputs.points_nd(5000, 3, seed=7, half=0.5)
+    x2, y2 = inputs.points_nd(5000, 3, seed=7, half=0.5)
+    assert x.shape == (5000, 3) and y.shape == (5000,)
+    np.testing.assert_array_equal(x, x2); np.testing.assert_array_equal(y, y2)
+    assert np.all(np.abs(x) <= 0.5)
+    g, _ = inputs.points_nd(6000, 2, seed=3, half=0.5, grid=16)
+    assert len(np.unique(g[:, 0])) <= 17
+    assert len(np.unique(g, axis=0)) < len(g)
