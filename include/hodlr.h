@@ -136,7 +136,8 @@ hodlr_status hodlr_build(const double *x, int64_t n, hodlr_kernel kernel, const 
  * Table I functions of the Euclidean distance |x_i - x_j| (SE from its square).  x: device, n x dim row-major
  * (point i at x[i * dim .. i * dim + dim)).  1 <= dim <= 64 (dim = 1 is hodlr_build, bit for bit).  One GPU,
  * unbatched (no dist); noise, forced_ranks and rank_cap in opts as for hodlr_build.  The rest of the path (factor,
- * logdet, solve, factor_solve, gp_loglik, apply) is unchanged; gp_predict refuses d > 1 (HODLR_EINVAL).
+ * logdet, solve, factor_solve, gp_loglik, apply, gp_predict) is unchanged; gp_predict takes xt as m x dim
+ * row-major test points.
  * hodlr_get_order returns the sorted points coordinate-major (dim x n: coordinate k of sorted point i at
  * xs[k * n + i]).  Limits: the ranks must meet eps within the rank cap (<= 64, else HODLR_ERANKCAP) and each
  * coupling system's on-chip working set must fit one SM (else HODLR_EINVAL at factor) -- 2-D problems of moderate
@@ -185,7 +186,7 @@ hodlr_status hodlr_apply(hodlr_t h, const double *x, double *y, int64_t nrhs, in
 
 /* GP prediction at m test points (eq_reg1 / eq_reg2; NEXT-1): mean_j = k(xt_j, x) C^{-1} y and,
  * if var != NULL, the latent variance var_j = k(xt_j, xt_j) - k(xt_j, x) C^{-1} k(x, xt_j) (sigma^2 not added).
- * Cross-covariances on the fly, C^{-1} by the HODLR solve.  y: device n (original order); xt, mean, var: device m.
+ * Cross-covariances on the fly, C^{-1} by the HODLR solve.  y: device n (original order); xt: device m (m x dim row-major on a hodlr_build_nd handle); mean, var: device m.
  * Legal after hodlr_factor; single-GPU handles only (HODLR_EINVAL when sharded). */
 hodlr_status gp_predict(hodlr_t h, const double *y, const double *xt, int64_t m, double *mean, double *var);
 

@@ -192,7 +192,7 @@ __device__ __forceinline__ void aca_item(const AcaCtx &c, int item, AcaScratch &
   // vector path: thread t takes the ACA_E consecutive elements of each ACA_TILE-element sub-tile (double2
   // loads/stores); needs 16-byte alignment of every column segment (n and the chunk start even) -- the
   // scalar loop below handles the rest
-  const bool vec = SEO != KV_ND && ((ldx | (lo + it.start)) & 1) == 0 && (ilen % ACA_E) == 0;
+  const bool vec = ((ldx | (lo + it.start)) & 1) == 0 && (ilen % ACA_E) == 0;
   constexpr int NP = ACA_E / 2;                  // double2 pairs per thread
   constexpr int LS = 4;                          // factor columns per batch of loads
   if (vec) {
@@ -218,8 +218,13 @@ __device__ __forceinline__ void aca_item(const AcaCtx &c, int item, AcaScratch &
 #pragma unroll
         for (int pp = 0; pp < NP; pp++) {
           usedm |= ((uu[pp].x ? 1u : 0u) | (uu[pp].y ? 2u : 0u)) << (2 * pp);
-          r[2 * pp] = ok ? kval_ot<SEO>(kp, ROW ? xp - xx[pp].x : xx[pp].x - xp) : 0.0;
-          r[2 * pp + 1] = ok ? kval_ot<SEO>(kp, ROW ? xp - xx[pp].y : xx[pp].y - xp) : 0.0;
+          if (SEO == KV_ND) {                    // d-dimensional: the coordinate rows of points g0 + 2pp, g0 + 2pp + 1
+            r[2 * pp] = ok ? kval_nd(kp, c.xs, pg, g0 + 2 * pp) : 0.0;
+            r[2 * pp + 1] = ok ? kval_nd(kp, c.xs, pg, g0 + 2 * pp + 1) : 0.0;
+          } else {
+            r[2 * pp] = ok ? kval_ot<SEO>(kp, ROW ? xp - xx[pp].x : xx[pp].x - xp) : 0.0;
+            r[2 * pp + 1] = ok ? kval_ot<SEO>(kp, ROW ? xp - xx[pp].y : xx[pp].y - xp) : 0.0;
+          }
         }
       }
       // the newest column F_{k-1} first (normalised and stored back by the row pass)

@@ -744,7 +744,6 @@ hodlr_status gp_predict(hodlr_t h, const double *y, const double *xt, int64_t m,
   if (h->state != 2) return hodlr_set_error(HODLR_ESTATE, "predict: not factored");
   if (h->nranks > 1) return hodlr_set_error(HODLR_EINVAL, "predict: sharded handles are not supported");
   if (h->nonspd && var) return hodlr_set_error(HODLR_EINVAL, "predict: no variance for a kernel that is not positive definite");
-  if (h->dim > 1) return hodlr_set_error(HODLR_EINVAL, "predict: 1-D handles only (NEXT-3 covers build / factor / solve / apply)");
   h->launches = 0;
   cudaEventRecord(h->ev0, h->st);
   hodlr_status st = hodlr_predict_impl(h, y, xt, m, mean, var);

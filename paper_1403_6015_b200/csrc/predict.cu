@@ -9,6 +9,14 @@
 
 namespace {
 
+// d-dimensional handles (NEXT-3): k(xt_j, x_i) of sorted point i (coordinate-major xs) and test point j (row-major xt)
+__device__ __forceinline__ double kval_xt(const KParams &kp, const double *xs, long long i, const double *xt, long long j) {
+  double r2 = 0.0;
+  for (int k = 0; k < kp.dim; k++) { const double d = xs[k * kp.ldp + i] - xt[j * kp.dim + k]; r2 = fma(d, d, r2); }
+  if (kp.kern == HODLR_SE) return kp.a2 * exp(-r2 * kp.c);
+  return kval(kp, sqrt(r2));
+}
+
 constexpr int PB = 32;           // test points per variance batch
 
 // mean_j = sum_i k(xt_j - xs_i) alpha[perm[i]]: CTA (b, y) takes MT test points and the y-th slice of MSL points;
@@ -24,9 +32,16 @@ __global__ void __launch_bounds__(MT * 32) k_predict_mean(KParams kp, const doub
   __shared__ double sx[MCH], sa[MCH];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const long long j = (long long)blockIdx.x * MT + w;
-  const double x0 = j < m ? xt[j] : 0.0;
   const long long s0 = blockIdx.y * MSL, s1 = s0 + MSL < n ? s0 + MSL : n;
   double s = 0.0;
+  if (kp.dim > 1) {                              // d-dimensional: coordinate rows read directly (coalesced by lane)
+    const long long jj = j < m ? j : 0;
+    for (long long i = s0 + lane; i < s1; i += 32) s = fma(kval_xt(kp, xs, i, xt, jj), alpha[perm[i]], s);
+    s = warp_sum(s);
+    if (lane == 0 && j < m) partial[j * nsl + blockIdx.y] = s;
+    return;
+  }
+  const double x0 = j < m ? xt[j] : 0.0;
   for (long long c0 = s0; c0 < s1; c0 += MCH) {
     const int len = (int)(s1 - c0 < MCH ? s1 - c0 : MCH);
     __syncthreads();
@@ -52,7 +67,7 @@ __global__ void k_cross_cols(KParams kp, const double *xs, const long long *perm
   const long long tot = n * nb;
   for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < tot; p += (long long)gridDim.x * blockDim.x) {
     const int b = (int)(p / n); const long long i = p - (long long)b * n;
-    Kx[(long long)b * n + perm[i]] = kval(kp, xs[i] - xt[j0 + b]);
+    Kx[(long long)b * n + perm[i]] = kp.dim > 1 ? kval_xt(kp, xs, i, xt, j0 + b) : kval(kp, xs[i] - xt[j0 + b]);
   }
 }
 

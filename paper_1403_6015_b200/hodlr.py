@@ -270,9 +270,10 @@ def gp_predict(h: int, y: torch.Tensor, xt: torch.Tensor, variance: bool = True)
     """Predictive mean (and latent variance) at test points xt (CUDA float64); returns (mean, var or None)."""
     lib = load()
     y = _dev_f64(y, "y"); xt = _dev_f64(xt, "xt")
-    mean = torch.empty_like(xt)
-    var = torch.empty_like(xt) if variance else None
-    _check(lib.gp_predict(h, y.data_ptr(), xt.data_ptr(), xt.numel(), mean.data_ptr(),
+    m = xt.shape[0] if xt.dim() == 2 else xt.numel()      # (m, d) test points on a d-dimensional handle
+    mean = torch.empty(m, dtype=torch.float64, device=xt.device)
+    var = torch.empty(m, dtype=torch.float64, device=xt.device) if variance else None
+    _check(lib.gp_predict(h, y.data_ptr(), xt.data_ptr(), m, mean.data_ptr(),
                           var.data_ptr() if var is not None else None))
     return mean, var
 

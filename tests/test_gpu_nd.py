@@ -123,13 +123,28 @@ def test_nd_forced_ranks(hb):
     assert float(np.linalg.norm(x_g - x_o) / np.linalg.norm(x_o)) <= 1e-10
 
 
+@pytest.mark.parametrize("d", [2, 3])
+def test_nd_predict(hb, d):
+    """gp_predict at (m, d) test points: mean and latent variance against the oracle's predict (eq_reg1 / eq_reg2,
+    PAPER.md:341-354; cross-covariances entry by entry): mean 1e-9, variance 1e-9 absolute (relative to k(0) = a^2)."""
+    _, half, kernel, theta, s2, leaf, eps = inputs.ND_CONFIGS["nd2" if d == 2 else "nd3"]
+    x, y = inputs.points_nd(4096, d, seed=21 + d)
+    xt, _ = inputs.points_nd(37, d, seed=99 + d, half=0.6)       # some test points outside the training cube
+    o = OracleHODLR(x, kernel, theta, s2, leaf, eps).factor()
+    mo, vo = o.predict(y, xt)
+    g = hb.HODLR(torch.from_numpy(x).cuda(), kernel, theta, s2, leaf, eps).factor()
+    mg, vg = g.predict(torch.from_numpy(y).cuda(), torch.from_numpy(xt).cuda())
+    mg = mg.cpu().numpy(); vg = vg.cpu().numpy()
+    em = float(np.max(np.abs(mg - mo)) / np.max(np.abs(mo))); ev = float(np.max(np.abs(vg - vo)))
+    print(f"[nd predict d={d}] mean rel {em:.2e} var abs {ev:.2e}")
+    assert em <= 1e-9 and ev <= 1e-9
+    g.close()
+
+
 def test_nd_errors(hb):
     x, y = inputs.points_nd(4096, 2, seed=11)
     xd = torch.from_numpy(x).cuda()
     g = hb.HODLR(xd, SE, (1.0, 1.0), 1e-2, 128, 1e-10).factor()
-    with pytest.raises(hb.HodlrError) as e:           # prediction is 1-D only
-        g.predict(torch.from_numpy(y).cuda(), torch.zeros(4, dtype=torch.float64, device="cuda"))
-    assert e.value.status == "EINVAL"
     bad = x.copy(); bad[17, 1] = np.nan
     with pytest.raises(hb.HodlrError) as e:
         hb.HODLR(torch.from_numpy(bad).cuda(), SE, (1.0, 1.0), 1e-2, 128, 1e-10)
