@@ -45,7 +45,7 @@ __global__ void k_aca_init(AcaCtx c, int nblocks, int cap) {
   s->ipiv = m1 - 1;                      // DESIGN.md R2: last row of c1 (the point nearest c2)
   s->jpiv = -1; s->pivval = 0.0; s->S2 = 0.0; s->nv2 = 0.0;
   int e = c.bdepth[b] + 1;
-  mark_row_run(c, c.used + (long long)(e - 1) * c.n, c.lo[c1], m1, m1 - 1);
+  mark_row_run(c, c.used + (long long)(e - 1) * c.ldx, c.lo[c1], m1, m1 - 1);
   c.rank[b] = 0;
 }
 
@@ -164,7 +164,7 @@ __device__ __forceinline__ void aca_item(const AcaCtx &c, int item, AcaScratch &
   const long long lo1 = it.lo1, m1 = it.m1, lo2 = it.lo2, m2 = it.m2;
   const int e = it.e;
   double *slot = c.Xh + it.slot_off;
-  const unsigned char *used = c.used + (long long)(e - 1) * n;
+  const unsigned char *used = c.used + (long long)(e - 1) * ldx;   // (row stride ldx: even, so uchar2 loads align)
   const long long ilen = it.len;
   const KParams &kp = kp_of(c.kp, c.kps, c.nseg, lo1);
   // The row pass of step k divides the previous step's column V[:, k-1] (stored as the raw residual v~) by that
@@ -207,7 +207,9 @@ __device__ __forceinline__ void aca_item(const AcaCtx &c, int item, AcaScratch &
     for (long long s0 = it.start; s0 < end; s0 += ACA_TILE) {
       const long long g0 = lo + s0 + ACA_E * t;        // elements g0 .. g0 + ACA_E - 1
       const bool ok = s0 + ACA_E * t < end;            // whole group valid (len is a multiple of ACA_E)
-      const double *colp = slot + (ok ? g0 : lo + it.start);
+      // a group beyond the chunk (!ok: the partial last tile of a chunk) reads the zero padding rows of the factor
+      // columns, so that it adds nothing to the dots
+      const double *colp = slot + (ok ? g0 : c.zrow);
       double r[ACA_E], Fk[ACA_E];
       unsigned usedm = 0;
       {
@@ -407,7 +409,7 @@ __device__ __forceinline__ void aca_item(const AcaCtx &c, int item, AcaScratch &
           st->done = 1; c.rank[b] = k; atomicSub(c.active, 1);
         } else {
           st->jpiv = bi; st->pivval = bv;
-          c.used[(long long)(e - 1) * n + lo2 + bi] = 1;
+          c.used[(long long)(e - 1) * c.ldx + lo2 + bi] = 1;
         }
       }
     } else {
@@ -435,7 +437,7 @@ __device__ __forceinline__ void aca_item(const AcaCtx &c, int item, AcaScratch &
         if ((fr >= 0 && k1 >= fr) || k1 == mn) { done = 1; rank = k1; st->raw_last = 1; }
         else if (k1 == st->cap) st->donly = 1;       // the test of term k decides: one dots-only step
         else if (bi < 0 || ba == 0.0) { done = 1; rank = k1; st->raw_last = 1; }
-        else { st->ipiv = bi; mark_row_run(c, c.used + (long long)(e - 1) * n, lo1, m1, bi); }
+        else { st->ipiv = bi; mark_row_run(c, c.used + (long long)(e - 1) * c.ldx, lo1, m1, bi); }
       }
       if (done) { st->done = done; st->k = rank; c.rank[b] = rank; atomicSub(c.active, 1); }
     }
@@ -683,6 +685,7 @@ struct AcaPlan {
   AcaCtx *d_ctx = nullptr;                 // [0] row pass, [1] column pass
   cudaGraphExec_t ge = nullptr;
   bool busy = false;
+  bool zpad = false;                       // some chunk ends in a partial tile (zero padding rows of Xh needed)
 };
 static std::mutex g_plan_mu;
 static std::vector<AcaPlan *> g_plans;
@@ -714,6 +717,7 @@ static cudaError_t plan_create(AcaPlan *P, const hodlr_s *h) {
       int q = 0;
       for (long long s = 0; s < m; s += chunk, q++) {
         AcaItem it; it.block = (int)b; it.q = q; it.start = s; it.len = (int)std::min(chunk, m - s);
+        if (it.len % ACA_TILE) P->zpad = true;   // a partial last tile: its idle groups read the zero rows
         it.e = bdepth[b] + 1;
         it.lo1 = h->h_lo[2 * b + 1]; it.m1 = m1; it.lo2 = h->h_lo[2 * b + 2]; it.m2 = m2;
         it.slot_off = h->dt.colbase[it.e] * h->ldx;
@@ -825,7 +829,7 @@ hodlr_status hodlr_aca(hodlr_s *h) {
   double *d_rec = (double *)hodlr_dalloc_tmp(h, sizeof(double) * ACA_RECW * (size_t)(P->nrec_r + P->nrec_c + 1));
   h->ast = (AcaState *)hodlr_dalloc_tmp(h, sizeof(AcaState) * nb);
   h->rank = (int *)hodlr_dalloc(h, sizeof(int) * nb);
-  h->used = (unsigned char *)hodlr_dalloc_tmp(h, (size_t)h->kappa * n);
+  h->used = (unsigned char *)hodlr_dalloc_tmp(h, (size_t)h->kappa * h->ldx);   // kappa rows of stride ldx
   if (!d_rec || !h->ast || !h->rank || !h->used) return hodlr_set_error(HODLR_ENOMEM, "aca: device allocation failed");
   h->bdepth = P->d_bdepth;
   // The step loop is latency-bound: everything of the ACA phase runs on a high-priority stream so that the
@@ -836,14 +840,17 @@ hodlr_status hodlr_aca(hodlr_s *h) {
   struct Restore { hodlr_s *h; cudaStream_t s; ~Restore() { h->st = s; } } restore{h, sm_main};   // every return path
   h->st = h->sthi;
   ph_begin(h, PH_ACA);
-  HCUDA(cudaMemsetAsync(h->used, 0, (size_t)h->kappa * n, h->st));
+  HCUDA(cudaMemsetAsync(h->used, 0, (size_t)h->kappa * h->ldx, h->st));
+  if (P->zpad && h->xh_cols > 0)           // rows [ldx - 32, ldx) of every factor column: zeros (c.zrow)
+    HCUDA(cudaMemset2DAsync(h->Xh + (h->ldx - 32), sizeof(double) * h->ldx, 0, sizeof(double) * 32,
+                            (size_t)h->xh_cols, h->st));
   {
     int init[3] = {nbig, 0, 0};   // dflags[4] active big blocks, [5] rank-cap hits, [6] step counter
     HCUDA(cudaMemcpyAsync(h->dflags + 4, init, sizeof(init), cudaMemcpyHostToDevice, h->st));
   }
   AcaCtx c;
   memset(&c, 0, sizeof(c));
-  c.kp = h->kp; c.n = n; c.ldx = h->ldx; c.eps = h->eps; c.xs = h->xs; c.lo = h->lo; c.hi = h->hi; c.Xh = h->Xh;
+  c.kp = h->kp; c.n = n; c.ldx = h->ldx; c.zrow = h->ldx - 32; c.eps = h->eps; c.xs = h->xs; c.lo = h->lo; c.hi = h->hi; c.Xh = h->Xh;
   c.used = h->used; c.st = h->ast; c.active = h->dflags + 4; c.rank = h->rank; c.bdepth = P->d_bdepth;
   c.dt = h->d_dt; c.bigidx = P->d_bigidx; c.flags = h->dflags; c.step = h->dflags + 6;
   c.maxsteps = h->cap + 2;                 // + the dots-only step of the lagged stop test

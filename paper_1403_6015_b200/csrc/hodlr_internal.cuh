@@ -136,11 +136,12 @@ struct AcaCtx {
   KParams kp;
   long long n;
   long long ldx;            // column stride of Xh (n padded, see hodlr_s::ldx)
+  long long zrow;           // first of the 32 padding rows of every Xh column (>= n; zeroed when a chunk needs them)
   double eps;
   const double *xs;
   const long long *lo, *hi;
   double *Xh;
-  unsigned char *used;      // kappa x n flags: used[(e-1)*n + row]
+  unsigned char *used;      // kappa x ldx flags: used[(e-1)*ldx + row]
   AcaState *st;
   const AcaItem *items;
   const int *nq;            // chunks per block for this pass

@@ -54,6 +54,7 @@ struct SolveCtx {
   unsigned long long *stamps;   // HODLR_TRACE: %globaltimer after each phase (block 0), or NULL
   int R;                    // right-hand sides of this launch (columns r of y / x at r * ldy)
   long long xdoubles;       // X tile staging (doubles) at the start of the dynamic shared memory
+  int xglobal;              // leaves too large to stage X (p > ~235): the triangular products read X from global
   long long ldy;
   long long vcol, tcol, hcol;   // per-column strides of V, Tv and hv
   int aug;                  // the factorization carries a fused right-hand side: B_c / T_c rows have Kf[d] = Kdim[d] + 1
@@ -98,6 +99,7 @@ __device__ __forceinline__ int leaf_colsrc(const SolveCtx &c, long long id, int 
 // ---------------------------------------------------------------------------------------------
 __device__ void issue_x(const SolveCtx &c, long long leaf, double *sX) {
   const double *Xg = c.Lf + leaf * c.lstride;
+  if (c.xglobal) { cp_commit(); return; }
   const int nx2 = (c.T * (c.T + 1) / 2) * 32;
   for (int p = threadIdx.x; p < nx2; p += LT) cp16(sX + 2 * p, Xg + 2 * p);
   cp_commit();
@@ -216,11 +218,11 @@ __device__ void leaf_up_phase(const SolveCtx &c, double *sX, LeafSmem &S) {
         const int *lp = c.lperm + leaf * Rr;
         for (int i = t; i < Rr; i += LT) S.red[VMAX + i] = S.sb[lp[i]];
         __syncthreads();
-        tri_mv(sX, c.T, S.red + VMAX, S.su, nullptr);
+        tri_mv(c.xglobal ? c.Lf + leaf * c.lstride : sX, c.T, S.red + VMAX, S.su, nullptr);
         tri_mvt(c.Uf + leaf * c.lstride, c.T, S.su, S.red, nullptr);
       } else {
-        tri_mv(sX, c.T, S.sb, S.su, S.red);      // u = X b
-        tri_mvt(sX, c.T, S.su, S.red, nullptr);  // v = X^T u  (into red[0..R))
+        tri_mv(c.xglobal ? c.Lf + leaf * c.lstride : sX, c.T, S.sb, S.su, S.red);      // u = X b
+        tri_mvt(c.xglobal ? c.Lf + leaf * c.lstride : sX, c.T, S.su, S.red, nullptr);  // v = X^T u  (into red[0..R))
       }
       if (r + 1 == c.R && nxt < end) issue_x(c, nxt, sX);   // X is free
       double hs = 0.0;
@@ -362,11 +364,11 @@ __device__ void leaf_down_phase(const SolveCtx &c, double *sX, LeafSmem &S) {
         const int *lp = c.lperm + leaf * Rr;
         for (int i = t; i < Rr; i += LT) S.red[VMAX + i] = S.sb[lp[i]];
         __syncthreads();
-        tri_mv(sX, c.T, S.red + VMAX, S.su, nullptr);
+        tri_mv(c.xglobal ? c.Lf + leaf * c.lstride : sX, c.T, S.red + VMAX, S.su, nullptr);
         tri_mvt(c.Uf + leaf * c.lstride, c.T, S.su, S.sb, nullptr);
       } else {
-        tri_mv(sX, c.T, S.sb, S.su, S.red);
-        tri_mvt(sX, c.T, S.su, S.sb, S.red);
+        tri_mv(c.xglobal ? c.Lf + leaf * c.lstride : sX, c.T, S.sb, S.su, S.red);
+        tri_mvt(c.xglobal ? c.Lf + leaf * c.lstride : sX, c.T, S.su, S.sb, S.red);
       }
       if (r + 1 == c.R && nxt < end) issue_x(c, nxt, sX);
       if (c.xsorted) for (int i2 = t; i2 < m; i2 += LT) c.xsorted[lo + i2] = S.sb[i2];
@@ -470,8 +472,8 @@ __device__ void leaf_up_phase8(const SolveCtx &c, double *sX, LeafSmem8 &S) {
       load_b8(c, lo, m, r0, nr, S.b);
       if (r0 == 0) cp_wait<0>();
       __syncthreads();
-      tri_mv8(sX, c.T, S.b, S.u);               // u = X b
-      tri_mvt8(sX, c.T, S.u, S.v);              // v = X^T u
+      tri_mv8(c.xglobal ? c.Lf + leaf * c.lstride : sX, c.T, S.b, S.u);               // u = X b
+      tri_mvt8(c.xglobal ? c.Lf + leaf * c.lstride : sX, c.T, S.u, S.v);              // v = X^T u
       if (r0 + 8 >= c.R && nxt < end) issue_x(c, nxt, sX);   // X is free
       {                                          // h_c = b_c . v_c: warp c
         double hs = 0.0;
@@ -562,8 +564,8 @@ __device__ void leaf_down_phase8(const SolveCtx &c, double *sX, LeafSmem8 &S) {
       }
       if (r0 == 0) cp_wait<0>();
       __syncthreads();
-      tri_mv8(sX, T, S.b, S.u);
-      tri_mvt8(sX, T, S.u, S.b);
+      tri_mv8(c.xglobal ? c.Lf + leaf * c.lstride : sX, T, S.b, S.u);
+      tri_mvt8(c.xglobal ? c.Lf + leaf * c.lstride : sX, T, S.u, S.b);
       if (r0 + 8 >= c.R && nxt < end) issue_x(c, nxt, sX);
       for (int p = t; p < 8 * m; p += LT) {
         const int cc = p / m, i = p - cc * m;
@@ -818,7 +820,7 @@ __device__ void tree_down_rows(const SolveCtx &c, int d, long long i, int col, i
 // ---------------------------------------------------------------------------------------------
 // RB = 1: one right-hand side at a time through the leaves (two CTAs per SM); RB = 8: the leaves take 8 columns per
 // pass (k_solve<8>, larger shared state: one CTA per SM).  The tree levels are the same code.
-template <int RB>
+template <int RB, bool XG = false>
 __global__ void __launch_bounds__(LT, (RB == 1 ? 2 : 1)) k_solve(SolveCtx c0, Phases ph) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double sm[];
@@ -832,6 +834,7 @@ __global__ void __launch_bounds__(LT, (RB == 1 ? 2 : 1)) k_solve(SolveCtx c0, Ph
   for (int i = threadIdx.x; i < (int)(sizeof(DepthTab) / 8); i += LT) ((long long *)&sdt)[i] = ((const long long *)c0.dt)[i];
   __syncthreads();
   SolveCtx c = c0;
+  c.xglobal = XG;                              // compile-time: the staged-X path carries no run-time test
   c.dt = &sdt;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double *sX = sm;
@@ -965,17 +968,23 @@ hodlr_status hodlr_solve_impl(hodlr_s *h, const double *y, double *x, int64_t nr
   HCUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev));
   HCUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->dev));
   const bool rb8 = RM > 1 && !h->nonspd;         // LU leaves: the one-column leaf phases (R20)
-  const void *kfun = rb8 ? (const void *)k_solve<8> : (const void *)k_solve<1>;
+  const void *kfun = rb8 ? (const void *)k_solve<8> : (const void *)k_solve<1>;   // (X global: <RB, true> below)
   cudaFuncAttributes fa;
-  HCUDA(cudaFuncGetAttributes(&fa, kfun));
+  HCUDA(cudaFuncGetAttributes(&fa, kfun));     // (static shared memory: the same for both X modes)
   const size_t static_smem = fa.sharedSizeBytes;
   const size_t avail = ((size_t)maxsm - static_smem - 256) / sizeof(double);
   // Stage only X (68 KB at p = 128) and read E from global memory: two CTAs per SM overlap one leaf's loads with
   // the other's arithmetic (measured faster than staging X + E at one CTA per SM)
-  const size_t x_db0 = 64 * (size_t)(h->ltiles * (h->ltiles + 1) / 2);
+  size_t x_db0 = 64 * (size_t)(h->ltiles * (h->ltiles + 1) / 2);
+  const size_t x_extra = rb8 ? (sizeof(LeafSmem8) + 7) / 8 : 0;
+  c.xglobal = x_db0 + x_extra > avail ? 1 : 0;   // (leaves of more than ~235 points: X read from global memory)
+  if (c.xglobal) {
+    x_db0 = 0;
+    kfun = rb8 ? (const void *)k_solve<8, true> : (const void *)k_solve<1, true>;
+  }
   c.xdoubles = (long long)x_db0;
   // RB = 8: the 8-column leaf scratch follows the X tiles in dynamic shared memory
-  const size_t x_db = x_db0 + (rb8 ? (sizeof(LeafSmem8) + 7) / 8 : 0);
+  const size_t x_db = x_db0 + x_extra;
   const size_t need = std::max(x_db, (size_t)c.tree_scratch);
   if (need > avail)
     return hodlr_set_error(HODLR_EINVAL, "solve: leaf inverse (%d rows) or coupling size %zu exceeds shared memory", Rr, qmax);
