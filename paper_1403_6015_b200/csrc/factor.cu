@@ -72,46 +72,58 @@ struct LeafCtx {
   const KParams *kps; long long nseg;     // batched handle (kp_of), or NULL
 };
 
-__global__ void __launch_bounds__(LT) k_leaf_factor(LeafCtx c) {
+// Threads: any multiple of 32 up to 1024 (256 with everything in shared memory; 1024 and one CTA per SM when the
+// leaf lives in global scratch, so that all CTAs' scratch -- 148 x ~0.4 MB -- stays in L2: with 592 CTAs of 256
+// threads the 247 MB of scratch thrashed L2, 106 GB of DRAM traffic and 105 ms for the paper's n = 10^6 / leaf 128 row).
+__global__ void __launch_bounds__(1024) k_leaf_factor(LeafCtx c) {
   extern __shared__ double sm[];
   __shared__ long long colsrc[1024];
   __shared__ int bad;
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nth = blockDim.x, nw = nth >> 5;
   const int K = c.K, ldz = c.ldz;
-  double *base = c.use_smem ? sm : c.scratch + (long long)blockIdx.x * c.scratch_per_cta;
+  double *colj = sm;                           // mmax: the current Cholesky column
+  double *base = c.use_smem ? sm + c.mmax : c.scratch + (long long)blockIdx.x * c.scratch_per_cta;
   for (long long leaf = c.leaf0 + blockIdx.x; leaf < c.leaf0 + c.nown; leaf += gridDim.x) {
     const long long id = c.ninternal + leaf, lo = c.lo[id], m = c.hi[id] - lo;
     const KParams kp = kp_of(c.kp, c.kps, c.nseg, lo);
     double *xl = base;                       // m
     double *L = base + c.mmax;               // packed lower m(m+1)/2
     double *Z = L + c.lsz;                   // m x ldz
-    for (long long i = t; i < m; i += LT) xl[i] = c.xs[lo + i];
+    double *Zb = Z + (long long)c.mmax * ldz;   // 8 x ldz: one row block of Z = X E before it replaces E's rows
+    for (long long i = t; i < m; i += nth) xl[i] = c.xs[lo + i];
     if (t == 0) bad = 0;
     __syncthreads();
-    const long long np = m * (m + 1) / 2;
-    for (long long p = t; p < np; p += LT) {
-      long long i = (long long)((sqrt(8.0 * (double)p + 1.0) - 1.0) * 0.5);
-      while (i * (i + 1) / 2 > p) i--;
-      while ((i + 1) * (i + 2) / 2 <= p) i++;
-      long long j = p - i * (i + 1) / 2;
-      double v = kp.dim > 1 ? kval_nd_fast(kp, c.xs, lo + i, lo + j) : kval(kp, xl[i] - xl[j]);
-      if (i == j) v += sig2(kp, lo + i);
-      L[p] = v;
+    for (long long i = warp; i < m; i += nw) {          // assemble the packed lower triangle, a warp per row
+      double *Li = L + P(i, 0);
+      for (long long j = lane; j <= i; j += 32) {
+        double v = kp.dim > 1 ? kval_nd_fast(kp, c.xs, lo + i, lo + j) : kval(kp, xl[i] - xl[j]);
+        if (i == j) v += sig2(kp, lo + i);
+        Li[j] = v;
+      }
     }
     __syncthreads();
     for (long long j = 0; j < m; j++) {        // right-looking Cholesky A = L L^T
-      if (t == 0) {
-        double d = L[P(j, j)];
-        if (!(d > 0.0)) { bad = 1; d = 1.0; }
-        L[P(j, j)] = sqrt(d);
-      }
+      // The scaled column j also goes to shared memory (colj): the trailing update reads both of its factors
+      // there, so its only global accesses are the coalesced read-modify-writes of the packed rows, two rows per
+      // warp in flight.
+      const double d = L[P(j, j)];
+      const bool ok = d > 0.0;
+      const double ljj = sqrt(ok ? d : 1.0);
+      for (long long i = j + 1 + t; i < m; i += nth) { const double v = L[P(i, j)] / ljj; colj[i] = v; L[P(i, j)] = v; }
       __syncthreads();
-      const double ljj = L[P(j, j)];
-      for (long long i = j + 1 + t; i < m; i += LT) L[P(i, j)] /= ljj;
-      __syncthreads();
-      for (long long i = j + 1 + warp; i < m; i += LT / 32) {
-        const double lij = L[P(i, j)];
-        for (long long k = j + 1 + lane; k <= i; k += 32) L[P(i, k)] -= lij * L[P(k, j)];
+      if (t == 0) { L[P(j, j)] = ljj; if (!ok) bad = 1; }
+      for (long long i = j + 1 + warp; i < m; i += 2 * nw) {
+        const long long i2 = i + nw;
+        const bool two = i2 < m;
+        double *La = L + P(i, 0), *Lb = L + P(two ? i2 : i, 0);
+        const double la = colj[i], lb = two ? colj[i2] : 0.0;
+        const long long eb = two ? i2 : j, ke = two ? i2 : i;      // last column of each row (eb = j: no second row)
+        for (long long k = j + 1 + lane; k <= ke; k += 32) {
+          const double ck = colj[k];
+          const double va = k <= i ? La[k] : 0.0, vb = k <= eb ? Lb[k] : 0.0;
+          if (k <= i) La[k] = va - la * ck;
+          if (k <= eb) Lb[k] = vb - lb * ck;
+        }
       }
       __syncthreads();
     }
@@ -121,18 +133,28 @@ __global__ void __launch_bounds__(LT) k_leaf_factor(LeafCtx c) {
       c.leaf_ld[leaf] = 2.0 * s;
       if (bad) { atomicAdd(&c.flags[1], 1); atomicMin(&c.flags[2], (int)id); }
     }
-    // X = L^{-1} as fragment-order tiles (identity padding beyond m): forward substitution L x = e_j,
-    // one thread per column (fallback path; the fast path forms X on the tensor pipe)
+    // X = L^{-1} as fragment-order tiles (identity padding beyond m): forward substitution L x = e_j, four lanes
+    // per column (each a quarter of the row's dot product, summed by shuffles; fallback path -- the fast path forms
+    // X on the tensor pipe)
     const int T = c.T, NT = T * (T + 1) / 2;
     double *Lg = c.Lf + leaf * c.lstride;
-    for (long long p = t; p < (long long)NT * 64; p += LT) Lg[p] = 0.0;
+    for (long long p = t; p < (long long)NT * 64; p += nth) Lg[p] = 0.0;
     __syncthreads();
-    for (int j = t; j < 8 * T; j += LT) {
-      if (j >= m) { Lg[tix(j >> 3, j >> 3) * 64 + fo(j & 7, j & 7)] = 1.0; continue; }
-      for (int i = j; i < m; i++) {
-        double s = i == j ? 1.0 : 0.0;
-        for (int k = j; k < i; k++) s -= L[P(i, k)] * Lg[tix(k >> 3, j >> 3) * 64 + fo(k & 7, j & 7)];
-        Lg[tix(i >> 3, j >> 3) * 64 + fo(i & 7, j & 7)] = s / L[P(i, i)];
+    {
+      const int sub = lane & 3;
+      const unsigned gmask = 0xFu << (lane & ~3);
+      for (int j = t >> 2; j < 8 * T; j += nth >> 2) {
+        if (j >= m) { if (sub == 0) Lg[tix(j >> 3, j >> 3) * 64 + fo(j & 7, j & 7)] = 1.0; continue; }
+        const int Jt = j >> 3, jc = j & 7;
+        for (int i = j; i < m; i++) {
+          const double *Li = L + P(i, 0);
+          double s = 0.0;
+          for (int k = j + sub; k < i; k += 4) s += Li[k] * Lg[tix(k >> 3, Jt) * 64 + fo(k & 7, jc)];
+          s += __shfl_xor_sync(gmask, s, 1);
+          s += __shfl_xor_sync(gmask, s, 2);
+          if (sub == 0) Lg[tix(i >> 3, Jt) * 64 + fo(i & 7, jc)] = ((i == j ? 1.0 : 0.0) - s) / Li[i];
+          __syncwarp(gmask);
+        }
       }
     }
     if (K > 0) {
@@ -147,28 +169,37 @@ __global__ void __launch_bounds__(LT) k_leaf_factor(LeafCtx c) {
         }
         if (c.aug) colsrc[0] = -2;
       }
-      __syncthreads();
-      for (long long p = t; p < (long long)K * m; p += LT) {
-        long long col = p / m, i = p - col * m;
-        long long src = colsrc[col];
-        double v = 0.0;
-        if (src >= 0) v = c.Xh[src * c.ldx + lo + i];
-        else if (src == -2) { v = c.y[c.perm[lo + i]]; if (!isfinite(v)) atomicOr(&c.flags[3], 1); }
-        Z[i * ldz + col] = v;
-      }
-      __syncthreads();
-      for (int col = t; col < K; col += LT) {     // Z <- L^{-1} Z
-        for (long long i = 0; i < m; i++) {
-          double s = Z[i * ldz + col];
-          const double *Li = L + P(i, 0);
-          for (long long j = 0; j < i; j++) s -= Li[j] * Z[j * ldz + col];
-          Z[i * ldz + col] = s / Li[i];
+      __syncthreads();                 // colsrc, and X complete
+      for (int col = warp; col < K; col += nw) {          // E: the leaf's rows of its ancestors' factor columns
+        const long long src = colsrc[col];
+        for (long long i = lane; i < m; i += 32) {
+          double v = 0.0;
+          if (src >= 0) v = c.Xh[src * c.ldx + lo + i];
+          else if (src == -2) { v = c.y[c.perm[lo + i]]; if (!isfinite(v)) atomicOr(&c.flags[3], 1); }
+          Z[i * ldz + col] = v;
         }
       }
       __syncthreads();
+      // Z <- X E in place, row blocks from the bottom up (block I needs E's rows <= 8 I + 7 only; the block is
+      // staged in Zb so that every thread has read E's rows of the block before they are replaced)
+      for (int I = (int)((m - 1) >> 3); I >= 0; I--) {
+        const int rows = (int)(m - 8 * I < 8 ? m - 8 * I : 8);
+        for (int o = t; o < rows * K; o += nth) {
+          const int r = o / K, col = o - r * K, i = 8 * I + r;
+          double s = 0.0;
+          for (int j = 0; j <= i; j++) s += Lg[tix(I, j >> 3) * 64 + fo(r, j & 7)] * Z[(long long)j * ldz + col];
+          Zb[r * ldz + col] = s;
+        }
+        __syncthreads();
+        for (int o = t; o < rows * K; o += nth) {
+          const int r = o / K, col = o - r * K;
+          Z[(long long)(8 * I + r) * ldz + col] = Zb[r * ldz + col];
+        }
+        __syncthreads();
+      }
       double *Pl = c.Pi + leaf * ((long long)K * (K + 1) / 2);   // Pi_l = Z^T Z, packed lower
       const long long npk = (long long)K * (K + 1) / 2;
-      for (long long p = t; p < npk; p += LT) {
+      for (long long p = t; p < npk; p += nth) {
         long long a = (long long)((sqrt(8.0 * (double)p + 1.0) - 1.0) * 0.5);
         while (a * (a + 1) / 2 > p) a--;
         while ((a + 1) * (a + 2) / 2 <= p) a++;
@@ -653,20 +684,23 @@ hodlr_status hodlr_factor_impl(hodlr_s *h) {
     lc.mmax = mmax;
     hodlr_own_nodes(h, kappa, &lc.leaf0, &lc.nown);
     lc.lsz = (long long)mmax * (mmax + 1) / 2 + 1;
-    size_t need = sizeof(double) * (mmax + lc.lsz + (size_t)mmax * lc.ldz);
-    int grid = (int)lc.nown;
+    size_t need = sizeof(double) * (2 * (size_t)mmax + lc.lsz + (size_t)(mmax + 8) * lc.ldz);   // colj, xl, L, Z, Zb
+    int grid = (int)lc.nown, nthreads = LT;
     lc.scratch = nullptr; lc.scratch_per_cta = 0;
     if (need <= (size_t)maxsm - 12 * 1024) {
       lc.use_smem = 1;
       HCUDA(hodlr_allow_smem((const void *)k_leaf_factor, h->dev));
     } else {
-      lc.use_smem = 0; need = 0;
-      grid = (int)(lc.nown < 148 * 4 ? lc.nown : 148 * 4);
-      lc.scratch_per_cta = mmax + lc.lsz + (long long)mmax * lc.ldz;
+      lc.use_smem = 0; need = sizeof(double) * (size_t)mmax;     // colj only; xl, L, Z in global scratch
+      if (need > (size_t)maxsm - 12 * 1024) return hodlr_set_error(HODLR_EINVAL, "factor: leaf size %d too large", mmax);
+      int nsm = 148;
+      HCUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->dev));
+      grid = (int)(lc.nown < nsm ? lc.nown : nsm); nthreads = 1024;      // one CTA per SM: the scratch stays in L2
+      lc.scratch_per_cta = mmax + lc.lsz + (long long)(mmax + 8) * lc.ldz;
       lc.scratch = (double *)hodlr_dalloc(h, sizeof(double) * lc.scratch_per_cta * grid);
       if (!lc.scratch) return hodlr_set_error(HODLR_ENOMEM, "factor: scratch allocation failed");
     }
-    k_leaf_factor<<<grid, LT, need, h->st>>>(lc);
+    k_leaf_factor<<<grid, nthreads, need, h->st>>>(lc);
     HLAUNCH(h, "k_leaf_factor");
   }
   ph_end(h, PH_LEAF);
