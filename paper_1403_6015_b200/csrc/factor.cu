@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(1024) k_leaf_factor(LeafCtx c) {
     __syncthreads();
     for (long long j = 0; j < m; j++) {        // right-looking Cholesky A = L L^T
       // The scaled column j also goes to shared memory (colj): the trailing update reads both of its factors
-      // there, so its only global accesses are the coalesced read-modify-writes of the packed rows, two rows per
+      // there, so its only global accesses are the coalesced read-modify-writes of the packed rows, four rows per
       // warp in flight.
       const double d = L[P(j, j)];
       const bool ok = d > 0.0;
@@ -112,17 +112,23 @@ __global__ void __launch_bounds__(1024) k_leaf_factor(LeafCtx c) {
       for (long long i = j + 1 + t; i < m; i += nth) { const double v = L[P(i, j)] / ljj; colj[i] = v; L[P(i, j)] = v; }
       __syncthreads();
       if (t == 0) { L[P(j, j)] = ljj; if (!ok) bad = 1; }
-      for (long long i = j + 1 + warp; i < m; i += 2 * nw) {
-        const long long i2 = i + nw;
-        const bool two = i2 < m;
-        double *La = L + P(i, 0), *Lb = L + P(two ? i2 : i, 0);
-        const double la = colj[i], lb = two ? colj[i2] : 0.0;
-        const long long eb = two ? i2 : j, ke = two ? i2 : i;      // last column of each row (eb = j: no second row)
-        for (long long k = j + 1 + lane; k <= ke; k += 32) {
+      constexpr int NR = 4;                       // rows per warp in flight
+      for (int i0 = (int)j + 1 + warp; i0 < (int)m; i0 += NR * nw) {
+        double *Lr[NR]; double lr[NR]; int er[NR];
+#pragma unroll
+        for (int q = 0; q < NR; q++) {
+          const int iq = i0 + q * nw;
+          const bool v = iq < (int)m;
+          Lr[q] = L + P(v ? iq : i0, 0); lr[q] = v ? colj[iq] : 0.0; er[q] = v ? iq : (int)j;   // er = j: no such row
+        }
+        const int ke = max(max(er[0], er[1]), max(er[2], er[3]));
+        for (int k = (int)j + 1 + lane; k <= ke; k += 32) {
           const double ck = colj[k];
-          const double va = k <= i ? La[k] : 0.0, vb = k <= eb ? Lb[k] : 0.0;
-          if (k <= i) La[k] = va - la * ck;
-          if (k <= eb) Lb[k] = vb - lb * ck;
+          double v[NR];
+#pragma unroll
+          for (int q = 0; q < NR; q++) v[q] = k <= er[q] ? Lr[q][k] : 0.0;
+#pragma unroll
+          for (int q = 0; q < NR; q++) if (k <= er[q]) Lr[q][k] = v[q] - lr[q] * ck;
         }
       }
       __syncthreads();
@@ -149,7 +155,13 @@ __global__ void __launch_bounds__(1024) k_leaf_factor(LeafCtx c) {
         for (int i = j; i < m; i++) {
           const double *Li = L + P(i, 0);
           double s = 0.0;
-          for (int k = j + sub; k < i; k += 4) s += Li[k] * Lg[tix(k >> 3, Jt) * 64 + fo(k & 7, jc)];
+          const double *Xc = Lg + fo(sub, jc);                       // rows sub and sub + 4 of each tile of column j
+          for (int Kt = Jt; 8 * Kt < i; Kt++) {
+            const double *Xt = Xc + tix(Kt, Jt) * 64;
+            const int k0 = 8 * Kt + sub, k1 = k0 + 4;
+            if (k0 >= j && k0 < i) s += Li[k0] * Xt[0];
+            if (k1 >= j && k1 < i) s += Li[k1] * Xt[16];
+          }
           s += __shfl_xor_sync(gmask, s, 1);
           s += __shfl_xor_sync(gmask, s, 2);
           if (sub == 0) Lg[tix(i >> 3, Jt) * 64 + fo(i & 7, jc)] = ((i == j ? 1.0 : 0.0) - s) / Li[i];
@@ -172,11 +184,22 @@ __global__ void __launch_bounds__(1024) k_leaf_factor(LeafCtx c) {
       __syncthreads();                 // colsrc, and X complete
       for (int col = warp; col < K; col += nw) {          // E: the leaf's rows of its ancestors' factor columns
         const long long src = colsrc[col];
-        for (long long i = lane; i < m; i += 32) {
-          double v = 0.0;
-          if (src >= 0) v = c.Xh[src * c.ldx + lo + i];
-          else if (src == -2) { v = c.y[c.perm[lo + i]]; if (!isfinite(v)) atomicOr(&c.flags[3], 1); }
-          Z[i * ldz + col] = v;
+        for (long long ib = 0; ib < m; ib += 256) {       // 8 loads in flight per lane
+          double v[8];
+#pragma unroll
+          for (int q = 0; q < 8; q++) {
+            const long long i = ib + lane + 32 * q;
+            v[q] = 0.0;
+            if (i < m) {
+              if (src >= 0) v[q] = c.Xh[src * c.ldx + lo + i];
+              else if (src == -2) v[q] = c.y[c.perm[lo + i]];
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 8; q++) {
+            const long long i = ib + lane + 32 * q;
+            if (i < m) { if (src == -2 && !isfinite(v[q])) atomicOr(&c.flags[3], 1); Z[i * ldz + col] = v[q]; }
+          }
         }
       }
       __syncthreads();
@@ -187,7 +210,13 @@ __global__ void __launch_bounds__(1024) k_leaf_factor(LeafCtx c) {
         for (int o = t; o < rows * K; o += nth) {
           const int r = o / K, col = o - r * K, i = 8 * I + r;
           double s = 0.0;
-          for (int j = 0; j <= i; j++) s += Lg[tix(I, j >> 3) * 64 + fo(r, j & 7)] * Z[(long long)j * ldz + col];
+          const double *Xr = Lg + tix(I, 0) * 64 + r * 4;            // row r of the tiles (I, 0 .. I): fo(r, c)
+          const double *Zc = Z + col;
+          for (int J = 0; J < I; J++, Xr += 64, Zc += 8 * ldz) {
+#pragma unroll
+            for (int cc = 0; cc < 8; cc++) s += Xr[(cc >> 2) * 32 + (cc & 3)] * Zc[cc * ldz];
+          }
+          for (int cc = 0; cc <= r; cc++) s += Xr[(cc >> 2) * 32 + (cc & 3)] * Zc[cc * ldz];
           Zb[r * ldz + col] = s;
         }
         __syncthreads();
