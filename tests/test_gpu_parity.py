@@ -119,7 +119,10 @@ def test_cfg4_full_size_extreme(hb, k):
 
 
 @pytest.mark.parametrize("n,leaf", [(1, 64), (17, 64), (64, 64), (127, 64), (128, 64), (1999, 50), (3001, 37),
-                                    (4097, 128)])
+                                    (4097, 128),
+                                    # leaves of more than 128 points: the scalar leaf kernel k_leaf_factor, a single
+                                    # leaf (K = 0), all in shared memory (256 threads), in global scratch (1024 threads)
+                                    (200, 200), (300, 128), (2000, 128), (5001, 100)])
 def test_edge_sizes(hb, n, leaf):
     rng = np.random.default_rng(n)
     x = rng.uniform(-3, 3, n); y = rng.standard_normal(n)
